@@ -1,0 +1,412 @@
+#!/usr/bin/env python3
+"""Benchmark: AlexNet conv1-5 forward / backward-data / backward-filter, fp32,
+N=128 per GPU (BASELINE.json configs[1]; weak scaling to N=1024 on 8 GPUs =
+configs[3], with the dW NCCL allreduce).
+
+One step = fwd + bwd-data + bwd-filter of all five layers over one batch of
+synthetic inputs (uniform(-0.5, 0.5) from default_rng([2014, layer]) as the
+reference bench, pkg/src/dnnp/bench.py:151-157), inputs resident in HBM.
+Metric = algorithmic conv TFLOP/s, F = 2*N*K*C*R*S*P*Q per pass
+(bench.py:126-129).  L2 is flushed (256 MiB write) between timed steps,
+outside the per-step CUDA-event windows.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+# torchvision / "one weird trick" AlexNet convs: name, C, H(=W), K, R(=S), stride, pad
+ALEXNET = [
+    ("conv1", 3, 224, 64, 11, 4, 2),
+    ("conv2", 64, 27, 192, 5, 1, 2),
+    ("conv3", 192, 13, 384, 3, 1, 1),
+    ("conv4", 384, 13, 256, 3, 1, 1),
+    ("conv5", 256, 13, 256, 3, 1, 1),
+]
+PASSES = ("fwd", "bwd_data", "bwd_filter")
+N_PER_GPU = 128
+
+
+def out_extent(h, r, u, pad):
+    return -(-(h - r + 1 + 2 * pad) // u)
+
+
+def layer_flops(n, c, h, k, r, u, pad):
+    p = out_extent(h, r, u, pad)
+    return 2 * n * k * c * r * r * p * p
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            m = json.load(fh)
+        return m["hbm_gbs"], m["bf16_tflops"], "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return 6650.0, 1590.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+                self.lines = [ln for ln in out.splitlines() if ln.strip()]
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in getattr(self, "lines", []):
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def make_inputs(n, device, torch):
+    """Per-layer x, f, dy (synthetic, reference bench generator) on device."""
+    layers = []
+    for idx, (name, c, h, k, r, u, pad) in enumerate(ALEXNET):
+        p = out_extent(h, r, u, pad)
+        g = np.random.default_rng([2014, idx])
+        x = torch.from_numpy(g.uniform(-0.5, 0.5, n * c * h * h).astype(np.float32))
+        f = torch.from_numpy(g.uniform(-0.5, 0.5, k * c * r * r).astype(np.float32))
+        dy = torch.from_numpy(g.uniform(-0.5, 0.5, n * k * p * p).astype(np.float32))
+        layers.append(dict(name=name, n=n, c=c, h=h, k=k, r=r, u=u, pad=pad, p=p,
+                           x=x.to(device), f=f.to(device), dy=dy.to(device),
+                           flops=layer_flops(n, c, h, k, r, u, pad)))
+    return layers
+
+
+def build_views(dp, layers, torch, device):
+    for L in layers:
+        n, c, h, k, r, p = L["n"], L["c"], L["h"], L["k"], L["r"], L["p"]
+        L["cd"] = dp.ConvDesc(L["u"], L["u"], L["pad"], L["pad"], "convolution")
+        L["xv"] = dp.TensorView(dp.make_desc(n, c, h, h), L["x"])
+        L["fv"] = dp.FilterView(dp.make_filter_desc(k, c, r, r), L["f"])
+        L["yv"] = dp.empty_view(dp.make_desc(n, k, p, p), device=device)
+        L["dyv"] = dp.TensorView(dp.make_desc(n, k, p, p), L["dy"])
+        L["dxv"] = dp.empty_view(dp.make_desc(n, c, h, h), device=device)
+        L["df"] = torch.empty(k * c * r * r, device=device)
+        L["dfv"] = dp.FilterView(dp.make_filter_desc(k, c, r, r), L["df"])
+
+
+def run_step(dp, layers, torch, events=None, allreduce=None):
+    for li, L in enumerate(layers):
+        ops = (
+            lambda: dp.conv_forward(L["xv"], L["fv"], L["cd"], "implicit", L["yv"]),
+            lambda: dp.conv_backward_data(L["dyv"], L["fv"], L["cd"], "implicit", L["dxv"]),
+            lambda: dp.conv_backward_filter(L["dyv"], L["xv"], L["cd"], "implicit", L["dfv"]),
+        )
+        for pi, op in enumerate(ops):
+            if events is not None:
+                events[(li, pi)][0].record()
+            op()
+            if events is not None:
+                events[(li, pi)][1].record()
+        if allreduce is not None:
+            allreduce(L["df"])
+
+
+def cpu_baseline(threads, sample_n=2):
+    """The C oracle (restatement of the reference implicit engine) on host
+    cores, on a bounded sample of the same workload (N=sample_n per layer)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as orc
+    total_flops = 0
+    t0 = time.perf_counter()
+    for idx, (name, c, h, k, r, u, pad) in enumerate(ALEXNET):
+        n = sample_n
+        p = out_extent(h, r, u, pad)
+        g = np.random.default_rng([2014, idx])
+        x = g.uniform(-0.5, 0.5, n * c * h * h).astype(np.float32)
+        f = g.uniform(-0.5, 0.5, k * c * r * r).astype(np.float32)
+        dy = g.uniform(-0.5, 0.5, n * k * p * p).astype(np.float32)
+        xg = [n, c, h, h, c * h * h, h * h, h, 1]
+        yg = [n, k, p, p, k * p * p, p * p, p, 1]
+        cg = [u, u, pad, pad, 0, 0]
+        y = np.zeros(n * k * p * p, np.float32)
+        orc.conv_forward(xg, x, [k, c, r, r], f, cg, yg, y, threads=threads)
+        dx = np.zeros(n * c * h * h, np.float32)
+        orc.conv_backward_data([k, c, r, r], f, yg, dy, cg, xg, dx)
+        df = np.zeros(k * c * r * r, np.float32)
+        orc.conv_backward_filter(xg, x, yg, dy, cg, [k, c, r, r], df, threads=threads)
+        total_flops += 3 * layer_flops(n, c, h, k, r, u, pad)
+    dt = time.perf_counter() - t0
+    return total_flops / dt / 1e12, dt
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def main_reference(args):
+    """--impl reference: the reference algorithm's CPU implementation (the C
+    oracle port; the reference is pure numpy and is not built here) on the
+    host cores, same metric/config, bounded sample per step."""
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    vals = []
+    for _ in range(args.warmup):
+        cpu_baseline(threads, sample_n=1)
+    for _ in range(args.steps):
+        v, dt = cpu_baseline(threads, sample_n=1)
+        vals.append((v, dt))
+    value = float(np.median([v for v, _ in vals]))
+    ms = float(np.median([dt for _, dt in vals])) * 1e3
+    sample = ("AlexNet conv1-5 fwd+bwd_data+bwd_filter fp32 at N=1 per step (config N=128 "
+              "scaled; flops linear in N); C oracle restating the reference implicit engine, "
+              f"fwd/bwd-filter threaded over {threads} cores, bwd-data serial as the reference")
+    print(json.dumps({
+        "impl": "reference", "metric": "conv TFLOP/s fwd/bwd-data/bwd-filter (AlexNet conv1-5)",
+        "value": value, "unit": "TFLOP/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": "alexnet_conv1-5_fwd_bwdd_bwdf_N128_fp32_nchw", "sample_n": 1},
+        "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": threads, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="native", choices=["native", "reference"])
+    ap.add_argument("--math", type=int, default=0, help="0 default, 1 SIMT fp32, 2 tcgen05")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--batch", type=int, default=N_PER_GPU)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return main_reference(args)
+    args.warmup = max(args.warmup, 3)
+
+    import torch
+    import torch.distributed as dist
+    import paper_1410_0759_b200 as dp
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=device)
+    dp.set_math(args.math)
+
+    layers = make_inputs(args.batch, device, torch)
+    build_views(dp, layers, torch, device)
+    allreduce = (lambda t: dist.all_reduce(t)) if ws > 1 else None
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=device)
+
+    for _ in range(args.warmup):
+        run_step(dp, layers, torch, allreduce=allreduce)
+    torch.cuda.synchronize()
+
+    nl = len(layers)
+    step_ms = []
+    op_ms = {(li, pi): [] for li in range(nl) for pi in range(3)}
+    launches0 = dp.kernel_launch_count()
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush.fill_(1.0)  # L2 flush, outside the timed window
+            evs = {(li, pi): (torch.cuda.Event(enable_timing=True),
+                              torch.cuda.Event(enable_timing=True))
+                   for li in range(nl) for pi in range(3)}
+            if ws > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            s0 = torch.cuda.Event(enable_timing=True)
+            s1 = torch.cuda.Event(enable_timing=True)
+            s0.record()
+            run_step(dp, layers, torch, events=evs, allreduce=allreduce)
+            s1.record()
+            torch.cuda.synchronize()
+            step_ms.append(s0.elapsed_time(s1))
+            for key, (a, b) in evs.items():
+                op_ms[key].append(a.elapsed_time(b))
+    launches = dp.kernel_launch_count() - launches0
+    total_ms = float(np.sum(step_ms))
+    if ws > 1:
+        t = torch.tensor([total_ms], device=device, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    step_flops = 3 * sum(L["flops"] for L in layers)
+    value = step_flops * ws * args.steps / (total_ms / 1e3) / 1e12
+
+    hbm, bf16, peak_src = peaks()
+    tf32_peak = bf16 / 2.0
+    per = {}
+    dominant, dom_ms = None, -1.0
+    for (li, pi), v in op_ms.items():
+        L = layers[li]
+        avg = float(np.mean(v))
+        tf = L["flops"] / (avg / 1e3) / 1e12
+        per[f"{L['name']}.{PASSES[pi]}"] = {"ms": round(avg, 4), "tflops": round(tf, 2),
+                                            "pct_tf32_peak": round(100 * tf / tf32_peak, 1)}
+        if avg * len(v) > dom_ms:
+            dom_ms, dominant = avg * len(v), (li, pi)
+
+    dl, dpi = dominant
+    dom_avg = float(np.mean(op_ms[dominant]))
+    achieved = layers[dl]["flops"] / (dom_avg / 1e3) / 1e12
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "dominant_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(f"{layers[dl]['name']}.{PASSES[dpi]}")
+        except Exception:
+            traffic = None
+
+    # ---- e2e: same step through the C ABI with pinned HOST buffers --------
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(dp, layers, torch, device, ws, args, step_flops)
+
+    line = {
+        "metric": "conv TFLOP/s fwd/bwd-data/bwd-filter (AlexNet conv1-5), % TF32 tensor peak",
+        "value": round(value, 3), "unit": "TFLOP/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(total_ms / args.steps, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic uniform(-0.5,0.5), default_rng([2014, layer]) as reference bench",
+        "config": {"workload": "alexnet_conv1-5_fwd_bwdd_bwdf_N128_fp32_nchw",
+                   "batch_per_gpu": args.batch, "global_batch": args.batch * ws,
+                   "layers": "torchvision AlexNet conv1-5 (64/192/384/256/256)",
+                   "parallelism": f"batch-shard dp{ws}" + (" + dW allreduce" if ws > 1 else ""),
+                   "l2": "flushed (256 MiB write) between timed steps",
+                   "math": ["default(tcgen05 BF16x3 when eligible)", "simt_fp32",
+                            "tcgen05_bf16x3"][args.math]},
+        "pct_tf32_peak": round(100 * value / ws / tf32_peak, 2),
+        "per_layer": per,
+        "roofline": {"bound": "tensor", "achieved": round(achieved, 2), "peak": tf32_peak,
+                     "unit": "TFLOP/s", "frac": round(achieved / tf32_peak, 4),
+                     "traffic": traffic,
+                     "kernel": f"{layers[dl]['name']}.{PASSES[dpi]}",
+                     "peak_basis": f"TF32 dense = 1/2 of bf16 {bf16} TF/s, {peak_src}",
+                     "work_per_launch_flops": layers[dl]["flops"]},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+    }
+    if e2e is not None:
+        line["e2e"] = e2e
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        threads = os.cpu_count() or 1
+        v, dt = cpu_baseline(threads, sample_n=2)
+        line["cpu_baseline"] = {
+            "value": round(v, 5), "unit": "TFLOP/s", "cores": threads, "kind": "port",
+            "sample": f"AlexNet conv1-5 fwd+bwd_data+bwd_filter fp32 at N=2 ({dt:.1f} s), C "
+                      "oracle restating the reference implicit engine (bwd-data serial)"}
+    if ws > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(line))
+
+
+def run_e2e(dp, layers, torch, device, ws, args, step_flops):
+    """Same step through the public API with pinned host buffers: every step
+    copies its inputs host->device and results device->host (C-ABI staging)."""
+    host = []
+    h2d = d2h = 0
+    for L in layers:
+        n, c, h, k, r, p = L["n"], L["c"], L["h"], L["k"], L["r"], L["p"]
+        hx = L["x"].cpu().pin_memory()
+        hf = L["f"].cpu().pin_memory()
+        hdy = L["dy"].cpu().pin_memory()
+        hy = torch.empty(n * k * p * p, pin_memory=True)
+        hdx = torch.empty(n * c * h * h, pin_memory=True)
+        hdf = torch.empty(k * c * r * r, pin_memory=True)
+        host.append(dict(
+            cd=L["cd"], x=dp.TensorView(dp.make_desc(n, c, h, h), hx.numpy()),
+            f=dp.FilterView(dp.make_filter_desc(k, c, r, r), hf.numpy()),
+            dy=dp.TensorView(dp.make_desc(n, k, p, p), hdy.numpy()),
+            y=dp.TensorView(dp.make_desc(n, k, p, p), hy.numpy()),
+            dx=dp.TensorView(dp.make_desc(n, c, h, h), hdx.numpy()),
+            df=dp.FilterView(dp.make_filter_desc(k, c, r, r), hdf.numpy()), keep=(hx, hf, hdy, hy, hdx, hdf)))
+        fb = k * c * r * r * 4
+        xb, yb = n * c * h * h * 4, n * k * p * p * 4
+        h2d += (xb + fb) + (yb + fb) + (xb + yb)   # fwd, bwd-data, bwd-filter inputs
+        d2h += yb + xb + fb
+    def step():
+        for H in host:
+            dp.conv_forward(H["x"], H["f"], H["cd"], "implicit", H["y"])
+            dp.conv_backward_data(H["dy"], H["f"], H["cd"], "implicit", H["dx"])
+            dp.conv_backward_filter(H["dy"], H["x"], H["cd"], "implicit", H["df"])
+    step()
+    torch.cuda.synchronize()
+    steps = max(2, min(args.steps, 5))
+    ms = []
+    for _ in range(steps):
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        a.record()
+        step()
+        b.record()
+        torch.cuda.synchronize()
+        ms.append(a.elapsed_time(b))
+    tot = float(np.sum(ms))
+    if ws > 1:
+        import torch.distributed as dist
+        t = torch.tensor([tot], device=device, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot = float(t.item())
+    val = step_flops * ws * steps / (tot / 1e3) / 1e12
+    return {"value": round(val, 3), "unit": "TFLOP/s", "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h), "steps": steps,
+            "path": "C ABI with pinned host buffers (staged H2D/D2H inside every call)"}
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,449 @@
+// SIMT implicit-GEMM convolution (forward, backward-data, backward-filter)
+// for fp64 (production path) and fp32 (DNNP_MATH_SIMT_FP32 / ineligible
+// shapes).  The lowered data matrix is never materialised: every tile of it
+// is gathered straight from the strided input with magic-number index
+// decode, as in the reference's virtual provider (conv.py:235-356) driven by
+// the tiled engine (gemm.py:140-181).
+//
+// GEMM orientation (M rows are output pixels so the epilogue writes
+// contiguous runs of q):
+//   forward      C[NPQ x K]   = im2col(x)[NPQ x CRS] . F[K x CRS]^T
+//   backward-data C[NHW x C]  = gather(dy)[NHW x KRS] . F^T      (gather form,
+//                 no scatter/atomics: every dx element is owned by one thread)
+//   backward-filter C[K x CRS] = dy[K x NPQ] . im2col(x)[NPQ x CRS], split-K
+//                 over NPQ with a fixed-order reduction (deterministic).
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace dnnp {
+
+enum Pass { FWD = 0, DGRAD = 1, WGRAD = 2 };
+
+struct SimtArgs {
+  ConvProblem p;
+  const void* a_src;  // FWD: x, DGRAD: dy, WGRAD: dy
+  const void* b_src;  // FWD: f, DGRAD: f,  WGRAD: x
+  void* out;          // FWD: y, DGRAD: dx, WGRAD: df or split workspace
+  int64_t M, Ncol, Kred;
+  int64_t k_per_split;
+  double alpha, beta;
+  int accumulate;
+  int splits;
+  // decoders
+  MagicDiv dRS, dS, dPQ, dQ, dHW, dW, dU, dV;
+};
+
+template <typename T>
+struct SimtCfg;
+template <>
+struct SimtCfg<float> {
+  static constexpr int BM = 128, BN = 128, BK = 8, TM = 8, TN = 8;
+};
+template <>
+struct SimtCfg<double> {
+  static constexpr int BM = 64, BN = 64, BK = 8, TM = 4, TN = 4;
+};
+
+// A(m, k) element of the pass' left operand.
+template <typename T, int PASS>
+struct RowCtx {
+  int64_t base;     // pass-specific row base offset
+  int32_t hb, wb;   // FWD: p*u - pad_h, q*v - pad_w; DGRAD: h + pad_h, w + pad_w
+  uint32_t n;
+  bool valid;
+};
+
+template <typename T, int PASS>
+__device__ __forceinline__ RowCtx<T, PASS> row_ctx(const SimtArgs& a, int64_t m) {
+  RowCtx<T, PASS> rc;
+  rc.valid = m < a.M;
+  const ConvProblem& p = a.p;
+  if (!rc.valid) {
+    rc.base = 0; rc.hb = rc.wb = 0; rc.n = 0;
+    return rc;
+  }
+  if (PASS == FWD) {
+    uint32_t n, rem, pp, qq;
+    mdivmod(uint32_t(m), a.dPQ, n, rem);
+    mdivmod(rem, a.dQ, pp, qq);
+    rc.n = n;
+    rc.base = int64_t(n) * p.x.sn;
+    rc.hb = int32_t(pp * p.u - p.pad_h);
+    rc.wb = int32_t(qq * p.v - p.pad_w);
+  } else if (PASS == DGRAD) {
+    uint32_t n, rem, h, w;
+    mdivmod(uint32_t(m), a.dHW, n, rem);
+    mdivmod(rem, a.dW, h, w);
+    rc.n = n;
+    rc.base = int64_t(n) * p.y.sn;
+    rc.hb = int32_t(h + p.pad_h);
+    rc.wb = int32_t(w + p.pad_w);
+  } else {  // WGRAD: row = output channel k of dy
+    rc.n = 0;
+    rc.base = m * p.y.sc;
+    rc.hb = rc.wb = 0;
+  }
+  return rc;
+}
+
+template <typename T, int PASS>
+__device__ __forceinline__ T load_a(const SimtArgs& a, const RowCtx<T, PASS>& rc, int64_t k) {
+  const ConvProblem& p = a.p;
+  if (!rc.valid || k >= a.Kred) return T(0);
+  const T* src = static_cast<const T*>(a.a_src);
+  if (PASS == FWD) {
+    uint32_t c, rs, r, s;
+    mdivmod(uint32_t(k), a.dRS, c, rs);
+    mdivmod(rs, a.dS, r, s);
+    const int32_t hr = p.flip ? int32_t(p.R - 1 - r) : int32_t(r);
+    const int32_t wr = p.flip ? int32_t(p.S - 1 - s) : int32_t(s);
+    const int32_t h = rc.hb + hr, w = rc.wb + wr;
+    if (uint32_t(h) >= uint32_t(p.H) || uint32_t(w) >= uint32_t(p.W)) return T(0);
+    return src[rc.base + int64_t(c) * p.x.sc + int64_t(h) * p.x.sh + int64_t(w) * p.x.sw];
+  } else if (PASS == DGRAD) {
+    uint32_t kk, rs, r, s;
+    mdivmod(uint32_t(k), a.dRS, kk, rs);
+    mdivmod(rs, a.dS, r, s);
+    const int32_t hr = p.flip ? int32_t(p.R - 1 - r) : int32_t(r);
+    const int32_t wr = p.flip ? int32_t(p.S - 1 - s) : int32_t(s);
+    const int32_t th = rc.hb - hr, tw = rc.wb - wr;  // = p*u, q*v
+    if (th < 0 || tw < 0) return T(0);
+    uint32_t pp, ph, qq, qw;
+    mdivmod(uint32_t(th), a.dU, pp, ph);
+    mdivmod(uint32_t(tw), a.dV, qq, qw);
+    if (ph | qw) return T(0);
+    if (pp >= uint32_t(p.P) || qq >= uint32_t(p.Q)) return T(0);
+    return src[rc.base + int64_t(kk) * p.y.sc + int64_t(pp) * p.y.sh + int64_t(qq) * p.y.sw];
+  } else {
+    uint32_t n, rem, pp, qq;
+    mdivmod(uint32_t(k), a.dPQ, n, rem);
+    mdivmod(rem, a.dQ, pp, qq);
+    return src[rc.base + int64_t(n) * p.y.sn + int64_t(pp) * p.y.sh + int64_t(qq) * p.y.sw];
+  }
+}
+
+// B(col, k) element of the right operand (stored as [col][k]).
+template <typename T, int PASS>
+__device__ __forceinline__ T load_b(const SimtArgs& a, int64_t col, int64_t k) {
+  const ConvProblem& p = a.p;
+  if (col >= a.Ncol || k >= a.Kred) return T(0);
+  const T* src = static_cast<const T*>(a.b_src);
+  if (PASS == FWD) {
+    return src[col * a.Kred + k];  // f[kout][crs]
+  } else if (PASS == DGRAD) {
+    uint32_t kk, rs;
+    mdivmod(uint32_t(k), a.dRS, kk, rs);
+    return src[(int64_t(kk) * p.C + col) * (p.R * p.S) + rs];  // f[kout][c][r][s]
+  } else {
+    uint32_t c, rs, r, s, n, rem, pp, qq;
+    mdivmod(uint32_t(col), a.dRS, c, rs);
+    mdivmod(rs, a.dS, r, s);
+    mdivmod(uint32_t(k), a.dPQ, n, rem);
+    mdivmod(rem, a.dQ, pp, qq);
+    const int32_t hr = p.flip ? int32_t(p.R - 1 - r) : int32_t(r);
+    const int32_t wr = p.flip ? int32_t(p.S - 1 - s) : int32_t(s);
+    const int32_t h = int32_t(pp * p.u - p.pad_h) + hr;
+    const int32_t w = int32_t(qq * p.v - p.pad_w) + wr;
+    if (uint32_t(h) >= uint32_t(p.H) || uint32_t(w) >= uint32_t(p.W)) return T(0);
+    return src[int64_t(n) * p.x.sn + int64_t(c) * p.x.sc + int64_t(h) * p.x.sh +
+               int64_t(w) * p.x.sw];
+  }
+}
+
+template <typename T, int PASS>
+__global__ void __launch_bounds__((SimtCfg<T>::BM / SimtCfg<T>::TM) *
+                                  (SimtCfg<T>::BN / SimtCfg<T>::TN))
+    conv_simt_kernel(SimtArgs a) {
+  constexpr int BM = SimtCfg<T>::BM, BN = SimtCfg<T>::BN, BK = SimtCfg<T>::BK;
+  constexpr int TM = SimtCfg<T>::TM, TN = SimtCfg<T>::TN;
+  constexpr int NT = (BM / TM) * (BN / TN);
+  constexpr int LA = BM * BK / NT, LB = BN * BK / NT;
+  static_assert(NT % BM == 0 || PASS == WGRAD, "row-fast A mapping");
+  __shared__ T As[2][BK][BM + 4];
+  __shared__ T Bs[2][BK][BN + 4];
+
+  const int tid = threadIdx.x;
+  const int64_t m0 = int64_t(blockIdx.x) * BM, n0 = int64_t(blockIdx.y) * BN;
+  const int64_t kbeg = int64_t(blockIdx.z) * a.k_per_split;
+  const int64_t kend = min(a.Kred, kbeg + a.k_per_split);
+
+  // A mapping: FWD/DGRAD rows fastest (coalesced along q / w); WGRAD k fastest.
+  int a_mi[LA], a_ki[LA];
+  RowCtx<T, PASS> rc[LA];
+#pragma unroll
+  for (int j = 0; j < LA; j++) {
+    int e = tid + j * NT;
+    if (PASS == WGRAD) {
+      a_ki[j] = e % BK;
+      a_mi[j] = e / BK;
+    } else {
+      a_mi[j] = e % BM;
+      a_ki[j] = e / BM;
+    }
+    rc[j] = row_ctx<T, PASS>(a, m0 + a_mi[j]);
+  }
+  int b_ni[LB], b_ki[LB];
+#pragma unroll
+  for (int j = 0; j < LB; j++) {
+    int e = tid + j * NT;
+    b_ki[j] = e % BK;
+    b_ni[j] = e / BK;
+  }
+
+  T acc[TM][TN];
+#pragma unroll
+  for (int i = 0; i < TM; i++)
+#pragma unroll
+    for (int j = 0; j < TN; j++) acc[i][j] = T(0);
+
+  T ra[LA], rb[LB];
+  auto gload = [&](int64_t k0) {
+#pragma unroll
+    for (int j = 0; j < LA; j++) {
+      int64_t k = k0 + a_ki[j];
+      ra[j] = k < kend ? load_a<T, PASS>(a, rc[j], k) : T(0);
+    }
+#pragma unroll
+    for (int j = 0; j < LB; j++) {
+      int64_t k = k0 + b_ki[j];
+      rb[j] = k < kend ? load_b<T, PASS>(a, n0 + b_ni[j], k) : T(0);
+    }
+  };
+  auto sstore = [&](int buf) {
+#pragma unroll
+    for (int j = 0; j < LA; j++) As[buf][a_ki[j]][a_mi[j]] = ra[j];
+#pragma unroll
+    for (int j = 0; j < LB; j++) Bs[buf][b_ki[j]][b_ni[j]] = rb[j];
+  };
+
+  const int tr = tid / (BN / TN), tc = tid % (BN / TN);
+  int buf = 0;
+  if (kbeg < kend) {
+    gload(kbeg);
+    sstore(0);
+    __syncthreads();
+    for (int64_t k0 = kbeg; k0 < kend; k0 += BK) {
+      const bool more = k0 + BK < kend;
+      if (more) gload(k0 + BK);
+#pragma unroll
+      for (int kk = 0; kk < BK; kk++) {
+        T av[TM], bv[TN];
+#pragma unroll
+        for (int i = 0; i < TM; i++) av[i] = As[buf][kk][tr + i * (BM / TM)];
+#pragma unroll
+        for (int j = 0; j < TN; j++) bv[j] = Bs[buf][kk][tc + j * (BN / TN)];
+#pragma unroll
+        for (int i = 0; i < TM; i++)
+#pragma unroll
+          for (int j = 0; j < TN; j++) acc[i][j] = fma(av[i], bv[j], acc[i][j]);
+      }
+      if (more) {
+        sstore(buf ^ 1);
+        __syncthreads();
+        buf ^= 1;
+      }
+    }
+  }
+
+  // epilogue
+  const ConvProblem& p = a.p;
+  T* out = static_cast<T*>(a.out);
+#pragma unroll
+  for (int i = 0; i < TM; i++) {
+    const int64_t m = m0 + tr + i * (BM / TM);
+    if (m >= a.M) continue;
+    int64_t rowoff;
+    if (PASS == FWD) {
+      uint32_t n, rem, pp, qq;
+      mdivmod(uint32_t(m), a.dPQ, n, rem);
+      mdivmod(rem, a.dQ, pp, qq);
+      rowoff = int64_t(n) * p.y.sn + int64_t(pp) * p.y.sh + int64_t(qq) * p.y.sw;
+    } else if (PASS == DGRAD) {
+      uint32_t n, rem, h, w;
+      mdivmod(uint32_t(m), a.dHW, n, rem);
+      mdivmod(rem, a.dW, h, w);
+      rowoff = int64_t(n) * p.x.sn + int64_t(h) * p.x.sh + int64_t(w) * p.x.sw;
+    } else {
+      rowoff = m * a.Ncol + int64_t(blockIdx.z) * a.M * a.Ncol * (a.splits > 1 ? 1 : 0);
+    }
+#pragma unroll
+    for (int j = 0; j < TN; j++) {
+      const int64_t col = n0 + tc + j * (BN / TN);
+      if (col >= a.Ncol) continue;
+      const T v = acc[i][j];
+      if (PASS == FWD) {
+        T* dst = out + rowoff + col * p.y.sc;
+        T r = dmul<T>(v, T(a.alpha));
+        if (a.beta != 0.0) r = dadd<T>(dmul<T>(*dst, T(a.beta)), r);
+        *dst = r;
+      } else if (PASS == DGRAD) {
+        T* dst = out + rowoff + col * p.x.sc;
+        *dst = a.accumulate ? dadd<T>(*dst, v) : v;
+      } else {
+        T* dst = out + rowoff + col;
+        *dst = (a.splits == 1 && a.accumulate) ? dadd<T>(*dst, v) : v;
+      }
+    }
+  }
+}
+
+// df[i] (+)= sum_z ws[z][i] in ascending z (deterministic split-K reduction)
+template <typename T>
+__global__ void splitk_reduce(const T* __restrict__ ws, int splits, int64_t count, T* df,
+                              int accumulate) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < count; i += stride) {
+    T s = ws[i];
+    for (int z = 1; z < splits; z++) s = dadd<T>(s, ws[int64_t(z) * count + i]);
+    df[i] = accumulate ? dadd<T>(df[i], s) : s;
+  }
+}
+
+static void fill_divs(SimtArgs& a) {
+  const ConvProblem& p = a.p;
+  a.dRS = make_magic(uint32_t(p.R * p.S));
+  a.dS = make_magic(uint32_t(p.S));
+  a.dPQ = make_magic(uint32_t(p.P * p.Q));
+  a.dQ = make_magic(uint32_t(p.Q));
+  a.dHW = make_magic(uint32_t(p.H * p.W));
+  a.dW = make_magic(uint32_t(p.W));
+  a.dU = make_magic(uint32_t(p.u));
+  a.dV = make_magic(uint32_t(p.v));
+}
+
+template <typename T, int PASS>
+static cudaError_t launch_simt(SimtArgs& a, cudaStream_t st) {
+  constexpr int BM = SimtCfg<T>::BM, BN = SimtCfg<T>::BN, BK = SimtCfg<T>::BK;
+  constexpr int NT = (BM / SimtCfg<T>::TM) * (BN / SimtCfg<T>::TN);
+  fill_divs(a);
+  const int64_t gm = ceil_div(a.M, BM), gn = ceil_div(a.Ncol, BN);
+  a.splits = 1;
+  a.k_per_split = a.Kred;
+  T* ws = nullptr;
+  void* final_out = a.out;
+  if (PASS == WGRAD) {
+    int64_t tiles = gm * gn;
+    int64_t want = ceil_div(int64_t(kNumSMs) * 3, tiles);
+    int64_t maxs = std::max<int64_t>(1, a.Kred / (BK * 16));
+    int64_t s = std::max<int64_t>(1, std::min<int64_t>({want, maxs, 256}));
+    if (s > 1) {
+      a.k_per_split = ceil_div(ceil_div(a.Kred, s), BK) * BK;
+      s = ceil_div(a.Kred, a.k_per_split);
+    }
+    a.splits = int(s);
+    if (a.splits > 1) {
+      cudaError_t e = cudaMallocAsync(&ws, sizeof(T) * a.splits * a.M * a.Ncol, st);
+      if (e != cudaSuccess) return e;
+      a.out = ws;
+    }
+  }
+  dim3 grid(unsigned(gm), unsigned(gn), unsigned(a.splits));
+  if (gn > 65535) return cudaErrorInvalidConfiguration;
+  conv_simt_kernel<T, PASS><<<grid, NT, 0, st>>>(a);
+  note_launch();
+  cudaError_t e = cudaGetLastError();
+  if (ws) {
+    const int64_t count = a.M * a.Ncol;
+    splitk_reduce<T><<<grid_for(count, 256, 8), 256, 0, st>>>(ws, a.splits, count,
+                                                              static_cast<T*>(final_out),
+                                                              a.accumulate);
+    note_launch();
+    if (e == cudaSuccess) e = cudaGetLastError();
+    cudaFreeAsync(ws, st);
+  }
+  return e;
+}
+
+template <typename T>
+static cudaError_t simt_forward(const ConvProblem& p, const void* x, const void* f, void* y,
+                                double alpha, double beta, cudaStream_t st) {
+  SimtArgs a{};
+  a.p = p;
+  a.a_src = x;
+  a.b_src = f;
+  a.out = y;
+  a.M = p.N * p.P * p.Q;
+  a.Ncol = p.K;
+  a.Kred = p.C * p.R * p.S;
+  a.alpha = alpha;
+  a.beta = beta;
+  return launch_simt<T, FWD>(a, st);
+}
+template <typename T>
+static cudaError_t simt_bwd_data(const ConvProblem& p, const void* dy, const void* f, void* dx,
+                                 bool acc, cudaStream_t st) {
+  SimtArgs a{};
+  a.p = p;
+  a.a_src = dy;
+  a.b_src = f;
+  a.out = dx;
+  a.M = p.N * p.H * p.W;
+  a.Ncol = p.C;
+  a.Kred = p.K * p.R * p.S;
+  a.accumulate = acc;
+  return launch_simt<T, DGRAD>(a, st);
+}
+template <typename T>
+static cudaError_t simt_bwd_filter(const ConvProblem& p, const void* dy, const void* x, void* df,
+                                  bool acc, cudaStream_t st) {
+  SimtArgs a{};
+  a.p = p;
+  a.a_src = dy;
+  a.b_src = x;
+  a.out = df;
+  a.M = p.K;
+  a.Ncol = p.C * p.R * p.S;
+  a.Kred = p.N * p.P * p.Q;
+  a.accumulate = acc;
+  return launch_simt<T, WGRAD>(a, st);
+}
+
+// ---- tensor-core path (conv_tc.cu) -----------------------------------------
+cudaError_t tc_forward(const ConvProblem& p, const float* x, const float* f, float* y,
+                       double alpha, double beta, cudaStream_t st);
+cudaError_t tc_backward_data(const ConvProblem& p, const float* dy, const float* f, float* dx,
+                             bool acc, cudaStream_t st);
+cudaError_t tc_backward_filter(const ConvProblem& p, const float* dy, const float* x, float* df,
+                               bool acc, cudaStream_t st);
+
+// math: 0 default (tensor cores when eligible), 1 SIMT fp32, 2 force tensor cores
+static bool use_tc(const ConvProblem& p, Dtype dt, int math, int pass, cudaError_t* err) {
+  *err = cudaSuccess;
+  if (dt != F32 || math == 1) return false;
+  bool ok = tc_eligible(p, pass);
+  if (!ok && math == 2) *err = cudaErrorNotSupported;
+  return ok;
+}
+
+cudaError_t conv_forward(const ConvProblem& p, Dtype dt, const void* x, const void* f, void* y,
+                         double alpha, double beta, int math, cudaStream_t st) {
+  cudaError_t e;
+  if (use_tc(p, dt, math, FWD, &e))
+    return tc_forward(p, (const float*)x, (const float*)f, (float*)y, alpha, beta, st);
+  if (e != cudaSuccess) return e;
+  return dt == F32 ? simt_forward<float>(p, x, f, y, alpha, beta, st)
+                   : simt_forward<double>(p, x, f, y, alpha, beta, st);
+}
+
+cudaError_t conv_backward_data(const ConvProblem& p, Dtype dt, const void* dy, const void* f,
+                               void* dx, bool accumulate, int math, cudaStream_t st) {
+  cudaError_t e;
+  if (use_tc(p, dt, math, DGRAD, &e))
+    return tc_backward_data(p, (const float*)dy, (const float*)f, (float*)dx, accumulate, st);
+  if (e != cudaSuccess) return e;
+  return dt == F32 ? simt_bwd_data<float>(p, dy, f, dx, accumulate, st)
+                   : simt_bwd_data<double>(p, dy, f, dx, accumulate, st);
+}
+
+cudaError_t conv_backward_filter(const ConvProblem& p, Dtype dt, const void* dy, const void* x,
+                                 void* df, bool accumulate, int math, cudaStream_t st) {
+  cudaError_t e;
+  if (use_tc(p, dt, math, WGRAD, &e))
+    return tc_backward_filter(p, (const float*)dy, (const float*)x, (float*)df, accumulate, st);
+  if (e != cudaSuccess) return e;
+  return dt == F32 ? simt_bwd_filter<float>(p, dy, x, df, accumulate, st)
+                   : simt_bwd_filter<double>(p, dy, x, df, accumulate, st);
+}
+
+}  // namespace dnnp

@@ -1,0 +1,87 @@
+// Internal interface between the C-ABI host core (api.cpp) and the CUDA
+// kernel launchers (*.cu).  Plain structs, no torch types.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace dnnp {
+
+enum Dtype : int { F32 = 0, F64 = 1 };
+
+// A 4-D strided view: extents and element strides (reference tensor.py:104-139).
+struct View4 {
+  int64_t n, c, h, w;
+  int64_t sn, sc, sh, sw;
+  int64_t size() const { return n * c * h * w; }
+};
+
+// Exact unsigned magic division for 32-bit numerators
+// (reference intdiv.py:74-101, Hacker's Delight 2nd ed. ch. 10).
+struct MagicDiv {
+  uint32_t d;     // divisor
+  uint32_t mul;   // multiplier (low 32 bits when add == 1)
+  uint32_t shift;
+  uint32_t add;   // 1 -> 33-bit multiplier, add-corrected form
+};
+MagicDiv make_magic(uint32_t d);
+
+// One convolution problem, shared by forward / backward-data / backward-filter.
+// x is the convolution input (or dx), y the output (or dy); the filter is
+// always dense KCRS (reference conv.py:72-97).
+struct ConvProblem {
+  int64_t N, C, H, W, K, R, S, P, Q;
+  int64_t u, v, pad_h, pad_w;
+  bool flip;  // CONVOLUTION mode: tap r reads h = p*u + (R-1-r) - pad (conv.py:182-192)
+  View4 x, y;
+};
+
+// Launch bookkeeping: every kernel this library launches bumps a counter
+// so benches/tests can prove native kernels ran.
+void note_launch(int count = 1);
+
+// ---- convolution (conv_simt.cu, conv_tc.cu) -------------------------------
+// y := alpha*conv(x,f) + beta*y      (beta == 0: y never read)
+cudaError_t conv_forward(const ConvProblem& p, Dtype dt, const void* x, const void* f,
+                         void* y, double alpha, double beta, int math, cudaStream_t st);
+// dx := conv_bwd_data(dy, f) (+ dx if accumulate)
+cudaError_t conv_backward_data(const ConvProblem& p, Dtype dt, const void* dy, const void* f,
+                               void* dx, bool accumulate, int math, cudaStream_t st);
+// df := conv_bwd_filter(dy, x) (+ df if accumulate)
+cudaError_t conv_backward_filter(const ConvProblem& p, Dtype dt, const void* dy, const void* x,
+                                 void* df, bool accumulate, int math, cudaStream_t st);
+// db[k] = sum_{n,p,q} dy[n,k,p,q]  (dy dtype dt, db dtype dbt)
+cudaError_t conv_backward_bias(const View4& dy, Dtype dt, const void* dyp, const View4& db,
+                               Dtype dbt, void* dbp, cudaStream_t st);
+// whether the tcgen05 path would be used for a forward problem (tests/bench)
+bool tc_eligible(const ConvProblem& p, int pass);
+
+// ---- elementwise / reductions (nnops.cu) -----------------------------------
+cudaError_t activation_forward(int kind, Dtype dt, const View4& xv, const void* x,
+                               const View4& yv, void* y, cudaStream_t st);
+cudaError_t activation_backward(int kind, Dtype dt, const View4& yv, const void* y,
+                                const View4& dyv, const void* dy, const View4& dxv, void* dx,
+                                cudaStream_t st);
+cudaError_t softmax_forward(int mode, Dtype dt, const View4& xv, const void* x,
+                            const View4& yv, void* y, cudaStream_t st);
+cudaError_t softmax_backward(int mode, Dtype dt, const View4& yv, const void* y,
+                             const View4& dyv, const void* dy, const View4& dxv, void* dx,
+                             cudaStream_t st);
+
+struct PoolProblem {
+  int kind;  // 0 max, 1 average
+  int64_t wh, ww, sh, sw, ph, pw;
+  int64_t P, Q;
+};
+cudaError_t pool_forward(const PoolProblem& pp, Dtype dt, const View4& xv, const void* x,
+                         const View4& yv, void* y, int64_t* argmax, cudaStream_t st);
+cudaError_t pool_backward(const PoolProblem& pp, Dtype dt, const View4& dyv, const void* dy,
+                          const View4& dxv, void* dx, const int64_t* argmax,
+                          cudaStream_t st);
+
+// ---- tensor utilities (nnops.cu) -------------------------------------------
+cudaError_t transform(Dtype dt, const View4& sv, const void* s, const View4& dv, void* d,
+                      double alpha, double beta, cudaStream_t st);
+cudaError_t add_broadcast(Dtype dt, const View4& bv, const void* b, const View4& ov, void* o,
+                          double alpha, double beta, cudaStream_t st);
+
+}  // namespace dnnp

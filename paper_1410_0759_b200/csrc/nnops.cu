@@ -1,0 +1,777 @@
+// Bandwidth-bound primitives on strided 4-D views: activation, softmax,
+// pooling (forward + backward), transform, add_broadcast and the conv bias
+// gradient.  Reference semantics: pkg/src/dnnp/nnops.py, tensor.py:241-271,
+// conv.py:754-760.
+//
+// Element-wise ops run either over the raw span (all operands share one dense
+// layout: 128-bit vectorised grid-stride loop) or over rows of the innermost
+// output dimension (any strides: one warp per row, lanes along the row).
+// Roundings follow numpy's evaluation order with explicit _rn intrinsics so
+// that e.g. activation backward, transform and pooling backward are bit-exact.
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+
+#include "common.cuh"
+
+namespace dnnp {
+
+static std::atomic<long long> g_launches{0};
+void note_launch(int count) { g_launches += count; }
+
+MagicDiv make_magic(uint32_t d) {
+  // reference intdiv.py:74-101 (Hacker's Delight unsigned magic numbers)
+  MagicDiv m{d, 1, 0, 0};
+  if (d <= 1) return m;
+  const unsigned __int128 word = (unsigned __int128)1 << 32;
+  const unsigned __int128 nc = (word / d) * d - 1;
+  unsigned __int128 mul = 0;
+  int p = 32;
+  for (; p <= 64; p++) {
+    unsigned __int128 two_p = (unsigned __int128)1 << p;
+    unsigned __int128 rem = (two_p - 1) % d;
+    if (two_p > nc * (d - 1 - rem)) {
+      mul = (two_p + d - 1 - rem) / d;
+      break;
+    }
+  }
+  m.shift = uint32_t(p - 32);
+  if (mul < word) {
+    m.mul = uint32_t(mul);
+    m.add = 0;
+  } else {
+    m.mul = uint32_t(mul - word);
+    m.add = 1;
+  }
+  return m;
+}
+
+// ------------------------------------------------------------ iteration
+
+// An element-wise launch over up to three operands sharing extents; dims are
+// permuted so the output's finest-stride dim is innermost.
+struct EwGeom {
+  int64_t ext[4];
+  int64_t st[3][4];
+  int64_t rows;   // ext[0]*ext[1]*ext[2]
+  MagicDiv d2, d1;  // row decode: r -> (i0, i1, i2)
+  int use_magic;
+};
+
+static EwGeom make_ew(const View4* views[3], int nops, int out_index) {
+  const View4& o = *views[out_index];
+  int64_t oe[4] = {o.n, o.c, o.h, o.w};
+  int64_t os[4] = {o.sn, o.sc, o.sh, o.sw};
+  int perm[4] = {0, 1, 2, 3};
+  // stable sort by |stride| descending, extent-1 dims pushed outward
+  for (int i = 0; i < 4; i++)
+    for (int j = i + 1; j < 4; j++) {
+      auto key = [&](int d) { return oe[d] == 1 ? INT64_MAX : (os[d] < 0 ? -os[d] : os[d]); };
+      if (key(perm[j]) > key(perm[i])) std::swap(perm[i], perm[j]);
+    }
+  EwGeom g;
+  for (int k = 0; k < 4; k++) g.ext[k] = oe[perm[k]];
+  for (int op = 0; op < 3; op++) {
+    if (op >= nops) {
+      for (int k = 0; k < 4; k++) g.st[op][k] = 0;
+      continue;
+    }
+    const View4& v = *views[op];
+    int64_t s[4] = {v.sn, v.sc, v.sh, v.sw};
+    int64_t e[4] = {v.n, v.c, v.h, v.w};
+    for (int k = 0; k < 4; k++) g.st[op][k] = e[perm[k]] == 1 ? 0 : s[perm[k]];
+  }
+  g.rows = g.ext[0] * g.ext[1] * g.ext[2];
+  g.use_magic = g.rows < (int64_t(1) << 32);
+  g.d2 = make_magic(uint32_t(g.ext[2]));
+  g.d1 = make_magic(uint32_t(g.ext[1]));
+  return g;
+}
+
+// shared dense layout: identical strides and span == size
+static bool same_dense(const View4* views[3], int nops) {
+  const View4& a = *views[0];
+  for (int i = 1; i < nops; i++) {
+    const View4& b = *views[i];
+    if (a.sn != b.sn || a.sc != b.sc || a.sh != b.sh || a.sw != b.sw) return false;
+  }
+  int64_t e[4] = {a.n, a.c, a.h, a.w}, s[4] = {a.sn, a.sc, a.sh, a.sw};
+  int64_t maxo = 0;
+  for (int k = 0; k < 4; k++) maxo += (e[k] - 1) * (s[k] > 0 ? s[k] : 0);
+  for (int k = 0; k < 4; k++)
+    if (s[k] < 0) return false;
+  return maxo + 1 == a.size();
+}
+
+template <typename Op, typename T>
+__global__ void __launch_bounds__(256) ew_rows_kernel(EwGeom g, const T* __restrict__ a,
+                                                      const T* __restrict__ b, T* out, Op op) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t r = warp; r < g.rows; r += nwarps) {
+    int64_t i0, i1, i2;
+    if (g.use_magic) {
+      uint32_t q, rem;
+      mdivmod(uint32_t(r), g.d2, q, rem);
+      i2 = rem;
+      uint32_t q2, rem2;
+      mdivmod(q, g.d1, q2, rem2);
+      i1 = rem2;
+      i0 = q2;
+    } else {
+      i2 = r % g.ext[2];
+      int64_t t = r / g.ext[2];
+      i1 = t % g.ext[1];
+      i0 = t / g.ext[1];
+    }
+    int64_t base[3];
+#pragma unroll
+    for (int k = 0; k < 3; k++) base[k] = i0 * g.st[k][0] + i1 * g.st[k][1] + i2 * g.st[k][2];
+    for (int64_t j = lane; j < g.ext[3]; j += 32) {
+      T va = a ? a[base[0] + j * g.st[0][3]] : T(0);
+      T vb = b ? b[base[1] + j * g.st[1][3]] : T(0);
+      T* po = out + base[2] + j * g.st[2][3];
+      *po = op(va, vb, Op::kReadsOut ? *po : T(0));
+    }
+  }
+}
+
+template <typename Op, typename T>
+__global__ void __launch_bounds__(256) ew_dense_kernel(int64_t n, const T* __restrict__ a,
+                                                       const T* __restrict__ b, T* out, Op op,
+                                                       int vec) {
+  const int64_t tid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t nth = int64_t(gridDim.x) * blockDim.x;
+  if (vec) {
+    constexpr int V = 16 / sizeof(T);
+    using Vec = typename std::conditional<sizeof(T) == 4, float4, double2>::type;
+    const int64_t nv = n / V;
+    for (int64_t i = tid; i < nv; i += nth) {
+      Vec va, vb, vo;
+      if (a) va = reinterpret_cast<const Vec*>(a)[i];
+      if (b) vb = reinterpret_cast<const Vec*>(b)[i];
+      if (Op::kReadsOut) vo = reinterpret_cast<const Vec*>(out)[i];
+      const T* pa = reinterpret_cast<const T*>(&va);
+      const T* pb = reinterpret_cast<const T*>(&vb);
+      T* po = reinterpret_cast<T*>(&vo);
+#pragma unroll
+      for (int k = 0; k < V; k++)
+        po[k] = op(a ? pa[k] : T(0), b ? pb[k] : T(0), Op::kReadsOut ? po[k] : T(0));
+      reinterpret_cast<Vec*>(out)[i] = vo;
+    }
+    for (int64_t i = nv * V + tid; i < n; i += nth)
+      out[i] = op(a ? a[i] : T(0), b ? b[i] : T(0), Op::kReadsOut ? out[i] : T(0));
+  } else {
+    for (int64_t i = tid; i < n; i += nth)
+      out[i] = op(a ? a[i] : T(0), b ? b[i] : T(0), Op::kReadsOut ? out[i] : T(0));
+  }
+}
+
+template <typename Op, typename T>
+static cudaError_t run_ew(const View4& va, const T* a, const View4* vb, const T* b,
+                          const View4& vo, T* out, Op op, cudaStream_t st) {
+  const View4* views[3] = {&va, vb ? vb : &va, &vo};
+  const View4* dense_views[3] = {&va, vb ? vb : &vo, &vo};
+  const int64_t n = vo.size();
+  if (n == 0) return cudaSuccess;
+  if (same_dense(dense_views, 3)) {
+    bool aligned = (reinterpret_cast<uintptr_t>(a) % 16 == 0) &&
+                   (!b || reinterpret_cast<uintptr_t>(b) % 16 == 0) &&
+                   (reinterpret_cast<uintptr_t>(out) % 16 == 0);
+    const int V = 16 / sizeof(T);
+    unsigned grid = grid_for(aligned ? ceil_div(n, V) : n, 256, 8);
+    ew_dense_kernel<Op, T><<<grid, 256, 0, st>>>(n, a, b, out, op, aligned ? 1 : 0);
+  } else {
+    EwGeom g = make_ew(views, 3, 2);
+    if (!vb)
+      for (int k = 0; k < 4; k++) g.st[1][k] = 0;
+    unsigned grid = grid_for(g.rows * 32, 256, 16);
+    ew_rows_kernel<Op, T><<<grid, 256, 0, st>>>(g, a, b, out, op);
+  }
+  note_launch();
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------- activation
+
+// reference nnops.py:54-70: stable sigmoid, relu = np.maximum(x, 0) (NaN
+// propagates, -0 -> +0), tanh.
+template <int KIND>
+struct ActFwd {
+  static constexpr bool kReadsOut = false;
+  template <typename T>
+  __device__ T operator()(T x, T, T) const {
+    if (KIND == 1) return (x > T(0) || x != x) ? x : T(0);
+    if (KIND == 2) return tanh(x);
+    T e = exp(-fabs(x));
+    return x >= T(0) ? T(1) / dadd<T>(T(1), e) : e / dadd<T>(T(1), e);
+  }
+};
+// reference nnops.py:73-88, evaluated in numpy's order:
+//   sigmoid (dy*y)*(1-y); relu dy*(y>0); tanh dy*(1-y*y)
+template <int KIND>
+struct ActBwd {
+  static constexpr bool kReadsOut = false;
+  template <typename T>
+  __device__ T operator()(T y, T dy, T) const {
+    if (KIND == 1) return dmul<T>(dy, y > T(0) ? T(1) : T(0));
+    if (KIND == 2) return dmul<T>(dy, dsub<T>(T(1), dmul<T>(y, y)));
+    return dmul<T>(dmul<T>(dy, y), dsub<T>(T(1), y));
+  }
+};
+
+template <typename T>
+static cudaError_t act_fwd_t(int kind, const View4& xv, const T* x, const View4& yv, T* y,
+                             cudaStream_t st) {
+  switch (kind) {
+    case 0: return run_ew(xv, x, nullptr, (const T*)nullptr, yv, y, ActFwd<0>{}, st);
+    case 1: return run_ew(xv, x, nullptr, (const T*)nullptr, yv, y, ActFwd<1>{}, st);
+    default: return run_ew(xv, x, nullptr, (const T*)nullptr, yv, y, ActFwd<2>{}, st);
+  }
+}
+template <typename T>
+static cudaError_t act_bwd_t(int kind, const View4& yv, const T* y, const View4& dyv, const T* dy,
+                             const View4& dxv, T* dx, cudaStream_t st) {
+  switch (kind) {
+    case 0: return run_ew(yv, y, &dyv, dy, dxv, dx, ActBwd<0>{}, st);
+    case 1: return run_ew(yv, y, &dyv, dy, dxv, dx, ActBwd<1>{}, st);
+    default: return run_ew(yv, y, &dyv, dy, dxv, dx, ActBwd<2>{}, st);
+  }
+}
+
+cudaError_t activation_forward(int kind, Dtype dt, const View4& xv, const void* x,
+                               const View4& yv, void* y, cudaStream_t st) {
+  return dt == F32 ? act_fwd_t(kind, xv, (const float*)x, yv, (float*)y, st)
+                   : act_fwd_t(kind, xv, (const double*)x, yv, (double*)y, st);
+}
+cudaError_t activation_backward(int kind, Dtype dt, const View4& yv, const void* y,
+                                const View4& dyv, const void* dy, const View4& dxv, void* dx,
+                                cudaStream_t st) {
+  return dt == F32 ? act_bwd_t(kind, yv, (const float*)y, dyv, (const float*)dy, dxv,
+                               (float*)dx, st)
+                   : act_bwd_t(kind, yv, (const double*)y, dyv, (const double*)dy, dxv,
+                               (double*)dx, st);
+}
+
+// -------------------------------------------------- transform / broadcast
+
+// dst := alpha*src (+ beta*dst): numpy `d *= beta; d += alpha * s`
+// (reference tensor.py:241-251), each product/sum rounded separately.
+template <bool BETA>
+struct Axpby {
+  static constexpr bool kReadsOut = BETA;
+  double alpha, beta;
+  template <typename T>
+  __device__ T operator()(T s, T, T d) const {
+    T as = dmul<T>(s, T(alpha));
+    return BETA ? dadd<T>(dmul<T>(d, T(beta)), as) : as;
+  }
+};
+
+cudaError_t transform(Dtype dt, const View4& sv, const void* s, const View4& dv, void* d,
+                      double alpha, double beta, cudaStream_t st) {
+  if (dt == F32) {
+    if (beta == 0.0)
+      return run_ew(sv, (const float*)s, nullptr, (const float*)nullptr, dv, (float*)d,
+                    Axpby<false>{alpha, beta}, st);
+    return run_ew(sv, (const float*)s, nullptr, (const float*)nullptr, dv, (float*)d,
+                  Axpby<true>{alpha, beta}, st);
+  }
+  if (beta == 0.0)
+    return run_ew(sv, (const double*)s, nullptr, (const double*)nullptr, dv, (double*)d,
+                  Axpby<false>{alpha, beta}, st);
+  return run_ew(sv, (const double*)s, nullptr, (const double*)nullptr, dv, (double*)d,
+                Axpby<true>{alpha, beta}, st);
+}
+
+cudaError_t add_broadcast(Dtype dt, const View4& bv, const void* b, const View4& ov, void* o,
+                          double alpha, double beta, cudaStream_t st) {
+  // broadcast dims of the bias carry stride 0 and the output's extent
+  View4 bb = bv;
+  if (bb.n == 1) { bb.n = ov.n; bb.sn = 0; }
+  if (bb.c == 1) { bb.c = ov.c; bb.sc = 0; }
+  if (bb.h == 1) { bb.h = ov.h; bb.sh = 0; }
+  if (bb.w == 1) { bb.w = ov.w; bb.sw = 0; }
+  const View4* views[3] = {&bb, &bb, &ov};
+  EwGeom g = make_ew(views, 3, 2);
+  // make_ew zeroes strides of extent-1 dims using the op's own extents; the
+  // broadcast view already has stride 0 there.
+  for (int k = 0; k < 4; k++) g.st[1][k] = 0;
+  unsigned grid = grid_for(g.rows * 32, 256, 16);
+  if (dt == F32) {
+    if (beta == 0.0)
+      ew_rows_kernel<Axpby<false>, float><<<grid, 256, 0, st>>>(
+          g, (const float*)b, nullptr, (float*)o, Axpby<false>{alpha, beta});
+    else
+      ew_rows_kernel<Axpby<true>, float><<<grid, 256, 0, st>>>(
+          g, (const float*)b, nullptr, (float*)o, Axpby<true>{alpha, beta});
+  } else {
+    if (beta == 0.0)
+      ew_rows_kernel<Axpby<false>, double><<<grid, 256, 0, st>>>(
+          g, (const double*)b, nullptr, (double*)o, Axpby<false>{alpha, beta});
+    else
+      ew_rows_kernel<Axpby<true>, double><<<grid, 256, 0, st>>>(
+          g, (const double*)b, nullptr, (double*)o, Axpby<true>{alpha, beta});
+  }
+  note_launch();
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- softmax
+//
+// per_image: one group = the (c, h, w) box of one image; per_spatial: one
+// group = the c fibre at one (n, h, w) (reference nnops.py:91-117).
+
+template <typename T>
+__device__ __forceinline__ T warp_max(T v) {
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Group element g (0 <= g < C*H*W) of image n -> offset.
+struct ImgGeom {
+  View4 v;
+  MagicDiv dHW, dW;
+};
+__device__ __forceinline__ int64_t img_off(const ImgGeom& ig, int64_t n, uint32_t g) {
+  uint32_t c, rem, h, w;
+  mdivmod(g, ig.dHW, c, rem);
+  mdivmod(rem, ig.dW, h, w);
+  return n * ig.v.sn + c * ig.v.sc + h * ig.v.sh + w * ig.v.sw;
+}
+
+// Block reduction helpers (256 threads).
+template <typename T>
+__device__ T block_reduce_max(T v, T* sh) {
+  v = warp_max(v);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+  __syncthreads();
+  T r = sh[0];
+  for (int i = 1; i < (int)(blockDim.x >> 5); i++) r = fmax(r, sh[i]);
+  __syncthreads();
+  return r;
+}
+template <typename T>
+__device__ T block_reduce_sum(T v, T* sh) {
+  v = warp_sum(v);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+  __syncthreads();
+  T r = T(0);
+  for (int i = 0; i < (int)(blockDim.x >> 5); i++) r += sh[i];
+  __syncthreads();
+  return r;
+}
+
+// Phase 1 of per-image softmax: each block reduces a chunk of a group to
+// (max, sum exp(x - max)) [forward] or sum(y*dy) [backward].
+template <typename T, bool BWD>
+__global__ void __launch_bounds__(256) softmax_img_partial(ImgGeom ga, const T* a, ImgGeom gb,
+                                                          const T* b, int64_t G, int chunks,
+                                                          T* part) {
+  __shared__ T sh[32];
+  const int64_t n = blockIdx.y;
+  const int64_t per = (G + chunks - 1) / chunks;
+  const int64_t g0 = blockIdx.x * per, g1 = min(G, g0 + per);
+  if (!BWD) {
+    T m = T(-INFINITY);
+    for (int64_t g = g0 + threadIdx.x; g < g1; g += blockDim.x) m = fmax(m, a[img_off(ga, n, g)]);
+    m = block_reduce_max(m, sh);
+    T s = T(0);
+    for (int64_t g = g0 + threadIdx.x; g < g1; g += blockDim.x) s += exp(a[img_off(ga, n, g)] - m);
+    s = block_reduce_sum(s, sh);
+    if (threadIdx.x == 0) {
+      part[(n * chunks + blockIdx.x) * 2] = m;
+      part[(n * chunks + blockIdx.x) * 2 + 1] = s;
+    }
+  } else {
+    T s = T(0);
+    for (int64_t g = g0 + threadIdx.x; g < g1; g += blockDim.x)
+      s += a[img_off(ga, n, g)] * b[img_off(gb, n, g)];
+    s = block_reduce_sum(s, sh);
+    if (threadIdx.x == 0) part[n * chunks + blockIdx.x] = s;
+  }
+}
+
+// Phase 2: combine the partials of the group and write the chunk.
+template <typename T, bool BWD>
+__global__ void __launch_bounds__(256) softmax_img_apply(ImgGeom ga, const T* a, ImgGeom gb,
+                                                        const T* b, ImgGeom go, T* o, int64_t G,
+                                                        int chunks, const T* part) {
+  const int64_t n = blockIdx.y;
+  const int64_t per = (G + chunks - 1) / chunks;
+  const int64_t g0 = blockIdx.x * per, g1 = min(G, g0 + per);
+  if (!BWD) {
+    T M = T(-INFINITY);
+    for (int i = 0; i < chunks; i++) M = fmax(M, part[(n * chunks + i) * 2]);
+    T S = T(0);
+    for (int i = 0; i < chunks; i++) {
+      T mi = part[(n * chunks + i) * 2];
+      S += part[(n * chunks + i) * 2 + 1] * exp(mi - M);
+    }
+    for (int64_t g = g0 + threadIdx.x; g < g1; g += blockDim.x)
+      o[img_off(go, n, g)] = exp(a[img_off(ga, n, g)] - M) / S;
+  } else {
+    T D = T(0);
+    for (int i = 0; i < chunks; i++) D += part[n * chunks + i];
+    for (int64_t g = g0 + threadIdx.x; g < g1; g += blockDim.x) {
+      T yv = a[img_off(ga, n, g)];
+      o[img_off(go, n, g)] = dmul<T>(yv, dsub<T>(b[img_off(gb, n, g)], D));
+    }
+  }
+}
+
+// per_spatial: one thread per (n, h, w) position, loop over channels.
+struct PosGeom {
+  View4 v;
+  MagicDiv dHW, dW;
+};
+__device__ __forceinline__ int64_t pos_base(const PosGeom& pg, uint32_t pos) {
+  uint32_t n, rem, h, w;
+  mdivmod(pos, pg.dHW, n, rem);
+  mdivmod(rem, pg.dW, h, w);
+  return n * pg.v.sn + h * pg.v.sh + w * pg.v.sw;
+}
+
+template <typename T, bool BWD>
+__global__ void __launch_bounds__(256) softmax_spatial(PosGeom ga, const T* a, PosGeom gb,
+                                                      const T* b, PosGeom go, T* o, int64_t npos,
+                                                      int64_t C) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t pos = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; pos < npos; pos += stride) {
+    const int64_t ba = pos_base(ga, pos), bo = pos_base(go, pos);
+    if (!BWD) {
+      T m = T(-INFINITY);
+      for (int64_t c = 0; c < C; c++) m = fmax(m, a[ba + c * ga.v.sc]);
+      T s = T(0);
+      for (int64_t c = 0; c < C; c++) s += exp(a[ba + c * ga.v.sc] - m);
+      for (int64_t c = 0; c < C; c++) o[bo + c * go.v.sc] = exp(a[ba + c * ga.v.sc] - m) / s;
+    } else {
+      const int64_t bb = pos_base(gb, pos);
+      T d = T(0);
+      for (int64_t c = 0; c < C; c++) d += a[ba + c * ga.v.sc] * b[bb + c * gb.v.sc];
+      for (int64_t c = 0; c < C; c++)
+        o[bo + c * go.v.sc] = dmul<T>(a[ba + c * ga.v.sc], dsub<T>(b[bb + c * gb.v.sc], d));
+    }
+  }
+}
+
+static ImgGeom img_geom(const View4& v) {
+  return ImgGeom{v, make_magic(uint32_t(v.h * v.w)), make_magic(uint32_t(v.w))};
+}
+static PosGeom pos_geom(const View4& v) {
+  return PosGeom{v, make_magic(uint32_t(v.h * v.w)), make_magic(uint32_t(v.w))};
+}
+
+template <typename T, bool BWD>
+static cudaError_t softmax_t(int mode, const View4& av, const T* a, const View4* bv, const T* b,
+                             const View4& ov, T* o, cudaStream_t st) {
+  if (av.c * av.h * av.w >= (int64_t(1) << 32) || av.n * av.h * av.w >= (int64_t(1) << 32))
+    return cudaErrorInvalidValue;
+  if (mode == 0) {
+    const int64_t G = av.c * av.h * av.w;
+    // enough blocks to fill the GPU, at least ~2K elements per block
+    int64_t chunks = ceil_div(int64_t(kNumSMs) * 4, av.n);
+    chunks = std::max<int64_t>(1, std::min<int64_t>(chunks, ceil_div(G, 2048)));
+    chunks = std::min<int64_t>(chunks, 65535);
+    T* part = nullptr;
+    cudaError_t e = cudaMallocAsync(&part, sizeof(T) * 2 * av.n * chunks, st);
+    if (e != cudaSuccess) return e;
+    dim3 grid(unsigned(chunks), unsigned(av.n));
+    ImgGeom ga = img_geom(av), gb = img_geom(bv ? *bv : av), go = img_geom(ov);
+    softmax_img_partial<T, BWD><<<grid, 256, 0, st>>>(ga, a, gb, b, G, int(chunks), part);
+    softmax_img_apply<T, BWD><<<grid, 256, 0, st>>>(ga, a, gb, b, go, o, G, int(chunks), part);
+    note_launch(2);
+    e = cudaGetLastError();
+    cudaFreeAsync(part, st);
+    return e;
+  }
+  const int64_t npos = av.n * av.h * av.w;
+  softmax_spatial<T, BWD><<<grid_for(npos, 256, 8), 256, 0, st>>>(
+      pos_geom(av), a, pos_geom(bv ? *bv : av), b, pos_geom(ov), o, npos, av.c);
+  note_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t softmax_forward(int mode, Dtype dt, const View4& xv, const void* x, const View4& yv,
+                            void* y, cudaStream_t st) {
+  return dt == F32 ? softmax_t<float, false>(mode, xv, (const float*)x, nullptr, nullptr, yv,
+                                             (float*)y, st)
+                   : softmax_t<double, false>(mode, xv, (const double*)x, nullptr, nullptr, yv,
+                                              (double*)y, st);
+}
+cudaError_t softmax_backward(int mode, Dtype dt, const View4& yv, const void* y,
+                             const View4& dyv, const void* dy, const View4& dxv, void* dx,
+                             cudaStream_t st) {
+  return dt == F32 ? softmax_t<float, true>(mode, yv, (const float*)y, &dyv, (const float*)dy,
+                                            dxv, (float*)dx, st)
+                   : softmax_t<double, true>(mode, yv, (const double*)y, &dyv,
+                                             (const double*)dy, dxv, (double*)dx, st);
+}
+
+// ---------------------------------------------------------------- pooling
+
+struct PoolGeom {
+  View4 x, y;  // y: pooled output (or dy)
+  int64_t N, C, H, W, P, Q;
+  int64_t wh, ww, sh, sw, ph, pw;
+  MagicDiv dQ, dP, dC, dW, dH;
+};
+
+// Forward: one thread per pooled element; window clipped to the image
+// (reference nnops.py:150-200).  Max takes the first maximum in (h, w) scan
+// order with numpy argmax NaN semantics (the first NaN wins); argmax is the
+// LOGICAL NCHW index.  Average divides by the in-image count.
+template <typename T>
+__global__ void __launch_bounds__(256) pool_fwd_kernel(PoolGeom g, const T* __restrict__ x,
+                                                       T* __restrict__ y, int64_t* argmax,
+                                                       int kind, int64_t total) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += stride) {
+    uint32_t t, q, p, c, n;
+    mdivmod(uint32_t(i), g.dQ, t, q);
+    mdivmod(t, g.dP, t, p);
+    mdivmod(t, g.dC, n, c);
+    const int64_t hs0 = int64_t(p) * g.sh - g.ph, ws0 = int64_t(q) * g.sw - g.pw;
+    const int64_t hs = max(int64_t(0), hs0), he = min(g.H, hs0 + g.wh);
+    const int64_t ws = max(int64_t(0), ws0), we = min(g.W, ws0 + g.ww);
+    const T* xb = x + int64_t(n) * g.x.sn + int64_t(c) * g.x.sc;
+    T out;
+    if (kind == 0) {
+      T best = xb[hs * g.x.sh + ws * g.x.sw];
+      int64_t bh = hs, bw = ws;
+      for (int64_t h = hs; h < he; h++)
+        for (int64_t w = ws; w < we; w++) {
+          T v = xb[h * g.x.sh + w * g.x.sw];
+          if (best != best) continue;  // a NaN already won
+          if (v != v || v > best) {
+            best = v;
+            bh = h;
+            bw = w;
+          }
+        }
+      out = best;
+      if (argmax) argmax[i] = ((int64_t(n) * g.C + c) * g.H + bh) * g.W + bw;
+    } else {
+      T s = T(0);
+      for (int64_t h = hs; h < he; h++)
+        for (int64_t w = ws; w < we; w++) s = dadd<T>(s, xb[h * g.x.sh + w * g.x.sw]);
+      out = s / T((he - hs) * (we - ws));
+    }
+    y[int64_t(n) * g.y.sn + int64_t(c) * g.y.sc + int64_t(p) * g.y.sh + int64_t(q) * g.y.sw] = out;
+  }
+}
+
+// Backward as a gather over the windows covering each input element, in
+// ascending (p, q) order starting from 0: this is exactly the summation
+// order of the reference's zero-fill + np.add.at / per-window += loops
+// (nnops.py:218-246), so max and average backward are bit-exact.
+template <typename T>
+__global__ void __launch_bounds__(256) pool_bwd_kernel(PoolGeom g, const T* __restrict__ dy,
+                                                       T* __restrict__ dx,
+                                                       const int64_t* __restrict__ argmax,
+                                                       int kind, int64_t total) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += stride) {
+    uint32_t t, w, h, c, n;
+    mdivmod(uint32_t(i), g.dW, t, w);
+    mdivmod(t, g.dH, t, h);
+    mdivmod(t, g.dC, n, c);
+    // p covers h iff p*sh - ph <= h < p*sh - ph + wh
+    const int64_t hp = int64_t(h) + g.ph, wp = int64_t(w) + g.pw;
+    int64_t p0 = hp - g.wh + 1 > 0 ? (hp - g.wh + 1 + g.sh - 1) / g.sh : 0;
+    int64_t p1 = min(g.P - 1, hp / g.sh);
+    int64_t q0 = wp - g.ww + 1 > 0 ? (wp - g.ww + 1 + g.sw - 1) / g.sw : 0;
+    int64_t q1 = min(g.Q - 1, wp / g.sw);
+    const int64_t plane = int64_t(n) * g.C + c;
+    const int64_t me = (plane * g.H + h) * g.W + w;
+    T acc = T(0);
+    for (int64_t p = p0; p <= p1; p++)
+      for (int64_t q = q0; q <= q1; q++) {
+        const int64_t oi = (plane * g.P + p) * g.Q + q;
+        const T d = dy[int64_t(n) * g.y.sn + int64_t(c) * g.y.sc + p * g.y.sh + q * g.y.sw];
+        if (kind == 0) {
+          if (argmax[oi] == me) acc = dadd<T>(acc, d);
+        } else {
+          const int64_t hs0 = p * g.sh - g.ph, ws0 = q * g.sw - g.pw;
+          const int64_t cnt = (min(g.H, hs0 + g.wh) - max(int64_t(0), hs0)) *
+                              (min(g.W, ws0 + g.ww) - max(int64_t(0), ws0));
+          acc = dadd<T>(acc, d / T(cnt));
+        }
+      }
+    dx[int64_t(n) * g.x.sn + int64_t(c) * g.x.sc + int64_t(h) * g.x.sh + int64_t(w) * g.x.sw] = acc;
+  }
+}
+
+// Flags argmax entries that do not point inside their own window (only
+// possible for caller-made argmax buffers); those take the serial path.
+__global__ void pool_argmax_check(PoolGeom g, const int64_t* __restrict__ argmax, int64_t total,
+                                  int* bad) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += stride) {
+    const int64_t q = i % g.Q, p = (i / g.Q) % g.P, plane = i / (g.Q * g.P);
+    const int64_t a = argmax[i];
+    const int64_t hw = a - plane * g.H * g.W;
+    bool ok = hw >= 0 && hw < g.H * g.W;
+    if (ok) {
+      const int64_t h = hw / g.W, w = hw % g.W;
+      const int64_t hs0 = p * g.sh - g.ph, ws0 = q * g.sw - g.pw;
+      ok = h >= hs0 && h < hs0 + g.wh && w >= ws0 && w < ws0 + g.ww;
+    }
+    if (!ok) *bad = 1;
+  }
+}
+
+// Serial reference-order scatter (np.add.at in flat (n,c,p,q) order).
+template <typename T>
+__global__ void pool_bwd_serial(PoolGeom g, const T* dy, T* dx, const int64_t* argmax,
+                                int64_t total, const int* bad) {
+  if (!*bad || threadIdx.x != 0 || blockIdx.x != 0) return;
+  // reset dx (the gather pass wrote it) then scatter in order
+  for (int64_t i = 0; i < g.N * g.C * g.H * g.W; i++) {
+    int64_t w = i % g.W, h = (i / g.W) % g.H, c = (i / (g.W * g.H)) % g.C, n = i / (g.W * g.H * g.C);
+    dx[voff(g.x, n, c, h, w)] = T(0);
+  }
+  const int64_t limit = g.N * g.C * g.H * g.W;
+  for (int64_t i = 0; i < total; i++) {
+    int64_t a = argmax[i];
+    if (a < 0 || a >= limit) continue;
+    int64_t w = a % g.W, h = (a / g.W) % g.H, c = (a / (g.W * g.H)) % g.C, n = a / (g.W * g.H * g.C);
+    const int64_t q = i % g.Q, p = (i / g.Q) % g.P, pc = (i / (g.Q * g.P)) % g.C,
+                  pn = i / (g.Q * g.P * g.C);
+    T* t = dx + voff(g.x, n, c, h, w);
+    *t = dadd<T>(*t, dy[voff(g.y, pn, pc, p, q)]);
+  }
+}
+
+static PoolGeom pool_geom(const PoolProblem& pp, const View4& xv, const View4& yv) {
+  PoolGeom g;
+  g.x = xv;
+  g.y = yv;
+  g.N = xv.n; g.C = xv.c; g.H = xv.h; g.W = xv.w; g.P = pp.P; g.Q = pp.Q;
+  g.wh = pp.wh; g.ww = pp.ww; g.sh = pp.sh; g.sw = pp.sw; g.ph = pp.ph; g.pw = pp.pw;
+  g.dQ = make_magic(uint32_t(pp.Q));
+  g.dP = make_magic(uint32_t(pp.P));
+  g.dC = make_magic(uint32_t(xv.c));
+  g.dW = make_magic(uint32_t(xv.w));
+  g.dH = make_magic(uint32_t(xv.h));
+  return g;
+}
+
+cudaError_t pool_forward(const PoolProblem& pp, Dtype dt, const View4& xv, const void* x,
+                         const View4& yv, void* y, int64_t* argmax, cudaStream_t st) {
+  const int64_t total = yv.size();
+  if (total >= (int64_t(1) << 32) || xv.size() >= (int64_t(1) << 32))
+    return cudaErrorInvalidValue;
+  PoolGeom g = pool_geom(pp, xv, yv);
+  unsigned grid = grid_for(total, 256, 8);
+  if (dt == F32)
+    pool_fwd_kernel<float><<<grid, 256, 0, st>>>(g, (const float*)x, (float*)y, argmax, pp.kind,
+                                                 total);
+  else
+    pool_fwd_kernel<double><<<grid, 256, 0, st>>>(g, (const double*)x, (double*)y, argmax,
+                                                  pp.kind, total);
+  note_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t pool_backward(const PoolProblem& pp, Dtype dt, const View4& dyv, const void* dy,
+                          const View4& dxv, void* dx, const int64_t* argmax, cudaStream_t st) {
+  const int64_t total = dxv.size(), ptotal = dyv.size();
+  if (total >= (int64_t(1) << 32) || ptotal >= (int64_t(1) << 32)) return cudaErrorInvalidValue;
+  PoolGeom g = pool_geom(pp, dxv, dyv);
+  unsigned grid = grid_for(total, 256, 8);
+  if (dt == F32)
+    pool_bwd_kernel<float><<<grid, 256, 0, st>>>(g, (const float*)dy, (float*)dx, argmax,
+                                                 pp.kind, total);
+  else
+    pool_bwd_kernel<double><<<grid, 256, 0, st>>>(g, (const double*)dy, (double*)dx, argmax,
+                                                  pp.kind, total);
+  note_launch();
+  if (pp.kind == 0) {
+    int* bad = nullptr;
+    cudaError_t e = cudaMallocAsync(&bad, sizeof(int), st);
+    if (e != cudaSuccess) return e;
+    cudaMemsetAsync(bad, 0, sizeof(int), st);
+    pool_argmax_check<<<grid_for(ptotal, 256, 4), 256, 0, st>>>(g, argmax, ptotal, bad);
+    if (dt == F32)
+      pool_bwd_serial<float><<<1, 32, 0, st>>>(g, (const float*)dy, (float*)dx, argmax, ptotal,
+                                               bad);
+    else
+      pool_bwd_serial<double><<<1, 32, 0, st>>>(g, (const double*)dy, (double*)dx, argmax,
+                                                ptotal, bad);
+    note_launch(2);
+    cudaFreeAsync(bad, st);
+  }
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------- conv bias gradient
+//
+// db[k] = sum_{n,p,q} dy[n,k,p,q] (reference conv.py:754-760).  Two
+// deterministic phases: K x S blocks reduce contiguous slices of the
+// (n, p, q) range, then one thread per k adds the S partials in order.
+template <typename T>
+__global__ void __launch_bounds__(256) bias_partial(View4 v, const T* __restrict__ dy, int S,
+                                                    MagicDiv dPQ, MagicDiv dQ, T* part) {
+  __shared__ T sh[32];
+  const int64_t k = blockIdx.y;
+  const int64_t L = v.n * v.h * v.w;
+  const int64_t per = (L + S - 1) / S;
+  const int64_t j0 = blockIdx.x * per, j1 = min(L, j0 + per);
+  T s = T(0);
+  for (int64_t j = j0 + threadIdx.x; j < j1; j += blockDim.x) {
+    uint32_t n, rem, p, q;
+    mdivmod(uint32_t(j), dPQ, n, rem);
+    mdivmod(rem, dQ, p, q);
+    s += dy[n * v.sn + k * v.sc + p * v.sh + q * v.sw];
+  }
+  s = block_reduce_sum(s, sh);
+  if (threadIdx.x == 0) part[k * S + blockIdx.x] = s;
+}
+template <typename T, typename TO>
+__global__ void bias_final(const T* part, int S, int64_t K, View4 ov, TO* db) {
+  int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= K) return;
+  T s = T(0);
+  for (int i = 0; i < S; i++) s += part[k * S + i];
+  db[k * ov.sc] = TO(s);
+}
+
+template <typename T>
+static cudaError_t bias_t(const View4& v, const T* dy, const View4& ov, Dtype dbt, void* db,
+                          cudaStream_t st) {
+  const int64_t L = v.n * v.h * v.w;
+  if (L >= (int64_t(1) << 32)) return cudaErrorInvalidValue;
+  int64_t S = std::max<int64_t>(1, ceil_div(int64_t(kNumSMs) * 8, v.c));
+  S = std::min<int64_t>(S, std::max<int64_t>(1, ceil_div(L, 1024)));
+  T* part = nullptr;
+  cudaError_t e = cudaMallocAsync(&part, sizeof(T) * v.c * S, st);
+  if (e != cudaSuccess) return e;
+  bias_partial<T><<<dim3(unsigned(S), unsigned(v.c)), 256, 0, st>>>(
+      v, dy, int(S), make_magic(uint32_t(v.h * v.w)), make_magic(uint32_t(v.w)), part);
+  unsigned g = unsigned(ceil_div(v.c, 128));
+  if (dbt == F32)
+    bias_final<T, float><<<g, 128, 0, st>>>(part, int(S), v.c, ov, (float*)db);
+  else
+    bias_final<T, double><<<g, 128, 0, st>>>(part, int(S), v.c, ov, (double*)db);
+  note_launch(2);
+  e = cudaGetLastError();
+  cudaFreeAsync(part, st);
+  return e;
+}
+
+cudaError_t conv_backward_bias(const View4& dyv, Dtype dt, const void* dy, const View4& dbv,
+                               Dtype dbt, void* db, cudaStream_t st) {
+  return dt == F32 ? bias_t(dyv, (const float*)dy, dbv, dbt, db, st)
+                   : bias_t(dyv, (const double*)dy, dbv, dbt, db, st);
+}
+
+}  // namespace dnnp
+
+extern "C" int64_t dnnp_kernel_launch_count(void) { return dnnp::g_launches.load(); }
