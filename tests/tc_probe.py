@@ -49,15 +49,20 @@ def main():
             ry = np.zeros(N * K * P * Q, np.float32)
             orc.conv_forward(xg, x, [K, C, R, S], f, cg, yg, ry, threads=8)
             ef = orc.rel_err(yv.buf.cpu().numpy(), ry)
-            ed = -1.0
-            if u == 1:
-                dp.conv_backward_data(dyv, fv, cd, "implicit", dxv)
-                torch.cuda.synchronize()
-                rdx = np.zeros(N * C * H * W, np.float32)
-                orc.conv_backward_data([K, C, R, S], f, yg, dy, cg, xg, rdx)
-                ed = orc.rel_err(dxv.buf.cpu().numpy(), rdx)
-            print(f"{(N, C, H, W, K, R, S, u, pad)} {mode[:4]} fwd_err={ef:.2e} dgrad_err={ed:.2e}",
-                  flush=True)
+            dp.conv_backward_data(dyv, fv, cd, "implicit", dxv)
+            torch.cuda.synchronize()
+            rdx = np.zeros(N * C * H * W, np.float32)
+            orc.conv_backward_data([K, C, R, S], f, yg, dy, cg, xg, rdx)
+            ed = orc.rel_err(dxv.buf.cpu().numpy(), rdx)
+            dft = torch.zeros(K * C * R * S, device="cuda")
+            dfv = dp.FilterView(dp.make_filter_desc(K, C, R, S), dft)
+            dp.conv_backward_filter(dyv, xv, cd, "implicit", dfv)
+            torch.cuda.synchronize()
+            rdf = np.zeros(K * C * R * S, np.float32)
+            orc.conv_backward_filter(xg, x, yg, dy, cg, [K, C, R, S], rdf, threads=8)
+            ew = orc.rel_err(dft.cpu().numpy(), rdf)
+            print(f"{(N, C, H, W, K, R, S, u, pad)} {mode[:4]} fwd_err={ef:.2e} "
+                  f"dgrad_err={ed:.2e} wgrad_err={ew:.2e}", flush=True)
 
 
 if __name__ == "__main__":
