@@ -1,0 +1,37 @@
+// Shared host/device helpers of the tensor-core convolution kernels.
+#pragma once
+#include <cuda_bf16.h>
+
+#include "common.cuh"
+
+namespace dnnp {
+namespace tc {
+
+// fp32 -> (hi, lo) bf16 pair, a ~= hi + lo with 16 mantissa bits
+__device__ __forceinline__ void split_bf16(float v, __nv_bfloat16& hi, __nv_bfloat16& lo) {
+  hi = __float2bfloat16_rn(v);
+  lo = __float2bfloat16_rn(v - __bfloat162float(hi));
+}
+
+// Stream-ordered scratch allocation released at scope exit (the pool keeps
+// the memory, so steady-state calls do not hit the driver).
+struct Workspace {
+  void* p = nullptr;
+  cudaStream_t st;
+  explicit Workspace(cudaStream_t s) : st(s) {}
+  ~Workspace() {
+    if (p) cudaFreeAsync(p, st);
+  }
+  Workspace(const Workspace&) = delete;
+  Workspace& operator=(const Workspace&) = delete;
+};
+
+void pool_keep_memory();
+
+// Strided fp32 4-D view -> channel-innermost bf16 hi/lo planes
+// [n][h][w][Cp] (Cp = channels padded to a multiple of 8, zero filled).
+cudaError_t pack_act(const View4& v, const float* x, int Cp, __nv_bfloat16* hi, __nv_bfloat16* lo,
+                     cudaStream_t st);
+
+}  // namespace tc
+}  // namespace dnnp

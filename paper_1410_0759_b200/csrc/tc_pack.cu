@@ -1,0 +1,83 @@
+// Operand packing for the tensor-core convolution: strided fp32 activations
+// -> channel-innermost BF16 hi/lo planes, staged through shared memory so
+// that both the (pixel-contiguous) reads and the (channel-contiguous)
+// 16-byte writes are coalesced.
+#include "tc_common.cuh"
+
+namespace dnnp {
+namespace tc {
+
+namespace {
+
+constexpr int kPix = 64;   // pixels per tile
+constexpr int kCh = 64;    // channels per slab
+
+__global__ void __launch_bounds__(256) pack_act_kernel(View4 v, const float* __restrict__ x, int Cp,
+                                                       __nv_bfloat16* __restrict__ hi,
+                                                       __nv_bfloat16* __restrict__ lo, int64_t npix,
+                                                       MagicDiv dHW, MagicDiv dW) {
+  __shared__ float tile[kPix][kCh + 1];
+  const int tp = threadIdx.x & 63, tcg = threadIdx.x >> 6;
+  const int64_t ntiles = (npix + kPix - 1) / kPix;
+  const int nslabs = (Cp + kCh - 1) / kCh;
+  for (int64_t job = blockIdx.x; job < ntiles * nslabs; job += gridDim.x) {
+    const int64_t pt = job / nslabs;
+    const int slab = int(job % nslabs);
+    const int c_lo = slab * kCh, nch = min(kCh, Cp - c_lo);
+    const int64_t pix = pt * kPix + tp;
+    if (pix < npix) {
+      uint32_t n, rem, h, w;
+      mdivmod(uint32_t(pix), dHW, n, rem);
+      mdivmod(rem, dW, h, w);
+      const float* src = x + int64_t(n) * v.sn + int64_t(h) * v.sh + int64_t(w) * v.sw;
+      for (int c = tcg; c < nch; c += 4) {
+        const int cc = c_lo + c;
+        tile[tp][c] = cc < v.c ? __ldg(src + int64_t(cc) * v.sc) : 0.0f;
+      }
+    }
+    __syncthreads();
+    const int groups = nch / 8;
+    for (int q = threadIdx.x; q < kPix * groups; q += blockDim.x) {
+      const int p = q / groups, g = q % groups;
+      const int64_t opix = pt * kPix + p;
+      if (opix >= npix) continue;
+      __align__(16) __nv_bfloat16 vh[8], vl[8];
+#pragma unroll
+      for (int k = 0; k < 8; k++) split_bf16(tile[p][g * 8 + k], vh[k], vl[k]);
+      const int64_t o = opix * Cp + c_lo + g * 8;
+      *reinterpret_cast<uint4*>(hi + o) = *reinterpret_cast<const uint4*>(vh);
+      *reinterpret_cast<uint4*>(lo + o) = *reinterpret_cast<const uint4*>(vl);
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace
+
+void pool_keep_memory() {
+  static bool done = false;
+  if (done) return;
+  done = true;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+}
+
+cudaError_t pack_act(const View4& v, const float* x, int Cp, __nv_bfloat16* hi, __nv_bfloat16* lo,
+                     cudaStream_t st) {
+  const int64_t npix = v.n * v.h * v.w;
+  if (npix >= (int64_t(1) << 32)) return cudaErrorInvalidValue;
+  const int64_t jobs = ceil_div(npix, kPix) * ceil_div(Cp, kCh);
+  const unsigned grid = unsigned(std::min<int64_t>(jobs, int64_t(kNumSMs) * 16));
+  pack_act_kernel<<<grid, 256, 0, st>>>(v, x, Cp, hi, lo, npix, make_magic(uint32_t(v.h * v.w)),
+                                        make_magic(uint32_t(v.w)));
+  note_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace tc
+}  // namespace dnnp

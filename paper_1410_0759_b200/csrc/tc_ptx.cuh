@@ -86,6 +86,17 @@ __device__ __forceinline__ uint64_t desc_kmajor_sw128(uint32_t smem_addr) {
   d |= uint64_t(2) << 61;
   return d;
 }
+// K-major operand tile, 64-byte swizzle: rows of 32 bf16 (64 B), 8-row
+// atoms of 512 B (SBO = 512 B), layout type 4 (SWIZZLE_64B).
+__device__ __forceinline__ uint64_t desc_kmajor_sw64(uint32_t smem_addr) {
+  uint64_t d = 0;
+  d |= uint64_t((smem_addr >> 4) & 0x3FFF);
+  d |= uint64_t(1) << 16;
+  d |= uint64_t(512 >> 4) << 32;
+  d |= uint64_t(1) << 46;
+  d |= uint64_t(4) << 61;
+  return d;
+}
 // MN-major operand tile, 128-byte swizzle: 64 MN-contiguous bf16 per 128 B
 // row, 8 K-rows per 1024 B atom; LBO = byte stride between 64-wide MN
 // blocks, SBO = byte stride between 8-row K groups.

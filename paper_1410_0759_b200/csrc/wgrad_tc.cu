@@ -1,0 +1,333 @@
+// tcgen05 backward-filter convolution, fp32 via the BF16x3 split.
+//
+// dW[k][(dh, dw, c)] = sum over output pixels g of dy[g][k] * x[g + (dh,dw)][c]
+// (reference conv.py:710-717: gemm(dy_map [K x NPQ], lowered^T [NPQ x CRS])).
+// GEMM rows = output channels k, columns = the forward reduction order
+// (tap, channel), reduction = pixels, split over gridDim.z (split-K).
+//   A = packed dy [pixel][Kp]: MN-major (the k of one pixel are contiguous)
+//   B = im2col of packed x: MN-major, 8 channels of one tap per 16-byte
+//       chunk gathered per pixel through the chunk table (zero-fill outside)
+// Stages hold 32 pixels in 128B-swizzled MN-major tiles.  Every split writes
+// its partial tile to a workspace; wgrad_reduce sums the splits in fixed order
+// and scatters into the KCRS filter (deterministic; accumulate adds last).
+#include <algorithm>
+
+#include "tc_common.cuh"
+#include "tc_ptx.cuh"
+
+namespace dnnp {
+namespace tc {
+namespace {
+
+constexpr int kThreads = 160;  // 4 producer warps + MMA warp (epilogue reuses producers)
+constexpr int kPx = 32;        // pixels (reduction rows) per stage
+
+struct WgParams {
+  int64_t NPQ;
+  int64_t pix_per_split;
+  int P, Q, H, W;
+  int u, v, pad_h, pad_w;
+  int Kp, Cp;
+  int KC;
+  int ncol_p, mrows_p;
+  const uint32_t* ctab;
+  const __nv_bfloat16* dy_hi;
+  const __nv_bfloat16* dy_lo;
+  const __nv_bfloat16* x_hi;
+  const __nv_bfloat16* x_lo;
+  float* ws;
+  MagicDiv dPQ, dQ;
+};
+
+template <int BN>
+struct WCfg {
+  static constexpr uint32_t LBO = (kPx / 8) * 1024;  // stride of 64-wide MN blocks
+  static constexpr uint32_t SBO = 1024;              // stride of 8-pixel K groups
+  static constexpr int A_BYTES = 2 * LBO;            // 128 channels
+  static constexpr int B_BYTES = (BN / 64) * LBO;
+  static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
+  static constexpr int STAGES =
+      (200 * 1024) / STAGE_BYTES > 8 ? 8 : (200 * 1024) / STAGE_BYTES;
+  static constexpr int LAG = STAGES >= 6 ? 3 : (STAGES >= 4 ? 2 : 1);
+  static constexpr int TMEM_COLS = BN <= 64 ? 64 : (BN <= 128 ? 128 : 256);
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+};
+
+template <int BN>
+__device__ __forceinline__ uint32_t mn_off(int mn_chunk, int kp) {
+  const int blk = mn_chunk >> 3, jj = mn_chunk & 7;
+  return uint32_t(blk * WCfg<BN>::LBO + (kp >> 3) * 1024 + (kp & 7) * 128 + ((jj ^ (kp & 7)) << 4));
+}
+
+template <int BN>
+__global__ void __launch_bounds__(kThreads, 1) wgrad_tc_kernel(const __grid_constant__ WgParams P) {
+  using C = WCfg<BN>;
+  constexpr int S = C::STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * C::STAGE_BYTES);
+  uint64_t* empty = full + S;
+  uint64_t* tmem_full = empty + S;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.x * 128;
+  const int n0 = blockIdx.y * BN;
+  const int64_t pbeg = int64_t(blockIdx.z) * P.pix_per_split;
+  const int64_t pend = min(P.NPQ, pbeg + P.pix_per_split);
+  const int nkb = pend > pbeg ? int((pend - pbeg + kPx - 1) / kPx) : 0;
+
+  if (warp == 4) {
+    if (lane == 0) {
+      for (int s = 0; s < S; s++) {
+        ptx::mbar_init(&full[s], 128);
+        ptx::mbar_init(&empty[s], 1);
+      }
+      ptx::mbar_init(tmem_full, 1);
+      ptx::fence_mbar_init();
+    }
+    __syncwarp();
+    ptx::tmem_alloc<C::TMEM_COLS>(tmem_slot);
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem_d = *tmem_slot;
+  const uint32_t smem0 = ptx::smem_u32(smem);
+
+  if (warp < 4) {
+    const int t = threadIdx.x;
+    const int kp = t & (kPx - 1), qd = t >> 5;  // pixel of the stage, quarter of the chunks
+    for (int kb = 0; kb < nkb; kb++) {
+      const int s = kb % S;
+      if (kb >= S) ptx::mbar_wait(&empty[s], ((kb / S) - 1) & 1);
+      const uint32_t sa_hi = smem0 + s * C::STAGE_BYTES;
+      const uint32_t sa_lo = sa_hi + C::A_BYTES;
+      const uint32_t sb_hi = sa_lo + C::A_BYTES;
+      const uint32_t sb_lo = sb_hi + C::B_BYTES;
+      const int64_t g = pbeg + int64_t(kb) * kPx + kp;
+      const bool pix_ok = g < pend;
+      uint32_t n = 0, pp = 0, qq = 0;
+      if (pix_ok) {
+        uint32_t rem;
+        mdivmod(uint32_t(g), P.dPQ, n, rem);
+        mdivmod(rem, P.dQ, pp, qq);
+      }
+#pragma unroll
+      for (int jj = 0; jj < 4; jj++) {  // A: 4 of the 16 channel chunks
+        const int j = qd * 4 + jj;
+        const int c0 = m0 + j * 8;
+        const bool ok = pix_ok && c0 < P.Kp;
+        const int64_t src = ok ? g * P.Kp + c0 : 0;
+        const uint32_t dst = mn_off<BN>(j, kp);
+        ptx::cp_async16(sa_hi + dst, P.dy_hi + src, ok ? 16u : 0u);
+        ptx::cp_async16(sa_lo + dst, P.dy_lo + src, ok ? 16u : 0u);
+      }
+      const int ih0 = int(pp) * P.u - P.pad_h, iw0 = int(qq) * P.v - P.pad_w;
+      const int64_t pix0 = int64_t(n) * P.H * P.W;
+#pragma unroll
+      for (int jj = 0; jj < BN / 32; jj++) {  // B: a quarter of the BN/8 column chunks
+        const int j = qd * (BN / 32) + jj;
+        const int ch = n0 / 8 + j;
+        bool ok = pix_ok && ch < P.KC;
+        int64_t src = 0;
+        if (ok) {
+          const uint32_t e = __ldg(P.ctab + ch);
+          const int ih = ih0 + int(e >> 24), iw = iw0 + int((e >> 16) & 255);
+          ok = unsigned(ih) < unsigned(P.H) && unsigned(iw) < unsigned(P.W);
+          src = (pix0 + int64_t(ih) * P.W + iw) * P.Cp + (e & 0xFFFF);
+        }
+        const uint32_t dst = mn_off<BN>(j, kp);
+        ptx::cp_async16(sb_hi + dst, P.x_hi + (ok ? src : 0), ok ? 16u : 0u);
+        ptx::cp_async16(sb_lo + dst, P.x_lo + (ok ? src : 0), ok ? 16u : 0u);
+      }
+      ptx::cp_async_commit();
+      if (kb >= C::LAG) {
+        ptx::cp_async_wait<C::LAG>();
+        ptx::fence_proxy_async();
+        ptx::mbar_arrive(&full[(kb - C::LAG) % S]);
+      }
+    }
+    ptx::cp_async_wait<0>();
+    ptx::fence_proxy_async();
+    for (int kb = max(0, nkb - C::LAG); kb < nkb; kb++) ptx::mbar_arrive(&full[kb % S]);
+
+    // epilogue: row = output channel m0 + t, partial sums -> ws[z][row][col]
+    ptx::mbar_wait(tmem_full, 0);
+    ptx::tc_fence_after();
+    float* dst = P.ws + (int64_t(blockIdx.z) * P.mrows_p + m0 + t) * P.ncol_p + n0;
+#pragma unroll 1
+    for (int c0 = 0; c0 < BN; c0 += 32) {
+      uint32_t r[32];
+      ptx::tmem_ld32(tmem_d + (uint32_t(warp * 32) << 16) + uint32_t(c0), r);
+      ptx::tmem_ld_wait();
+#pragma unroll
+      for (int i = 0; i < 32; i += 4) {
+        const float4 v4 =
+            nkb > 0 ? make_float4(__uint_as_float(r[i]), __uint_as_float(r[i + 1]),
+                                  __uint_as_float(r[i + 2]), __uint_as_float(r[i + 3]))
+                    : make_float4(0.f, 0.f, 0.f, 0.f);
+        *reinterpret_cast<float4*>(dst + c0 + i) = v4;
+      }
+    }
+    ptx::tc_fence_before();
+  } else if (lane == 0) {
+    constexpr uint32_t idesc = ptx::idesc_bf16(128, BN, 1, 1);
+    uint32_t acc = 0;
+    for (int kb = 0; kb < nkb; kb++) {
+      const int s = kb % S;
+      ptx::mbar_wait(&full[s], (kb / S) & 1);
+      ptx::tc_fence_after();
+      const uint32_t sa_hi = smem0 + s * C::STAGE_BYTES;
+      const uint32_t sa_lo = sa_hi + C::A_BYTES;
+      const uint32_t sb_hi = sa_lo + C::A_BYTES;
+      const uint32_t sb_lo = sb_hi + C::B_BYTES;
+      const uint64_t dah = ptx::desc_mnmajor_sw128(sa_hi, C::LBO, C::SBO);
+      const uint64_t dal = ptx::desc_mnmajor_sw128(sa_lo, C::LBO, C::SBO);
+      const uint64_t dbh = ptx::desc_mnmajor_sw128(sb_hi, C::LBO, C::SBO);
+      const uint64_t dbl = ptx::desc_mnmajor_sw128(sb_lo, C::LBO, C::SBO);
+#pragma unroll
+      for (int kk = 0; kk < kPx / 16; kk++) {
+        const uint64_t o = uint64_t(kk * 2 * C::SBO) >> 4;  // 16 pixels = 2 K groups
+        ptx::mma_bf16(tmem_d, dal + o, dbh + o, idesc, acc);
+        acc = 1;
+        ptx::mma_bf16(tmem_d, dah + o, dbl + o, idesc, 1);
+        ptx::mma_bf16(tmem_d, dah + o, dbh + o, idesc, 1);
+      }
+      ptx::mma_commit(&empty[s]);
+    }
+    ptx::mma_commit(tmem_full);
+  }
+  __syncthreads();
+  if (warp == 4) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc<C::TMEM_COLS>(tmem_d);
+  }
+}
+
+// dW[k][c][r][s] (+)= sum_z ws[z][k][col], col = chunk*8 + i decoded by the
+// forward chunk table; fixed z order => deterministic.
+__global__ void __launch_bounds__(256) wgrad_reduce(const float* __restrict__ ws, int splits,
+                                                    int mrows_p, int ncol_p, int K, int Cc, int R,
+                                                    int S, int flip, int KC,
+                                                    const uint32_t* __restrict__ ctab,
+                                                    float* __restrict__ df, int accumulate) {
+  const int64_t total = int64_t(K) * KC * 8;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  const int64_t plane = int64_t(mrows_p) * ncol_p;
+  for (int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; idx < total; idx += stride) {
+    const int k = int(idx / (int64_t(KC) * 8)), col = int(idx % (int64_t(KC) * 8));
+    const uint32_t e = ctab[col >> 3];
+    const int cin = int(e & 0xFFFF) + (col & 7);
+    if (cin >= Cc) continue;
+    const int dh = int(e >> 24), dw = int((e >> 16) & 255);
+    const int r = flip ? R - 1 - dh : dh, s = flip ? S - 1 - dw : dw;
+    const float* src = ws + int64_t(k) * ncol_p + col;
+    float acc = src[0];
+    for (int z = 1; z < splits; z++) acc = __fadd_rn(acc, src[z * plane]);
+    float* d = df + ((int64_t(k) * Cc + cin) * R + r) * S + s;
+    *d = accumulate ? __fadd_rn(*d, acc) : acc;
+  }
+}
+
+// Chunk table of the forward reduction order (tap = dh*S + dw, then channel group).
+__global__ void fwd_ctab_kernel(int S, int Cgrp, int KC, uint32_t* ctab) {
+  const int ch = blockIdx.x * blockDim.x + threadIdx.x;
+  if (ch >= KC) return;
+  const int tap = ch / Cgrp, g = ch % Cgrp;
+  ctab[ch] = (uint32_t(tap / S) << 24) | (uint32_t(tap % S) << 16) | uint32_t(g * 8);
+}
+
+template <int BN>
+cudaError_t launch_wgrad(const WgParams& prm, int mt, int nt, int splits, cudaStream_t st) {
+  using CC = WCfg<BN>;
+  static int attr_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (attr_dev != dev) {
+    cudaError_t e = cudaFuncSetAttribute(wgrad_tc_kernel<BN>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, CC::SMEM);
+    if (e != cudaSuccess) return e;
+    attr_dev = dev;
+  }
+  const dim3 grid{unsigned(mt), unsigned(nt), unsigned(splits)};
+  wgrad_tc_kernel<BN><<<grid, kThreads, CC::SMEM, st>>>(prm);
+  note_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace
+}  // namespace tc
+
+cudaError_t tc_backward_filter(const ConvProblem& p, const float* dy, const float* x, float* df,
+                               bool acc, cudaStream_t st) {
+  using namespace tc;
+  pool_keep_memory();
+  const int Kp = int(ceil_div(p.K, 8) * 8), Cp = int(ceil_div(p.C, 8) * 8), Cgrp = Cp / 8;
+  const int KC = int(p.R * p.S) * Cgrp;
+  const int64_t NPQ = p.N * p.P * p.Q, NHW = p.N * p.H * p.W;
+  const int ncol = KC * 8;
+  const int bn = ncol <= 64 ? 64 : (ncol <= 128 ? 128 : 256);
+  const int nt = int(ceil_div(ncol, bn)), mt = int(ceil_div(p.K, 128));
+  const int ncol_p = nt * bn, mrows_p = mt * 128;
+  const int64_t kblocks = ceil_div(NPQ, kPx);
+  int64_t splits = ceil_div(int64_t(kNumSMs) * 2, int64_t(mt) * nt);
+  splits = std::max<int64_t>(1, std::min<int64_t>({splits, std::max<int64_t>(1, kblocks / 8), 128}));
+  const int64_t pps = ceil_div(kblocks, splits) * kPx;
+  splits = ceil_div(NPQ, pps);
+
+  const size_t dy_elems = size_t(NPQ) * Kp, x_elems = size_t(NHW) * Cp;
+  const size_t ws_floats = size_t(splits) * mrows_p * ncol_p;
+  Workspace ws(st);
+  cudaError_t e = cudaMallocAsync(&ws.p, (dy_elems + x_elems) * 4 + ws_floats * 4 + size_t(KC) * 4 + 512, st);
+  if (e != cudaSuccess) return e;
+  auto* dy_hi = static_cast<__nv_bfloat16*>(ws.p);
+  auto* dy_lo = dy_hi + dy_elems;
+  auto* x_hi = dy_lo + dy_elems;
+  auto* x_lo = x_hi + x_elems;
+  float* part = reinterpret_cast<float*>(x_lo + x_elems);
+  auto* ctab = reinterpret_cast<uint32_t*>(part + ws_floats);
+
+  if ((e = pack_act(p.y, dy, Kp, dy_hi, dy_lo, st)) != cudaSuccess) return e;
+  if ((e = pack_act(p.x, x, Cp, x_hi, x_lo, st)) != cudaSuccess) return e;
+  fwd_ctab_kernel<<<unsigned(ceil_div(KC, 256)), 256, 0, st>>>(int(p.S), Cgrp, KC, ctab);
+  note_launch();
+
+  WgParams prm{};
+  prm.NPQ = NPQ;
+  prm.pix_per_split = pps;
+  prm.P = int(p.P);
+  prm.Q = int(p.Q);
+  prm.H = int(p.H);
+  prm.W = int(p.W);
+  prm.u = int(p.u);
+  prm.v = int(p.v);
+  prm.pad_h = int(p.pad_h);
+  prm.pad_w = int(p.pad_w);
+  prm.Kp = Kp;
+  prm.Cp = Cp;
+  prm.KC = KC;
+  prm.ncol_p = ncol_p;
+  prm.mrows_p = mrows_p;
+  prm.ctab = ctab;
+  prm.dy_hi = dy_hi;
+  prm.dy_lo = dy_lo;
+  prm.x_hi = x_hi;
+  prm.x_lo = x_lo;
+  prm.ws = part;
+  prm.dPQ = make_magic(uint32_t(p.P * p.Q));
+  prm.dQ = make_magic(uint32_t(p.Q));
+  switch (bn) {
+    case 64: e = launch_wgrad<64>(prm, mt, nt, int(splits), st); break;
+    case 128: e = launch_wgrad<128>(prm, mt, nt, int(splits), st); break;
+    default: e = launch_wgrad<256>(prm, mt, nt, int(splits), st); break;
+  }
+  if (e != cudaSuccess) return e;
+  wgrad_reduce<<<grid_for(int64_t(p.K) * ncol, 256, 16), 256, 0, st>>>(
+      part, int(splits), mrows_p, ncol_p, int(p.K), int(p.C), int(p.R), int(p.S), p.flip ? 1 : 0,
+      KC, ctab, df, acc ? 1 : 0);
+  note_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace dnnp
