@@ -46,6 +46,8 @@ constexpr int kBK = 32;          // reduction elements per stage (64 B swizzle r
 constexpr int kThreads = 288;    // 4 producer + 1 MMA + 4 epilogue warps
 
 struct TcParams {
+  CUtensorMap tm_bhi;            // packed filter planes [Np][Ktot], box {32, BN}, 64B swizzle
+  CUtensorMap tm_blo;
   int64_t M;                     // GEMM rows
   int Ncol;                      // valid columns
   int OH, OW;                    // GEMM row grid of one image
@@ -102,7 +104,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
   if (warp == 4) {
     if (lane == 0) {
       for (int s = 0; s < S; s++) {
-        ptx::mbar_init(&full[s], 128);
+        ptx::mbar_init(&full[s], 129);  // 128 A-gather arrivals + 1 expect_tx (TMA B)
         ptx::mbar_init(&empty[s], 1);
       }
       for (int b = 0; b < 2; b++) {
@@ -122,22 +124,36 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
 
   if (warp < 4) {
     // =================================================== producers
+    // A: lane quad (t & 3) = 16-byte chunk of the 64-byte k-block row, rows
+    // (t >> 2) + 32*i: 4 lanes read one pixel's contiguous 64 bytes.
+    // B: one elected thread streams the filter tile with TMA.
     const int t = threadIdx.x;
-    const uint32_t a_row = uint32_t((t >> 3) * 512 + (t & 7) * 64);
-    const int asw = (t >> 1) & 3;
+    const int j = t & 3, rb = t >> 2;
+    if (t == 0) {
+      ptx::tma_prefetch(&P.tm_bhi);
+      ptx::tma_prefetch(&P.tm_blo);
+    }
     int it = 0;
     for (int tile = blockIdx.x; tile < P.tiles; tile += gridDim.x) {
-      const int64_t m = int64_t(tile / P.nt) * kBM + t;
+      const int64_t mbase = int64_t(tile / P.nt) * kBM;
       const int n0 = (tile % P.nt) * BN;
-      const bool row_ok = m < P.M;
-      uint32_t img = 0, oh = 0, ow = 0;
-      if (row_ok) {
-        uint32_t rem;
-        mdivmod(uint32_t(m), P.dOHW, img, rem);
-        mdivmod(rem, P.dOW, oh, ow);
+      int ih0[4], iw0[4];
+      int64_t pix0[4];
+      bool rok[4];
+#pragma unroll
+      for (int i = 0; i < 4; i++) {
+        const int64_t m = mbase + rb + 32 * i;
+        rok[i] = m < P.M;
+        uint32_t img = 0, oh = 0, ow = 0;
+        if (rok[i]) {
+          uint32_t rem;
+          mdivmod(uint32_t(m), P.dOHW, img, rem);
+          mdivmod(rem, P.dOW, oh, ow);
+        }
+        ih0[i] = int(oh) * P.u - P.pad_h;
+        iw0[i] = int(ow) * P.v - P.pad_w;
+        pix0[i] = int64_t(img) * P.IH * P.IW;
       }
-      const int ih0 = int(oh) * P.u - P.pad_h, iw0 = int(ow) * P.v - P.pad_w;
-      const int64_t pix0 = int64_t(img) * P.IH * P.IW;
       for (int kb = 0; kb < P.nkb; kb++, it++) {
         const int s = it % S;
         if (it >= S) ptx::mbar_wait(&empty[s], ((it / S) - 1) & 1);
@@ -145,29 +161,24 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
         const uint32_t sa_lo = sa_hi + C::A_BYTES;
         const uint32_t sb_hi = sa_lo + C::A_BYTES;
         const uint32_t sb_lo = sb_hi + C::B_BYTES;
-#pragma unroll
-        for (int j = 0; j < 4; j++) {
-          const int ch = kb * 4 + j;
-          bool ok = row_ok && ch < P.KC;
-          int64_t src = 0;
-          if (ok) {
-            const uint32_t e = __ldg(P.ctab + ch);
-            const int ih = ih0 + int(e >> 24), iw = iw0 + int((e >> 16) & 255);
-            ok = unsigned(ih) < unsigned(P.IH) && unsigned(iw) < unsigned(P.IW);
-            src = (pix0 + int64_t(ih) * P.IW + iw) * P.Cp + (e & 0xFFFF);
-          }
-          const uint32_t dst = a_row + uint32_t((j ^ asw) << 4);
-          ptx::cp_async16(sa_hi + dst, P.a_hi + (ok ? src : 0), ok ? 16u : 0u);
-          ptx::cp_async16(sa_lo + dst, P.a_lo + (ok ? src : 0), ok ? 16u : 0u);
+        if (t == 0) {
+          ptx::mbar_arrive_expect_tx(&full[s], 2 * C::B_BYTES);
+          ptx::tma_load_2d(sb_hi, &P.tm_bhi, kb * kBK, n0, &full[s]);
+          ptx::tma_load_2d(sb_lo, &P.tm_blo, kb * kBK, n0, &full[s]);
         }
+        const int ch = kb * 4 + j;
+        const bool ch_ok = ch < P.KC;
+        const uint32_t e = ch_ok ? __ldg(P.ctab + ch) : 0u;
+        const int dh = int(e >> 24), dw = int((e >> 16) & 255), c0 = int(e & 0xFFFF);
 #pragma unroll
-        for (int i = 0; i < BN / 32; i++) {
-          const int q = t + i * 128;
-          const int row = q >> 2, j = q & 3;
-          const int64_t src = int64_t(n0 + row) * P.Ktot + kb * kBK + j * 8;
-          const uint32_t dst = sw64(row, j);
-          ptx::cp_async16(sb_hi + dst, P.b_hi + src, 16u);
-          ptx::cp_async16(sb_lo + dst, P.b_lo + src, 16u);
+        for (int i = 0; i < 4; i++) {
+          const int ih = ih0[i] + dh, iw = iw0[i] + dw;
+          const bool ok = ch_ok && rok[i] && unsigned(ih) < unsigned(P.IH) &&
+                          unsigned(iw) < unsigned(P.IW);
+          const int64_t src = ok ? (pix0[i] + int64_t(ih) * P.IW + iw) * P.Cp + c0 : 0;
+          const uint32_t dst = sw64(rb + 32 * i, j);
+          ptx::cp_async16(sa_hi + dst, P.a_hi + src, ok ? 16u : 0u);
+          ptx::cp_async16(sa_lo + dst, P.a_lo + src, ok ? 16u : 0u);
         }
         ptx::cp_async_commit();
         if (it >= C::LAG) {
@@ -431,6 +442,12 @@ cudaError_t run_gemm(const ConvProblem& p, Gemm g, const __nv_bfloat16* a_hi,
   const int64_t tiles = ceil_div(M, kBM) * prm.nt;
   if (tiles >= (int64_t(1) << 31)) return cudaErrorInvalidValue;
   prm.tiles = int(tiles);
+  e = make_tmap_2d(&prm.tm_bhi, b_hi, uint64_t(pg.Ktot), uint64_t(pg.Np), uint64_t(pg.Ktot), kBK,
+                   uint32_t(bn), CU_TENSOR_MAP_SWIZZLE_64B);
+  if (e != cudaSuccess) return e;
+  e = make_tmap_2d(&prm.tm_blo, b_lo, uint64_t(pg.Ktot), uint64_t(pg.Np), uint64_t(pg.Ktot), kBK,
+                   uint32_t(bn), CU_TENSOR_MAP_SWIZZLE_64B);
+  if (e != cudaSuccess) return e;
   prm.ctab = ctab;
   prm.a_hi = a_hi;
   prm.a_lo = a_lo;

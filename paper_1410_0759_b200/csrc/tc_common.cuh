@@ -1,5 +1,6 @@
 // Shared host/device helpers of the tensor-core convolution kernels.
 #pragma once
+#include <cuda.h>
 #include <cuda_bf16.h>
 
 #include "common.cuh"
@@ -27,6 +28,12 @@ struct Workspace {
 };
 
 void pool_keep_memory();
+
+// Row-major 2-D bf16 matrix [rows][cols] (row pitch `pitch_elems`) as a TMA
+// tiled tensor map with a {box_cols, box_rows} box and the given swizzle.
+cudaError_t make_tmap_2d(CUtensorMap* map, const void* base, uint64_t cols, uint64_t rows,
+                         uint64_t pitch_elems, uint32_t box_cols, uint32_t box_rows,
+                         CUtensorMapSwizzle swizzle);
 
 // Strided fp32 4-D view -> channel-innermost bf16 hi/lo planes
 // [n][h][w][Cp] (Cp = channels padded to a multiple of 8, zero filled).
