@@ -19,10 +19,13 @@ namespace dnnp {
 namespace tc {
 namespace {
 
-constexpr int kThreads = 160;  // 4 producer warps + MMA warp (epilogue reuses producers)
+constexpr int kProdWarps = 8;  // gather/TMA producers; warps 0-3 also run the epilogue
+constexpr int kThreads = (kProdWarps + 1) * 32;  // + MMA warp
 constexpr int kPx = 32;        // pixels (reduction rows) per stage
 
 struct WgParams {
+  CUtensorMap tm_dyhi;   // packed dy [NPQ][Kp], box {64 channels, 32 pixels}, 128B swizzle
+  CUtensorMap tm_dylo;
   int64_t NPQ;
   int64_t pix_per_split;
   int P, Q, H, W;
@@ -77,10 +80,10 @@ __global__ void __launch_bounds__(kThreads, 1) wgrad_tc_kernel(const __grid_cons
   const int64_t pend = min(P.NPQ, pbeg + P.pix_per_split);
   const int nkb = pend > pbeg ? int((pend - pbeg + kPx - 1) / kPx) : 0;
 
-  if (warp == 4) {
+  if (warp == kProdWarps) {
     if (lane == 0) {
       for (int s = 0; s < S; s++) {
-        ptx::mbar_init(&full[s], 128);
+        ptx::mbar_init(&full[s], kProdWarps * 32 + 1);  // gather arrivals + expect_tx (TMA dy)
         ptx::mbar_init(&empty[s], 1);
       }
       ptx::mbar_init(tmem_full, 1);
@@ -95,9 +98,35 @@ __global__ void __launch_bounds__(kThreads, 1) wgrad_tc_kernel(const __grid_cons
   const uint32_t tmem_d = *tmem_slot;
   const uint32_t smem0 = ptx::smem_u32(smem);
 
-  if (warp < 4) {
+  if (warp < kProdWarps) {
+    // A (dy, dense per pixel) arrives by TMA; B (im2col of x) is gathered with
+    // one lane per 16-byte column chunk so that a warp reads one pixel's
+    // contiguous channel runs.  Pixel decodes are done once per warp (one lane
+    // per pixel) and broadcast; each lane keeps its chunk's constant offset.
     const int t = threadIdx.x;
-    const int kp = t & (kPx - 1), qd = t >> 5;  // pixel of the stage, quarter of the chunks
+    constexpr int NCH = BN / 8;                  // column chunks per pixel
+    constexpr int LP = NCH < 32 ? NCH : 32;      // lanes per pixel
+    constexpr int PPI = 32 / LP;                 // pixels per warp instruction
+    constexpr int PPW = kPx / kProdWarps;        // pixels per warp per stage
+    constexpr int ITER = PPW / PPI;
+    constexpr int NQ = (NCH + 31) / 32;
+    const int jl = lane % LP, sub = lane / LP;
+    const int nbox = min(2, (P.Kp - m0 + 63) / 64);
+    const uint32_t a_bytes = uint32_t(nbox) * C::LBO;  // per plane
+    if (t == 0) {
+      ptx::tma_prefetch(&P.tm_dyhi);
+      ptx::tma_prefetch(&P.tm_dylo);
+    }
+    int cdh[NQ], cdw[NQ];
+    int64_t coff[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; q++) {
+      const int ch = n0 / 8 + jl + q * 32;
+      const uint32_t e = ch < P.KC ? __ldg(P.ctab + ch) : 0u;
+      cdh[q] = ch < P.KC ? int(e >> 24) : (1 << 20);  // out of range => masked
+      cdw[q] = int((e >> 16) & 255);
+      coff[q] = (int64_t(cdh[q] & 0xFF) * P.W + cdw[q]) * P.Cp + (e & 0xFFFF);
+    }
     for (int kb = 0; kb < nkb; kb++) {
       const int s = kb % S;
       if (kb >= S) ptx::mbar_wait(&empty[s], ((kb / S) - 1) & 1);
@@ -105,41 +134,44 @@ __global__ void __launch_bounds__(kThreads, 1) wgrad_tc_kernel(const __grid_cons
       const uint32_t sa_lo = sa_hi + C::A_BYTES;
       const uint32_t sb_hi = sa_lo + C::A_BYTES;
       const uint32_t sb_lo = sb_hi + C::B_BYTES;
-      const int64_t g = pbeg + int64_t(kb) * kPx + kp;
-      const bool pix_ok = g < pend;
-      uint32_t n = 0, pp = 0, qq = 0;
-      if (pix_ok) {
-        uint32_t rem;
-        mdivmod(uint32_t(g), P.dPQ, n, rem);
-        mdivmod(rem, P.dQ, pp, qq);
-      }
-#pragma unroll
-      for (int jj = 0; jj < 4; jj++) {  // A: 4 of the 16 channel chunks
-        const int j = qd * 4 + jj;
-        const int c0 = m0 + j * 8;
-        const bool ok = pix_ok && c0 < P.Kp;
-        const int64_t src = ok ? g * P.Kp + c0 : 0;
-        const uint32_t dst = mn_off<BN>(j, kp);
-        ptx::cp_async16(sa_hi + dst, P.dy_hi + src, ok ? 16u : 0u);
-        ptx::cp_async16(sa_lo + dst, P.dy_lo + src, ok ? 16u : 0u);
-      }
-      const int ih0 = int(pp) * P.u - P.pad_h, iw0 = int(qq) * P.v - P.pad_w;
-      const int64_t pix0 = int64_t(n) * P.H * P.W;
-#pragma unroll
-      for (int jj = 0; jj < BN / 32; jj++) {  // B: a quarter of the BN/8 column chunks
-        const int j = qd * (BN / 32) + jj;
-        const int ch = n0 / 8 + j;
-        bool ok = pix_ok && ch < P.KC;
-        int64_t src = 0;
-        if (ok) {
-          const uint32_t e = __ldg(P.ctab + ch);
-          const int ih = ih0 + int(e >> 24), iw = iw0 + int((e >> 16) & 255);
-          ok = unsigned(ih) < unsigned(P.H) && unsigned(iw) < unsigned(P.W);
-          src = (pix0 + int64_t(ih) * P.W + iw) * P.Cp + (e & 0xFFFF);
+      const int64_t gk = pbeg + int64_t(kb) * kPx;
+      if (t == 0) {
+        ptx::mbar_arrive_expect_tx(&full[s], 2 * a_bytes);
+        for (int b = 0; b < nbox; b++) {
+          ptx::tma_load_2d(sa_hi + b * C::LBO, &P.tm_dyhi, m0 + 64 * b, int(gk), &full[s]);
+          ptx::tma_load_2d(sa_lo + b * C::LBO, &P.tm_dylo, m0 + 64 * b, int(gk), &full[s]);
         }
-        const uint32_t dst = mn_off<BN>(j, kp);
-        ptx::cp_async16(sb_hi + dst, P.x_hi + (ok ? src : 0), ok ? 16u : 0u);
-        ptx::cp_async16(sb_lo + dst, P.x_lo + (ok ? src : 0), ok ? 16u : 0u);
+      }
+      // lane l < PPW decodes pixel warp*PPW + l of this stage
+      int my_ih0 = -(1 << 20), my_iw0 = 0;
+      int64_t my_base = 0;
+      if (lane < PPW) {
+        const int64_t g = gk + warp * PPW + lane;
+        if (g < pend) {
+          uint32_t n, rem, pp, qq;
+          mdivmod(uint32_t(g), P.dPQ, n, rem);
+          mdivmod(rem, P.dQ, pp, qq);
+          my_ih0 = int(pp) * P.u - P.pad_h;
+          my_iw0 = int(qq) * P.v - P.pad_w;
+          my_base = ((int64_t(n) * P.H + my_ih0) * P.W + my_iw0) * P.Cp;
+        }
+      }
+#pragma unroll
+      for (int ii = 0; ii < ITER; ii++) {
+        const int pl = ii * PPI + sub;  // pixel within this warp's set
+        const int ih0 = __shfl_sync(0xffffffffu, my_ih0, pl);
+        const int iw0 = __shfl_sync(0xffffffffu, my_iw0, pl);
+        const int64_t base = __shfl_sync(0xffffffffu, my_base, pl);
+        const int kp = warp * PPW + pl;
+#pragma unroll
+        for (int q = 0; q < NQ; q++) {
+          const int ih = ih0 + cdh[q], iw = iw0 + cdw[q];
+          const bool ok = unsigned(ih) < unsigned(P.H) && unsigned(iw) < unsigned(P.W);
+          const int64_t src = ok ? base + coff[q] : 0;
+          const uint32_t dst = mn_off<BN>(jl + q * 32, kp);
+          ptx::cp_async16(sb_hi + dst, P.x_hi + src, ok ? 16u : 0u);
+          ptx::cp_async16(sb_lo + dst, P.x_lo + src, ok ? 16u : 0u);
+        }
       }
       ptx::cp_async_commit();
       if (kb >= C::LAG) {
@@ -152,7 +184,8 @@ __global__ void __launch_bounds__(kThreads, 1) wgrad_tc_kernel(const __grid_cons
     ptx::fence_proxy_async();
     for (int kb = max(0, nkb - C::LAG); kb < nkb; kb++) ptx::mbar_arrive(&full[kb % S]);
 
-    // epilogue: row = output channel m0 + t, partial sums -> ws[z][row][col]
+    // epilogue (warps 0-3 = TMEM lane quadrants): row = output channel m0 + t
+    if (warp < 4) {
     ptx::mbar_wait(tmem_full, 0);
     ptx::tc_fence_after();
     float* dst = P.ws + (int64_t(blockIdx.z) * P.mrows_p + m0 + t) * P.ncol_p + n0;
@@ -171,6 +204,7 @@ __global__ void __launch_bounds__(kThreads, 1) wgrad_tc_kernel(const __grid_cons
       }
     }
     ptx::tc_fence_before();
+    }
   } else if (lane == 0) {
     constexpr uint32_t idesc = ptx::idesc_bf16(128, BN, 1, 1);
     uint32_t acc = 0;
@@ -199,7 +233,7 @@ __global__ void __launch_bounds__(kThreads, 1) wgrad_tc_kernel(const __grid_cons
     ptx::mma_commit(tmem_full);
   }
   __syncthreads();
-  if (warp == 4) {
+  if (warp == kProdWarps) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc<C::TMEM_COLS>(tmem_d);
   }
@@ -310,6 +344,12 @@ cudaError_t tc_backward_filter(const ConvProblem& p, const float* dy, const floa
   prm.ncol_p = ncol_p;
   prm.mrows_p = mrows_p;
   prm.ctab = ctab;
+  if ((e = make_tmap_2d(&prm.tm_dyhi, dy_hi, uint64_t(Kp), uint64_t(NPQ), uint64_t(Kp), 64, kPx,
+                       CU_TENSOR_MAP_SWIZZLE_128B)) != cudaSuccess)
+    return e;
+  if ((e = make_tmap_2d(&prm.tm_dylo, dy_lo, uint64_t(Kp), uint64_t(NPQ), uint64_t(Kp), 64, kPx,
+                       CU_TENSOR_MAP_SWIZZLE_128B)) != cudaSuccess)
+    return e;
   prm.dy_hi = dy_hi;
   prm.dy_lo = dy_lo;
   prm.x_hi = x_hi;
