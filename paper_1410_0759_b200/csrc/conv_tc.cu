@@ -16,10 +16,11 @@
 // reduction chunk into its (dh, dw, c0) im2col offset.
 //
 // Kernel: persistent, warp specialised, one CTA per SM, 128 x BN tiles.
-//   warps 0-3  producers: A gather (one output pixel per thread) + B copy into
-//              64B-swizzled K-major stages of 32 reduction elements
-//   warp  4    TMEM allocation; lane 0 issues the tcgen05.mma stream
-//   warps 5-8  epilogue: tcgen05.ld from a double-buffered TMEM accumulator,
+//   warps 0-7  producers: A gather (4 lanes per output pixel row, 16-byte
+//              cp.async) + B tile by TMA into 64B-swizzled K-major stages
+//              of 32 reduction elements
+//   warp  8    TMEM allocation; lane 0 issues the tcgen05.mma stream
+//   warps 9-12 epilogue: tcgen05.ld from a double-buffered TMEM accumulator,
 //              alpha/beta blend straight into the caller's strided output,
 //              overlapping the next tile's main loop
 // mbarrier rings: full/empty per stage (producers <-> MMA), tfull/tempty per
@@ -43,7 +44,9 @@ namespace {
 
 constexpr int kBM = 128;         // tile rows (UMMA M)
 constexpr int kBK = 32;          // reduction elements per stage (64 B swizzle rows)
-constexpr int kThreads = 288;    // 4 producer + 1 MMA + 4 epilogue warps
+constexpr int kProdWarps = 8;    // A-gather producers (thread 0 also issues the B TMA)
+constexpr int kMmaWarp = kProdWarps;
+constexpr int kThreads = (kProdWarps + 1 + 4) * 32;  // + MMA warp + 4 epilogue warps
 
 struct TcParams {
   CUtensorMap tm_bhi;            // packed filter planes [Np][Ktot], box {32, BN}, 64B swizzle
@@ -76,7 +79,6 @@ struct Cfg {
   static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
   static constexpr int STAGES =
       (200 * 1024) / STAGE_BYTES > 8 ? 8 : (200 * 1024) / STAGE_BYTES;
-  static constexpr int LAG = STAGES >= 6 ? 3 : (STAGES >= 4 ? 2 : 1);
   static constexpr int TMEM_COLS =
       2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512));
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
@@ -101,10 +103,10 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (warp == 4) {
+  if (warp == kMmaWarp) {
     if (lane == 0) {
       for (int s = 0; s < S; s++) {
-        ptx::mbar_init(&full[s], 129);  // 128 A-gather arrivals + 1 expect_tx (TMA B)
+        ptx::mbar_init(&full[s], kProdWarps * 32 + 1);  // gather arrivals + expect_tx (TMA B)
         ptx::mbar_init(&empty[s], 1);
       }
       for (int b = 0; b < 2; b++) {
@@ -122,12 +124,14 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
   const uint32_t tmem_base = *tmem_slot;
   const uint32_t smem0 = ptx::smem_u32(smem);
 
-  if (warp < 4) {
+  if (warp < kProdWarps) {
     // =================================================== producers
     // A: lane quad (t & 3) = 16-byte chunk of the 64-byte k-block row, rows
-    // (t >> 2) + 32*i: 4 lanes read one pixel's contiguous 64 bytes.
+    // (t >> 2) + RSTEP*i: 4 lanes read one pixel's contiguous 64 bytes.
     // B: one elected thread streams the filter tile with TMA.
     const int t = threadIdx.x;
+    constexpr int RSTEP = kProdWarps * 8;   // rows covered per i-step
+    constexpr int RPT = kBM / RSTEP;        // rows per thread
     const int j = t & 3, rb = t >> 2;
     if (t == 0) {
       ptx::tma_prefetch(&P.tm_bhi);
@@ -137,12 +141,12 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
     for (int tile = blockIdx.x; tile < P.tiles; tile += gridDim.x) {
       const int64_t mbase = int64_t(tile / P.nt) * kBM;
       const int n0 = (tile % P.nt) * BN;
-      int ih0[4], iw0[4];
-      int64_t pix0[4];
-      bool rok[4];
+      int ih0[RPT], iw0[RPT];
+      int64_t pix0[RPT];
+      bool rok[RPT];
 #pragma unroll
-      for (int i = 0; i < 4; i++) {
-        const int64_t m = mbase + rb + 32 * i;
+      for (int i = 0; i < RPT; i++) {
+        const int64_t m = mbase + rb + RSTEP * i;
         rok[i] = m < P.M;
         uint32_t img = 0, oh = 0, ow = 0;
         if (rok[i]) {
@@ -171,27 +175,20 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
         const uint32_t e = ch_ok ? __ldg(P.ctab + ch) : 0u;
         const int dh = int(e >> 24), dw = int((e >> 16) & 255), c0 = int(e & 0xFFFF);
 #pragma unroll
-        for (int i = 0; i < 4; i++) {
+        for (int i = 0; i < RPT; i++) {
           const int ih = ih0[i] + dh, iw = iw0[i] + dw;
           const bool ok = ch_ok && rok[i] && unsigned(ih) < unsigned(P.IH) &&
                           unsigned(iw) < unsigned(P.IW);
           const int64_t src = ok ? (pix0[i] + int64_t(ih) * P.IW + iw) * P.Cp + c0 : 0;
-          const uint32_t dst = sw64(rb + 32 * i, j);
+          const uint32_t dst = sw64(rb + RSTEP * i, j);
           ptx::cp_async16(sa_hi + dst, P.a_hi + src, ok ? 16u : 0u);
           ptx::cp_async16(sa_lo + dst, P.a_lo + src, ok ? 16u : 0u);
         }
-        ptx::cp_async_commit();
-        if (it >= C::LAG) {
-          ptx::cp_async_wait<C::LAG>();
-          ptx::fence_proxy_async();
-          ptx::mbar_arrive(&full[(it - C::LAG) % S]);
-        }
+        ptx::cp_async_mbar_arrive(&full[s]);
       }
     }
     ptx::cp_async_wait<0>();
-    ptx::fence_proxy_async();
-    for (int k = std::max(0, it - C::LAG); k < it; k++) ptx::mbar_arrive(&full[k % S]);
-  } else if (warp == 4) {
+  } else if (warp == kMmaWarp) {
     // =================================================== MMA issuer
     if (lane == 0) {
       constexpr uint32_t idesc = ptx::idesc_bf16(kBM, BN, 0, 0);
@@ -205,6 +202,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
         for (int kb = 0; kb < P.nkb; kb++, it++) {
           const int s = it % S;
           ptx::mbar_wait(&full[s], (it / S) & 1);
+          ptx::fence_proxy_async();  // producers' cp.async writes -> async proxy
           ptx::tc_fence_after();
           const uint32_t sa_hi = smem0 + s * C::STAGE_BYTES;
           const uint32_t sa_lo = sa_hi + C::A_BYTES;
@@ -278,7 +276,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
     }
   }
   __syncthreads();
-  if (warp == 4) {
+  if (warp == kMmaWarp) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc<C::TMEM_COLS>(tmem_base);
   }

@@ -51,7 +51,6 @@ struct WCfg {
   static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
   static constexpr int STAGES =
       (200 * 1024) / STAGE_BYTES > 8 ? 8 : (200 * 1024) / STAGE_BYTES;
-  static constexpr int LAG = STAGES >= 6 ? 3 : (STAGES >= 4 ? 2 : 1);
   static constexpr int TMEM_COLS = BN <= 64 ? 64 : (BN <= 128 ? 128 : 256);
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
 };
@@ -173,16 +172,9 @@ __global__ void __launch_bounds__(kThreads, 1) wgrad_tc_kernel(const __grid_cons
           ptx::cp_async16(sb_lo + dst, P.x_lo + src, ok ? 16u : 0u);
         }
       }
-      ptx::cp_async_commit();
-      if (kb >= C::LAG) {
-        ptx::cp_async_wait<C::LAG>();
-        ptx::fence_proxy_async();
-        ptx::mbar_arrive(&full[(kb - C::LAG) % S]);
-      }
+      ptx::cp_async_mbar_arrive(&full[s]);
     }
     ptx::cp_async_wait<0>();
-    ptx::fence_proxy_async();
-    for (int kb = max(0, nkb - C::LAG); kb < nkb; kb++) ptx::mbar_arrive(&full[kb % S]);
 
     // epilogue (warps 0-3 = TMEM lane quadrants): row = output channel m0 + t
     if (warp < 4) {
@@ -211,6 +203,7 @@ __global__ void __launch_bounds__(kThreads, 1) wgrad_tc_kernel(const __grid_cons
     for (int kb = 0; kb < nkb; kb++) {
       const int s = kb % S;
       ptx::mbar_wait(&full[s], (kb / S) & 1);
+      ptx::fence_proxy_async();  // producers' cp.async writes -> async proxy
       ptx::tc_fence_after();
       const uint32_t sa_hi = smem0 + s * C::STAGE_BYTES;
       const uint32_t sa_lo = sa_hi + C::A_BYTES;
