@@ -34,6 +34,8 @@
 //   (window tap, k) computes every phase at once (gather form, no atomics,
 //   deterministic); for u = v = 1 it is the plain transposed convolution.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 
 #include "tc_common.cuh"
 #include "tc_ptx.cuh"
@@ -46,7 +48,9 @@ constexpr int kBM = 128;         // tile rows (UMMA M)
 constexpr int kBK = 32;          // reduction elements per stage (64 B swizzle rows)
 constexpr int kProdWarps = 8;    // A-gather producers (thread 0 also issues the B TMA)
 constexpr int kMmaWarp = kProdWarps;
-constexpr int kThreads = (kProdWarps + 1 + 4) * 32;  // + MMA warp + 4 epilogue warps
+constexpr int kTmaWarp = kProdWarps + 1;
+constexpr int kThreads = (kProdWarps + 2 + 4) * 32;  // + MMA warp + TMA warp + 4 epilogue warps
+constexpr int kCtabSmem = 4096;  // chunk-table entries staged in shared memory
 
 struct TcParams {
   CUtensorMap tm_bhi;            // packed filter planes [Np][Ktot], box {32, BN}, 64B swizzle
@@ -69,6 +73,10 @@ struct TcParams {
   int o_u, o_v, o_H, o_W;        // super-pixel: h = oh*o_u + ph < o_H
   const uint32_t* coltab;        // column -> (ph << 24) | (pw << 16) | c
   float alpha, beta;
+  int products;                  // 3 (BF16x3); 1 only for bottleneck experiments
+  int plain;                     // alpha == 1, beta == 0, nkb > 0: epilogue stores acc as is
+  int skip;                      // experiments: 1 = skip A gather, 2 = skip B TMA
+  unsigned long long* trace;     // debug: per-stage clock64 stamps of CTA 0 (or null)
   MagicDiv dOHW, dOW;
 };
 
@@ -81,7 +89,7 @@ struct Cfg {
       (200 * 1024) / STAGE_BYTES > 8 ? 8 : (200 * 1024) / STAGE_BYTES;
   static constexpr int TMEM_COLS =
       2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512));
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256 + kCtabSmem * 4;
 };
 
 // byte offset of 16-byte chunk j of row r in a K-major 64B-swizzled tile
@@ -101,6 +109,10 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
   uint64_t* tfull = empty + S;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint32_t* ctab_s = reinterpret_cast<uint32_t*>(smem + S * C::STAGE_BYTES + 256);
+  const bool ctab_in_smem = P.KC <= kCtabSmem;
+  if (ctab_in_smem)
+    for (int i = threadIdx.x; i < P.KC; i += blockDim.x) ctab_s[i] = __ldg(P.ctab + i);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == kMmaWarp) {
@@ -123,6 +135,12 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   const uint32_t smem0 = ptx::smem_u32(smem);
+  if (P.trace && threadIdx.x == 0) {
+    uint64_t gt;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+    P.trace[3000 + blockIdx.x * 4 + 0] = gt;
+    P.trace[3000 + blockIdx.x * 4 + 1] = clock64();
+  }
 
   if (warp < kProdWarps) {
     // =================================================== producers
@@ -133,10 +151,6 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
     constexpr int RSTEP = kProdWarps * 8;   // rows covered per i-step
     constexpr int RPT = kBM / RSTEP;        // rows per thread
     const int j = t & 3, rb = t >> 2;
-    if (t == 0) {
-      ptx::tma_prefetch(&P.tm_bhi);
-      ptx::tma_prefetch(&P.tm_blo);
-    }
     int it = 0;
     for (int tile = blockIdx.x; tile < P.tiles; tile += gridDim.x) {
       const int64_t mbase = int64_t(tile / P.nt) * kBM;
@@ -160,22 +174,20 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
       }
       for (int kb = 0; kb < P.nkb; kb++, it++) {
         const int s = it % S;
+        const bool tr = P.trace && blockIdx.x == 0 && t == 0 && it < 256;
+        if (tr) P.trace[it * 8 + 0] = clock64();
         if (it >= S) ptx::mbar_wait(&empty[s], ((it / S) - 1) & 1);
+        if (tr) P.trace[it * 8 + 1] = clock64();
         const uint32_t sa_hi = smem0 + s * C::STAGE_BYTES;
         const uint32_t sa_lo = sa_hi + C::A_BYTES;
         const uint32_t sb_hi = sa_lo + C::A_BYTES;
         const uint32_t sb_lo = sb_hi + C::B_BYTES;
-        if (t == 0) {
-          ptx::mbar_arrive_expect_tx(&full[s], 2 * C::B_BYTES);
-          ptx::tma_load_2d(sb_hi, &P.tm_bhi, kb * kBK, n0, &full[s]);
-          ptx::tma_load_2d(sb_lo, &P.tm_blo, kb * kBK, n0, &full[s]);
-        }
         const int ch = kb * 4 + j;
         const bool ch_ok = ch < P.KC;
-        const uint32_t e = ch_ok ? __ldg(P.ctab + ch) : 0u;
+        const uint32_t e = ch_ok ? (ctab_in_smem ? ctab_s[ch] : __ldg(P.ctab + ch)) : 0u;
         const int dh = int(e >> 24), dw = int((e >> 16) & 255), c0 = int(e & 0xFFFF);
 #pragma unroll
-        for (int i = 0; i < RPT; i++) {
+        for (int i = 0; i < RPT && !(P.skip & 1); i++) {
           const int ih = ih0[i] + dh, iw = iw0[i] + dw;
           const bool ok = ch_ok && rok[i] && unsigned(ih) < unsigned(P.IH) &&
                           unsigned(iw) < unsigned(P.IW);
@@ -185,12 +197,15 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
           ptx::cp_async16(sa_lo + dst, P.a_lo + src, ok ? 16u : 0u);
         }
         ptx::cp_async_mbar_arrive(&full[s]);
+        if (tr) P.trace[it * 8 + 2] = clock64();
       }
     }
     ptx::cp_async_wait<0>();
   } else if (warp == kMmaWarp) {
     // =================================================== MMA issuer
-    if (lane == 0) {
+    // The whole warp runs the loop (warp-uniform descriptors stay in uniform
+    // registers); one elected lane issues each tcgen05.mma / commit.
+    {
       constexpr uint32_t idesc = ptx::idesc_bf16(kBM, BN, 0, 0);
       int it = 0, lt = 0;
       for (int tile = blockIdx.x; tile < P.tiles; tile += gridDim.x, lt++) {
@@ -201,26 +216,56 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
         uint32_t acc = 0;
         for (int kb = 0; kb < P.nkb; kb++, it++) {
           const int s = it % S;
+          const bool tr = P.trace && blockIdx.x == 0 && lane == 0 && it < 256;
+          if (tr) P.trace[it * 8 + 3] = clock64();
           ptx::mbar_wait(&full[s], (it / S) & 1);
+          if (tr) P.trace[it * 8 + 4] = clock64();
           ptx::fence_proxy_async();  // producers' cp.async writes -> async proxy
           ptx::tc_fence_after();
+          if (tr) P.trace[it * 8 + 6] = clock64();
           const uint32_t sa_hi = smem0 + s * C::STAGE_BYTES;
-          const uint32_t sa_lo = sa_hi + C::A_BYTES;
-          const uint32_t sb_hi = sa_lo + C::A_BYTES;
-          const uint32_t sb_lo = sb_hi + C::B_BYTES;
-          const uint64_t dah = ptx::desc_kmajor_sw64(sa_hi), dal = ptx::desc_kmajor_sw64(sa_lo);
-          const uint64_t dbh = ptx::desc_kmajor_sw64(sb_hi), dbl = ptx::desc_kmajor_sw64(sb_lo);
+          const uint64_t dah = ptx::desc_kmajor_sw64(sa_hi);
+          const uint64_t dal = ptx::desc_kmajor_sw64(sa_hi + C::A_BYTES);
+          const uint64_t dbh = ptx::desc_kmajor_sw64(sa_hi + 2 * C::A_BYTES);
+          const uint64_t dbl = ptx::desc_kmajor_sw64(sa_hi + 2 * C::A_BYTES + C::B_BYTES);
 #pragma unroll
           for (int kk = 0; kk < kBK / 16; kk++) {
             const uint64_t o = uint64_t(kk * 2);  // +32 bytes along K
-            ptx::mma_bf16(dacc, dal + o, dbh + o, idesc, acc);
+            if (P.products == 3) {
+              ptx::mma_bf16_elect(dacc, dal + o, dbh + o, idesc, acc);
+              acc = 1;
+              ptx::mma_bf16_elect(dacc, dah + o, dbl + o, idesc, 1);
+            }
+            ptx::mma_bf16_elect(dacc, dah + o, dbh + o, idesc, acc);
             acc = 1;
-            ptx::mma_bf16(dacc, dah + o, dbl + o, idesc, 1);
-            ptx::mma_bf16(dacc, dah + o, dbh + o, idesc, 1);
+            if (tr && kk == 0) P.trace[it * 8 + 7] = clock64();
           }
-          ptx::mma_commit(&empty[s]);
+          ptx::mma_commit_elect(&empty[s]);
+          if (tr) P.trace[it * 8 + 5] = clock64();
         }
-        ptx::mma_commit(&tfull[buf]);
+        ptx::mma_commit_elect(&tfull[buf]);
+      }
+    }
+  } else if (warp == kTmaWarp) {
+    // =================================================== B tile by TMA
+    if (lane == 0) {
+      ptx::tma_prefetch(&P.tm_bhi);
+      ptx::tma_prefetch(&P.tm_blo);
+      int it = 0;
+      for (int tile = blockIdx.x; tile < P.tiles; tile += gridDim.x) {
+        const int n0 = (tile % P.nt) * BN;
+        for (int kb = 0; kb < P.nkb; kb++, it++) {
+          const int s = it % S;
+          if (it >= S) ptx::mbar_wait(&empty[s], ((it / S) - 1) & 1);
+          const uint32_t sb_hi = smem0 + s * C::STAGE_BYTES + 2 * C::A_BYTES;
+          if (P.skip & 2) {
+            ptx::mbar_arrive(&full[s]);
+          } else {
+            ptx::mbar_arrive_expect_tx(&full[s], 2 * C::B_BYTES);
+            ptx::tma_load_2d(sb_hi, &P.tm_bhi, kb * kBK, n0, &full[s]);
+            ptx::tma_load_2d(sb_hi + C::B_BYTES, &P.tm_blo, kb * kBK, n0, &full[s]);
+          }
+        }
       }
     }
   } else {
@@ -239,7 +284,10 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
         mdivmod(uint32_t(m), P.dOHW, img, rem);
         mdivmod(rem, P.dOW, oh, ow);
       }
+      const bool etr = P.trace && blockIdx.x == 0 && threadIdx.x == kThreads - 128 && lt < 16;
+      if (etr) P.trace[2048 + lt * 4 + 0] = clock64();
       ptx::mbar_wait(&tfull[buf], (lt >> 1) & 1);
+      if (etr) P.trace[2048 + lt * 4 + 1] = clock64();
       ptx::tc_fence_after();
       const int64_t rowoff =
           P.out_mode == 0 ? int64_t(img) * P.o_sn + int64_t(oh) * P.o_sh + int64_t(ow) * P.o_sw
@@ -250,32 +298,60 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
         ptx::tmem_ld32(tmem_base + (uint32_t(ew * 32) << 16) + uint32_t(buf * BN + c0), v);
         ptx::tmem_ld_wait();
         if (!row_ok) continue;
-#pragma unroll 8
-        for (int i = 0; i < 32; i++) {
-          const int col = n0 + c0 + i;
-          if (col >= P.Ncol) break;
-          int64_t off;
-          if (P.out_mode == 0) {
-            off = rowoff + int64_t(col) * P.o_sc;
-          } else {
-            const uint32_t e = __ldg(P.coltab + col);
-            const int h = int(oh) * P.o_u + int(e >> 24);
-            const int w = int(ow) * P.o_v + int((e >> 16) & 255);
-            if (h >= P.o_H || w >= P.o_W) continue;
-            off = rowoff + int64_t(e & 0xFFFF) * P.o_sc + int64_t(h) * P.o_sh + int64_t(w) * P.o_sw;
+        const int cbase = n0 + c0;
+        if (P.out_mode == 0 && P.plain && cbase + 32 <= P.Ncol) {
+          // y = acc: one store per element through a running column pointer
+          float* dst = P.out + rowoff + int64_t(cbase) * P.o_sc;
+          const int64_t sc = P.o_sc;
+#pragma unroll
+          for (int i = 0; i < 32; i++) {
+            *dst = __uint_as_float(v[i]);
+            dst += sc;
           }
-          float* dst = P.out + off;
-          const float accv = P.nkb > 0 ? __uint_as_float(v[i]) : 0.0f;
-          float val = __fmul_rn(accv, P.alpha);
-          if (P.beta != 0.0f) val = __fadd_rn(__fmul_rn(*dst, P.beta), val);
-          *dst = val;
+        } else if (P.out_mode == 0) {
+          float* rowp = P.out + rowoff + int64_t(cbase) * P.o_sc;
+#pragma unroll
+          for (int i = 0; i < 32; i++) {
+            if (cbase + i < P.Ncol) {
+              float* dst = rowp + int64_t(i) * P.o_sc;
+              const float accv = P.nkb > 0 ? __uint_as_float(v[i]) : 0.0f;
+              float val = __fmul_rn(accv, P.alpha);
+              if (P.beta != 0.0f) val = __fadd_rn(__fmul_rn(*dst, P.beta), val);
+              *dst = val;
+            }
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; i++) {
+            const int col = cbase + i;
+            if (col < P.Ncol) {
+              const uint32_t e = __ldg(P.coltab + col);
+              const int h = int(oh) * P.o_u + int(e >> 24);
+              const int w = int(ow) * P.o_v + int((e >> 16) & 255);
+              if (h < P.o_H && w < P.o_W) {
+                float* dst = P.out + rowoff + int64_t(e & 0xFFFF) * P.o_sc + int64_t(h) * P.o_sh +
+                             int64_t(w) * P.o_sw;
+                const float accv = P.nkb > 0 ? __uint_as_float(v[i]) : 0.0f;
+                float val = __fmul_rn(accv, P.alpha);
+                if (P.beta != 0.0f) val = __fadd_rn(__fmul_rn(*dst, P.beta), val);
+                *dst = val;
+              }
+            }
+          }
         }
       }
       ptx::tc_fence_before();
+      if (etr) P.trace[2048 + lt * 4 + 2] = clock64();
       ptx::mbar_arrive(&tempty[buf]);
     }
   }
   __syncthreads();
+  if (P.trace && threadIdx.x == 0) {
+    uint64_t gt;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+    P.trace[3000 + blockIdx.x * 4 + 2] = gt;
+    P.trace[3000 + blockIdx.x * 4 + 3] = clock64();
+  }
   if (warp == kMmaWarp) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc<C::TMEM_COLS>(tmem_base);
@@ -464,15 +540,55 @@ cudaError_t run_gemm(const ConvProblem& p, Gemm g, const __nv_bfloat16* a_hi,
   prm.coltab = coltab;
   prm.alpha = alpha;
   prm.beta = beta;
+  prm.plain = (alpha == 1.0f && beta == 0.0f && nkb > 0) ? 1 : 0;
+  static unsigned long long* trace_buf = nullptr;
+  const bool want_trace = getenv("DNNP_TC_TRACE") != nullptr;
+  if (want_trace && !trace_buf) cudaMalloc(&trace_buf, 8192 * sizeof(unsigned long long));
+  if (want_trace) cudaMemsetAsync(trace_buf, 0, 8192 * sizeof(unsigned long long), st);
+  prm.trace = want_trace ? trace_buf : nullptr;
+  prm.skip = getenv("DNNP_TC_SKIP") ? atoi(getenv("DNNP_TC_SKIP")) : 0;
+  prm.products = getenv("DNNP_TC_PRODUCTS") ? atoi(getenv("DNNP_TC_PRODUCTS")) : 3;
   prm.dOHW = make_magic(uint32_t(g.OH * g.OW));
   prm.dOW = make_magic(uint32_t(g.OW));
   switch (bn) {
-    case 32: return launch_gemm<32>(prm, st);
-    case 64: return launch_gemm<64>(prm, st);
-    case 128: return launch_gemm<128>(prm, st);
-    case 192: return launch_gemm<192>(prm, st);
-    default: return launch_gemm<256>(prm, st);
+    case 32: e = launch_gemm<32>(prm, st); break;
+    case 64: e = launch_gemm<64>(prm, st); break;
+    case 128: e = launch_gemm<128>(prm, st); break;
+    case 192: e = launch_gemm<192>(prm, st); break;
+    default: e = launch_gemm<256>(prm, st); break;
   }
+  if (want_trace) {
+    static unsigned long long h[8192];
+    cudaStreamSynchronize(st);
+    cudaMemcpy(h, trace_buf, sizeof h, cudaMemcpyDeviceToHost);
+    fprintf(stderr, "TRACE M=%lld ncol=%d bn=%d nkb=%d tiles=%d\n", (long long)M, pg.Ncol, bn, nkb,
+            prm.tiles);
+    const unsigned long long t0 = h[0];
+    for (int i = 0; i < 256 && i < nkb * 3; i++)
+      fprintf(stderr, "st %3d P[%7lld %7lld %7lld] M[%7lld %7lld fence %7lld kk0 %7lld commit %7lld]\n", i,
+              (long long)(h[i * 8] - t0), (long long)(h[i * 8 + 1] - t0), (long long)(h[i * 8 + 2] - t0),
+              (long long)(h[i * 8 + 3] - t0), (long long)(h[i * 8 + 4] - t0), (long long)(h[i * 8 + 6] - t0),
+              (long long)(h[i * 8 + 7] - t0), (long long)(h[i * 8 + 5] - t0));
+    {
+      unsigned long long gmin = ~0ull, gmax = 0;
+      double fsum = 0;
+      int nf = 0;
+      for (int b = 0; b < 148; b++) {
+        const unsigned long long* q = h + 3000 + b * 4;
+        if (!q[0] || !q[2]) continue;
+        gmin = std::min(gmin, q[0]);
+        gmax = std::max(gmax, q[2]);
+        fsum += double(q[3] - q[1]) / double(q[2] - q[0]);
+        nf++;
+      }
+      fprintf(stderr, "CLOCK ctas=%d kernel_span_ns=%llu mean_GHz=%.3f cta0_ns=%llu cta0_cycles=%llu\n", nf,
+              gmax - gmin, nf ? fsum / nf : 0.0, h[3002] - h[3000], h[3003] - h[3001]);
+    }
+    for (int i = 0; i < 8; i++)
+      fprintf(stderr, "ep %d [%lld %lld %lld]\n", i, (long long)(h[2048 + i * 4] - t0),
+              (long long)(h[2048 + i * 4 + 1] - t0), (long long)(h[2048 + i * 4 + 2] - t0));
+  }
+  return e;
 }
 
 // super-pixel window of one spatial dim: offsets base(ph) - jr over all phases
@@ -537,7 +653,7 @@ cudaError_t run_tc(bool dgrad, const ConvProblem& p, const float* in, const View
     g.pad_h = -pg.lo_h;
     g.pad_w = -pg.lo_w;
     pg.Ncol = int(p.u * p.v * p.C);
-    g.out_mode = 1;
+    g.out_mode = (p.u == 1 && p.v == 1) ? 0 : 1;  // unit stride: column = channel
     g.o_u = int(p.u);
     g.o_v = int(p.v);
     g.o_H = int(p.H);

@@ -197,7 +197,8 @@ __global__ void __launch_bounds__(kThreads, 1) wgrad_tc_kernel(const __grid_cons
     }
     ptx::tc_fence_before();
     }
-  } else if (lane == 0) {
+  } else {
+    // whole MMA warp runs the loop; one elected lane issues (uniform registers)
     constexpr uint32_t idesc = ptx::idesc_bf16(128, BN, 1, 1);
     uint32_t acc = 0;
     for (int kb = 0; kb < nkb; kb++) {
@@ -206,24 +207,21 @@ __global__ void __launch_bounds__(kThreads, 1) wgrad_tc_kernel(const __grid_cons
       ptx::fence_proxy_async();  // producers' cp.async writes -> async proxy
       ptx::tc_fence_after();
       const uint32_t sa_hi = smem0 + s * C::STAGE_BYTES;
-      const uint32_t sa_lo = sa_hi + C::A_BYTES;
-      const uint32_t sb_hi = sa_lo + C::A_BYTES;
-      const uint32_t sb_lo = sb_hi + C::B_BYTES;
       const uint64_t dah = ptx::desc_mnmajor_sw128(sa_hi, C::LBO, C::SBO);
-      const uint64_t dal = ptx::desc_mnmajor_sw128(sa_lo, C::LBO, C::SBO);
-      const uint64_t dbh = ptx::desc_mnmajor_sw128(sb_hi, C::LBO, C::SBO);
-      const uint64_t dbl = ptx::desc_mnmajor_sw128(sb_lo, C::LBO, C::SBO);
+      const uint64_t dal = ptx::desc_mnmajor_sw128(sa_hi + C::A_BYTES, C::LBO, C::SBO);
+      const uint64_t dbh = ptx::desc_mnmajor_sw128(sa_hi + 2 * C::A_BYTES, C::LBO, C::SBO);
+      const uint64_t dbl = ptx::desc_mnmajor_sw128(sa_hi + 2 * C::A_BYTES + C::B_BYTES, C::LBO, C::SBO);
 #pragma unroll
       for (int kk = 0; kk < kPx / 16; kk++) {
         const uint64_t o = uint64_t(kk * 2 * C::SBO) >> 4;  // 16 pixels = 2 K groups
-        ptx::mma_bf16(tmem_d, dal + o, dbh + o, idesc, acc);
+        ptx::mma_bf16_elect(tmem_d, dal + o, dbh + o, idesc, acc);
         acc = 1;
-        ptx::mma_bf16(tmem_d, dah + o, dbl + o, idesc, 1);
-        ptx::mma_bf16(tmem_d, dah + o, dbh + o, idesc, 1);
+        ptx::mma_bf16_elect(tmem_d, dah + o, dbl + o, idesc, 1);
+        ptx::mma_bf16_elect(tmem_d, dah + o, dbh + o, idesc, 1);
       }
-      ptx::mma_commit(&empty[s]);
+      ptx::mma_commit_elect(&empty[s]);
     }
-    ptx::mma_commit(tmem_full);
+    ptx::mma_commit_elect(tmem_full);
   }
   __syncthreads();
   if (warp == kProdWarps) {
