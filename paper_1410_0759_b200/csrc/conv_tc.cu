@@ -214,34 +214,38 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
         ptx::tc_fence_after();
         const uint32_t dacc = tmem_base + uint32_t(buf * BN);
         uint32_t acc = 0;
-        for (int kb = 0; kb < P.nkb; kb++, it++) {
-          const int s = it % S;
+        // two stages per iteration: one barrier-wait/fence/loop overhead per 12 MMAs
+        for (int kb = 0; kb < P.nkb; kb += 2) {
+          const int npair = P.nkb - kb >= 2 ? 2 : 1;
           const bool tr = P.trace && blockIdx.x == 0 && lane == 0 && it < 256;
           if (tr) P.trace[it * 8 + 3] = clock64();
-          ptx::mbar_wait(&full[s], (it / S) & 1);
+          ptx::mbar_wait(&full[it % S], (it / S) & 1);
+          if (npair == 2) ptx::mbar_wait(&full[(it + 1) % S], ((it + 1) / S) & 1);
           if (tr) P.trace[it * 8 + 4] = clock64();
           ptx::fence_proxy_async();  // producers' cp.async writes -> async proxy
           ptx::tc_fence_after();
           if (tr) P.trace[it * 8 + 6] = clock64();
-          const uint32_t sa_hi = smem0 + s * C::STAGE_BYTES;
-          const uint64_t dah = ptx::desc_kmajor_sw64(sa_hi);
-          const uint64_t dal = ptx::desc_kmajor_sw64(sa_hi + C::A_BYTES);
-          const uint64_t dbh = ptx::desc_kmajor_sw64(sa_hi + 2 * C::A_BYTES);
-          const uint64_t dbl = ptx::desc_kmajor_sw64(sa_hi + 2 * C::A_BYTES + C::B_BYTES);
+          for (int q = 0; q < npair; q++, it++) {
+            const int s = it % S;
+            const uint32_t sa_hi = smem0 + s * C::STAGE_BYTES;
+            const uint64_t dah = ptx::desc_kmajor_sw64(sa_hi);
+            const uint64_t dal = ptx::desc_kmajor_sw64(sa_hi + C::A_BYTES);
+            const uint64_t dbh = ptx::desc_kmajor_sw64(sa_hi + 2 * C::A_BYTES);
+            const uint64_t dbl = ptx::desc_kmajor_sw64(sa_hi + 2 * C::A_BYTES + C::B_BYTES);
 #pragma unroll
-          for (int kk = 0; kk < kBK / 16; kk++) {
-            const uint64_t o = uint64_t(kk * 2);  // +32 bytes along K
-            if (P.products == 3) {
-              ptx::mma_bf16_elect(dacc, dal + o, dbh + o, idesc, acc);
+            for (int kk = 0; kk < kBK / 16; kk++) {
+              const uint64_t o = uint64_t(kk * 2);  // +32 bytes along K
+              if (P.products == 3) {
+                ptx::mma_bf16_elect(dacc, dal + o, dbh + o, idesc, acc);
+                acc = 1;
+                ptx::mma_bf16_elect(dacc, dah + o, dbl + o, idesc, 1);
+              }
+              ptx::mma_bf16_elect(dacc, dah + o, dbh + o, idesc, acc);
               acc = 1;
-              ptx::mma_bf16_elect(dacc, dah + o, dbl + o, idesc, 1);
             }
-            ptx::mma_bf16_elect(dacc, dah + o, dbh + o, idesc, acc);
-            acc = 1;
-            if (tr && kk == 0) P.trace[it * 8 + 7] = clock64();
+            ptx::mma_commit_elect(&empty[s]);
           }
-          ptx::mma_commit_elect(&empty[s]);
-          if (tr) P.trace[it * 8 + 5] = clock64();
+          if (tr) P.trace[(it - npair) * 8 + 5] = clock64();
         }
         ptx::mma_commit_elect(&tfull[buf]);
       }

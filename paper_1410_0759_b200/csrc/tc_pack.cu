@@ -52,6 +52,32 @@ __global__ void __launch_bounds__(256) pack_act_kernel(View4 v, const float* __r
   }
 }
 
+// Cp <= 16: one thread per pixel reads its C values (pixel-contiguous across
+// the warp for NCHW) and writes Cp/8 16-byte chunks (contiguous across the warp).
+__global__ void __launch_bounds__(256) pack_act_small_kernel(View4 v, const float* __restrict__ x,
+                                                             int Cp, __nv_bfloat16* __restrict__ hi,
+                                                             __nv_bfloat16* __restrict__ lo,
+                                                             int64_t npix, MagicDiv dHW, MagicDiv dW) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t pix = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; pix < npix; pix += stride) {
+    uint32_t n, rem, h, w;
+    mdivmod(uint32_t(pix), dHW, n, rem);
+    mdivmod(rem, dW, h, w);
+    const float* src = x + int64_t(n) * v.sn + int64_t(h) * v.sh + int64_t(w) * v.sw;
+    for (int g = 0; g < Cp / 8; g++) {
+      __align__(16) __nv_bfloat16 vh[8], vl[8];
+#pragma unroll
+      for (int k = 0; k < 8; k++) {
+        const int c = g * 8 + k;
+        split_bf16(c < v.c ? __ldg(src + int64_t(c) * v.sc) : 0.0f, vh[k], vl[k]);
+      }
+      const int64_t o = pix * Cp + g * 8;
+      *reinterpret_cast<uint4*>(hi + o) = *reinterpret_cast<const uint4*>(vh);
+      *reinterpret_cast<uint4*>(lo + o) = *reinterpret_cast<const uint4*>(vl);
+    }
+  }
+}
+
 }  // namespace
 
 void pool_keep_memory() {
@@ -96,6 +122,12 @@ cudaError_t pack_act(const View4& v, const float* x, int Cp, __nv_bfloat16* hi, 
                      cudaStream_t st) {
   const int64_t npix = v.n * v.h * v.w;
   if (npix >= (int64_t(1) << 32)) return cudaErrorInvalidValue;
+  if (Cp <= 16) {
+    pack_act_small_kernel<<<grid_for(npix, 256, 8), 256, 0, st>>>(
+        v, x, Cp, hi, lo, npix, make_magic(uint32_t(v.h * v.w)), make_magic(uint32_t(v.w)));
+    note_launch();
+    return cudaGetLastError();
+  }
   const int64_t jobs = ceil_div(npix, kPix) * ceil_div(Cp, kCh);
   const unsigned grid = unsigned(std::min<int64_t>(jobs, int64_t(kNumSMs) * 16));
   pack_act_kernel<<<grid, 256, 0, st>>>(v, x, Cp, hi, lo, npix, make_magic(uint32_t(v.h * v.w)),

@@ -201,25 +201,30 @@ __global__ void __launch_bounds__(kThreads, 1) wgrad_tc_kernel(const __grid_cons
     // whole MMA warp runs the loop; one elected lane issues (uniform registers)
     constexpr uint32_t idesc = ptx::idesc_bf16(128, BN, 1, 1);
     uint32_t acc = 0;
-    for (int kb = 0; kb < nkb; kb++) {
-      const int s = kb % S;
-      ptx::mbar_wait(&full[s], (kb / S) & 1);
+    for (int kb = 0; kb < nkb; kb += 2) {
+      const int npair = nkb - kb >= 2 ? 2 : 1;
+      ptx::mbar_wait(&full[kb % S], (kb / S) & 1);
+      if (npair == 2) ptx::mbar_wait(&full[(kb + 1) % S], ((kb + 1) / S) & 1);
       ptx::fence_proxy_async();  // producers' cp.async writes -> async proxy
       ptx::tc_fence_after();
-      const uint32_t sa_hi = smem0 + s * C::STAGE_BYTES;
-      const uint64_t dah = ptx::desc_mnmajor_sw128(sa_hi, C::LBO, C::SBO);
-      const uint64_t dal = ptx::desc_mnmajor_sw128(sa_hi + C::A_BYTES, C::LBO, C::SBO);
-      const uint64_t dbh = ptx::desc_mnmajor_sw128(sa_hi + 2 * C::A_BYTES, C::LBO, C::SBO);
-      const uint64_t dbl = ptx::desc_mnmajor_sw128(sa_hi + 2 * C::A_BYTES + C::B_BYTES, C::LBO, C::SBO);
+      for (int q = 0; q < npair; q++) {
+        const int s = (kb + q) % S;
+        const uint32_t sa_hi = smem0 + s * C::STAGE_BYTES;
+        const uint64_t dah = ptx::desc_mnmajor_sw128(sa_hi, C::LBO, C::SBO);
+        const uint64_t dal = ptx::desc_mnmajor_sw128(sa_hi + C::A_BYTES, C::LBO, C::SBO);
+        const uint64_t dbh = ptx::desc_mnmajor_sw128(sa_hi + 2 * C::A_BYTES, C::LBO, C::SBO);
+        const uint64_t dbl =
+            ptx::desc_mnmajor_sw128(sa_hi + 2 * C::A_BYTES + C::B_BYTES, C::LBO, C::SBO);
 #pragma unroll
-      for (int kk = 0; kk < kPx / 16; kk++) {
-        const uint64_t o = uint64_t(kk * 2 * C::SBO) >> 4;  // 16 pixels = 2 K groups
-        ptx::mma_bf16_elect(tmem_d, dal + o, dbh + o, idesc, acc);
-        acc = 1;
-        ptx::mma_bf16_elect(tmem_d, dah + o, dbl + o, idesc, 1);
-        ptx::mma_bf16_elect(tmem_d, dah + o, dbh + o, idesc, 1);
+        for (int kk = 0; kk < kPx / 16; kk++) {
+          const uint64_t o = uint64_t(kk * 2 * C::SBO) >> 4;  // 16 pixels = 2 K groups
+          ptx::mma_bf16_elect(tmem_d, dal + o, dbh + o, idesc, acc);
+          acc = 1;
+          ptx::mma_bf16_elect(tmem_d, dah + o, dbl + o, idesc, 1);
+          ptx::mma_bf16_elect(tmem_d, dah + o, dbh + o, idesc, 1);
+        }
+        ptx::mma_commit_elect(&empty[s]);
       }
-      ptx::mma_commit_elect(&empty[s]);
     }
     ptx::mma_commit_elect(tmem_full);
   }
