@@ -296,3 +296,30 @@ def test_native_kernels_launched():
     y = dp.empty_view(x.desc, device="cuda")
     dp.activation_forward("relu", x, y)
     assert dp.kernel_launch_count() > before
+
+
+REF_DIR = os.path.join(ROOT, "oracle", "_ref")
+
+
+@pytest.mark.skipif(not os.path.exists(os.path.join(REF_DIR, "test_capi_ref")),
+                    reason="reference C test not built (oracle/build_ref.sh)")
+def test_reference_capi_program_unchanged():
+    """The reference's own pkg/capi/tests/test_capi.c, compiled unchanged
+    against include/dnnp.h and linked to libdnnp.so: all 58 checks pass."""
+    r = subprocess.run([os.path.join(REF_DIR, "test_capi_ref")], capture_output=True, text=True,
+                       timeout=300)
+    assert r.returncode == 0, r.stdout[-3000:]
+    assert "58 passed, 0 failed" in r.stdout
+
+
+@pytest.mark.skipif(not os.path.exists(os.path.join(REF_DIR, "conv_example_ref")),
+                    reason="reference example not built (oracle/build_ref.sh)")
+def test_reference_example_golden_bytes(tmp_path):
+    """pkg/capi/examples/conv_example.c unchanged: its raw f32 output equals
+    the reference native golden bytes (Makefile:36-41 `cmp`)."""
+    out = tmp_path / "example.bin"
+    r = subprocess.run([os.path.join(REF_DIR, "conv_example_ref"), str(out)], capture_output=True,
+                       text=True, timeout=120)
+    assert r.returncode == 0, r.stderr
+    golden = np.array([7, -36, 10, -11, -5, 5, 25, -9], dtype=np.float32).tobytes()
+    assert out.read_bytes() == golden
