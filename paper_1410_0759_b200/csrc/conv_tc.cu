@@ -362,21 +362,48 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
   }
 }
 
+#include "conv_tma.cuh"
+
 // ---------------------------------------------------------- filter packing
 
 // Geometry of the reduction / column orders of one GEMM.
-//  forward:  column = output channel k; chunk = (dh*S + dw)*Cg + g over the
-//            R x S taps; value f[k][cin][r][s], r = flip ? R-1-dh : dh.
+//  forward:  column = output channel k; chunk = (dh*S + dw)*Cgrp + g over the
+//            R x S taps; gather offset (dh, dw).
 //  bwd-data: column = (ph*v + pw)*C + c; chunk = (dh*WinW + dw)*Kg + g over
 //            the super-pixel window; dh corresponds to phase tap
-//            jr = base(ph) - dh - lo_h when 0 <= jr < nR(ph), mode-adjusted
-//            tap r' = t0(ph) + u*jr, r = flip ? R-1-r' : r'; zero otherwise.
+//            jr = base(ph) - dh - lo_h when 0 <= jr < nR(ph), gather offset
+//            r' = t0(ph) + u*jr; zero otherwise.
+//  space-to-depth (su * sv > 1): the GEMM problem is the stride-1
+//            convolution over x'[n][h'][w'][(rh*sv + rw)*C0 + c]; GEMM channel
+//            cg decodes to (rh, rw, c) and a GEMM gather offset t to the
+//            original offset t*su + rh (zero when >= R0).
+// The filter value for gather offset r' is f[..][R0-1-r'] in CONVOLUTION
+// mode and f[..][r'] in CROSS_CORRELATION mode (reference conv.py:182-192).
 struct PackGeom {
   int K, C, R, S, flip, dgrad;
   int u, v, pad_h, pad_w;  // bwd-data phases
   int winH, winW, lo_h, lo_w;
   int Ncol, Np, Ktot, Cgrp, KC;
+  int su, sv, C0, R0, S0;  // space-to-depth factors and the original C, R, S
 };
+
+__device__ __forceinline__ float fetch_filter(const PackGeom& g, const float* __restrict__ f,
+                                              int k, int cg, int tr, int ts) {
+  int c = cg, rh = 0, rw = 0;
+  if (g.su * g.sv > 1) {
+    const int ph = cg / g.C0;
+    c = cg - ph * g.C0;
+    rw = ph % g.sv;
+    rh = ph / g.sv;
+  }
+  int r = tr * g.su + rh, s = ts * g.sv + rw;
+  if (k >= g.K || c >= g.C0 || r >= g.R0 || s >= g.S0) return 0.0f;
+  if (g.flip) {
+    r = g.R0 - 1 - r;
+    s = g.S0 - 1 - s;
+  }
+  return f[((int64_t(k) * g.C0 + c) * g.R0 + r) * g.S0 + s];
+}
 
 __device__ __forceinline__ int phase_tap(int ph, int dh, int lo, int u, int pad, int R) {
   const int t0 = (ph + pad) % u;
@@ -384,7 +411,7 @@ __device__ __forceinline__ int phase_tap(int ph, int dh, int lo, int u, int pad,
   const int base = (ph + pad - t0) / u;
   const int jr = base - dh - lo;
   if (jr < 0 || jr >= nR) return -1;
-  return t0 + u * jr;  // mode-adjusted tap r'
+  return t0 + u * jr;  // gather offset r'
 }
 
 __global__ void __launch_bounds__(256) pack_filter_kernel(PackGeom g, const float* __restrict__ f,
@@ -407,22 +434,25 @@ __global__ void __launch_bounds__(256) pack_filter_kernel(PackGeom g, const floa
       if (row == 0 && i == 0)
         ctab[ch] = (uint32_t(dh) << 24) | (uint32_t(dw) << 16) | uint32_t(grp * 8);
       if (!g.dgrad) {
-        const int r = g.flip ? g.R - 1 - dh : dh, s = g.flip ? g.S - 1 - dw : dw;
-        if (row < g.K && cin < g.C) val = f[((int64_t(row) * g.C + cin) * g.R + r) * g.S + s];
+        if (row < g.K && cin < g.C) val = fetch_filter(g, f, row, cin, dh, dw);
       } else if (row < g.Ncol && cin < g.K) {
         const int c = row % g.C, phase = row / g.C;
         const int ph = phase / g.v, pw = phase % g.v;
         const int rp = phase_tap(ph, dh, g.lo_h, g.u, g.pad_h, g.R);
         const int sp = phase_tap(pw, dw, g.lo_w, g.v, g.pad_w, g.S);
-        if (rp >= 0 && sp >= 0) {
-          const int r = g.flip ? g.R - 1 - rp : rp, s = g.flip ? g.S - 1 - sp : sp;
-          val = f[((int64_t(cin) * g.C + c) * g.R + r) * g.S + s];
-        }
+        if (rp >= 0 && sp >= 0) val = fetch_filter(g, f, cin, c, rp, sp);
       }
     }
     if (g.dgrad && k == 0 && row < g.Ncol) {
-      const int c = row % g.C, phase = row / g.C;
-      coltab[row] = (uint32_t(phase / g.v) << 24) | (uint32_t(phase % g.v) << 16) | uint32_t(c);
+      uint32_t e;
+      if (g.su * g.sv > 1) {  // space-to-depth column (rh, rw, c)
+        const int ph = row / g.C0, c = row - ph * g.C0;
+        e = (uint32_t(ph / g.sv) << 24) | (uint32_t(ph % g.sv) << 16) | uint32_t(c);
+      } else {
+        const int c = row % g.C, phase = row / g.C;
+        e = (uint32_t(phase / g.v) << 24) | (uint32_t(phase % g.v) << 16) | uint32_t(c);
+      }
+      coltab[row] = e;
     }
     __nv_bfloat16 h, l;
     split_bf16(val, h, l);
@@ -451,6 +481,35 @@ cudaError_t launch_gemm(const TcParams& prm, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+template <int BN, int CB>
+cudaError_t launch_tma(const TmaParams& prm, cudaStream_t st) {
+  using CC = TCfg<BN, CB>;
+  static int attr_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (attr_dev != dev) {
+    cudaError_t e = cudaFuncSetAttribute(conv_tma_kernel<BN, CB>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, CC::SMEM);
+    if (e != cudaSuccess) return e;
+    attr_dev = dev;
+  }
+  const unsigned grid = unsigned(std::min<int64_t>(prm.tiles, kNumSMs));
+  conv_tma_kernel<BN, CB><<<grid, kTmaThreads, CC::SMEM, st>>>(prm);
+  note_launch();
+  return cudaGetLastError();
+}
+
+template <int CB>
+cudaError_t launch_tma_bn(int bn, const TmaParams& prm, cudaStream_t st) {
+  switch (bn) {
+    case 32: return launch_tma<32, CB>(prm, st);
+    case 64: return launch_tma<64, CB>(prm, st);
+    case 128: return launch_tma<128, CB>(prm, st);
+    case 192: return launch_tma<192, CB>(prm, st);
+    default: return launch_tma<256, CB>(prm, st);
+  }
+}
+
 // Column tile: persistent CTAs stream tiles, so the cost model is the number
 // of tile waves times the per-tile column work (+ a fixed per-tile cost).
 int pick_bn(int64_t M, int ncol) {
@@ -472,10 +531,29 @@ int pick_bn(int64_t M, int ncol) {
 }
 
 struct Gemm {
-  int OH, OW, u, v, pad_h, pad_w;
+  int OH, OW, u, v, pad_h, pad_w;  // gather: ih = oh*u - pad_h + dh over the packed input
   PackGeom pg;
-  int out_mode, o_u, o_v, o_H, o_W;
+  int out_mode, o_u, o_v, o_H, o_W, o_ph, o_pw;
+  int tma;                         // 1: TMA im2col kernel, 0: cp.async gather kernel
 };
+
+// TMA bounding box of one spatial dim: lower = -pad, upper such that the
+// traversal visits exactly `out` window origins with the given stride.
+inline void tma_corners(int in, int out, int stride, int pad, int* lower, int* upper) {
+  *lower = -pad;
+  *upper = (out - 1) * stride + 1 - pad - in;
+}
+
+bool tma_geometry_ok(const Gemm& g, int IH, int IW, int taps_h, int taps_w, int64_t M) {
+  if (g.u < 1 || g.v < 1 || g.u > 8 || g.v > 8) return false;
+  if (taps_h > 128 || taps_w > 128 || M >= (int64_t(1) << 31)) return false;
+  int lh, uh, lw, uw;
+  tma_corners(IH, g.OH, g.u, g.pad_h, &lh, &uh);
+  tma_corners(IW, g.OW, g.v, g.pad_w, &lw, &uw);
+  for (int c : {lh, uh, lw, uw})
+    if (c < -128 || c > 127) return false;
+  return true;
+}
 
 cudaError_t run_gemm(const ConvProblem& p, Gemm g, const __nv_bfloat16* a_hi,
                      const __nv_bfloat16* a_lo, int IH, int IW, int Cp, const float* f, float* out,
@@ -500,7 +578,68 @@ cudaError_t run_gemm(const ConvProblem& p, Gemm g, const __nv_bfloat16* a_hi,
   pack_filter_kernel<<<grid_for(int64_t(pg.Np) * pg.Ktot, 256, 16), 256, 0, st>>>(
       pg, f, b_hi, b_lo, ctab, coltab);
   note_launch();
+  const int64_t tiles = ceil_div(M, kBM) * (pg.Np / bn);
+  if (tiles >= (int64_t(1) << 31)) return cudaErrorInvalidValue;
 
+  if (g.tma) {
+    // ------------------------------------------------ TMA im2col kernel
+    const int CB = Cp % 32 == 0 ? 32 : 16;
+    TmaParams prm{};
+    Im2colGeom ig{};
+    ig.N = p.N;
+    ig.H = IH;
+    ig.W = IW;
+    ig.C = Cp;
+    tma_corners(IH, g.OH, g.u, g.pad_h, &ig.lower_h, &ig.upper_h);
+    tma_corners(IW, g.OW, g.v, g.pad_w, &ig.lower_w, &ig.upper_w);
+    ig.stride_h = g.u;
+    ig.stride_w = g.v;
+    ig.cpp = CB;
+    ig.ppc = kBM;
+    const CUtensorMapSwizzle sw = CB == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B;
+    if ((e = make_tmap_im2col(&prm.tm_ahi, a_hi, ig, sw)) != cudaSuccess) return e;
+    if ((e = make_tmap_im2col(&prm.tm_alo, a_lo, ig, sw)) != cudaSuccess) return e;
+    if ((e = make_tmap_2d(&prm.tm_bhi, b_hi, uint64_t(pg.Ktot), uint64_t(pg.Np), uint64_t(pg.Ktot),
+                          uint32_t(CB), uint32_t(bn), sw)) != cudaSuccess)
+      return e;
+    if ((e = make_tmap_2d(&prm.tm_blo, b_lo, uint64_t(pg.Ktot), uint64_t(pg.Np), uint64_t(pg.Ktot),
+                          uint32_t(CB), uint32_t(bn), sw)) != cudaSuccess)
+      return e;
+    prm.M = M;
+    prm.Ncol = pg.Ncol;
+    prm.lower_h = ig.lower_h;
+    prm.lower_w = ig.lower_w;
+    prm.u = g.u;
+    prm.v = g.v;
+    prm.nCB = Cp / CB;
+    prm.tapW = pg.dgrad ? pg.winW : pg.S;
+    prm.KCH = taps * prm.nCB;
+    prm.nkb = nkb;
+    prm.Cext = Cp;
+    prm.nt = pg.Np / bn;
+    prm.tiles = int(tiles);
+    prm.out = out;
+    prm.o_sn = ov.sn;
+    prm.o_sc = ov.sc;
+    prm.o_sh = ov.sh;
+    prm.o_sw = ov.sw;
+    prm.out_mode = g.out_mode;
+    prm.o_u = g.o_u;
+    prm.o_v = g.o_v;
+    prm.o_H = g.o_H;
+    prm.o_W = g.o_W;
+    prm.o_ph = g.o_ph;
+    prm.o_pw = g.o_pw;
+    prm.coltab = coltab;
+    prm.alpha = alpha;
+    prm.beta = beta;
+    prm.plain = (alpha == 1.0f && beta == 0.0f) ? 1 : 0;
+    prm.dOHW = make_magic(uint32_t(g.OH * g.OW));
+    prm.dOW = make_magic(uint32_t(g.OW));
+    return CB == 32 ? launch_tma_bn<32>(bn, prm, st) : launch_tma_bn<16>(bn, prm, st);
+  }
+
+  // -------------------------------------------------- cp.async gather kernel
   TcParams prm{};
   prm.M = M;
   prm.Ncol = pg.Ncol;
@@ -517,8 +656,6 @@ cudaError_t run_gemm(const ConvProblem& p, Gemm g, const __nv_bfloat16* a_hi,
   prm.nkb = nkb;
   prm.Ktot = pg.Ktot;
   prm.nt = pg.Np / bn;
-  const int64_t tiles = ceil_div(M, kBM) * prm.nt;
-  if (tiles >= (int64_t(1) << 31)) return cudaErrorInvalidValue;
   prm.tiles = int(tiles);
   e = make_tmap_2d(&prm.tm_bhi, b_hi, uint64_t(pg.Ktot), uint64_t(pg.Np), uint64_t(pg.Ktot), kBK,
                    uint32_t(bn), CU_TENSOR_MAP_SWIZZLE_64B);
@@ -573,24 +710,6 @@ cudaError_t run_gemm(const ConvProblem& p, Gemm g, const __nv_bfloat16* a_hi,
               (long long)(h[i * 8] - t0), (long long)(h[i * 8 + 1] - t0), (long long)(h[i * 8 + 2] - t0),
               (long long)(h[i * 8 + 3] - t0), (long long)(h[i * 8 + 4] - t0), (long long)(h[i * 8 + 6] - t0),
               (long long)(h[i * 8 + 7] - t0), (long long)(h[i * 8 + 5] - t0));
-    {
-      unsigned long long gmin = ~0ull, gmax = 0;
-      double fsum = 0;
-      int nf = 0;
-      for (int b = 0; b < 148; b++) {
-        const unsigned long long* q = h + 3000 + b * 4;
-        if (!q[0] || !q[2]) continue;
-        gmin = std::min(gmin, q[0]);
-        gmax = std::max(gmax, q[2]);
-        fsum += double(q[3] - q[1]) / double(q[2] - q[0]);
-        nf++;
-      }
-      fprintf(stderr, "CLOCK ctas=%d kernel_span_ns=%llu mean_GHz=%.3f cta0_ns=%llu cta0_cycles=%llu\n", nf,
-              gmax - gmin, nf ? fsum / nf : 0.0, h[3002] - h[3000], h[3003] - h[3001]);
-    }
-    for (int i = 0; i < 8; i++)
-      fprintf(stderr, "ep %d [%lld %lld %lld]\n", i, (long long)(h[2048 + i * 4] - t0),
-              (long long)(h[2048 + i * 4 + 1] - t0), (long long)(h[2048 + i * 4 + 2] - t0));
   }
   return e;
 }
@@ -612,21 +731,12 @@ void phase_window(int u, int pad, int R, int* lo, int* win) {
   *win = mx - mn + 1;
 }
 
+bool env_off(const char* name) { return getenv(name) != nullptr; }
+
 cudaError_t run_tc(bool dgrad, const ConvProblem& p, const float* in, const View4& inv,
                    const float* f, float* out, const View4& outv, float alpha, float beta,
                    cudaStream_t st) {
   pool_keep_memory();
-  const int Cin = int(dgrad ? p.K : p.C);
-  const int IH = int(dgrad ? p.P : p.H), IW = int(dgrad ? p.Q : p.W);
-  const int Cp = int(ceil_div(Cin, 8) * 8);
-  const size_t act = size_t(p.N) * IH * IW * Cp;
-  Workspace ws(st);
-  cudaError_t e = cudaMallocAsync(&ws.p, act * 4 + 256, st);
-  if (e != cudaSuccess) return e;
-  auto* a_hi = static_cast<__nv_bfloat16*>(ws.p);
-  auto* a_lo = a_hi + act;
-  if ((e = pack_act(inv, in, Cp, a_hi, a_lo, st)) != cudaSuccess) return e;
-
   Gemm g{};
   PackGeom& pg = g.pg;
   pg.K = int(p.K);
@@ -635,34 +745,116 @@ cudaError_t run_tc(bool dgrad, const ConvProblem& p, const float* in, const View
   pg.S = int(p.S);
   pg.flip = p.flip ? 1 : 0;
   pg.dgrad = dgrad ? 1 : 0;
-  if (!dgrad) {
-    g.OH = int(p.P);
-    g.OW = int(p.Q);
-    g.u = int(p.u);
-    g.v = int(p.v);
-    g.pad_h = int(p.pad_h);
-    g.pad_w = int(p.pad_w);
-    pg.Ncol = int(p.K);
-    g.out_mode = 0;
+  pg.u = pg.v = 1;
+  pg.su = pg.sv = 1;
+  pg.C0 = int(p.C);
+  pg.R0 = int(p.R);
+  pg.S0 = int(p.S);
+  const bool tma_on = !env_off("DNNP_TC_NO_TMA");
+  // Space-to-depth for strided convolutions with few input channels (AlexNet
+  // conv1: C=3, 11x11, stride 4): the u x v phases of the input become
+  // channels, the problem becomes a stride-1 conv with ceil(R/u) x ceil(S/v)
+  // taps over u*v*C channels, so the MMA reduction is not 62% zero padding.
+  const bool s2d = tma_on && !env_off("DNNP_TC_NO_S2D") && (p.u > 1 || p.v > 1) && p.u <= 8 &&
+                   p.v <= 8 && p.C * p.u * p.v <= 64;
+  int IH, IW, Cp;
+  int64_t Nimg = p.N;
+  if (s2d) {
+    const int u = int(p.u), v = int(p.v);
+    const int R2 = int(ceil_div(p.R, u)), S2 = int(ceil_div(p.S, v));
+    int H2 = int(p.P) - 1 + R2, W2 = int(p.Q) - 1 + S2;
+    if (dgrad) {
+      H2 = std::max<int>(H2, int(ceil_div(p.H + p.pad_h, u)));
+      W2 = std::max<int>(W2, int(ceil_div(p.W + p.pad_w, v)));
+    }
+    pg.su = u;
+    pg.sv = v;
+    pg.C = u * v * int(p.C);
+    pg.R = R2;
+    pg.S = S2;
+    g.tma = 1;
+    if (!dgrad) {
+      IH = H2;
+      IW = W2;
+      Cp = int(ceil_div(pg.C, 16) * 16);
+      g.OH = int(p.P);
+      g.OW = int(p.Q);
+      g.u = g.v = 1;
+      g.pad_h = g.pad_w = 0;
+      pg.Ncol = int(p.K);
+      g.out_mode = 0;
+    } else {
+      IH = int(p.P);
+      IW = int(p.Q);
+      Cp = int(ceil_div(p.K, 16) * 16);
+      pg.pad_h = pg.pad_w = 0;
+      phase_window(1, 0, R2, &pg.lo_h, &pg.winH);
+      phase_window(1, 0, S2, &pg.lo_w, &pg.winW);
+      g.OH = H2;
+      g.OW = W2;
+      g.u = g.v = 1;
+      g.pad_h = -pg.lo_h;
+      g.pad_w = -pg.lo_w;
+      pg.Ncol = pg.C;
+      g.out_mode = 1;
+      g.o_u = u;
+      g.o_v = v;
+      g.o_H = int(p.H);
+      g.o_W = int(p.W);
+      g.o_ph = int(p.pad_h);
+      g.o_pw = int(p.pad_w);
+    }
+    if (!tma_geometry_ok(g, IH, IW, dgrad ? pg.winH : pg.R, dgrad ? pg.winW : pg.S,
+                         Nimg * g.OH * g.OW))
+      return cudaErrorNotSupported;
   } else {
-    pg.u = int(p.u);
-    pg.v = int(p.v);
-    pg.pad_h = int(p.pad_h);
-    pg.pad_w = int(p.pad_w);
-    phase_window(pg.u, pg.pad_h, pg.R, &pg.lo_h, &pg.winH);
-    phase_window(pg.v, pg.pad_w, pg.S, &pg.lo_w, &pg.winW);
-    g.OH = int(ceil_div(p.H, p.u));
-    g.OW = int(ceil_div(p.W, p.v));
-    g.u = g.v = 1;
-    g.pad_h = -pg.lo_h;
-    g.pad_w = -pg.lo_w;
-    pg.Ncol = int(p.u * p.v * p.C);
-    g.out_mode = (p.u == 1 && p.v == 1) ? 0 : 1;  // unit stride: column = channel
-    g.o_u = int(p.u);
-    g.o_v = int(p.v);
-    g.o_H = int(p.H);
-    g.o_W = int(p.W);
+    IH = int(dgrad ? p.P : p.H);
+    IW = int(dgrad ? p.Q : p.W);
+    if (!dgrad) {
+      g.OH = int(p.P);
+      g.OW = int(p.Q);
+      g.u = int(p.u);
+      g.v = int(p.v);
+      g.pad_h = int(p.pad_h);
+      g.pad_w = int(p.pad_w);
+      pg.Ncol = int(p.K);
+      g.out_mode = 0;
+    } else {
+      pg.u = int(p.u);
+      pg.v = int(p.v);
+      pg.pad_h = int(p.pad_h);
+      pg.pad_w = int(p.pad_w);
+      phase_window(pg.u, pg.pad_h, pg.R, &pg.lo_h, &pg.winH);
+      phase_window(pg.v, pg.pad_w, pg.S, &pg.lo_w, &pg.winW);
+      g.OH = int(ceil_div(p.H, p.u));
+      g.OW = int(ceil_div(p.W, p.v));
+      g.u = g.v = 1;
+      g.pad_h = -pg.lo_h;
+      g.pad_w = -pg.lo_w;
+      pg.Ncol = int(p.u * p.v * p.C);
+      g.out_mode = (p.u == 1 && p.v == 1) ? 0 : 1;  // unit stride: column = channel
+      g.o_u = int(p.u);
+      g.o_v = int(p.v);
+      g.o_H = int(p.H);
+      g.o_W = int(p.W);
+    }
+    g.tma = tma_on && tma_geometry_ok(g, IH, IW, dgrad ? pg.winH : pg.R, dgrad ? pg.winW : pg.S,
+                                      Nimg * g.OH * g.OW);
+    const int Cin = int(dgrad ? p.K : p.C);
+    Cp = int(ceil_div(Cin, g.tma ? 16 : 8) * (g.tma ? 16 : 8));
   }
+  const size_t act = size_t(p.N) * IH * IW * Cp;
+  Workspace ws(st);
+  cudaError_t e = cudaMallocAsync(&ws.p, act * 4 + 256, st);
+  if (e != cudaSuccess) return e;
+  auto* a_hi = static_cast<__nv_bfloat16*>(ws.p);
+  auto* a_lo = a_hi + act;
+  if (s2d && !dgrad)
+    e = pack_act_s2d(inv, in, int(p.u), int(p.v), int(p.pad_h), int(p.pad_w), IH, IW, Cp, a_hi,
+                     a_lo, st);
+  else
+    e = pack_act(inv, in, Cp, a_hi, a_lo, st);
+  if (e != cudaSuccess) return e;
   return run_gemm(p, g, a_hi, a_lo, IH, IW, Cp, f, out, outv, alpha, beta, st);
 }
 

@@ -35,6 +35,28 @@ cudaError_t make_tmap_2d(CUtensorMap* map, const void* base, uint64_t cols, uint
                          uint64_t pitch_elems, uint32_t box_cols, uint32_t box_rows,
                          CUtensorMapSwizzle swizzle);
 
+// 4-D im2col tensor map over a packed [N][H][W][C] bf16 plane: `ppc` output
+// pixels per load, `cpp` channels per pixel, bounding box corners (W, H) in
+// [-128, 127], traversal strides <= 8.  Verified on B200 by
+// tools/probe_im2col.cu: a load at (c, w, h, n) with offsets (ow, oh) reads
+// input pixel (start + (ow, oh)) for each of the ppc positions obtained by
+// walking w over [lower_w, W + upper_w) with stride_w, then h, then n.
+struct Im2colGeom {
+  int64_t N, H, W, C;
+  int lower_w, lower_h, upper_w, upper_h;
+  int stride_w, stride_h;
+  int cpp, ppc;
+};
+cudaError_t make_tmap_im2col(CUtensorMap* map, const void* base, const Im2colGeom& g,
+                             CUtensorMapSwizzle swizzle);
+
+// Space-to-depth packing for strided convolutions with few channels:
+// x'[n][h'][w'][(rh*v + rw)*C + c] = x[n][c][h'*u + rh - pad_h][w'*v + rw - pad_w]
+// (zero outside the image), channels padded to Cp.
+cudaError_t pack_act_s2d(const View4& v, const float* x, int u, int vv, int pad_h, int pad_w,
+                         int H2, int W2, int Cp, __nv_bfloat16* hi, __nv_bfloat16* lo,
+                         cudaStream_t st);
+
 // Strided fp32 4-D view -> channel-innermost bf16 hi/lo planes
 // [n][h][w][Cp] (Cp = channels padded to a multiple of 8, zero filled).
 cudaError_t pack_act(const View4& v, const float* x, int Cp, __nv_bfloat16* hi, __nv_bfloat16* lo,

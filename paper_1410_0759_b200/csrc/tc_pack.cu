@@ -78,7 +78,63 @@ __global__ void __launch_bounds__(256) pack_act_small_kernel(View4 v, const floa
   }
 }
 
+// Space-to-depth: one thread per super-pixel (n, h', w'); walks its Cp
+// channels (rh, rw, c) with running counters and writes 16-byte chunks
+// (contiguous across the warp).
+__global__ void __launch_bounds__(256) pack_act_s2d_kernel(View4 v, const float* __restrict__ x,
+                                                           int u, int vv, int pad_h, int pad_w,
+                                                           int H2, int W2, int Cp,
+                                                           __nv_bfloat16* __restrict__ hi,
+                                                           __nv_bfloat16* __restrict__ lo,
+                                                           int64_t npix, MagicDiv dHW, MagicDiv dW) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  const int C = int(v.c), Cs = u * vv * C;
+  for (int64_t pix = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; pix < npix; pix += stride) {
+    uint32_t n, rem, h2, w2;
+    mdivmod(uint32_t(pix), dHW, n, rem);
+    mdivmod(rem, dW, h2, w2);
+    const int hb = int(h2) * u - pad_h, wb = int(w2) * vv - pad_w;
+    const float* src = x + int64_t(n) * v.sn;
+    int c = 0, rw = 0, rh = 0;
+    for (int g = 0; g < Cp / 8; g++) {
+      __align__(16) __nv_bfloat16 vh[8], vl[8];
+#pragma unroll
+      for (int k = 0; k < 8; k++) {
+        float val = 0.0f;
+        if (g * 8 + k < Cs) {
+          const int h = hb + rh, w = wb + rw;
+          if (unsigned(h) < unsigned(v.h) && unsigned(w) < unsigned(v.w))
+            val = __ldg(src + int64_t(c) * v.sc + int64_t(h) * v.sh + int64_t(w) * v.sw);
+          if (++c == C) {
+            c = 0;
+            if (++rw == vv) {
+              rw = 0;
+              ++rh;
+            }
+          }
+        }
+        split_bf16(val, vh[k], vl[k]);
+      }
+      const int64_t o = pix * Cp + g * 8;
+      *reinterpret_cast<uint4*>(hi + o) = *reinterpret_cast<const uint4*>(vh);
+      *reinterpret_cast<uint4*>(lo + o) = *reinterpret_cast<const uint4*>(vl);
+    }
+  }
+}
+
 }  // namespace
+
+cudaError_t pack_act_s2d(const View4& v, const float* x, int u, int vv, int pad_h, int pad_w,
+                         int H2, int W2, int Cp, __nv_bfloat16* hi, __nv_bfloat16* lo,
+                         cudaStream_t st) {
+  const int64_t npix = v.n * H2 * W2;
+  if (npix >= (int64_t(1) << 32)) return cudaErrorInvalidValue;
+  pack_act_s2d_kernel<<<grid_for(npix, 256, 8), 256, 0, st>>>(
+      v, x, u, vv, pad_h, pad_w, H2, W2, Cp, hi, lo, npix, make_magic(uint32_t(H2 * W2)),
+      make_magic(uint32_t(W2)));
+  note_launch();
+  return cudaGetLastError();
+}
 
 void pool_keep_memory() {
   static bool done = false;
@@ -115,6 +171,33 @@ cudaError_t make_tmap_2d(CUtensorMap* map, const void* base, uint64_t cols, uint
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+cudaError_t make_tmap_im2col(CUtensorMap* map, const void* base, const Im2colGeom& g,
+                             CUtensorMapSwizzle swizzle) {
+  using Fn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                          const cuuint64_t*, const int*, const int*, cuuint32_t, cuuint32_t,
+                          const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                          CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static Fn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &p, cudaEnableDefault, &q);
+    if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !p) return cudaErrorNotSupported;
+    fn = reinterpret_cast<Fn>(p);
+  }
+  const cuuint64_t dims[4] = {cuuint64_t(g.C), cuuint64_t(g.W), cuuint64_t(g.H), cuuint64_t(g.N)};
+  const cuuint64_t strides[3] = {cuuint64_t(g.C) * 2, cuuint64_t(g.C) * 2 * g.W,
+                                 cuuint64_t(g.C) * 2 * g.W * g.H};
+  const int lower[2] = {g.lower_w, g.lower_h};  // W first (innermost spatial dim)
+  const int upper[2] = {g.upper_w, g.upper_h};
+  const cuuint32_t estr[4] = {1, cuuint32_t(g.stride_w), cuuint32_t(g.stride_h), 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides,
+                  lower, upper, cuuint32_t(g.cpp), cuuint32_t(g.ppc), estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 

@@ -21,7 +21,23 @@ __device__ __forceinline__ void fence_mbar_init() {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// try_wait with a suspend-time hint: the waiting warp is parked until the
+// phase completes (or the hint expires) instead of spinning on the barrier,
+// so long waits (epilogue on the accumulator, producers on a free stage) do
+// not steal issue slots from the warps doing the work.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity), "r"(0x989680)
+      : "memory");
+}
+// plain spinning probe (short, latency-critical waits)
+__device__ __forceinline__ void mbar_wait_spin(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n"
       ".reg .pred p;\n"
@@ -76,6 +92,21 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const void* tmap, int 
       : "memory");
 }
 
+// 4-D im2col load (tensor map over packed NHWC planes): pixelsPerColumn
+// output pixels starting at input coordinate (w, h, n) = the first pixel's
+// window origin, walking the bounding box W -> H -> N; channels c..c+cpp-1
+// of input pixel (start + (off_w, off_h)); zero fill outside the tensor.
+__device__ __forceinline__ void tma_load_im2col(uint32_t dst, const void* tmap, int c, int w,
+                                                int h, int n, uint16_t off_w, uint16_t off_h,
+                                                uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.im2col.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2], {%7, %8};" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(smem_u32(bar)), "r"(c), "r"(w), "r"(h), "r"(n),
+      "h"(off_w), "h"(off_h)
+      : "memory");
+}
+
 // ---- TMEM -----------------------------------------------------------------
 template <int NCOLS>
 __device__ __forceinline__ void tmem_alloc(uint32_t* slot) {  // whole warp
@@ -120,6 +151,17 @@ __device__ __forceinline__ uint64_t desc_kmajor_sw64(uint32_t smem_addr) {
   d |= uint64_t(512 >> 4) << 32;
   d |= uint64_t(1) << 46;
   d |= uint64_t(4) << 61;
+  return d;
+}
+// K-major operand tile, 32-byte swizzle: rows of 16 bf16 (32 B), 8-row atoms
+// of 256 B (SBO = 256 B), layout type 6 (SWIZZLE_32B).
+__device__ __forceinline__ uint64_t desc_kmajor_sw32(uint32_t smem_addr) {
+  uint64_t d = 0;
+  d |= uint64_t((smem_addr >> 4) & 0x3FFF);
+  d |= uint64_t(1) << 16;
+  d |= uint64_t(256 >> 4) << 32;
+  d |= uint64_t(1) << 46;
+  d |= uint64_t(6) << 61;
   return d;
 }
 // MN-major operand tile, 128-byte swizzle: 64 MN-contiguous bf16 per 128 B
