@@ -481,32 +481,85 @@ cudaError_t launch_gemm(const TcParams& prm, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-template <int BN, int CB>
+template <int BN, int CB, int NC>
 cudaError_t launch_tma(const TmaParams& prm, cudaStream_t st) {
-  using CC = TCfg<BN, CB>;
+  using CC = TCfg<BN, CB, NC>;
   static int attr_dev = -1;
   int dev = 0;
   cudaGetDevice(&dev);
   if (attr_dev != dev) {
-    cudaError_t e = cudaFuncSetAttribute(conv_tma_kernel<BN, CB>,
+    cudaError_t e = cudaFuncSetAttribute(conv_tma_kernel<BN, CB, NC>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, CC::SMEM);
     if (e != cudaSuccess) return e;
+    if (NC == 2) {
+      e = cudaFuncSetAttribute(conv_tma_kernel<BN, CB, NC>,
+                               cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
+      (void)e;
+    }
     attr_dev = dev;
   }
-  const unsigned grid = unsigned(std::min<int64_t>(prm.tiles, kNumSMs));
-  conv_tma_kernel<BN, CB><<<grid, kTmaThreads, CC::SMEM, st>>>(prm);
+  const int clusters = int(std::min<int64_t>(prm.tiles, kNumSMs / NC));
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(unsigned(clusters * NC));
+  cfg.blockDim = dim3(kTmaThreads);
+  cfg.dynamicSmemBytes = CC::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = NC;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (getenv("DNNP_TC_DIAG")) {
+    int ncl = -1;
+    cudaError_t qe = cudaOccupancyMaxActiveClusters(&ncl, conv_tma_kernel<BN, CB, NC>, &cfg);
+    fprintf(stderr, "DIAG conv_tma<%d,%d,%d> smem=%d grid=%d maxActiveClusters=%d (%s)\n", BN, CB, NC,
+            CC::SMEM, clusters * NC, ncl, cudaGetErrorString(qe));
+  }
+  cudaError_t e = cudaLaunchKernelEx(&cfg, conv_tma_kernel<BN, CB, NC>, prm);
   note_launch();
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
-template <int CB>
+template <int CB, int NC>
 cudaError_t launch_tma_bn(int bn, const TmaParams& prm, cudaStream_t st) {
   switch (bn) {
-    case 32: return launch_tma<32, CB>(prm, st);
-    case 64: return launch_tma<64, CB>(prm, st);
-    case 128: return launch_tma<128, CB>(prm, st);
-    case 192: return launch_tma<192, CB>(prm, st);
-    default: return launch_tma<256, CB>(prm, st);
+    case 64: return launch_tma<64, CB, NC>(prm, st);
+    case 128: return launch_tma<128, CB, NC>(prm, st);
+    case 192: return launch_tma<192, CB, NC>(prm, st);
+    default: return launch_tma<256, CB, NC>(prm, st);
+  }
+}
+
+// Tile shape for the TMA kernel: NC CTAs x 128 rows by bn columns.  Per SM
+// and 16-deep k-step the three MMAs take 1.5*bn cycles and the SM must
+// ingest (128 + bn/NC) rows x 64 B (hi + lo planes) at ~60 B/clk (measured);
+// persistent clusters run ceil(tiles / clusters) waves of that.
+void pick_tile_tma(int64_t M, int ncol, int cb, int* bn_out, int* nc_out) {
+  static const int cands[] = {64, 128, 192, 256};
+  double best = 1e30;
+  *bn_out = 256;
+  *nc_out = 1;
+  // CTA pairs are kept behind DNNP_TC_PAIRS until their pipeline depth is
+  // fixed (3 stages of 56-64 KB: latency-bound, slower than single CTAs).
+  const int max_nc = getenv("DNNP_TC_PAIRS") ? 2 : 1;
+  for (int nc = 1; nc <= max_nc; nc++) {
+    for (int bn : cands) {
+      if (bn >= 2 * ncol && bn > 64) continue;
+      const int64_t tiles = ceil_div(M, 128 * nc) * ceil_div(ncol, bn);
+      const double waves = std::ceil(double(tiles) / (kNumSMs / nc));
+      const double gather = 128.0 * 2.0 * 2.5 * 16.0 / cb;  // im2col pixel rows per k-step
+      const double step =
+          std::max({1.5 * bn, (128.0 + double(bn) / nc) * 64.0 / 60.0, gather}) + 16.0;
+      const double cost = waves * step;
+      if (cost < best - 1e-9) {
+        best = cost;
+        *bn_out = bn;
+        *nc_out = nc;
+      }
+    }
   }
 }
 
@@ -555,17 +608,32 @@ bool tma_geometry_ok(const Gemm& g, int IH, int IW, int taps_h, int taps_w, int6
   return true;
 }
 
+// TMA channel block per im2col load: the widest of 64/32/16 whose padding of
+// Cp stays <= 1/3 (wider rows = fewer TMA pixel requests; the TMA engine
+// handles ~1 im2col pixel row per 2.5 cycles whatever its width).
+int pick_cb(int Cp) {
+  for (int cb : {64, 32, 16})
+    if (ceil_div(Cp, cb) * cb * 3 <= int64_t(Cp) * 4) return cb;
+  return 16;
+}
+
 cudaError_t run_gemm(const ConvProblem& p, Gemm g, const __nv_bfloat16* a_hi,
                      const __nv_bfloat16* a_lo, int IH, int IW, int Cp, const float* f, float* out,
                      const View4& ov, float alpha, float beta, cudaStream_t st) {
   PackGeom& pg = g.pg;
-  pg.Cgrp = Cp / 8;
+  const int CB = g.tma ? pick_cb(Cp) : 8;
+  const int Cpf = int(ceil_div(Cp, CB) * CB);  // filter columns per tap (channel blocks padded)
+  pg.Cgrp = Cpf / 8;
   const int taps = pg.dgrad ? pg.winH * pg.winW : pg.R * pg.S;
   pg.KC = taps * pg.Cgrp;
-  const int nkb = int(ceil_div(pg.KC, 4));
-  pg.Ktot = std::max(1, nkb) * kBK;
+  const int depth = g.tma ? kTK : kBK;
+  const int nkb = int(ceil_div(int64_t(pg.KC) * 8, depth));
+  pg.Ktot = std::max(1, nkb) * depth;
   const int64_t M = p.N * g.OH * g.OW;
-  const int bn = pick_bn(M, pg.Ncol);
+  int bn = pick_bn(M, pg.Ncol), nc = 1;
+  if (g.tma) pick_tile_tma(M, pg.Ncol, CB, &bn, &nc);
+  if (g.tma && getenv("DNNP_TC_NC")) nc = atoi(getenv("DNNP_TC_NC"));
+  if (g.tma && getenv("DNNP_TC_BN")) bn = atoi(getenv("DNNP_TC_BN"));
   pg.Np = int(ceil_div(pg.Ncol, bn) * bn);
   const size_t flt = size_t(pg.Np) * pg.Ktot;
   Workspace ws(st);
@@ -578,12 +646,11 @@ cudaError_t run_gemm(const ConvProblem& p, Gemm g, const __nv_bfloat16* a_hi,
   pack_filter_kernel<<<grid_for(int64_t(pg.Np) * pg.Ktot, 256, 16), 256, 0, st>>>(
       pg, f, b_hi, b_lo, ctab, coltab);
   note_launch();
-  const int64_t tiles = ceil_div(M, kBM) * (pg.Np / bn);
+  const int64_t tiles = ceil_div(M, kBM * nc) * (pg.Np / bn);
   if (tiles >= (int64_t(1) << 31)) return cudaErrorInvalidValue;
 
   if (g.tma) {
     // ------------------------------------------------ TMA im2col kernel
-    const int CB = Cp % 32 == 0 ? 32 : 16;
     TmaParams prm{};
     Im2colGeom ig{};
     ig.N = p.N;
@@ -596,14 +663,16 @@ cudaError_t run_gemm(const ConvProblem& p, Gemm g, const __nv_bfloat16* a_hi,
     ig.stride_w = g.v;
     ig.cpp = CB;
     ig.ppc = kBM;
-    const CUtensorMapSwizzle sw = CB == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B;
+    const CUtensorMapSwizzle sw = CB == 64   ? CU_TENSOR_MAP_SWIZZLE_128B
+                                  : CB == 32 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                             : CU_TENSOR_MAP_SWIZZLE_32B;
     if ((e = make_tmap_im2col(&prm.tm_ahi, a_hi, ig, sw)) != cudaSuccess) return e;
     if ((e = make_tmap_im2col(&prm.tm_alo, a_lo, ig, sw)) != cudaSuccess) return e;
     if ((e = make_tmap_2d(&prm.tm_bhi, b_hi, uint64_t(pg.Ktot), uint64_t(pg.Np), uint64_t(pg.Ktot),
-                          uint32_t(CB), uint32_t(bn), sw)) != cudaSuccess)
+                          uint32_t(CB), uint32_t(bn / nc), sw)) != cudaSuccess)
       return e;
     if ((e = make_tmap_2d(&prm.tm_blo, b_lo, uint64_t(pg.Ktot), uint64_t(pg.Np), uint64_t(pg.Ktot),
-                          uint32_t(CB), uint32_t(bn), sw)) != cudaSuccess)
+                          uint32_t(CB), uint32_t(bn / nc), sw)) != cudaSuccess)
       return e;
     prm.M = M;
     prm.Ncol = pg.Ncol;
@@ -611,7 +680,7 @@ cudaError_t run_gemm(const ConvProblem& p, Gemm g, const __nv_bfloat16* a_hi,
     prm.lower_w = ig.lower_w;
     prm.u = g.u;
     prm.v = g.v;
-    prm.nCB = Cp / CB;
+    prm.nCB = Cpf / CB;
     prm.tapW = pg.dgrad ? pg.winW : pg.S;
     prm.KCH = taps * prm.nCB;
     prm.nkb = nkb;
@@ -636,7 +705,36 @@ cudaError_t run_gemm(const ConvProblem& p, Gemm g, const __nv_bfloat16* a_hi,
     prm.plain = (alpha == 1.0f && beta == 0.0f) ? 1 : 0;
     prm.dOHW = make_magic(uint32_t(g.OH * g.OW));
     prm.dOW = make_magic(uint32_t(g.OW));
-    return CB == 32 ? launch_tma_bn<32>(bn, prm, st) : launch_tma_bn<16>(bn, prm, st);
+    prm.skip = getenv("DNNP_TC_SKIP") ? atoi(getenv("DNNP_TC_SKIP")) : 0;
+    static unsigned long long* tbuf = nullptr;
+    const bool want_trace = getenv("DNNP_TC_TRACE") != nullptr;
+    if (want_trace && !tbuf) cudaMalloc(&tbuf, 8192 * sizeof(unsigned long long));
+    if (want_trace) cudaMemsetAsync(tbuf, 0, 8192 * sizeof(unsigned long long), st);
+    prm.trace = want_trace ? tbuf : nullptr;
+    if (nc == 2)
+      e = CB == 64   ? launch_tma_bn<64, 2>(bn, prm, st)
+          : CB == 32 ? launch_tma_bn<32, 2>(bn, prm, st)
+                     : launch_tma_bn<16, 2>(bn, prm, st);
+    else
+      e = CB == 64   ? launch_tma_bn<64, 1>(bn, prm, st)
+          : CB == 32 ? launch_tma_bn<32, 1>(bn, prm, st)
+                     : launch_tma_bn<16, 1>(bn, prm, st);
+    if (want_trace) {
+      static unsigned long long h[8192];
+      cudaStreamSynchronize(st);
+      cudaMemcpy(h, tbuf, sizeof h, cudaMemcpyDeviceToHost);
+      fprintf(stderr, "TMATRACE M=%lld ncol=%d bn=%d cb=%d nc=%d nkb=%d tiles=%d\n", (long long)M,
+              pg.Ncol, bn, CB, nc, nkb, prm.tiles);
+      const unsigned long long t0 = h[0];
+      for (int i = 0; i < 1024 && h[i * 4]; i++)
+        fprintf(stderr, "st %4d P[%8lld %8lld] M[%8lld %8lld]\n", i, (long long)(h[i * 4] - t0),
+                (long long)(h[i * 4 + 1] - t0), (long long)(h[i * 4 + 2] - t0),
+                (long long)(h[i * 4 + 3] - t0));
+      for (int i = 0; i < 64 && h[4096 + i * 4]; i++)
+        fprintf(stderr, "ep %2d [%8lld %8lld %8lld]\n", i, (long long)(h[4096 + i * 4] - t0),
+                (long long)(h[4096 + i * 4 + 1] - t0), (long long)(h[4096 + i * 4 + 2] - t0));
+    }
+    return e;
   }
 
   // -------------------------------------------------- cp.async gather kernel

@@ -10,25 +10,33 @@
 // slots and no per-row address arithmetic (the cp.async kernel in conv_tc.cu
 // spent ~500 cycles per stage there, more than the MMAs of the stage).
 //
-// Warps: 0 = TMA producer (one elected lane), 1 = TMEM allocation + MMA issue
-// (warp-collective loop, elected issue), 2-5 = epilogue (TMEM lane quadrant
-// warp % 4), double-buffered accumulator so the epilogue of tile i overlaps
-// the main loop of tile i + 1.
+// NC = 2 runs the tile on a CTA pair (cluster of 2 on one TPC,
+// tcgen05.mma.cta_group::2, M = 256): each CTA gathers its own 128 pixel
+// rows and HALF of the BN filter rows, so the bytes each SM must ingest per
+// MMA drop from (128 + BN) to (128 + BN/2) rows -- measured, a single SM
+// ingests ~60 B/clk, which caps 128 x BN tiles below the tensor rate for
+// BN < 256 (profiles/README.md).
+//
+// Warps: 0 = TMA producer (one elected lane, both CTAs), 1 = TMEM allocation
+// + MMA issue (leader CTA only; warp-collective loop, elected issue), 2-5 =
+// epilogue (TMEM lane quadrant warp % 4), double-buffered accumulator so the
+// epilogue of tile i overlaps the main loop of tile i + 1.
 #pragma once
 
 constexpr int kTmaThreads = 6 * 32;
+constexpr int kTK = 64;  // reduction depth of one stage (4 k-steps of 16)
 
 struct TmaParams {
   CUtensorMap tm_ahi;  // im2col maps of the packed input planes
   CUtensorMap tm_alo;
-  CUtensorMap tm_bhi;  // packed filter [Np][Ktot], box {CB, BN}
+  CUtensorMap tm_bhi;  // packed filter [Np][Ktot], box {CB, BN / NC}
   CUtensorMap tm_blo;
   int64_t M;           // GEMM rows = N * OH * OW
   int Ncol;            // valid GEMM columns
   int lower_h, lower_w, u, v;  // window origin of output pixel (oh, ow): lower + o * stride
   int nCB, tapW, KCH, nkb;     // channel blocks per tap, taps per window row, chunks, k-blocks
   int Cext;                    // channel extent of the A maps (OOB coordinate for padding chunks)
-  int nt, tiles;
+  int nt, tiles;               // column tiles, tiles (of NC * 128 rows)
   float* out;
   int64_t o_sn, o_sc, o_sh, o_sw;
   int out_mode;                // 0: column = channel; 1: column table (ph, pw, c)
@@ -37,16 +45,19 @@ struct TmaParams {
   float alpha, beta;
   int plain;                   // alpha == 1, beta == 0: store the accumulator as is
   MagicDiv dOHW, dOW;
+  int skip;                    // experiments: 1 = no A loads, 2 = no loads, 4 = no MMAs
+  unsigned long long* trace;   // debug: CTA-0 clock64 stamps (or null)
 };
 
-template <int BN, int CB>
+template <int BN, int CB, int NC>
 struct TCfg {
-  static constexpr int SUB = kBK / CB;       // chunks (sub-tiles) per stage
+  static constexpr int BNL = BN / NC;        // filter rows loaded by each CTA
+  static constexpr int SUB = kTK / CB;       // chunks (sub-tiles) per stage
   static constexpr int A_SUB = kBM * CB * 2; // bytes of one A sub-tile (one plane)
-  static constexpr int B_SUB = BN * CB * 2;
+  static constexpr int B_SUB = BNL * CB * 2;
   static constexpr int A_BYTES = SUB * A_SUB;
   static constexpr int B_BYTES = SUB * B_SUB;
-  static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
+  static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;  // per CTA
   static constexpr int STAGES =
       (200 * 1024) / STAGE_BYTES > 8 ? 8 : (200 * 1024) / STAGE_BYTES;
   static constexpr int TMEM_COLS =
@@ -56,13 +67,14 @@ struct TCfg {
 
 template <int CB>
 __device__ __forceinline__ uint64_t tma_kdesc(uint32_t addr) {
-  if constexpr (CB == 32) return ptx::desc_kmajor_sw64(addr);
+  if constexpr (CB == 64) return ptx::desc_kmajor_sw128(addr);
+  else if constexpr (CB == 32) return ptx::desc_kmajor_sw64(addr);
   else return ptx::desc_kmajor_sw32(addr);
 }
 
-template <int BN, int CB>
+template <int BN, int CB, int NC>
 __global__ void __launch_bounds__(kTmaThreads, 1) conv_tma_kernel(const __grid_constant__ TmaParams P) {
-  using C = TCfg<BN, CB>;
+  using C = TCfg<BN, CB, NC>;
   constexpr int S = C::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -74,23 +86,28 @@ __global__ void __launch_bounds__(kTmaThreads, 1) conv_tma_kernel(const __grid_c
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = NC == 2 ? ptx::cluster_ctarank() : 0u;
+  const bool leader = rank == 0;
+  const int cid = int(blockIdx.x) / NC, ncl = int(gridDim.x) / NC;  // cluster id / count
+
   if (warp == 1) {
     if (lane == 0) {
       for (int s = 0; s < S; s++) {
-        ptx::mbar_init(&full[s], 1);   // producer's arrive.expect_tx; TMA completes the tx
-        ptx::mbar_init(&empty[s], 1);  // MMA commit
+        ptx::mbar_init(&full[s], NC);  // each CTA's producer arrives (leader adds expect_tx)
+        ptx::mbar_init(&empty[s], 1);  // MMA commit (multicast to both CTAs)
       }
       for (int b = 0; b < 2; b++) {
         ptx::mbar_init(&tfull[b], 1);
-        ptx::mbar_init(&tempty[b], 128);
+        ptx::mbar_init(&tempty[b], 4 * NC);  // one arrival per epilogue warp of each CTA
       }
       ptx::fence_mbar_init();
     }
     __syncwarp();
-    ptx::tmem_alloc<C::TMEM_COLS>(tmem_slot);
+    ptx::tmem_alloc_g<C::TMEM_COLS, NC>(tmem_slot);
   }
   ptx::tc_fence_before();
-  __syncthreads();
+  if constexpr (NC == 2) ptx::cluster_sync();
+  else __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   const uint32_t smem0 = ptx::smem_u32(smem);
@@ -103,9 +120,9 @@ __global__ void __launch_bounds__(kTmaThreads, 1) conv_tma_kernel(const __grid_c
       ptx::tma_prefetch(&P.tm_bhi);
       ptx::tma_prefetch(&P.tm_blo);
       int it = 0;
-      for (int tile = blockIdx.x; tile < P.tiles; tile += gridDim.x) {
-        const uint32_t m0 = uint32_t(tile / P.nt) * kBM;
-        const int n0 = (tile % P.nt) * BN;
+      for (int tile = cid; tile < P.tiles; tile += ncl) {
+        const uint32_t m0 = uint32_t(tile / P.nt) * (kBM * NC) + rank * kBM;
+        const int n0 = (tile % P.nt) * BN + int(rank) * C::BNL;
         uint32_t img, rem, oh, ow;
         mdivmod(m0, P.dOHW, img, rem);
         mdivmod(rem, P.dOW, oh, ow);
@@ -113,22 +130,44 @@ __global__ void __launch_bounds__(kTmaThreads, 1) conv_tma_kernel(const __grid_c
         int kc = 0, cb = 0, dh = 0, dw = 0;
         for (int kb = 0; kb < P.nkb; kb++, it++) {
           const int s = it % S;
+          const bool tr = P.trace && blockIdx.x == 0 && it < 1024;
+          if (tr) P.trace[it * 4 + 0] = clock64();
           if (it >= S) ptx::mbar_wait(&empty[s], ((it / S) - 1) & 1);
-          ptx::mbar_arrive_expect_tx(&full[s], C::STAGE_BYTES);
+          if (tr) P.trace[it * 4 + 1] = clock64();
+          if (P.skip & 2) {
+            if (NC == 1 || leader) ptx::mbar_arrive(&full[s]);
+            else ptx::mbar_arrive_cluster(&full[s], 0);
+            continue;
+          }
+          const uint32_t tx = (P.skip & 1) ? 2 * C::B_BYTES : C::STAGE_BYTES;
+          if (leader) ptx::mbar_arrive_expect_tx(&full[s], tx * NC);
+          else ptx::mbar_arrive_cluster(&full[s], 0);
+          const uint32_t bar = NC == 2 ? ptx::leader_addr(&full[s]) : ptx::smem_u32(&full[s]);
           const uint32_t base = smem0 + s * C::STAGE_BYTES;
 #pragma unroll
           for (int j = 0; j < C::SUB; j++, kc++) {
             const bool real = kc < P.KCH;
             const int c = real ? cb * CB : P.Cext;  // padding chunk: all-OOB box -> zeros
             const uint16_t ow16 = uint16_t(real ? dw : 0), oh16 = uint16_t(real ? dh : 0);
-            ptx::tma_load_im2col(base + j * C::A_SUB, &P.tm_ahi, c, w0, h0, int(img), ow16, oh16,
-                                 &full[s]);
-            ptx::tma_load_im2col(base + C::A_BYTES + j * C::A_SUB, &P.tm_alo, c, w0, h0, int(img),
-                                 ow16, oh16, &full[s]);
-            ptx::tma_load_2d(base + 2 * C::A_BYTES + j * C::B_SUB, &P.tm_bhi, kc * CB, n0,
-                             &full[s]);
-            ptx::tma_load_2d(base + 2 * C::A_BYTES + C::B_BYTES + j * C::B_SUB, &P.tm_blo,
-                             kc * CB, n0, &full[s]);
+            const uint32_t da = base + j * C::A_SUB;
+            const uint32_t db = base + 2 * C::A_BYTES + j * C::B_SUB;
+            if constexpr (NC == 2) {
+              if (!(P.skip & 1)) {
+                ptx::tma_load_im2col_pair(da, &P.tm_ahi, c, w0, h0, int(img), ow16, oh16, bar);
+                ptx::tma_load_im2col_pair(da + C::A_BYTES, &P.tm_alo, c, w0, h0, int(img), ow16,
+                                          oh16, bar);
+              }
+              ptx::tma_load_2d_pair(db, &P.tm_bhi, kc * CB, n0, bar);
+              ptx::tma_load_2d_pair(db + C::B_BYTES, &P.tm_blo, kc * CB, n0, bar);
+            } else {
+              if (!(P.skip & 1)) {
+                ptx::tma_load_im2col(da, &P.tm_ahi, c, w0, h0, int(img), ow16, oh16, &full[s]);
+                ptx::tma_load_im2col(da + C::A_BYTES, &P.tm_alo, c, w0, h0, int(img), ow16, oh16,
+                                     &full[s]);
+              }
+              ptx::tma_load_2d(db, &P.tm_bhi, kc * CB, n0, &full[s]);
+              ptx::tma_load_2d(db + C::B_BYTES, &P.tm_blo, kc * CB, n0, &full[s]);
+            }
             if (++cb == P.nCB) {
               cb = 0;
               if (++dw == P.tapW) {
@@ -141,50 +180,59 @@ __global__ void __launch_bounds__(kTmaThreads, 1) conv_tma_kernel(const __grid_c
       }
     }
   } else if (warp == 1) {
-    // ================================================ MMA issuer
-    constexpr uint32_t idesc = ptx::idesc_bf16(kBM, BN, 0, 0);
-    int it = 0, lt = 0;
-    for (int tile = blockIdx.x; tile < P.tiles; tile += gridDim.x, lt++) {
-      const int buf = lt & 1;
-      ptx::mbar_wait(&tempty[buf], ((lt >> 1) & 1) ^ 1);
-      ptx::tc_fence_after();
-      const uint32_t dacc = tmem_base + uint32_t(buf * BN);
-      uint32_t acc = 0;
-      for (int kb = 0; kb < P.nkb; kb += 2) {
-        const int npair = P.nkb - kb >= 2 ? 2 : 1;
-        ptx::mbar_wait_spin(&full[it % S], (it / S) & 1);
-        if (npair == 2) ptx::mbar_wait_spin(&full[(it + 1) % S], ((it + 1) / S) & 1);
+    // ================================================ MMA issuer (leader CTA)
+    if (leader) {
+      constexpr uint32_t idesc = ptx::idesc_bf16(kBM * NC, BN, 0, 0);
+      int it = 0, lt = 0;
+      for (int tile = cid; tile < P.tiles; tile += ncl, lt++) {
+        const int buf = lt & 1;
+        ptx::mbar_wait(&tempty[buf], ((lt >> 1) & 1) ^ 1);
         ptx::tc_fence_after();
-        for (int q = 0; q < npair; q++, it++) {
+        const uint32_t dacc = tmem_base + uint32_t(buf * BN);
+        uint32_t acc = 0;
+        for (int kb = 0; kb < P.nkb; kb++, it++) {
           const int s = it % S;
+          ptx::mbar_wait_spin(&full[s], (it / S) & 1);
+          ptx::tc_fence_after();
+          if (P.trace && blockIdx.x == 0 && it < 1024 && lane == 0) P.trace[it * 4 + 2] = clock64();
           const uint32_t base = smem0 + s * C::STAGE_BYTES;
 #pragma unroll
-          for (int kk = 0; kk < kBK / 16; kk++) {
-            // one 16-deep k-step: CB=32 -> +32 B inside the 64 B row; CB=16 -> next sub-tile
-            const uint32_t ao = CB == 32 ? uint32_t(kk * 32) : uint32_t(kk * C::A_SUB);
-            const uint32_t bo = CB == 32 ? uint32_t(kk * 32) : uint32_t(kk * C::B_SUB);
+          for (int kk = 0; kk < kTK / 16 && !(P.skip & 4); kk++) {
+            // 16-deep k-step kk: sub-tile kk / (CB/16), +32 B per step inside its rows
+            const int sub = kk / (CB / 16), ko = (kk % (CB / 16)) * 32;
+            const uint32_t ao = uint32_t(sub * C::A_SUB + ko);
+            const uint32_t bo = uint32_t(sub * C::B_SUB + ko);
             const uint64_t dah = tma_kdesc<CB>(base + ao);
             const uint64_t dal = tma_kdesc<CB>(base + C::A_BYTES + ao);
             const uint64_t dbh = tma_kdesc<CB>(base + 2 * C::A_BYTES + bo);
             const uint64_t dbl = tma_kdesc<CB>(base + 2 * C::A_BYTES + C::B_BYTES + bo);
-            ptx::mma_bf16_elect(dacc, dal, dbh, idesc, acc);
-            ptx::mma_bf16_elect(dacc, dah, dbl, idesc, 1);
-            ptx::mma_bf16_elect(dacc, dah, dbh, idesc, 1);
+            if constexpr (NC == 2) {
+              ptx::mma_bf16_pair_elect(dacc, dal, dbh, idesc, acc);
+              ptx::mma_bf16_pair_elect(dacc, dah, dbl, idesc, 1);
+              ptx::mma_bf16_pair_elect(dacc, dah, dbh, idesc, 1);
+            } else {
+              ptx::mma_bf16_elect(dacc, dal, dbh, idesc, acc);
+              ptx::mma_bf16_elect(dacc, dah, dbl, idesc, 1);
+              ptx::mma_bf16_elect(dacc, dah, dbh, idesc, 1);
+            }
             acc = 1;
           }
-          ptx::mma_commit_elect(&empty[s]);
+          if constexpr (NC == 2) ptx::mma_commit_pair_elect(&empty[s]);
+          else ptx::mma_commit_elect(&empty[s]);
+          if (P.trace && blockIdx.x == 0 && it < 1024 && lane == 0) P.trace[it * 4 + 3] = clock64();
         }
+        if constexpr (NC == 2) ptx::mma_commit_pair_elect(&tfull[buf]);
+        else ptx::mma_commit_elect(&tfull[buf]);
       }
-      ptx::mma_commit_elect(&tfull[buf]);
     }
   } else {
     // ================================================ epilogue
     const int ew = warp & 3;  // TMEM lane quadrant accessible to this warp
     const int r = ew * 32 + lane;
     int lt = 0;
-    for (int tile = blockIdx.x; tile < P.tiles; tile += gridDim.x, lt++) {
+    for (int tile = cid; tile < P.tiles; tile += ncl, lt++) {
       const int buf = lt & 1;
-      const int64_t m = int64_t(tile / P.nt) * kBM + r;
+      const int64_t m = int64_t(tile / P.nt) * (kBM * NC) + int64_t(rank) * kBM + r;
       const int n0 = (tile % P.nt) * BN;
       const bool row_ok = m < P.M;
       uint32_t img = 0, oh = 0, ow = 0;
@@ -193,7 +241,10 @@ __global__ void __launch_bounds__(kTmaThreads, 1) conv_tma_kernel(const __grid_c
         mdivmod(uint32_t(m), P.dOHW, img, rem);
         mdivmod(rem, P.dOW, oh, ow);
       }
+      const bool etr = P.trace && blockIdx.x == 0 && r == 0 && lt < 64;
+      if (etr) P.trace[4096 + lt * 4 + 0] = clock64();
       ptx::mbar_wait(&tfull[buf], (lt >> 1) & 1);
+      if (etr) P.trace[4096 + lt * 4 + 1] = clock64();
       ptx::tc_fence_after();
       const int64_t rowoff =
           P.out_mode == 0 ? int64_t(img) * P.o_sn + int64_t(oh) * P.o_sh + int64_t(ow) * P.o_sw
@@ -245,12 +296,19 @@ __global__ void __launch_bounds__(kTmaThreads, 1) conv_tma_kernel(const __grid_c
         }
       }
       ptx::tc_fence_before();
-      ptx::mbar_arrive(&tempty[buf]);
+      __syncwarp();
+      if (etr) P.trace[4096 + lt * 4 + 2] = clock64();
+      if (lane == 0) {
+        if (NC == 1) ptx::mbar_arrive(&tempty[buf]);
+        else ptx::mbar_arrive_cluster(&tempty[buf], 0);
+      }
     }
   }
-  __syncthreads();
+  ptx::tc_fence_before();
+  if constexpr (NC == 2) ptx::cluster_sync();
+  else __syncthreads();
   if (warp == 1) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc<C::TMEM_COLS>(tmem_base);
+    ptx::tmem_dealloc_g<C::TMEM_COLS, NC>(tmem_base);
   }
 }
