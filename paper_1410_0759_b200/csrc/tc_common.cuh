@@ -35,6 +35,12 @@ cudaError_t make_tmap_2d(CUtensorMap* map, const void* base, uint64_t cols, uint
                          uint64_t pitch_elems, uint32_t box_cols, uint32_t box_rows,
                          CUtensorMapSwizzle swizzle);
 
+// 3-D bf16 tiled tensor map (dims innermost first, byte strides of dims 1, 2;
+// strides need not be monotonic, e.g. {channel, pixel, channel block}).
+cudaError_t make_tmap_3d(CUtensorMap* map, const void* base, const uint64_t dims[3],
+                         const uint64_t strides_bytes[2], const uint32_t box[3],
+                         CUtensorMapSwizzle swizzle);
+
 // 4-D im2col tensor map over a packed [N][H][W][C] bf16 plane: `ppc` output
 // pixels per load, `cpp` channels per pixel, bounding box corners (W, H) in
 // [-128, 127], traversal strides <= 8.  Verified on B200 by

@@ -11,6 +11,8 @@
 // its partial tile to a workspace; wgrad_reduce sums the splits in fixed order
 // and scatters into the KCRS filter (deterministic; accumulate adds last).
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 
 #include "tc_common.cuh"
 #include "tc_ptx.cuh"
@@ -287,12 +289,438 @@ cudaError_t launch_wgrad(const WgParams& prm, int mt, int nt, int splits, cudaSt
 }
 
 }  // namespace
+// ===========================================================================
+// TMA im2col backward-filter.
+//
+// GEMM: D[col][k] = sum over output pixels g of x_im2col[g][col] * dy[g][k],
+// rows = the forward reduction columns col = tap * Cpf + c (x operand, A),
+// columns = output channels k (dy operand, B), reduction = pixels.  Both
+// operands are MN-major 128B-swizzled tiles of 64-wide blocks x kWPx pixels:
+//   x  block = one im2col TMA load (kWPx pixels x 64 channels of one tap,
+//              zero fill at the border / past the last image),
+//   dy blocks = ONE 3-D tiled TMA load per plane over the view
+//              {64 channels, pixels, channel block} (block-major in smem).
+// TMA costs ~190-270 cycles per instruction whatever the box size
+// (profiles/r01/tma_rate_probe_v2_depth.txt), so stages are 64 pixels deep
+// and dy needs one instruction per plane.  NC = 2 runs the tile on a CTA
+// pair (M = 256 rows, each CTA loads half of the BN dy channels).
+// Split-K over pixels (multiples of kWPx: only the last stage of the last
+// split runs past NPQ, where both loads zero-fill); each split writes an fp32
+// partial tile, wgrad_reduce_tma sums splits in fixed order and scatters into
+// KCRS (deterministic).
+// ===========================================================================
+namespace {
+
+constexpr int kWgThreads = 6 * 32;  // warp 0 TMA, warp 1 MMA + TMEM, warps 2-5 epilogue
+constexpr int kWPx = 64;            // pixels (reduction depth) per stage
+
+struct WgTmaParams {
+  CUtensorMap tm_xhi;   // im2col maps of the packed x planes, 64 channels x kWPx pixels
+  CUtensorMap tm_xlo;
+  CUtensorMap tm_dyhi;  // packed dy as {64, NPQ, Kp/64}, box {64, kWPx, BN/NC/64}
+  CUtensorMap tm_dylo;
+  int64_t pix_per_split, NPQ;
+  int lower_h, lower_w, u, v;  // window origin of output pixel (p, q): lower + o * stride
+  int nCB, tapW, taps, Cext;   // x column blocks per tap, taps per window row, taps, OOB channel
+  int mrows_p, ncol_p;         // workspace tile pitch
+  float* ws;
+  MagicDiv dPQ, dQ;
+  unsigned long long* trace;
+};
+
+template <int BN, int NC>
+struct WgCfg {
+  static constexpr int BLK = kWPx * 128;       // one 64-wide MN block
+  static constexpr int B_BLKS = BN / NC / 64;  // dy blocks loaded by each CTA
+  static constexpr int A_BYTES = 2 * BLK;      // 128 x-columns
+  static constexpr int B_BYTES = B_BLKS * BLK;
+  static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
+  static constexpr int STAGES =
+      (225 * 1024 - 2048) / STAGE_BYTES > 8 ? 8 : (225 * 1024 - 2048) / STAGE_BYTES;
+  static constexpr int TMEM_COLS = BN <= 64 ? 64 : (BN <= 128 ? 128 : 256);
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+};
+
+template <int BN, int NC>
+__global__ void __launch_bounds__(kWgThreads, 1) wgrad_tma_kernel(const __grid_constant__ WgTmaParams P) {
+  using C = WgCfg<BN, NC>;
+  constexpr int S = C::STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * C::STAGE_BYTES);
+  uint64_t* empty = full + S;
+  uint64_t* tmem_full = empty + S;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = NC == 2 ? ptx::cluster_ctarank() : 0u;
+  const bool leader = rank == 0;
+  const int m0 = (blockIdx.x / NC) * (128 * NC) + int(rank) * 128;  // this CTA's x columns
+  const int n0 = blockIdx.y * BN;
+  const int64_t pbeg = int64_t(blockIdx.z) * P.pix_per_split;
+  const int64_t pend = min(P.NPQ, pbeg + P.pix_per_split);
+  const int nkb = pend > pbeg ? int((pend - pbeg + kWPx - 1) / kWPx) : 0;
+
+  if (warp == 1) {
+    if (lane == 0) {
+      for (int s = 0; s < S; s++) {
+        ptx::mbar_init(&full[s], NC);
+        ptx::mbar_init(&empty[s], 1);
+      }
+      ptx::mbar_init(tmem_full, 1);
+      ptx::fence_mbar_init();
+    }
+    __syncwarp();
+    ptx::tmem_alloc_g<C::TMEM_COLS, NC>(tmem_slot);
+  }
+  ptx::tc_fence_before();
+  if constexpr (NC == 2) ptx::cluster_sync();
+  else __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem_d = *tmem_slot;
+  const uint32_t smem0 = ptx::smem_u32(smem);
+
+  if (warp == 0) {
+    if (lane == 0) {
+      ptx::tma_prefetch(&P.tm_xhi);
+      ptx::tma_prefetch(&P.tm_xlo);
+      ptx::tma_prefetch(&P.tm_dyhi);
+      ptx::tma_prefetch(&P.tm_dylo);
+      const int dyblk0 = (n0 + int(rank) * (BN / NC)) / 64;  // this CTA's first dy channel block
+      for (int kb = 0; kb < nkb; kb++) {
+        const int s = kb % S;
+        const bool tr = P.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && kb < 1024;
+        if (tr) P.trace[kb * 4 + 0] = clock64();
+        if (kb >= S) ptx::mbar_wait(&empty[s], ((kb / S) - 1) & 1);
+        if (tr) P.trace[kb * 4 + 1] = clock64();
+        if (leader) ptx::mbar_arrive_expect_tx(&full[s], C::STAGE_BYTES * NC);
+        else ptx::mbar_arrive_cluster(&full[s], 0);
+        const uint32_t bar = NC == 2 ? ptx::leader_addr(&full[s]) : ptx::smem_u32(&full[s]);
+        const int64_t g = pbeg + int64_t(kb) * kWPx;
+        uint32_t img, rem, pp, qq;
+        mdivmod(uint32_t(g), P.dPQ, img, rem);
+        mdivmod(rem, P.dQ, pp, qq);
+        const int h0 = P.lower_h + int(pp) * P.u, w0 = P.lower_w + int(qq) * P.v;
+        const uint32_t base = smem0 + s * C::STAGE_BYTES;
+#pragma unroll
+        for (int j = 0; j < 2; j++) {
+          const int blk = m0 / 64 + j;
+          const int tap = blk / P.nCB, cb = blk - tap * P.nCB;
+          const bool real = tap < P.taps;
+          const int c = real ? cb * 64 : P.Cext;
+          const uint16_t dh = uint16_t(real ? tap / P.tapW : 0), dw = uint16_t(real ? tap % P.tapW : 0);
+          const uint32_t dst = base + j * C::BLK;
+          if constexpr (NC == 2) {
+            ptx::tma_load_im2col_pair(dst, &P.tm_xhi, c, w0, h0, int(img), dw, dh, bar);
+            ptx::tma_load_im2col_pair(dst + C::A_BYTES, &P.tm_xlo, c, w0, h0, int(img), dw, dh, bar);
+          } else {
+            ptx::tma_load_im2col(dst, &P.tm_xhi, c, w0, h0, int(img), dw, dh, &full[s]);
+            ptx::tma_load_im2col(dst + C::A_BYTES, &P.tm_xlo, c, w0, h0, int(img), dw, dh, &full[s]);
+          }
+        }
+        const uint32_t db = base + 2 * C::A_BYTES;
+        if constexpr (NC == 2) {
+          ptx::tma_load_3d_pair(db, &P.tm_dyhi, 0, int(g), dyblk0, bar);
+          ptx::tma_load_3d_pair(db + C::B_BYTES, &P.tm_dylo, 0, int(g), dyblk0, bar);
+        } else {
+          ptx::tma_load_3d(db, &P.tm_dyhi, 0, int(g), dyblk0, &full[s]);
+          ptx::tma_load_3d(db + C::B_BYTES, &P.tm_dylo, 0, int(g), dyblk0, &full[s]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader) {
+      constexpr uint32_t idesc = ptx::idesc_bf16(128 * NC, BN, 1, 1);
+      uint32_t acc = 0;
+      for (int kb = 0; kb < nkb; kb++) {
+        const int s = kb % S;
+        ptx::mbar_wait_spin(&full[s], (kb / S) & 1);
+        ptx::tc_fence_after();
+        if (P.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && kb < 1024 && lane == 0)
+          P.trace[kb * 4 + 2] = clock64();
+        const uint32_t sa = smem0 + s * C::STAGE_BYTES;
+        const uint64_t dah = ptx::desc_mnmajor_sw128(sa, C::BLK, 1024);
+        const uint64_t dal = ptx::desc_mnmajor_sw128(sa + C::A_BYTES, C::BLK, 1024);
+        const uint64_t dbh = ptx::desc_mnmajor_sw128(sa + 2 * C::A_BYTES, C::BLK, 1024);
+        const uint64_t dbl = ptx::desc_mnmajor_sw128(sa + 2 * C::A_BYTES + C::B_BYTES, C::BLK, 1024);
+#pragma unroll
+        for (int kk = 0; kk < kWPx / 16; kk++) {
+          const uint64_t o = uint64_t(kk * 2048) >> 4;  // 16 pixels = 2 groups of 8 rows
+          if constexpr (NC == 2) {
+            ptx::mma_bf16_pair_elect(tmem_d, dal + o, dbh + o, idesc, acc);
+            ptx::mma_bf16_pair_elect(tmem_d, dah + o, dbl + o, idesc, 1);
+            ptx::mma_bf16_pair_elect(tmem_d, dah + o, dbh + o, idesc, 1);
+          } else {
+            ptx::mma_bf16_elect(tmem_d, dal + o, dbh + o, idesc, acc);
+            ptx::mma_bf16_elect(tmem_d, dah + o, dbl + o, idesc, 1);
+            ptx::mma_bf16_elect(tmem_d, dah + o, dbh + o, idesc, 1);
+          }
+          acc = 1;
+        }
+        if constexpr (NC == 2) ptx::mma_commit_pair_elect(&empty[s]);
+        else ptx::mma_commit_elect(&empty[s]);
+      }
+      if constexpr (NC == 2) ptx::mma_commit_pair_elect(tmem_full);
+      else ptx::mma_commit_elect(tmem_full);
+    }
+  } else {
+    const int ew = warp & 3;
+    const int r = ew * 32 + lane;
+    ptx::mbar_wait(tmem_full, 0);
+    ptx::tc_fence_after();
+    float* dst = P.ws + (int64_t(blockIdx.z) * P.mrows_p + m0 + r) * P.ncol_p + n0;
+#pragma unroll 1
+    for (int c0 = 0; c0 < BN; c0 += 32) {
+      uint32_t v[32];
+      ptx::tmem_ld32(tmem_d + (uint32_t(ew * 32) << 16) + uint32_t(c0), v);
+      ptx::tmem_ld_wait();
+#pragma unroll
+      for (int i = 0; i < 32; i += 4) {
+        const float4 v4 =
+            nkb > 0 ? make_float4(__uint_as_float(v[i]), __uint_as_float(v[i + 1]),
+                                  __uint_as_float(v[i + 2]), __uint_as_float(v[i + 3]))
+                    : make_float4(0.f, 0.f, 0.f, 0.f);
+        *reinterpret_cast<float4*>(dst + c0 + i) = v4;
+      }
+    }
+  }
+  ptx::tc_fence_before();
+  if constexpr (NC == 2) ptx::cluster_sync();
+  else __syncthreads();
+  if (warp == 1) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc_g<C::TMEM_COLS, NC>(tmem_d);
+  }
+}
+
+// df[k][c][r][s] (+)= sum_z ws[z][col][k] for the x column col = tap * Cpf +
+// cg of filter element (c, r, s): tap = (r' / su, s' / sv) with r' the
+// gather offset of r (R-1-r in CONVOLUTION mode), cg = ((r' % su) * sv +
+// s' % sv) * C + c.
+struct WgReduceGeom {
+  int K, C, R, S, flip;
+  int su, sv, S2, Cpf;  // space-to-depth factors, taps per window row, columns per tap
+  int splits, mrows_p, ncol_p;
+};
+
+__global__ void __launch_bounds__(256) wgrad_reduce_tma(WgReduceGeom g, const float* __restrict__ ws,
+                                                        float* __restrict__ df, int accumulate) {
+  const int64_t total = int64_t(g.K) * g.C * g.R * g.S;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  const int64_t plane = int64_t(g.mrows_p) * g.ncol_p;
+  for (int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; idx < total; idx += stride) {
+    const int s = int(idx % g.S);
+    int64_t t = idx / g.S;
+    const int r = int(t % g.R);
+    t /= g.R;
+    const int c = int(t % g.C);
+    const int k = int(t / g.C);
+    const int ro = g.flip ? g.R - 1 - r : r, so = g.flip ? g.S - 1 - s : s;  // gather offsets
+    const int tap = (ro / g.su) * g.S2 + so / g.sv;
+    const int cg = ((ro % g.su) * g.sv + so % g.sv) * g.C + c;
+    const int col = tap * g.Cpf + cg;
+    const float* src = ws + int64_t(col) * g.ncol_p + k;
+    float acc = src[0];
+    for (int z = 1; z < g.splits; z++) acc = __fadd_rn(acc, src[z * plane]);
+    df[idx] = accumulate ? __fadd_rn(df[idx], acc) : acc;
+  }
+}
+
+template <int BN, int NC>
+cudaError_t launch_wgrad_tma(const WgTmaParams& prm, dim3 grid, cudaStream_t st) {
+  using CC = WgCfg<BN, NC>;
+  static int attr_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (attr_dev != dev) {
+    cudaError_t e = cudaFuncSetAttribute(wgrad_tma_kernel<BN, NC>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, CC::SMEM);
+    if (e != cudaSuccess) return e;
+    attr_dev = dev;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(kWgThreads);
+  cfg.dynamicSmemBytes = CC::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = NC;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, wgrad_tma_kernel<BN, NC>, prm);
+  note_launch();
+  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+// TMA path of backward-filter; returns cudaErrorNotSupported when the
+// geometry does not fit the im2col tensor map (caller falls back).
+cudaError_t wgrad_tma(const ConvProblem& p, const float* dy, const float* x, float* df, bool acc,
+                      cudaStream_t st) {
+  if (getenv("DNNP_TC_NO_TMA")) return cudaErrorNotSupported;
+  const bool s2d = !getenv("DNNP_TC_NO_S2D") && (p.u > 1 || p.v > 1) && p.u <= 8 && p.v <= 8 &&
+                   p.C * p.u * p.v <= 64;
+  const int su = s2d ? int(p.u) : 1, sv = s2d ? int(p.v) : 1;
+  const int R2 = int(ceil_div(p.R, su)), S2 = int(ceil_div(p.S, sv));
+  const int Cg = su * sv * int(p.C);                 // GEMM channels per tap
+  const int Cp = int(ceil_div(Cg, 16) * 16);         // packed x channels
+  const int nCB = int(ceil_div(Cp, 64)), Cpf = nCB * 64;
+  const int taps = R2 * S2;
+  const int ncolx = taps * Cpf;                      // x-operand extent (padded)
+  const int IH = s2d ? int(p.P) - 1 + R2 : int(p.H);
+  const int IW = s2d ? int(p.Q) - 1 + S2 : int(p.W);
+  const int gu = s2d ? 1 : int(p.u), gv = s2d ? 1 : int(p.v);
+  const int gph = s2d ? 0 : int(p.pad_h), gpw = s2d ? 0 : int(p.pad_w);
+  if (gu > 8 || gv > 8 || R2 > 128 || S2 > 128) return cudaErrorNotSupported;
+  const int lower_h = -gph, lower_w = -gpw;
+  const int upper_h = (int(p.P) - 1) * gu + 1 - gph - IH;
+  const int upper_w = (int(p.Q) - 1) * gv + 1 - gpw - IW;
+  for (int c : {lower_h, lower_w, upper_h, upper_w})
+    if (c < -128 || c > 127) return cudaErrorNotSupported;
+  const int64_t NPQ = p.N * p.P * p.Q;
+  if (NPQ >= (int64_t(1) << 31) || p.N * IH * IW >= (int64_t(1) << 31)) return cudaErrorNotSupported;
+
+  // tile: 128*nc x-columns by bn output channels; pairs when both halves of
+  // the dy columns are whole 64-channel blocks
+  const int Kp64 = int(ceil_div(p.K, 64) * 64);
+  int bn = Kp64 <= 256 ? Kp64 : (Kp64 % 256 == 0 ? 256 : (Kp64 % 192 == 0 ? 192 : 128));
+  if (getenv("DNNP_TC_BN")) bn = atoi(getenv("DNNP_TC_BN"));
+  int nc = (bn % 128 == 0) ? 2 : 1;
+  if (getenv("DNNP_TC_NC")) nc = atoi(getenv("DNNP_TC_NC"));
+  if (nc == 2 && bn % 128) nc = 1;
+  const int mrows = int(ceil_div(ncolx, 128 * nc) * 128 * nc);
+  const int ncols = int(ceil_div(Kp64, bn) * bn);
+  const int mt = mrows / (128 * nc), nt = ncols / bn;
+  const int64_t kblocks = ceil_div(NPQ, kWPx);
+  int64_t splits = std::max<int64_t>(1, int64_t(kNumSMs) / (int64_t(mt) * nt * nc));
+  splits = std::min<int64_t>({splits, std::max<int64_t>(1, kblocks / 4), 256});
+  const int64_t pps = ceil_div(kblocks, splits) * kWPx;
+  splits = ceil_div(NPQ, pps);
+
+  const size_t dy_elems = size_t(NPQ) * Kp64, x_elems = size_t(p.N) * IH * IW * Cp;
+  const size_t ws_floats = size_t(splits) * mrows * ncols;
+  Workspace wsp(st);
+  cudaError_t e = cudaMallocAsync(&wsp.p, (dy_elems + x_elems) * 4 + ws_floats * 4 + 512, st);
+  if (e != cudaSuccess) return e;
+  auto* dy_hi = static_cast<__nv_bfloat16*>(wsp.p);
+  auto* dy_lo = dy_hi + dy_elems;
+  auto* x_hi = dy_lo + dy_elems;
+  auto* x_lo = x_hi + x_elems;
+  float* part = reinterpret_cast<float*>(x_lo + x_elems);
+  if ((e = pack_act(p.y, dy, Kp64, dy_hi, dy_lo, st)) != cudaSuccess) return e;
+  if (s2d)
+    e = pack_act_s2d(p.x, x, su, sv, int(p.pad_h), int(p.pad_w), IH, IW, Cp, x_hi, x_lo, st);
+  else
+    e = pack_act(p.x, x, Cp, x_hi, x_lo, st);
+  if (e != cudaSuccess) return e;
+
+  WgTmaParams prm{};
+  Im2colGeom ig{};
+  ig.N = p.N;
+  ig.H = IH;
+  ig.W = IW;
+  ig.C = Cp;
+  ig.lower_h = lower_h;
+  ig.lower_w = lower_w;
+  ig.upper_h = upper_h;
+  ig.upper_w = upper_w;
+  ig.stride_h = gu;
+  ig.stride_w = gv;
+  ig.cpp = 64;
+  ig.ppc = kWPx;
+  if ((e = make_tmap_im2col(&prm.tm_xhi, x_hi, ig, CU_TENSOR_MAP_SWIZZLE_128B)) != cudaSuccess) return e;
+  if ((e = make_tmap_im2col(&prm.tm_xlo, x_lo, ig, CU_TENSOR_MAP_SWIZZLE_128B)) != cudaSuccess) return e;
+  {
+    const uint64_t dims[3] = {64, uint64_t(NPQ), uint64_t(Kp64 / 64)};
+    const uint64_t strides[2] = {uint64_t(Kp64) * 2, 128};
+    const uint32_t box[3] = {64, uint32_t(kWPx), uint32_t(bn / nc / 64)};
+    if ((e = make_tmap_3d(&prm.tm_dyhi, dy_hi, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B)) !=
+        cudaSuccess)
+      return e;
+    if ((e = make_tmap_3d(&prm.tm_dylo, dy_lo, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B)) !=
+        cudaSuccess)
+      return e;
+  }
+  prm.pix_per_split = pps;
+  prm.NPQ = NPQ;
+  prm.lower_h = lower_h;
+  prm.lower_w = lower_w;
+  prm.u = gu;
+  prm.v = gv;
+  prm.nCB = nCB;
+  prm.tapW = S2;
+  prm.taps = taps;
+  prm.Cext = Cp;
+  prm.mrows_p = mrows;
+  prm.ncol_p = ncols;
+  prm.ws = part;
+  prm.dPQ = make_magic(uint32_t(p.P * p.Q));
+  prm.dQ = make_magic(uint32_t(p.Q));
+  static unsigned long long* tbuf = nullptr;
+  const bool want_trace = getenv("DNNP_TC_TRACE") != nullptr;
+  if (want_trace && !tbuf) cudaMalloc(&tbuf, 8192 * sizeof(unsigned long long));
+  if (want_trace) cudaMemsetAsync(tbuf, 0, 8192 * sizeof(unsigned long long), st);
+  prm.trace = want_trace ? tbuf : nullptr;
+  const dim3 grid{unsigned(mt * nc), unsigned(nt), unsigned(splits)};
+  if (nc == 2) {
+    switch (bn) {
+      case 128: e = launch_wgrad_tma<128, 2>(prm, grid, st); break;
+      default: e = launch_wgrad_tma<256, 2>(prm, grid, st); break;
+    }
+  } else {
+    switch (bn) {
+      case 64: e = launch_wgrad_tma<64, 1>(prm, grid, st); break;
+      case 128: e = launch_wgrad_tma<128, 1>(prm, grid, st); break;
+      case 192: e = launch_wgrad_tma<192, 1>(prm, grid, st); break;
+      default: e = launch_wgrad_tma<256, 1>(prm, grid, st); break;
+    }
+  }
+  if (e != cudaSuccess) return e;
+  if (want_trace) {
+    static unsigned long long h[8192];
+    cudaStreamSynchronize(st);
+    cudaMemcpy(h, tbuf, sizeof h, cudaMemcpyDeviceToHost);
+    fprintf(stderr, "WGTRACE mt=%d nt=%d bn=%d nc=%d splits=%lld\n", mt, nt, bn, nc,
+            (long long)splits);
+    const unsigned long long t0 = h[0];
+    for (int i = 0; i < 1024 && h[i * 4]; i++)
+      fprintf(stderr, "st %4d P[%8lld %8lld] M[%8lld]\n", i, (long long)(h[i * 4] - t0),
+              (long long)(h[i * 4 + 1] - t0), (long long)(h[i * 4 + 2] - t0));
+  }
+  WgReduceGeom rg{};
+  rg.K = int(p.K);
+  rg.C = int(p.C);
+  rg.R = int(p.R);
+  rg.S = int(p.S);
+  rg.flip = p.flip ? 1 : 0;
+  rg.su = su;
+  rg.sv = sv;
+  rg.S2 = S2;
+  rg.Cpf = Cpf;
+  rg.splits = int(splits);
+  rg.mrows_p = mrows;
+  rg.ncol_p = ncols;
+  wgrad_reduce_tma<<<grid_for(int64_t(p.K) * p.C * p.R * p.S, 256, 16), 256, 0, st>>>(
+      rg, part, df, acc ? 1 : 0);
+  note_launch();
+  return cudaGetLastError();
+}
+
 }  // namespace tc
 
 cudaError_t tc_backward_filter(const ConvProblem& p, const float* dy, const float* x, float* df,
                                bool acc, cudaStream_t st) {
   using namespace tc;
   pool_keep_memory();
+  {
+    const cudaError_t te = wgrad_tma(p, dy, x, df, acc, st);
+    if (te != cudaErrorNotSupported) return te;
+  }
   const int Kp = int(ceil_div(p.K, 8) * 8), Cp = int(ceil_div(p.C, 8) * 8), Cgrp = Cp / 8;
   const int KC = int(p.R * p.S) * Cgrp;
   const int64_t NPQ = p.N * p.P * p.Q, NHW = p.N * p.H * p.W;
