@@ -281,6 +281,10 @@ def main():
             for key, (a, b) in evs.items():
                 op_ms[key].append(a.elapsed_time(b))
     launches = dp.kernel_launch_count() - launches0
+    if os.environ.get("DNNP_BENCH_DEBUG"):
+        for (li, pi), v in op_ms.items():
+            print(f"{layers[li]['name']}.{PASSES[pi]}: " + " ".join(f"{x:.3f}" for x in v),
+                  file=sys.stderr)
     total_ms = float(np.sum(step_ms))
     if ws > 1:
         t = torch.tensor([total_ms], device=device, dtype=torch.float64)

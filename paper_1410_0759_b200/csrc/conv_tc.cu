@@ -414,50 +414,54 @@ __device__ __forceinline__ int phase_tap(int ph, int dh, int lo, int u, int pad,
   return t0 + u * jr;  // gather offset r'
 }
 
+// One block row per GEMM column (filter row `row`), threads along the packed
+// reduction index k: coalesced 16-bit stores, 32-bit index math only.
 __global__ void __launch_bounds__(256) pack_filter_kernel(PackGeom g, const float* __restrict__ f,
                                                           __nv_bfloat16* __restrict__ hi,
                                                           __nv_bfloat16* __restrict__ lo,
                                                           uint32_t* __restrict__ ctab,
                                                           uint32_t* __restrict__ coltab) {
-  const int64_t total = int64_t(g.Np) * g.Ktot;
-  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-  for (int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
-       idx += stride) {
-    const int row = int(idx / g.Ktot), k = int(idx % g.Ktot);
+  const int row = blockIdx.y;
+  const int nS = g.dgrad ? g.winW : g.S;
+  int c_col = 0, ph = 0, pw = 0;
+  if (g.dgrad) {
+    const int phase = row / g.C;
+    c_col = row - phase * g.C;
+    ph = phase / g.v;
+    pw = phase - ph * g.v;
+  }
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < g.Ktot; k += gridDim.x * blockDim.x) {
     const int ch = k >> 3, i = k & 7;
     float val = 0.0f;
     if (ch < g.KC) {
-      const int tap = ch / g.Cgrp, grp = ch % g.Cgrp;
-      const int nS = g.dgrad ? g.winW : g.S;
-      const int dh = tap / nS, dw = tap % nS;
+      const int tap = ch / g.Cgrp, grp = ch - tap * g.Cgrp;
+      const int dh = tap / nS, dw = tap - dh * nS;
       const int cin = grp * 8 + i;
       if (row == 0 && i == 0)
         ctab[ch] = (uint32_t(dh) << 24) | (uint32_t(dw) << 16) | uint32_t(grp * 8);
       if (!g.dgrad) {
         if (row < g.K && cin < g.C) val = fetch_filter(g, f, row, cin, dh, dw);
       } else if (row < g.Ncol && cin < g.K) {
-        const int c = row % g.C, phase = row / g.C;
-        const int ph = phase / g.v, pw = phase % g.v;
         const int rp = phase_tap(ph, dh, g.lo_h, g.u, g.pad_h, g.R);
         const int sp = phase_tap(pw, dw, g.lo_w, g.v, g.pad_w, g.S);
-        if (rp >= 0 && sp >= 0) val = fetch_filter(g, f, cin, c, rp, sp);
+        if (rp >= 0 && sp >= 0) val = fetch_filter(g, f, cin, c_col, rp, sp);
       }
     }
     if (g.dgrad && k == 0 && row < g.Ncol) {
       uint32_t e;
       if (g.su * g.sv > 1) {  // space-to-depth column (rh, rw, c)
-        const int ph = row / g.C0, c = row - ph * g.C0;
-        e = (uint32_t(ph / g.sv) << 24) | (uint32_t(ph % g.sv) << 16) | uint32_t(c);
+        const int q = row / g.C0, c = row - q * g.C0;
+        e = (uint32_t(q / g.sv) << 24) | (uint32_t(q % g.sv) << 16) | uint32_t(c);
       } else {
-        const int c = row % g.C, phase = row / g.C;
-        e = (uint32_t(phase / g.v) << 24) | (uint32_t(phase % g.v) << 16) | uint32_t(c);
+        e = (uint32_t(ph) << 24) | (uint32_t(pw) << 16) | uint32_t(c_col);
       }
       coltab[row] = e;
     }
     __nv_bfloat16 h, l;
     split_bf16(val, h, l);
-    hi[idx] = h;
-    lo[idx] = l;
+    const int64_t o = int64_t(row) * g.Ktot + k;
+    hi[o] = h;
+    lo[o] = l;
   }
 }
 
@@ -534,25 +538,25 @@ cudaError_t launch_tma_bn(int bn, const TmaParams& prm, cudaStream_t st) {
 }
 
 // Tile shape for the TMA kernel: NC CTAs x 128 rows by bn columns.  Per SM
-// and 16-deep k-step the three MMAs take 1.5*bn cycles and the SM must
-// ingest (128 + bn/NC) rows x 64 B (hi + lo planes) at ~60 B/clk (measured);
-// persistent clusters run ceil(tiles / clusters) waves of that.
+// and 64-deep stage: the MMAs take 6*bn cycles; the SM ingests the A tile
+// (128 rows x 128 B x hi/lo = 32 KB) plus its share of B (bn/NC rows x
+// 256 B) at ~57 B/clk when every SM streams (profiles/r01/tma_burst_probe.txt);
+// the single producer issues (64/cb) * 4 TMA instructions at ~120 cycles.
+// Persistent clusters run ceil(tiles / clusters) waves of such tiles.
 void pick_tile_tma(int64_t M, int ncol, int cb, int* bn_out, int* nc_out) {
   static const int cands[] = {64, 128, 192, 256};
   double best = 1e30;
   *bn_out = 256;
   *nc_out = 1;
-  // CTA pairs are kept behind DNNP_TC_PAIRS until their pipeline depth is
-  // fixed (3 stages of 56-64 KB: latency-bound, slower than single CTAs).
-  const int max_nc = getenv("DNNP_TC_PAIRS") ? 2 : 1;
+  const int max_nc = getenv("DNNP_TC_NO_PAIRS") ? 1 : 2;
   for (int nc = 1; nc <= max_nc; nc++) {
     for (int bn : cands) {
       if (bn >= 2 * ncol && bn > 64) continue;
       const int64_t tiles = ceil_div(M, 128 * nc) * ceil_div(ncol, bn);
       const double waves = std::ceil(double(tiles) / (kNumSMs / nc));
-      const double gather = 128.0 * 2.0 * 2.5 * 16.0 / cb;  // im2col pixel rows per k-step
-      const double step =
-          std::max({1.5 * bn, (128.0 + double(bn) / nc) * 64.0 / 60.0, gather}) + 16.0;
+      const double bytes = 32768.0 + 256.0 * bn / nc;
+      const double issue = 4.0 * (64 / cb) * 120.0;
+      const double step = std::max({6.0 * bn, bytes / 57.0, issue}) + (nc == 2 ? 150.0 : 100.0);
       const double cost = waves * step;
       if (cost < best - 1e-9) {
         best = cost;
@@ -563,8 +567,8 @@ void pick_tile_tma(int64_t M, int ncol, int cb, int* bn_out, int* nc_out) {
   }
 }
 
-// Column tile: persistent CTAs stream tiles, so the cost model is the number
-// of tile waves times the per-tile column work (+ a fixed per-tile cost).
+// Column tile of the cp.async kernel: persistent CTAs stream tiles, so the
+// cost model is the number of tile waves times the per-tile column work.
 int pick_bn(int64_t M, int ncol) {
   static const int cands[] = {32, 64, 128, 192, 256};
   const int64_t mt = ceil_div(M, kBM);
@@ -637,14 +641,16 @@ cudaError_t run_gemm(const ConvProblem& p, Gemm g, const __nv_bfloat16* a_hi,
   pg.Np = int(ceil_div(pg.Ncol, bn) * bn);
   const size_t flt = size_t(pg.Np) * pg.Ktot;
   Workspace ws(st);
-  cudaError_t e = cudaMallocAsync(&ws.p, flt * 4 + size_t(pg.KC + pg.Np + 2) * 4 + 256, st);
+  cudaError_t e = ws.alloc(flt * 4 + size_t(pg.KC + pg.Np + 2) * 4 + 256);
   if (e != cudaSuccess) return e;
   auto* b_hi = static_cast<__nv_bfloat16*>(ws.p);
   auto* b_lo = b_hi + flt;
   auto* ctab = reinterpret_cast<uint32_t*>(b_lo + flt);
   auto* coltab = ctab + pg.KC + 1;
-  pack_filter_kernel<<<grid_for(int64_t(pg.Np) * pg.Ktot, 256, 16), 256, 0, st>>>(
-      pg, f, b_hi, b_lo, ctab, coltab);
+  {
+    const dim3 fgrid(unsigned(std::min<int64_t>(ceil_div(pg.Ktot, 256), 8)), unsigned(pg.Np));
+    pack_filter_kernel<<<fgrid, 256, 0, st>>>(pg, f, b_hi, b_lo, ctab, coltab);
+  }
   note_launch();
   const int64_t tiles = ceil_div(M, kBM * nc) * (pg.Np / bn);
   if (tiles >= (int64_t(1) << 31)) return cudaErrorInvalidValue;
@@ -943,7 +949,7 @@ cudaError_t run_tc(bool dgrad, const ConvProblem& p, const float* in, const View
   }
   const size_t act = size_t(p.N) * IH * IW * Cp;
   Workspace ws(st);
-  cudaError_t e = cudaMallocAsync(&ws.p, act * 4 + 256, st);
+  cudaError_t e = ws.alloc(act * 4 + 256);
   if (e != cudaSuccess) return e;
   auto* a_hi = static_cast<__nv_bfloat16*>(ws.p);
   auto* a_lo = a_hi + act;

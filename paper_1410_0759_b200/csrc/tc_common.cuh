@@ -14,17 +14,29 @@ __device__ __forceinline__ void split_bf16(float v, __nv_bfloat16& hi, __nv_bflo
   lo = __float2bfloat16_rn(v - __bfloat162float(hi));
 }
 
-// Stream-ordered scratch allocation released at scope exit (the pool keeps
-// the memory, so steady-state calls do not hit the driver).
+// Stream-ordered scratch memory.  Every op takes its scratch from a
+// grow-only arena kept per (device, stream): nested Workspaces of one op
+// bump-allocate from it and release in LIFO order; consecutive ops reuse the
+// same bytes (the stream orders them).  When an op needs more than the arena
+// holds it falls back to cudaMallocAsync for that call and the arena is
+// regrown (stream-ordered) to the op's high-water mark when the outermost
+// Workspace closes, so steady-state calls allocate nothing.  The arena lock
+// is held from the first Workspace of an op to its last (host-side calls on
+// one stream are serialized; the reference serializes on the GIL).
+struct ArenaState;
 struct Workspace {
   void* p = nullptr;
   cudaStream_t st;
-  explicit Workspace(cudaStream_t s) : st(s) {}
-  ~Workspace() {
-    if (p) cudaFreeAsync(p, st);
-  }
+  explicit Workspace(cudaStream_t s);
+  ~Workspace();
+  cudaError_t alloc(size_t bytes);
   Workspace(const Workspace&) = delete;
   Workspace& operator=(const Workspace&) = delete;
+
+ private:
+  ArenaState* a_;
+  size_t saved_off_ = 0;
+  bool fallback_ = false;
 };
 
 void pool_keep_memory();

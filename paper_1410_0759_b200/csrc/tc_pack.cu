@@ -2,6 +2,11 @@
 // -> channel-innermost BF16 hi/lo planes, staged through shared memory so
 // that both the (pixel-contiguous) reads and the (channel-contiguous)
 // 16-byte writes are coalesced.
+#include <algorithm>
+#include <cstdlib>
+#include <map>
+#include <mutex>
+
 #include "tc_common.cuh"
 
 namespace dnnp {
@@ -122,6 +127,55 @@ __global__ void __launch_bounds__(256) pack_act_s2d_kernel(View4 v, const float*
   }
 }
 
+// Space-to-depth, one block per output row (n, h'): the u input rows of
+// every channel are read coalesced along w into shared memory as
+// [w'][(rh*v + rw)*C + c], then the contiguous W' x Cp output row is written
+// with 16-byte stores.
+__global__ void __launch_bounds__(256) pack_act_s2d_row_kernel(View4 v, const float* __restrict__ x,
+                                                               int u, int vv, int pad_h, int pad_w,
+                                                               int H2, int W2, int Cp,
+                                                               __nv_bfloat16* __restrict__ hi,
+                                                               __nv_bfloat16* __restrict__ lo) {
+  extern __shared__ float srow[];
+  const int Cps = Cp + 1;  // odd pitch: fewer bank conflicts on the scatter
+  const int C = int(v.c);
+  const int WV = W2 * vv;  // input columns covered by the row
+  for (int row = blockIdx.x; row < int(v.n) * H2; row += gridDim.x) {
+    const int n = row / H2, h2 = row - n * H2;
+    const float* src = x + int64_t(n) * v.sn;
+    const int items = C * u * WV;
+    for (int t = threadIdx.x; t < items; t += blockDim.x) {
+      const int wc = t % WV, q = t / WV;
+      const int rh = q % u, c = q / u;
+      const int h = h2 * u + rh - pad_h, w = wc - pad_w;
+      float val = 0.0f;
+      if (unsigned(h) < unsigned(v.h) && unsigned(w) < unsigned(v.w))
+        val = __ldg(src + int64_t(c) * v.sc + int64_t(h) * v.sh + int64_t(w) * v.sw);
+      const int w2 = wc / vv, rw = wc - w2 * vv;
+      srow[w2 * Cps + (rh * vv + rw) * C + c] = val;
+    }
+    // zero the channel padding
+    const int Cs = u * vv * C;
+    for (int t = threadIdx.x; t < W2 * (Cp - Cs); t += blockDim.x) {
+      const int w2 = t / (Cp - Cs), cc = Cs + t % (Cp - Cs);
+      srow[w2 * Cps + cc] = 0.0f;
+    }
+    __syncthreads();
+    const int groups = Cp / 8;
+    const int64_t obase = int64_t(row) * W2 * Cp;
+    for (int t = threadIdx.x; t < W2 * groups; t += blockDim.x) {
+      const int w2 = t / groups, g = t - w2 * groups;
+      __align__(16) __nv_bfloat16 vh[8], vl[8];
+#pragma unroll
+      for (int k = 0; k < 8; k++) split_bf16(srow[w2 * Cps + g * 8 + k], vh[k], vl[k]);
+      const int64_t o = obase + int64_t(w2) * Cp + g * 8;
+      *reinterpret_cast<uint4*>(hi + o) = *reinterpret_cast<const uint4*>(vh);
+      *reinterpret_cast<uint4*>(lo + o) = *reinterpret_cast<const uint4*>(vl);
+    }
+    __syncthreads();
+  }
+}
+
 }  // namespace
 
 cudaError_t pack_act_s2d(const View4& v, const float* x, int u, int vv, int pad_h, int pad_w,
@@ -129,11 +183,72 @@ cudaError_t pack_act_s2d(const View4& v, const float* x, int u, int vv, int pad_
                          cudaStream_t st) {
   const int64_t npix = v.n * H2 * W2;
   if (npix >= (int64_t(1) << 32)) return cudaErrorInvalidValue;
+  const size_t row_smem = size_t(W2) * (Cp + 1) * sizeof(float);
+  if (getenv("DNNP_S2D_ROWS") && row_smem <= 48 * 1024 && v.n * H2 < (int64_t(1) << 31)) {
+    const unsigned grid = unsigned(std::min<int64_t>(v.n * H2, int64_t(kNumSMs) * 8));
+    pack_act_s2d_row_kernel<<<grid, 256, row_smem, st>>>(v, x, u, vv, pad_h, pad_w, H2, W2, Cp, hi,
+                                                         lo);
+    note_launch();
+    return cudaGetLastError();
+  }
   pack_act_s2d_kernel<<<grid_for(npix, 256, 8), 256, 0, st>>>(
       v, x, u, vv, pad_h, pad_w, H2, W2, Cp, hi, lo, npix, make_magic(uint32_t(H2 * W2)),
       make_magic(uint32_t(W2)));
   note_launch();
   return cudaGetLastError();
+}
+
+struct ArenaState {
+  std::recursive_mutex mu;
+  void* base = nullptr;
+  size_t cap = 0, off = 0, high = 0;
+  int depth = 0;
+};
+
+static ArenaState* arena_for(cudaStream_t st) {
+  static std::mutex map_mu;
+  static std::map<std::pair<int, cudaStream_t>, ArenaState*> arenas;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> g(map_mu);
+  ArenaState*& a = arenas[{dev, st}];
+  if (!a) a = new ArenaState;  // lives for the process
+  return a;
+}
+
+Workspace::Workspace(cudaStream_t s) : st(s), a_(arena_for(s)) {
+  a_->mu.lock();
+  a_->depth++;
+  saved_off_ = a_->off;
+}
+
+cudaError_t Workspace::alloc(size_t bytes) {
+  bytes = (bytes + 1023) & ~size_t(1023);
+  a_->high = std::max(a_->high, a_->off + bytes);
+  if (a_->base && a_->off + bytes <= a_->cap) {
+    p = static_cast<char*>(a_->base) + a_->off;
+    a_->off += bytes;
+    return cudaSuccess;
+  }
+  fallback_ = true;
+  return cudaMallocAsync(&p, bytes, st);
+}
+
+Workspace::~Workspace() {
+  if (fallback_ && p) cudaFreeAsync(p, st);
+  a_->off = saved_off_;
+  if (--a_->depth == 0 && a_->high > a_->cap) {
+    if (a_->base) cudaFreeAsync(a_->base, st);
+    const size_t ncap = a_->high + a_->high / 4;
+    if (cudaMallocAsync(&a_->base, ncap, st) == cudaSuccess) {
+      a_->cap = ncap;
+    } else {
+      cudaGetLastError();
+      a_->base = nullptr;
+      a_->cap = 0;
+    }
+  }
+  a_->mu.unlock();
 }
 
 void pool_keep_memory() {

@@ -493,36 +493,37 @@ __global__ void __launch_bounds__(kWgThreads, 1) wgrad_tma_kernel(const __grid_c
   }
 }
 
-// df[k][c][r][s] (+)= sum_z ws[z][col][k] for the x column col = tap * Cpf +
-// cg of filter element (c, r, s): tap = (r' / su, s' / sv) with r' the
-// gather offset of r (R-1-r in CONVOLUTION mode), cg = ((r' % su) * sv +
-// s' % sv) * C + c.
+// df[k][c][r][s] (+)= sum_z ws[z][col][k].  One thread per workspace
+// element (col, k), k fastest, so the split reads are coalesced; the x column
+// col = tap * Cpf + cg decodes to the filter element it holds: tap = (dh', dw'),
+// cg = ((rh * sv) + rw) * C + c, gather offset r' = dh' * su + rh (zero-padding
+// columns and offsets >= R hold no filter element), r = R-1-r' in CONVOLUTION mode.
 struct WgReduceGeom {
   int K, C, R, S, flip;
   int su, sv, S2, Cpf;  // space-to-depth factors, taps per window row, columns per tap
+  int ncolx;            // taps * Cpf
   int splits, mrows_p, ncol_p;
 };
 
 __global__ void __launch_bounds__(256) wgrad_reduce_tma(WgReduceGeom g, const float* __restrict__ ws,
                                                         float* __restrict__ df, int accumulate) {
-  const int64_t total = int64_t(g.K) * g.C * g.R * g.S;
-  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  const int total = g.ncolx * g.K;
+  const int stride = gridDim.x * blockDim.x;
   const int64_t plane = int64_t(g.mrows_p) * g.ncol_p;
-  for (int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; idx < total; idx += stride) {
-    const int s = int(idx % g.S);
-    int64_t t = idx / g.S;
-    const int r = int(t % g.R);
-    t /= g.R;
-    const int c = int(t % g.C);
-    const int k = int(t / g.C);
-    const int ro = g.flip ? g.R - 1 - r : r, so = g.flip ? g.S - 1 - s : s;  // gather offsets
-    const int tap = (ro / g.su) * g.S2 + so / g.sv;
-    const int cg = ((ro % g.su) * g.sv + so % g.sv) * g.C + c;
-    const int col = tap * g.Cpf + cg;
+  const int Cg = g.su * g.sv * g.C;
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += stride) {
+    const int k = idx % g.K, col = idx / g.K;
+    const int tap = col / g.Cpf, cg = col - tap * g.Cpf;
+    if (cg >= Cg) continue;
+    const int ph = cg / g.C, c = cg - ph * g.C;
+    const int ro = (tap / g.S2) * g.su + ph / g.sv, so = (tap % g.S2) * g.sv + ph % g.sv;
+    if (ro >= g.R || so >= g.S) continue;
+    const int r = g.flip ? g.R - 1 - ro : ro, s = g.flip ? g.S - 1 - so : so;
     const float* src = ws + int64_t(col) * g.ncol_p + k;
     float acc = src[0];
     for (int z = 1; z < g.splits; z++) acc = __fadd_rn(acc, src[z * plane]);
-    df[idx] = accumulate ? __fadd_rn(df[idx], acc) : acc;
+    float* d = df + ((int64_t(k) * g.C + c) * g.R + r) * g.S + s;
+    *d = accumulate ? __fadd_rn(*d, acc) : acc;
   }
 }
 
@@ -605,7 +606,7 @@ cudaError_t wgrad_tma(const ConvProblem& p, const float* dy, const float* x, flo
   const size_t dy_elems = size_t(NPQ) * Kp64, x_elems = size_t(p.N) * IH * IW * Cp;
   const size_t ws_floats = size_t(splits) * mrows * ncols;
   Workspace wsp(st);
-  cudaError_t e = cudaMallocAsync(&wsp.p, (dy_elems + x_elems) * 4 + ws_floats * 4 + 512, st);
+  cudaError_t e = wsp.alloc((dy_elems + x_elems) * 4 + ws_floats * 4 + 512);
   if (e != cudaSuccess) return e;
   auto* dy_hi = static_cast<__nv_bfloat16*>(wsp.p);
   auto* dy_lo = dy_hi + dy_elems;
@@ -702,11 +703,12 @@ cudaError_t wgrad_tma(const ConvProblem& p, const float* dy, const float* x, flo
   rg.sv = sv;
   rg.S2 = S2;
   rg.Cpf = Cpf;
+  rg.ncolx = ncolx;
   rg.splits = int(splits);
   rg.mrows_p = mrows;
   rg.ncol_p = ncols;
-  wgrad_reduce_tma<<<grid_for(int64_t(p.K) * p.C * p.R * p.S, 256, 16), 256, 0, st>>>(
-      rg, part, df, acc ? 1 : 0);
+  wgrad_reduce_tma<<<grid_for(int64_t(ncolx) * p.K, 256, 16), 256, 0, st>>>(rg, part, df,
+                                                                            acc ? 1 : 0);
   note_launch();
   return cudaGetLastError();
 }
@@ -737,7 +739,7 @@ cudaError_t tc_backward_filter(const ConvProblem& p, const float* dy, const floa
   const size_t dy_elems = size_t(NPQ) * Kp, x_elems = size_t(NHW) * Cp;
   const size_t ws_floats = size_t(splits) * mrows_p * ncol_p;
   Workspace ws(st);
-  cudaError_t e = cudaMallocAsync(&ws.p, (dy_elems + x_elems) * 4 + ws_floats * 4 + size_t(KC) * 4 + 512, st);
+  cudaError_t e = ws.alloc((dy_elems + x_elems) * 4 + ws_floats * 4 + size_t(KC) * 4 + 512);
   if (e != cudaSuccess) return e;
   auto* dy_hi = static_cast<__nv_bfloat16*>(ws.p);
   auto* dy_lo = dy_hi + dy_elems;
