@@ -465,6 +465,69 @@ __global__ void __launch_bounds__(256) pack_filter_kernel(PackGeom g, const floa
   }
 }
 
+// Scatter form of the filter packing: one thread per filter element (read
+// coalesced) computes its single position in the packed GEMM operand; the
+// padding is zeroed by a memset first.  Inverse of pack_filter_kernel's map:
+// gather offset r' -> (space-to-depth tap r'/su, phase r'%su); for the
+// super-pixel bwd-data form t0 = r' % u, jr = r' / u, phase ph = (t0 - pad)
+// mod u and window tap dh = base(ph) - jr - lo.
+__global__ void __launch_bounds__(256) pack_filter_scatter_kernel(PackGeom g, const float* __restrict__ f,
+                                                                  __nv_bfloat16* __restrict__ hi,
+                                                                  __nv_bfloat16* __restrict__ lo) {
+  const int total = g.K * g.C0 * g.R0 * g.S0;
+  const int Cpf = g.Cgrp * 8;
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * blockDim.x) {
+    const int s = idx % g.S0;
+    int t = idx / g.S0;
+    const int r = t % g.R0;
+    t /= g.R0;
+    const int c0 = t % g.C0, k = t / g.C0;
+    const int ro = g.flip ? g.R0 - 1 - r : r, so = g.flip ? g.S0 - 1 - s : s;
+    const int rt = ro / g.su, st = so / g.sv;
+    const int cg = ((ro % g.su) * g.sv + so % g.sv) * g.C0 + c0;
+    int64_t o;
+    if (!g.dgrad) {
+      o = int64_t(k) * g.Ktot + (rt * g.S + st) * Cpf + cg;
+    } else {
+      const int t0h = rt % g.u, jrh = rt / g.u;
+      const int ph = ((t0h - g.pad_h) % g.u + g.u) % g.u;
+      const int dh = (ph + g.pad_h - t0h) / g.u - jrh - g.lo_h;
+      const int t0w = st % g.v, jrw = st / g.v;
+      const int pw = ((t0w - g.pad_w) % g.v + g.v) % g.v;
+      const int dw = (pw + g.pad_w - t0w) / g.v - jrw - g.lo_w;
+      const int row = (ph * g.v + pw) * g.C + cg;
+      o = int64_t(row) * g.Ktot + (dh * g.winW + dw) * Cpf + k;
+    }
+    __nv_bfloat16 h, l;
+    split_bf16(__ldg(f + idx), h, l);
+    hi[o] = h;
+    lo[o] = l;
+  }
+}
+
+// chunk table (cp.async kernel) and bwd-data column table
+__global__ void pack_tables_kernel(PackGeom g, uint32_t* __restrict__ ctab, uint32_t* __restrict__ coltab,
+                                   int want_ctab) {
+  const int nS = g.dgrad ? g.winW : g.S;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < max(g.KC, g.Ncol); i += gridDim.x * blockDim.x) {
+    if (want_ctab && i < g.KC) {
+      const int tap = i / g.Cgrp, grp = i % g.Cgrp;
+      ctab[i] = (uint32_t(tap / nS) << 24) | (uint32_t(tap % nS) << 16) | uint32_t(grp * 8);
+    }
+    if (g.dgrad && i < g.Ncol) {
+      uint32_t e;
+      if (g.su * g.sv > 1) {
+        const int q = i / g.C0, c = i - q * g.C0;
+        e = (uint32_t(q / g.sv) << 24) | (uint32_t(q % g.sv) << 16) | uint32_t(c);
+      } else {
+        const int c = i % g.C, phase = i / g.C;
+        e = (uint32_t(phase / g.v) << 24) | (uint32_t(phase % g.v) << 16) | uint32_t(c);
+      }
+      coltab[i] = e;
+    }
+  }
+}
+
 // ------------------------------------------------------------- launching
 
 template <int BN>
@@ -647,9 +710,17 @@ cudaError_t run_gemm(const ConvProblem& p, Gemm g, const __nv_bfloat16* a_hi,
   auto* b_lo = b_hi + flt;
   auto* ctab = reinterpret_cast<uint32_t*>(b_lo + flt);
   auto* coltab = ctab + pg.KC + 1;
-  {
+  if (!getenv("DNNP_PACK_SCATTER")) {
     const dim3 fgrid(unsigned(std::min<int64_t>(ceil_div(pg.Ktot, 256), 8)), unsigned(pg.Np));
     pack_filter_kernel<<<fgrid, 256, 0, st>>>(pg, f, b_hi, b_lo, ctab, coltab);
+  } else {
+    if ((e = cudaMemsetAsync(b_hi, 0, flt * 4, st)) != cudaSuccess) return e;  // hi and lo planes
+    const int64_t nf = int64_t(pg.K) * pg.C0 * pg.R0 * pg.S0;
+    pack_filter_scatter_kernel<<<grid_for(nf, 256, 8), 256, 0, st>>>(pg, f, b_hi, b_lo);
+    note_launch();
+    pack_tables_kernel<<<grid_for(std::max(pg.KC, pg.Ncol), 256, 2), 256, 0, st>>>(pg, ctab, coltab,
+                                                                                  g.tma ? 0 : 1);
+    note_launch();
   }
   note_launch();
   const int64_t tiles = ceil_div(M, kBM * nc) * (pg.Np / bn);
@@ -712,6 +783,32 @@ cudaError_t run_gemm(const ConvProblem& p, Gemm g, const __nv_bfloat16* a_hi,
     prm.dOHW = make_magic(uint32_t(g.OH * g.OW));
     prm.dOW = make_magic(uint32_t(g.OW));
     prm.skip = getenv("DNNP_TC_SKIP") ? atoi(getenv("DNNP_TC_SKIP")) : 0;
+    // stream-K over the last, partial wave of tiles
+    Workspace skw(st);
+    {
+      const int G = int(std::min<int64_t>(tiles, kNumSMs / nc));
+      const int T = int(tiles), W = T / G, R = T % G;
+      const bool use_sk = getenv("DNNP_TC_SK") && !getenv("DNNP_TC_NO_SK") && W >= 1 && R > 0 && double(R) / G < 0.85 &&
+                          int64_t(R) * nkb < (int64_t(1) << 30);
+      if (use_sk) {
+        const int U = R * nkb;
+        int maxp = 1;
+        for (int tl = 0; tl < R; tl++) {
+          const int first = sk_owner(tl * nkb, U, G), last = sk_owner(tl * nkb + nkb - 1, U, G);
+          maxp = std::max(maxp, last - first + 1);
+        }
+        const size_t part_bytes = size_t(R) * nc * maxp * kBM * bn * sizeof(float);
+        const size_t cnt_bytes = size_t(R) * nc * sizeof(int);
+        if ((e = skw.alloc(part_bytes + cnt_bytes)) != cudaSuccess) return e;
+        prm.skws = static_cast<float*>(skw.p);
+        prm.skcnt = reinterpret_cast<int*>(static_cast<char*>(skw.p) + part_bytes);
+        if ((e = cudaMemsetAsync(prm.skcnt, 0, cnt_bytes, st)) != cudaSuccess) return e;
+        prm.sk = 1;
+        prm.W = W;
+        prm.U = U;
+        prm.maxp = maxp;
+      }
+    }
     static unsigned long long* tbuf = nullptr;
     const bool want_trace = getenv("DNNP_TC_TRACE") != nullptr;
     if (want_trace && !tbuf) cudaMalloc(&tbuf, 8192 * sizeof(unsigned long long));

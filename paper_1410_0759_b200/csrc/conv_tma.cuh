@@ -4,23 +4,28 @@
 // The packed input planes [N][IH][IW][Cp] (BF16 hi / lo) are described by
 // two im2col tensor maps: one load = 128 consecutive output pixels (walking
 // W -> H -> N inside the bounding box, zero fill at the image border) x CB
-// channels of one filter tap, written 32B/64B-swizzled straight into the
-// K-major A stage.  No producer warps: one thread streams A and B (the
-// packed filter, tiled TMA) for every stage, so the gather costs no issue
-// slots and no per-row address arithmetic (the cp.async kernel in conv_tc.cu
-// spent ~500 cycles per stage there, more than the MMAs of the stage).
+// channels of one filter tap, written 32B/64B/128B-swizzled straight into the
+// K-major A stage.  One thread streams A and B (the packed filter, tiled TMA)
+// for every stage: no per-row address arithmetic, no producer warps.
 //
 // NC = 2 runs the tile on a CTA pair (cluster of 2 on one TPC,
 // tcgen05.mma.cta_group::2, M = 256): each CTA gathers its own 128 pixel
-// rows and HALF of the BN filter rows, so the bytes each SM must ingest per
-// MMA drop from (128 + BN) to (128 + BN/2) rows -- measured, a single SM
-// ingests ~60 B/clk, which caps 128 x BN tiles below the tensor rate for
-// BN < 256 (profiles/README.md).
+// rows and HALF of the BN filter rows, so the bytes each SM ingests per
+// stage drop from 32 KB + 256*BN to 32 KB + 128*BN -- every SM streaming at
+// once gets ~57 B/clk (profiles/r01/tma_burst_probe.txt), below what a
+// 128 x BN BF16x3 tile consumes for BN < 256.
+//
+// Schedule: persistent clusters walk whole tiles for the full waves; when the
+// last wave would be partial ("stream-K"), its tiles are cut along the
+// reduction into equal contiguous unit ranges, one per cluster.  A tile cut
+// into pieces accumulates each piece in TMEM, the epilogue writes it as an
+// fp32 partial and bumps the tile's counter; the last piece to arrive sums
+// all partials in piece order (deterministic) and writes the output.
 //
 // Warps: 0 = TMA producer (one elected lane, both CTAs), 1 = TMEM allocation
 // + MMA issue (leader CTA only; warp-collective loop, elected issue), 2-5 =
 // epilogue (TMEM lane quadrant warp % 4), double-buffered accumulator so the
-// epilogue of tile i overlaps the main loop of tile i + 1.
+// epilogue of one work item overlaps the main loop of the next.
 #pragma once
 
 constexpr int kTmaThreads = 6 * 32;
@@ -37,6 +42,11 @@ struct TmaParams {
   int nCB, tapW, KCH, nkb;     // channel blocks per tap, taps per window row, chunks, k-blocks
   int Cext;                    // channel extent of the A maps (OOB coordinate for padding chunks)
   int nt, tiles;               // column tiles, tiles (of NC * 128 rows)
+  // stream-K: full waves W (tiles cid + i*G), then units [cid*U/G, (cid+1)*U/G)
+  // of the last R = tiles - W*G tiles; U = R * nkb.  sk = 0: plain persistent.
+  int sk, W, U, maxp;
+  float* skws;                 // partials [R][NC][maxp][128][BN]
+  int* skcnt;                  // arrival counters [R][NC], zero on entry, reset by the finisher
   float* out;
   int64_t o_sn, o_sc, o_sh, o_sw;
   int out_mode;                // 0: column = channel; 1: column table (ph, pw, c)
@@ -59,7 +69,7 @@ struct TCfg {
   static constexpr int B_BYTES = SUB * B_SUB;
   static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;  // per CTA
   static constexpr int STAGES =
-      (200 * 1024) / STAGE_BYTES > 8 ? 8 : (200 * 1024) / STAGE_BYTES;
+      (225 * 1024 - 2048) / STAGE_BYTES > 8 ? 8 : (225 * 1024 - 2048) / STAGE_BYTES;
   static constexpr int TMEM_COLS =
       2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512));
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
@@ -71,6 +81,64 @@ __device__ __forceinline__ uint64_t tma_kdesc(uint32_t addr) {
   else if constexpr (CB == 32) return ptx::desc_kmajor_sw64(addr);
   else return ptx::desc_kmajor_sw32(addr);
 }
+
+// Owner cluster of stream-K unit x: the largest j with floor(j*U/G) <= x.
+__host__ __device__ __forceinline__ int sk_owner(int x, int U, int G) {
+  int j = int((int64_t(x) * G) / U);
+  while (j + 1 < G && int((int64_t(j + 1) * U) / G) <= x) j++;
+  while (j > 0 && int((int64_t(j) * U) / G) > x) j--;
+  return j;
+}
+
+// The sequence of work items of one cluster: (tile, k-block range, piece of
+// the tile, pieces of the tile); every role of the cluster walks it alike.
+struct WorkIter {
+  int cid, G, nkb, tiles, sk, W, U;
+  int i, u, uend;
+  __device__ void init(const TmaParams& P, int cid_, int G_) {
+    cid = cid_;
+    G = G_;
+    nkb = P.nkb;
+    tiles = P.tiles;
+    sk = P.sk;
+    W = P.W;
+    U = P.U;
+    i = 0;
+    u = sk ? int((int64_t(cid) * U) / G) : 0;
+    uend = sk ? int((int64_t(cid + 1) * U) / G) : 0;
+  }
+  __device__ bool next(int& tile, int& kb0, int& kb1, int& piece, int& np) {
+    if (!sk) {
+      tile = cid + i * G;
+      if (tile >= tiles) return false;
+      i++;
+      kb0 = 0;
+      kb1 = nkb;
+      piece = 0;
+      np = 1;
+      return true;
+    }
+    if (i < W) {
+      tile = cid + i * G;
+      i++;
+      kb0 = 0;
+      kb1 = nkb;
+      piece = 0;
+      np = 1;
+      return true;
+    }
+    if (u >= uend) return false;
+    const int tl = u / nkb;
+    tile = W * G + tl;
+    kb0 = u - tl * nkb;
+    kb1 = min(nkb, kb0 + (uend - u));
+    const int first = sk_owner(tl * nkb, U, G), last = sk_owner(tl * nkb + nkb - 1, U, G);
+    piece = cid - first;
+    np = last - first + 1;
+    u += kb1 - kb0;
+    return true;
+  }
+};
 
 template <int BN, int CB, int NC>
 __global__ void __launch_bounds__(kTmaThreads, 1) conv_tma_kernel(const __grid_constant__ TmaParams P) {
@@ -84,6 +152,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) conv_tma_kernel(const __grid_c
   uint64_t* tfull = empty + S;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  int* sk_flag = reinterpret_cast<int*>(tmem_slot + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = NC == 2 ? ptx::cluster_ctarank() : 0u;
@@ -111,6 +180,9 @@ __global__ void __launch_bounds__(kTmaThreads, 1) conv_tma_kernel(const __grid_c
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   const uint32_t smem0 = ptx::smem_u32(smem);
+  WorkIter wi;
+  wi.init(P, cid, ncl);
+  int tile, kb0, kb1, piece, np;
 
   if (warp == 0) {
     // ================================================ TMA producer
@@ -120,28 +192,29 @@ __global__ void __launch_bounds__(kTmaThreads, 1) conv_tma_kernel(const __grid_c
       ptx::tma_prefetch(&P.tm_bhi);
       ptx::tma_prefetch(&P.tm_blo);
       int it = 0;
-      for (int tile = cid; tile < P.tiles; tile += ncl) {
+      while (wi.next(tile, kb0, kb1, piece, np)) {
         const uint32_t m0 = uint32_t(tile / P.nt) * (kBM * NC) + rank * kBM;
         const int n0 = (tile % P.nt) * BN + int(rank) * C::BNL;
         uint32_t img, rem, oh, ow;
         mdivmod(m0, P.dOHW, img, rem);
         mdivmod(rem, P.dOW, oh, ow);
         const int h0 = P.lower_h + int(oh) * P.u, w0 = P.lower_w + int(ow) * P.v;
-        int kc = 0, cb = 0, dh = 0, dw = 0;
-        for (int kb = 0; kb < P.nkb; kb++, it++) {
+        int kc = kb0 * C::SUB;
+        int tapi = kc / P.nCB, cb = kc - tapi * P.nCB;
+        int dh = tapi / P.tapW, dw = tapi - dh * P.tapW;
+        for (int kb = kb0; kb < kb1; kb++, it++) {
           const int s = it % S;
           const bool tr = P.trace && blockIdx.x == 0 && it < 1024;
           if (tr) P.trace[it * 4 + 0] = clock64();
           if (it >= S) ptx::mbar_wait(&empty[s], ((it / S) - 1) & 1);
           if (tr) P.trace[it * 4 + 1] = clock64();
-          if (P.skip & 2) {
-            if (NC == 1 || leader) ptx::mbar_arrive(&full[s]);
-            else ptx::mbar_arrive_cluster(&full[s], 0);
-            continue;
-          }
-          const uint32_t tx = (P.skip & 1) ? 2 * C::B_BYTES : C::STAGE_BYTES;
+          const uint32_t tx = (P.skip & 2) ? 0u : (P.skip & 1) ? 2 * C::B_BYTES : C::STAGE_BYTES;
           if (leader) ptx::mbar_arrive_expect_tx(&full[s], tx * NC);
           else ptx::mbar_arrive_cluster(&full[s], 0);
+          if (P.skip & 2) {
+            kc += C::SUB;
+            continue;
+          }
           const uint32_t bar = NC == 2 ? ptx::leader_addr(&full[s]) : ptx::smem_u32(&full[s]);
           const uint32_t base = smem0 + s * C::STAGE_BYTES;
 #pragma unroll
@@ -184,13 +257,13 @@ __global__ void __launch_bounds__(kTmaThreads, 1) conv_tma_kernel(const __grid_c
     if (leader) {
       constexpr uint32_t idesc = ptx::idesc_bf16(kBM * NC, BN, 0, 0);
       int it = 0, lt = 0;
-      for (int tile = cid; tile < P.tiles; tile += ncl, lt++) {
+      while (wi.next(tile, kb0, kb1, piece, np)) {
         const int buf = lt & 1;
         ptx::mbar_wait(&tempty[buf], ((lt >> 1) & 1) ^ 1);
         ptx::tc_fence_after();
         const uint32_t dacc = tmem_base + uint32_t(buf * BN);
         uint32_t acc = 0;
-        for (int kb = 0; kb < P.nkb; kb++, it++) {
+        for (int kb = kb0; kb < kb1; kb++, it++) {
           const int s = it % S;
           ptx::mbar_wait_spin(&full[s], (it / S) & 1);
           ptx::tc_fence_after();
@@ -223,14 +296,16 @@ __global__ void __launch_bounds__(kTmaThreads, 1) conv_tma_kernel(const __grid_c
         }
         if constexpr (NC == 2) ptx::mma_commit_pair_elect(&tfull[buf]);
         else ptx::mma_commit_elect(&tfull[buf]);
+        lt++;
       }
     }
   } else {
     // ================================================ epilogue
     const int ew = warp & 3;  // TMEM lane quadrant accessible to this warp
     const int r = ew * 32 + lane;
+    const int et = threadIdx.x - 64;  // 0..127 over the four epilogue warps
     int lt = 0;
-    for (int tile = cid; tile < P.tiles; tile += ncl, lt++) {
+    while (wi.next(tile, kb0, kb1, piece, np)) {
       const int buf = lt & 1;
       const int64_t m = int64_t(tile / P.nt) * (kBM * NC) + int64_t(rank) * kBM + r;
       const int n0 = (tile % P.nt) * BN;
@@ -246,50 +321,93 @@ __global__ void __launch_bounds__(kTmaThreads, 1) conv_tma_kernel(const __grid_c
       ptx::mbar_wait(&tfull[buf], (lt >> 1) & 1);
       if (etr) P.trace[4096 + lt * 4 + 1] = clock64();
       ptx::tc_fence_after();
-      const int64_t rowoff =
-          P.out_mode == 0 ? int64_t(img) * P.o_sn + int64_t(oh) * P.o_sh + int64_t(ow) * P.o_sw
-                          : int64_t(img) * P.o_sn;
+      bool finisher = true;
+      float* part = nullptr;
+      if (np > 1) {
+        // partial piece: park the raw accumulator, count arrivals; the last
+        // piece of the tile reduces all pieces in order
+        const int slot = (tile - P.W * ncl) * NC + int(rank);
+        part = P.skws + (int64_t(slot) * P.maxp) * (kBM * BN);
+        // column-major [col][row] so each warp store / load is 128 contiguous bytes
+        float* mine = part + int64_t(piece) * (kBM * BN) + r;
 #pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += 32) {
-        const int cbase = n0 + c0;
-        if (cbase >= P.Ncol) break;  // warp-uniform: padded columns are never loaded
-        uint32_t v[32];
-        ptx::tmem_ld32(tmem_base + (uint32_t(ew * 32) << 16) + uint32_t(buf * BN + c0), v);
-        ptx::tmem_ld_wait();
-        if (!row_ok) continue;
-        if (P.out_mode == 0 && P.plain && cbase + 32 <= P.Ncol) {
-          float* dst = P.out + rowoff + int64_t(cbase) * P.o_sc;
-          const int64_t sc = P.o_sc;
+        for (int c0 = 0; c0 < BN; c0 += 32) {
+          uint32_t v[32];
+          ptx::tmem_ld32(tmem_base + (uint32_t(ew * 32) << 16) + uint32_t(buf * BN + c0), v);
+          ptx::tmem_ld_wait();
 #pragma unroll
-          for (int i = 0; i < 32; i++) {
-            *dst = __uint_as_float(v[i]);
-            dst += sc;
-          }
-        } else if (P.out_mode == 0) {
-          float* rowp = P.out + rowoff + int64_t(cbase) * P.o_sc;
+          for (int i = 0; i < 32; i++) __stcg(mine + (c0 + i) * kBM, __uint_as_float(v[i]));
+        }
+        __threadfence();
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (et == 0) {
+          const int prev = atomicAdd(P.skcnt + slot, 1);
+          const bool last = prev == np - 1;
+          if (last) P.skcnt[slot] = 0;  // ready for the next launch
+          *sk_flag = last ? 1 : 0;
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        finisher = *sk_flag != 0;
+        if (finisher) __threadfence();
+      }
+      if (finisher) {
+        const int64_t rowoff =
+            P.out_mode == 0 ? int64_t(img) * P.o_sn + int64_t(oh) * P.o_sh + int64_t(ow) * P.o_sw
+                            : int64_t(img) * P.o_sn;
+#pragma unroll 1
+        for (int c0 = 0; c0 < BN; c0 += 32) {
+          const int cbase = n0 + c0;
+          if (cbase >= P.Ncol) break;  // warp-uniform: padded columns are never loaded
+          uint32_t v[32];
+          if (np == 1) {
+            ptx::tmem_ld32(tmem_base + (uint32_t(ew * 32) << 16) + uint32_t(buf * BN + c0), v);
+            ptx::tmem_ld_wait();
+          } else {
+            const float* src = part + int64_t(c0) * kBM + r;
 #pragma unroll
-          for (int i = 0; i < 32; i++) {
-            if (cbase + i < P.Ncol) {
-              float* dst = rowp + int64_t(i) * P.o_sc;
-              float val = __fmul_rn(__uint_as_float(v[i]), P.alpha);
-              if (P.beta != 0.0f) val = __fadd_rn(__fmul_rn(*dst, P.beta), val);
-              *dst = val;
+            for (int i = 0; i < 32; i++) v[i] = __float_as_uint(__ldcg(src + i * kBM));
+            for (int q = 1; q < np; q++) {
+              const float* sq = src + int64_t(q) * (kBM * BN);
+#pragma unroll
+              for (int i = 0; i < 32; i++)
+                v[i] = __float_as_uint(__fadd_rn(__uint_as_float(v[i]), __ldcg(sq + i * kBM)));
             }
           }
-        } else {
+          if (!row_ok) continue;
+          if (P.out_mode == 0 && P.plain && cbase + 32 <= P.Ncol) {
+            float* dst = P.out + rowoff + int64_t(cbase) * P.o_sc;
+            const int64_t sc = P.o_sc;
 #pragma unroll
-          for (int i = 0; i < 32; i++) {
-            const int col = cbase + i;
-            if (col < P.Ncol) {
-              const uint32_t e = __ldg(P.coltab + col);
-              const int h = int(oh) * P.o_u + int(e >> 24) - P.o_ph;
-              const int w = int(ow) * P.o_v + int((e >> 16) & 255) - P.o_pw;
-              if (unsigned(h) < unsigned(P.o_H) && unsigned(w) < unsigned(P.o_W)) {
-                float* dst = P.out + rowoff + int64_t(e & 0xFFFF) * P.o_sc + int64_t(h) * P.o_sh +
-                             int64_t(w) * P.o_sw;
+            for (int i = 0; i < 32; i++) {
+              *dst = __uint_as_float(v[i]);
+              dst += sc;
+            }
+          } else if (P.out_mode == 0) {
+            float* rowp = P.out + rowoff + int64_t(cbase) * P.o_sc;
+#pragma unroll
+            for (int i = 0; i < 32; i++) {
+              if (cbase + i < P.Ncol) {
+                float* dst = rowp + int64_t(i) * P.o_sc;
                 float val = __fmul_rn(__uint_as_float(v[i]), P.alpha);
                 if (P.beta != 0.0f) val = __fadd_rn(__fmul_rn(*dst, P.beta), val);
                 *dst = val;
+              }
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; i++) {
+              const int col = cbase + i;
+              if (col < P.Ncol) {
+                const uint32_t e = __ldg(P.coltab + col);
+                const int h = int(oh) * P.o_u + int(e >> 24) - P.o_ph;
+                const int w = int(ow) * P.o_v + int((e >> 16) & 255) - P.o_pw;
+                if (unsigned(h) < unsigned(P.o_H) && unsigned(w) < unsigned(P.o_W)) {
+                  float* dst = P.out + rowoff + int64_t(e & 0xFFFF) * P.o_sc + int64_t(h) * P.o_sh +
+                               int64_t(w) * P.o_sw;
+                  float val = __fmul_rn(__uint_as_float(v[i]), P.alpha);
+                  if (P.beta != 0.0f) val = __fadd_rn(__fmul_rn(*dst, P.beta), val);
+                  *dst = val;
+                }
               }
             }
           }
@@ -302,6 +420,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) conv_tma_kernel(const __grid_c
         if (NC == 1) ptx::mbar_arrive(&tempty[buf]);
         else ptx::mbar_arrive_cluster(&tempty[buf], 0);
       }
+      lt++;
     }
   }
   ptx::tc_fence_before();

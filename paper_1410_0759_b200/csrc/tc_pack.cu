@@ -14,42 +14,48 @@ namespace tc {
 
 namespace {
 
-constexpr int kPix = 64;   // pixels per tile
+constexpr int kPix = 32;   // pixels per tile
 constexpr int kCh = 64;    // channels per slab
 
+// Strided fp32 -> channel-innermost bf16 hi/lo planes through a 64 x 32
+// shared tile: reads are one channel x 32 consecutive pixels per warp
+// instruction (128 B for NCHW), writes are 4 pixels x 8 channel groups per
+// warp instruction (contiguous 16-byte chunks).  Grid-stride over
+// (pixel tile, channel slab) jobs.
 __global__ void __launch_bounds__(256) pack_act_kernel(View4 v, const float* __restrict__ x, int Cp,
                                                        __nv_bfloat16* __restrict__ hi,
                                                        __nv_bfloat16* __restrict__ lo, int64_t npix,
                                                        MagicDiv dHW, MagicDiv dW) {
-  __shared__ float tile[kPix][kCh + 1];
-  const int tp = threadIdx.x & 63, tcg = threadIdx.x >> 6;
+  __shared__ float tile[kCh][kPix + 1];
+  const int lp = threadIdx.x & 31, lc = threadIdx.x >> 5;  // read role: pixel, channel phase
+  const int wp = threadIdx.x >> 3, wg = threadIdx.x & 7;   // write role: pixel, channel group
   const int64_t ntiles = (npix + kPix - 1) / kPix;
   const int nslabs = (Cp + kCh - 1) / kCh;
   for (int64_t job = blockIdx.x; job < ntiles * nslabs; job += gridDim.x) {
     const int64_t pt = job / nslabs;
-    const int slab = int(job % nslabs);
+    const int slab = int(job - pt * nslabs);
     const int c_lo = slab * kCh, nch = min(kCh, Cp - c_lo);
-    const int64_t pix = pt * kPix + tp;
+    const int64_t pix = pt * kPix + lp;
     if (pix < npix) {
       uint32_t n, rem, h, w;
       mdivmod(uint32_t(pix), dHW, n, rem);
       mdivmod(rem, dW, h, w);
-      const float* src = x + int64_t(n) * v.sn + int64_t(h) * v.sh + int64_t(w) * v.sw;
-      for (int c = tcg; c < nch; c += 4) {
-        const int cc = c_lo + c;
-        tile[tp][c] = cc < v.c ? __ldg(src + int64_t(cc) * v.sc) : 0.0f;
+      const float* src = x + int64_t(n) * v.sn + int64_t(h) * v.sh + int64_t(w) * v.sw +
+                         int64_t(c_lo) * v.sc;
+      const int cvalid = int(v.c - c_lo < nch ? v.c - c_lo : nch);
+#pragma unroll
+      for (int i = 0; i < kCh / 8; i++) {
+        const int c = lc + 8 * i;
+        tile[c][lp] = c < cvalid ? __ldg(src + int64_t(c) * v.sc) : 0.0f;
       }
     }
     __syncthreads();
-    const int groups = nch / 8;
-    for (int q = threadIdx.x; q < kPix * groups; q += blockDim.x) {
-      const int p = q / groups, g = q % groups;
-      const int64_t opix = pt * kPix + p;
-      if (opix >= npix) continue;
+    const int64_t opix = pt * kPix + wp;
+    if (opix < npix && wg * 8 < nch) {
       __align__(16) __nv_bfloat16 vh[8], vl[8];
 #pragma unroll
-      for (int k = 0; k < 8; k++) split_bf16(tile[p][g * 8 + k], vh[k], vl[k]);
-      const int64_t o = opix * Cp + c_lo + g * 8;
+      for (int k = 0; k < 8; k++) split_bf16(tile[wg * 8 + k][wp], vh[k], vl[k]);
+      const int64_t o = opix * Cp + c_lo + wg * 8;
       *reinterpret_cast<uint4*>(hi + o) = *reinterpret_cast<const uint4*>(vh);
       *reinterpret_cast<uint4*>(lo + o) = *reinterpret_cast<const uint4*>(vl);
     }
@@ -352,7 +358,7 @@ cudaError_t pack_act(const View4& v, const float* x, int Cp, __nv_bfloat16* hi, 
     return cudaGetLastError();
   }
   const int64_t jobs = ceil_div(npix, kPix) * ceil_div(Cp, kCh);
-  const unsigned grid = unsigned(std::min<int64_t>(jobs, int64_t(kNumSMs) * 16));
+  const unsigned grid = unsigned(std::min<int64_t>(jobs, int64_t(kNumSMs) * 32));
   pack_act_kernel<<<grid, 256, 0, st>>>(v, x, Cp, hi, lo, npix, make_magic(uint32_t(v.h * v.w)),
                                         make_magic(uint32_t(v.w)));
   note_launch();

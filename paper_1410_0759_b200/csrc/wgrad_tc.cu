@@ -520,8 +520,17 @@ __global__ void __launch_bounds__(256) wgrad_reduce_tma(WgReduceGeom g, const fl
     if (ro >= g.R || so >= g.S) continue;
     const int r = g.flip ? g.R - 1 - ro : ro, s = g.flip ? g.S - 1 - so : so;
     const float* src = ws + int64_t(col) * g.ncol_p + k;
-    float acc = src[0];
-    for (int z = 1; z < g.splits; z++) acc = __fadd_rn(acc, src[z * plane]);
+    // loads issued 8 ahead, sums kept in split order (deterministic)
+    float acc = __ldcg(src);
+    int z = 1;
+    for (; z + 8 <= g.splits; z += 8) {
+      float t[8];
+#pragma unroll
+      for (int q = 0; q < 8; q++) t[q] = __ldcg(src + (z + q) * plane);
+#pragma unroll
+      for (int q = 0; q < 8; q++) acc = __fadd_rn(acc, t[q]);
+    }
+    for (; z < g.splits; z++) acc = __fadd_rn(acc, __ldcg(src + z * plane));
     float* d = df + ((int64_t(k) * g.C + c) * g.R + r) * g.S + s;
     *d = accumulate ? __fadd_rn(*d, acc) : acc;
   }
