@@ -465,6 +465,62 @@ __global__ void __launch_bounds__(256) pack_filter_kernel(PackGeom g, const floa
   }
 }
 
+// Filter packing, one block per (GEMM column row, tap): the tap's gather
+// offsets (and the bwd-data phase taps) are resolved once per block, threads
+// walk the tap's Cpf reduction channels (coalesced 2-byte stores).  Block
+// x == taps zero-fills the K padding tail.
+__global__ void __launch_bounds__(128) pack_filter_tap_kernel(PackGeom g, const float* __restrict__ f,
+                                                              __nv_bfloat16* __restrict__ hi,
+                                                              __nv_bfloat16* __restrict__ lo,
+                                                              uint32_t* __restrict__ ctab,
+                                                              uint32_t* __restrict__ coltab, int taps) {
+  const int row = blockIdx.y, tap = blockIdx.x;
+  const int Cpf = g.Cgrp * 8;
+  const int64_t rbase = int64_t(row) * g.Ktot;
+  if (tap == taps) {  // padding tail of the reduction
+    for (int k = taps * Cpf + threadIdx.x; k < g.Ktot; k += blockDim.x) {
+      hi[rbase + k] = __float2bfloat16_rn(0.0f);
+      lo[rbase + k] = __float2bfloat16_rn(0.0f);
+    }
+    return;
+  }
+  const int nS = g.dgrad ? g.winW : g.S;
+  const int dh = tap / nS, dw = tap - (tap / nS) * nS;
+  int c_col = 0, rp = -1, sp = -1;
+  if (g.dgrad && row < g.Ncol) {
+    const int phase = row / g.C;
+    c_col = row - phase * g.C;
+    const int ph = phase / g.v, pw = phase - (phase / g.v) * g.v;
+    rp = phase_tap(ph, dh, g.lo_h, g.u, g.pad_h, g.R);
+    sp = phase_tap(pw, dw, g.lo_w, g.v, g.pad_w, g.S);
+    if (tap == 0 && threadIdx.x == 0) {
+      uint32_t e;
+      if (g.su * g.sv > 1) {
+        const int q = row / g.C0, c = row - q * g.C0;
+        e = (uint32_t(q / g.sv) << 24) | (uint32_t(q % g.sv) << 16) | uint32_t(c);
+      } else {
+        e = (uint32_t(ph) << 24) | (uint32_t(pw) << 16) | uint32_t(c_col);
+      }
+      coltab[row] = e;
+    }
+  }
+  if (row == 0)
+    for (int grp = threadIdx.x; grp < g.Cgrp; grp += blockDim.x)
+      ctab[tap * g.Cgrp + grp] = (uint32_t(dh) << 24) | (uint32_t(dw) << 16) | uint32_t(grp * 8);
+  for (int cin = threadIdx.x; cin < Cpf; cin += blockDim.x) {
+    float val = 0.0f;
+    if (!g.dgrad) {
+      if (row < g.K && cin < g.C) val = fetch_filter(g, f, row, cin, dh, dw);
+    } else if (row < g.Ncol && cin < g.K && rp >= 0 && sp >= 0) {
+      val = fetch_filter(g, f, cin, c_col, rp, sp);
+    }
+    __nv_bfloat16 h, l;
+    split_bf16(val, h, l);
+    hi[rbase + tap * Cpf + cin] = h;
+    lo[rbase + tap * Cpf + cin] = l;
+  }
+}
+
 // Scatter form of the filter packing: one thread per filter element (read
 // coalesced) computes its single position in the packed GEMM operand; the
 // padding is zeroed by a memset first.  Inverse of pack_filter_kernel's map:
@@ -711,8 +767,8 @@ cudaError_t run_gemm(const ConvProblem& p, Gemm g, const __nv_bfloat16* a_hi,
   auto* ctab = reinterpret_cast<uint32_t*>(b_lo + flt);
   auto* coltab = ctab + pg.KC + 1;
   if (!getenv("DNNP_PACK_SCATTER")) {
-    const dim3 fgrid(unsigned(std::min<int64_t>(ceil_div(pg.Ktot, 256), 8)), unsigned(pg.Np));
-    pack_filter_kernel<<<fgrid, 256, 0, st>>>(pg, f, b_hi, b_lo, ctab, coltab);
+    const dim3 fgrid(unsigned(taps + 1), unsigned(pg.Np));
+    pack_filter_tap_kernel<<<fgrid, 128, 0, st>>>(pg, f, b_hi, b_lo, ctab, coltab, taps);
   } else {
     if ((e = cudaMemsetAsync(b_hi, 0, flt * 4, st)) != cudaSuccess) return e;  // hi and lo planes
     const int64_t nf = int64_t(pg.K) * pg.C0 * pg.R0 * pg.S0;

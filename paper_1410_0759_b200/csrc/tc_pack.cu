@@ -21,16 +21,24 @@ constexpr int kCh = 64;    // channels per slab
 // shared tile: reads are one channel x 32 consecutive pixels per warp
 // instruction (128 B for NCHW), writes are 4 pixels x 8 channel groups per
 // warp instruction (contiguous 16-byte chunks).  Grid-stride over
-// (pixel tile, channel slab) jobs.
+// (pixel tile, channel slab) jobs.  S2D: the packed pixel grid is the
+// space-to-depth grid (H2 x W2 super-pixels, channel c' = (rh*u2 + rw)*C + c
+// reading x[c][h2*u + rh - pad_h][w2*v + rw - pad_w], zero outside).
+struct S2dGeom {
+  int u, v, pad_h, pad_w;
+};
+
+template <bool S2D>
 __global__ void __launch_bounds__(256) pack_act_kernel(View4 v, const float* __restrict__ x, int Cp,
                                                        __nv_bfloat16* __restrict__ hi,
                                                        __nv_bfloat16* __restrict__ lo, int64_t npix,
-                                                       MagicDiv dHW, MagicDiv dW) {
+                                                       MagicDiv dHW, MagicDiv dW, S2dGeom sg) {
   __shared__ float tile[kCh][kPix + 1];
   const int lp = threadIdx.x & 31, lc = threadIdx.x >> 5;  // read role: pixel, channel phase
   const int wp = threadIdx.x >> 3, wg = threadIdx.x & 7;   // write role: pixel, channel group
   const int64_t ntiles = (npix + kPix - 1) / kPix;
   const int nslabs = (Cp + kCh - 1) / kCh;
+  const int Cs = S2D ? sg.u * sg.v * int(v.c) : int(v.c);  // real channels of the packed grid
   for (int64_t job = blockIdx.x; job < ntiles * nslabs; job += gridDim.x) {
     const int64_t pt = job / nslabs;
     const int slab = int(job - pt * nslabs);
@@ -40,13 +48,30 @@ __global__ void __launch_bounds__(256) pack_act_kernel(View4 v, const float* __r
       uint32_t n, rem, h, w;
       mdivmod(uint32_t(pix), dHW, n, rem);
       mdivmod(rem, dW, h, w);
-      const float* src = x + int64_t(n) * v.sn + int64_t(h) * v.sh + int64_t(w) * v.sw +
-                         int64_t(c_lo) * v.sc;
-      const int cvalid = int(v.c - c_lo < nch ? v.c - c_lo : nch);
+      if (!S2D) {
+        const float* src = x + int64_t(n) * v.sn + int64_t(h) * v.sh + int64_t(w) * v.sw +
+                           int64_t(c_lo) * v.sc;
+        const int cvalid = Cs - c_lo < nch ? Cs - c_lo : nch;
 #pragma unroll
-      for (int i = 0; i < kCh / 8; i++) {
-        const int c = lc + 8 * i;
-        tile[c][lp] = c < cvalid ? __ldg(src + int64_t(c) * v.sc) : 0.0f;
+        for (int i = 0; i < kCh / 8; i++) {
+          const int c = lc + 8 * i;
+          tile[c][lp] = c < cvalid ? __ldg(src + int64_t(c) * v.sc) : 0.0f;
+        }
+      } else {
+        const float* src = x + int64_t(n) * v.sn;
+        const int hb = int(h) * sg.u - sg.pad_h, wb = int(w) * sg.v - sg.pad_w;
+#pragma unroll
+        for (int i = 0; i < kCh / 8; i++) {
+          const int cp = c_lo + lc + 8 * i;
+          float val = 0.0f;
+          if (cp < Cs) {
+            const int q = cp / int(v.c), c = cp - q * int(v.c);
+            const int hh = hb + q / sg.v, ww = wb + q % sg.v;
+            if (unsigned(hh) < unsigned(v.h) && unsigned(ww) < unsigned(v.w))
+              val = __ldg(src + int64_t(c) * v.sc + int64_t(hh) * v.sh + int64_t(ww) * v.sw);
+          }
+          tile[lc + 8 * i][lp] = val;
+        }
       }
     }
     __syncthreads();
@@ -189,6 +214,15 @@ cudaError_t pack_act_s2d(const View4& v, const float* x, int u, int vv, int pad_
                          cudaStream_t st) {
   const int64_t npix = v.n * H2 * W2;
   if (npix >= (int64_t(1) << 32)) return cudaErrorInvalidValue;
+  if (getenv("DNNP_S2D_TILE")) {
+    const int64_t jobs = ceil_div(npix, kPix) * ceil_div(Cp, kCh);
+    const unsigned grid = unsigned(std::min<int64_t>(jobs, int64_t(kNumSMs) * 32));
+    pack_act_kernel<true><<<grid, 256, 0, st>>>(v, x, Cp, hi, lo, npix,
+                                                make_magic(uint32_t(H2 * W2)), make_magic(uint32_t(W2)),
+                                                S2dGeom{u, vv, pad_h, pad_w});
+    note_launch();
+    return cudaGetLastError();
+  }
   const size_t row_smem = size_t(W2) * (Cp + 1) * sizeof(float);
   if (getenv("DNNP_S2D_ROWS") && row_smem <= 48 * 1024 && v.n * H2 < (int64_t(1) << 31)) {
     const unsigned grid = unsigned(std::min<int64_t>(v.n * H2, int64_t(kNumSMs) * 8));
@@ -359,8 +393,9 @@ cudaError_t pack_act(const View4& v, const float* x, int Cp, __nv_bfloat16* hi, 
   }
   const int64_t jobs = ceil_div(npix, kPix) * ceil_div(Cp, kCh);
   const unsigned grid = unsigned(std::min<int64_t>(jobs, int64_t(kNumSMs) * 32));
-  pack_act_kernel<<<grid, 256, 0, st>>>(v, x, Cp, hi, lo, npix, make_magic(uint32_t(v.h * v.w)),
-                                        make_magic(uint32_t(v.w)));
+  pack_act_kernel<false><<<grid, 256, 0, st>>>(v, x, Cp, hi, lo, npix,
+                                               make_magic(uint32_t(v.h * v.w)),
+                                               make_magic(uint32_t(v.w)), S2dGeom{1, 1, 0, 0});
   note_launch();
   return cudaGetLastError();
 }
