@@ -385,6 +385,10 @@ struct PackGeom {
   int winH, winW, lo_h, lo_w;
   int Ncol, Np, Ktot, Cgrp, KC;
   int su, sv, C0, R0, S0;  // space-to-depth factors and the original C, R, S
+  // column blocking (TMA path, small GEMM N): GEMM row j covers bw adjacent
+  // output columns, GEMM column = e * Ncol0 + n; the blocked taps along w
+  // (tapW) map to the unblocked tap dw = dwb - e * vstep (valid in [0, Sg)).
+  int tapH, tapW, bw, Ncol0, vstep, Sg;
 };
 
 __device__ __forceinline__ float fetch_filter(const PackGeom& g, const float* __restrict__ f,
@@ -484,33 +488,38 @@ __global__ void __launch_bounds__(128) pack_filter_tap_kernel(PackGeom g, const 
     }
     return;
   }
-  const int nS = g.dgrad ? g.winW : g.S;
-  const int dh = tap / nS, dw = tap - (tap / nS) * nS;
-  int c_col = 0, rp = -1, sp = -1;
+  const int dh = tap / g.tapW, dwb = tap - (tap / g.tapW) * g.tapW;
+  const int e = row / g.Ncol0, r0 = row - e * g.Ncol0;  // column block, unblocked column
+  const int dw = dwb - e * g.vstep;
+  const bool tap_ok = row < g.Ncol && dw >= 0 && dw < g.Sg;
+  int c_col = 0, rp = -1, sp = -1, ph = 0, pw = 0;
   if (g.dgrad && row < g.Ncol) {
-    const int phase = row / g.C;
-    c_col = row - phase * g.C;
-    const int ph = phase / g.v, pw = phase - (phase / g.v) * g.v;
+    const int phase = r0 / g.C;
+    c_col = r0 - phase * g.C;
+    ph = phase / g.v;
+    pw = phase - ph * g.v;
     rp = phase_tap(ph, dh, g.lo_h, g.u, g.pad_h, g.R);
-    sp = phase_tap(pw, dw, g.lo_w, g.v, g.pad_w, g.S);
-    if (tap == 0 && threadIdx.x == 0) {
-      uint32_t e;
-      if (g.su * g.sv > 1) {
-        const int q = row / g.C0, c = row - q * g.C0;
-        e = (uint32_t(q / g.sv) << 24) | (uint32_t(q % g.sv) << 16) | uint32_t(c);
-      } else {
-        e = (uint32_t(ph) << 24) | (uint32_t(pw) << 16) | uint32_t(c_col);
-      }
-      coltab[row] = e;
+    sp = tap_ok ? phase_tap(pw, dw, g.lo_w, g.v, g.pad_w, g.S) : -1;
+  }
+  if (tap == 0 && threadIdx.x == 0 && row < g.Ncol && (g.dgrad || g.bw > 1)) {
+    uint32_t eh, ew, ec;
+    if (!g.dgrad) {
+      eh = 0, ew = uint32_t(e), ec = uint32_t(r0);
+    } else if (g.su * g.sv > 1) {  // space-to-depth column (rh, rw, c)
+      const int q = r0 / g.C0;
+      eh = uint32_t(q / g.sv), ew = uint32_t(e * g.sv + q % g.sv), ec = uint32_t(r0 - q * g.C0);
+    } else {
+      eh = uint32_t(ph), ew = uint32_t(e * g.v + pw), ec = uint32_t(c_col);
     }
+    coltab[row] = (eh << 24) | (ew << 16) | ec;
   }
   if (row == 0)
     for (int grp = threadIdx.x; grp < g.Cgrp; grp += blockDim.x)
-      ctab[tap * g.Cgrp + grp] = (uint32_t(dh) << 24) | (uint32_t(dw) << 16) | uint32_t(grp * 8);
+      ctab[tap * g.Cgrp + grp] = (uint32_t(dh) << 24) | (uint32_t(dwb) << 16) | uint32_t(grp * 8);
   for (int cin = threadIdx.x; cin < Cpf; cin += blockDim.x) {
     float val = 0.0f;
     if (!g.dgrad) {
-      if (row < g.K && cin < g.C) val = fetch_filter(g, f, row, cin, dh, dw);
+      if (tap_ok && r0 < g.K && cin < g.C) val = fetch_filter(g, f, r0, cin, dh, dw);
     } else if (row < g.Ncol && cin < g.K && rp >= 0 && sp >= 0) {
       val = fetch_filter(g, f, cin, c_col, rp, sp);
     }
@@ -747,7 +756,7 @@ cudaError_t run_gemm(const ConvProblem& p, Gemm g, const __nv_bfloat16* a_hi,
   const int CB = g.tma ? pick_cb(Cp) : 8;
   const int Cpf = int(ceil_div(Cp, CB) * CB);  // filter columns per tap (channel blocks padded)
   pg.Cgrp = Cpf / 8;
-  const int taps = pg.dgrad ? pg.winH * pg.winW : pg.R * pg.S;
+  const int taps = pg.tapH * pg.tapW;
   pg.KC = taps * pg.Cgrp;
   const int depth = g.tma ? kTK : kBK;
   const int nkb = int(ceil_div(int64_t(pg.KC) * 8, depth));
@@ -766,7 +775,7 @@ cudaError_t run_gemm(const ConvProblem& p, Gemm g, const __nv_bfloat16* a_hi,
   auto* b_lo = b_hi + flt;
   auto* ctab = reinterpret_cast<uint32_t*>(b_lo + flt);
   auto* coltab = ctab + pg.KC + 1;
-  if (!getenv("DNNP_PACK_SCATTER")) {
+  if (!getenv("DNNP_PACK_SCATTER") || pg.bw > 1) {
     const dim3 fgrid(unsigned(taps + 1), unsigned(pg.Np));
     pack_filter_tap_kernel<<<fgrid, 128, 0, st>>>(pg, f, b_hi, b_lo, ctab, coltab, taps);
   } else {
@@ -814,7 +823,7 @@ cudaError_t run_gemm(const ConvProblem& p, Gemm g, const __nv_bfloat16* a_hi,
     prm.u = g.u;
     prm.v = g.v;
     prm.nCB = Cpf / CB;
-    prm.tapW = pg.dgrad ? pg.winW : pg.S;
+    prm.tapW = pg.tapW;
     prm.KCH = taps * prm.nCB;
     prm.nkb = nkb;
     prm.Cext = Cp;
@@ -1099,6 +1108,47 @@ cudaError_t run_tc(bool dgrad, const ConvProblem& p, const float* in, const View
                                       Nimg * g.OH * g.OW);
     const int Cin = int(dgrad ? p.K : p.C);
     Cp = int(ceil_div(Cin, g.tma ? 16 : 8) * (g.tma ? 16 : 8));
+  }
+  pg.tapH = dgrad ? pg.winH : pg.R;
+  pg.tapW = dgrad ? pg.winW : pg.S;
+  pg.Sg = pg.tapW;
+  pg.bw = 1;
+  pg.Ncol0 = pg.Ncol;
+  pg.vstep = dgrad ? 1 : g.v;
+  // Column blocking for small GEMM N (conv2 bwd-data C=64): one GEMM row computes bw = 2
+  // adjacent output columns, doubling N; the A operand (im2col, the bulk of
+  // the TMA traffic) shrinks to (S + v) / (2 S) of its bytes.
+  // (measured: helps the unit-stride bwd-data of conv2, 233 -> 204 us; not the
+  // space-to-depth conv1 passes, whose epilogue then dominates)
+  const bool blockable = g.tma && pg.Ncol <= 64 && !s2d && g.out_mode == 0 &&
+                         (env_off("DNNP_TC_BLOCK") || dgrad) && !env_off("DNNP_TC_NO_BLOCK");
+  if (blockable) {
+    const int bw = 2;
+    Gemm gb = g;
+    PackGeom& pb = gb.pg;
+    pb.bw = bw;
+    pb.Ncol = bw * pg.Ncol;
+    pb.tapW = pg.tapW + (bw - 1) * pg.vstep;
+    gb.OW = int(ceil_div(g.OW, bw));
+    gb.v = g.v * bw;
+    if (!dgrad) {
+      gb.out_mode = 1;
+      gb.o_u = 1;
+      gb.o_v = bw;
+      gb.o_H = g.OH;
+      gb.o_W = g.OW;
+      gb.o_ph = gb.o_pw = 0;
+    } else if (s2d) {
+      gb.o_v = g.o_v * bw;
+    } else {
+      gb.out_mode = 1;
+      gb.o_u = 1;
+      gb.o_v = bw;
+      gb.o_H = int(p.H);
+      gb.o_W = int(p.W);
+      gb.o_ph = gb.o_pw = 0;
+    }
+    if (tma_geometry_ok(gb, IH, IW, pb.tapH, pb.tapW, Nimg * gb.OH * gb.OW)) g = gb;
   }
   const size_t act = size_t(p.N) * IH * IW * Cp;
   Workspace ws(st);

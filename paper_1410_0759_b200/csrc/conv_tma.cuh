@@ -28,7 +28,8 @@
 // epilogue of one work item overlaps the main loop of the next.
 #pragma once
 
-constexpr int kTmaThreads = 6 * 32;
+constexpr int kTmaThreads = 10 * 32;  // TMA warp, MMA warp, 8 epilogue warps
+constexpr int kColCache = 512;        // mode-1 column table cached in shared memory
 constexpr int kTK = 64;  // reduction depth of one stage (4 k-steps of 16)
 
 struct TmaParams {
@@ -68,11 +69,13 @@ struct TCfg {
   static constexpr int A_BYTES = SUB * A_SUB;
   static constexpr int B_BYTES = SUB * B_SUB;
   static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;  // per CTA
-  static constexpr int STAGES =
-      (225 * 1024 - 2048) / STAGE_BYTES > 8 ? 8 : (225 * 1024 - 2048) / STAGE_BYTES;
+  static constexpr int COLTAB_BYTES = kColCache * 12;  // int64 offset + packed (ph, pw)
+  static constexpr int STAGES = (225 * 1024 - 2048 - COLTAB_BYTES) / STAGE_BYTES > 8
+                                    ? 8
+                                    : (225 * 1024 - 2048 - COLTAB_BYTES) / STAGE_BYTES;
   static constexpr int TMEM_COLS =
       2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512));
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256 + COLTAB_BYTES;
 };
 
 template <int CB>
@@ -153,6 +156,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1) conv_tma_kernel(const __grid_c
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   int* sk_flag = reinterpret_cast<int*>(tmem_slot + 1);
+  long long* col_off = reinterpret_cast<long long*>(smem + S * C::STAGE_BYTES + 256);
+  int* col_hw = reinterpret_cast<int*>(col_off + kColCache);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = NC == 2 ? ptx::cluster_ctarank() : 0u;
@@ -167,7 +172,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) conv_tma_kernel(const __grid_c
       }
       for (int b = 0; b < 2; b++) {
         ptx::mbar_init(&tfull[b], 1);
-        ptx::mbar_init(&tempty[b], 4 * NC);  // one arrival per epilogue warp of each CTA
+        ptx::mbar_init(&tempty[b], 8 * NC);  // one arrival per epilogue warp of each CTA
       }
       ptx::fence_mbar_init();
     }
@@ -301,9 +306,22 @@ __global__ void __launch_bounds__(kTmaThreads, 1) conv_tma_kernel(const __grid_c
     }
   } else {
     // ================================================ epilogue
-    const int ew = warp & 3;  // TMEM lane quadrant accessible to this warp
+    // 8 warps: quadrant ew = warp % 4 holds TMEM lanes (rows) 32*ew.., the
+    // two warp sets split the 32-column chunks between them
+    const int ew = warp & 3, es = (warp - 2) >> 2;
     const int r = ew * 32 + lane;
-    const int et = threadIdx.x - 64;  // 0..127 over the four epilogue warps
+    const int et = threadIdx.x - 64;  // 0..255 over the eight epilogue warps
+    const bool ctab_smem = P.out_mode == 1 && P.Ncol <= kColCache;
+    if (ctab_smem) {
+      // column -> (offset of (c, ph, pw) from the row base, (ph, pw)) in shared memory
+      for (int c = et; c < P.Ncol; c += 256) {
+        const uint32_t e = __ldg(P.coltab + c);
+        const int ph = int(e >> 24), pw = int((e >> 16) & 255);
+        col_off[c] = int64_t(e & 0xFFFF) * P.o_sc + int64_t(ph) * P.o_sh + int64_t(pw) * P.o_sw;
+        col_hw[c] = (ph << 16) | pw;
+      }
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+    }
     int lt = 0;
     while (wi.next(tile, kb0, kb1, piece, np)) {
       const int buf = lt & 1;
@@ -316,7 +334,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) conv_tma_kernel(const __grid_c
         mdivmod(uint32_t(m), P.dOHW, img, rem);
         mdivmod(rem, P.dOW, oh, ow);
       }
-      const bool etr = P.trace && blockIdx.x == 0 && r == 0 && lt < 64;
+      const bool etr = P.trace && blockIdx.x == 0 && r == 0 && es == 0 && lt < 64;
       if (etr) P.trace[4096 + lt * 4 + 0] = clock64();
       ptx::mbar_wait(&tfull[buf], (lt >> 1) & 1);
       if (etr) P.trace[4096 + lt * 4 + 1] = clock64();
@@ -331,7 +349,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) conv_tma_kernel(const __grid_c
         // column-major [col][row] so each warp store / load is 128 contiguous bytes
         float* mine = part + int64_t(piece) * (kBM * BN) + r;
 #pragma unroll 1
-        for (int c0 = 0; c0 < BN; c0 += 32) {
+        for (int c0 = 32 * es; c0 < BN; c0 += 64) {
           uint32_t v[32];
           ptx::tmem_ld32(tmem_base + (uint32_t(ew * 32) << 16) + uint32_t(buf * BN + c0), v);
           ptx::tmem_ld_wait();
@@ -339,23 +357,25 @@ __global__ void __launch_bounds__(kTmaThreads, 1) conv_tma_kernel(const __grid_c
           for (int i = 0; i < 32; i++) __stcg(mine + (c0 + i) * kBM, __uint_as_float(v[i]));
         }
         __threadfence();
-        asm volatile("bar.sync 1, 128;" ::: "memory");
+        asm volatile("bar.sync 1, 256;" ::: "memory");
         if (et == 0) {
           const int prev = atomicAdd(P.skcnt + slot, 1);
           const bool last = prev == np - 1;
           if (last) P.skcnt[slot] = 0;  // ready for the next launch
           *sk_flag = last ? 1 : 0;
         }
-        asm volatile("bar.sync 1, 128;" ::: "memory");
+        asm volatile("bar.sync 1, 256;" ::: "memory");
         finisher = *sk_flag != 0;
         if (finisher) __threadfence();
       }
       if (finisher) {
+        // mode 0: row base at the output pixel; mode 1: at (oh*o_u - o_ph, ow*o_v - o_pw)
+        const int hb = int(oh) * P.o_u - P.o_ph, wb = int(ow) * P.o_v - P.o_pw;
         const int64_t rowoff =
             P.out_mode == 0 ? int64_t(img) * P.o_sn + int64_t(oh) * P.o_sh + int64_t(ow) * P.o_sw
-                            : int64_t(img) * P.o_sn;
+                            : int64_t(img) * P.o_sn + int64_t(hb) * P.o_sh + int64_t(wb) * P.o_sw;
 #pragma unroll 1
-        for (int c0 = 0; c0 < BN; c0 += 32) {
+        for (int c0 = 32 * es; c0 < BN; c0 += 64) {
           const int cbase = n0 + c0;
           if (cbase >= P.Ncol) break;  // warp-uniform: padded columns are never loaded
           uint32_t v[32];
@@ -393,17 +413,34 @@ __global__ void __launch_bounds__(kTmaThreads, 1) conv_tma_kernel(const __grid_c
                 *dst = val;
               }
             }
+          } else if (ctab_smem) {
+#pragma unroll
+            for (int i = 0; i < 32; i++) {
+              const int col = cbase + i;
+              if (col < P.Ncol) {
+                const int hw = col_hw[col];
+                if (unsigned(hb + (hw >> 16)) < unsigned(P.o_H) &&
+                    unsigned(wb + (hw & 0xFFFF)) < unsigned(P.o_W)) {
+                  float* dst = P.out + rowoff + col_off[col];
+                  float val = __uint_as_float(v[i]);
+                  if (!P.plain) {
+                    val = __fmul_rn(val, P.alpha);
+                    if (P.beta != 0.0f) val = __fadd_rn(__fmul_rn(*dst, P.beta), val);
+                  }
+                  *dst = val;
+                }
+              }
+            }
           } else {
 #pragma unroll
             for (int i = 0; i < 32; i++) {
               const int col = cbase + i;
               if (col < P.Ncol) {
                 const uint32_t e = __ldg(P.coltab + col);
-                const int h = int(oh) * P.o_u + int(e >> 24) - P.o_ph;
-                const int w = int(ow) * P.o_v + int((e >> 16) & 255) - P.o_pw;
-                if (unsigned(h) < unsigned(P.o_H) && unsigned(w) < unsigned(P.o_W)) {
-                  float* dst = P.out + rowoff + int64_t(e & 0xFFFF) * P.o_sc + int64_t(h) * P.o_sh +
-                               int64_t(w) * P.o_sw;
+                const int ph = int(e >> 24), pw = int((e >> 16) & 255);
+                if (unsigned(hb + ph) < unsigned(P.o_H) && unsigned(wb + pw) < unsigned(P.o_W)) {
+                  float* dst = P.out + rowoff + int64_t(e & 0xFFFF) * P.o_sc + int64_t(ph) * P.o_sh +
+                               int64_t(pw) * P.o_sw;
                   float val = __fmul_rn(__uint_as_float(v[i]), P.alpha);
                   if (P.beta != 0.0f) val = __fadd_rn(__fmul_rn(*dst, P.beta), val);
                   *dst = val;
