@@ -207,6 +207,63 @@ __global__ void __launch_bounds__(256) pack_act_s2d_row_kernel(View4 v, const fl
   }
 }
 
+// Space-to-depth fast path for dense NCHW rows (sw == 1, sh == W, W % 4 == 0):
+// one block per output row (n, h'): the C x u input rows are read with
+// 16-byte loads into shared memory (zero margins for the padding), then the
+// W' x Cp output row -- contiguous in the packed plane -- is written with
+// 16-byte stores.
+__global__ void __launch_bounds__(256) pack_act_s2d_dense_kernel(View4 v, const float* __restrict__ x,
+                                                                 int u, int vv, int pad_h, int pad_w,
+                                                                 int H2, int W2, int Cp,
+                                                                 __nv_bfloat16* __restrict__ hi,
+                                                                 __nv_bfloat16* __restrict__ lo) {
+  extern __shared__ float srow[];  // [C*u][SW], SW = W2*v rounded up to 4
+  const int C = int(v.c), W = int(v.w);
+  const int SW = (W2 * vv + 3) & ~3;
+  const int nrow = C * u;
+  const int row = blockIdx.x;
+  const int n = row / H2, h2 = row - n * H2;
+  // zero the whole staging row block, then drop the in-range input in
+  for (int t = threadIdx.x; t < nrow * SW; t += blockDim.x) srow[t] = 0.0f;
+  __syncthreads();
+  const int W4 = W >> 2;
+  for (int t = threadIdx.x; t < nrow * W4; t += blockDim.x) {
+    const int q = t / W4, w4 = t - q * W4;
+    const int c = q / u, rh = q - c * u;
+    const int h = h2 * u + rh - pad_h;
+    if (unsigned(h) >= unsigned(v.h)) continue;
+    const float4 val = __ldg(reinterpret_cast<const float4*>(x + int64_t(n) * v.sn + int64_t(c) * v.sc +
+                                                              int64_t(h) * v.sh) + w4);
+    const int wp = w4 * 4 + pad_w;  // staging column of input column 4*w4
+    float* d = srow + q * SW;
+    if (wp + 0 < SW) d[wp + 0] = val.x;
+    if (wp + 1 < SW) d[wp + 1] = val.y;
+    if (wp + 2 < SW) d[wp + 2] = val.z;
+    if (wp + 3 < SW) d[wp + 3] = val.w;
+  }
+  __syncthreads();
+  const int groups = Cp / 8, Cs = u * vv * C;
+  const int64_t obase = int64_t(row) * W2 * Cp;
+  for (int t = threadIdx.x; t < W2 * groups; t += blockDim.x) {
+    const int w2 = t / groups, g = t - w2 * groups;
+    __align__(16) __nv_bfloat16 vh[8], vl[8];
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+      const int cp = g * 8 + k;
+      float val = 0.0f;
+      if (cp < Cs) {
+        const int qq = cp / C, c = cp - qq * C;  // qq = rh * v + rw
+        const int rh = qq / vv, rw = qq - rh * vv;
+        val = srow[(c * u + rh) * SW + w2 * vv + rw];
+      }
+      split_bf16(val, vh[k], vl[k]);
+    }
+    const int64_t o = obase + int64_t(w2) * Cp + g * 8;
+    *reinterpret_cast<uint4*>(hi + o) = *reinterpret_cast<const uint4*>(vh);
+    *reinterpret_cast<uint4*>(lo + o) = *reinterpret_cast<const uint4*>(vl);
+  }
+}
+
 }  // namespace
 
 cudaError_t pack_act_s2d(const View4& v, const float* x, int u, int vv, int pad_h, int pad_w,
@@ -214,6 +271,20 @@ cudaError_t pack_act_s2d(const View4& v, const float* x, int u, int vv, int pad_
                          cudaStream_t st) {
   const int64_t npix = v.n * H2 * W2;
   if (npix >= (int64_t(1) << 32)) return cudaErrorInvalidValue;
+  {
+    const int SW = (W2 * vv + 3) & ~3;
+    const size_t sm = size_t(v.c) * u * SW * sizeof(float);
+    const bool dense = v.sw == 1 && v.sh == v.w && v.w % 4 == 0 && v.h * v.w <= v.sc &&
+                       (reinterpret_cast<uintptr_t>(x) & 15) == 0 && (v.sn % 4) == 0 &&
+                       (v.sc % 4) == 0 && sm <= 48 * 1024 && W2 * vv >= v.w + pad_w &&
+                       getenv("DNNP_S2D_DENSE") != nullptr;
+    if (dense && v.n * H2 < (int64_t(1) << 31)) {
+      pack_act_s2d_dense_kernel<<<unsigned(v.n * H2), 256, sm, st>>>(v, x, u, vv, pad_h, pad_w, H2,
+                                                                     W2, Cp, hi, lo);
+      note_launch();
+      return cudaGetLastError();
+    }
+  }
   if (getenv("DNNP_S2D_TILE")) {
     const int64_t jobs = ceil_div(npix, kPix) * ceil_div(Cp, kCh);
     const unsigned grid = unsigned(std::min<int64_t>(jobs, int64_t(kNumSMs) * 32));

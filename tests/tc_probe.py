@@ -17,6 +17,8 @@ SHAPES = [
     # N C H W K R S u pad
     (1, 8, 8, 8, 32, 3, 3, 1, 1),
     (2, 3, 31, 31, 16, 11, 11, 4, 2),
+    (2, 3, 32, 36, 64, 11, 11, 4, 2),
+    (3, 3, 40, 40, 64, 11, 11, 4, 2),
     (2, 16, 15, 15, 24, 5, 5, 1, 2),
     (3, 24, 9, 9, 40, 3, 3, 1, 1),
     (1, 64, 8, 8, 72, 3, 3, 1, 1),
