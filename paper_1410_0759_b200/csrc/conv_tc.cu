@@ -856,10 +856,10 @@ cudaError_t run_gemm(const ConvProblem& p, Gemm g, const __nv_bfloat16* a_hi,
       const bool use_sk = getenv("DNNP_TC_SK") && !getenv("DNNP_TC_NO_SK") && W >= 1 && R > 0 && double(R) / G < 0.85 &&
                           int64_t(R) * nkb < (int64_t(1) << 30);
       if (use_sk) {
-        const int U = R * nkb;
+        const int U = R * nkb, G2 = std::min(G, U);
         int maxp = 1;
         for (int tl = 0; tl < R; tl++) {
-          const int first = sk_owner(tl * nkb, U, G), last = sk_owner(tl * nkb + nkb - 1, U, G);
+          const int first = sk_owner(tl * nkb, U, G2), last = sk_owner(tl * nkb + nkb - 1, U, G2);
           maxp = std::max(maxp, last - first + 1);
         }
         const size_t part_bytes = size_t(R) * nc * maxp * kBM * bn * sizeof(float);

@@ -85,7 +85,8 @@ __device__ __forceinline__ uint64_t tma_kdesc(uint32_t addr) {
   else return ptx::desc_kmajor_sw32(addr);
 }
 
-// Owner cluster of stream-K unit x: the largest j with floor(j*U/G) <= x.
+// Owner cluster of stream-K unit x: the largest j with floor(j*U/G) <= x
+// (G <= U, so every cluster owns at least one unit).
 __host__ __device__ __forceinline__ int sk_owner(int x, int U, int G) {
   int j = int((int64_t(x) * G) / U);
   while (j + 1 < G && int((int64_t(j + 1) * U) / G) <= x) j++;
@@ -96,7 +97,7 @@ __host__ __device__ __forceinline__ int sk_owner(int x, int U, int G) {
 // The sequence of work items of one cluster: (tile, k-block range, piece of
 // the tile, pieces of the tile); every role of the cluster walks it alike.
 struct WorkIter {
-  int cid, G, nkb, tiles, sk, W, U;
+  int cid, G, nkb, tiles, sk, W, U, G2;
   int i, u, uend;
   __device__ void init(const TmaParams& P, int cid_, int G_) {
     cid = cid_;
@@ -107,8 +108,11 @@ struct WorkIter {
     W = P.W;
     U = P.U;
     i = 0;
-    u = sk ? int((int64_t(cid) * U) / G) : 0;
-    uend = sk ? int((int64_t(cid + 1) * U) / G) : 0;
+    // the last-wave units are spread over G2 = min(G, U) clusters so that
+    // every participating cluster owns >= 1 unit (consecutive piece numbers)
+    G2 = min(G, U);
+    u = (sk && cid < G2) ? int((int64_t(cid) * U) / G2) : 0;
+    uend = (sk && cid < G2) ? int((int64_t(cid + 1) * U) / G2) : 0;
   }
   __device__ bool next(int& tile, int& kb0, int& kb1, int& piece, int& np) {
     if (!sk) {
@@ -135,7 +139,7 @@ struct WorkIter {
     tile = W * G + tl;
     kb0 = u - tl * nkb;
     kb1 = min(nkb, kb0 + (uend - u));
-    const int first = sk_owner(tl * nkb, U, G), last = sk_owner(tl * nkb + nkb - 1, U, G);
+    const int first = sk_owner(tl * nkb, U, G2), last = sk_owner(tl * nkb + nkb - 1, U, G2);
     piece = cid - first;
     np = last - first + 1;
     u += kb1 - kb0;

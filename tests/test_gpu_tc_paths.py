@@ -1,0 +1,187 @@
+"""GPU parity of every variant of the tensor-core convolution path against the
+C oracle (fp32, normalised error <= 1e-4, the test_acceptance.py:91-96
+metric).  Variants are selected per call through the library's environment
+switches (read on every call):
+
+  space-to-depth (strided, few channels)   DNNP_TC_NO_S2D
+  CTA pairs / single CTAs                  DNNP_TC_NC=2 / DNNP_TC_NC=1
+  stream-K last wave                       DNNP_TC_SK=1 (+ DNNP_TC_NC / DNNP_TC_BN)
+  column blocking (unit-stride small N)    DNNP_TC_NO_BLOCK
+  cp.async gather kernel (no TMA)          DNNP_TC_NO_TMA
+and through the problem shape: 16/32/64-channel TMA blocks, super-pixel
+strided bwd-data, strided output views with alpha/beta/accumulate."""
+import contextlib
+import os
+
+import numpy as np
+import pytest
+
+import oracle as orc
+import paper_1410_0759_b200 as dp
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-4
+
+
+@contextlib.contextmanager
+def env(**kv):
+    old = {k: os.environ.get(k) for k in kv}
+    try:
+        for k, v in kv.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = str(v)
+        yield
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
+def rand_view(rng, n, c, h, w, layout="nchw", fill=None):
+    import torch
+    desc = dp.make_desc(n, c, h, w, layout=layout)
+    buf = rng.uniform(-0.5, 0.5, desc.max_offset() + 1).astype(np.float32)
+    if fill is not None:
+        buf[:] = fill
+    g = np.array([n, c, h, w, *desc.strides], dtype=np.int64)
+    t = torch.from_numpy(buf.copy()).cuda()
+    return dp.TensorView(desc, t), buf, g, t
+
+
+def run_case(shape, passes=("fwd", "bwd_data", "bwd_filter"), layout_in="nchw",
+             layout_out="nchw", mode="convolution", seed=0, alpha=1.0, beta=0.0,
+             accumulate=False):
+    import torch
+    rng = np.random.default_rng(seed)
+    N, C, H, W, K, R, S, u, v, ph, pw = shape
+    cd = dp.ConvDesc(u, v, ph, pw, mode, accumulate)
+    cg = [u, v, ph, pw, 0 if mode == "convolution" else 1, 1 if accumulate else 0]
+    P, Q = dp.output_extent(H, R, u, ph), dp.output_extent(W, S, v, pw)
+    f = rng.uniform(-0.5, 0.5, K * C * R * S).astype(np.float32)
+    fv = dp.FilterView(dp.make_filter_desc(K, C, R, S), torch.from_numpy(f).cuda())
+    errs = {}
+    if "fwd" in passes:
+        xv, x, xg, _ = rand_view(rng, N, C, H, W, layout_in)
+        yv, y0, yg, yt = rand_view(rng, N, K, P, Q, layout_out)
+        dp.conv_forward(xv, fv, cd, "implicit", yv, alpha=alpha, beta=beta)
+        ref = y0.copy()
+        orc.conv_forward(xg, x, [K, C, R, S], f, cg, yg, ref, alpha=alpha, beta=beta, threads=8)
+        errs["fwd"] = orc.rel_err(yt.cpu().numpy(), ref)
+    if "bwd_data" in passes:
+        dyv, dy, dyg, _ = rand_view(rng, N, K, P, Q, layout_in)
+        dxv, dx0, dxg, dxt = rand_view(rng, N, C, H, W, layout_out)
+        dp.conv_backward_data(dyv, fv, cd, "implicit", dxv)
+        ref = dx0.copy()
+        orc.conv_backward_data([K, C, R, S], f, dyg, dy, cg, dxg, ref)
+        errs["bwd_data"] = orc.rel_err(dxt.cpu().numpy(), ref)
+    if "bwd_filter" in passes:
+        xv, x, xg, _ = rand_view(rng, N, C, H, W, layout_in)
+        dyv, dy, dyg, _ = rand_view(rng, N, K, P, Q, layout_out)
+        df0 = rng.uniform(-0.5, 0.5, K * C * R * S).astype(np.float32)
+        dft = torch.from_numpy(df0.copy()).cuda()
+        dfv = dp.FilterView(dp.make_filter_desc(K, C, R, S), dft)
+        dp.conv_backward_filter(dyv, xv, cd, "implicit", dfv)
+        ref = df0.copy()
+        orc.conv_backward_filter(xg, x, dyg, dy, cg, [K, C, R, S], ref, threads=8)
+        errs["bwd_filter"] = orc.rel_err(dft.cpu().numpy(), ref)
+    return errs
+
+
+def check(errs):
+    bad = {k: v for k, v in errs.items() if not v <= TOL}
+    assert not bad, errs
+
+
+#       N  C   H   W   K   R   S  u  v ph pw
+S2D_SHAPES = [
+    (2, 3, 31, 31, 16, 11, 11, 4, 4, 2, 2),    # ragged width (per-pixel space-to-depth pack)
+    (2, 3, 32, 36, 64, 11, 11, 4, 4, 2, 2),    # W % 4 == 0
+    (3, 4, 20, 20, 24, 5, 5, 2, 2, 2, 2),      # stride 2, 16 phase channels
+    (2, 2, 17, 23, 40, 7, 5, 3, 2, 1, 2),      # anisotropic stride / filter / padding
+]
+
+
+@pytest.mark.parametrize("shape", S2D_SHAPES)
+@pytest.mark.parametrize("mode", ["convolution", "cross_correlation"])
+def test_space_to_depth(shape, mode):
+    check(run_case(shape, mode=mode, seed=1))
+    with env(DNNP_TC_NO_S2D=1):
+        check(run_case(shape, mode=mode, seed=1))
+
+
+@pytest.mark.parametrize("shape", [
+    (2, 32, 13, 13, 48, 3, 3, 2, 2, 1, 1),     # super-pixel bwd-data, 4 phases
+    (1, 40, 15, 14, 24, 5, 4, 3, 2, 2, 1),     # 6 phases, ragged image
+])
+def test_strided_super_pixel(shape):
+    check(run_case(shape, seed=2))
+
+
+@pytest.mark.parametrize("block", [None, 1])
+@pytest.mark.parametrize("shape", [
+    (2, 64, 15, 15, 96, 5, 5, 1, 1, 2, 2),     # conv2-like bwd-data, N = 64 -> blocked 128
+    (3, 16, 9, 11, 32, 3, 3, 1, 1, 1, 1),      # odd output width: ragged last block
+])
+def test_column_blocking(shape, block):
+    with env(DNNP_TC_NO_BLOCK=block):
+        check(run_case(shape, seed=3))
+
+
+@pytest.mark.parametrize("nc", [1, 2])
+@pytest.mark.parametrize("shape", [
+    (4, 64, 14, 14, 192, 3, 3, 1, 1, 1, 1),
+    (2, 96, 13, 13, 256, 3, 3, 1, 1, 1, 1),
+])
+def test_cta_pairs(shape, nc):
+    with env(DNNP_TC_NC=nc):
+        check(run_case(shape, seed=4))
+
+
+@pytest.mark.parametrize("cin", [16, 24, 40])  # 16 / 32 / 64-channel TMA blocks (40 -> OOB fill)
+def test_channel_blocks(cin):
+    check(run_case((2, cin, 10, 12, 32, 3, 3, 1, 1, 1, 1), seed=5))
+
+
+def test_stream_k_last_wave():
+    # 160 row tiles of 128 on 148 persistent CTAs: 12-tile last wave split along K
+    shape = (20, 32, 32, 32, 64, 3, 3, 1, 1, 1, 1)
+    with env(DNNP_TC_SK=1, DNNP_TC_NC=1, DNNP_TC_BN=64):
+        check(run_case(shape, passes=("fwd", "bwd_data"), seed=6))
+    with env(DNNP_TC_SK=1, DNNP_TC_NC=2, DNNP_TC_BN=64):
+        check(run_case(shape, passes=("fwd",), seed=6))
+
+
+@pytest.mark.parametrize("shape", [
+    (2, 3, 31, 31, 16, 11, 11, 4, 4, 2, 2),
+    (2, 16, 15, 15, 24, 5, 5, 1, 1, 2, 2),
+    (2, 32, 13, 13, 48, 3, 3, 2, 2, 1, 1),
+])
+def test_cp_async_fallback(shape):
+    with env(DNNP_TC_NO_TMA=1):
+        check(run_case(shape, seed=7))
+
+
+@pytest.mark.parametrize("lin,lout", [("nhwc", "nchw"), ("nchw", "nhwc"), ("nhwc", "nhwc")])
+def test_layouts(lin, lout):
+    check(run_case((2, 24, 11, 9, 40, 3, 3, 1, 1, 1, 1), layout_in=lin, layout_out=lout, seed=8))
+    check(run_case((2, 3, 32, 36, 64, 11, 11, 4, 4, 2, 2), layout_in=lin, layout_out=lout, seed=8))
+
+
+@pytest.mark.parametrize("alpha,beta", [(0.5, 0.0), (2.0, -1.5), (1.0, 1.0)])
+def test_alpha_beta(alpha, beta):
+    check(run_case((2, 24, 11, 9, 40, 3, 3, 1, 1, 1, 1), passes=("fwd",), alpha=alpha, beta=beta,
+                   seed=9))
+    check(run_case((2, 3, 32, 36, 64, 11, 11, 4, 4, 2, 2), passes=("fwd",), alpha=alpha,
+                   beta=beta, seed=9))
+
+
+def test_accumulate_all_passes():
+    check(run_case((2, 24, 11, 9, 40, 3, 3, 1, 1, 1, 1), accumulate=True, seed=10))
+    check(run_case((2, 3, 32, 36, 64, 11, 11, 4, 4, 2, 2), accumulate=True, seed=10))
+    check(run_case((2, 64, 15, 15, 96, 5, 5, 1, 1, 2, 2), passes=("bwd_data",), accumulate=True,
+                   seed=10))
