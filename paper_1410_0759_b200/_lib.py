@@ -29,6 +29,8 @@ _SIGS = {
     "dnnp_status_string": [ctypes.c_int],
     "dnnp_last_error": [],
     "dnnp_kernel_launch_count": [],
+    "dnnp_kernel_timing": [ctypes.c_int],
+    "dnnp_kernel_times": [ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_int), ctypes.c_int],
     "dnnp_create": [ctypes.POINTER(vp)],
     "dnnp_destroy": [vp],
     "dnnp_set_threads": [vp, c_i64],
@@ -140,6 +142,20 @@ def get_math():
 
 def kernel_launch_count():
     return int(lib().dnnp_kernel_launch_count())
+
+
+def kernel_timing(enable=True):
+    """Start (clearing) or stop CUDA-event timing of the main GEMM kernels."""
+    lib().dnnp_kernel_timing(1 if enable else 0)
+
+
+def kernel_times():
+    """[(ms, tag), ...] of the main GEMM kernels timed since kernel_timing(True)."""
+    n = int(lib().dnnp_kernel_times(None, None, 0))
+    ms = (ctypes.c_float * max(n, 1))()
+    tags = (ctypes.c_int * max(n, 1))()
+    lib().dnnp_kernel_times(ms, tags, n)
+    return [(float(ms[i]), int(tags[i])) for i in range(n)]
 
 
 class TensorDescHandle:

@@ -608,7 +608,9 @@ cudaError_t launch_gemm(const TcParams& prm, cudaStream_t st) {
     attr_dev = dev;
   }
   const unsigned grid = unsigned(std::min<int64_t>(prm.tiles, kNumSMs));
+  ktime_begin(st, 3);
   conv_tc_kernel<BN><<<grid, kThreads, CC::SMEM, st>>>(prm);
+  ktime_end(st);
   note_launch();
   return cudaGetLastError();
 }
@@ -649,7 +651,9 @@ cudaError_t launch_tma(const TmaParams& prm, cudaStream_t st) {
     fprintf(stderr, "DIAG conv_tma<%d,%d,%d> smem=%d grid=%d maxActiveClusters=%d (%s)\n", BN, CB, NC,
             CC::SMEM, clusters * NC, ncl, cudaGetErrorString(qe));
   }
+  ktime_begin(st, 1);
   cudaError_t e = cudaLaunchKernelEx(&cfg, conv_tma_kernel<BN, CB, NC>, prm);
+  ktime_end(st);
   note_launch();
   if (e != cudaSuccess) return e;
   return cudaGetLastError();

@@ -41,6 +41,11 @@ struct Workspace {
 
 void pool_keep_memory();
 
+// main-kernel timing hooks (no-ops unless dnnp_kernel_timing(1)); tags:
+// 1 conv TMA, 2 wgrad TMA, 3 conv cp.async, 4 wgrad cp.async
+void ktime_begin(cudaStream_t st, int tag);
+void ktime_end(cudaStream_t st);
+
 // Row-major 2-D bf16 matrix [rows][cols] (row pitch `pitch_elems`) as a TMA
 // tiled tensor map with a {box_cols, box_rows} box and the given swizzle.
 cudaError_t make_tmap_2d(CUtensorMap* map, const void* base, uint64_t cols, uint64_t rows,

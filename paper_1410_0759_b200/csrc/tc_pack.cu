@@ -6,6 +6,8 @@
 #include <cstdlib>
 #include <map>
 #include <mutex>
+#include <atomic>
+#include <vector>
 
 #include "tc_common.cuh"
 
@@ -362,6 +364,31 @@ Workspace::~Workspace() {
   a_->mu.unlock();
 }
 
+// ---- main-kernel timing (bench roofline) ----------------------------------
+struct KTime {
+  int tag;
+  cudaEvent_t a, b;
+};
+static std::mutex g_kt_mu;
+static std::vector<KTime> g_kt;
+static std::atomic<int> g_kt_on{0};
+
+void ktime_begin(cudaStream_t st, int tag) {
+  if (!g_kt_on.load()) return;
+  KTime k{tag, nullptr, nullptr};
+  cudaEventCreate(&k.a);
+  cudaEventCreate(&k.b);
+  cudaEventRecord(k.a, st);
+  std::lock_guard<std::mutex> g(g_kt_mu);
+  g_kt.push_back(k);
+}
+
+void ktime_end(cudaStream_t st) {
+  if (!g_kt_on.load()) return;
+  std::lock_guard<std::mutex> g(g_kt_mu);
+  if (!g_kt.empty()) cudaEventRecord(g_kt.back().b, st);
+}
+
 void pool_keep_memory() {
   static bool done = false;
   if (done) return;
@@ -473,3 +500,36 @@ cudaError_t pack_act(const View4& v, const float* x, int Cp, __nv_bfloat16* hi, 
 
 }  // namespace tc
 }  // namespace dnnp
+
+// additive C entries: time every main GEMM kernel (CUDA events around the
+// launch on the caller's stream) so a benchmark can report per-kernel
+// durations measured inside its own timed region
+extern "C" int dnnp_kernel_timing(int enable) {
+  using namespace dnnp::tc;
+  std::lock_guard<std::mutex> g(g_kt_mu);
+  for (auto& k : g_kt) {
+    cudaEventDestroy(k.a);
+    cudaEventDestroy(k.b);
+  }
+  g_kt.clear();
+  g_kt_on.store(enable ? 1 : 0);
+  return 0;
+}
+
+// fills up to max (duration ms, kernel tag) pairs in launch order and
+// returns how many kernels were timed; synchronizes on the recorded events
+extern "C" int dnnp_kernel_times(float* ms, int* tags, int max) {
+  using namespace dnnp::tc;
+  std::lock_guard<std::mutex> g(g_kt_mu);
+  int n = 0;
+  for (auto& k : g_kt) {
+    if (n < max) {
+      float t = -1.0f;
+      if (cudaEventSynchronize(k.b) == cudaSuccess) cudaEventElapsedTime(&t, k.a, k.b);
+      if (ms) ms[n] = t;
+      if (tags) tags[n] = k.tag;
+    }
+    n++;
+  }
+  return n;
+}

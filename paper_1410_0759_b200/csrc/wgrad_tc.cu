@@ -283,7 +283,9 @@ cudaError_t launch_wgrad(const WgParams& prm, int mt, int nt, int splits, cudaSt
     attr_dev = dev;
   }
   const dim3 grid{unsigned(mt), unsigned(nt), unsigned(splits)};
+  ktime_begin(st, 4);
   wgrad_tc_kernel<BN><<<grid, kThreads, CC::SMEM, st>>>(prm);
+  ktime_end(st);
   note_launch();
   return cudaGetLastError();
 }
@@ -560,7 +562,9 @@ cudaError_t launch_wgrad_tma(const WgTmaParams& prm, dim3 grid, cudaStream_t st)
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  ktime_begin(st, 2);
   cudaError_t e = cudaLaunchKernelEx(&cfg, wgrad_tma_kernel<BN, NC>, prm);
+  ktime_end(st);
   note_launch();
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
