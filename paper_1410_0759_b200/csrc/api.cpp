@@ -295,6 +295,7 @@ class Stager {
     if (!b.host) {
       b.dev = const_cast<void*>(user);
     } else {
+      dnnp::tc::pool_keep_memory();  // staging buffers recycle through the stream pool
       cudaError_t e = cudaMallocAsync(&b.dev, std::max<size_t>(bytes, 16), st_);
       if (e != cudaSuccess) return cuda_status(e, "staging allocation");
       if (copy_in) {

@@ -15,6 +15,7 @@
 #include <algorithm>
 
 #include "common.cuh"
+#include "tc_common.cuh"
 
 namespace dnnp {
 
@@ -321,6 +322,7 @@ static cudaError_t launch_simt(SimtArgs& a, cudaStream_t st) {
   a.splits = 1;
   a.k_per_split = a.Kred;
   T* ws = nullptr;
+  tc::Workspace wsa(st);
   void* final_out = a.out;
   if (PASS == WGRAD) {
     int64_t tiles = gm * gn;
@@ -333,8 +335,9 @@ static cudaError_t launch_simt(SimtArgs& a, cudaStream_t st) {
     }
     a.splits = int(s);
     if (a.splits > 1) {
-      cudaError_t e = cudaMallocAsync(&ws, sizeof(T) * a.splits * a.M * a.Ncol, st);
+      cudaError_t e = wsa.alloc(sizeof(T) * a.splits * a.M * a.Ncol);
       if (e != cudaSuccess) return e;
+      ws = static_cast<T*>(wsa.p);
       a.out = ws;
     }
   }
@@ -350,7 +353,6 @@ static cudaError_t launch_simt(SimtArgs& a, cudaStream_t st) {
                                                               a.accumulate);
     note_launch();
     if (e == cudaSuccess) e = cudaGetLastError();
-    cudaFreeAsync(ws, st);
   }
   return e;
 }

@@ -35,6 +35,11 @@ struct ConvProblem {
   View4 x, y;
 };
 
+namespace tc {
+// keep stream-ordered pool memory across synchronizations (release threshold max)
+void pool_keep_memory();
+}  // namespace tc
+
 // Launch bookkeeping: every kernel this library launches bumps a counter
 // so benches/tests can prove native kernels ran.
 void note_launch(int count = 1);

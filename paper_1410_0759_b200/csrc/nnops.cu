@@ -9,10 +9,12 @@
 // Roundings follow numpy's evaluation order with explicit _rn intrinsics so
 // that e.g. activation backward, transform and pooling backward are bit-exact.
 #include <atomic>
+#include <type_traits>
 #include <cmath>
 #include <cstdio>
 
 #include "common.cuh"
+#include "tc_common.cuh"
 
 namespace dnnp {
 
@@ -56,7 +58,10 @@ struct EwGeom {
   int64_t rows;   // ext[0]*ext[1]*ext[2]
   MagicDiv d2, d1;  // row decode: r -> (i0, i1, i2)
   int use_magic;
+  int64_t chunks;   // pieces of length kEwChunk per row (long merged rows)
+  int vec;          // innermost stride 1 for every operand and 16-byte aligned rows
 };
+constexpr int64_t kEwChunk = 2048;
 
 static EwGeom make_ew(const View4* views[3], int nops, int out_index) {
   const View4& o = *views[out_index];
@@ -81,7 +86,29 @@ static EwGeom make_ew(const View4* views[3], int nops, int out_index) {
     int64_t e[4] = {v.n, v.c, v.h, v.w};
     for (int k = 0; k < 4; k++) g.st[op][k] = e[perm[k]] == 1 ? 0 : s[perm[k]];
   }
+  // merge adjacent dims that are contiguous for every operand (a channel
+  // slice of an NCHW parent becomes one long row per image)
+  for (int k = 2; k >= 0; k--) {
+    if (g.ext[k] == 1) continue;
+    bool ok = true;
+    for (int op = 0; op < nops; op++)
+      if (g.st[op][k] != g.st[op][k + 1] * g.ext[k + 1]) ok = false;
+    if (!ok) continue;
+    // fold dim k into k+1, shift the outer dims in (extent-1 dim at the top)
+    g.ext[k + 1] *= g.ext[k];
+    for (int j = k; j > 0; j--) {
+      g.ext[j] = g.ext[j - 1];
+      for (int op = 0; op < 3; op++) g.st[op][j] = g.st[op][j - 1];
+    }
+    g.ext[0] = 1;
+    for (int op = 0; op < 3; op++) g.st[op][0] = 0;
+    k++;  // re-examine position k (now the next outer dim) against the merged one
+  }
   g.rows = g.ext[0] * g.ext[1] * g.ext[2];
+  g.chunks = (g.ext[3] + kEwChunk - 1) / kEwChunk;
+  g.vec = 1;
+  for (int op = 0; op < nops; op++)
+    if (g.st[op][3] != 1 || g.st[op][0] % 4 || g.st[op][1] % 4 || g.st[op][2] % 4) g.vec = 0;
   g.use_magic = g.rows < (int64_t(1) << 32);
   g.d2 = make_magic(uint32_t(g.ext[2]));
   g.d1 = make_magic(uint32_t(g.ext[1]));
@@ -103,13 +130,18 @@ static bool same_dense(const View4* views[3], int nops) {
   return maxo + 1 == a.size();
 }
 
+// Strided rows: work item = (row, chunk of kEwChunk innermost elements), one
+// warp per item; when every operand's rows are contiguous and 16-byte aligned
+// (g.vec and aligned bases, checked on the host) lanes move 16-byte vectors.
 template <typename Op, typename T>
 __global__ void __launch_bounds__(256) ew_rows_kernel(EwGeom g, const T* __restrict__ a,
                                                       const T* __restrict__ b, T* out, Op op) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
-  for (int64_t r = warp; r < g.rows; r += nwarps) {
+  const int64_t items = g.rows * g.chunks;
+  for (int64_t it = warp; it < items; it += nwarps) {
+    const int64_t r = it / g.chunks, ch = it - r * g.chunks;
     int64_t i0, i1, i2;
     if (g.use_magic) {
       uint32_t q, rem;
@@ -128,15 +160,57 @@ __global__ void __launch_bounds__(256) ew_rows_kernel(EwGeom g, const T* __restr
     int64_t base[3];
 #pragma unroll
     for (int k = 0; k < 3; k++) base[k] = i0 * g.st[k][0] + i1 * g.st[k][1] + i2 * g.st[k][2];
-    for (int64_t j = lane; j < g.ext[3]; j += 32) {
-      T va = a ? a[base[0] + j * g.st[0][3]] : T(0);
-      T vb = b ? b[base[1] + j * g.st[1][3]] : T(0);
-      T* po = out + base[2] + j * g.st[2][3];
-      *po = op(va, vb, Op::kReadsOut ? *po : T(0));
+    const int64_t j0 = ch * kEwChunk, j1 = min(g.ext[3], j0 + kEwChunk);
+    if (g.vec) {
+      constexpr int V = 16 / sizeof(T);
+      using Vec = typename std::conditional<sizeof(T) == 4, float4, double2>::type;
+      // batches of 4 vectors per lane, all loaded before any store
+      constexpr int NV = int(kEwChunk / (32 * V)), U = 4;
+      const int64_t jend = j1 - (j1 - j0) % V;
+      for (int u0 = 0; u0 < NV; u0 += U) {
+        Vec va[U], vb[U], vo[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+          const int64_t j = j0 + (int64_t(u0 + u) * 32 + lane) * V;
+          if (j < jend) {
+            if (a) va[u] = *reinterpret_cast<const Vec*>(a + base[0] + j);
+            if (b) vb[u] = *reinterpret_cast<const Vec*>(b + base[1] + j);
+            if (Op::kReadsOut) vo[u] = *reinterpret_cast<const Vec*>(out + base[2] + j);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+          const int64_t j = j0 + (int64_t(u0 + u) * 32 + lane) * V;
+          if (j < jend) {
+            const T* pa = reinterpret_cast<const T*>(&va[u]);
+            const T* pb = reinterpret_cast<const T*>(&vb[u]);
+            T* po = reinterpret_cast<T*>(&vo[u]);
+#pragma unroll
+            for (int k = 0; k < V; k++)
+              po[k] = op(a ? pa[k] : T(0), b ? pb[k] : T(0), Op::kReadsOut ? po[k] : T(0));
+            *reinterpret_cast<Vec*>(out + base[2] + j) = vo[u];
+          }
+        }
+      }
+      const int64_t tail = j1 - (j1 - j0) % V;  // ragged end of the chunk
+      for (int64_t j = tail + lane; j < j1; j += 32) {
+        T* po = out + base[2] + j;
+        *po = op(a ? a[base[0] + j] : T(0), b ? b[base[1] + j] : T(0), Op::kReadsOut ? *po : T(0));
+      }
+    } else {
+      for (int64_t j = j0 + lane; j < j1; j += 32) {
+        T va = a ? a[base[0] + j * g.st[0][3]] : T(0);
+        T vb = b ? b[base[1] + j * g.st[1][3]] : T(0);
+        T* po = out + base[2] + j * g.st[2][3];
+        *po = op(va, vb, Op::kReadsOut ? *po : T(0));
+      }
     }
   }
 }
 
+// Dense elementwise: every lane moves U 16-byte vectors per iteration,
+// all loads issued before any store (out may alias an input element-wise, so
+// the batching is explicit rather than left to __restrict__).
 template <typename Op, typename T>
 __global__ void __launch_bounds__(256) ew_dense_kernel(int64_t n, const T* __restrict__ a,
                                                        const T* __restrict__ b, T* out, Op op,
@@ -145,9 +219,31 @@ __global__ void __launch_bounds__(256) ew_dense_kernel(int64_t n, const T* __res
   const int64_t nth = int64_t(gridDim.x) * blockDim.x;
   if (vec) {
     constexpr int V = 16 / sizeof(T);
+    constexpr int U = 4;
     using Vec = typename std::conditional<sizeof(T) == 4, float4, double2>::type;
     const int64_t nv = n / V;
-    for (int64_t i = tid; i < nv; i += nth) {
+    int64_t i = tid;
+    for (; i + (U - 1) * nth < nv; i += U * nth) {
+      Vec va[U], vb[U], vo[U];
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        if (a) va[u] = reinterpret_cast<const Vec*>(a)[i + u * nth];
+        if (b) vb[u] = reinterpret_cast<const Vec*>(b)[i + u * nth];
+        if (Op::kReadsOut) vo[u] = reinterpret_cast<const Vec*>(out)[i + u * nth];
+      }
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        const T* pa = reinterpret_cast<const T*>(&va[u]);
+        const T* pb = reinterpret_cast<const T*>(&vb[u]);
+        T* po = reinterpret_cast<T*>(&vo[u]);
+#pragma unroll
+        for (int k = 0; k < V; k++)
+          po[k] = op(a ? pa[k] : T(0), b ? pb[k] : T(0), Op::kReadsOut ? po[k] : T(0));
+      }
+#pragma unroll
+      for (int u = 0; u < U; u++) reinterpret_cast<Vec*>(out)[i + u * nth] = vo[u];
+    }
+    for (; i < nv; i += nth) {
       Vec va, vb, vo;
       if (a) va = reinterpret_cast<const Vec*>(a)[i];
       if (b) vb = reinterpret_cast<const Vec*>(b)[i];
@@ -160,8 +256,8 @@ __global__ void __launch_bounds__(256) ew_dense_kernel(int64_t n, const T* __res
         po[k] = op(a ? pa[k] : T(0), b ? pb[k] : T(0), Op::kReadsOut ? po[k] : T(0));
       reinterpret_cast<Vec*>(out)[i] = vo;
     }
-    for (int64_t i = nv * V + tid; i < n; i += nth)
-      out[i] = op(a ? a[i] : T(0), b ? b[i] : T(0), Op::kReadsOut ? out[i] : T(0));
+    for (int64_t j = nv * V + tid; j < n; j += nth)
+      out[j] = op(a ? a[j] : T(0), b ? b[j] : T(0), Op::kReadsOut ? out[j] : T(0));
   } else {
     for (int64_t i = tid; i < n; i += nth)
       out[i] = op(a ? a[i] : T(0), b ? b[i] : T(0), Op::kReadsOut ? out[i] : T(0));
@@ -183,10 +279,13 @@ static cudaError_t run_ew(const View4& va, const T* a, const View4* vb, const T*
     unsigned grid = grid_for(aligned ? ceil_div(n, V) : n, 256, 8);
     ew_dense_kernel<Op, T><<<grid, 256, 0, st>>>(n, a, b, out, op, aligned ? 1 : 0);
   } else {
-    EwGeom g = make_ew(views, 3, 2);
+    EwGeom g = make_ew(views, vb ? 3 : 3, 2);
     if (!vb)
       for (int k = 0; k < 4; k++) g.st[1][k] = 0;
-    unsigned grid = grid_for(g.rows * 32, 256, 16);
+    if ((reinterpret_cast<uintptr_t>(a) | (b ? reinterpret_cast<uintptr_t>(b) : 0) |
+         reinterpret_cast<uintptr_t>(out)) % 16)
+      g.vec = 0;
+    unsigned grid = grid_for(g.rows * g.chunks * 32, 256, 16);
     ew_rows_kernel<Op, T><<<grid, 256, 0, st>>>(g, a, b, out, op);
   }
   note_launch();
@@ -479,17 +578,16 @@ static cudaError_t softmax_t(int mode, const View4& av, const T* a, const View4*
     int64_t chunks = ceil_div(int64_t(kNumSMs) * 4, av.n);
     chunks = std::max<int64_t>(1, std::min<int64_t>(chunks, ceil_div(G, 2048)));
     chunks = std::min<int64_t>(chunks, 65535);
-    T* part = nullptr;
-    cudaError_t e = cudaMallocAsync(&part, sizeof(T) * 2 * av.n * chunks, st);
+    tc::Workspace ws(st);
+    cudaError_t e = ws.alloc(sizeof(T) * 2 * av.n * chunks);
     if (e != cudaSuccess) return e;
+    T* part = static_cast<T*>(ws.p);
     dim3 grid(unsigned(chunks), unsigned(av.n));
     ImgGeom ga = img_geom(av), gb = img_geom(bv ? *bv : av), go = img_geom(ov);
     softmax_img_partial<T, BWD><<<grid, 256, 0, st>>>(ga, a, gb, b, G, int(chunks), part);
     softmax_img_apply<T, BWD><<<grid, 256, 0, st>>>(ga, a, gb, b, go, o, G, int(chunks), part);
     note_launch(2);
-    e = cudaGetLastError();
-    cudaFreeAsync(part, st);
-    return e;
+    return cudaGetLastError();
   }
   const int64_t npos = av.n * av.h * av.w;
   softmax_spatial<T, BWD><<<grid_for(npos, 256, 8), 256, 0, st>>>(
@@ -520,47 +618,57 @@ struct PoolGeom {
   View4 x, y;  // y: pooled output (or dy)
   int64_t N, C, H, W, P, Q;
   int64_t wh, ww, sh, sw, ph, pw;
-  MagicDiv dQ, dP, dC, dW, dH;
+  MagicDiv dQ, dP, dC, dW, dH, dSH, dSW;
 };
 
 // Forward: one thread per pooled element; window clipped to the image
 // (reference nnops.py:150-200).  Max takes the first maximum in (h, w) scan
 // order with numpy argmax NaN semantics (the first NaN wins); argmax is the
-// LOGICAL NCHW index.  Average divides by the in-image count.
+// LOGICAL NCHW index.  Average divides by the in-image count.  32-bit index
+// arithmetic (extents < 2^31 checked on the host), 64-bit only for offsets.
 template <typename T>
 __global__ void __launch_bounds__(256) pool_fwd_kernel(PoolGeom g, const T* __restrict__ x,
                                                        T* __restrict__ y, int64_t* argmax,
                                                        int kind, int64_t total) {
-  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += stride) {
+  const int H = int(g.H), W = int(g.W), C = int(g.C);
+  const int wh = int(g.wh), ww = int(g.ww);
+  const int64_t xsh = g.x.sh, xsw = g.x.sw;
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < uint32_t(total); i += stride) {
     uint32_t t, q, p, c, n;
-    mdivmod(uint32_t(i), g.dQ, t, q);
+    mdivmod(i, g.dQ, t, q);
     mdivmod(t, g.dP, t, p);
     mdivmod(t, g.dC, n, c);
-    const int64_t hs0 = int64_t(p) * g.sh - g.ph, ws0 = int64_t(q) * g.sw - g.pw;
-    const int64_t hs = max(int64_t(0), hs0), he = min(g.H, hs0 + g.wh);
-    const int64_t ws = max(int64_t(0), ws0), we = min(g.W, ws0 + g.ww);
+    const int hs0 = int(p) * int(g.sh) - int(g.ph), ws0 = int(q) * int(g.sw) - int(g.pw);
+    const int hs = max(0, hs0), he = min(H, hs0 + wh);
+    const int ws = max(0, ws0), we = min(W, ws0 + ww);
     const T* xb = x + int64_t(n) * g.x.sn + int64_t(c) * g.x.sc;
     T out;
     if (kind == 0) {
-      T best = xb[hs * g.x.sh + ws * g.x.sw];
-      int64_t bh = hs, bw = ws;
-      for (int64_t h = hs; h < he; h++)
-        for (int64_t w = ws; w < we; w++) {
-          T v = xb[h * g.x.sh + w * g.x.sw];
-          if (best != best) continue;  // a NaN already won
+      T best = xb[hs * xsh + ws * xsw];
+      int bh = hs, bw = ws;
+      bool nan = best != best;
+      for (int h = hs; h < he && !nan; h++) {
+        const T* xr = xb + h * xsh;
+        for (int w = ws; w < we; w++) {
+          const T v = xr[w * xsw];
           if (v != v || v > best) {
             best = v;
             bh = h;
             bw = w;
+            if (v != v) {
+              nan = true;  // the first NaN wins
+              break;
+            }
           }
         }
+      }
       out = best;
-      if (argmax) argmax[i] = ((int64_t(n) * g.C + c) * g.H + bh) * g.W + bw;
+      if (argmax) argmax[i] = ((int64_t(n) * C + c) * H + bh) * W + bw;
     } else {
       T s = T(0);
-      for (int64_t h = hs; h < he; h++)
-        for (int64_t w = ws; w < we; w++) s = dadd<T>(s, xb[h * g.x.sh + w * g.x.sw]);
+      for (int h = hs; h < he; h++)
+        for (int w = ws; w < we; w++) s = dadd<T>(s, xb[h * xsh + w * xsw]);
       out = s / T((he - hs) * (we - ws));
     }
     y[int64_t(n) * g.y.sn + int64_t(c) * g.y.sc + int64_t(p) * g.y.sh + int64_t(q) * g.y.sw] = out;
@@ -576,31 +684,33 @@ __global__ void __launch_bounds__(256) pool_bwd_kernel(PoolGeom g, const T* __re
                                                        T* __restrict__ dx,
                                                        const int64_t* __restrict__ argmax,
                                                        int kind, int64_t total) {
-  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += stride) {
+  const int H = int(g.H), W = int(g.W), P = int(g.P), Q = int(g.Q);
+  const int wh = int(g.wh), ww = int(g.ww), sh = int(g.sh), sw = int(g.sw);
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < uint32_t(total); i += stride) {
     uint32_t t, w, h, c, n;
-    mdivmod(uint32_t(i), g.dW, t, w);
+    mdivmod(i, g.dW, t, w);
     mdivmod(t, g.dH, t, h);
     mdivmod(t, g.dC, n, c);
     // p covers h iff p*sh - ph <= h < p*sh - ph + wh
-    const int64_t hp = int64_t(h) + g.ph, wp = int64_t(w) + g.pw;
-    int64_t p0 = hp - g.wh + 1 > 0 ? (hp - g.wh + 1 + g.sh - 1) / g.sh : 0;
-    int64_t p1 = min(g.P - 1, hp / g.sh);
-    int64_t q0 = wp - g.ww + 1 > 0 ? (wp - g.ww + 1 + g.sw - 1) / g.sw : 0;
-    int64_t q1 = min(g.Q - 1, wp / g.sw);
-    const int64_t plane = int64_t(n) * g.C + c;
-    const int64_t me = (plane * g.H + h) * g.W + w;
+    const int hp = int(h) + int(g.ph), wp = int(w) + int(g.pw);
+    const int p0 = hp - wh + 1 > 0 ? int(mdiv(uint32_t(hp - wh + sh), g.dSH)) : 0;
+    const int p1 = min(P - 1, int(mdiv(uint32_t(hp), g.dSH)));
+    const int q0 = wp - ww + 1 > 0 ? int(mdiv(uint32_t(wp - ww + sw), g.dSW)) : 0;
+    const int q1 = min(Q - 1, int(mdiv(uint32_t(wp), g.dSW)));
+    const uint32_t plane = n * uint32_t(g.C) + c;
+    const int64_t me = (int64_t(plane) * H + h) * W + w;
+    const T* dyb = dy + int64_t(n) * g.y.sn + int64_t(c) * g.y.sc;
+    const int64_t* amb = argmax ? argmax + int64_t(plane) * P * Q : nullptr;
     T acc = T(0);
-    for (int64_t p = p0; p <= p1; p++)
-      for (int64_t q = q0; q <= q1; q++) {
-        const int64_t oi = (plane * g.P + p) * g.Q + q;
-        const T d = dy[int64_t(n) * g.y.sn + int64_t(c) * g.y.sc + p * g.y.sh + q * g.y.sw];
+    for (int p = p0; p <= p1; p++)
+      for (int q = q0; q <= q1; q++) {
+        const T d = dyb[p * g.y.sh + q * g.y.sw];
         if (kind == 0) {
-          if (argmax[oi] == me) acc = dadd<T>(acc, d);
+          if (amb[p * Q + q] == me) acc = dadd<T>(acc, d);
         } else {
-          const int64_t hs0 = p * g.sh - g.ph, ws0 = q * g.sw - g.pw;
-          const int64_t cnt = (min(g.H, hs0 + g.wh) - max(int64_t(0), hs0)) *
-                              (min(g.W, ws0 + g.ww) - max(int64_t(0), ws0));
+          const int hs0 = p * sh - int(g.ph), ws0 = q * sw - int(g.pw);
+          const int cnt = (min(H, hs0 + wh) - max(0, hs0)) * (min(W, ws0 + ww) - max(0, ws0));
           acc = dadd<T>(acc, d / T(cnt));
         }
       }
@@ -612,18 +722,212 @@ __global__ void __launch_bounds__(256) pool_bwd_kernel(PoolGeom g, const T* __re
 // possible for caller-made argmax buffers); those take the serial path.
 __global__ void pool_argmax_check(PoolGeom g, const int64_t* __restrict__ argmax, int64_t total,
                                   int* bad) {
-  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += stride) {
-    const int64_t q = i % g.Q, p = (i / g.Q) % g.P, plane = i / (g.Q * g.P);
-    const int64_t a = argmax[i];
-    const int64_t hw = a - plane * g.H * g.W;
-    bool ok = hw >= 0 && hw < g.H * g.W;
+  const uint32_t stride = gridDim.x * blockDim.x;
+  const int64_t HW = g.H * g.W;
+  bool any = false;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < uint32_t(total); i += stride) {
+    uint32_t t, q, p;
+    mdivmod(i, g.dQ, t, q);
+    mdivmod(t, g.dP, t, p);  // t = plane
+    const int64_t hw = argmax[i] - int64_t(t) * HW;
+    bool ok = hw >= 0 && hw < HW;
     if (ok) {
-      const int64_t h = hw / g.W, w = hw % g.W;
-      const int64_t hs0 = p * g.sh - g.ph, ws0 = q * g.sw - g.pw;
-      ok = h >= hs0 && h < hs0 + g.wh && w >= ws0 && w < ws0 + g.ww;
+      uint32_t h, w;
+      mdivmod(uint32_t(hw), g.dW, h, w);
+      const int hs0 = int(p) * int(g.sh) - int(g.ph), ws0 = int(q) * int(g.sw) - int(g.pw);
+      ok = int(h) >= hs0 && int(h) < hs0 + int(g.wh) && int(w) >= ws0 && int(w) < ws0 + int(g.ww);
     }
-    if (!ok) *bad = 1;
+    any |= !ok;
+  }
+  if (__any_sync(0xffffffffu, any) && (threadIdx.x & 31) == 0) *bad = 1;
+}
+
+// Plane-tiled forms (one block per (n, c) plane, the plane staged in shared
+// memory with coalesced loads; same window semantics and summation order as
+// the per-element kernels above).
+template <typename T>
+__global__ void __launch_bounds__(256) pool_fwd_plane_kernel(PoolGeom g, const T* __restrict__ x,
+                                                             T* __restrict__ y, int64_t* argmax,
+                                                             int kind) {
+  extern __shared__ __align__(16) uint8_t psm[];
+  T* xs = reinterpret_cast<T*>(psm);
+  const int H = int(g.H), W = int(g.W), P = int(g.P), Q = int(g.Q), C = int(g.C);
+  const int wh = int(g.wh), ww = int(g.ww);
+  const int planes = int(g.N) * C;
+  for (int pl = blockIdx.x; pl < planes; pl += gridDim.x) {
+    uint32_t nu, cu;
+    mdivmod(uint32_t(pl), g.dC, nu, cu);
+    const int n = int(nu), c = int(cu);
+    const T* xb = x + int64_t(n) * g.x.sn + int64_t(c) * g.x.sc;
+    if (g.x.sw == 1 && g.x.sh == W) {
+      // contiguous plane: batches of 4 independent loads per thread
+      const int HW = H * W;
+      int i = threadIdx.x;
+      for (; i + 3 * 256 < HW; i += 4 * 256) {
+        T v0 = xb[i], v1 = xb[i + 256], v2 = xb[i + 512], v3 = xb[i + 768];
+        xs[i] = v0;
+        xs[i + 256] = v1;
+        xs[i + 512] = v2;
+        xs[i + 768] = v3;
+      }
+      for (; i < HW; i += 256) xs[i] = xb[i];
+    } else {
+      for (int i = threadIdx.x; i < H * W; i += blockDim.x) {
+        uint32_t h, w;
+        mdivmod(uint32_t(i), g.dW, h, w);
+        xs[i] = xb[int(h) * g.x.sh + int(w) * g.x.sw];
+      }
+    }
+    __syncthreads();
+    T* yb = y + int64_t(n) * g.y.sn + int64_t(c) * g.y.sc;
+    for (int o = threadIdx.x; o < P * Q; o += blockDim.x) {
+      uint32_t pu, qu;
+      mdivmod(uint32_t(o), g.dQ, pu, qu);
+      const int p = int(pu), q = int(qu);
+      const int hs0 = p * int(g.sh) - int(g.ph), ws0 = q * int(g.sw) - int(g.pw);
+      const int hs = max(0, hs0), he = min(H, hs0 + wh);
+      const int ws = max(0, ws0), we = min(W, ws0 + ww);
+      T out;
+      if (kind == 0) {
+        T best = xs[hs * W + ws];
+        int bi = hs * W + ws;
+        bool nan = best != best;
+        for (int h = hs; h < he && !nan; h++)
+          for (int w = ws; w < we; w++) {
+            const T v = xs[h * W + w];
+            if (v != v || v > best) {
+              best = v;
+              bi = h * W + w;
+              if (v != v) {
+                nan = true;  // the first NaN wins
+                break;
+              }
+            }
+          }
+        out = best;
+        if (argmax) argmax[int64_t(pl) * P * Q + o] = int64_t(pl) * H * W + bi;
+      } else {
+        T sacc = T(0);
+        for (int h = hs; h < he; h++)
+          for (int w = ws; w < we; w++) sacc = dadd<T>(sacc, xs[h * W + w]);
+        out = sacc / T((he - hs) * (we - ws));
+      }
+      yb[p * g.y.sh + q * g.y.sw] = out;
+    }
+    __syncthreads();
+  }
+}
+
+// Backward: the plane's dy (and argmax) staged in shared memory; argmax
+// entries are validated on the way in (an entry outside its own window sets
+// *bad and the serial reference-order scatter redoes the whole op).
+template <typename T, int KIND, int MAXK>
+__global__ void __launch_bounds__(256) pool_bwd_plane_kernel(PoolGeom g, const T* __restrict__ dy,
+                                                             T* __restrict__ dx,
+                                                             const int64_t* __restrict__ argmax,
+                                                             int* bad) {
+  extern __shared__ __align__(16) uint8_t psm[];
+  const int H = int(g.H), W = int(g.W), P = int(g.P), Q = int(g.Q), C = int(g.C);
+  const int wh = int(g.wh), ww = int(g.ww), sh = int(g.sh), sw = int(g.sw);
+  const int ph = int(g.ph), pw = int(g.pw);
+  const int PQ = P * Q, HW = H * W;
+  int* as = reinterpret_cast<int*>(psm);  // max: plane-local argmax (h * W + w) or -1
+  T* ds = reinterpret_cast<T*>(psm + ((size_t(PQ) * 4 + 15) & ~size_t(15)));  // dy (avg: dy / count)
+  T* xs = ds + PQ;                        // max: the dx plane being assembled
+  const int planes = int(g.N) * C;
+  for (int pl = blockIdx.x; pl < planes; pl += gridDim.x) {
+    uint32_t nu, cu;
+    mdivmod(uint32_t(pl), g.dC, nu, cu);
+    const T* dyb = dy + int64_t(nu) * g.y.sn + int64_t(cu) * g.y.sc;
+    bool badl = false;
+    const int64_t abase = int64_t(pl) * HW;
+    for (int i = threadIdx.x; i < PQ; i += blockDim.x) {
+      uint32_t pu, qu;
+      mdivmod(uint32_t(i), g.dQ, pu, qu);
+      const int p = int(pu), q = int(qu);
+      const T d = dyb[p * g.y.sh + q * g.y.sw];
+      const int hs0 = p * sh - ph, ws0 = q * sw - pw;
+      if (KIND == 0) {
+        ds[i] = d;
+        const int64_t hw = argmax[int64_t(pl) * PQ + i] - abase;
+        int loc = -1;
+        if (hw >= 0 && hw < int64_t(HW)) {
+          uint32_t h, w;
+          mdivmod(uint32_t(hw), g.dW, h, w);
+          if (int(h) >= hs0 && int(h) < hs0 + wh && int(w) >= ws0 && int(w) < ws0 + ww) loc = int(hw);
+        }
+        badl |= loc < 0;
+        as[i] = loc;
+      } else {
+        const int cnt = (min(H, hs0 + wh) - max(0, hs0)) * (min(W, ws0 + ww) - max(0, ws0));
+        ds[i] = d / T(cnt);  // the reference adds dy / count per window (nnops.py:237-246)
+      }
+    }
+    if (KIND == 0) {
+      if (badl) *bad = 1;
+      for (int i = threadIdx.x; i < HW; i += blockDim.x) xs[i] = T(0);
+    }
+    __syncthreads();
+    T* dxb = dx + int64_t(nu) * g.x.sn + int64_t(cu) * g.x.sc;
+    if (KIND == 0) {
+      // window-driven: the first window (ascending (p, q)) whose argmax is
+      // element t sums every covering window targeting t, in order
+      for (int o = threadIdx.x; o < PQ; o += blockDim.x) {
+        const int t = as[o];
+        if (t < 0) continue;
+        uint32_t hu, wu;
+        mdivmod(uint32_t(t), g.dW, hu, wu);
+        const int hp = int(hu) + ph, wp = int(wu) + pw;
+        const int p0 = hp - wh + 1 > 0 ? int(mdiv(uint32_t(hp - wh + sh), g.dSH)) : 0;
+        const int p1 = min(P - 1, int(mdiv(uint32_t(hp), g.dSH)));
+        const int q0 = wp - ww + 1 > 0 ? int(mdiv(uint32_t(wp - ww + sw), g.dSW)) : 0;
+        const int q1 = min(Q - 1, int(mdiv(uint32_t(wp), g.dSW)));
+        bool first = true;
+        T acc = T(0);
+        for (int p = p0; p <= p1; p++)
+          for (int q = q0; q <= q1; q++) {
+            const int oo = p * Q + q;
+            if (as[oo] == t) {
+              if (oo < o) first = false;
+              acc = dadd<T>(acc, ds[oo]);
+            }
+          }
+        if (first) xs[t] = acc;
+      }
+      __syncthreads();
+      if (g.x.sw == 1 && g.x.sh == W) {
+        for (int i = threadIdx.x; i < HW; i += blockDim.x) dxb[i] = xs[i];
+      } else {
+        for (int i = threadIdx.x; i < HW; i += blockDim.x) {
+          uint32_t hu, wu;
+          mdivmod(uint32_t(i), g.dW, hu, wu);
+          dxb[int(hu) * g.x.sh + int(wu) * g.x.sw] = xs[i];
+        }
+      }
+    } else {
+      for (int i = threadIdx.x; i < HW; i += blockDim.x) {
+        uint32_t hu, wu;
+        mdivmod(uint32_t(i), g.dW, hu, wu);
+        const int hp = int(hu) + ph, wp = int(wu) + pw;
+        const int p0 = hp - wh + 1 > 0 ? int(mdiv(uint32_t(hp - wh + sh), g.dSH)) : 0;
+        const int p1 = min(P - 1, int(mdiv(uint32_t(hp), g.dSH)));
+        const int q0 = wp - ww + 1 > 0 ? int(mdiv(uint32_t(wp - ww + sw), g.dSW)) : 0;
+        const int q1 = min(Q - 1, int(mdiv(uint32_t(wp), g.dSW)));
+        T acc = T(0);
+        if (MAXK > 0) {
+#pragma unroll
+          for (int dp = 0; dp < MAXK; dp++)
+#pragma unroll
+            for (int dq = 0; dq < MAXK; dq++)
+              if (p0 + dp <= p1 && q0 + dq <= q1) acc = dadd<T>(acc, ds[(p0 + dp) * Q + q0 + dq]);
+        } else {
+          for (int p = p0; p <= p1; p++)
+            for (int q = q0; q <= q1; q++) acc = dadd<T>(acc, ds[p * Q + q]);
+        }
+        dxb[int(hu) * g.x.sh + int(wu) * g.x.sw] = acc;
+      }
+    }
+    __syncthreads();
   }
 }
 
@@ -660,6 +964,8 @@ static PoolGeom pool_geom(const PoolProblem& pp, const View4& xv, const View4& y
   g.dC = make_magic(uint32_t(xv.c));
   g.dW = make_magic(uint32_t(xv.w));
   g.dH = make_magic(uint32_t(xv.h));
+  g.dSH = make_magic(uint32_t(pp.sh));
+  g.dSW = make_magic(uint32_t(pp.sw));
   return g;
 }
 
@@ -669,6 +975,19 @@ cudaError_t pool_forward(const PoolProblem& pp, Dtype dt, const View4& xv, const
   if (total >= (int64_t(1) << 32) || xv.size() >= (int64_t(1) << 32))
     return cudaErrorInvalidValue;
   PoolGeom g = pool_geom(pp, xv, yv);
+  const size_t eb = dt == F32 ? 4 : 8;
+  const size_t psm = size_t(xv.h) * xv.w * eb;
+  if (psm <= 48 * 1024 && xv.n * xv.c < (int64_t(1) << 31)) {
+    const unsigned pg = unsigned(std::min<int64_t>(xv.n * xv.c, int64_t(kNumSMs) * 16));
+    if (dt == F32)
+      pool_fwd_plane_kernel<float><<<pg, 256, psm, st>>>(g, (const float*)x, (float*)y, argmax,
+                                                         pp.kind);
+    else
+      pool_fwd_plane_kernel<double><<<pg, 256, psm, st>>>(g, (const double*)x, (double*)y,
+                                                          argmax, pp.kind);
+    note_launch();
+    return cudaGetLastError();
+  }
   unsigned grid = grid_for(total, 256, 8);
   if (dt == F32)
     pool_fwd_kernel<float><<<grid, 256, 0, st>>>(g, (const float*)x, (float*)y, argmax, pp.kind,
@@ -685,6 +1004,54 @@ cudaError_t pool_backward(const PoolProblem& pp, Dtype dt, const View4& dyv, con
   const int64_t total = dxv.size(), ptotal = dyv.size();
   if (total >= (int64_t(1) << 32) || ptotal >= (int64_t(1) << 32)) return cudaErrorInvalidValue;
   PoolGeom g = pool_geom(pp, dxv, dyv);
+  const size_t eb = dt == F32 ? 4 : 8;
+  const size_t psm = ((size_t(dyv.h) * dyv.w * 4 + 15) & ~size_t(15)) + size_t(dyv.h) * dyv.w * eb +
+                     (pp.kind == 0 ? size_t(dxv.h) * dxv.w * eb : 0);
+  if (psm <= 48 * 1024 && dxv.n * dxv.c < (int64_t(1) << 31) &&
+      dxv.h * dxv.w < (int64_t(1) << 31)) {
+    tc::Workspace ws(st);
+    cudaError_t e = ws.alloc(sizeof(int));
+    if (e != cudaSuccess) return e;
+    int* bad = static_cast<int*>(ws.p);
+    cudaMemsetAsync(bad, 0, sizeof(int), st);
+    const unsigned pg = unsigned(std::min<int64_t>(dxv.n * dxv.c, int64_t(kNumSMs) * 16));
+    // windows covering one element per dim: ceil(window / stride)
+    const int64_t kmax = std::max(ceil_div(pp.wh, pp.sh), ceil_div(pp.ww, pp.sw));
+    const int mk = kmax <= 2 ? 2 : (kmax <= 4 ? 4 : 0);
+    auto launch = [&](auto tag, auto kindc, auto mkc) {
+      using TT = decltype(tag);
+      pool_bwd_plane_kernel<TT, decltype(kindc)::value, decltype(mkc)::value>
+          <<<pg, 256, psm, st>>>(g, (const TT*)dy, (TT*)dx, argmax, bad);
+    };
+    using I0 = std::integral_constant<int, 0>;
+    using I1 = std::integral_constant<int, 1>;
+    using I2 = std::integral_constant<int, 2>;
+    using I4 = std::integral_constant<int, 4>;
+    if (dt == F32) {
+      if (pp.kind == 0) {
+        if (mk == 2) launch(float(), I0(), I2()); else if (mk == 4) launch(float(), I0(), I4()); else launch(float(), I0(), I0());
+      } else {
+        if (mk == 2) launch(float(), I1(), I2()); else if (mk == 4) launch(float(), I1(), I4()); else launch(float(), I1(), I0());
+      }
+    } else {
+      if (pp.kind == 0) {
+        if (mk == 2) launch(double(), I0(), I2()); else if (mk == 4) launch(double(), I0(), I4()); else launch(double(), I0(), I0());
+      } else {
+        if (mk == 2) launch(double(), I1(), I2()); else if (mk == 4) launch(double(), I1(), I4()); else launch(double(), I1(), I0());
+      }
+    }
+    note_launch();
+    if (pp.kind == 0) {
+      if (dt == F32)
+        pool_bwd_serial<float><<<1, 32, 0, st>>>(g, (const float*)dy, (float*)dx, argmax,
+                                                 ptotal, bad);
+      else
+        pool_bwd_serial<double><<<1, 32, 0, st>>>(g, (const double*)dy, (double*)dx, argmax,
+                                                  ptotal, bad);
+      note_launch();
+    }
+    return cudaGetLastError();
+  }
   unsigned grid = grid_for(total, 256, 8);
   if (dt == F32)
     pool_bwd_kernel<float><<<grid, 256, 0, st>>>(g, (const float*)dy, (float*)dx, argmax,
@@ -694,9 +1061,10 @@ cudaError_t pool_backward(const PoolProblem& pp, Dtype dt, const View4& dyv, con
                                                   pp.kind, total);
   note_launch();
   if (pp.kind == 0) {
-    int* bad = nullptr;
-    cudaError_t e = cudaMallocAsync(&bad, sizeof(int), st);
+    tc::Workspace ws(st);
+    cudaError_t e = ws.alloc(sizeof(int));
     if (e != cudaSuccess) return e;
+    int* bad = static_cast<int*>(ws.p);
     cudaMemsetAsync(bad, 0, sizeof(int), st);
     pool_argmax_check<<<grid_for(ptotal, 256, 4), 256, 0, st>>>(g, argmax, ptotal, bad);
     if (dt == F32)
@@ -706,7 +1074,6 @@ cudaError_t pool_backward(const PoolProblem& pp, Dtype dt, const View4& dyv, con
       pool_bwd_serial<double><<<1, 32, 0, st>>>(g, (const double*)dy, (double*)dx, argmax,
                                                 ptotal, bad);
     note_launch(2);
-    cudaFreeAsync(bad, st);
   }
   return cudaGetLastError();
 }
@@ -750,9 +1117,10 @@ static cudaError_t bias_t(const View4& v, const T* dy, const View4& ov, Dtype db
   if (L >= (int64_t(1) << 32)) return cudaErrorInvalidValue;
   int64_t S = std::max<int64_t>(1, ceil_div(int64_t(kNumSMs) * 8, v.c));
   S = std::min<int64_t>(S, std::max<int64_t>(1, ceil_div(L, 1024)));
-  T* part = nullptr;
-  cudaError_t e = cudaMallocAsync(&part, sizeof(T) * v.c * S, st);
+  tc::Workspace ws(st);
+  cudaError_t e = ws.alloc(sizeof(T) * v.c * S);
   if (e != cudaSuccess) return e;
+  T* part = static_cast<T*>(ws.p);
   bias_partial<T><<<dim3(unsigned(S), unsigned(v.c)), 256, 0, st>>>(
       v, dy, int(S), make_magic(uint32_t(v.h * v.w)), make_magic(uint32_t(v.w)), part);
   unsigned g = unsigned(ceil_div(v.c, 128));
@@ -761,9 +1129,7 @@ static cudaError_t bias_t(const View4& v, const T* dy, const View4& ov, Dtype db
   else
     bias_final<T, double><<<g, 128, 0, st>>>(part, int(S), v.c, ov, (double*)db);
   note_launch(2);
-  e = cudaGetLastError();
-  cudaFreeAsync(part, st);
-  return e;
+  return cudaGetLastError();
 }
 
 cudaError_t conv_backward_bias(const View4& dyv, Dtype dt, const void* dy, const View4& dbv,

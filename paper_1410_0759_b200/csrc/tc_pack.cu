@@ -325,7 +325,10 @@ static ArenaState* arena_for(cudaStream_t st) {
   cudaGetDevice(&dev);
   std::lock_guard<std::mutex> g(map_mu);
   ArenaState*& a = arenas[{dev, st}];
-  if (!a) a = new ArenaState;  // lives for the process
+  if (!a) {
+    pool_keep_memory();
+    a = new ArenaState;  // lives for the process
+  }
   return a;
 }
 
