@@ -33,6 +33,12 @@ struct SimtArgs {
   int splits;
   // decoders
   MagicDiv dRS, dS, dPQ, dQ, dHW, dW, dU, dV;
+  // backward-data stride phases: blockIdx.z = phase (ph, pw); rows (n, i, j)
+  // of the phase grid Hph x Wph (h = i*u + ph), reduction (k, jr, js) over
+  // the gather offsets r' = t0(ph) + u*jr only (the other u-1 of every u taps
+  // never reach a pixel of this phase)
+  int Hph, Wph, nRp, nSp;
+  MagicDiv dHWph, dWph, dRSph, dSph;
 };
 
 template <typename T>
@@ -73,9 +79,13 @@ __device__ __forceinline__ RowCtx<T, PASS> row_ctx(const SimtArgs& a, int64_t m)
     rc.hb = int32_t(pp * p.u - p.pad_h);
     rc.wb = int32_t(qq * p.v - p.pad_w);
   } else if (PASS == DGRAD) {
-    uint32_t n, rem, h, w;
-    mdivmod(uint32_t(m), a.dHW, n, rem);
-    mdivmod(rem, a.dW, h, w);
+    uint32_t n, rem, i, j;
+    mdivmod(uint32_t(m), a.dHWph, n, rem);
+    mdivmod(rem, a.dWph, i, j);
+    const int u = int(p.u), v = int(p.v);
+    const int ph = int(blockIdx.z) / v, pw = int(blockIdx.z) - (int(blockIdx.z) / v) * v;
+    const int h = int(i) * u + ph, w = int(j) * v + pw;
+    rc.valid = h < p.H && w < p.W;
     rc.n = n;
     rc.base = int64_t(n) * p.y.sn;
     rc.hb = int32_t(h + p.pad_h);
@@ -89,7 +99,8 @@ __device__ __forceinline__ RowCtx<T, PASS> row_ctx(const SimtArgs& a, int64_t m)
 }
 
 template <typename T, int PASS>
-__device__ __forceinline__ T load_a(const SimtArgs& a, const RowCtx<T, PASS>& rc, int64_t k) {
+__device__ __forceinline__ T load_a(const SimtArgs& a, const RowCtx<T, PASS>& rc, int64_t k,
+                                    int t0h, int t0w) {
   const ConvProblem& p = a.p;
   if (!rc.valid || k >= a.Kred) return T(0);
   const T* src = static_cast<const T*>(a.a_src);
@@ -103,17 +114,15 @@ __device__ __forceinline__ T load_a(const SimtArgs& a, const RowCtx<T, PASS>& rc
     if (uint32_t(h) >= uint32_t(p.H) || uint32_t(w) >= uint32_t(p.W)) return T(0);
     return src[rc.base + int64_t(c) * p.x.sc + int64_t(h) * p.x.sh + int64_t(w) * p.x.sw];
   } else if (PASS == DGRAD) {
-    uint32_t kk, rs, r, s;
-    mdivmod(uint32_t(k), a.dRS, kk, rs);
-    mdivmod(rs, a.dS, r, s);
-    const int32_t hr = p.flip ? int32_t(p.R - 1 - r) : int32_t(r);
-    const int32_t wr = p.flip ? int32_t(p.S - 1 - s) : int32_t(s);
-    const int32_t th = rc.hb - hr, tw = rc.wb - wr;  // = p*u, q*v
+    uint32_t kk, rs, jr, js;
+    mdivmod(uint32_t(k), a.dRSph, kk, rs);
+    mdivmod(rs, a.dSph, jr, js);
+    const int32_t ro = t0h + int32_t(p.u) * int32_t(jr);  // gather offset
+    const int32_t so = t0w + int32_t(p.v) * int32_t(js);
+    if (ro >= p.R || so >= p.S) return T(0);
+    const int32_t th = rc.hb - ro, tw = rc.wb - so;  // = p*u, q*v exactly
     if (th < 0 || tw < 0) return T(0);
-    uint32_t pp, ph, qq, qw;
-    mdivmod(uint32_t(th), a.dU, pp, ph);
-    mdivmod(uint32_t(tw), a.dV, qq, qw);
-    if (ph | qw) return T(0);
+    const uint32_t pp = mdiv(uint32_t(th), a.dU), qq = mdiv(uint32_t(tw), a.dV);
     if (pp >= uint32_t(p.P) || qq >= uint32_t(p.Q)) return T(0);
     return src[rc.base + int64_t(kk) * p.y.sc + int64_t(pp) * p.y.sh + int64_t(qq) * p.y.sw];
   } else {
@@ -126,16 +135,21 @@ __device__ __forceinline__ T load_a(const SimtArgs& a, const RowCtx<T, PASS>& rc
 
 // B(col, k) element of the right operand (stored as [col][k]).
 template <typename T, int PASS>
-__device__ __forceinline__ T load_b(const SimtArgs& a, int64_t col, int64_t k) {
+__device__ __forceinline__ T load_b(const SimtArgs& a, int64_t col, int64_t k, int t0h, int t0w) {
   const ConvProblem& p = a.p;
   if (col >= a.Ncol || k >= a.Kred) return T(0);
   const T* src = static_cast<const T*>(a.b_src);
   if (PASS == FWD) {
     return src[col * a.Kred + k];  // f[kout][crs]
   } else if (PASS == DGRAD) {
-    uint32_t kk, rs;
-    mdivmod(uint32_t(k), a.dRS, kk, rs);
-    return src[(int64_t(kk) * p.C + col) * (p.R * p.S) + rs];  // f[kout][c][r][s]
+    uint32_t kk, rs, jr, js;
+    mdivmod(uint32_t(k), a.dRSph, kk, rs);
+    mdivmod(rs, a.dSph, jr, js);
+    const int32_t ro = t0h + int32_t(p.u) * int32_t(jr);
+    const int32_t so = t0w + int32_t(p.v) * int32_t(js);
+    if (ro >= p.R || so >= p.S) return T(0);
+    const int32_t r = p.flip ? int32_t(p.R - 1 - ro) : ro, s = p.flip ? int32_t(p.S - 1 - so) : so;
+    return src[((int64_t(kk) * p.C + col) * p.R + r) * p.S + s];  // f[kout][c][r][s]
   } else {
     uint32_t c, rs, r, s, n, rem, pp, qq;
     mdivmod(uint32_t(col), a.dRS, c, rs);
@@ -166,7 +180,7 @@ __global__ void __launch_bounds__((SimtCfg<T>::BM / SimtCfg<T>::TM) *
 
   const int tid = threadIdx.x;
   const int64_t m0 = int64_t(blockIdx.x) * BM, n0 = int64_t(blockIdx.y) * BN;
-  const int64_t kbeg = int64_t(blockIdx.z) * a.k_per_split;
+  const int64_t kbeg = (PASS == WGRAD ? int64_t(blockIdx.z) : 0) * a.k_per_split;
   const int64_t kend = min(a.Kred, kbeg + a.k_per_split);
 
   // A mapping: FWD/DGRAD rows fastest (coalesced along q / w); WGRAD k fastest.
@@ -198,17 +212,23 @@ __global__ void __launch_bounds__((SimtCfg<T>::BM / SimtCfg<T>::TM) *
 #pragma unroll
     for (int j = 0; j < TN; j++) acc[i][j] = T(0);
 
+  int t0h = 0, t0w = 0;
+  if (PASS == DGRAD) {
+    const int v = int(a.p.v);
+    t0h = (int(blockIdx.z) / v + int(a.p.pad_h)) % int(a.p.u);
+    t0w = (int(blockIdx.z) - (int(blockIdx.z) / v) * v + int(a.p.pad_w)) % v;
+  }
   T ra[LA], rb[LB];
   auto gload = [&](int64_t k0) {
 #pragma unroll
     for (int j = 0; j < LA; j++) {
       int64_t k = k0 + a_ki[j];
-      ra[j] = k < kend ? load_a<T, PASS>(a, rc[j], k) : T(0);
+      ra[j] = k < kend ? load_a<T, PASS>(a, rc[j], k, t0h, t0w) : T(0);
     }
 #pragma unroll
     for (int j = 0; j < LB; j++) {
       int64_t k = k0 + b_ki[j];
-      rb[j] = k < kend ? load_b<T, PASS>(a, n0 + b_ni[j], k) : T(0);
+      rb[j] = k < kend ? load_b<T, PASS>(a, n0 + b_ni[j], k, t0h, t0w) : T(0);
     }
   };
   auto sstore = [&](int buf) {
@@ -261,9 +281,12 @@ __global__ void __launch_bounds__((SimtCfg<T>::BM / SimtCfg<T>::TM) *
       mdivmod(rem, a.dQ, pp, qq);
       rowoff = int64_t(n) * p.y.sn + int64_t(pp) * p.y.sh + int64_t(qq) * p.y.sw;
     } else if (PASS == DGRAD) {
-      uint32_t n, rem, h, w;
-      mdivmod(uint32_t(m), a.dHW, n, rem);
-      mdivmod(rem, a.dW, h, w);
+      uint32_t n, rem, ii, jj;
+      mdivmod(uint32_t(m), a.dHWph, n, rem);
+      mdivmod(rem, a.dWph, ii, jj);
+      const int h = int(ii) * int(p.u) + int(blockIdx.z) / int(p.v);
+      const int w = int(jj) * int(p.v) + int(blockIdx.z) % int(p.v);
+      if (h >= p.H || w >= p.W) continue;
       rowoff = int64_t(n) * p.x.sn + int64_t(h) * p.x.sh + int64_t(w) * p.x.sw;
     } else {
       rowoff = m * a.Ncol + int64_t(blockIdx.z) * a.M * a.Ncol * (a.splits > 1 ? 1 : 0);
@@ -311,6 +334,10 @@ static void fill_divs(SimtArgs& a) {
   a.dW = make_magic(uint32_t(p.W));
   a.dU = make_magic(uint32_t(p.u));
   a.dV = make_magic(uint32_t(p.v));
+  a.dHWph = make_magic(uint32_t(a.Hph * a.Wph > 0 ? a.Hph * a.Wph : 1));
+  a.dWph = make_magic(uint32_t(a.Wph > 0 ? a.Wph : 1));
+  a.dRSph = make_magic(uint32_t(a.nRp * a.nSp > 0 ? a.nRp * a.nSp : 1));
+  a.dSph = make_magic(uint32_t(a.nSp > 0 ? a.nSp : 1));
 }
 
 template <typename T, int PASS>
@@ -341,7 +368,8 @@ static cudaError_t launch_simt(SimtArgs& a, cudaStream_t st) {
       a.out = ws;
     }
   }
-  dim3 grid(unsigned(gm), unsigned(gn), unsigned(a.splits));
+  dim3 grid(unsigned(gm), unsigned(gn),
+            unsigned(PASS == DGRAD ? a.p.u * a.p.v : a.splits));
   if (gn > 65535) return cudaErrorInvalidConfiguration;
   conv_simt_kernel<T, PASS><<<grid, NT, 0, st>>>(a);
   note_launch();
@@ -380,9 +408,13 @@ static cudaError_t simt_bwd_data(const ConvProblem& p, const void* dy, const voi
   a.a_src = dy;
   a.b_src = f;
   a.out = dx;
-  a.M = p.N * p.H * p.W;
+  a.Hph = int(ceil_div(p.H, p.u));
+  a.Wph = int(ceil_div(p.W, p.v));
+  a.nRp = int(ceil_div(p.R, p.u));
+  a.nSp = int(ceil_div(p.S, p.v));
+  a.M = p.N * a.Hph * a.Wph;
   a.Ncol = p.C;
-  a.Kred = p.K * p.R * p.S;
+  a.Kred = p.K * a.nRp * a.nSp;
   a.accumulate = acc;
   return launch_simt<T, DGRAD>(a, st);
 }
