@@ -11,6 +11,7 @@
 // its partial tile to a workspace; wgrad_reduce sums the splits in fixed order
 // and scatters into the KCRS filter (deterministic; accumulate adds last).
 #include <algorithm>
+#include <type_traits>
 #include <cstdio>
 #include <cstdlib>
 
@@ -297,8 +298,8 @@ cudaError_t launch_wgrad(const WgParams& prm, int mt, int nt, int splits, cudaSt
 // GEMM: D[col][k] = sum over output pixels g of x_im2col[g][col] * dy[g][k],
 // rows = the forward reduction columns col = tap * Cpf + c (x operand, A),
 // columns = output channels k (dy operand, B), reduction = pixels.  Both
-// operands are MN-major 128B-swizzled tiles of 64-wide blocks x kWPx pixels:
-//   x  block = one im2col TMA load (kWPx pixels x 64 channels of one tap,
+// operands are MN-major 128B-swizzled tiles of 64-wide blocks x PX (32 or 64) pixels:
+//   x  block = one im2col TMA load (PX pixels x 64 channels of one tap,
 //              zero fill at the border / past the last image),
 //   dy blocks = ONE 3-D tiled TMA load per plane over the view
 //              {64 channels, pixels, channel block} (block-major in smem).
@@ -306,20 +307,19 @@ cudaError_t launch_wgrad(const WgParams& prm, int mt, int nt, int splits, cudaSt
 // (profiles/r01/tma_rate_probe_v2_depth.txt), so stages are 64 pixels deep
 // and dy needs one instruction per plane.  NC = 2 runs the tile on a CTA
 // pair (M = 256 rows, each CTA loads half of the BN dy channels).
-// Split-K over pixels (multiples of kWPx: only the last stage of the last
+// Split-K over pixels (multiples of PX: only the last stage of the last
 // split runs past NPQ, where both loads zero-fill); each split writes an fp32
 // partial tile, wgrad_reduce_tma sums splits in fixed order and scatters into
 // KCRS (deterministic).
 // ===========================================================================
 namespace {
 
-constexpr int kWgThreads = 6 * 32;  // warp 0 TMA, warp 1 MMA + TMEM, warps 2-5 epilogue
-constexpr int kWPx = 64;            // pixels (reduction depth) per stage
+constexpr int kWgThreads = 8 * 32;  // warps 0-2 TMA, 3 MMA + TMEM, 4-7 epilogue
 
 struct WgTmaParams {
-  CUtensorMap tm_xhi;   // im2col maps of the packed x planes, 64 channels x kWPx pixels
+  CUtensorMap tm_xhi;   // im2col maps of the packed x planes, 64 channels x PX pixels
   CUtensorMap tm_xlo;
-  CUtensorMap tm_dyhi;  // packed dy as {64, NPQ, Kp/64}, box {64, kWPx, BN/NC/64}
+  CUtensorMap tm_dyhi;  // packed dy as {64, NPQ, Kp/64}, box {64, PX, BN/NC/64}
   CUtensorMap tm_dylo;
   int64_t pix_per_split, NPQ;
   int lower_h, lower_w, u, v;  // window origin of output pixel (p, q): lower + o * stride
@@ -330,9 +330,9 @@ struct WgTmaParams {
   unsigned long long* trace;
 };
 
-template <int BN, int NC>
+template <int BN, int NC, int PX>
 struct WgCfg {
-  static constexpr int BLK = kWPx * 128;       // one 64-wide MN block
+  static constexpr int BLK = PX * 128;         // one 64-wide MN block
   static constexpr int B_BLKS = BN / NC / 64;  // dy blocks loaded by each CTA
   static constexpr int A_BYTES = 2 * BLK;      // 128 x-columns
   static constexpr int B_BYTES = B_BLKS * BLK;
@@ -343,9 +343,9 @@ struct WgCfg {
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
 };
 
-template <int BN, int NC>
+template <int BN, int NC, int PX>
 __global__ void __launch_bounds__(kWgThreads, 1) wgrad_tma_kernel(const __grid_constant__ WgTmaParams P) {
-  using C = WgCfg<BN, NC>;
+  using C = WgCfg<BN, NC, PX>;
   constexpr int S = C::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -361,9 +361,10 @@ __global__ void __launch_bounds__(kWgThreads, 1) wgrad_tma_kernel(const __grid_c
   const int n0 = blockIdx.y * BN;
   const int64_t pbeg = int64_t(blockIdx.z) * P.pix_per_split;
   const int64_t pend = min(P.NPQ, pbeg + P.pix_per_split);
-  const int nkb = pend > pbeg ? int((pend - pbeg + kWPx - 1) / kWPx) : 0;
+  const int nkb = pend > pbeg ? int((pend - pbeg + PX - 1) / PX) : 0;
+  constexpr int kMmaW = 3;  // warps 0-2 TMA producers, 3 MMA, 4-7 epilogue
 
-  if (warp == 1) {
+  if (warp == kMmaW) {
     if (lane == 0) {
       for (int s = 0; s < S; s++) {
         ptx::mbar_init(&full[s], NC);
@@ -382,55 +383,64 @@ __global__ void __launch_bounds__(kWgThreads, 1) wgrad_tma_kernel(const __grid_c
   const uint32_t tmem_d = *tmem_slot;
   const uint32_t smem0 = ptx::smem_u32(smem);
 
-  if (warp == 0) {
+  if (warp < 3) {
+    // three producers (one TMA instruction costs its thread ~110-130 cycles):
+    // warp 0 x hi (and arms the stage), warp 1 x lo, warp 2 dy hi + lo
+    const int pw = warp;
     if (lane == 0) {
-      ptx::tma_prefetch(&P.tm_xhi);
-      ptx::tma_prefetch(&P.tm_xlo);
-      ptx::tma_prefetch(&P.tm_dyhi);
-      ptx::tma_prefetch(&P.tm_dylo);
+      if (pw == 0) ptx::tma_prefetch(&P.tm_xhi);
+      if (pw == 1) ptx::tma_prefetch(&P.tm_xlo);
+      if (pw == 2) {
+        ptx::tma_prefetch(&P.tm_dyhi);
+        ptx::tma_prefetch(&P.tm_dylo);
+      }
+      const CUtensorMap* tmx = pw == 0 ? &P.tm_xhi : &P.tm_xlo;
       const int dyblk0 = (n0 + int(rank) * (BN / NC)) / 64;  // this CTA's first dy channel block
       for (int kb = 0; kb < nkb; kb++) {
         const int s = kb % S;
-        const bool tr = P.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && kb < 1024;
+        const bool tr = P.trace && pw == 0 && blockIdx.x == 0 && blockIdx.y == 0 &&
+                        blockIdx.z == 0 && kb < 1024;
         if (tr) P.trace[kb * 4 + 0] = clock64();
         if (kb >= S) ptx::mbar_wait(&empty[s], ((kb / S) - 1) & 1);
         if (tr) P.trace[kb * 4 + 1] = clock64();
-        if (leader) ptx::mbar_arrive_expect_tx(&full[s], C::STAGE_BYTES * NC);
-        else ptx::mbar_arrive_cluster(&full[s], 0);
-        const uint32_t bar = NC == 2 ? ptx::leader_addr(&full[s]) : ptx::smem_u32(&full[s]);
-        const int64_t g = pbeg + int64_t(kb) * kWPx;
-        uint32_t img, rem, pp, qq;
-        mdivmod(uint32_t(g), P.dPQ, img, rem);
-        mdivmod(rem, P.dQ, pp, qq);
-        const int h0 = P.lower_h + int(pp) * P.u, w0 = P.lower_w + int(qq) * P.v;
-        const uint32_t base = smem0 + s * C::STAGE_BYTES;
-#pragma unroll
-        for (int j = 0; j < 2; j++) {
-          const int blk = m0 / 64 + j;
-          const int tap = blk / P.nCB, cb = blk - tap * P.nCB;
-          const bool real = tap < P.taps;
-          const int c = real ? cb * 64 : P.Cext;
-          const uint16_t dh = uint16_t(real ? tap / P.tapW : 0), dw = uint16_t(real ? tap % P.tapW : 0);
-          const uint32_t dst = base + j * C::BLK;
-          if constexpr (NC == 2) {
-            ptx::tma_load_im2col_pair(dst, &P.tm_xhi, c, w0, h0, int(img), dw, dh, bar);
-            ptx::tma_load_im2col_pair(dst + C::A_BYTES, &P.tm_xlo, c, w0, h0, int(img), dw, dh, bar);
-          } else {
-            ptx::tma_load_im2col(dst, &P.tm_xhi, c, w0, h0, int(img), dw, dh, &full[s]);
-            ptx::tma_load_im2col(dst + C::A_BYTES, &P.tm_xlo, c, w0, h0, int(img), dw, dh, &full[s]);
-          }
+        if (pw == 0) {
+          if (leader) ptx::mbar_arrive_expect_tx(&full[s], C::STAGE_BYTES * NC);
+          else ptx::mbar_arrive_cluster(&full[s], 0);
         }
-        const uint32_t db = base + 2 * C::A_BYTES;
-        if constexpr (NC == 2) {
-          ptx::tma_load_3d_pair(db, &P.tm_dyhi, 0, int(g), dyblk0, bar);
-          ptx::tma_load_3d_pair(db + C::B_BYTES, &P.tm_dylo, 0, int(g), dyblk0, bar);
+        const uint32_t bar = NC == 2 ? ptx::leader_addr(&full[s]) : ptx::smem_u32(&full[s]);
+        const int64_t g = pbeg + int64_t(kb) * PX;
+        const uint32_t base = smem0 + s * C::STAGE_BYTES;
+        if (pw < 2) {
+          uint32_t img, rem, pp, qq;
+          mdivmod(uint32_t(g), P.dPQ, img, rem);
+          mdivmod(rem, P.dQ, pp, qq);
+          const int h0 = P.lower_h + int(pp) * P.u, w0 = P.lower_w + int(qq) * P.v;
+          const uint32_t xb = base + (pw == 1 ? C::A_BYTES : 0);
+#pragma unroll
+          for (int j = 0; j < 2; j++) {
+            const int blk = m0 / 64 + j;
+            const int tap = blk / P.nCB, cb = blk - tap * P.nCB;
+            const bool real = tap < P.taps;
+            const int c = real ? cb * 64 : P.Cext;
+            const uint16_t dh = uint16_t(real ? tap / P.tapW : 0), dw = uint16_t(real ? tap % P.tapW : 0);
+            if constexpr (NC == 2)
+              ptx::tma_load_im2col_pair(xb + j * C::BLK, tmx, c, w0, h0, int(img), dw, dh, bar);
+            else
+              ptx::tma_load_im2col(xb + j * C::BLK, tmx, c, w0, h0, int(img), dw, dh, &full[s]);
+          }
         } else {
-          ptx::tma_load_3d(db, &P.tm_dyhi, 0, int(g), dyblk0, &full[s]);
-          ptx::tma_load_3d(db + C::B_BYTES, &P.tm_dylo, 0, int(g), dyblk0, &full[s]);
+          const uint32_t db = base + 2 * C::A_BYTES;
+          if constexpr (NC == 2) {
+            ptx::tma_load_3d_pair(db, &P.tm_dyhi, 0, int(g), dyblk0, bar);
+            ptx::tma_load_3d_pair(db + C::B_BYTES, &P.tm_dylo, 0, int(g), dyblk0, bar);
+          } else {
+            ptx::tma_load_3d(db, &P.tm_dyhi, 0, int(g), dyblk0, &full[s]);
+            ptx::tma_load_3d(db + C::B_BYTES, &P.tm_dylo, 0, int(g), dyblk0, &full[s]);
+          }
         }
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == kMmaW) {
     if (leader) {
       constexpr uint32_t idesc = ptx::idesc_bf16(128 * NC, BN, 1, 1);
       uint32_t acc = 0;
@@ -446,7 +456,7 @@ __global__ void __launch_bounds__(kWgThreads, 1) wgrad_tma_kernel(const __grid_c
         const uint64_t dbh = ptx::desc_mnmajor_sw128(sa + 2 * C::A_BYTES, C::BLK, 1024);
         const uint64_t dbl = ptx::desc_mnmajor_sw128(sa + 2 * C::A_BYTES + C::B_BYTES, C::BLK, 1024);
 #pragma unroll
-        for (int kk = 0; kk < kWPx / 16; kk++) {
+        for (int kk = 0; kk < PX / 16; kk++) {
           const uint64_t o = uint64_t(kk * 2048) >> 4;  // 16 pixels = 2 groups of 8 rows
           if constexpr (NC == 2) {
             ptx::mma_bf16_pair_elect(tmem_d, dal + o, dbh + o, idesc, acc);
@@ -489,7 +499,7 @@ __global__ void __launch_bounds__(kWgThreads, 1) wgrad_tma_kernel(const __grid_c
   ptx::tc_fence_before();
   if constexpr (NC == 2) ptx::cluster_sync();
   else __syncthreads();
-  if (warp == 1) {
+  if (warp == kMmaW) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc_g<C::TMEM_COLS, NC>(tmem_d);
   }
@@ -538,14 +548,14 @@ __global__ void __launch_bounds__(256) wgrad_reduce_tma(WgReduceGeom g, const fl
   }
 }
 
-template <int BN, int NC>
+template <int BN, int NC, int PX>
 cudaError_t launch_wgrad_tma(const WgTmaParams& prm, dim3 grid, cudaStream_t st) {
-  using CC = WgCfg<BN, NC>;
+  using CC = WgCfg<BN, NC, PX>;
   static int attr_dev = -1;
   int dev = 0;
   cudaGetDevice(&dev);
   if (attr_dev != dev) {
-    cudaError_t e = cudaFuncSetAttribute(wgrad_tma_kernel<BN, NC>,
+    cudaError_t e = cudaFuncSetAttribute(wgrad_tma_kernel<BN, NC, PX>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, CC::SMEM);
     if (e != cudaSuccess) return e;
     attr_dev = dev;
@@ -563,7 +573,7 @@ cudaError_t launch_wgrad_tma(const WgTmaParams& prm, dim3 grid, cudaStream_t st)
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   ktime_begin(st, 2);
-  cudaError_t e = cudaLaunchKernelEx(&cfg, wgrad_tma_kernel<BN, NC>, prm);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, wgrad_tma_kernel<BN, NC, PX>, prm);
   ktime_end(st);
   note_launch();
   if (e != cudaSuccess) return e;
@@ -610,10 +620,14 @@ cudaError_t wgrad_tma(const ConvProblem& p, const float* dy, const float* x, flo
   const int mrows = int(ceil_div(ncolx, 128 * nc) * 128 * nc);
   const int ncols = int(ceil_div(Kp64, bn) * bn);
   const int mt = mrows / (128 * nc), nt = ncols / bn;
-  const int64_t kblocks = ceil_div(NPQ, kWPx);
+  // pixels per stage: 64 (measured faster than 32 even where only two
+  // 64-deep stages fit, e.g. conv2 BN=192: 202 vs 266 us)
+  int px = 64;
+  if (getenv("DNNP_WG_PX")) px = atoi(getenv("DNNP_WG_PX")) == 32 ? 32 : 64;
+  const int64_t kblocks = ceil_div(NPQ, px);
   int64_t splits = std::max<int64_t>(1, int64_t(kNumSMs) / (int64_t(mt) * nt * nc));
   splits = std::min<int64_t>({splits, std::max<int64_t>(1, kblocks / 4), 256});
-  const int64_t pps = ceil_div(kblocks, splits) * kWPx;
+  const int64_t pps = ceil_div(kblocks, splits) * px;
   splits = ceil_div(NPQ, pps);
 
   const size_t dy_elems = size_t(NPQ) * Kp64, x_elems = size_t(p.N) * IH * IW * Cp;
@@ -646,13 +660,13 @@ cudaError_t wgrad_tma(const ConvProblem& p, const float* dy, const float* x, flo
   ig.stride_h = gu;
   ig.stride_w = gv;
   ig.cpp = 64;
-  ig.ppc = kWPx;
+  ig.ppc = px;
   if ((e = make_tmap_im2col(&prm.tm_xhi, x_hi, ig, CU_TENSOR_MAP_SWIZZLE_128B)) != cudaSuccess) return e;
   if ((e = make_tmap_im2col(&prm.tm_xlo, x_lo, ig, CU_TENSOR_MAP_SWIZZLE_128B)) != cudaSuccess) return e;
   {
     const uint64_t dims[3] = {64, uint64_t(NPQ), uint64_t(Kp64 / 64)};
     const uint64_t strides[2] = {uint64_t(Kp64) * 2, 128};
-    const uint32_t box[3] = {64, uint32_t(kWPx), uint32_t(bn / nc / 64)};
+    const uint32_t box[3] = {64, uint32_t(px), uint32_t(bn / nc / 64)};
     if ((e = make_tmap_3d(&prm.tm_dyhi, dy_hi, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B)) !=
         cudaSuccess)
       return e;
@@ -681,19 +695,22 @@ cudaError_t wgrad_tma(const ConvProblem& p, const float* dy, const float* x, flo
   if (want_trace) cudaMemsetAsync(tbuf, 0, 8192 * sizeof(unsigned long long), st);
   prm.trace = want_trace ? tbuf : nullptr;
   const dim3 grid{unsigned(mt * nc), unsigned(nt), unsigned(splits)};
-  if (nc == 2) {
-    switch (bn) {
-      case 128: e = launch_wgrad_tma<128, 2>(prm, grid, st); break;
-      default: e = launch_wgrad_tma<256, 2>(prm, grid, st); break;
+  auto go = [&](auto pxc) {
+    constexpr int PX = decltype(pxc)::value;
+    if (nc == 2) {
+      switch (bn) {
+        case 128: return launch_wgrad_tma<128, 2, PX>(prm, grid, st);
+        default: return launch_wgrad_tma<256, 2, PX>(prm, grid, st);
+      }
     }
-  } else {
     switch (bn) {
-      case 64: e = launch_wgrad_tma<64, 1>(prm, grid, st); break;
-      case 128: e = launch_wgrad_tma<128, 1>(prm, grid, st); break;
-      case 192: e = launch_wgrad_tma<192, 1>(prm, grid, st); break;
-      default: e = launch_wgrad_tma<256, 1>(prm, grid, st); break;
+      case 64: return launch_wgrad_tma<64, 1, PX>(prm, grid, st);
+      case 128: return launch_wgrad_tma<128, 1, PX>(prm, grid, st);
+      case 192: return launch_wgrad_tma<192, 1, PX>(prm, grid, st);
+      default: return launch_wgrad_tma<256, 1, PX>(prm, grid, st);
     }
-  }
+  };
+  e = px == 32 ? go(std::integral_constant<int, 32>()) : go(std::integral_constant<int, 64>());
   if (e != cudaSuccess) return e;
   if (want_trace) {
     static unsigned long long h[8192];

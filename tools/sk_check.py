@@ -42,15 +42,16 @@ def main():
             else:
                 op = lambda: dp.conv_backward_data(L["dyv"], L["fv"], L["cd"], "implicit", L["dxv"])
                 out = L["dxv"].buf
-            os.environ["DNNP_TC_NO_SK"] = "1"
+            os.environ.pop("DNNP_TC_SK", None)
             t_dp = timed(op)
             op()
             torch.cuda.synchronize()
             ref = out.clone()
-            os.environ.pop("DNNP_TC_NO_SK")
+            os.environ["DNNP_TC_SK"] = "1"
             t_sk = timed(op)
             op()
             torch.cuda.synchronize()
+            os.environ.pop("DNNP_TC_SK", None)
             d = (out - ref).abs().max().item() / max(ref.abs().max().item(), 1e-30)
             print(f"{L['name']}.{pas}: no-SK {t_dp:7.1f} us  SK {t_sk:7.1f} us  max|diff|/max|ref| {d:.2e}",
                   flush=True)
