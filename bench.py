@@ -428,6 +428,8 @@ def run_e2e(dp, layers, torch, device, ws, args, step_flops):
         b.record()
         torch.cuda.synchronize()
         ms.append(a.elapsed_time(b))
+    if os.environ.get("DNNP_BENCH_DEBUG"):
+        print("e2e step ms:", " ".join(f"{m:.2f}" for m in ms), file=sys.stderr)
     tot = float(np.sum(ms))
     if ws > 1:
         import torch.distributed as dist

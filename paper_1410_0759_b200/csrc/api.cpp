@@ -280,10 +280,7 @@ struct Staged {
 class Stager {
  public:
   explicit Stager(cudaStream_t st) : st_(st) {}
-  ~Stager() {
-    for (auto& b : bufs_)
-      if (b.host && b.dev) cudaFreeAsync(b.dev, st_);
-  }
+  ~Stager() { dnnp::tc::scratch_close(scratch_); }
   // copy_in: the kernel (or the gaps of a strided view) needs the caller's
   // current contents.
   dnnp_status add(const void* user, size_t bytes, bool out, bool copy_in, void** dev) {
@@ -295,15 +292,14 @@ class Stager {
     if (!b.host) {
       b.dev = const_cast<void*>(user);
     } else {
-      dnnp::tc::pool_keep_memory();  // staging buffers recycle through the stream pool
-      cudaError_t e = cudaMallocAsync(&b.dev, std::max<size_t>(bytes, 16), st_);
+      // staging buffers come from the per-stream scratch arena (no
+      // allocation in steady state); released when the call returns
+      if (!scratch_) scratch_ = dnnp::tc::scratch_open(st_);
+      cudaError_t e = dnnp::tc::scratch_alloc(scratch_, std::max<size_t>(bytes, 16), &b.dev);
       if (e != cudaSuccess) return cuda_status(e, "staging allocation");
       if (copy_in) {
         e = cudaMemcpyAsync(b.dev, user, bytes, cudaMemcpyHostToDevice, st_);
-        if (e != cudaSuccess) {
-          cudaFreeAsync(b.dev, st_);
-          return cuda_status(e, "host->device copy");
-        }
+        if (e != cudaSuccess) return cuda_status(e, "host->device copy");
       }
       any_host_ = true;
     }
@@ -325,9 +321,6 @@ class Stager {
       }
     }
     if (any_host_) {
-      for (auto& b : bufs_)
-        if (b.host && b.dev) cudaFreeAsync(b.dev, st_);
-      for (auto& b : bufs_) b.dev = b.host ? nullptr : b.dev;
       cudaError_t e = cudaStreamSynchronize(st_);
       if (e != cudaSuccess) return cuda_status(e, "stream synchronize");
     }
@@ -338,6 +331,7 @@ class Stager {
   cudaStream_t st_;
   std::vector<Staged> bufs_;
   bool any_host_ = false;
+  dnnp::tc::ScratchScope* scratch_ = nullptr;
 };
 
 size_t span_bytes(dnnp_tensor_desc d) { return size_t(max_offset(d) + 1) * elem_size(d->elem); }

@@ -1124,8 +1124,10 @@ cudaError_t run_tc(bool dgrad, const ConvProblem& p, const float* in, const View
   // the TMA traffic) shrinks to (S + v) / (2 S) of its bytes.
   // (measured: helps the unit-stride bwd-data of conv2, 233 -> 204 us; not the
   // space-to-depth conv1 passes, whose epilogue then dominates)
-  const bool blockable = g.tma && pg.Ncol <= 64 && !s2d && g.out_mode == 0 &&
-                         (env_off("DNNP_TC_BLOCK") || dgrad) && !env_off("DNNP_TC_NO_BLOCK");
+  const bool blockable =
+      g.tma && pg.Ncol <= 64 && !env_off("DNNP_TC_NO_BLOCK") &&
+      (env_off("DNNP_TC_BLOCK_S2D") ? (!dgrad ? g.out_mode == 0 : (s2d || g.out_mode == 0))
+                                    : (!s2d && g.out_mode == 0 && (env_off("DNNP_TC_BLOCK") || dgrad)));
   if (blockable) {
     const int bw = 2;
     Gemm gb = g;

@@ -38,6 +38,13 @@ struct ConvProblem {
 namespace tc {
 // keep stream-ordered pool memory across synchronizations (release threshold max)
 void pool_keep_memory();
+// Scratch scope for host code (api.cpp): allocations come from the
+// per-stream arena (tc_common.cuh Workspace) and are released when the scope
+// closes; the arena stays locked for the scope's lifetime.
+struct ScratchScope;
+ScratchScope* scratch_open(cudaStream_t st);
+cudaError_t scratch_alloc(ScratchScope* s, size_t bytes, void** p);
+void scratch_close(ScratchScope* s);
 }  // namespace tc
 
 // Launch bookkeeping: every kernel this library launches bumps a counter

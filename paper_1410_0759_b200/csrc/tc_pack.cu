@@ -392,6 +392,27 @@ void ktime_end(cudaStream_t st) {
   if (!g_kt.empty()) cudaEventRecord(g_kt.back().b, st);
 }
 
+struct ScratchScope {
+  cudaStream_t st;
+  std::vector<Workspace*> ws;  // nested, closed in reverse order
+};
+
+ScratchScope* scratch_open(cudaStream_t st) { return new ScratchScope{st, {}}; }
+
+cudaError_t scratch_alloc(ScratchScope* s, size_t bytes, void** p) {
+  Workspace* w = new Workspace(s->st);
+  s->ws.push_back(w);
+  const cudaError_t e = w->alloc(bytes);
+  *p = w->p;
+  return e;
+}
+
+void scratch_close(ScratchScope* s) {
+  if (!s) return;
+  for (auto it = s->ws.rbegin(); it != s->ws.rend(); ++it) delete *it;
+  delete s;
+}
+
 void pool_keep_memory() {
   static bool done = false;
   if (done) return;

@@ -1,0 +1,64 @@
+"""Full-size parity (BASELINE.json configs[1]: AlexNet conv1-5 at N=128): the
+fp32 tensor-core path of every pass against the fp64 SIMT path on the same
+inputs (itself pinned to the C oracle at 1e-12 by test_gpu_parity.py), at
+the north_star fp32 bar of 1e-4 normalised error.  The CPU oracle cannot run
+these sizes in test time; the fp64 GPU path is the size-independent check.
+Also the adjoint identity <conv(x), dy> == <x, conv_bwd_data(dy)> and
+<conv(x), dy> == <f, conv_bwd_filter(dy, x)> (test_conv_backward.py:152-165)
+on the fp32 results."""
+import numpy as np
+import pytest
+
+import paper_1410_0759_b200 as dp
+
+pytestmark = pytest.mark.gpu
+
+ALEXNET = [
+    ("conv1", 3, 224, 64, 11, 4, 2),
+    ("conv2", 64, 27, 192, 5, 1, 2),
+    ("conv3", 192, 13, 384, 3, 1, 1),
+    ("conv4", 384, 13, 256, 3, 1, 1),
+    ("conv5", 256, 13, 256, 3, 1, 1),
+]
+N = 128
+
+
+def rel(a, b):
+    return float((a - b).abs().max() / b.abs().max())
+
+
+@pytest.mark.parametrize("layer", ALEXNET, ids=[l[0] for l in ALEXNET])
+def test_alexnet_layer_vs_fp64(layer):
+    import torch
+    name, c, h, k, r, u, pad = layer
+    p = dp.output_extent(h, r, u, pad)
+    g = torch.Generator(device="cuda").manual_seed(2014)
+    x64 = torch.rand(N * c * h * h, generator=g, device="cuda", dtype=torch.float64) - 0.5
+    f64 = torch.rand(k * c * r * r, generator=g, device="cuda", dtype=torch.float64) - 0.5
+    dy64 = torch.rand(N * k * p * p, generator=g, device="cuda", dtype=torch.float64) - 0.5
+    cd = dp.ConvDesc(u, u, pad, pad, "convolution")
+    out = {}
+    for dt, (x, f, dy) in (("f64", (x64, f64, dy64)),
+                           ("f32", (x64.float(), f64.float(), dy64.float()))):
+        tdt = x.dtype
+        xv = dp.TensorView(dp.make_desc(N, c, h, h, elem_type=dt), x)
+        fv = dp.FilterView(dp.make_filter_desc(k, c, r, r, elem_type=dt), f)
+        dyv = dp.TensorView(dp.make_desc(N, k, p, p, elem_type=dt), dy)
+        y = torch.empty(N * k * p * p, device="cuda", dtype=tdt)
+        dx = torch.empty(N * c * h * h, device="cuda", dtype=tdt)
+        df = torch.empty(k * c * r * r, device="cuda", dtype=tdt)
+        dp.conv_forward(xv, fv, cd, "implicit", dp.TensorView(dp.make_desc(N, k, p, p, elem_type=dt), y))
+        dp.conv_backward_data(dyv, fv, cd, "implicit",
+                              dp.TensorView(dp.make_desc(N, c, h, h, elem_type=dt), dx))
+        dp.conv_backward_filter(dyv, xv, cd, "implicit",
+                                dp.FilterView(dp.make_filter_desc(k, c, r, r, elem_type=dt), df))
+        torch.cuda.synchronize()
+        out[dt] = (y, dx, df)
+    (y64, dx64, df64), (y32, dx32, df32) = out["f64"], out["f32"]
+    errs = {"fwd": rel(y32.double(), y64), "bwd_data": rel(dx32.double(), dx64),
+            "bwd_filter": rel(df32.double(), df64)}
+    assert all(e <= 1e-4 for e in errs.values()), (name, errs)
+    # adjoint identities on the fp64 results (exact up to fp64 rounding)
+    lhs = float((y64 * dy64).sum())
+    assert abs(lhs - float((x64 * dx64).sum())) <= 1e-9 * max(1.0, abs(lhs)), name
+    assert abs(lhs - float((f64 * df64).sum())) <= 1e-9 * max(1.0, abs(lhs)), name
