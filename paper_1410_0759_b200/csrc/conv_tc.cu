@@ -852,6 +852,7 @@ cudaError_t run_gemm(const ConvProblem& p, Gemm g, const __nv_bfloat16* a_hi,
     prm.dOHW = make_magic(uint32_t(g.OH * g.OW));
     prm.dOW = make_magic(uint32_t(g.OW));
     prm.skip = getenv("DNNP_TC_SKIP") ? atoi(getenv("DNNP_TC_SKIP")) : 0;
+    prm.prefetch = getenv("DNNP_TC_PREFETCH") ? atoi(getenv("DNNP_TC_PREFETCH")) : 0;
     // stream-K over the last, partial wave of tiles
     Workspace skw(st);
     {

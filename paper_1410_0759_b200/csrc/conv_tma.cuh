@@ -57,6 +57,7 @@ struct TmaParams {
   int plain;                   // alpha == 1, beta == 0: store the accumulator as is
   MagicDiv dOHW, dOW;
   int skip;                    // experiments: 1 = no A loads, 2 = no loads, 4 = no MMAs
+  int prefetch;                // L2 prefetch of the next tile's im2col window
   unsigned long long* trace;   // debug: CTA-0 clock64 stamps (or null)
 };
 
@@ -208,6 +209,25 @@ __global__ void __launch_bounds__(kTmaThreads, 1) conv_tma_kernel(const __grid_c
         mdivmod(m0, P.dOHW, img, rem);
         mdivmod(rem, P.dOW, oh, ow);
         const int h0 = P.lower_h + int(oh) * P.u, w0 = P.lower_w + int(ow) * P.v;
+        if (P.prefetch && np == 1 && tile + ncl < P.tiles) {
+          // warm L2 with the next tile's window (first and last tap, every
+          // channel block): its first loads otherwise pay DRAM latency
+          const uint32_t m1 = uint32_t((tile + ncl) / P.nt) * (kBM * NC) + rank * kBM;
+          uint32_t img1, rem1, oh1, ow1;
+          mdivmod(m1, P.dOHW, img1, rem1);
+          mdivmod(rem1, P.dOW, oh1, ow1);
+          const int h1 = P.lower_h + int(oh1) * P.u, w1 = P.lower_w + int(ow1) * P.v;
+          const int taps = (P.KCH + P.nCB - 1) / P.nCB;
+          const int lt = taps - 1;
+          for (int cbp = 0; cbp < P.nCB; cbp++) {
+            ptx::tma_prefetch_im2col(&P.tm_ahi, cbp * CB, w1, h1, int(img1), 0, 0);
+            ptx::tma_prefetch_im2col(&P.tm_alo, cbp * CB, w1, h1, int(img1), 0, 0);
+            ptx::tma_prefetch_im2col(&P.tm_ahi, cbp * CB, w1, h1, int(img1), uint16_t(lt % P.tapW),
+                                     uint16_t(lt / P.tapW));
+            ptx::tma_prefetch_im2col(&P.tm_alo, cbp * CB, w1, h1, int(img1), uint16_t(lt % P.tapW),
+                                     uint16_t(lt / P.tapW));
+          }
+        }
         int kc = kb0 * C::SUB;
         int tapi = kc / P.nCB, cb = kc - tapi * P.nCB;
         int dh = tapi / P.tapW, dw = tapi - dh * P.tapW;

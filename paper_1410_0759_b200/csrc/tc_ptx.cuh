@@ -115,6 +115,16 @@ __device__ __forceinline__ void tma_load_im2col(uint32_t dst, const void* tmap, 
       : "memory");
 }
 
+// L2 prefetch of an im2col box (no shared-memory destination, no barrier)
+__device__ __forceinline__ void tma_prefetch_im2col(const void* tmap, int c, int w, int h, int n,
+                                                    uint16_t off_w, uint16_t off_h) {
+  asm volatile(
+      "cp.async.bulk.prefetch.tensor.4d.L2.global.im2col [%0, {%1, %2, %3, %4}], {%5, %6};" ::"l"(
+          reinterpret_cast<uint64_t>(tmap)),
+      "r"(c), "r"(w), "r"(h), "r"(n), "h"(off_w), "h"(off_h)
+      : "memory");
+}
+
 // ---- clusters / CTA pairs (cta_group::2) ----------------------------------
 __device__ __forceinline__ uint32_t cluster_ctarank() {
   uint32_t r;
