@@ -330,6 +330,17 @@ struct WgTmaParams {
   unsigned long long* trace;
 };
 
+// Longest reduction (pixels) accumulated in one TMEM accumulator.  The
+// tensor-core fp32 accumulation truncates, so its error grows linearly with
+// the chain (measured: ~3.5e-5 of max|dW| at 8k pixels); longer reductions
+// are split and the splits summed in IEEE fp32 by the reduce kernel, which
+// keeps every wgrad at the north_star 1e-4 bar whatever N*P*Q is.
+static int64_t max_chain(int px) {
+  int64_t c = 8192;
+  if (const char* e = getenv("DNNP_WG_CHAIN")) c = std::max<int64_t>(atoll(e), px);
+  return c / px * px;
+}
+
 template <int BN, int NC, int PX>
 struct WgCfg {
   static constexpr int BLK = PX * 128;         // one 64-wide MN block
@@ -627,7 +638,7 @@ cudaError_t wgrad_tma(const ConvProblem& p, const float* dy, const float* x, flo
   const int64_t kblocks = ceil_div(NPQ, px);
   int64_t splits = std::max<int64_t>(1, int64_t(kNumSMs) / (int64_t(mt) * nt * nc));
   splits = std::min<int64_t>({splits, std::max<int64_t>(1, kblocks / 4), 256});
-  const int64_t pps = ceil_div(kblocks, splits) * px;
+  const int64_t pps = std::min(ceil_div(kblocks, splits) * px, max_chain(px));
   splits = ceil_div(NPQ, pps);
 
   const size_t dy_elems = size_t(NPQ) * Kp64, x_elems = size_t(p.N) * IH * IW * Cp;
@@ -763,7 +774,7 @@ cudaError_t tc_backward_filter(const ConvProblem& p, const float* dy, const floa
   const int64_t kblocks = ceil_div(NPQ, kPx);
   int64_t splits = ceil_div(int64_t(kNumSMs) * 2, int64_t(mt) * nt);
   splits = std::max<int64_t>(1, std::min<int64_t>({splits, std::max<int64_t>(1, kblocks / 8), 128}));
-  const int64_t pps = ceil_div(kblocks, splits) * kPx;
+  const int64_t pps = std::min(ceil_div(kblocks, splits) * kPx, max_chain(kPx));
   splits = ceil_div(NPQ, pps);
 
   const size_t dy_elems = size_t(NPQ) * Kp, x_elems = size_t(NHW) * Cp;

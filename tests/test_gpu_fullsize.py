@@ -62,3 +62,40 @@ def test_alexnet_layer_vs_fp64(layer):
     lhs = float((y64 * dy64).sum())
     assert abs(lhs - float((x64 * dx64).sum())) <= 1e-9 * max(1.0, abs(lhs)), name
     assert abs(lhs - float((f64 * df64).sum())) <= 1e-9 * max(1.0, abs(lhs)), name
+
+
+# Paper Table 2 layers (suites/table2.suite) at the reference's verify batch:
+# long reductions (layer1 dW sums 16*118*118 = 222784 products per weight,
+# layer3 forward sums 10368) that expose the tensor-core accumulator's
+# truncation unless the reduction chain is bounded.
+TABLE2 = [("layer1", 3, 128, 96, 11), ("layer2", 96, 64, 128, 9), ("layer3", 128, 32, 128, 9),
+          ("layer4", 128, 16, 128, 7), ("layer5", 128, 13, 384, 3)]
+
+
+@pytest.mark.parametrize("layer", TABLE2, ids=[l[0] for l in TABLE2])
+def test_table2_layer_vs_fp64(layer):
+    import torch
+    name, c, h, k, r = layer
+    n, p = 16, h - r + 1
+    g = torch.Generator(device="cuda").manual_seed(7)
+    x64 = torch.rand(n * c * h * h, generator=g, device="cuda", dtype=torch.float64) - 0.5
+    f64 = torch.rand(k * c * r * r, generator=g, device="cuda", dtype=torch.float64) - 0.5
+    dy64 = torch.rand(n * k * p * p, generator=g, device="cuda", dtype=torch.float64) - 0.5
+    cd = dp.ConvDesc(1, 1, 0, 0)
+    out = {}
+    for dt, (x, f, dy) in (("f64", (x64, f64, dy64)),
+                           ("f32", (x64.float(), f64.float(), dy64.float()))):
+        y = dp.empty_view(dp.make_desc(n, k, p, p, elem_type=dt), device="cuda")
+        dx = dp.empty_view(dp.make_desc(n, c, h, h, elem_type=dt), device="cuda")
+        df = dp.FilterView(dp.make_filter_desc(k, c, r, r, elem_type=dt), torch.empty_like(f))
+        xv = dp.TensorView(dp.make_desc(n, c, h, h, elem_type=dt), x)
+        fv = dp.FilterView(dp.make_filter_desc(k, c, r, r, elem_type=dt), f)
+        dyv = dp.TensorView(dp.make_desc(n, k, p, p, elem_type=dt), dy)
+        dp.conv_forward(xv, fv, cd, "implicit", y)
+        dp.conv_backward_data(dyv, fv, cd, "implicit", dx)
+        dp.conv_backward_filter(dyv, xv, cd, "implicit", df)
+        torch.cuda.synchronize()
+        out[dt] = (y.buf, dx.buf, df.buf)
+    errs = {pas: rel(a.double(), b) for pas, a, b in zip(("fwd", "bwd_data", "bwd_filter"),
+                                                        out["f32"], out["f64"])}
+    assert all(e <= 1e-4 for e in errs.values()), (name, errs)
