@@ -41,6 +41,9 @@ struct TmaParams {
   int Ncol;            // valid GEMM columns
   int lower_h, lower_w, u, v;  // window origin of output pixel (oh, ow): lower + o * stride
   int nCB, tapW, KCH, nkb;     // channel blocks per tap, taps per window row, chunks, k-blocks
+  int kb_lo;                   // first k-block of this launch (reduction segment [kb_lo, nkb))
+  int nseg;                    // reduction segments per tile (consecutive work items of one
+                               // cluster; segment s > 0 adds alpha*acc to the stored output)
   int Cext;                    // channel extent of the A maps (OOB coordinate for padding chunks)
   int nt, tiles;               // column tiles, tiles (of NC * 128 rows)
   // stream-K: full waves W (tiles cid + i*G), then units [cid*U/G, (cid+1)*U/G)
@@ -98,12 +101,16 @@ __host__ __device__ __forceinline__ int sk_owner(int x, int U, int G) {
 // The sequence of work items of one cluster: (tile, k-block range, piece of
 // the tile, pieces of the tile); every role of the cluster walks it alike.
 struct WorkIter {
-  int cid, G, nkb, tiles, sk, W, U, G2;
+  int cid, G, nkb, kb_lo, tiles, sk, W, U, G2, nseg;
   int i, u, uend;
+  int seg;  // reduction segment of the last item (0 unless P.nseg > 1)
   __device__ void init(const TmaParams& P, int cid_, int G_) {
     cid = cid_;
     G = G_;
     nkb = P.nkb;
+    kb_lo = P.kb_lo;
+    nseg = P.nseg;
+    seg = 0;
     tiles = P.tiles;
     sk = P.sk;
     W = P.W;
@@ -116,11 +123,24 @@ struct WorkIter {
     uend = (sk && cid < G2) ? int((int64_t(cid + 1) * U) / G2) : 0;
   }
   __device__ bool next(int& tile, int& kb0, int& kb1, int& piece, int& np) {
+    if (nseg > 1) {
+      const int t = i / nseg;
+      seg = i - t * nseg;
+      tile = cid + t * G;
+      if (tile >= tiles) return false;
+      i++;
+      const int span = nkb - kb_lo;
+      kb0 = kb_lo + int(int64_t(span) * seg / nseg);
+      kb1 = kb_lo + int(int64_t(span) * (seg + 1) / nseg);
+      piece = 0;
+      np = 1;
+      return true;
+    }
     if (!sk) {
       tile = cid + i * G;
       if (tile >= tiles) return false;
       i++;
-      kb0 = 0;
+      kb0 = kb_lo;
       kb1 = nkb;
       piece = 0;
       np = 1;
@@ -393,6 +413,9 @@ __global__ void __launch_bounds__(kTmaThreads, 1) conv_tma_kernel(const __grid_c
         if (finisher) __threadfence();
       }
       if (finisher) {
+        // segments after the first add to what the first stored
+        const float beta = wi.seg ? 1.0f : P.beta;
+        const bool plain = P.plain && wi.seg == 0;
         // mode 0: row base at the output pixel; mode 1: at (oh*o_u - o_ph, ow*o_v - o_pw)
         const int hb = int(oh) * P.o_u - P.o_ph, wb = int(ow) * P.o_v - P.o_pw;
         const int64_t rowoff =
@@ -418,7 +441,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) conv_tma_kernel(const __grid_c
             }
           }
           if (!row_ok) continue;
-          if (P.out_mode == 0 && P.plain && cbase + 32 <= P.Ncol) {
+          if (P.out_mode == 0 && plain && cbase + 32 <= P.Ncol) {
             float* dst = P.out + rowoff + int64_t(cbase) * P.o_sc;
             const int64_t sc = P.o_sc;
 #pragma unroll
@@ -428,13 +451,17 @@ __global__ void __launch_bounds__(kTmaThreads, 1) conv_tma_kernel(const __grid_c
             }
           } else if (P.out_mode == 0) {
             float* rowp = P.out + rowoff + int64_t(cbase) * P.o_sc;
+            // all 32 old values are loaded before any store (one latency, not 32)
+            float old[32];
+#pragma unroll
+            for (int i = 0; i < 32; i++)
+              old[i] = (beta != 0.0f && cbase + i < P.Ncol) ? rowp[int64_t(i) * P.o_sc] : 0.0f;
 #pragma unroll
             for (int i = 0; i < 32; i++) {
               if (cbase + i < P.Ncol) {
-                float* dst = rowp + int64_t(i) * P.o_sc;
                 float val = __fmul_rn(__uint_as_float(v[i]), P.alpha);
-                if (P.beta != 0.0f) val = __fadd_rn(__fmul_rn(*dst, P.beta), val);
-                *dst = val;
+                if (beta != 0.0f) val = __fadd_rn(__fmul_rn(old[i], beta), val);
+                rowp[int64_t(i) * P.o_sc] = val;
               }
             }
           } else if (ctab_smem) {
@@ -447,9 +474,9 @@ __global__ void __launch_bounds__(kTmaThreads, 1) conv_tma_kernel(const __grid_c
                     unsigned(wb + (hw & 0xFFFF)) < unsigned(P.o_W)) {
                   float* dst = P.out + rowoff + col_off[col];
                   float val = __uint_as_float(v[i]);
-                  if (!P.plain) {
+                  if (!plain) {
                     val = __fmul_rn(val, P.alpha);
-                    if (P.beta != 0.0f) val = __fadd_rn(__fmul_rn(*dst, P.beta), val);
+                    if (beta != 0.0f) val = __fadd_rn(__fmul_rn(*dst, beta), val);
                   }
                   *dst = val;
                 }
@@ -466,7 +493,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) conv_tma_kernel(const __grid_c
                   float* dst = P.out + rowoff + int64_t(e & 0xFFFF) * P.o_sc + int64_t(ph) * P.o_sh +
                                int64_t(pw) * P.o_sw;
                   float val = __fmul_rn(__uint_as_float(v[i]), P.alpha);
-                  if (P.beta != 0.0f) val = __fadd_rn(__fmul_rn(*dst, P.beta), val);
+                  if (beta != 0.0f) val = __fadd_rn(__fmul_rn(*dst, beta), val);
                   *dst = val;
                 }
               }

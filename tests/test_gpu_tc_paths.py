@@ -185,3 +185,27 @@ def test_accumulate_all_passes():
     check(run_case((2, 3, 32, 36, 64, 11, 11, 4, 4, 2, 2), accumulate=True, seed=10))
     check(run_case((2, 64, 15, 15, 96, 5, 5, 1, 1, 2, 2), passes=("bwd_data",), accumulate=True,
                    seed=10))
+
+
+@pytest.mark.parametrize("tma", [1, 0], ids=["tma", "cp_async"])
+@pytest.mark.parametrize("alpha,beta,accumulate", [(1.0, 0.0, False), (0.5, -0.75, False),
+                                                   (1.0, 0.0, True)])
+def test_reduction_segments(tma, alpha, beta, accumulate):
+    """Reductions split into k-block segments chained through the output
+    (DNNP_TC_CHAIN forces several segments on a small problem; the wgrad
+    analogue DNNP_WG_CHAIN forces more splits)."""
+    kv = dict(DNNP_TC_CHAIN=128, DNNP_WG_CHAIN=64)
+    if not tma:
+        kv["DNNP_TC_NO_TMA"] = 1
+    with env(**kv):
+        check(run_case((2, 40, 11, 9, 24, 3, 3, 1, 1, 1, 1), alpha=alpha, beta=beta,
+                       accumulate=accumulate, seed=11))
+        check(run_case((2, 3, 32, 36, 64, 11, 11, 4, 4, 2, 2), passes=("fwd", "bwd_data"),
+                       alpha=alpha, beta=beta, accumulate=accumulate, seed=11))
+
+
+def test_long_reduction_accuracy():
+    """C*R*S = 512*49 = 25088 products per output: past the single-accumulator
+    truncation budget, so the forward / bwd-data run segmented (vs fp64)."""
+    check(run_case((2, 512, 9, 9, 64, 7, 7, 1, 1, 3, 3), passes=("fwd",), seed=12))
+    check(run_case((2, 64, 9, 9, 512, 7, 7, 1, 1, 3, 3), passes=("bwd_data",), seed=12))
