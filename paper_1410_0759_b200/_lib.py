@@ -62,6 +62,10 @@ _SIGS = {
     "dnnp_conv_output_shape": [vp, vp, vp, c_i64p, c_i64p, c_i64p, c_i64p],
     "dnnp_convolution_forward": [vp, vp, vp, vp, vp, vp, vp, ctypes.c_int, vp, vp, vp],
     "dnnp_convolution_backward_data": [vp, vp, vp, vp, vp, vp, ctypes.c_int, vp, vp],
+    "dnnp_convolution_bias_activation_forward": [vp, vp, vp, vp, vp, vp, vp, ctypes.c_int, vp,
+                                                 vp, vp, ctypes.c_int, vp, vp],
+    "dnnp_convolution_backward_data_activation": [vp, vp, vp, vp, vp, vp, ctypes.c_int,
+                                                  ctypes.c_int, vp, vp, vp, vp],
     "dnnp_convolution_backward_filter": [vp, vp, vp, vp, vp, vp, ctypes.c_int, vp, vp],
     "dnnp_convolution_backward_bias": [vp, vp, vp, vp, vp],
     "dnnp_activation_forward": [vp, ctypes.c_int, vp, vp, vp, vp],

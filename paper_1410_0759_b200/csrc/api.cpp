@@ -779,6 +779,99 @@ dnnp_status dnnp_convolution_backward_bias(dnnp_handle handle, dnnp_tensor_desc 
   return sg.finish(e);
 }
 
+// ------------------------------------------------ fused epilogues (additive)
+
+static bool act_valid(dnnp_activation_kind k);
+static dnnp_status check_like(dnnp_tensor_desc a, dnnp_tensor_desc b, const char* what);
+
+dnnp_status dnnp_convolution_bias_activation_forward(
+    dnnp_handle handle, const void* alpha, dnnp_tensor_desc xd, const void* x, dnnp_filter_desc fd,
+    const void* f, dnnp_conv_desc cd, dnnp_engine engine, const void* beta, dnnp_tensor_desc bd,
+    const void* bias, int activation, dnnp_tensor_desc yd, void* y) {
+  if (!reg_has(handle, KIND_HANDLE) || !alpha || !beta)
+    return fail(DNNP_STATUS_BAD_PARAM, "conv_bias_act: bad handle or scalar pointer");
+  if (activation != DNNP_ACTIVATION_NONE && !act_valid(dnnp_activation_kind(activation)))
+    return fail(DNNP_STATUS_BAD_PARAM, "conv_bias_act: bad activation kind");
+  if (!tensor_usable(xd, x) || !filter_usable(fd, f) || !tensor_usable(yd, y))
+    return fail(DNNP_STATUS_BAD_PARAM, "conv_bias_act: unusable descriptor or NULL buffer");
+  if ((bd == nullptr) != (bias == nullptr) || (bd && !tensor_usable(bd, bias)))
+    return fail(DNNP_STATUS_BAD_PARAM, "conv_bias_act: bias descriptor and buffer must pair");
+  if (!reg_has(cd, KIND_CONV) || !cd->configured)
+    return fail(DNNP_STATUS_BAD_PARAM, "conv_bias_act: conv descriptor not configured");
+  if (!engine_valid(engine)) return fail(DNNP_STATUS_BAD_PARAM, "conv_bias_act: bad engine");
+  dnnp_status st;
+  if ((st = bind_view(xd, "x")) || (st = bind_view(yd, "y"))) return st;
+  if (bd && (st = bind_view(bd, "bias"))) return st;
+  double a = read_scalar(alpha, yd->elem), b = read_scalar(beta, yd->elem);
+  int64_t P, Q;
+  if ((st = conv_shape(xd, fd, cd, &P, &Q))) return st;
+  if ((st = check_out(yd, xd->n, fd->k, P, Q, xd->elem, "output"))) return st;
+  if (bd && (bd->n != 1 || bd->c != fd->k || bd->h != 1 || bd->w != 1 || bd->elem != yd->elem))
+    return fail(DNNP_STATUS_SHAPE_MISMATCH, "bias must be (1, %lld, 1, 1) of y's type",
+                (long long)fd->k);
+  if (cd->accumulate) b = 1.0;  // reference conv.py:573-574
+  dnnp::ConvProblem pr = make_problem(xd, fd, cd, yd, P, Q);
+  if ((st = check_decode_range(pr))) return st;
+  if ((st = need_device())) return st;
+  Stager sg(handle->stream);
+  void *dx, *df, *dy, *db = nullptr;
+  size_t fbytes = size_t(fd->k * fd->c * fd->r * fd->s) * elem_size(fd->elem);
+  if ((st = sg.add(x, span_bytes(xd), false, true, &dx))) return st;
+  if ((st = sg.add(f, fbytes, false, true, &df))) return st;
+  if (bd && (st = sg.add(bias, span_bytes(bd), false, true, &db))) return st;
+  if ((st = sg.add(y, span_bytes(yd), true, b != 0.0 || !dense_view(yd), &dy))) return st;
+  dnnp::ConvEpilogue ep;
+  ep.act = activation;
+  if (bd) {
+    ep.bias = db;
+    ep.biasv = view_of(bd);
+    ep.bias_stride = ep.biasv.sc;
+  }
+  cudaError_t e = dnnp::conv_forward_fused(pr, dnnp::Dtype(xd->elem), dx, df, dy, a, b,
+                                           handle->math, ep, handle->stream);
+  return sg.finish(e);
+}
+
+dnnp_status dnnp_convolution_backward_data_activation(
+    dnnp_handle handle, dnnp_filter_desc fd, const void* f, dnnp_tensor_desc dyd, const void* dy,
+    dnnp_conv_desc cd, dnnp_engine engine, dnnp_activation_kind activation, dnnp_tensor_desc gd,
+    const void* g, dnnp_tensor_desc dxd, void* dx) {
+  if (!reg_has(handle, KIND_HANDLE) || !act_valid(activation))
+    return fail(DNNP_STATUS_BAD_PARAM, "conv_bwd_data_act: bad handle or activation kind");
+  if (!filter_usable(fd, f) || !tensor_usable(dyd, dy) || !tensor_usable(dxd, dx) ||
+      !tensor_usable(gd, g))
+    return fail(DNNP_STATUS_BAD_PARAM, "conv_bwd_data_act: unusable descriptor or buffer");
+  if (!reg_has(cd, KIND_CONV) || !cd->configured)
+    return fail(DNNP_STATUS_BAD_PARAM, "conv descriptor not configured");
+  if (!engine_valid(engine)) return fail(DNNP_STATUS_BAD_PARAM, "bad engine");
+  dnnp_status st;
+  if ((st = bind_view(dyd, "dy")) || (st = bind_view(dxd, "dx")) || (st = bind_view(gd, "y")))
+    return st;
+  int64_t P, Q;
+  if ((st = conv_shape(dxd, fd, cd, &P, &Q))) return st;
+  if ((st = check_out(dyd, dxd->n, fd->k, P, Q, dxd->elem, "output gradient"))) return st;
+  if ((st = check_like(gd, dxd, "conv_bwd_data_act"))) return st;
+  dnnp::ConvProblem pr = make_problem(dxd, fd, cd, dyd, P, Q);
+  if ((st = check_decode_range(pr))) return st;
+  if ((st = need_device())) return st;
+  Stager sg(handle->stream);
+  void *ddy, *dff, *ddx, *dg;
+  size_t fbytes = size_t(fd->k * fd->c * fd->r * fd->s) * elem_size(fd->elem);
+  if ((st = sg.add(f, fbytes, false, true, &dff))) return st;
+  if ((st = sg.add(dy, span_bytes(dyd), false, true, &ddy))) return st;
+  if ((st = sg.add(g, span_bytes(gd), false, true, &dg))) return st;
+  if ((st = sg.add(dx, span_bytes(dxd), true, cd->accumulate || !dense_view(dxd), &ddx)))
+    return st;
+  dnnp::ConvEpilogue ep;
+  ep.gate = activation;
+  ep.gatep = dg;
+  ep.gatev = view_of(gd);
+  cudaError_t e = dnnp::conv_backward_data_fused(pr, dnnp::Dtype(dxd->elem), ddy, dff, ddx,
+                                                 cd->accumulate != 0, handle->math, ep,
+                                                 handle->stream);
+  return sg.finish(e);
+}
+
 // ------------------------------------------------ activation / softmax
 
 static bool act_valid(dnnp_activation_kind k) {

@@ -440,6 +440,10 @@ cudaError_t tc_backward_data(const ConvProblem& p, const float* dy, const float*
                              bool acc, cudaStream_t st);
 cudaError_t tc_backward_filter(const ConvProblem& p, const float* dy, const float* x, float* df,
                                bool acc, cudaStream_t st);
+cudaError_t tc_forward_fused(const ConvProblem& p, const float* x, const float* f, float* y,
+                             double alpha, double beta, const ConvEpilogue& ep, cudaStream_t st);
+cudaError_t tc_backward_data_fused(const ConvProblem& p, const float* dy, const float* f,
+                                   float* dx, bool acc, const ConvEpilogue& ep, cudaStream_t st);
 
 // math: 0 default (tensor cores when eligible), 1 SIMT fp32, 2 force tensor cores
 static bool use_tc(const ConvProblem& p, Dtype dt, int math, int pass, cudaError_t* err) {
@@ -478,6 +482,68 @@ cudaError_t conv_backward_filter(const ConvProblem& p, Dtype dt, const void* dy,
   if (e != cudaSuccess) return e;
   return dt == F32 ? simt_bwd_filter<float>(p, dy, x, df, accumulate, st)
                    : simt_bwd_filter<double>(p, dy, x, df, accumulate, st);
+}
+
+static bool same_strides(const View4& a, const View4& b) {
+  return a.sn == b.sn && a.sc == b.sc && a.sh == b.sh && a.sw == b.sw;
+}
+
+// Fused forward: in the tensor-core epilogue when the path allows, else the
+// same result as conv -> add_broadcast -> activation (all device kernels).
+cudaError_t conv_forward_fused(const ConvProblem& p, Dtype dt, const void* x, const void* f,
+                               void* y, double alpha, double beta, int math,
+                               const ConvEpilogue& ep, cudaStream_t st) {
+  cudaError_t e;
+  if (use_tc(p, dt, math, FWD, &e)) {
+    e = tc_forward_fused(p, (const float*)x, (const float*)f, (float*)y, alpha, beta, ep, st);
+    if (e != cudaErrorNotSupported) return e;
+    cudaGetLastError();
+  } else if (e != cudaSuccess) {
+    return e;
+  }
+  if ((e = conv_forward(p, dt, x, f, y, alpha, beta, math, st)) != cudaSuccess) return e;
+  if (ep.bias && (e = add_broadcast(dt, ep.biasv, ep.bias, p.y, y, 1.0, 1.0, st)) != cudaSuccess)
+    return e;
+  if (ep.act >= 0) return activation_forward(ep.act, dt, p.y, y, p.y, y, st);
+  return cudaSuccess;
+}
+
+// Fused backward-data: gated in the epilogue when g shares dx's strides,
+// else conv_bwd_data into scratch -> activation_backward -> (+)= dx.
+cudaError_t conv_backward_data_fused(const ConvProblem& p, Dtype dt, const void* dy,
+                                     const void* f, void* dx, bool accumulate, int math,
+                                     const ConvEpilogue& ep, cudaStream_t st) {
+  cudaError_t e;
+  if (use_tc(p, dt, math, DGRAD, &e)) {
+    if (same_strides(ep.gatev, p.x)) {
+      e = tc_backward_data_fused(p, (const float*)dy, (const float*)f, (float*)dx, accumulate,
+                                 ep, st);
+      if (e != cudaErrorNotSupported) return e;
+      cudaGetLastError();
+    }
+  } else if (e != cudaSuccess) {
+    return e;
+  }
+  if (!accumulate) {
+    if ((e = conv_backward_data(p, dt, dy, f, dx, false, math, st)) != cudaSuccess) return e;
+    return activation_backward(ep.gate, dt, ep.gatev, ep.gatep, p.x, dx, p.x, dx, st);
+  }
+  const size_t es = dt == F64 ? 8 : 4;
+  tc::ScratchScope* sc = tc::scratch_open(st);
+  void* tmp = nullptr;
+  e = tc::scratch_alloc(sc, size_t(p.x.size()) * es, &tmp);
+  if (e == cudaSuccess) {
+    ConvProblem q = p;  // dense NCHW scratch for the un-gated gradient
+    q.x.sw = 1;
+    q.x.sh = q.x.w;
+    q.x.sc = q.x.h * q.x.w;
+    q.x.sn = q.x.c * q.x.sc;
+    e = conv_backward_data(q, dt, dy, f, tmp, false, math, st);
+    if (e == cudaSuccess) e = activation_backward(ep.gate, dt, ep.gatev, ep.gatep, q.x, tmp, q.x, tmp, st);
+    if (e == cudaSuccess) e = transform(dt, q.x, tmp, p.x, dx, 1.0, 1.0, st);
+  }
+  tc::scratch_close(sc);
+  return e;
 }
 
 }  // namespace dnnp

@@ -769,7 +769,9 @@ int reduction_segments(int nkb, int depth) {
 
 cudaError_t run_gemm(const ConvProblem& p, Gemm g, const __nv_bfloat16* a_hi,
                      const __nv_bfloat16* a_lo, int IH, int IW, int Cp, const float* f, float* out,
-                     const View4& ov, float alpha, float beta, cudaStream_t st) {
+                     const View4& ov, float alpha, float beta, const EpiOp& epi, cudaStream_t st) {
+  const bool fused = epi.act >= 0 || epi.gate >= 0 || epi.bias != nullptr;
+  if (fused && !g.tma) return cudaErrorNotSupported;  // caller runs the unfused sequence
   PackGeom& pg = g.pg;
   const int CB = g.tma ? pick_cb(Cp) : 8;
   const int Cpf = int(ceil_div(Cp, CB) * CB);  // filter columns per tap (channel blocks padded)
@@ -862,12 +864,15 @@ cudaError_t run_gemm(const ConvProblem& p, Gemm g, const __nv_bfloat16* a_hi,
     prm.coltab = coltab;
     prm.alpha = alpha;
     prm.beta = beta;
-    prm.plain = (alpha == 1.0f && beta == 0.0f) ? 1 : 0;
+    prm.plain = (alpha == 1.0f && beta == 0.0f && !fused) ? 1 : 0;
+    prm.epi = epi;
     prm.dOHW = make_magic(uint32_t(g.OH * g.OW));
     prm.dOW = make_magic(uint32_t(g.OW));
     prm.skip = getenv("DNNP_TC_SKIP") ? atoi(getenv("DNNP_TC_SKIP")) : 0;
     prm.prefetch = getenv("DNNP_TC_PREFETCH") ? atoi(getenv("DNNP_TC_PREFETCH")) : 0;
     const int nseg = reduction_segments(nkb, kTK);
+    // a gated sum spread over segments cannot also add the caller's dx
+    if (epi.gate >= 0 && nseg > 1 && beta != 0.0f) return cudaErrorNotSupported;
     // stream-K over the last, partial wave of tiles
     Workspace skw(st);
     {
@@ -1034,7 +1039,7 @@ bool env_off(const char* name) { return getenv(name) != nullptr; }
 
 cudaError_t run_tc(bool dgrad, const ConvProblem& p, const float* in, const View4& inv,
                    const float* f, float* out, const View4& outv, float alpha, float beta,
-                   cudaStream_t st) {
+                   const EpiOp& epi, cudaStream_t st) {
   pool_keep_memory();
   Gemm g{};
   PackGeom& pg = g.pg;
@@ -1197,7 +1202,7 @@ cudaError_t run_tc(bool dgrad, const ConvProblem& p, const float* in, const View
   else
     e = pack_act(inv, in, Cp, a_hi, a_lo, st);
   if (e != cudaSuccess) return e;
-  return run_gemm(p, g, a_hi, a_lo, IH, IW, Cp, f, out, outv, alpha, beta, st);
+  return run_gemm(p, g, a_hi, a_lo, IH, IW, Cp, f, out, outv, alpha, beta, epi, st);
 }
 
 }  // namespace
@@ -1219,14 +1224,35 @@ bool tc_eligible(const ConvProblem& p, int pass) {
   return false;
 }
 
+static tc::EpiOp no_epi() { return tc::EpiOp{-1, -1, nullptr, 0, nullptr}; }
+
 cudaError_t tc_forward(const ConvProblem& p, const float* x, const float* f, float* y,
                        double alpha, double beta, cudaStream_t st) {
-  return tc::run_tc(false, p, x, p.x, f, y, p.y, float(alpha), float(beta), st);
+  return tc::run_tc(false, p, x, p.x, f, y, p.y, float(alpha), float(beta), no_epi(), st);
 }
 
 cudaError_t tc_backward_data(const ConvProblem& p, const float* dy, const float* f, float* dx,
                              bool acc, cudaStream_t st) {
-  return tc::run_tc(true, p, dy, p.y, f, dx, p.x, 1.0f, acc ? 1.0f : 0.0f, st);
+  return tc::run_tc(true, p, dy, p.y, f, dx, p.x, 1.0f, acc ? 1.0f : 0.0f, no_epi(), st);
+}
+
+// Fused forms; cudaErrorNotSupported (before any write to the output) when
+// the geometry takes a kernel without the fused epilogue.
+cudaError_t tc_forward_fused(const ConvProblem& p, const float* x, const float* f, float* y,
+                             double alpha, double beta, const ConvEpilogue& ep, cudaStream_t st) {
+  tc::EpiOp e = no_epi();
+  e.act = ep.act;
+  e.bias = static_cast<const float*>(ep.bias);
+  e.bias_sc = ep.bias_stride;
+  return tc::run_tc(false, p, x, p.x, f, y, p.y, float(alpha), float(beta), e, st);
+}
+
+cudaError_t tc_backward_data_fused(const ConvProblem& p, const float* dy, const float* f,
+                                   float* dx, bool acc, const ConvEpilogue& ep, cudaStream_t st) {
+  tc::EpiOp e = no_epi();
+  e.gate = ep.gate;
+  e.gatep = static_cast<const float*>(ep.gatep);
+  return tc::run_tc(true, p, dy, p.y, f, dx, p.x, 1.0f, acc ? 1.0f : 0.0f, e, st);
 }
 
 }  // namespace dnnp

@@ -32,6 +32,150 @@ constexpr int kTmaThreads = 10 * 32;  // TMA warp, MMA warp, 8 epilogue warps
 constexpr int kColCache = 512;        // mode-1 column table cached in shared memory
 constexpr int kTK = 64;  // reduction depth of one stage (4 k-steps of 16)
 
+// Fused epilogue operations (additive C entries
+// dnnp_convolution_bias_activation_forward / _backward_data_activation).
+// Forward: y = act(alpha*conv + beta*y + bias[k]).  Backward-data: dx =
+// act'(g) * conv (+ beta*dx), g = the activation output that fed the conv,
+// read at the same offset as dx (the host requires identical strides).
+// Activation formulas: reference nnops.py:54-88 (same as nnops.cu ActFwd/ActBwd).
+struct EpiOp {
+  int act;              // forward activation of the sum: -1 none, 0 sigmoid, 1 relu, 2 tanh
+  int gate;             // backward-data: -1 none, else the activation kind of g
+  const float* bias;    // per output channel (stride bias_sc), or null
+  int64_t bias_sc;
+  const float* gatep;   // g, same strides as the output
+  __device__ __forceinline__ bool any() const { return act >= 0 || gate >= 0 || bias != nullptr; }
+};
+
+__device__ __forceinline__ float epi_act_fwd(int kind, float x) {
+  if (kind == 1) return (x > 0.0f || x != x) ? x : 0.0f;
+  if (kind == 2) return tanhf(x);
+  const float e = expf(-fabsf(x));
+  return x >= 0.0f ? 1.0f / __fadd_rn(1.0f, e) : e / __fadd_rn(1.0f, e);
+}
+
+__device__ __forceinline__ float epi_act_bwd(int kind, float y, float dy) {
+  if (kind == 1) return __fmul_rn(dy, y > 0.0f ? 1.0f : 0.0f);
+  if (kind == 2) return __fmul_rn(dy, __fsub_rn(1.0f, __fmul_rn(y, y)));
+  return __fmul_rn(__fmul_rn(dy, y), __fsub_rn(1.0f, y));
+}
+
+// Per-element output operations, one functor per (op, activation) so that the
+// 32-column store loops are branch-free (a runtime switch per element made
+// the epilogue instruction-latency bound: 5x the plain store time).
+// acc = accumulator, old = stored value (read only when needed), aux = the
+// gate value g (backward-data) or bias[k] (forward).
+struct OpAxpby {  // alpha * acc + beta * old (also the non-final reduction segments)
+  float alpha, beta;
+  __device__ __forceinline__ float operator()(float acc, float old, float) const {
+    const float v = __fmul_rn(acc, alpha);
+    return beta != 0.0f ? __fadd_rn(__fmul_rn(old, beta), v) : v;
+  }
+};
+template <int ACT>
+struct OpBiasAct {  // act(alpha * acc + beta * old + bias)
+  float alpha, beta;
+  bool bias;
+  __device__ __forceinline__ float operator()(float acc, float old, float aux) const {
+    float v = __fmul_rn(acc, alpha);
+    if (beta != 0.0f) v = __fadd_rn(__fmul_rn(old, beta), v);
+    if (bias) v = __fadd_rn(v, aux);
+    return ACT < 0 ? v : epi_act_fwd(ACT, v);
+  }
+};
+template <int KIND, bool SEGD>
+struct OpGate {  // act'(g) * acc (+ beta * old); segmented: act'(g) * (old + acc)
+  float beta;
+  __device__ __forceinline__ float operator()(float acc, float old, float g) const {
+    if (SEGD) return epi_act_bwd(KIND, g, __fadd_rn(old, acc));
+    const float v = epi_act_bwd(KIND, g, acc);
+    return beta != 0.0f ? __fadd_rn(__fmul_rn(old, beta), v) : v;
+  }
+};
+
+// 32 channel columns of one row at rowp (stride sc), nv of them valid; all
+// loads of a half are issued before its stores
+template <class Op>
+__device__ __forceinline__ void store_cols(float* rowp, int64_t sc, int nv, const uint32_t* v,
+                                           bool rd_old, const float* auxp, int64_t aux_sc,
+                                           const Op& op) {
+#pragma unroll
+  for (int h = 0; h < 32; h += 16) {
+    // unconditional loads (invalid columns read column 0): predicated or
+    // branched loads let the compiler pair each load with its use
+    float old[16], aux[16];
+    if (rd_old) {
+#pragma unroll
+      for (int j = 0; j < 16; j++) old[j] = rowp[h + j < nv ? int64_t(h + j) * sc : 0];
+    } else {
+#pragma unroll
+      for (int j = 0; j < 16; j++) old[j] = 0.0f;
+    }
+    if (auxp) {
+#pragma unroll
+      for (int j = 0; j < 16; j++) aux[j] = __ldg(auxp + (h + j < nv ? int64_t(h + j) * aux_sc : 0));
+    } else {
+#pragma unroll
+      for (int j = 0; j < 16; j++) aux[j] = 0.0f;
+    }
+#pragma unroll
+    for (int j = 0; j < 16; j++)
+      if (h + j < nv) rowp[int64_t(h + j) * sc] = op(__uint_as_float(v[h + j]), old[j], aux[j]);
+  }
+}
+
+// scattered columns: element offsets off[] (relative to out) with valid mask;
+// aux from auxp + off (gate) or bias + ch * bsc
+template <class Op>
+__device__ __forceinline__ void store_scatter(float* out, const int64_t* off, uint32_t okm,
+                                              const int* ch, const float* v, bool rd_old,
+                                              const float* gatep, const float* biasp, int64_t bsc,
+                                              const Op& op) {
+  // unconditional loads (invalid elements have off = 0, ch = 0)
+  float old[16], aux[16];
+#pragma unroll
+  for (int j = 0; j < 16; j++) old[j] = rd_old ? out[off[j]] : 0.0f;
+  if (gatep) {
+#pragma unroll
+    for (int j = 0; j < 16; j++) aux[j] = __ldg(gatep + off[j]);
+  } else if (biasp) {
+#pragma unroll
+    for (int j = 0; j < 16; j++) aux[j] = __ldg(biasp + ch[j] * bsc);
+  } else {
+#pragma unroll
+    for (int j = 0; j < 16; j++) aux[j] = 0.0f;
+  }
+#pragma unroll
+  for (int j = 0; j < 16; j++)
+    if ((okm >> j) & 1u) out[off[j]] = op(v[j], old[j], aux[j]);
+}
+
+// Calls f(op) with the functor for this element class (one switch per chunk).
+template <class F>
+__device__ __forceinline__ void with_op(const EpiOp& E, bool fuse, bool segd, float alpha,
+                                        float beta, F&& f) {
+  if (!fuse) {
+    f(OpAxpby{alpha, beta});
+  } else if (E.gate >= 0) {
+    switch (E.gate * 2 + (segd ? 1 : 0)) {
+      case 0: f(OpGate<0, false>{beta}); break;
+      case 1: f(OpGate<0, true>{beta}); break;
+      case 2: f(OpGate<1, false>{beta}); break;
+      case 3: f(OpGate<1, true>{beta}); break;
+      case 4: f(OpGate<2, false>{beta}); break;
+      default: f(OpGate<2, true>{beta}); break;
+    }
+  } else {
+    const bool b = E.bias != nullptr;
+    switch (E.act) {
+      case 0: f(OpBiasAct<0>{alpha, beta, b}); break;
+      case 1: f(OpBiasAct<1>{alpha, beta, b}); break;
+      case 2: f(OpBiasAct<2>{alpha, beta, b}); break;
+      default: f(OpBiasAct<-1>{alpha, beta, b}); break;
+    }
+  }
+}
+
 struct TmaParams {
   CUtensorMap tm_ahi;  // im2col maps of the packed input planes
   CUtensorMap tm_alo;
@@ -58,6 +202,7 @@ struct TmaParams {
   const uint32_t* coltab;
   float alpha, beta;
   int plain;                   // alpha == 1, beta == 0: store the accumulator as is
+  EpiOp epi;                   // fused bias / activation / activation-backward (plain == 0)
   MagicDiv dOHW, dOW;
   int skip;                    // experiments: 1 = no A loads, 2 = no loads, 4 = no MMAs
   int prefetch;                // L2 prefetch of the next tile's im2col window
@@ -416,6 +561,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1) conv_tma_kernel(const __grid_c
         // segments after the first add to what the first stored
         const float beta = wi.seg ? 1.0f : P.beta;
         const bool plain = P.plain && wi.seg == 0;
+        const bool last = wi.seg == P.nseg - 1 || P.nseg <= 1;
+        const bool segd = P.nseg > 1;
         // mode 0: row base at the output pixel; mode 1: at (oh*o_u - o_ph, ow*o_v - o_pw)
         const int hb = int(oh) * P.o_u - P.o_ph, wb = int(ow) * P.o_v - P.o_pw;
         const int64_t rowoff =
@@ -451,51 +598,76 @@ __global__ void __launch_bounds__(kTmaThreads, 1) conv_tma_kernel(const __grid_c
             }
           } else if (P.out_mode == 0) {
             float* rowp = P.out + rowoff + int64_t(cbase) * P.o_sc;
-            // all 32 old values are loaded before any store (one latency, not 32)
-            float old[32];
-#pragma unroll
-            for (int i = 0; i < 32; i++)
-              old[i] = (beta != 0.0f && cbase + i < P.Ncol) ? rowp[int64_t(i) * P.o_sc] : 0.0f;
-#pragma unroll
-            for (int i = 0; i < 32; i++) {
-              if (cbase + i < P.Ncol) {
-                float val = __fmul_rn(__uint_as_float(v[i]), P.alpha);
-                if (beta != 0.0f) val = __fadd_rn(__fmul_rn(old[i], beta), val);
-                rowp[int64_t(i) * P.o_sc] = val;
-              }
-            }
-          } else if (ctab_smem) {
+            const int nv = min(32, P.Ncol - cbase);
+            const bool fuse = last && P.epi.any();
+            const bool gate = fuse && P.epi.gate >= 0;
+            const float* auxp = gate ? P.epi.gatep + rowoff + int64_t(cbase) * P.o_sc
+                                : (fuse && P.epi.bias) ? P.epi.bias + int64_t(cbase) * P.epi.bias_sc
+                                                       : nullptr;
+            const int64_t aux_sc = gate ? P.o_sc : P.epi.bias_sc;
+            with_op(P.epi, fuse, segd, P.alpha, beta, [&](const auto& op) {
+              store_cols(rowp, P.o_sc, nv, v, beta != 0.0f, auxp, aux_sc, op);
+            });
+          } else if (plain && ctab_smem) {
 #pragma unroll
             for (int i = 0; i < 32; i++) {
               const int col = cbase + i;
               if (col < P.Ncol) {
                 const int hw = col_hw[col];
                 if (unsigned(hb + (hw >> 16)) < unsigned(P.o_H) &&
-                    unsigned(wb + (hw & 0xFFFF)) < unsigned(P.o_W)) {
-                  float* dst = P.out + rowoff + col_off[col];
-                  float val = __uint_as_float(v[i]);
-                  if (!plain) {
-                    val = __fmul_rn(val, P.alpha);
-                    if (beta != 0.0f) val = __fadd_rn(__fmul_rn(*dst, beta), val);
-                  }
-                  *dst = val;
-                }
+                    unsigned(wb + (hw & 0xFFFF)) < unsigned(P.o_W))
+                  P.out[rowoff + col_off[col]] = __uint_as_float(v[i]);
               }
             }
           } else {
+            // scattered columns (super-pixel / space-to-depth / blocked):
+            // offsets from the column table, loads of a half before its stores
+            const bool fuse = last && P.epi.any();
+            const bool gate = fuse && P.epi.gate >= 0, bias = fuse && P.epi.bias != nullptr;
 #pragma unroll
-            for (int i = 0; i < 32; i++) {
-              const int col = cbase + i;
-              if (col < P.Ncol) {
-                const uint32_t e = __ldg(P.coltab + col);
-                const int ph = int(e >> 24), pw = int((e >> 16) & 255);
-                if (unsigned(hb + ph) < unsigned(P.o_H) && unsigned(wb + pw) < unsigned(P.o_W)) {
-                  float* dst = P.out + rowoff + int64_t(e & 0xFFFF) * P.o_sc + int64_t(ph) * P.o_sh +
-                               int64_t(pw) * P.o_sw;
-                  float val = __fmul_rn(__uint_as_float(v[i]), P.alpha);
-                  if (beta != 0.0f) val = __fadd_rn(__fmul_rn(*dst, beta), val);
-                  *dst = val;
+            for (int h = 0; h < 32; h += 16) {
+              int64_t off[16];
+              int ch[16];
+              float acc[16];
+              uint32_t okm = 0;
+#pragma unroll
+              for (int j = 0; j < 16; j++) {
+                const int col = cbase + h + j;
+                off[j] = 0;
+                ch[j] = 0;
+                acc[j] = __uint_as_float(v[h + j]);
+                if (col < P.Ncol) {
+                  int ph, pw;
+                  int64_t o;
+                  if (ctab_smem) {
+                    const int hw = col_hw[col];
+                    ph = hw >> 16;
+                    pw = hw & 0xFFFF;
+                    o = col_off[col];
+                    if (bias) ch[j] = int(__ldg(P.coltab + col) & 0xFFFF);
+                  } else {
+                    const uint32_t e = __ldg(P.coltab + col);
+                    ph = int(e >> 24);
+                    pw = int((e >> 16) & 255);
+                    ch[j] = int(e & 0xFFFF);
+                    o = int64_t(ch[j]) * P.o_sc + int64_t(ph) * P.o_sh + int64_t(pw) * P.o_sw;
+                  }
+                  if (unsigned(hb + ph) < unsigned(P.o_H) && unsigned(wb + pw) < unsigned(P.o_W)) {
+                    okm |= 1u << j;
+                    off[j] = rowoff + o;
+                  }
                 }
+              }
+              if (plain) {
+#pragma unroll
+                for (int j = 0; j < 16; j++)
+                  if ((okm >> j) & 1u) P.out[off[j]] = acc[j];
+              } else {
+                with_op(P.epi, fuse, segd, P.alpha, beta, [&](const auto& op) {
+                  store_scatter(P.out, off, okm, ch, acc, beta != 0.0f,
+                                gate ? P.epi.gatep : nullptr, bias ? P.epi.bias : nullptr,
+                                P.epi.bias_sc, op);
+                });
               }
             }
           }

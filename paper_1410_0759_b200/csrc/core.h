@@ -58,6 +58,25 @@ cudaError_t conv_forward(const ConvProblem& p, Dtype dt, const void* x, const vo
 // dx := conv_bwd_data(dy, f) (+ dx if accumulate)
 cudaError_t conv_backward_data(const ConvProblem& p, Dtype dt, const void* dy, const void* f,
                                void* dx, bool accumulate, int math, cudaStream_t st);
+// Fused epilogues (additive).  Forward: y := act(alpha*conv
+// + beta*y + bias[k]) (act -1: none; bias null: none).  Backward-data: dx :=
+// act'(g) * conv_bwd_data(dy) (+ dx if accumulate), g the activation output
+// that fed the convolution, viewed by gatev.
+struct ConvEpilogue {
+  int act = -1;
+  const void* bias = nullptr;
+  int64_t bias_stride = 0;  // element stride of the bias over k
+  View4 biasv{};
+  int gate = -1;
+  const void* gatep = nullptr;
+  View4 gatev{};
+};
+cudaError_t conv_forward_fused(const ConvProblem& p, Dtype dt, const void* x, const void* f,
+                               void* y, double alpha, double beta, int math,
+                               const ConvEpilogue& ep, cudaStream_t st);
+cudaError_t conv_backward_data_fused(const ConvProblem& p, Dtype dt, const void* dy,
+                                     const void* f, void* dx, bool accumulate, int math,
+                                     const ConvEpilogue& ep, cudaStream_t st);
 // df := conv_bwd_filter(dy, x) (+ df if accumulate)
 cudaError_t conv_backward_filter(const ConvProblem& p, Dtype dt, const void* dy, const void* x,
                                  void* df, bool accumulate, int math, cudaStream_t st);

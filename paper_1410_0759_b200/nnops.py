@@ -195,3 +195,49 @@ def pool_backward(pd: PoolingDesc, y: TensorView, dy: TensorView, x: TensorView,
         _lib.handle(), pd.c_desc(), y.desc.c_desc(), y.ptr, dy.desc.c_desc(), dy.ptr,
         x.desc.c_desc(), x.ptr, dx.desc.c_desc(), dx.ptr,
         ctypes.c_void_p(am) if am else None), "pooling_backward")
+
+
+# ---------------------------------------------------------- fused epilogues
+# Additive: the Caffe layer sequence conv -> bias -> act
+# and its backward conv_bwd_data -> act_bwd in one pass over the output
+# (include/dnnp.h dnnp_convolution_bias_activation_forward /
+# dnnp_convolution_backward_data_activation).
+
+def conv_bias_activation_forward(x: TensorView, f, conv, engine, y: TensorView, bias=None,
+                                 activation=None, alpha: float = 1.0, beta: float = 0.0) -> None:
+    """y := act(alpha * conv(x, f) + beta * y + bias[k]); bias (1, K, 1, 1) or None,
+    activation an ActivationKind / name or None."""
+    from .conv import _ENGINE_CODE, _check_out, _check_triplet, as_engine
+    from .tensor import scalar_ptr
+    engine = as_engine(engine)
+    out_shape = _check_triplet(x, f, conv)
+    _check_out(y, out_shape, x.desc.dtype, "output")
+    act = -1 if activation is None else _ACT[_as_enum(ActivationKind, activation)]
+    if bias is not None and bias.desc.extents != (1, out_shape[1], 1, 1):
+        raise ShapeMismatch(f"bias must be (1, {out_shape[1]}, 1, 1)")
+    views = (x, f, y) if bias is None else (x, f, y, bias)
+    bind_stream(*views)
+    a_keep, a = scalar_ptr(alpha, y.desc.dtype)
+    b_keep, b = scalar_ptr(beta, y.desc.dtype)
+    _lib.check(_lib.lib().dnnp_convolution_bias_activation_forward(
+        _lib.handle(), a, x.desc.c_desc(), x.ptr, f.desc.c_desc(), f.ptr, conv.c_desc(),
+        _ENGINE_CODE[engine], b, None if bias is None else bias.desc.c_desc(),
+        None if bias is None else bias.ptr, act, y.desc.c_desc(), y.ptr),
+        "convolution_bias_activation_forward")
+
+
+def conv_backward_data_activation(dy: TensorView, f, conv, engine, dx: TensorView, activation,
+                                  y: TensorView) -> None:
+    """dx (+)= act'(y) * conv_backward_data(dy, f); y = the activation output
+    that was this convolution's input (extents of dx)."""
+    from .conv import _ENGINE_CODE, _check_out, _check_triplet, as_engine
+    engine = as_engine(engine)
+    kind = _as_enum(ActivationKind, activation)
+    out_shape = _check_triplet(dx, f, conv)
+    _check_out(dy, out_shape, dx.desc.dtype, "output gradient")
+    _check_like(y, dx, "convolution backward-data activation")
+    bind_stream(dy, f, dx, y)
+    _lib.check(_lib.lib().dnnp_convolution_backward_data_activation(
+        _lib.handle(), f.desc.c_desc(), f.ptr, dy.desc.c_desc(), dy.ptr, conv.c_desc(),
+        _ENGINE_CODE[engine], _ACT[kind], y.desc.c_desc(), y.ptr, dx.desc.c_desc(), dx.ptr),
+        "convolution_backward_data_activation")
