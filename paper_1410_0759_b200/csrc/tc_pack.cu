@@ -38,14 +38,16 @@ __global__ void __launch_bounds__(256) pack_act_kernel(View4 v, const float* __r
   __shared__ float tile[kCh][kPix + 1];
   const int lp = threadIdx.x & 31, lc = threadIdx.x >> 5;  // read role: pixel, channel phase
   const int wp = threadIdx.x >> 3, wg = threadIdx.x & 7;   // write role: pixel, channel group
-  const int64_t ntiles = (npix + kPix - 1) / kPix;
-  const int nslabs = (Cp + kCh - 1) / kCh;
+  // 32-bit job arithmetic (the host guarantees jobs < 2^31): a 64-bit
+  // division per job cost as much as the 8 elements it moves
+  const uint32_t ntiles = uint32_t((npix + kPix - 1) / kPix);
+  const uint32_t nslabs = uint32_t((Cp + kCh - 1) / kCh);
   const int Cs = S2D ? sg.u * sg.v * int(v.c) : int(v.c);  // real channels of the packed grid
-  for (int64_t job = blockIdx.x; job < ntiles * nslabs; job += gridDim.x) {
-    const int64_t pt = job / nslabs;
+  for (uint32_t job = blockIdx.x; job < ntiles * nslabs; job += gridDim.x) {
+    const uint32_t pt = nslabs == 1 ? job : job / nslabs;
     const int slab = int(job - pt * nslabs);
     const int c_lo = slab * kCh, nch = min(kCh, Cp - c_lo);
-    const int64_t pix = pt * kPix + lp;
+    const int64_t pix = int64_t(pt) * kPix + lp;
     if (pix < npix) {
       uint32_t n, rem, h, w;
       mdivmod(uint32_t(pix), dHW, n, rem);
@@ -77,7 +79,7 @@ __global__ void __launch_bounds__(256) pack_act_kernel(View4 v, const float* __r
       }
     }
     __syncthreads();
-    const int64_t opix = pt * kPix + wp;
+    const int64_t opix = int64_t(pt) * kPix + wp;
     if (opix < npix && wg * 8 < nch) {
       __align__(16) __nv_bfloat16 vh[8], vl[8];
 #pragma unroll
@@ -266,6 +268,75 @@ __global__ void __launch_bounds__(256) pack_act_s2d_dense_kernel(View4 v, const 
   }
 }
 
+// Space-to-depth for dense NCHW input with even v and pad_w (AlexNet conv1:
+// 4 x 4 phases, pad 2): one block = 64 consecutive super-pixels of one
+// super-row (n, h') x all (rh, c); warp (rh, c) reads, per super-pixel, the v
+// input columns [w'v - pad_w, w'v - pad_w + v) of row h'u + rh - pad_h as
+// v/2 float2 loads (the warp covers 32 v consecutive floats: coalesced, an
+// input byte is read once), stages them in shared memory as [pixel][Cs],
+// then each thread splits and writes 16-byte hi / lo chunks of the
+// contiguous 64 x Cp output block.  (32 super-pixels per block: 3.4 TB/s,
+// latency-bound; measured per call under ncu.)
+template <int V>
+__global__ void __launch_bounds__(512) pack_act_s2d_quad_kernel(View4 v, const float* __restrict__ x,
+                                                                int u, int pad_h, int pad_w, int H2,
+                                                                int W2, int Cp, int nwb,
+                                                                __nv_bfloat16* __restrict__ hi,
+                                                                __nv_bfloat16* __restrict__ lo) {
+  constexpr int PIX = 64;           // super-pixels per block (two per lane): ~2x the bytes in flight
+  extern __shared__ float stile[];  // [PIX][Cp + 1]
+  const int C = int(v.c), Cs = u * V * C, pitch = Cp + 1;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const uint32_t job = blockIdx.x;
+  const uint32_t row = job / uint32_t(nwb), wb = job - row * uint32_t(nwb);
+  const int n = int(row / uint32_t(H2)), h2 = int(row - uint32_t(n) * uint32_t(H2));
+  for (int q = warp; q < u * C; q += nwarps) {  // q = rh * C + c
+    const int rh = q / C, c = q - rh * C;
+    const int h = h2 * u + rh - pad_h;
+    const float* src = x + int64_t(n) * v.sn + int64_t(c) * v.sc + int64_t(h) * v.sh;
+    const bool hok = unsigned(h) < unsigned(v.h);
+    float2 val[2][V / 2];
+#pragma unroll
+    for (int s2 = 0; s2 < 2; s2++) {
+      const int w2 = int(wb) * PIX + s2 * 32 + lane;
+      const int w0 = w2 * V - pad_w;
+#pragma unroll
+      for (int k = 0; k < V / 2; k++) {
+        const int w = w0 + 2 * k;  // pairs are all-in or all-out (even pad, even W)
+        val[s2][k] = (w2 < W2 && hok && unsigned(w) < unsigned(v.w))
+                         ? __ldg(reinterpret_cast<const float2*>(src + w))
+                         : make_float2(0.0f, 0.0f);
+      }
+    }
+#pragma unroll
+    for (int s2 = 0; s2 < 2; s2++) {
+#pragma unroll
+      for (int k = 0; k < V / 2; k++) {
+        float* d = stile + (s2 * 32 + lane) * pitch + (rh * V + 2 * k) * C + c;
+        d[0] = val[s2][k].x;
+        d[C] = val[s2][k].y;
+      }
+    }
+  }
+  for (int t = threadIdx.x; t < PIX * (Cp - Cs); t += blockDim.x) {
+    const int pi = t / (Cp - Cs), cc = Cs + t % (Cp - Cs);
+    stile[pi * pitch + cc] = 0.0f;
+  }
+  __syncthreads();
+  const int groups = Cp / 8;
+  const int64_t obase = (int64_t(row) * W2 + int64_t(wb) * PIX) * Cp;
+  for (int t = threadIdx.x; t < PIX * groups; t += blockDim.x) {
+    const int pi = t / groups, g = t - pi * groups;
+    if (int(wb) * PIX + pi >= W2) continue;
+    __align__(16) __nv_bfloat16 vh[8], vl[8];
+#pragma unroll
+    for (int k = 0; k < 8; k++) split_bf16(stile[pi * pitch + g * 8 + k], vh[k], vl[k]);
+    const int64_t o = obase + int64_t(pi) * Cp + g * 8;
+    *reinterpret_cast<uint4*>(hi + o) = *reinterpret_cast<const uint4*>(vh);
+    *reinterpret_cast<uint4*>(lo + o) = *reinterpret_cast<const uint4*>(vl);
+  }
+}
+
 }  // namespace
 
 cudaError_t pack_act_s2d(const View4& v, const float* x, int u, int vv, int pad_h, int pad_w,
@@ -273,6 +344,32 @@ cudaError_t pack_act_s2d(const View4& v, const float* x, int u, int vv, int pad_
                          cudaStream_t st) {
   const int64_t npix = v.n * H2 * W2;
   if (npix >= (int64_t(1) << 32)) return cudaErrorInvalidValue;
+  {
+    // float2 quads: dense rows, even v / pad_w / W / strides, 8-byte base
+    const int nwb = int(ceil_div(W2, 64));
+    const size_t sm = size_t(64) * (Cp + 1) * sizeof(float);
+    const bool quad = (vv == 2 || vv == 4 || vv == 8) && v.sw == 1 && pad_w % 2 == 0 &&
+                      v.w % 2 == 0 && v.sh % 2 == 0 && v.sc % 2 == 0 && v.sn % 2 == 0 &&
+                      (reinterpret_cast<uintptr_t>(x) & 7) == 0 && sm <= 48 * 1024 &&
+                      v.n * H2 * nwb < (int64_t(1) << 31) && !getenv("DNNP_S2D_NO_QUAD");
+    if (quad) {
+      const unsigned grid = unsigned(v.n * H2 * nwb);
+      const int threads = int(std::min<int64_t>(512, std::max<int64_t>(128, v.c * u * 32)));
+      cudaError_t e;
+      if (vv == 2)
+        pack_act_s2d_quad_kernel<2><<<grid, threads, sm, st>>>(v, x, u, pad_h, pad_w, H2, W2, Cp,
+                                                               nwb, hi, lo);
+      else if (vv == 4)
+        pack_act_s2d_quad_kernel<4><<<grid, threads, sm, st>>>(v, x, u, pad_h, pad_w, H2, W2, Cp,
+                                                               nwb, hi, lo);
+      else
+        pack_act_s2d_quad_kernel<8><<<grid, threads, sm, st>>>(v, x, u, pad_h, pad_w, H2, W2, Cp,
+                                                               nwb, hi, lo);
+      e = cudaGetLastError();
+      note_launch();
+      return e;
+    }
+  }
   {
     const int SW = (W2 * vv + 3) & ~3;
     const size_t sm = size_t(v.c) * u * SW * sizeof(float);
@@ -289,6 +386,7 @@ cudaError_t pack_act_s2d(const View4& v, const float* x, int u, int vv, int pad_
   }
   if (getenv("DNNP_S2D_TILE")) {
     const int64_t jobs = ceil_div(npix, kPix) * ceil_div(Cp, kCh);
+    if (jobs >= (int64_t(1) << 31)) return cudaErrorInvalidValue;
     const unsigned grid = unsigned(std::min<int64_t>(jobs, int64_t(kNumSMs) * 32));
     pack_act_kernel<true><<<grid, 256, 0, st>>>(v, x, Cp, hi, lo, npix,
                                                 make_magic(uint32_t(H2 * W2)), make_magic(uint32_t(W2)),
@@ -514,6 +612,7 @@ cudaError_t pack_act(const View4& v, const float* x, int Cp, __nv_bfloat16* hi, 
     return cudaGetLastError();
   }
   const int64_t jobs = ceil_div(npix, kPix) * ceil_div(Cp, kCh);
+  if (jobs >= (int64_t(1) << 31)) return cudaErrorInvalidValue;
   const unsigned grid = unsigned(std::min<int64_t>(jobs, int64_t(kNumSMs) * 32));
   pack_act_kernel<false><<<grid, 256, 0, st>>>(v, x, Cp, hi, lo, npix,
                                                make_magic(uint32_t(v.h * v.w)),

@@ -332,11 +332,13 @@ struct WgTmaParams {
 
 // Longest reduction (pixels) accumulated in one TMEM accumulator.  The
 // tensor-core fp32 accumulation truncates, so its error grows linearly with
-// the chain (measured: ~3.5e-5 of max|dW| at 8k pixels); longer reductions
-// are split and the splits summed in IEEE fp32 by the reduce kernel, which
-// keeps every wgrad at the north_star 1e-4 bar whatever N*P*Q is.
+// the chain (measured: 2.8e-5 of max|dW| at 8k pixels, 4.7e-5 at 16k,
+// 3.7e-4 at 222k); longer reductions are split and the splits summed in IEEE
+// fp32 by the reduce kernel, which keeps every wgrad at the north_star 1e-4
+// bar whatever N*P*Q is.  16k costs nothing on AlexNet (8k cost conv1/conv2
+// ~10%, tools/wg_chain.py).
 static int64_t max_chain(int px) {
-  int64_t c = 8192;
+  int64_t c = 16384;
   if (const char* e = getenv("DNNP_WG_CHAIN")) c = std::max<int64_t>(atoll(e), px);
   return c / px * px;
 }
