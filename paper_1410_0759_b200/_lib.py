@@ -30,6 +30,7 @@ _SIGS = {
     "dnnp_last_error": [],
     "dnnp_kernel_launch_count": [],
     "dnnp_kernel_timing": [ctypes.c_int],
+    "dnnp_scratch_high_water": [ctypes.c_int],
     "dnnp_kernel_times": [ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_int), ctypes.c_int],
     "dnnp_create": [ctypes.POINTER(vp)],
     "dnnp_destroy": [vp],
@@ -82,6 +83,7 @@ _RESTYPES = {
     "dnnp_status_string": ctypes.c_char_p,
     "dnnp_last_error": ctypes.c_char_p,
     "dnnp_kernel_launch_count": c_i64,
+    "dnnp_scratch_high_water": c_i64,
 }
 SYMBOLS = tuple(_SIGS)
 
@@ -151,6 +153,11 @@ def kernel_launch_count():
 def kernel_timing(enable=True):
     """Start (clearing) or stop CUDA-event timing of the main GEMM kernels."""
     lib().dnnp_kernel_timing(1 if enable else 0)
+
+
+def scratch_high_water(reset=False):
+    """Largest scratch footprint (bytes) of any operation since the last reset."""
+    return int(lib().dnnp_scratch_high_water(1 if reset else 0))
 
 
 def kernel_times():

@@ -685,7 +685,12 @@ dnnp_status dnnp_convolution_forward(dnnp_handle handle, const void* alpha, dnnp
   if ((st = check_out(yd, xd->n, fd->k, P, Q, xd->elem, "output"))) return st;
   if (cd->accumulate) b = 1.0;  // reference conv.py:573-574
   dnnp::ConvProblem pr = make_problem(xd, fd, cd, yd, P, Q);
+  pr.engine = int(engine);
   if ((st = check_decode_range(pr))) return st;
+  if (engine == DNNP_ENGINE_EXPLICIT &&
+      pr.C * pr.R * pr.S * pr.N * pr.P * pr.Q * int64_t(elem_size(xd->elem)) > (int64_t(4) << 30))
+    return fail(DNNP_STATUS_ALLOC_FAILED,  // AllocTooLarge (reference conv.py:31, 507-511)
+                "explicit engine: lowered data matrix exceeds the 4 GiB limit");
   if ((st = need_device())) return st;
   Stager sg(handle->stream);
   void *dx, *df, *dy;

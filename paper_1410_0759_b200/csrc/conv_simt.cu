@@ -454,9 +454,78 @@ static bool use_tc(const ConvProblem& p, Dtype dt, int math, int pass, cudaError
   return ok;
 }
 
+// Explicit lowering (engine EXPLICIT, forward): D[n][(c,r,s)][p][q] =
+// x[n][c][access(p, r)][access(q, s)] (0 outside), the reference's
+// lower_explicit data matrix (conv.py:494-525) stored as an NCHW tensor of
+// C*R*S channels, then the 1x1 convolution of D with the filter viewed as
+// K x CRS.  The lowered matrix is the auxiliary memory the implicit kernels
+// avoid (the paper's point); kept as the negative control.
+template <typename T>
+__global__ void __launch_bounds__(256) lower_kernel(const ConvProblem p, const T* __restrict__ x,
+                                                    T* __restrict__ d, uint32_t total, MagicDiv dQ,
+                                                    MagicDiv dP, MagicDiv dCRS, MagicDiv dS,
+                                                    MagicDiv dR) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    uint32_t t, q, pp, cp, n, rs, s, c, r;
+    mdivmod(i, dQ, t, q);
+    mdivmod(t, dP, t, pp);
+    mdivmod(t, dCRS, n, cp);
+    mdivmod(cp, dS, rs, s);
+    mdivmod(rs, dR, c, r);
+    const int64_t h = int64_t(pp) * p.u + (p.flip ? p.R - 1 - r : r) - p.pad_h;
+    const int64_t w = int64_t(q) * p.v + (p.flip ? p.S - 1 - s : s) - p.pad_w;
+    T v = T(0);
+    if (h >= 0 && h < p.H && w >= 0 && w < p.W)
+      v = x[int64_t(n) * p.x.sn + int64_t(c) * p.x.sc + h * p.x.sh + w * p.x.sw];
+    d[i] = v;
+  }
+}
+
+static cudaError_t explicit_forward(const ConvProblem& p, Dtype dt, const void* x, const void* f,
+                                    void* y, double alpha, double beta, int math,
+                                    cudaStream_t st) {
+  const int64_t crs = p.C * p.R * p.S, total = p.N * crs * p.P * p.Q;
+  const size_t es = dt == F64 ? 8 : 4;
+  if (total * int64_t(es) > (int64_t(4) << 30) || total >= (int64_t(1) << 32))
+    return cudaErrorMemoryAllocation;  // AllocTooLarge (reference conv.py:31)
+  tc::ScratchScope* sc = tc::scratch_open(st);
+  void* d = nullptr;
+  cudaError_t e = tc::scratch_alloc(sc, size_t(total) * es, &d);
+  if (e == cudaSuccess) {
+    const unsigned grid = unsigned(std::min<int64_t>((total + 255) / 256, int64_t(148) * 16));
+    const MagicDiv dQ = make_magic(uint32_t(p.Q)), dP = make_magic(uint32_t(p.P)),
+                   dCRS = make_magic(uint32_t(crs)), dS = make_magic(uint32_t(p.S)),
+                   dR = make_magic(uint32_t(p.R));
+    if (dt == F32)
+      lower_kernel<float><<<grid, 256, 0, st>>>(p, (const float*)x, (float*)d, uint32_t(total), dQ,
+                                                dP, dCRS, dS, dR);
+    else
+      lower_kernel<double><<<grid, 256, 0, st>>>(p, (const double*)x, (double*)d, uint32_t(total),
+                                                 dQ, dP, dCRS, dS, dR);
+    note_launch();
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) {
+    ConvProblem q = p;  // 1x1 convolution of D (C*R*S channels) with the K x CRS filter
+    q.C = crs;
+    q.H = p.P;
+    q.W = p.Q;
+    q.R = q.S = 1;
+    q.u = q.v = 1;
+    q.pad_h = q.pad_w = 0;
+    q.flip = false;
+    q.engine = 2;
+    q.x = View4{p.N, crs, p.P, p.Q, crs * p.P * p.Q, p.P * p.Q, p.Q, 1};
+    e = conv_forward(q, dt, d, f, y, alpha, beta, math, st);
+  }
+  tc::scratch_close(sc);
+  return e;
+}
+
 cudaError_t conv_forward(const ConvProblem& p, Dtype dt, const void* x, const void* f, void* y,
                          double alpha, double beta, int math, cudaStream_t st) {
   cudaError_t e;
+  if (p.engine == 1) return explicit_forward(p, dt, x, f, y, alpha, beta, math, st);
   if (use_tc(p, dt, math, FWD, &e))
     return tc_forward(p, (const float*)x, (const float*)f, (float*)y, alpha, beta, st);
   if (e != cudaSuccess) return e;

@@ -855,6 +855,11 @@ cudaError_t run_gemm(const ConvProblem& p, Gemm g, const __nv_bfloat16* a_hi,
     prm.o_sh = ov.sh;
     prm.o_sw = ov.sw;
     prm.out_mode = g.out_mode;
+    {
+      const int64_t span = std::abs(ov.sc) * (ov.c + 1) + std::abs(ov.sh) * (g.o_u + 1) +
+                           std::abs(ov.sw) * (g.o_v + 1);
+      prm.off32 = span < (int64_t(1) << 31) ? 1 : 0;
+    }
     prm.o_u = g.o_u;
     prm.o_v = g.o_v;
     prm.o_H = g.o_H;

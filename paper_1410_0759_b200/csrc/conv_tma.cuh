@@ -198,6 +198,7 @@ struct TmaParams {
   float* out;
   int64_t o_sn, o_sc, o_sh, o_sw;
   int out_mode;                // 0: column = channel; 1: column table (ph, pw, c)
+  int off32;                   // mode 1: every column offset fits in int32
   int o_u, o_v, o_H, o_W, o_ph, o_pw;  // mode 1: h = oh * o_u + ph - o_ph
   const uint32_t* coltab;
   float alpha, beta;
@@ -218,7 +219,7 @@ struct TCfg {
   static constexpr int A_BYTES = SUB * A_SUB;
   static constexpr int B_BYTES = SUB * B_SUB;
   static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;  // per CTA
-  static constexpr int COLTAB_BYTES = kColCache * 12;  // int64 offset + packed (ph, pw)
+  static constexpr int COLTAB_BYTES = kColCache * 16;  // int64 + int32 offset, packed (ph, pw)
   static constexpr int STAGES = (225 * 1024 - 2048 - COLTAB_BYTES) / STAGE_BYTES > 8
                                     ? 8
                                     : (225 * 1024 - 2048 - COLTAB_BYTES) / STAGE_BYTES;
@@ -328,6 +329,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) conv_tma_kernel(const __grid_c
   int* sk_flag = reinterpret_cast<int*>(tmem_slot + 1);
   long long* col_off = reinterpret_cast<long long*>(smem + S * C::STAGE_BYTES + 256);
   int* col_hw = reinterpret_cast<int*>(col_off + kColCache);
+  int* col_off32 = col_hw + kColCache;  // when P.off32: the offsets as int32 (16-byte reads)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = NC == 2 ? ptx::cluster_ctarank() : 0u;
@@ -507,6 +509,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) conv_tma_kernel(const __grid_c
         const uint32_t e = __ldg(P.coltab + c);
         const int ph = int(e >> 24), pw = int((e >> 16) & 255);
         col_off[c] = int64_t(e & 0xFFFF) * P.o_sc + int64_t(ph) * P.o_sh + int64_t(pw) * P.o_sw;
+        col_off32[c] = int(col_off[c]);
         col_hw[c] = (ph << 16) | pw;
       }
       asm volatile("bar.sync 1, 256;" ::: "memory");
@@ -608,6 +611,20 @@ __global__ void __launch_bounds__(kTmaThreads, 1) conv_tma_kernel(const __grid_c
             with_op(P.epi, fuse, segd, P.alpha, beta, [&](const auto& op) {
               store_cols(rowp, P.o_sc, nv, v, beta != 0.0f, auxp, aux_sc, op);
             });
+          } else if (plain && ctab_smem && P.off32 && cbase + 32 <= P.Ncol &&
+                     hb >= 0 && hb + P.o_u <= P.o_H && wb >= 0 && wb + P.o_v <= P.o_W) {
+            // interior row (every (ph, pw) of the row's super-pixel in range):
+            // offsets four at a time, no per-element bounds checks
+            float* rb = P.out + rowoff;
+            const int4* co = reinterpret_cast<const int4*>(col_off32 + cbase);
+#pragma unroll
+            for (int q = 0; q < 8; q++) {
+              const int4 o = co[q];
+              rb[o.x] = __uint_as_float(v[4 * q + 0]);
+              rb[o.y] = __uint_as_float(v[4 * q + 1]);
+              rb[o.z] = __uint_as_float(v[4 * q + 2]);
+              rb[o.w] = __uint_as_float(v[4 * q + 3]);
+            }
           } else if (plain && ctab_smem) {
 #pragma unroll
             for (int i = 0; i < 32; i++) {

@@ -33,6 +33,10 @@ struct ConvProblem {
   int64_t u, v, pad_h, pad_w;
   bool flip;  // CONVOLUTION mode: tap r reads h = p*u + (R-1-r) - pad (conv.py:182-192)
   View4 x, y;
+  // dnnp_engine: 1 = EXPLICIT materialises the lowered data matrix (forward;
+  // the memory negative control, reference conv.py:494-535); DIRECT and
+  // IMPLICIT (and every backward pass) run the implicit-GEMM kernels
+  int engine = 2;
 };
 
 namespace tc {

@@ -416,9 +416,12 @@ struct ArenaState {
   int depth = 0;
 };
 
+static std::mutex g_arena_map_mu;
+static std::map<std::pair<int, cudaStream_t>, ArenaState*> g_arenas;
+
 static ArenaState* arena_for(cudaStream_t st) {
-  static std::mutex map_mu;
-  static std::map<std::pair<int, cudaStream_t>, ArenaState*> arenas;
+  std::mutex& map_mu = g_arena_map_mu;
+  auto& arenas = g_arenas;
   int dev = 0;
   cudaGetDevice(&dev);
   std::lock_guard<std::mutex> g(map_mu);
@@ -623,6 +626,29 @@ cudaError_t pack_act(const View4& v, const float* x, int Cp, __nv_bfloat16* hi, 
 
 }  // namespace tc
 }  // namespace dnnp
+
+// additive C entry: the largest scratch footprint (bytes) any operation
+// took from the per-stream arenas since the last reset -- the device
+// counterpart of the reference's scratch allocation log (scratch.py,
+// test_scratch.py): implicit kernels need the packed operands only, the
+// explicit engine also the lowered data matrix.
+extern "C" int64_t dnnp_scratch_high_water(int reset) {
+  using namespace dnnp::tc;
+  std::vector<ArenaState*> all;
+  {
+    // copy under the map lock, then lock arenas one at a time (an op holding
+    // its arena may be waiting for the map lock in a nested Workspace)
+    std::lock_guard<std::mutex> g(g_arena_map_mu);
+    for (auto& kv : g_arenas) all.push_back(kv.second);
+  }
+  size_t high = 0;
+  for (ArenaState* a : all) {
+    std::lock_guard<std::recursive_mutex> ga(a->mu);
+    high = std::max(high, a->high);
+    if (reset) a->high = a->off;
+  }
+  return int64_t(high);
+}
 
 // additive C entries: time every main GEMM kernel (CUDA events around the
 // launch on the caller's stream) so a benchmark can report per-kernel

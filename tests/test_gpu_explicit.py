@@ -1,0 +1,64 @@
+"""Explicit-lowering engine: the memory negative
+control of the reference's scratch tests (pkg/tests/test_scratch.py:64-87).
+The EXPLICIT engine materialises the C*R*S x N*P*Q data matrix (reference
+conv.py:494-535) and multiplies it; its scratch grows with the filter area,
+the implicit kernels' does not; results agree with the implicit engine."""
+import numpy as np
+import pytest
+
+import paper_1410_0759_b200 as dp
+
+pytestmark = pytest.mark.gpu
+
+
+def run(engine, r, dt="f32", seed=0, n=4, c=8, h=24, k=16, stride=1, pad=None):
+    import torch
+    rng = np.random.default_rng(seed)
+    pad = r // 2 if pad is None else pad
+    npdt = np.float32 if dt == "f32" else np.float64
+    x = dp.TensorView(dp.make_desc(n, c, h, h, elem_type=dt),
+                      torch.from_numpy(rng.uniform(-0.5, 0.5, n * c * h * h).astype(npdt)).cuda())
+    f = dp.FilterView(dp.make_filter_desc(k, c, r, r, elem_type=dt),
+                      torch.from_numpy(rng.uniform(-0.5, 0.5, k * c * r * r).astype(npdt)).cuda())
+    cd = dp.ConvDesc(stride, stride, pad, pad)
+    p = dp.output_extent(h, r, stride, pad)
+    y = dp.empty_view(dp.make_desc(n, k, p, p, elem_type=dt), device="cuda")
+    torch.cuda.synchronize()
+    dp.scratch_high_water(reset=True)
+    dp.conv_forward(x, f, cd, engine, y)
+    torch.cuda.synchronize()
+    return y.buf.cpu().numpy(), dp.scratch_high_water()
+
+
+@pytest.mark.parametrize("dt,tol", [("f32", 1e-5), ("f64", 1e-12)])
+@pytest.mark.parametrize("r,stride", [(1, 1), (3, 1), (5, 2), (4, 3)])
+def test_explicit_matches_implicit(dt, tol, r, stride):
+    a, _ = run("explicit", r, dt, stride=stride)
+    b, _ = run("implicit", r, dt, stride=stride)
+    assert np.abs(a - b).max() / np.abs(b).max() <= tol
+
+
+def test_explicit_scratch_scales_with_filter_area():
+    sizes = {r: run("explicit", r, n=8, c=16, h=32)[1] for r in (1, 3, 5)}
+    lowered = {r: 8 * 16 * r * r * 32 * 32 * 4 for r in (1, 3, 5)}  # P = Q = 32 ('same')
+    assert sizes[1] < sizes[3] < sizes[5]
+    for r in (1, 3, 5):
+        assert sizes[r] >= lowered[r]
+
+
+def test_implicit_scratch_independent_of_filter_area():
+    sizes = {r: run("implicit", r, n=8, c=16, h=32)[1] for r in (1, 3, 5)}
+    # packed input (and packed filter, K*C*R*S*4 bytes) only: no C*R*S*N*P*Q term
+    lowered5 = 8 * 16 * 25 * 32 * 32 * 4
+    assert max(sizes.values()) - min(sizes.values()) <= 16 * 16 * 25 * 8 + (1 << 20)
+    assert max(sizes.values()) < lowered5 / 4
+
+
+def test_explicit_limit_is_alloc_too_large():
+    import torch
+    # 4 GiB guard (reference conv.py:31): C*R*S*N*P*Q*4 = 64*121*16*128*128*4 > 4 GiB
+    x = dp.TensorView(dp.make_desc(16, 64, 138, 138), torch.zeros(16 * 64 * 138 * 138, device="cuda"))
+    f = dp.FilterView(dp.make_filter_desc(8, 64, 11, 11), torch.zeros(8 * 64 * 121, device="cuda"))
+    y = dp.empty_view(dp.make_desc(16, 8, 128, 128), device="cuda")
+    with pytest.raises(dp.AllocTooLarge):
+        dp.conv_forward(x, f, dp.ConvDesc(), "explicit", y)
