@@ -112,10 +112,12 @@ class FilterView:
         self.desc = desc
         self.buf = buf
         self.is_cuda = cuda
+        self._torch = _is_torch(buf)
 
     @property
     def ptr(self):
-        return buf_info(self.buf)[0]
+        b = self.buf
+        return b.data_ptr() if self._torch else b.ctypes.data
 
     @property
     def array(self):

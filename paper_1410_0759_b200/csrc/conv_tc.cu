@@ -633,7 +633,8 @@ cudaError_t launch_tma(const TmaParams& prm, cudaStream_t st) {
     }
     attr_dev = dev;
   }
-  const int clusters = int(std::min<int64_t>(prm.tiles, kNumSMs / NC));
+  const int clusters =
+      prm.clusters > 0 ? prm.clusters : int(std::min<int64_t>(prm.tiles, kNumSMs / NC));
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(unsigned(clusters * NC));
   cfg.blockDim = dim3(kTmaThreads);
@@ -875,16 +876,43 @@ cudaError_t run_gemm(const ConvProblem& p, Gemm g, const __nv_bfloat16* a_hi,
     prm.dOW = make_magic(uint32_t(g.OW));
     prm.skip = getenv("DNNP_TC_SKIP") ? atoi(getenv("DNNP_TC_SKIP")) : 0;
     prm.prefetch = getenv("DNNP_TC_PREFETCH") ? atoi(getenv("DNNP_TC_PREFETCH")) : 0;
-    const int nseg = reduction_segments(nkb, kTK);
+    int nseg = reduction_segments(nkb, kTK);
     // a gated sum spread over segments cannot also add the caller's dx
     if (epi.gate >= 0 && nseg > 1 && beta != 0.0f) return cudaErrorNotSupported;
     // stream-K over the last, partial wave of tiles
     Workspace skw(st);
     {
-      const int G = int(std::min<int64_t>(tiles, kNumSMs / nc));
-      const int T = int(tiles), W = T / G, R = T % G;
-      const bool use_sk = nseg == 1 && getenv("DNNP_TC_SK") && !getenv("DNNP_TC_NO_SK") && W >= 1 && R > 0 && double(R) / G < 0.85 &&
-                          int64_t(R) * nkb < (int64_t(1) << 30);
+      int G = int(std::min<int64_t>(tiles, kNumSMs / nc));
+      const int T = int(tiles);
+      int W = T / G, R = T % G;
+      // stream-K over a partial last wave: default when the reduction is long
+      // enough (>= 32 k-blocks) to amortise the partial-tile fixup (measured:
+      // conv3 bwd-data 88 -> 74 us, conv2 bwd-data 150 -> 144 us; neutral or
+      // worse for short reductions, conv1 fwd 115 -> 121 us, tools/env_ab.py)
+      const bool sk_want = getenv("DNNP_TC_SK") ? true : nkb >= 32;
+      bool use_sk = nseg == 1 && sk_want && !getenv("DNNP_TC_NO_SK") && W >= 1 && R > 0 &&
+                    double(R) / G < 0.85 && int64_t(R) * nkb < (int64_t(1) << 30);
+      // Split-K for grids under half a wave (small minibatches, SURVEY
+      // configs[2]): every tile is cut along the reduction into pieces of
+      // >= 4 k-blocks spread over up to all SMs; each piece's chain stays
+      // under the accumulation cap, the finisher adds pieces in IEEE fp32.
+      {
+        const int Gmax = kNumSMs / nc, per_cap = std::max(1, 8192 / kTK);
+        if (!use_sk && !getenv("DNNP_TC_NO_SPLIT") && T * 2 <= Gmax && nkb >= 8 &&
+            int64_t(T) * nkb < (int64_t(1) << 30)) {
+          int Gs = int(std::min<int64_t>(Gmax, int64_t(T) * (nkb / 4)));
+          const int64_t U = int64_t(T) * nkb;
+          if (ceil_div(U, int64_t(Gs)) > per_cap) Gs = int(std::min<int64_t>(Gmax, ceil_div(U, int64_t(per_cap))));
+          if (Gs > T && ceil_div(U, int64_t(Gs)) <= per_cap) {
+            G = Gs;
+            W = 0;
+            R = T;
+            use_sk = true;
+            nseg = 1;
+          }
+        }
+      }
+      prm.clusters = G;
       if (use_sk) {
         const int U = R * nkb, G2 = std::min(G, U);
         int maxp = 1;

@@ -193,6 +193,7 @@ struct TmaParams {
   // stream-K: full waves W (tiles cid + i*G), then units [cid*U/G, (cid+1)*U/G)
   // of the last R = tiles - W*G tiles; U = R * nkb.  sk = 0: plain persistent.
   int sk, W, U, maxp;
+  int clusters;                // launched clusters (0: min(tiles, SMs / NC))
   float* skws;                 // partials [R][NC][maxp][128][BN]
   int* skcnt;                  // arrival counters [R][NC], zero on entry, reset by the finisher
   float* out;
