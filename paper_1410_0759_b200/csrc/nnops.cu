@@ -626,7 +626,7 @@ struct PoolGeom {
 // order with numpy argmax NaN semantics (the first NaN wins); argmax is the
 // LOGICAL NCHW index.  Average divides by the in-image count.  32-bit index
 // arithmetic (extents < 2^31 checked on the host), 64-bit only for offsets.
-template <typename T>
+template <typename T, int KW>
 __global__ void __launch_bounds__(256) pool_fwd_kernel(PoolGeom g, const T* __restrict__ x,
                                                        T* __restrict__ y, int64_t* argmax,
                                                        int kind, int64_t total) {
@@ -644,7 +644,33 @@ __global__ void __launch_bounds__(256) pool_fwd_kernel(PoolGeom g, const T* __re
     const int ws = max(0, ws0), we = min(W, ws0 + ww);
     const T* xb = x + int64_t(n) * g.x.sn + int64_t(c) * g.x.sc;
     T out;
-    if (kind == 0) {
+    if (KW > 0 && hs0 >= 0 && ws0 >= 0 && hs0 + KW <= H && ws0 + KW <= W) {
+      // interior window of the specialised size: KW*KW independent loads,
+      // branch-free first-max / first-NaN selection (or the scan-order sum)
+      T v[KW > 0 ? KW * KW : 1];
+#pragma unroll
+      for (int a = 0; a < KW; a++)
+#pragma unroll
+        for (int b = 0; b < KW; b++) v[a * KW + b] = __ldg(xb + (hs0 + a) * xsh + (ws0 + b) * xsw);
+      if (kind == 0) {
+        T best = v[0];
+        int bk = 0;
+#pragma unroll
+        for (int k = 1; k < KW * KW; k++) {
+          const bool take = v[k] > best || (v[k] != v[k] && best == best);
+          best = take ? v[k] : best;
+          bk = take ? k : bk;
+        }
+        out = best;
+        if (argmax)
+          argmax[i] = ((int64_t(n) * C + c) * H + hs0 + bk / KW) * W + ws0 + bk % KW;
+      } else {
+        T sacc = T(0);
+#pragma unroll
+        for (int k = 0; k < KW * KW; k++) sacc = dadd<T>(sacc, v[k]);
+        out = sacc / T(KW * KW);
+      }
+    } else if (kind == 0) {
       T best = xb[hs * xsh + ws * xsw];
       int bh = hs, bw = ws;
       bool nan = best != best;
@@ -745,7 +771,80 @@ __global__ void pool_argmax_check(PoolGeom g, const int64_t* __restrict__ argmax
 // Plane-tiled forms (one block per (n, c) plane, the plane staged in shared
 // memory with coalesced loads; same window semantics and summation order as
 // the per-element kernels above).
+// Contiguous plane <-> shared memory with 16-byte global accesses: scalar
+// head up to the first 16-byte boundary, vectors, scalar tail (planes of odd
+// size start at any 4-byte offset).  Every vector is issued before any
+// shared-memory store, so a thread keeps all its loads in flight.
 template <typename T>
+__device__ __forceinline__ void plane_to_smem(T* xs, const T* __restrict__ xb, int n) {
+  constexpr int V = 16 / sizeof(T);
+  const int mis = int((reinterpret_cast<uintptr_t>(xb) / sizeof(T)) % V);
+  const int head = min(n, (V - mis) % V);
+  const int nv = (n - head) / V;
+  const int B = blockDim.x;
+  if (int(threadIdx.x) < head) xs[threadIdx.x] = xb[threadIdx.x];
+  const uint4* src = reinterpret_cast<const uint4*>(xb + head);
+  int j = threadIdx.x;
+  for (; j + 3 * B < nv; j += 4 * B) {
+    uint4 v[4];
+#pragma unroll
+    for (int k = 0; k < 4; k++) v[k] = __ldg(src + j + k * B);
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+      const T* e = reinterpret_cast<const T*>(&v[k]);
+#pragma unroll
+      for (int l = 0; l < V; l++) xs[head + (j + k * B) * V + l] = e[l];
+    }
+  }
+  for (; j < nv; j += B) {
+    const uint4 v = __ldg(src + j);
+    const T* e = reinterpret_cast<const T*>(&v);
+#pragma unroll
+    for (int l = 0; l < V; l++) xs[head + j * V + l] = e[l];
+  }
+  for (int i = head + nv * V + threadIdx.x; i < n; i += B) xs[i] = xb[i];
+}
+
+template <typename T>
+__device__ __forceinline__ void smem_to_plane(T* __restrict__ xb, const T* xs, int n) {
+  constexpr int V = 16 / sizeof(T);
+  const int mis = int((reinterpret_cast<uintptr_t>(xb) / sizeof(T)) % V);
+  const int head = min(n, (V - mis) % V);
+  const int nv = (n - head) / V;
+  const int B = blockDim.x;
+  if (int(threadIdx.x) < head) xb[threadIdx.x] = xs[threadIdx.x];
+  uint4* dst = reinterpret_cast<uint4*>(xb + head);
+  for (int j = threadIdx.x; j < nv; j += B) {
+    uint4 v;
+    T* e = reinterpret_cast<T*>(&v);
+#pragma unroll
+    for (int l = 0; l < V; l++) e[l] = xs[head + j * V + l];
+    dst[j] = v;
+  }
+  for (int i = head + nv * V + threadIdx.x; i < n; i += B) xb[i] = xs[i];
+}
+
+// Max over a KW x KW window in (h, w) scan order, branch-free: a later value
+// replaces the best when greater, or when it is NaN and the best is not, so
+// the first maximum and the first NaN win (reference nnops.py:180-197).
+template <typename T, int KW>
+__device__ __forceinline__ void window_max(const T* xs, int W, int base, T& best, int& bi) {
+  best = xs[base];
+  bi = base;
+#pragma unroll
+  for (int a = 0; a < KW; a++)
+#pragma unroll
+    for (int b = 0; b < KW; b++) {
+      if (a == 0 && b == 0) continue;
+      const int idx = base + a * W + b;
+      const T v = xs[idx];
+      const bool take = v > best || (v != v && best == best);
+      best = take ? v : best;
+      bi = take ? idx : bi;
+    }
+}
+
+template <typename T, int KW>
 __global__ void __launch_bounds__(256) pool_fwd_plane_kernel(PoolGeom g, const T* __restrict__ x,
                                                              T* __restrict__ y, int64_t* argmax,
                                                              int kind) {
@@ -760,17 +859,7 @@ __global__ void __launch_bounds__(256) pool_fwd_plane_kernel(PoolGeom g, const T
     const int n = int(nu), c = int(cu);
     const T* xb = x + int64_t(n) * g.x.sn + int64_t(c) * g.x.sc;
     if (g.x.sw == 1 && g.x.sh == W) {
-      // contiguous plane: batches of 4 independent loads per thread
-      const int HW = H * W;
-      int i = threadIdx.x;
-      for (; i + 3 * 256 < HW; i += 4 * 256) {
-        T v0 = xb[i], v1 = xb[i + 256], v2 = xb[i + 512], v3 = xb[i + 768];
-        xs[i] = v0;
-        xs[i + 256] = v1;
-        xs[i + 512] = v2;
-        xs[i + 768] = v3;
-      }
-      for (; i < HW; i += 256) xs[i] = xb[i];
+      plane_to_smem(xs, xb, H * W);  // contiguous plane: 16-byte loads
     } else {
       for (int i = threadIdx.x; i < H * W; i += blockDim.x) {
         uint32_t h, w;
@@ -788,7 +877,22 @@ __global__ void __launch_bounds__(256) pool_fwd_plane_kernel(PoolGeom g, const T
       const int hs = max(0, hs0), he = min(H, hs0 + wh);
       const int ws = max(0, ws0), we = min(W, ws0 + ww);
       T out;
-      if (kind == 0) {
+      if (KW > 0 && hs0 >= 0 && ws0 >= 0 && hs0 + KW <= H && ws0 + KW <= W) {
+        // interior window of the specialised size: unrolled, branch-free
+        const int base = hs0 * W + ws0;
+        if (kind == 0) {
+          int bi;
+          window_max<T, KW>(xs, W, base, out, bi);
+          if (argmax) argmax[int64_t(pl) * P * Q + o] = int64_t(pl) * H * W + bi;
+        } else {
+          T sacc = T(0);
+#pragma unroll
+          for (int a = 0; a < KW; a++)
+#pragma unroll
+            for (int b = 0; b < KW; b++) sacc = dadd<T>(sacc, xs[base + a * W + b]);
+          out = sacc / T(KW * KW);
+        }
+      } else if (kind == 0) {
         T best = xs[hs * W + ws];
         int bi = hs * W + ws;
         bool nan = best != best;
@@ -896,7 +1000,7 @@ __global__ void __launch_bounds__(256) pool_bwd_plane_kernel(PoolGeom g, const T
       }
       __syncthreads();
       if (g.x.sw == 1 && g.x.sh == W) {
-        for (int i = threadIdx.x; i < HW; i += blockDim.x) dxb[i] = xs[i];
+        smem_to_plane(dxb, xs, HW);
       } else {
         for (int i = threadIdx.x; i < HW; i += blockDim.x) {
           uint32_t hu, wu;
@@ -953,6 +1057,25 @@ __global__ void pool_bwd_serial(PoolGeom g, const T* dy, T* dx, const int64_t* a
   }
 }
 
+// Plane kernels: one (n, c) plane per block iteration, staged in shared
+// memory.  Small blocks and an uncapped grid keep many planes per SM in
+// flight, so one block's load phase overlaps another's compute phase.
+static int pool_threads() {
+  static int t = [] {
+    const char* e = getenv("DNNP_POOL_THREADS");
+    const int v = e ? atoi(e) : 128;
+    return (v == 64 || v == 128 || v == 256) ? v : 128;
+  }();
+  return t;
+}
+static int64_t pool_grid_cap() {
+  static int64_t c = [] {
+    const char* e = getenv("DNNP_POOL_GRID");
+    return e ? int64_t(atoll(e)) : (int64_t(1) << 30);
+  }();
+  return c;
+}
+
 static PoolGeom pool_geom(const PoolProblem& pp, const View4& xv, const View4& yv) {
   PoolGeom g;
   g.x = xv;
@@ -977,24 +1100,43 @@ cudaError_t pool_forward(const PoolProblem& pp, Dtype dt, const View4& xv, const
   PoolGeom g = pool_geom(pp, xv, yv);
   const size_t eb = dt == F32 ? 4 : 8;
   const size_t psm = size_t(xv.h) * xv.w * eb;
-  if (psm <= 48 * 1024 && xv.n * xv.c < (int64_t(1) << 31)) {
-    const unsigned pg = unsigned(std::min<int64_t>(xv.n * xv.c, int64_t(kNumSMs) * 16));
-    if (dt == F32)
-      pool_fwd_plane_kernel<float><<<pg, 256, psm, st>>>(g, (const float*)x, (float*)y, argmax,
-                                                         pp.kind);
-    else
-      pool_fwd_plane_kernel<double><<<pg, 256, psm, st>>>(g, (const double*)x, (double*)y,
-                                                          argmax, pp.kind);
+  if (psm <= 48 * 1024 && xv.n * xv.c < (int64_t(1) << 31) && !getenv("DNNP_POOL_DIRECT")) {
+    const int thr = pool_threads();
+    const unsigned pg = unsigned(std::min<int64_t>(xv.n * xv.c, pool_grid_cap()));
+    const int kw = (pp.wh == pp.ww && (pp.wh == 2 || pp.wh == 3)) ? int(pp.wh) : 0;
+    auto go = [&](auto tag, auto kwc) {
+      using TT = decltype(tag);
+      pool_fwd_plane_kernel<TT, decltype(kwc)::value><<<pg, thr, psm, st>>>(
+          g, (const TT*)x, (TT*)y, argmax, pp.kind);
+    };
+    using K0 = std::integral_constant<int, 0>;
+    using K2 = std::integral_constant<int, 2>;
+    using K3 = std::integral_constant<int, 3>;
+    if (dt == F32) {
+      if (kw == 3) go(float(), K3()); else if (kw == 2) go(float(), K2()); else go(float(), K0());
+    } else {
+      if (kw == 3) go(double(), K3()); else if (kw == 2) go(double(), K2()); else go(double(), K0());
+    }
     note_launch();
     return cudaGetLastError();
   }
   unsigned grid = grid_for(total, 256, 8);
-  if (dt == F32)
-    pool_fwd_kernel<float><<<grid, 256, 0, st>>>(g, (const float*)x, (float*)y, argmax, pp.kind,
-                                                 total);
-  else
-    pool_fwd_kernel<double><<<grid, 256, 0, st>>>(g, (const double*)x, (double*)y, argmax,
-                                                  pp.kind, total);
+  const int kwd = (pp.wh == pp.ww && (pp.wh == 2 || pp.wh == 3)) ? int(pp.wh) : 0;
+  auto god = [&](auto tag, auto kwc) {
+    using TT = decltype(tag);
+    pool_fwd_kernel<TT, decltype(kwc)::value><<<grid, 256, 0, st>>>(g, (const TT*)x, (TT*)y,
+                                                                     argmax, pp.kind, total);
+  };
+  {
+    using K0 = std::integral_constant<int, 0>;
+    using K2 = std::integral_constant<int, 2>;
+    using K3 = std::integral_constant<int, 3>;
+    if (dt == F32) {
+      if (kwd == 3) god(float(), K3()); else if (kwd == 2) god(float(), K2()); else god(float(), K0());
+    } else {
+      if (kwd == 3) god(double(), K3()); else if (kwd == 2) god(double(), K2()); else god(double(), K0());
+    }
+  }
   note_launch();
   return cudaGetLastError();
 }
@@ -1014,14 +1156,15 @@ cudaError_t pool_backward(const PoolProblem& pp, Dtype dt, const View4& dyv, con
     if (e != cudaSuccess) return e;
     int* bad = static_cast<int*>(ws.p);
     cudaMemsetAsync(bad, 0, sizeof(int), st);
-    const unsigned pg = unsigned(std::min<int64_t>(dxv.n * dxv.c, int64_t(kNumSMs) * 16));
+    const unsigned pg = unsigned(std::min<int64_t>(dxv.n * dxv.c, pool_grid_cap()));
+    const int thr = pool_threads();
     // windows covering one element per dim: ceil(window / stride)
     const int64_t kmax = std::max(ceil_div(pp.wh, pp.sh), ceil_div(pp.ww, pp.sw));
     const int mk = kmax <= 2 ? 2 : (kmax <= 4 ? 4 : 0);
     auto launch = [&](auto tag, auto kindc, auto mkc) {
       using TT = decltype(tag);
       pool_bwd_plane_kernel<TT, decltype(kindc)::value, decltype(mkc)::value>
-          <<<pg, 256, psm, st>>>(g, (const TT*)dy, (TT*)dx, argmax, bad);
+          <<<pg, thr, psm, st>>>(g, (const TT*)dy, (TT*)dx, argmax, bad);
     };
     using I0 = std::integral_constant<int, 0>;
     using I1 = std::integral_constant<int, 1>;
