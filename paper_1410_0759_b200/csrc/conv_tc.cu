@@ -1096,7 +1096,36 @@ cudaError_t run_tc(bool dgrad, const ConvProblem& p, const float* in, const View
                    p.v <= 8 && p.C * p.u * p.v <= 64;
   int IH, IW, Cp;
   int64_t Nimg = p.N;
-  if (s2d) {
+  bool fold = !dgrad && tma_on && fold_taps(p.C, p.S, p.u, p.v, s2d);
+  if (fold) {
+    // horizontal taps folded into channels: R x 1 over S*C channels (kept
+    // only when the im2col map accepts the geometry)
+    Gemm gf = g;
+    PackGeom& pf = gf.pg;
+    pf.su = 1;
+    pf.sv = int(p.S);
+    pf.C = int(p.S * p.C);
+    pf.S = 1;
+    gf.tma = 1;
+    gf.OH = int(p.P);
+    gf.OW = int(p.Q);
+    gf.u = int(p.u);
+    gf.v = 1;
+    gf.pad_h = int(p.pad_h);
+    gf.pad_w = 0;
+    pf.Ncol = int(p.K);
+    gf.out_mode = 0;
+    if (tma_geometry_ok(gf, int(p.H), int(p.Q), pf.R, 1, Nimg * gf.OH * gf.OW)) {
+      g = gf;
+      IH = int(p.H);
+      IW = int(p.Q);
+      Cp = int(ceil_div(pg.C, 16) * 16);
+    } else {
+      fold = false;
+    }
+  }
+  if (fold) {
+  } else if (s2d) {
     const int u = int(p.u), v = int(p.v);
     const int R2 = int(ceil_div(p.R, u)), S2 = int(ceil_div(p.S, v));
     int H2 = int(p.P) - 1 + R2, W2 = int(p.Q) - 1 + S2;
@@ -1192,7 +1221,7 @@ cudaError_t run_tc(bool dgrad, const ConvProblem& p, const float* in, const View
   // (measured: helps the unit-stride bwd-data of conv2, 233 -> 204 us; not the
   // space-to-depth conv1 passes, whose epilogue then dominates)
   const bool blockable =
-      g.tma && pg.Ncol <= 64 && !env_off("DNNP_TC_NO_BLOCK") &&
+      g.tma && !fold && pg.Ncol <= 64 && !env_off("DNNP_TC_NO_BLOCK") &&
       (env_off("DNNP_TC_BLOCK_S2D") ? (!dgrad ? g.out_mode == 0 : (s2d || g.out_mode == 0))
                                     : (!s2d && g.out_mode == 0 && (env_off("DNNP_TC_BLOCK") || dgrad)));
   if (blockable) {
@@ -1229,7 +1258,9 @@ cudaError_t run_tc(bool dgrad, const ConvProblem& p, const float* in, const View
   if (e != cudaSuccess) return e;
   auto* a_hi = static_cast<__nv_bfloat16*>(ws.p);
   auto* a_lo = a_hi + act;
-  if (s2d && !dgrad)
+  if (fold)
+    e = pack_act_fold(inv, in, int(p.S), int(p.v), int(p.pad_w), IW, Cp, a_hi, a_lo, st);
+  else if (s2d && !dgrad)
     e = pack_act_s2d(inv, in, int(p.u), int(p.v), int(p.pad_h), int(p.pad_w), IH, IW, Cp, a_hi,
                      a_lo, st);
   else

@@ -80,6 +80,16 @@ cudaError_t pack_act_s2d(const View4& v, const float* x, int u, int vv, int pad_
                          int H2, int W2, int Cp, __nv_bfloat16* hi, __nv_bfloat16* lo,
                          cudaStream_t st);
 
+// Horizontal tap folding for stride-(u, v) convolutions with few channels
+// (paper Table-2 layer1: C = 3, 11 x 11): the S horizontal taps become
+// channels, x'[n][h][q][j*C + c] = x[n][c][h][q*v + j - pad_w] (zero outside),
+// so the convolution runs as R x 1 over S*C channels with no horizontal
+// stride or padding (a reduction S*C padded once, not C padded S times).
+cudaError_t pack_act_fold(const View4& v, const float* x, int S, int vv, int pad_w, int Q, int Cp,
+                          __nv_bfloat16* hi, __nv_bfloat16* lo, cudaStream_t st);
+// whether folding applies (and pays) for a problem; s2d takes precedence
+bool fold_taps(int64_t C, int64_t S, int64_t u, int64_t v, bool s2d);
+
 // Strided fp32 4-D view -> channel-innermost bf16 hi/lo planes
 // [n][h][w][Cp] (Cp = channels padded to a multiple of 8, zero filled).
 cudaError_t pack_act(const View4& v, const float* x, int Cp, __nv_bfloat16* hi, __nv_bfloat16* lo,

@@ -337,6 +337,46 @@ __global__ void __launch_bounds__(512) pack_act_s2d_quad_kernel(View4 v, const f
   }
 }
 
+// Tap folding: one thread per output pixel (n, h, q), walking its Cp folded
+// channels (j, c) with running counters; loads are pixel-consecutive across
+// the warp (w = q v + j - pad_w), writes 16-byte hi / lo chunks.
+__global__ void __launch_bounds__(256) pack_act_fold_kernel(View4 v, const float* __restrict__ x,
+                                                            int S, int vv, int pad_w, int Q,
+                                                            int Cp, __nv_bfloat16* __restrict__ hi,
+                                                            __nv_bfloat16* __restrict__ lo,
+                                                            uint32_t npix, MagicDiv dHQ,
+                                                            MagicDiv dQ) {
+  const int C = int(v.c), Cs = S * C;
+  for (uint32_t pix = blockIdx.x * blockDim.x + threadIdx.x; pix < npix;
+       pix += gridDim.x * blockDim.x) {
+    uint32_t n, rem, h, q;
+    mdivmod(pix, dHQ, n, rem);
+    mdivmod(rem, dQ, h, q);
+    const float* src = x + int64_t(n) * v.sn + int64_t(h) * v.sh;
+    const int wb = int(q) * vv - pad_w;
+    int c = 0, j = 0;
+    for (int g = 0; g < Cp / 8; g++) {
+      __align__(16) __nv_bfloat16 vh[8], vl[8];
+#pragma unroll
+      for (int k = 0; k < 8; k++) {
+        float val = 0.0f;
+        if (g * 8 + k < Cs) {
+          const int w = wb + j;
+          if (unsigned(w) < unsigned(v.w)) val = __ldg(src + int64_t(c) * v.sc + int64_t(w) * v.sw);
+          if (++c == C) {
+            c = 0;
+            ++j;
+          }
+        }
+        split_bf16(val, vh[k], vl[k]);
+      }
+      const int64_t o = int64_t(pix) * Cp + g * 8;
+      *reinterpret_cast<uint4*>(hi + o) = *reinterpret_cast<const uint4*>(vh);
+      *reinterpret_cast<uint4*>(lo + o) = *reinterpret_cast<const uint4*>(vl);
+    }
+  }
+}
+
 }  // namespace
 
 cudaError_t pack_act_s2d(const View4& v, const float* x, int u, int vv, int pad_h, int pad_w,
@@ -602,6 +642,24 @@ cudaError_t make_tmap_im2col(CUtensorMap* map, const void* base, const Im2colGeo
                   CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+bool fold_taps(int64_t C, int64_t S, int64_t u, int64_t v, bool s2d) {
+  if (s2d || getenv("DNNP_TC_NO_FOLD") || S < 2 || S * C > 64 || v > 8) return false;
+  // reduction per vertical tap: folded S*C padded once vs C padded S times
+  const int64_t folded = ceil_div(S * C, 16) * 16, plain = S * ceil_div(C, 16) * 16;
+  return folded * 4 <= plain * 3;
+}
+
+cudaError_t pack_act_fold(const View4& v, const float* x, int S, int vv, int pad_w, int Q, int Cp,
+                          __nv_bfloat16* hi, __nv_bfloat16* lo, cudaStream_t st) {
+  const int64_t npix = v.n * v.h * Q;
+  if (npix >= (int64_t(1) << 32)) return cudaErrorInvalidValue;
+  pack_act_fold_kernel<<<grid_for(npix, 256, 8), 256, 0, st>>>(
+      v, x, S, vv, pad_w, Q, Cp, hi, lo, uint32_t(npix), make_magic(uint32_t(v.h * Q)),
+      make_magic(uint32_t(Q)));
+  note_launch();
+  return cudaGetLastError();
 }
 
 cudaError_t pack_act(const View4& v, const float* x, int Cp, __nv_bfloat16* hi, __nv_bfloat16* lo,

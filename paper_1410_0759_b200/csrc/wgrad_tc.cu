@@ -602,17 +602,20 @@ cudaError_t wgrad_tma(const ConvProblem& p, const float* dy, const float* x, flo
   if (getenv("DNNP_TC_NO_TMA")) return cudaErrorNotSupported;
   const bool s2d = !getenv("DNNP_TC_NO_S2D") && (p.u > 1 || p.v > 1) && p.u <= 8 && p.v <= 8 &&
                    p.C * p.u * p.v <= 64;
-  const int su = s2d ? int(p.u) : 1, sv = s2d ? int(p.v) : 1;
-  const int R2 = int(ceil_div(p.R, su)), S2 = int(ceil_div(p.S, sv));
+  // horizontal tap folding (stride-1-style few-channel layers): the S taps
+  // as channels, the reduce maps folded channel j*C + c back to s = j
+  const bool fold = fold_taps(p.C, p.S, p.u, p.v, s2d) && p.Q * p.v + p.S <= (int64_t(1) << 20);
+  const int su = s2d ? int(p.u) : 1, sv = s2d ? int(p.v) : (fold ? int(p.S) : 1);
+  const int R2 = int(ceil_div(p.R, su)), S2 = fold ? 1 : int(ceil_div(p.S, sv));
   const int Cg = su * sv * int(p.C);                 // GEMM channels per tap
   const int Cp = int(ceil_div(Cg, 16) * 16);         // packed x channels
   const int nCB = int(ceil_div(Cp, 64)), Cpf = nCB * 64;
   const int taps = R2 * S2;
   const int ncolx = taps * Cpf;                      // x-operand extent (padded)
   const int IH = s2d ? int(p.P) - 1 + R2 : int(p.H);
-  const int IW = s2d ? int(p.Q) - 1 + S2 : int(p.W);
-  const int gu = s2d ? 1 : int(p.u), gv = s2d ? 1 : int(p.v);
-  const int gph = s2d ? 0 : int(p.pad_h), gpw = s2d ? 0 : int(p.pad_w);
+  const int IW = s2d ? int(p.Q) - 1 + S2 : (fold ? int(p.Q) : int(p.W));
+  const int gu = s2d ? 1 : int(p.u), gv = (s2d || fold) ? 1 : int(p.v);
+  const int gph = s2d ? 0 : int(p.pad_h), gpw = (s2d || fold) ? 0 : int(p.pad_w);
   if (gu > 8 || gv > 8 || R2 > 128 || S2 > 128) return cudaErrorNotSupported;
   const int lower_h = -gph, lower_w = -gpw;
   const int upper_h = (int(p.P) - 1) * gu + 1 - gph - IH;
@@ -654,7 +657,9 @@ cudaError_t wgrad_tma(const ConvProblem& p, const float* dy, const float* x, flo
   auto* x_lo = x_hi + x_elems;
   float* part = reinterpret_cast<float*>(x_lo + x_elems);
   if ((e = pack_act(p.y, dy, Kp64, dy_hi, dy_lo, st)) != cudaSuccess) return e;
-  if (s2d)
+  if (fold)
+    e = pack_act_fold(p.x, x, int(p.S), int(p.v), int(p.pad_w), IW, Cp, x_hi, x_lo, st);
+  else if (s2d)
     e = pack_act_s2d(p.x, x, su, sv, int(p.pad_h), int(p.pad_w), IH, IW, Cp, x_hi, x_lo, st);
   else
     e = pack_act(p.x, x, Cp, x_hi, x_lo, st);

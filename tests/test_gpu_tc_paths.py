@@ -209,3 +209,28 @@ def test_long_reduction_accuracy():
     truncation budget, so the forward / bwd-data run segmented (vs fp64)."""
     check(run_case((2, 512, 9, 9, 64, 7, 7, 1, 1, 3, 3), passes=("fwd",), seed=12))
     check(run_case((2, 64, 9, 9, 512, 7, 7, 1, 1, 3, 3), passes=("bwd_data",), seed=12))
+
+
+#        N  C   H   W   K   R   S  u  v ph pw
+FOLD_SHAPES = [
+    (2, 3, 40, 44, 96, 11, 11, 1, 1, 0, 0),   # paper Table-2 layer1-like (C=3, 11x11, stride 1)
+    (2, 3, 17, 19, 24, 5, 7, 1, 1, 2, 3),     # anisotropic filter / padding
+    (2, 8, 23, 21, 16, 5, 5, 4, 4, 2, 2),     # strided, C*u*v > 64 (no space-to-depth)
+    (2, 4, 15, 15, 32, 3, 9, 2, 1, 1, 4),     # vertical stride only
+]
+
+
+@pytest.mark.parametrize("shape", FOLD_SHAPES)
+@pytest.mark.parametrize("mode", ["convolution", "cross_correlation"])
+def test_tap_folding(shape, mode):
+    """Horizontal taps folded into channels (forward, backward-filter) vs the
+    oracle, and the unfolded path for comparison (DNNP_TC_NO_FOLD)."""
+    check(run_case(shape, mode=mode, seed=13))
+    with env(DNNP_TC_NO_FOLD=1):
+        check(run_case(shape, passes=("fwd", "bwd_filter"), mode=mode, seed=13))
+
+
+def test_tap_folding_layouts_and_scalars():
+    check(run_case(FOLD_SHAPES[0], layout_in="nhwc", layout_out="nchw", seed=14))
+    check(run_case(FOLD_SHAPES[1], passes=("fwd",), alpha=0.5, beta=-1.0, seed=14))
+    check(run_case(FOLD_SHAPES[2], accumulate=True, seed=14))
