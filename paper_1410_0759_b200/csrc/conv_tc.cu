@@ -1225,7 +1225,23 @@ cudaError_t run_tc(bool dgrad, const ConvProblem& p, const float* in, const View
       (env_off("DNNP_TC_BLOCK_S2D") ? (!dgrad ? g.out_mode == 0 : (s2d || g.out_mode == 0))
                                     : (!s2d && g.out_mode == 0 && (env_off("DNNP_TC_BLOCK") || dgrad)));
   if (blockable) {
-    const int bw = 2;
+    // blocking factor: 2, or up to 8 (the im2col traversal stride limit) for
+    // very narrow unit-stride bwd-data outputs (table2 layer1: C = 3), by the
+    // useful fraction of the MMA work: (bw N / padded) * S / (S + bw - 1)
+    int bw = 2;
+    if (dgrad && !s2d && g.out_mode == 0 && !env_off("DNNP_TC_BW2")) {
+      double best = -1.0;
+      for (int b : {2, 4, 8}) {
+        const int n = b * pg.Ncol;
+        if (n > 256) break;
+        const double pad = double(ceil_div(n, 64) * 64);
+        const double sc = (n / pad) * double(pg.Sg) / double(pg.Sg + (b - 1) * pg.vstep);
+        if (sc > best + 1e-9) {
+          best = sc;
+          bw = b;
+        }
+      }
+    }
     Gemm gb = g;
     PackGeom& pb = gb.pg;
     pb.bw = bw;

@@ -234,3 +234,15 @@ def test_tap_folding_layouts_and_scalars():
     check(run_case(FOLD_SHAPES[0], layout_in="nhwc", layout_out="nchw", seed=14))
     check(run_case(FOLD_SHAPES[1], passes=("fwd",), alpha=0.5, beta=-1.0, seed=14))
     check(run_case(FOLD_SHAPES[2], accumulate=True, seed=14))
+
+
+@pytest.mark.parametrize("shape", [(2, 3, 40, 44, 96, 11, 11, 1, 1, 0, 0),
+                                   (2, 5, 19, 23, 24, 5, 7, 1, 1, 2, 3),
+                                   (3, 12, 17, 15, 40, 3, 3, 1, 1, 1, 1)])
+def test_wide_column_blocking(shape):
+    """Narrow unit-stride bwd-data outputs block 4 or 8 output columns per
+    GEMM row (DNNP_TC_BW2 pins the factor to 2)."""
+    check(run_case(shape, passes=("bwd_data",), seed=15))
+    check(run_case(shape, passes=("bwd_data",), accumulate=True, seed=15))
+    with env(DNNP_TC_BW2=1):
+        check(run_case(shape, passes=("bwd_data",), seed=15))
