@@ -92,6 +92,66 @@ __global__ void __launch_bounds__(256) pack_act_kernel(View4 v, const float* __r
   }
 }
 
+// Same transpose with 64-pixel jobs: each thread loads 16 values (two
+// 32-pixel halves x 8 channel phases) before the barrier, twice the bytes in
+// flight per synchronisation of the 32-pixel version.
+template <int PIXJ>
+__global__ void __launch_bounds__(256) pack_act_wide_kernel(View4 v, const float* __restrict__ x,
+                                                            int Cp, __nv_bfloat16* __restrict__ hi,
+                                                            __nv_bfloat16* __restrict__ lo,
+                                                            uint32_t npix, MagicDiv dHW,
+                                                            MagicDiv dW) {
+  __shared__ float tile[kCh][PIXJ + 1];
+  constexpr int HALVES = PIXJ / 32;
+  const int lp = threadIdx.x & 31, lc = threadIdx.x >> 5;  // read role: pixel, channel phase
+  const int wp = threadIdx.x >> 3, wg = threadIdx.x & 7;   // write role: pixel, channel group
+  const uint32_t ntiles = (npix + PIXJ - 1) / PIXJ;
+  const uint32_t nslabs = uint32_t((Cp + kCh - 1) / kCh);
+  const int C = int(v.c);
+  for (uint32_t job = blockIdx.x; job < ntiles * nslabs; job += gridDim.x) {
+    const uint32_t pt = nslabs == 1 ? job : job / nslabs;
+    const int slab = int(job - pt * nslabs);
+    const int c_lo = slab * kCh, nch = min(kCh, Cp - c_lo);
+    const int cvalid = C - c_lo < nch ? C - c_lo : nch;
+    float val[HALVES][kCh / 8];
+#pragma unroll
+    for (int hf = 0; hf < HALVES; hf++) {
+      const uint32_t pix = pt * PIXJ + hf * 32 + lp;
+      const float* src = nullptr;
+      if (pix < npix) {
+        uint32_t n, rem, h, w;
+        mdivmod(pix, dHW, n, rem);
+        mdivmod(rem, dW, h, w);
+        src = x + int64_t(n) * v.sn + int64_t(h) * v.sh + int64_t(w) * v.sw + int64_t(c_lo) * v.sc;
+      }
+#pragma unroll
+      for (int i = 0; i < kCh / 8; i++) {
+        const int c = lc + 8 * i;
+        val[hf][i] = (src && c < cvalid) ? __ldg(src + int64_t(c) * v.sc) : 0.0f;
+      }
+    }
+#pragma unroll
+    for (int hf = 0; hf < HALVES; hf++)
+#pragma unroll
+      for (int i = 0; i < kCh / 8; i++) tile[lc + 8 * i][hf * 32 + lp] = val[hf][i];
+    __syncthreads();
+#pragma unroll
+    for (int hf = 0; hf < PIXJ / 32; hf++) {
+      const int px = hf * 32 + wp;
+      const uint32_t opix = pt * PIXJ + px;
+      if (opix < npix && wg * 8 < nch) {
+        __align__(16) __nv_bfloat16 vh[8], vl[8];
+#pragma unroll
+        for (int k = 0; k < 8; k++) split_bf16(tile[wg * 8 + k][px], vh[k], vl[k]);
+        const int64_t o = int64_t(opix) * Cp + c_lo + wg * 8;
+        *reinterpret_cast<uint4*>(hi + o) = *reinterpret_cast<const uint4*>(vh);
+        *reinterpret_cast<uint4*>(lo + o) = *reinterpret_cast<const uint4*>(vl);
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // Cp <= 16: one thread per pixel reads its C values (pixel-contiguous across
 // the warp for NCHW) and writes Cp/8 16-byte chunks (contiguous across the warp).
 __global__ void __launch_bounds__(256) pack_act_small_kernel(View4 v, const float* __restrict__ x,
@@ -669,6 +729,22 @@ cudaError_t pack_act(const View4& v, const float* x, int Cp, __nv_bfloat16* hi, 
   if (Cp <= 16) {
     pack_act_small_kernel<<<grid_for(npix, 256, 8), 256, 0, st>>>(
         v, x, Cp, hi, lo, npix, make_magic(uint32_t(v.h * v.w)), make_magic(uint32_t(v.w)));
+    note_launch();
+    return cudaGetLastError();
+  }
+  const int pj = getenv("DNNP_PACK_PIX") ? atoi(getenv("DNNP_PACK_PIX")) : 64;
+  if (pj == 64 || pj == 128) {
+    const int64_t jobs = ceil_div(npix, int64_t(pj)) * ceil_div(Cp, kCh);
+    if (jobs >= (int64_t(1) << 31)) return cudaErrorInvalidValue;
+    const unsigned grid = unsigned(std::min<int64_t>(jobs, int64_t(kNumSMs) * 16));
+    if (pj == 64)
+      pack_act_wide_kernel<64><<<grid, 256, 0, st>>>(v, x, Cp, hi, lo, uint32_t(npix),
+                                                     make_magic(uint32_t(v.h * v.w)),
+                                                     make_magic(uint32_t(v.w)));
+    else
+      pack_act_wide_kernel<128><<<grid, 256, 0, st>>>(v, x, Cp, hi, lo, uint32_t(npix),
+                                                      make_magic(uint32_t(v.h * v.w)),
+                                                      make_magic(uint32_t(v.w)));
     note_launch();
     return cudaGetLastError();
   }
