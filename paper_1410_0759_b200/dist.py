@@ -46,6 +46,47 @@ def allreduce_filter_grad(df_local, group=None):
     return df_local
 
 
+class OverlappedAllreduce:
+    """dW allreduces off the compute stream (issue each layer's
+    allreduce as soon as its backward-filter finishes, overlapped with the
+    remaining backward work).  `submit(t)` records an event on the current
+    (compute) stream and enqueues the allreduce of `t` on a dedicated
+    communication stream behind it; `wait()` makes the compute stream wait
+    for every submitted reduction (call it before the gradients are read or
+    rewritten).  On CPU tensors (gloo) the reduction runs synchronously."""
+
+    def __init__(self, group=None):
+        import torch
+        self.group = group
+        self.cuda = torch.cuda.is_available() and torch.cuda.is_initialized()
+        self.stream = torch.cuda.Stream() if self.cuda else None
+        self.pending = 0
+
+    def submit(self, t):
+        import torch
+        import torch.distributed as dist
+        if not (dist.is_available() and dist.is_initialized()
+                and dist.get_world_size(self.group) > 1):
+            return t
+        if not (self.cuda and t.is_cuda):
+            dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
+            return t
+        ev = torch.cuda.Event()
+        ev.record()  # the producing kernels, on the compute stream
+        with torch.cuda.stream(self.stream):
+            self.stream.wait_event(ev)
+            dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
+            t.record_stream(self.stream)
+        self.pending += 1
+        return t
+
+    def wait(self):
+        import torch
+        if self.cuda and self.pending:
+            torch.cuda.current_stream().wait_stream(self.stream)
+        self.pending = 0
+
+
 def conv_backward_filter_dp(dy: TensorView, x: TensorView, conv: ConvDesc, engine,
                             df: FilterView, group=None) -> None:
     """Data-parallel backward-filter on this rank's shard (dy, x are the

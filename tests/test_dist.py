@@ -93,3 +93,70 @@ def test_dp_backward_filter_single_rank_gpu():
     dp.conv_backward_filter(dy, x, cd, "implicit", df1)
     dpd.conv_backward_filter_dp(dy, x, cd, "implicit", df2)
     assert torch.equal(df1.buf, df2.buf)
+
+
+def _overlap_worker(rank, world, port, results, use_cuda):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    if use_cuda:
+        torch.cuda.set_device(0)
+        torch.zeros(1, device="cuda")  # initialise the context before the helper
+    ov = dpd.OverlappedAllreduce()
+    rng = np.random.default_rng(21)
+    layers = []
+    for li in range(3):
+        N, C, H, K = 4, 3 + li, 9, 4 + 2 * li
+        x = rng.uniform(-0.5, 0.5, (N, C, H, H)).astype(np.float32)
+        dy = rng.uniform(-0.5, 0.5, (N, K, H, H)).astype(np.float32)
+        layers.append((x, dy, K, C))
+    outs = []
+    for x, dy, K, C in layers:
+        dev = "cuda" if use_cuda else None
+        xv = dpd.shard_view(dp.TensorView.from_array(x, device=dev), rank, world)
+        dyv = dpd.shard_view(dp.TensorView.from_array(dy, device=dev), rank, world)
+        if use_cuda:
+            df = dp.FilterView(dp.make_filter_desc(K, C, 3, 3), torch.zeros(K * C * 9, device="cuda"))
+            dp.conv_backward_filter(dyv, xv, dp.ConvDesc(1, 1, 1, 1), "implicit", df)
+            ov.submit(df.buf)
+            outs.append(df.buf)
+        else:
+            t = torch.from_numpy(np.full(K * C * 9, float(rank + 1), dtype=np.float32))
+            ov.submit(t)
+            outs.append(t)
+    ov.wait()
+    if use_cuda:
+        torch.cuda.synchronize()
+    results[rank] = [o.cpu().numpy().copy() for o in outs]
+    dist.destroy_process_group()
+
+
+def test_overlapped_allreduce_cpu():
+    mgr = mp.Manager()
+    results = mgr.dict()
+    mp.spawn(_overlap_worker, args=(2, _free_port(), results, False), nprocs=2, join=True)
+    for r in range(2):
+        for o in results[r]:
+            assert np.all(o == 3.0)
+
+
+@pytest.mark.gpu
+def test_overlapped_allreduce_two_ranks_one_gpu():
+    """Two gloo ranks sharing cuda:0: per-rank partial dW from the library,
+    allreduces on the communication stream, equal to the unsharded dW."""
+    mgr = mp.Manager()
+    results = mgr.dict()
+    mp.spawn(_overlap_worker, args=(2, _free_port(), results, True), nprocs=2, join=True)
+    rng = np.random.default_rng(21)
+    for li in range(3):
+        N, C, H, K = 4, 3 + li, 9, 4 + 2 * li
+        x = rng.uniform(-0.5, 0.5, (N, C, H, H)).astype(np.float32)
+        dy = rng.uniform(-0.5, 0.5, (N, K, H, H)).astype(np.float32)
+        full = np.zeros(K * C * 9)
+        orc.conv_backward_filter([N, C, H, H, C * H * H, H * H, H, 1], x.astype(np.float64).reshape(-1),
+                                 [N, K, H, H, K * H * H, H * H, H, 1],
+                                 dy.astype(np.float64).reshape(-1), [1, 1, 1, 1, 0, 0],
+                                 [K, C, 3, 3], full)
+        for r in range(2):
+            assert orc.rel_err(results[r][li], full) <= 1e-4
+        assert np.array_equal(results[0][li], results[1][li])
