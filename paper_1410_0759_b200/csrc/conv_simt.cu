@@ -51,6 +51,18 @@ template <>
 struct SimtCfg<double> {
   static constexpr int BM = 64, BN = 64, BK = 8, TM = 4, TN = 4;
 };
+// Narrow GEMM outputs (N <= 16 columns, e.g. table2 layer1 bwd-data: C = 3):
+// a 64-wide tile wastes >= 75% of its FMAs, so rows take the width.
+template <typename T>
+struct SimtNarrow;
+template <>
+struct SimtNarrow<float> {
+  static constexpr int BM = 128, BN = 16, BK = 16, TM = 8, TN = 2;
+};
+template <>
+struct SimtNarrow<double> {
+  static constexpr int BM = 128, BN = 16, BK = 16, TM = 4, TN = 2;
+};
 
 // A(m, k) element of the pass' left operand.
 template <typename T, int PASS>
@@ -166,12 +178,11 @@ __device__ __forceinline__ T load_b(const SimtArgs& a, int64_t col, int64_t k, i
   }
 }
 
-template <typename T, int PASS>
-__global__ void __launch_bounds__((SimtCfg<T>::BM / SimtCfg<T>::TM) *
-                                  (SimtCfg<T>::BN / SimtCfg<T>::TN))
+template <typename T, int PASS, class CFG>
+__global__ void __launch_bounds__((CFG::BM / CFG::TM) * (CFG::BN / CFG::TN))
     conv_simt_kernel(SimtArgs a) {
-  constexpr int BM = SimtCfg<T>::BM, BN = SimtCfg<T>::BN, BK = SimtCfg<T>::BK;
-  constexpr int TM = SimtCfg<T>::TM, TN = SimtCfg<T>::TN;
+  constexpr int BM = CFG::BM, BN = CFG::BN, BK = CFG::BK;
+  constexpr int TM = CFG::TM, TN = CFG::TN;
   constexpr int NT = (BM / TM) * (BN / TN);
   constexpr int LA = BM * BK / NT, LB = BN * BK / NT;
   static_assert(NT % BM == 0 || PASS == WGRAD, "row-fast A mapping");
@@ -340,10 +351,10 @@ static void fill_divs(SimtArgs& a) {
   a.dSph = make_magic(uint32_t(a.nSp > 0 ? a.nSp : 1));
 }
 
-template <typename T, int PASS>
-static cudaError_t launch_simt(SimtArgs& a, cudaStream_t st) {
-  constexpr int BM = SimtCfg<T>::BM, BN = SimtCfg<T>::BN, BK = SimtCfg<T>::BK;
-  constexpr int NT = (BM / SimtCfg<T>::TM) * (BN / SimtCfg<T>::TN);
+template <typename T, int PASS, class CFG = SimtCfg<T>>
+static cudaError_t launch_simt_cfg(SimtArgs& a, cudaStream_t st) {
+  constexpr int BM = CFG::BM, BN = CFG::BN, BK = CFG::BK;
+  constexpr int NT = (BM / CFG::TM) * (BN / CFG::TN);
   fill_divs(a);
   const int64_t gm = ceil_div(a.M, BM), gn = ceil_div(a.Ncol, BN);
   a.splits = 1;
@@ -371,7 +382,7 @@ static cudaError_t launch_simt(SimtArgs& a, cudaStream_t st) {
   dim3 grid(unsigned(gm), unsigned(gn),
             unsigned(PASS == DGRAD ? a.p.u * a.p.v : a.splits));
   if (gn > 65535) return cudaErrorInvalidConfiguration;
-  conv_simt_kernel<T, PASS><<<grid, NT, 0, st>>>(a);
+  conv_simt_kernel<T, PASS, CFG><<<grid, NT, 0, st>>>(a);
   note_launch();
   cudaError_t e = cudaGetLastError();
   if (ws) {
@@ -383,6 +394,13 @@ static cudaError_t launch_simt(SimtArgs& a, cudaStream_t st) {
     if (e == cudaSuccess) e = cudaGetLastError();
   }
   return e;
+}
+
+template <typename T, int PASS>
+static cudaError_t launch_simt(SimtArgs& a, cudaStream_t st) {
+  if (PASS != WGRAD && a.Ncol <= 16 && a.M >= 4096 && !getenv("DNNP_SIMT_NO_NARROW"))
+    return launch_simt_cfg<T, PASS, SimtNarrow<T>>(a, st);
+  return launch_simt_cfg<T, PASS, SimtCfg<T>>(a, st);
 }
 
 template <typename T>

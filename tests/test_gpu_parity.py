@@ -215,6 +215,8 @@ RANDOM_SHAPES = [
     (2, 8, 12, 10, 8, 3, 3, 2, 2, 1, 1),
     (1, 64, 8, 8, 72, 3, 3, 1, 1, 1, 1),      # channel counts past one k-block
     (4, 32, 7, 7, 130, 1, 1, 1, 1, 0, 0),     # 1x1, ragged K
+    (4, 3, 40, 40, 8, 5, 5, 1, 1, 2, 2),      # thin GEMMs (narrow SIMT tiles: fwd N=8, dgrad N=3)
+    (4, 2, 80, 72, 12, 3, 3, 2, 2, 1, 1),     # thin + strided bwd-data phases
 ]
 
 
