@@ -150,9 +150,13 @@ def kernel_launch_count():
     return int(lib().dnnp_kernel_launch_count())
 
 
-def kernel_timing(enable=True):
-    """Start (clearing) or stop CUDA-event timing of the main GEMM kernels."""
-    lib().dnnp_kernel_timing(1 if enable else 0)
+def kernel_timing(enable=True, only=None):
+    """Start (clearing) or stop CUDA-event timing of the main GEMM kernels;
+    only=i times just the i-th main launch after this call."""
+    if not enable:
+        lib().dnnp_kernel_timing(0)
+    else:
+        lib().dnnp_kernel_timing(1 if only is None else 2 + int(only))
 
 
 def scratch_high_water(reset=False):

@@ -577,20 +577,50 @@ static std::mutex g_kt_mu;
 static std::vector<KTime> g_kt;
 static std::atomic<int> g_kt_on{0};
 
+// Events come from a pool (created once, reused after every reset); inside
+// a CUDA-graph capture they are recorded as external event nodes, so a
+// replayed graph timestamps its kernels like an eager run.
+static std::vector<cudaEvent_t> g_kt_pool;
+static size_t g_kt_next = 0;
+
+static cudaEvent_t kt_event() {
+  if (g_kt_next == g_kt_pool.size()) {
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    g_kt_pool.push_back(e);
+  }
+  return g_kt_pool[g_kt_next++];
+}
+
+static void kt_record(cudaEvent_t e, cudaStream_t st) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(st, &cs);
+  if (cs == cudaStreamCaptureStatusActive)
+    cudaEventRecordWithFlags(e, st, cudaEventRecordExternal);
+  else
+    cudaEventRecord(e, st);
+}
+
+static int g_kt_sel = -1;     // time only the launch with this ordinal (-1: all)
+static int g_kt_count = 0;    // main-kernel launches since the last reset
+static bool g_kt_open = false;
+
 void ktime_begin(cudaStream_t st, int tag) {
   if (!g_kt_on.load()) return;
-  KTime k{tag, nullptr, nullptr};
-  cudaEventCreate(&k.a);
-  cudaEventCreate(&k.b);
-  cudaEventRecord(k.a, st);
   std::lock_guard<std::mutex> g(g_kt_mu);
+  const int ord = g_kt_count++;
+  g_kt_open = g_kt_sel < 0 || ord == g_kt_sel;
+  if (!g_kt_open) return;
+  KTime k{tag, kt_event(), kt_event()};
+  kt_record(k.a, st);
   g_kt.push_back(k);
 }
 
 void ktime_end(cudaStream_t st) {
   if (!g_kt_on.load()) return;
   std::lock_guard<std::mutex> g(g_kt_mu);
-  if (!g_kt.empty()) cudaEventRecord(g_kt.back().b, st);
+  if (g_kt_open && !g_kt.empty()) kt_record(g_kt.back().b, st);
+  g_kt_open = false;
 }
 
 struct ScratchScope {
@@ -790,11 +820,14 @@ extern "C" int64_t dnnp_scratch_high_water(int reset) {
 extern "C" int dnnp_kernel_timing(int enable) {
   using namespace dnnp::tc;
   std::lock_guard<std::mutex> g(g_kt_mu);
-  for (auto& k : g_kt) {
-    cudaEventDestroy(k.a);
-    cudaEventDestroy(k.b);
-  }
-  g_kt.clear();
+  g_kt.clear();  // the events return to the pool
+  g_kt_next = 0;
+  g_kt_count = 0;
+  g_kt_open = false;
+  // enable: 1 = every main GEMM launch; k >= 2 = only the launch with
+  // ordinal k - 2 (0-based, since this reset) -- two event nodes instead of
+  // two per kernel when a replayed graph times its dominant kernel
+  g_kt_sel = enable >= 2 ? enable - 2 : -1;
   g_kt_on.store(enable ? 1 : 0);
   return 0;
 }
