@@ -11,6 +11,8 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
+#include <map>
 #include <mutex>
 #include <new>
 #include <type_traits>
@@ -307,6 +309,14 @@ class Stager {
     *dev = b.dev;
     return DNNP_STATUS_OK;
   }
+  // A device staging buffer from this call's scratch scope (no copy).
+  dnnp_status scratch(size_t bytes, void** dev) {
+    if (!scratch_) scratch_ = dnnp::tc::scratch_open(st_);
+    cudaError_t e = dnnp::tc::scratch_alloc(scratch_, std::max<size_t>(bytes, 16), dev);
+    if (e != cudaSuccess) return cuda_status(e, "staging allocation");
+    any_host_ = true;
+    return DNNP_STATUS_OK;
+  }
   // Copy staged outputs back and wait when any host buffer took part.
   dnnp_status finish(cudaError_t launch) {
     if (launch != cudaSuccess) {
@@ -337,6 +347,124 @@ class Stager {
 size_t span_bytes(dnnp_tensor_desc d) { return size_t(max_offset(d) + 1) * elem_size(d->elem); }
 // A view with no gaps inside its span: writing the span writes only the view.
 bool dense_view(dnnp_tensor_desc d) { return max_offset(d) + 1 == d->n * d->c * d->h * d->w; }
+
+// ------------------------------------------- pipelined host staging
+// Batch-separable convolutions with HOST buffers: the N images go through in
+// chunks; chunk i's inputs copy host->device on a copy-in stream while chunk
+// i-1 computes on the handle's stream and chunk i-2's outputs copy back on a
+// copy-out stream, so both PCIe directions and the GPU work overlap (the
+// call stays synchronous, as the reference's).  A buffer qualifies when the
+// image stride covers its per-image footprint (chunk byte ranges disjoint).
+struct ChunkBuf {
+  const void* user;
+  dnnp_tensor_desc d;
+  bool out, copy_in;
+  void* dev = nullptr;
+};
+
+static void copy_streams(cudaStream_t* in, cudaStream_t* out) {
+  static std::mutex mu;
+  static std::map<int, std::pair<cudaStream_t, cudaStream_t>> m;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> g(mu);
+  auto& c = m[dev];
+  if (!c.first) {
+    cudaStreamCreateWithFlags(&c.first, cudaStreamNonBlocking);
+    cudaStreamCreateWithFlags(&c.second, cudaStreamNonBlocking);
+  }
+  *in = c.first;
+  *out = c.second;
+}
+
+static int64_t image_bytes(dnnp_tensor_desc d) {  // footprint of one image
+  return (max_offset(d) - (d->n - 1) * d->sn + 1) * int64_t(elem_size(d->elem));
+}
+
+static bool pipeline_ok(const std::vector<ChunkBuf>& bufs, int64_t N) {
+  static const bool off = getenv("DNNP_NO_PIPELINE") != nullptr;
+  if (off || N < 2) return false;
+  size_t total = 0;
+  for (const auto& b : bufs) {
+    const dnnp_tensor_desc d = b.d;
+    if (d->n != N || is_device_ptr(b.user) || d->sn < 0 || d->sc < 0 || d->sh < 0 || d->sw < 0)
+      return false;
+    if (d->sn * int64_t(elem_size(d->elem)) < image_bytes(d)) return false;
+    total += span_bytes(d);
+  }
+  return total >= (size_t(16) << 20);
+}
+
+// compute(n0, nb, devs): launch the work of images [n0, n0 + nb) on st.
+template <class F>
+static dnnp_status run_pipelined(cudaStream_t st, Stager& sg, std::vector<ChunkBuf>& bufs,
+                                 int64_t N, F&& compute) {
+  dnnp_status rs;
+  size_t total = 0;
+  for (auto& b : bufs) {
+    if ((rs = sg.scratch(span_bytes(b.d), &b.dev))) return rs;
+    total += span_bytes(b.d);
+  }
+  static const int64_t shift = getenv("DNNP_PIPE_SHIFT") ? atoll(getenv("DNNP_PIPE_SHIFT")) : 24;
+  const int64_t chunks = std::max<int64_t>(2, std::min<int64_t>({16, N, int64_t(total >> shift)}));
+  const int64_t nb = (N + chunks - 1) / chunks;
+  cudaStream_t ci, co;
+  copy_streams(&ci, &co);
+  std::vector<cudaEvent_t> evs;
+  auto mk = [&]() {
+    cudaEvent_t e = nullptr;
+    cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    evs.push_back(e);
+    return e;
+  };
+  cudaError_t e = cudaSuccess;
+  // the staging memory may still be read by earlier work on st
+  cudaEvent_t e0 = mk();
+  cudaEventRecord(e0, st);
+  cudaStreamWaitEvent(ci, e0, 0);
+  cudaStreamWaitEvent(co, e0, 0);
+  for (int64_t n0 = 0; n0 < N && e == cudaSuccess; n0 += nb) {
+    const int64_t cnt = std::min(nb, N - n0);
+    auto range = [&](const ChunkBuf& b, size_t* off, size_t* len) {
+      const int64_t es = int64_t(elem_size(b.d->elem));
+      *off = size_t(n0 * b.d->sn * es);
+      *len = size_t((cnt - 1) * b.d->sn * es + image_bytes(b.d));
+    };
+    for (const auto& b : bufs) {
+      if (b.out && !b.copy_in) continue;
+      size_t off, len;
+      range(b, &off, &len);
+      e = cudaMemcpyAsync(static_cast<char*>(b.dev) + off, static_cast<const char*>(b.user) + off,
+                          len, cudaMemcpyHostToDevice, ci);
+      if (e != cudaSuccess) break;
+    }
+    cudaEvent_t ein = mk();
+    cudaEventRecord(ein, ci);
+    cudaStreamWaitEvent(st, ein, 0);
+    if (e == cudaSuccess) e = compute(n0, cnt);
+    cudaEvent_t edone = mk();
+    cudaEventRecord(edone, st);
+    cudaStreamWaitEvent(co, edone, 0);
+    for (const auto& b : bufs) {
+      if (!b.out || e != cudaSuccess) continue;
+      size_t off, len;
+      range(b, &off, &len);
+      e = cudaMemcpyAsync(static_cast<char*>(const_cast<void*>(b.user)) + off,
+                          static_cast<char*>(b.dev) + off, len, cudaMemcpyDeviceToHost, co);
+    }
+  }
+  cudaEvent_t eend = mk();
+  cudaEventRecord(eend, co);
+  cudaStreamWaitEvent(st, eend, 0);
+  rs = sg.finish(e);  // remaining (non-batched) outputs, then synchronise st
+  for (cudaEvent_t ev : evs) cudaEventDestroy(ev);
+  return rs;
+}
+
+static View4 shift_images(View4 v, int64_t nb) {
+  v.n = nb;
+  return v;
+}
 
 double read_scalar(const void* p, dnnp_elem_type t) {
   return t == DNNP_F64 ? *static_cast<const double*>(p)
@@ -695,6 +823,23 @@ dnnp_status dnnp_convolution_forward(dnnp_handle handle, const void* alpha, dnnp
   Stager sg(handle->stream);
   void *dx, *df, *dy;
   size_t fbytes = size_t(fd->k * fd->c * fd->r * fd->s) * elem_size(fd->elem);
+  {
+    std::vector<ChunkBuf> cb = {{x, xd, false, true}, {y, yd, true, b != 0.0 || !dense_view(yd)}};
+    if (pr.engine != DNNP_ENGINE_EXPLICIT && pipeline_ok(cb, xd->n)) {
+      if ((st = sg.add(f, fbytes, false, true, &df))) return st;
+      const size_t es = elem_size(xd->elem);
+      return run_pipelined(handle->stream, sg, cb, xd->n, [&](int64_t n0, int64_t nb) {
+        dnnp::ConvProblem q = pr;
+        q.N = nb;
+        q.x = shift_images(pr.x, nb);
+        q.y = shift_images(pr.y, nb);
+        return dnnp::conv_forward(q, dnnp::Dtype(xd->elem),
+                                  static_cast<char*>(cb[0].dev) + n0 * xd->sn * es, df,
+                                  static_cast<char*>(cb[1].dev) + n0 * yd->sn * es, a, b,
+                                  handle->math, handle->stream);
+      });
+    }
+  }
   if ((st = sg.add(x, span_bytes(xd), false, true, &dx))) return st;
   if ((st = sg.add(f, fbytes, false, true, &df))) return st;
   if ((st = sg.add(y, span_bytes(yd), true, b != 0.0 || !dense_view(yd), &dy))) return st;
@@ -725,6 +870,23 @@ dnnp_status dnnp_convolution_backward_data(dnnp_handle handle, dnnp_filter_desc 
   void *ddy, *dff, *ddx;
   size_t fbytes = size_t(fd->k * fd->c * fd->r * fd->s) * elem_size(fd->elem);
   if ((st = sg.add(f, fbytes, false, true, &dff))) return st;
+  {
+    std::vector<ChunkBuf> cb = {{dy, dyd, false, true},
+                                {dx, dxd, true, cd->accumulate || !dense_view(dxd)}};
+    if (pipeline_ok(cb, dxd->n)) {
+      const size_t es = elem_size(dxd->elem);
+      return run_pipelined(handle->stream, sg, cb, dxd->n, [&](int64_t n0, int64_t nb) {
+        dnnp::ConvProblem q = pr;
+        q.N = nb;
+        q.x = shift_images(pr.x, nb);
+        q.y = shift_images(pr.y, nb);
+        return dnnp::conv_backward_data(q, dnnp::Dtype(dxd->elem),
+                                        static_cast<char*>(cb[0].dev) + n0 * dyd->sn * es, dff,
+                                        static_cast<char*>(cb[1].dev) + n0 * dxd->sn * es,
+                                        cd->accumulate != 0, handle->math, handle->stream);
+      });
+    }
+  }
   if ((st = sg.add(dy, span_bytes(dyd), false, true, &ddy))) return st;
   if ((st = sg.add(dx, span_bytes(dxd), true, cd->accumulate || !dense_view(dxd), &ddx)))
     return st;
@@ -754,6 +916,25 @@ dnnp_status dnnp_convolution_backward_filter(dnnp_handle handle, dnnp_tensor_des
   Stager sg(handle->stream);
   void *dxx, *ddy, *ddf;
   size_t fbytes = size_t(fd->k * fd->c * fd->r * fd->s) * elem_size(fd->elem);
+  {
+    std::vector<ChunkBuf> cb = {{x, xd, false, true}, {dy, dyd, false, true}};
+    if (pipeline_ok(cb, xd->n)) {
+      if ((st = sg.add(df, fbytes, true, cd->accumulate != 0, &ddf))) return st;
+      const size_t es = elem_size(xd->elem);
+      // later chunks add to the first chunks' partial dW (IEEE fp32 / fp64)
+      return run_pipelined(handle->stream, sg, cb, xd->n, [&](int64_t n0, int64_t nb) {
+        dnnp::ConvProblem q = pr;
+        q.N = nb;
+        q.x = shift_images(pr.x, nb);
+        q.y = shift_images(pr.y, nb);
+        return dnnp::conv_backward_filter(q, dnnp::Dtype(xd->elem),
+                                          static_cast<char*>(cb[1].dev) + n0 * dyd->sn * es,
+                                          static_cast<char*>(cb[0].dev) + n0 * xd->sn * es, ddf,
+                                          cd->accumulate != 0 || n0 > 0, handle->math,
+                                          handle->stream);
+      });
+    }
+  }
   if ((st = sg.add(x, span_bytes(xd), false, true, &dxx))) return st;
   if ((st = sg.add(dy, span_bytes(dyd), false, true, &ddy))) return st;
   if ((st = sg.add(df, fbytes, true, cd->accumulate != 0, &ddf))) return st;

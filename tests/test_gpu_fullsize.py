@@ -99,3 +99,40 @@ def test_table2_layer_vs_fp64(layer):
     errs = {pas: rel(a.double(), b) for pas, a, b in zip(("fwd", "bwd_data", "bwd_filter"),
                                                         out["f32"], out["f64"])}
     assert all(e <= 1e-4 for e in errs.values()), (name, errs)
+
+
+@pytest.mark.parametrize("n,acc,beta", [(32, False, 0.0), (7, True, 0.0), (9, False, 0.5)])
+def test_host_buffers_pipelined(n, acc, beta):
+    """Host (numpy) buffers large enough for the chunked copy-in / compute /
+    copy-out pipeline give the device-buffer results (within fp32 tolerance:
+    chunks change only the work split) for every pass, with accumulate and
+    beta semantics preserved."""
+    import torch
+    c, h, k, r, u, pad = 64, 27, 192, 5, 1, 2
+    if n < 16:
+        c, h, k = 96, 40, 256  # keep the staged bytes above the pipeline threshold
+    p = dp.output_extent(h, r, u, pad)
+    rng = np.random.default_rng(n)
+    x = rng.uniform(-0.5, 0.5, n * c * h * h).astype(np.float32)
+    f = rng.uniform(-0.5, 0.5, k * c * r * r).astype(np.float32)
+    dy = rng.uniform(-0.5, 0.5, n * k * p * p).astype(np.float32)
+    y0 = rng.uniform(-0.5, 0.5, n * k * p * p).astype(np.float32)
+    dx0 = rng.uniform(-0.5, 0.5, n * c * h * h).astype(np.float32)
+    df0 = rng.uniform(-0.5, 0.5, k * c * r * r).astype(np.float32)
+    cd = dp.ConvDesc(u, u, pad, pad, "convolution", acc)
+    mk = lambda nn, cc, hh, buf: dp.TensorView(dp.make_desc(nn, cc, hh, hh), buf)
+    res = {}
+    for where in ("host", "device"):
+        conv = (lambda a: a.copy()) if where == "host" else (lambda a: torch.from_numpy(a.copy()).cuda())
+        xv, dyv = mk(n, c, h, conv(x)), mk(n, k, p, conv(dy))
+        fv = dp.FilterView(dp.make_filter_desc(k, c, r, r), conv(f))
+        yv, dxv = mk(n, k, p, conv(y0)), mk(n, c, h, conv(dx0))
+        dfv = dp.FilterView(dp.make_filter_desc(k, c, r, r), conv(df0))
+        dp.conv_forward(xv, fv, cd, "implicit", yv, beta=beta)
+        dp.conv_backward_data(dyv, fv, cd, "implicit", dxv)
+        dp.conv_backward_filter(dyv, xv, cd, "implicit", dfv)
+        torch.cuda.synchronize()
+        get = (lambda t: t) if where == "host" else (lambda t: t.cpu().numpy())
+        res[where] = [get(v.buf).astype(np.float64) for v in (yv, dxv, dfv)]
+    for a, b in zip(res["host"], res["device"]):
+        assert np.abs(a - b).max() / np.abs(b).max() <= 1e-5
