@@ -844,6 +844,125 @@ __device__ __forceinline__ void window_max(const T* xs, int W, int base, T& best
     }
 }
 
+// Pipelined plane forward (dense NCHW planes): a persistent block streams
+// its planes through two shared-memory buffers with cp.async, the next
+// plane's bytes in flight while the current one is reduced (the one-plane-
+// per-block kernel waited a full memory latency per plane).  Element i of
+// a plane sits at buf + mis + i, mis = the plane's 16-byte misalignment in
+// elements, so the body moves as aligned 16-byte copies.
+__device__ __forceinline__ void cpa4(void* dst, const void* src) {
+  const uint32_t d = uint32_t(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cpa8(void* dst, const void* src) {
+  const uint32_t d = uint32_t(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cpa16(void* dst, const void* src) {
+  const uint32_t d = uint32_t(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+template <typename T>
+__device__ __forceinline__ int plane_async(T* buf, const T* __restrict__ xb, int n) {
+  constexpr int V = 16 / sizeof(T);
+  const int mis = int((reinterpret_cast<uintptr_t>(xb) / sizeof(T)) % V);
+  const int head = min(n, (V - mis) % V);
+  const int nv = (n - head) / V;
+  T* xs = buf + mis;
+  if (int(threadIdx.x) < head) {
+    if (sizeof(T) == 4) cpa4(xs + threadIdx.x, xb + threadIdx.x);
+    else cpa8(xs + threadIdx.x, xb + threadIdx.x);
+  }
+  for (int j = threadIdx.x; j < nv; j += blockDim.x) cpa16(xs + head + j * V, xb + head + j * V);
+  for (int i = head + nv * V + threadIdx.x; i < n; i += blockDim.x) {
+    if (sizeof(T) == 4) cpa4(xs + i, xb + i);
+    else cpa8(xs + i, xb + i);
+  }
+  return mis;
+}
+
+template <typename T, int KW>
+__global__ void __launch_bounds__(256) pool_fwd_pipe_kernel(PoolGeom g, const T* __restrict__ x,
+                                                            T* __restrict__ y, int64_t* argmax,
+                                                            int kind, int pitch) {
+  extern __shared__ __align__(16) uint8_t psm[];
+  T* bufs = reinterpret_cast<T*>(psm);  // [2][pitch], pitch >= H*W + 16 / sizeof(T)
+  const int H = int(g.H), W = int(g.W), P = int(g.P), Q = int(g.Q), C = int(g.C);
+  const int wh = int(g.wh), ww = int(g.ww);
+  const int planes = int(g.N) * C, HW = H * W;
+  auto base_of = [&](int pl) {
+    uint32_t nu, cu;
+    mdivmod(uint32_t(pl), g.dC, nu, cu);
+    return x + int64_t(nu) * g.x.sn + int64_t(cu) * g.x.sc;
+  };
+  int pl = blockIdx.x, it = 0;
+  int mis_cur = 0, mis_next = 0;
+  if (pl < planes) mis_cur = plane_async(bufs, base_of(pl), HW);
+  cpa_commit();
+  for (; pl < planes; pl += gridDim.x, it++) {
+    const int nxt = pl + gridDim.x;
+    if (nxt < planes) mis_next = plane_async(bufs + ((it + 1) & 1) * pitch, base_of(nxt), HW);
+    cpa_commit();
+    cpa_wait<1>();
+    __syncthreads();
+    const T* xs = bufs + (it & 1) * pitch + mis_cur;
+    uint32_t nu, cu;
+    mdivmod(uint32_t(pl), g.dC, nu, cu);
+    T* yb = y + int64_t(nu) * g.y.sn + int64_t(cu) * g.y.sc;
+    for (int o = threadIdx.x; o < P * Q; o += blockDim.x) {
+      uint32_t pu, qu;
+      mdivmod(uint32_t(o), g.dQ, pu, qu);
+      const int p = int(pu), q = int(qu);
+      const int hs0 = p * int(g.sh) - int(g.ph), ws0 = q * int(g.sw) - int(g.pw);
+      T out;
+      if (KW > 0 && hs0 >= 0 && ws0 >= 0 && hs0 + KW <= H && ws0 + KW <= W) {
+        const int b0 = hs0 * W + ws0;
+        if (kind == 0) {
+          int bi;
+          window_max<T, KW>(xs, W, b0, out, bi);
+          if (argmax) argmax[int64_t(pl) * P * Q + o] = int64_t(pl) * HW + bi;
+        } else {
+          T sacc = T(0);
+#pragma unroll
+          for (int a = 0; a < KW; a++)
+#pragma unroll
+            for (int b = 0; b < KW; b++) sacc = dadd<T>(sacc, xs[b0 + a * W + b]);
+          out = sacc / T(KW * KW);
+        }
+      } else {
+        const int hs = max(0, hs0), he = min(H, hs0 + wh);
+        const int ws = max(0, ws0), we = min(W, ws0 + ww);
+        if (kind == 0) {
+          T best = xs[hs * W + ws];
+          int bi = hs * W + ws;
+          for (int h = hs; h < he; h++)
+            for (int w = ws; w < we; w++) {
+              const T v = xs[h * W + w];
+              const bool take = v > best || (v != v && best == best);
+              best = take ? v : best;
+              bi = take ? h * W + w : bi;
+            }
+          out = best;
+          if (argmax) argmax[int64_t(pl) * P * Q + o] = int64_t(pl) * HW + bi;
+        } else {
+          T sacc = T(0);
+          for (int h = hs; h < he; h++)
+            for (int w = ws; w < we; w++) sacc = dadd<T>(sacc, xs[h * W + w]);
+          out = sacc / T((he - hs) * (we - ws));
+        }
+      }
+      yb[p * g.y.sh + q * g.y.sw] = out;
+    }
+    mis_cur = mis_next;
+    __syncthreads();  // the buffer is refilled two planes later
+  }
+  cpa_wait<0>();
+}
+
 template <typename T, int KW>
 __global__ void __launch_bounds__(256) pool_fwd_plane_kernel(PoolGeom g, const T* __restrict__ x,
                                                              T* __restrict__ y, int64_t* argmax,
@@ -1100,6 +1219,31 @@ cudaError_t pool_forward(const PoolProblem& pp, Dtype dt, const View4& xv, const
   PoolGeom g = pool_geom(pp, xv, yv);
   const size_t eb = dt == F32 ? 4 : 8;
   const size_t psm = size_t(xv.h) * xv.w * eb;
+  const bool dense_planes = xv.sw == 1 && xv.sh == xv.w;
+  const int pitch = int(((xv.h * xv.w + 16 / eb) * eb + 15) / 16 * 16 / eb);
+  const size_t ppipe = size_t(2) * pitch * eb;
+  if (dense_planes && ppipe <= 96 * 1024 && xv.n * xv.c < (int64_t(1) << 31) &&
+      !getenv("DNNP_POOL_NO_PIPE") && !getenv("DNNP_POOL_DIRECT")) {
+    const int kw = (pp.wh == pp.ww && (pp.wh == 2 || pp.wh == 3)) ? int(pp.wh) : 0;
+    const int per_sm = std::max(1, int(std::min<size_t>(4, (200 * 1024) / ppipe)));
+    const unsigned pg = unsigned(std::min<int64_t>(xv.n * xv.c, int64_t(kNumSMs) * per_sm));
+    auto go = [&](auto tag, auto kwc) {
+      using TT = decltype(tag);
+      auto kfn = pool_fwd_pipe_kernel<TT, decltype(kwc)::value>;
+      cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ppipe));
+      kfn<<<pg, 256, ppipe, st>>>(g, (const TT*)x, (TT*)y, argmax, pp.kind, pitch);
+    };
+    using K0 = std::integral_constant<int, 0>;
+    using K2 = std::integral_constant<int, 2>;
+    using K3 = std::integral_constant<int, 3>;
+    if (dt == F32) {
+      if (kw == 3) go(float(), K3()); else if (kw == 2) go(float(), K2()); else go(float(), K0());
+    } else {
+      if (kw == 3) go(double(), K3()); else if (kw == 2) go(double(), K2()); else go(double(), K0());
+    }
+    note_launch();
+    return cudaGetLastError();
+  }
   if (psm <= 48 * 1024 && xv.n * xv.c < (int64_t(1) << 31) && !getenv("DNNP_POOL_DIRECT")) {
     const int thr = pool_threads();
     const unsigned pg = unsigned(std::min<int64_t>(xv.n * xv.c, pool_grid_cap()));

@@ -21,11 +21,11 @@ def main():
     N, C, H = 128, 64, 55
     x, _ = make_view(N, C, H, H, lay, "f32")
     dx, _ = make_view(N, C, H, H, lay, "f32")
-    pd = dp.PoolingDesc("max", 3, 3, 2, 2, 0, 0)
+    pd = dp.PoolingDesc(os.environ.get("POOL_KIND", "max"), 3, 3, 2, 2, 0, 0)
     _, _, P, Q = dp.pool_out_shape(pd, x)
     y, _ = make_view(N, C, P, Q, lay, "f32")
     dy, _ = make_view(N, C, P, Q, lay, "f32")
-    am = torch.empty((N, C, P, Q), dtype=torch.int64, device="cuda")
+    am = torch.empty((N, C, P, Q), dtype=torch.int64, device="cuda") if pd.kind.value == "max" else None
     for _ in range(2):
         dp.pool_forward(pd, x, y, am)
         dp.pool_backward(pd, y, dy, x, dx, am)
