@@ -390,6 +390,9 @@ struct PackGeom {
   // output columns, GEMM column = e * Ncol0 + n; the blocked taps along w
   // (tapW) map to the unblocked tap dw = dwb - e * vstep (valid in [0, Sg)).
   int tapH, tapW, bw, Ncol0, vstep, Sg;
+  // bdir = 1: the block runs down the output rows instead (forward only):
+  // blocked tap row dhb maps to dh = dhb - e * ustep (valid in [0, Rg))
+  int bdir, ustep, Rg;
 };
 
 __device__ __forceinline__ float fetch_filter(const PackGeom& g, const float* __restrict__ f,
@@ -489,10 +492,11 @@ __global__ void __launch_bounds__(128) pack_filter_tap_kernel(PackGeom g, const 
     }
     return;
   }
-  const int dh = tap / g.tapW, dwb = tap - (tap / g.tapW) * g.tapW;
+  const int dhb = tap / g.tapW, dwb = tap - (tap / g.tapW) * g.tapW;
   const int e = row / g.Ncol0, r0 = row - e * g.Ncol0;  // column block, unblocked column
-  const int dw = dwb - e * g.vstep;
-  const bool tap_ok = row < g.Ncol && dw >= 0 && dw < g.Sg;
+  const int dw = g.bdir ? dwb : dwb - e * g.vstep;
+  const int dh = g.bdir ? dhb - e * g.ustep : dhb;
+  const bool tap_ok = row < g.Ncol && dw >= 0 && dw < g.Sg && dh >= 0 && dh < g.Rg;
   int c_col = 0, rp = -1, sp = -1, ph = 0, pw = 0;
   if (g.dgrad && row < g.Ncol) {
     const int phase = r0 / g.C;
@@ -505,10 +509,12 @@ __global__ void __launch_bounds__(128) pack_filter_tap_kernel(PackGeom g, const 
   if (tap == 0 && threadIdx.x == 0 && row < g.Ncol && (g.dgrad || g.bw > 1)) {
     uint32_t eh, ew, ec;
     if (!g.dgrad) {
-      eh = 0, ew = uint32_t(e), ec = uint32_t(r0);
+      eh = g.bdir ? uint32_t(e) : 0u, ew = g.bdir ? 0u : uint32_t(e), ec = uint32_t(r0);
     } else if (g.su * g.sv > 1) {  // space-to-depth column (rh, rw, c)
       const int q = r0 / g.C0;
       eh = uint32_t(q / g.sv), ew = uint32_t(e * g.sv + q % g.sv), ec = uint32_t(r0 - q * g.C0);
+    } else if (g.bdir) {
+      eh = uint32_t(e * g.u + ph), ew = uint32_t(pw), ec = uint32_t(c_col);
     } else {
       eh = uint32_t(ph), ew = uint32_t(e * g.v + pw), ec = uint32_t(c_col);
     }
@@ -516,7 +522,7 @@ __global__ void __launch_bounds__(128) pack_filter_tap_kernel(PackGeom g, const 
   }
   if (row == 0)
     for (int grp = threadIdx.x; grp < g.Cgrp; grp += blockDim.x)
-      ctab[tap * g.Cgrp + grp] = (uint32_t(dh) << 24) | (uint32_t(dwb) << 16) | uint32_t(grp * 8);
+      ctab[tap * g.Cgrp + grp] = (uint32_t(dhb) << 24) | (uint32_t(dwb) << 16) | uint32_t(grp * 8);
   for (int cin = threadIdx.x; cin < Cpf; cin += blockDim.x) {
     float val = 0.0f;
     if (!g.dgrad) {
@@ -1212,6 +1218,9 @@ cudaError_t run_tc(bool dgrad, const ConvProblem& p, const float* in, const View
   pg.tapH = dgrad ? pg.winH : pg.R;
   pg.tapW = dgrad ? pg.winW : pg.S;
   pg.Sg = pg.tapW;
+  pg.Rg = pg.tapH;
+  pg.bdir = 0;
+  pg.ustep = dgrad ? 1 : g.u;
   pg.bw = 1;
   pg.Ncol0 = pg.Ncol;
   pg.vstep = dgrad ? 1 : g.v;
@@ -1220,8 +1229,12 @@ cudaError_t run_tc(bool dgrad, const ConvProblem& p, const float* in, const View
   // the TMA traffic) shrinks to (S + v) / (2 S) of its bytes.
   // (measured: helps the unit-stride bwd-data of conv2, 233 -> 204 us; not the
   // space-to-depth conv1 passes, whose epilogue then dominates)
+  // unit-stride bwd-data: rows of 2 outputs (coalesced epilogue; conv2
+  // 144 -> 142 us), except very narrow outputs, which block up to 8 columns
+  const bool dgrad_rows = dgrad && !s2d && g.out_mode == 0 && pg.Ncol > 16 &&
+                          !env_off("DNNP_TC_DGRAD_COLS");
   const bool blockable =
-      g.tma && !fold && pg.Ncol <= 64 && !env_off("DNNP_TC_NO_BLOCK") &&
+      g.tma && !fold && !dgrad_rows && pg.Ncol <= 64 && !env_off("DNNP_TC_NO_BLOCK") &&
       (env_off("DNNP_TC_BLOCK_S2D") ? (!dgrad ? g.out_mode == 0 : (s2d || g.out_mode == 0))
                                     : (!s2d && g.out_mode == 0 && (env_off("DNNP_TC_BLOCK") || dgrad)));
   if (blockable) {
@@ -1267,6 +1280,29 @@ cudaError_t run_tc(bool dgrad, const ConvProblem& p, const float* in, const View
       gb.o_ph = gb.o_pw = 0;
     }
     if (tma_geometry_ok(gb, IH, IW, pb.tapH, pb.tapW, Nimg * gb.OH * gb.OW)) g = gb;
+  } else if ((!dgrad || dgrad_rows) && g.tma && !fold && g.out_mode == 0 && pg.Ncol <= 64 &&
+             !env_off("DNNP_TC_NO_VBLOCK")) {
+    // Row blocking for narrow forward GEMMs (conv1: K = 64): one GEMM row
+    // computes 2 vertically adjacent outputs, doubling N while the A bytes
+    // per output drop to (R + u) / 2R; unlike column blocking the epilogue
+    // stores stay contiguous (lanes = consecutive output columns).
+    int bh = 2;
+    if (const char* e = getenv("DNNP_TC_VBH")) bh = std::max(2, std::min(8, atoi(e)));
+    Gemm gb = g;
+    PackGeom& pb = gb.pg;
+    pb.bdir = 1;
+    pb.bw = bh;
+    pb.Ncol = bh * pg.Ncol;
+    pb.tapH = pg.tapH + (bh - 1) * pg.ustep;
+    gb.OH = int(ceil_div(g.OH, bh));
+    gb.u = g.u * bh;
+    gb.out_mode = 1;
+    gb.o_u = bh;
+    gb.o_v = 1;
+    gb.o_H = dgrad ? int(p.H) : g.OH;
+    gb.o_W = dgrad ? int(p.W) : g.OW;
+    gb.o_ph = gb.o_pw = 0;
+    if (gb.u <= 8 && tma_geometry_ok(gb, IH, IW, pb.tapH, pb.tapW, Nimg * gb.OH * gb.OW)) g = gb;
   }
   const size_t act = size_t(p.N) * IH * IW * Cp;
   Workspace ws(st);

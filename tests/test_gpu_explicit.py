@@ -48,10 +48,14 @@ def test_explicit_scratch_scales_with_filter_area():
 
 def test_implicit_scratch_independent_of_filter_area():
     sizes = {r: run("implicit", r, n=8, c=16, h=32)[1] for r in (1, 3, 5)}
-    # packed input (and packed filter, K*C*R*S*4 bytes) only: no C*R*S*N*P*Q term
+    # packed operands, the packed filter and (small grids / long reductions)
+    # split-K partial tiles -- sized by the output, never C*R*S*N*P*Q: the
+    # 5x5 problem stays far below its lowered matrix, which the explicit
+    # engine allocates in full
     lowered5 = 8 * 16 * 25 * 32 * 32 * 4
-    assert max(sizes.values()) - min(sizes.values()) <= 16 * 16 * 25 * 8 + (1 << 20)
-    assert max(sizes.values()) < lowered5 / 4
+    partial_cap = 148 * 128 * 256 * 4  # split-K partial tiles: one per SM at most
+    assert max(sizes.values()) < lowered5 / 4, sizes
+    assert max(sizes.values()) - min(sizes.values()) <= partial_cap + 16 * 16 * 25 * 8, sizes
 
 
 def test_explicit_limit_is_alloc_too_large():
