@@ -268,6 +268,19 @@ __device__ __forceinline__ uint64_t desc_mnmajor_sw128(uint32_t smem_addr, uint3
   d |= uint64_t(2) << 61;
   return d;
 }
+// MN-major operand tile, 64-byte swizzle: 32 MN-contiguous bf16 per 64 B row,
+// 8 K-rows per 512 B atom; LBO = byte stride between 32-wide MN blocks,
+// SBO = byte stride between 8-row K groups (512 B).
+__device__ __forceinline__ uint64_t desc_mnmajor_sw64(uint32_t smem_addr, uint32_t lbo,
+                                                      uint32_t sbo) {
+  uint64_t d = 0;
+  d |= uint64_t((smem_addr >> 4) & 0x3FFF);
+  d |= uint64_t((lbo >> 4) & 0x3FFF) << 16;
+  d |= uint64_t((sbo >> 4) & 0x3FFF) << 32;
+  d |= uint64_t(1) << 46;
+  d |= uint64_t(4) << 61;
+  return d;
+}
 // Instruction descriptor, kind::f16 with BF16 inputs and FP32 accumulate.
 __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, int a_mn_major, int b_mn_major) {
   return (1u << 4)                 // D format F32

@@ -343,12 +343,16 @@ static int64_t max_chain(int px) {
   return c / px * px;
 }
 
-template <int BN, int NC, int PX>
+// BW: width (channels) of one dy MN block: 64 (128-byte swizzle) or 32
+// (64-byte swizzle, lets a CTA pair split BN = 64 or 192 into halves)
+template <int BN, int NC, int PX, int BW = 64>
 struct WgCfg {
-  static constexpr int BLK = PX * 128;         // one 64-wide MN block
-  static constexpr int B_BLKS = BN / NC / 64;  // dy blocks loaded by each CTA
+  static constexpr int BLK = PX * 128;         // one 64-wide MN block of x
+  static constexpr int BBLK = PX * BW * 2;     // one BW-wide MN block of dy
+  static constexpr int B_BLKS = BN / NC / BW;  // dy blocks loaded by each CTA
+  static_assert(B_BLKS * BW * NC == BN, "dy blocks must tile the CTA's columns");
   static constexpr int A_BYTES = 2 * BLK;      // 128 x-columns
-  static constexpr int B_BYTES = B_BLKS * BLK;
+  static constexpr int B_BYTES = B_BLKS * BBLK;
   static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
   static constexpr int STAGES =
       (225 * 1024 - 2048) / STAGE_BYTES > 8 ? 8 : (225 * 1024 - 2048) / STAGE_BYTES;
@@ -356,9 +360,9 @@ struct WgCfg {
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
 };
 
-template <int BN, int NC, int PX>
+template <int BN, int NC, int PX, int BW>
 __global__ void __launch_bounds__(kWgThreads, 1) wgrad_tma_kernel(const __grid_constant__ WgTmaParams P) {
-  using C = WgCfg<BN, NC, PX>;
+  using C = WgCfg<BN, NC, PX, BW>;
   constexpr int S = C::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -408,7 +412,7 @@ __global__ void __launch_bounds__(kWgThreads, 1) wgrad_tma_kernel(const __grid_c
         ptx::tma_prefetch(&P.tm_dylo);
       }
       const CUtensorMap* tmx = pw == 0 ? &P.tm_xhi : &P.tm_xlo;
-      const int dyblk0 = (n0 + int(rank) * (BN / NC)) / 64;  // this CTA's first dy channel block
+      const int dyblk0 = (n0 + int(rank) * (BN / NC)) / BW;  // this CTA's first dy channel block
       for (int kb = 0; kb < nkb; kb++) {
         const int s = kb % S;
         const bool tr = P.trace && pw == 0 && blockIdx.x == 0 && blockIdx.y == 0 &&
@@ -466,19 +470,23 @@ __global__ void __launch_bounds__(kWgThreads, 1) wgrad_tma_kernel(const __grid_c
         const uint32_t sa = smem0 + s * C::STAGE_BYTES;
         const uint64_t dah = ptx::desc_mnmajor_sw128(sa, C::BLK, 1024);
         const uint64_t dal = ptx::desc_mnmajor_sw128(sa + C::A_BYTES, C::BLK, 1024);
-        const uint64_t dbh = ptx::desc_mnmajor_sw128(sa + 2 * C::A_BYTES, C::BLK, 1024);
-        const uint64_t dbl = ptx::desc_mnmajor_sw128(sa + 2 * C::A_BYTES + C::B_BYTES, C::BLK, 1024);
+        const uint32_t sb = sa + 2 * C::A_BYTES;
+        const uint64_t dbh = BW == 64 ? ptx::desc_mnmajor_sw128(sb, C::BBLK, 1024)
+                                      : ptx::desc_mnmajor_sw64(sb, C::BBLK, 512);
+        const uint64_t dbl = BW == 64 ? ptx::desc_mnmajor_sw128(sb + C::B_BYTES, C::BBLK, 1024)
+                                      : ptx::desc_mnmajor_sw64(sb + C::B_BYTES, C::BBLK, 512);
 #pragma unroll
         for (int kk = 0; kk < PX / 16; kk++) {
-          const uint64_t o = uint64_t(kk * 2048) >> 4;  // 16 pixels = 2 groups of 8 rows
+          const uint64_t o = uint64_t(kk * 2048) >> 4;         // 16 pixels of 128 B rows (x)
+          const uint64_t ob = uint64_t(kk * 16 * BW * 2) >> 4;  // 16 pixels of BW*2 B rows (dy)
           if constexpr (NC == 2) {
-            ptx::mma_bf16_pair_elect(tmem_d, dal + o, dbh + o, idesc, acc);
-            ptx::mma_bf16_pair_elect(tmem_d, dah + o, dbl + o, idesc, 1);
-            ptx::mma_bf16_pair_elect(tmem_d, dah + o, dbh + o, idesc, 1);
+            ptx::mma_bf16_pair_elect(tmem_d, dal + o, dbh + ob, idesc, acc);
+            ptx::mma_bf16_pair_elect(tmem_d, dah + o, dbl + ob, idesc, 1);
+            ptx::mma_bf16_pair_elect(tmem_d, dah + o, dbh + ob, idesc, 1);
           } else {
-            ptx::mma_bf16_elect(tmem_d, dal + o, dbh + o, idesc, acc);
-            ptx::mma_bf16_elect(tmem_d, dah + o, dbl + o, idesc, 1);
-            ptx::mma_bf16_elect(tmem_d, dah + o, dbh + o, idesc, 1);
+            ptx::mma_bf16_elect(tmem_d, dal + o, dbh + ob, idesc, acc);
+            ptx::mma_bf16_elect(tmem_d, dah + o, dbl + ob, idesc, 1);
+            ptx::mma_bf16_elect(tmem_d, dah + o, dbh + ob, idesc, 1);
           }
           acc = 1;
         }
@@ -561,14 +569,14 @@ __global__ void __launch_bounds__(256) wgrad_reduce_tma(WgReduceGeom g, const fl
   }
 }
 
-template <int BN, int NC, int PX>
+template <int BN, int NC, int PX, int BW = 64>
 cudaError_t launch_wgrad_tma(const WgTmaParams& prm, dim3 grid, cudaStream_t st) {
-  using CC = WgCfg<BN, NC, PX>;
+  using CC = WgCfg<BN, NC, PX, BW>;
   static int attr_dev = -1;
   int dev = 0;
   cudaGetDevice(&dev);
   if (attr_dev != dev) {
-    cudaError_t e = cudaFuncSetAttribute(wgrad_tma_kernel<BN, NC, PX>,
+    cudaError_t e = cudaFuncSetAttribute(wgrad_tma_kernel<BN, NC, PX, BW>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, CC::SMEM);
     if (e != cudaSuccess) return e;
     attr_dev = dev;
@@ -586,7 +594,7 @@ cudaError_t launch_wgrad_tma(const WgTmaParams& prm, dim3 grid, cudaStream_t st)
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   ktime_begin(st, 2);
-  cudaError_t e = cudaLaunchKernelEx(&cfg, wgrad_tma_kernel<BN, NC, PX>, prm);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, wgrad_tma_kernel<BN, NC, PX, BW>, prm);
   ktime_end(st);
   note_launch();
   if (e != cudaSuccess) return e;
@@ -630,9 +638,20 @@ cudaError_t wgrad_tma(const ConvProblem& p, const float* dy, const float* x, flo
   const int Kp64 = int(ceil_div(p.K, 64) * 64);
   int bn = Kp64 <= 256 ? Kp64 : (Kp64 % 256 == 0 ? 256 : (Kp64 % 192 == 0 ? 192 : 128));
   if (getenv("DNNP_TC_BN")) bn = atoi(getenv("DNNP_TC_BN"));
-  int nc = (bn % 128 == 0) ? 2 : 1;
+  // CTA pairs split the dy columns in halves: 64-channel blocks (128-byte
+  // swizzle) when bn / 2 is a multiple of 64, else 32-channel blocks (64-byte
+  // swizzle) for bn = 192 (conv2 122.9 vs 137.2 us, conv3 67.6 vs 73.9 us);
+  // bn = 64 keeps single CTAs (conv1: the 256-row pair tiles pad 576 x-columns
+  // to 768, 178 vs 147 us; DNNP_WG_BW32_64 forces the pair)
+  int nc = (bn % 128 == 0 || (bn == 192 && !getenv("DNNP_WG_NO_BW32")) ||
+            (bn == 64 && getenv("DNNP_WG_BW32_64")))
+               ? 2
+               : 1;
   if (getenv("DNNP_TC_NC")) nc = atoi(getenv("DNNP_TC_NC"));
-  if (nc == 2 && bn % 128) nc = 1;
+  if (nc == 2 && bn % 64) nc = 1;
+  if (nc == 2 && bn % 128 && bn != 64 && bn != 192) nc = 1;
+  const bool bw32 = nc == 2 && bn % 128 != 0;
+  const int dbw = bw32 ? 32 : 64;  // dy block width of the tensor map
   const int mrows = int(ceil_div(ncolx, 128 * nc) * 128 * nc);
   const int ncols = int(ceil_div(Kp64, bn) * bn);
   const int mt = mrows / (128 * nc), nt = ncols / bn;
@@ -682,14 +701,13 @@ cudaError_t wgrad_tma(const ConvProblem& p, const float* dy, const float* x, flo
   if ((e = make_tmap_im2col(&prm.tm_xhi, x_hi, ig, CU_TENSOR_MAP_SWIZZLE_128B)) != cudaSuccess) return e;
   if ((e = make_tmap_im2col(&prm.tm_xlo, x_lo, ig, CU_TENSOR_MAP_SWIZZLE_128B)) != cudaSuccess) return e;
   {
-    const uint64_t dims[3] = {64, uint64_t(NPQ), uint64_t(Kp64 / 64)};
-    const uint64_t strides[2] = {uint64_t(Kp64) * 2, 128};
-    const uint32_t box[3] = {64, uint32_t(px), uint32_t(bn / nc / 64)};
-    if ((e = make_tmap_3d(&prm.tm_dyhi, dy_hi, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B)) !=
-        cudaSuccess)
+    const uint64_t dims[3] = {uint64_t(dbw), uint64_t(NPQ), uint64_t(Kp64 / dbw)};
+    const uint64_t strides[2] = {uint64_t(Kp64) * 2, uint64_t(dbw) * 2};
+    const uint32_t box[3] = {uint32_t(dbw), uint32_t(px), uint32_t(bn / nc / dbw)};
+    const CUtensorMapSwizzle dsw = bw32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B;
+    if ((e = make_tmap_3d(&prm.tm_dyhi, dy_hi, dims, strides, box, dsw)) != cudaSuccess)
       return e;
-    if ((e = make_tmap_3d(&prm.tm_dylo, dy_lo, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B)) !=
-        cudaSuccess)
+    if ((e = make_tmap_3d(&prm.tm_dylo, dy_lo, dims, strides, box, dsw)) != cudaSuccess)
       return e;
   }
   prm.pix_per_split = pps;
@@ -715,6 +733,12 @@ cudaError_t wgrad_tma(const ConvProblem& p, const float* dy, const float* x, flo
   const dim3 grid{unsigned(mt * nc), unsigned(nt), unsigned(splits)};
   auto go = [&](auto pxc) {
     constexpr int PX = decltype(pxc)::value;
+    if (nc == 2 && bw32) {
+      switch (bn) {
+        case 64: return launch_wgrad_tma<64, 2, PX, 32>(prm, grid, st);
+        default: return launch_wgrad_tma<192, 2, PX, 32>(prm, grid, st);
+      }
+    }
     if (nc == 2) {
       switch (bn) {
         case 128: return launch_wgrad_tma<128, 2, PX>(prm, grid, st);

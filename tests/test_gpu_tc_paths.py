@@ -262,3 +262,16 @@ def test_simt_narrow_tiles(shape):
             check(run_case(shape, passes=("fwd", "bwd_data"), seed=16))
     finally:
         dp.set_math(dp.MATH_DEFAULT)
+
+
+@pytest.mark.parametrize("shape", [(2, 24, 11, 9, 192, 3, 3, 1, 1, 1, 1),
+                                   (2, 16, 13, 13, 64, 5, 5, 1, 1, 2, 2),
+                                   (3, 3, 32, 36, 192, 11, 11, 4, 4, 2, 2)])
+def test_wgrad_pairs_32_channel_dy_blocks(shape):
+    """Backward-filter on CTA pairs with 32-channel dy blocks (64-byte
+    swizzle, MN-major): bn = 192 by default, bn = 64 forced."""
+    check(run_case(shape, passes=("bwd_filter",), seed=17))
+    with env(DNNP_WG_BW32_64=1):
+        check(run_case(shape, passes=("bwd_filter",), seed=17))
+    with env(DNNP_WG_NO_BW32=1):
+        check(run_case(shape, passes=("bwd_filter",), seed=17))
