@@ -222,28 +222,63 @@ def _check_out(out: TensorView, extents, dtype, what):
         raise ShapeMismatch(f"{what} element type {out.desc.dtype}, expected {dtype}")
 
 
+def _ws(workspace):
+    """(pointer, bytes) of a caller workspace: a CUDA tensor (any dtype)."""
+    return workspace.data_ptr(), workspace.numel() * workspace.element_size()
+
+
+def convolution_workspace_size(pass_, x_desc, f_desc, conv: ConvDesc, y_desc,
+                               engine="implicit") -> int:
+    """Device workspace bytes of one pass (0 / "fwd", 1 / "bwd_data", 2 /
+    "bwd_filter") for these descriptors (additive, dnnp_get_convolution_
+    workspace_size: exact, measured by running the pass once on scratch
+    tensors -- a setup-time call)."""
+    import ctypes
+    code = {"fwd": 0, "bwd_data": 1, "bwd_filter": 2}.get(pass_, pass_)
+    out = ctypes.c_size_t(0)
+    _lib.check(_lib.lib().dnnp_get_convolution_workspace_size(
+        _lib.handle(), int(code), x_desc.c_desc(), f_desc.c_desc(), conv.c_desc(),
+        y_desc.c_desc(), _ENGINE_CODE[as_engine(engine)], ctypes.byref(out)),
+        "get_convolution_workspace_size")
+    return int(out.value)
+
+
 def conv_forward(x: TensorView, f: FilterView, conv: ConvDesc, engine, y: TensorView,
                  alpha: float = 1.0, beta: float = 0.0, *, tile=None, threads: int = 1,
-                 max_lowered_bytes: int = 4 << 30) -> None:
-    """y := alpha * conv(x, f) + beta * y (accumulate forces beta=1)."""
+                 max_lowered_bytes: int = 4 << 30, workspace=None) -> None:
+    """y := alpha * conv(x, f) + beta * y (accumulate forces beta=1).
+    workspace: optional CUDA tensor the pass takes its scratch from."""
     engine = as_engine(engine)
     out_shape = _check_triplet(x, f, conv)
     _check_out(y, out_shape, x.desc.dtype, "output")
     bind_stream(x, f, y)
     a_keep, a = scalar_ptr(alpha, y.desc.dtype)
     b_keep, b = scalar_ptr(beta, y.desc.dtype)
+    if workspace is not None:
+        _lib.check(_lib.lib().dnnp_convolution_forward_ex(
+            _lib.handle(), a, x.desc.c_desc(), x.ptr, f.desc.c_desc(), f.ptr, conv.c_desc(),
+            _ENGINE_CODE[engine], b, y.desc.c_desc(), y.ptr, *_ws(workspace)),
+            "convolution_forward_ex")
+        return
     _lib.check(_lib.lib().dnnp_convolution_forward(
         _lib.handle(), a, x.desc.c_desc(), x.ptr, f.desc.c_desc(), f.ptr, conv.c_desc(),
         _ENGINE_CODE[engine], b, y.desc.c_desc(), y.ptr), "convolution_forward")
 
 
 def conv_backward_data(dy: TensorView, f: FilterView, conv: ConvDesc, engine, dx: TensorView,
-                       *, tile=None, threads: int = 1, max_lowered_bytes: int = 4 << 30) -> None:
+                       *, tile=None, threads: int = 1, max_lowered_bytes: int = 4 << 30,
+                       workspace=None) -> None:
     """Gradient with respect to the input; accumulate mode adds into dx."""
     engine = as_engine(engine)
     out_shape = _check_triplet(dx, f, conv)
     _check_out(dy, out_shape, dx.desc.dtype, "output gradient")
     bind_stream(dy, f, dx)
+    if workspace is not None:
+        _lib.check(_lib.lib().dnnp_convolution_backward_data_ex(
+            _lib.handle(), f.desc.c_desc(), f.ptr, dy.desc.c_desc(), dy.ptr, conv.c_desc(),
+            _ENGINE_CODE[engine], dx.desc.c_desc(), dx.ptr, *_ws(workspace)),
+            "convolution_backward_data_ex")
+        return
     _lib.check(_lib.lib().dnnp_convolution_backward_data(
         _lib.handle(), f.desc.c_desc(), f.ptr, dy.desc.c_desc(), dy.ptr, conv.c_desc(),
         _ENGINE_CODE[engine], dx.desc.c_desc(), dx.ptr), "convolution_backward_data")
@@ -251,12 +286,18 @@ def conv_backward_data(dy: TensorView, f: FilterView, conv: ConvDesc, engine, dx
 
 def conv_backward_filter(dy: TensorView, x: TensorView, conv: ConvDesc, engine, df: FilterView,
                          *, tile=None, threads: int = 1,
-                         max_lowered_bytes: int = 4 << 30) -> None:
+                         max_lowered_bytes: int = 4 << 30, workspace=None) -> None:
     """Gradient with respect to the filter; accumulate mode adds into df."""
     engine = as_engine(engine)
     out_shape = _check_triplet(x, df, conv)
     _check_out(dy, out_shape, x.desc.dtype, "output gradient")
     bind_stream(dy, x, df)
+    if workspace is not None:
+        _lib.check(_lib.lib().dnnp_convolution_backward_filter_ex(
+            _lib.handle(), x.desc.c_desc(), x.ptr, dy.desc.c_desc(), dy.ptr, conv.c_desc(),
+            _ENGINE_CODE[engine], df.desc.c_desc(), df.ptr, *_ws(workspace)),
+            "convolution_backward_filter_ex")
+        return
     _lib.check(_lib.lib().dnnp_convolution_backward_filter(
         _lib.handle(), x.desc.c_desc(), x.ptr, dy.desc.c_desc(), dy.ptr, conv.c_desc(),
         _ENGINE_CODE[engine], df.desc.c_desc(), df.ptr), "convolution_backward_filter")

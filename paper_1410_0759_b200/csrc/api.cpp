@@ -348,6 +348,34 @@ size_t span_bytes(dnnp_tensor_desc d) { return size_t(max_offset(d) + 1) * elem_
 // A view with no gaps inside its span: writing the span writes only the view.
 bool dense_view(dnnp_tensor_desc d) { return max_offset(d) + 1 == d->n * d->c * d->h * d->w; }
 
+// ------------------------------------------- caller-supplied workspace
+// The *_ex entries run the plain entry with this thread's workspace set: the
+// compute's scratch is carved from the caller's device buffer (host operands
+// are still staged through the library's own arena), and the chunked host
+// pipeline is not used.
+struct ExWorkspace {
+  void* p = nullptr;
+  size_t bytes = 0;
+  bool on = false;
+};
+static thread_local ExWorkspace g_exws;
+
+template <class F>
+static cudaError_t with_workspace(F&& compute, size_t* need) {
+  if (!g_exws.on) return compute();
+  dnnp::tc::user_workspace_begin(g_exws.p, g_exws.bytes);
+  cudaError_t e = compute();
+  dnnp::tc::user_workspace_end(need);
+  return e;
+}
+
+static dnnp_status ws_status(cudaError_t e, size_t need, const char* what) {
+  if (e == cudaErrorMemoryAllocation && g_exws.on && need > g_exws.bytes)
+    return fail(DNNP_STATUS_ALLOC_FAILED, "%s: workspace of %zu bytes too small (needs %zu)", what,
+                g_exws.bytes, need);
+  return DNNP_STATUS_OK;
+}
+
 // ------------------------------------------- pipelined host staging
 // Batch-separable convolutions with HOST buffers: the N images go through in
 // chunks; chunk i's inputs copy host->device on a copy-in stream while chunk
@@ -383,7 +411,7 @@ static int64_t image_bytes(dnnp_tensor_desc d) {  // footprint of one image
 
 static bool pipeline_ok(const std::vector<ChunkBuf>& bufs, int64_t N) {
   static const bool off = getenv("DNNP_NO_PIPELINE") != nullptr;
-  if (off || N < 2) return false;
+  if (off || N < 2 || g_exws.on) return false;
   size_t total = 0;
   for (const auto& b : bufs) {
     const dnnp_tensor_desc d = b.d;
@@ -843,8 +871,15 @@ dnnp_status dnnp_convolution_forward(dnnp_handle handle, const void* alpha, dnnp
   if ((st = sg.add(x, span_bytes(xd), false, true, &dx))) return st;
   if ((st = sg.add(f, fbytes, false, true, &df))) return st;
   if ((st = sg.add(y, span_bytes(yd), true, b != 0.0 || !dense_view(yd), &dy))) return st;
-  cudaError_t e = dnnp::conv_forward(pr, dnnp::Dtype(xd->elem), dx, df, dy, a, b, handle->math,
-                                     handle->stream);
+  size_t need = 0;
+  cudaError_t e = with_workspace([&] {
+    return dnnp::conv_forward(pr, dnnp::Dtype(xd->elem), dx, df, dy, a, b, handle->math,
+                              handle->stream);
+  }, &need);
+  if ((st = ws_status(e, need, "convolution_forward_ex"))) {
+    sg.finish(cudaSuccess);
+    return st;
+  }
   return sg.finish(e);
 }
 
@@ -890,8 +925,15 @@ dnnp_status dnnp_convolution_backward_data(dnnp_handle handle, dnnp_filter_desc 
   if ((st = sg.add(dy, span_bytes(dyd), false, true, &ddy))) return st;
   if ((st = sg.add(dx, span_bytes(dxd), true, cd->accumulate || !dense_view(dxd), &ddx)))
     return st;
-  cudaError_t e = dnnp::conv_backward_data(pr, dnnp::Dtype(dxd->elem), ddy, dff, ddx,
-                                           cd->accumulate != 0, handle->math, handle->stream);
+  size_t need = 0;
+  cudaError_t e = with_workspace([&] {
+    return dnnp::conv_backward_data(pr, dnnp::Dtype(dxd->elem), ddy, dff, ddx,
+                                    cd->accumulate != 0, handle->math, handle->stream);
+  }, &need);
+  if ((st = ws_status(e, need, "convolution_backward_data_ex"))) {
+    sg.finish(cudaSuccess);
+    return st;
+  }
   return sg.finish(e);
 }
 
@@ -938,8 +980,15 @@ dnnp_status dnnp_convolution_backward_filter(dnnp_handle handle, dnnp_tensor_des
   if ((st = sg.add(x, span_bytes(xd), false, true, &dxx))) return st;
   if ((st = sg.add(dy, span_bytes(dyd), false, true, &ddy))) return st;
   if ((st = sg.add(df, fbytes, true, cd->accumulate != 0, &ddf))) return st;
-  cudaError_t e = dnnp::conv_backward_filter(pr, dnnp::Dtype(xd->elem), ddy, dxx, ddf,
-                                             cd->accumulate != 0, handle->math, handle->stream);
+  size_t need = 0;
+  cudaError_t e = with_workspace([&] {
+    return dnnp::conv_backward_filter(pr, dnnp::Dtype(xd->elem), ddy, dxx, ddf,
+                                      cd->accumulate != 0, handle->math, handle->stream);
+  }, &need);
+  if ((st = ws_status(e, need, "convolution_backward_filter_ex"))) {
+    sg.finish(cudaSuccess);
+    return st;
+  }
   return sg.finish(e);
 }
 
@@ -963,6 +1012,100 @@ dnnp_status dnnp_convolution_backward_bias(dnnp_handle handle, dnnp_tensor_desc 
                                            view_of(dbd), dnnp::Dtype(dbd->elem), ddb,
                                            handle->stream);
   return sg.finish(e);
+}
+
+// ------------------------------------------------ workspace (additive)
+
+dnnp_status dnnp_convolution_forward_ex(dnnp_handle handle, const void* alpha,
+                                        dnnp_tensor_desc xd, const void* x, dnnp_filter_desc fd,
+                                        const void* f, dnnp_conv_desc cd, dnnp_engine engine,
+                                        const void* beta, dnnp_tensor_desc yd, void* y,
+                                        void* workspace, size_t workspace_bytes) {
+  if (workspace_bytes && !workspace)
+    return fail(DNNP_STATUS_BAD_PARAM, "convolution_forward_ex: NULL workspace");
+  g_exws = ExWorkspace{workspace, workspace_bytes, true};
+  const dnnp_status st = dnnp_convolution_forward(handle, alpha, xd, x, fd, f, cd, engine, beta, yd, y);
+  g_exws = ExWorkspace{};
+  return st;
+}
+
+dnnp_status dnnp_convolution_backward_data_ex(dnnp_handle handle, dnnp_filter_desc fd,
+                                              const void* f, dnnp_tensor_desc dyd, const void* dy,
+                                              dnnp_conv_desc cd, dnnp_engine engine,
+                                              dnnp_tensor_desc dxd, void* dx, void* workspace,
+                                              size_t workspace_bytes) {
+  if (workspace_bytes && !workspace)
+    return fail(DNNP_STATUS_BAD_PARAM, "convolution_backward_data_ex: NULL workspace");
+  g_exws = ExWorkspace{workspace, workspace_bytes, true};
+  const dnnp_status st = dnnp_convolution_backward_data(handle, fd, f, dyd, dy, cd, engine, dxd, dx);
+  g_exws = ExWorkspace{};
+  return st;
+}
+
+dnnp_status dnnp_convolution_backward_filter_ex(dnnp_handle handle, dnnp_tensor_desc xd,
+                                                const void* x, dnnp_tensor_desc dyd,
+                                                const void* dy, dnnp_conv_desc cd,
+                                                dnnp_engine engine, dnnp_filter_desc fd, void* df,
+                                                void* workspace, size_t workspace_bytes) {
+  if (workspace_bytes && !workspace)
+    return fail(DNNP_STATUS_BAD_PARAM, "convolution_backward_filter_ex: NULL workspace");
+  g_exws = ExWorkspace{workspace, workspace_bytes, true};
+  const dnnp_status st =
+      dnnp_convolution_backward_filter(handle, xd, x, dyd, dy, cd, engine, fd, df);
+  g_exws = ExWorkspace{};
+  return st;
+}
+
+// Exact device workspace of one pass: the pass runs once on zero-filled
+// device tensors of the descriptors' shapes and the scratch it takes is
+// measured (a setup-time query: it allocates those tensors temporarily).
+dnnp_status dnnp_get_convolution_workspace_size(dnnp_handle handle, int pass,
+                                                dnnp_tensor_desc xd, dnnp_filter_desc fd,
+                                                dnnp_conv_desc cd, dnnp_tensor_desc yd,
+                                                dnnp_engine engine, size_t* bytes) {
+  if (!reg_has(handle, KIND_HANDLE) || !bytes || pass < 0 || pass > 2)
+    return fail(DNNP_STATUS_BAD_PARAM, "get_convolution_workspace_size: bad arguments");
+  if (!reg_has(xd, KIND_TENSOR) || !xd->configured || !reg_has(yd, KIND_TENSOR) ||
+      !yd->configured || !reg_has(fd, KIND_FILTER) || !fd->configured)
+    return fail(DNNP_STATUS_BAD_PARAM, "get_convolution_workspace_size: descriptor not configured");
+  if (!reg_has(cd, KIND_CONV) || !cd->configured)
+    return fail(DNNP_STATUS_BAD_PARAM, "conv descriptor not configured");
+  if (!engine_valid(engine)) return fail(DNNP_STATUS_BAD_PARAM, "bad engine");
+  dnnp_status st;
+  if ((st = bind_view(xd, "x")) || (st = bind_view(yd, "y"))) return st;
+  int64_t P, Q;
+  if ((st = conv_shape(xd, fd, cd, &P, &Q))) return st;
+  if ((st = check_out(yd, xd->n, fd->k, P, Q, xd->elem, "output"))) return st;
+  dnnp::ConvProblem pr = make_problem(xd, fd, cd, yd, P, Q);
+  pr.engine = pass == 0 ? int(engine) : 2;
+  if ((st = check_decode_range(pr))) return st;
+  if ((st = need_device())) return st;
+  cudaStream_t s = handle->stream;
+  const size_t xb = span_bytes(xd), yb = span_bytes(yd);
+  const size_t fb = size_t(fd->k * fd->c * fd->r * fd->s) * elem_size(fd->elem);
+  void *dx = nullptr, *dy = nullptr, *df = nullptr;
+  cudaError_t e = cudaMallocAsync(&dx, xb, s);
+  if (e == cudaSuccess) e = cudaMallocAsync(&dy, yb, s);
+  if (e == cudaSuccess) e = cudaMallocAsync(&df, fb, s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(dx, 0, xb, s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(dy, 0, yb, s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(df, 0, fb, s);
+  if (e == cudaSuccess) {
+    dnnp::tc::scratch_measure_begin(s);
+    const dnnp::Dtype dt = dnnp::Dtype(xd->elem);
+    if (pass == 0)
+      e = dnnp::conv_forward(pr, dt, dx, df, dy, 1.0, 0.0, handle->math, s);
+    else if (pass == 1)
+      e = dnnp::conv_backward_data(pr, dt, dy, df, dx, false, handle->math, s);
+    else
+      e = dnnp::conv_backward_filter(pr, dt, dy, dx, df, false, handle->math, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    *bytes = dnnp::tc::scratch_measure_end(s);
+  }
+  for (void* p : {dx, dy, df})
+    if (p) cudaFreeAsync(p, s);
+  cudaStreamSynchronize(s);
+  return cuda_status(e, "get_convolution_workspace_size");
 }
 
 // ------------------------------------------------ fused epilogues (additive)

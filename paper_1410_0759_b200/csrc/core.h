@@ -49,6 +49,16 @@ struct ScratchScope;
 ScratchScope* scratch_open(cudaStream_t st);
 cudaError_t scratch_alloc(ScratchScope* s, size_t bytes, void** p);
 void scratch_close(ScratchScope* s);
+// Caller-supplied workspace (the paper's minimal-workspace contract, additive
+// *_ex entries): while active on this thread, every scratch allocation is
+// carved from [base, base + bytes) instead of the library's arena, and an
+// allocation past the end fails with cudaErrorMemoryAllocation.
+void user_workspace_begin(void* base, size_t bytes);
+// ends the override; *need = the bytes the call asked for in total
+void user_workspace_end(size_t* need);
+// scratch footprint measurement of one call on stream st
+void scratch_measure_begin(cudaStream_t st);
+size_t scratch_measure_end(cudaStream_t st);
 }  // namespace tc
 
 // Launch bookkeeping: every kernel this library launches bumps a counter

@@ -37,6 +37,7 @@ struct Workspace {
   ArenaState* a_;
   size_t saved_off_ = 0;
   bool fallback_ = false;
+  size_t fb_bytes_ = 0;
 };
 
 void pool_keep_memory();

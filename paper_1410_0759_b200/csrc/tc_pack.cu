@@ -513,6 +513,7 @@ struct ArenaState {
   std::recursive_mutex mu;
   void* base = nullptr;
   size_t cap = 0, off = 0, high = 0;
+  size_t fb = 0;  // outstanding fallback bytes (allocated outside the arena)
   int depth = 0;
 };
 
@@ -533,26 +534,67 @@ static ArenaState* arena_for(cudaStream_t st) {
   return a;
 }
 
+// caller-supplied workspace override (thread local, LIFO like the arena)
+struct UserWs {
+  char* base = nullptr;
+  size_t cap = 0, off = 0, high = 0;
+  bool active = false;
+};
+static thread_local UserWs g_uws;
+
+void user_workspace_begin(void* base, size_t bytes) {
+  g_uws.base = static_cast<char*>(base);
+  g_uws.cap = bytes;
+  g_uws.off = g_uws.high = 0;
+  g_uws.active = true;
+}
+
+void user_workspace_end(size_t* need) {
+  if (need) *need = g_uws.high;
+  g_uws = UserWs{};
+}
+
 Workspace::Workspace(cudaStream_t s) : st(s), a_(arena_for(s)) {
   a_->mu.lock();
   a_->depth++;
-  saved_off_ = a_->off;
+  saved_off_ = g_uws.active ? g_uws.off : a_->off;
 }
 
 cudaError_t Workspace::alloc(size_t bytes) {
   bytes = (bytes + 1023) & ~size_t(1023);
-  a_->high = std::max(a_->high, a_->off + bytes);
+  if (g_uws.active) {
+    // 1024-byte aligned carve-outs of the caller's buffer
+    const uintptr_t b = (reinterpret_cast<uintptr_t>(g_uws.base) + 1023) & ~uintptr_t(1023);
+    const size_t skew = b - reinterpret_cast<uintptr_t>(g_uws.base);
+    g_uws.high = std::max(g_uws.high, skew + g_uws.off + bytes);
+    if (skew + g_uws.off + bytes > g_uws.cap) return cudaErrorMemoryAllocation;
+    p = reinterpret_cast<char*>(b) + g_uws.off;
+    g_uws.off += bytes;
+    return cudaSuccess;
+  }
+  // the high-water mark counts fallback bytes too, so a call's footprint is
+  // right even before the arena has grown to it
+  a_->high = std::max(a_->high, a_->off + a_->fb + bytes);
   if (a_->base && a_->off + bytes <= a_->cap) {
     p = static_cast<char*>(a_->base) + a_->off;
     a_->off += bytes;
     return cudaSuccess;
   }
   fallback_ = true;
+  fb_bytes_ = bytes;
+  a_->fb += bytes;
   return cudaMallocAsync(&p, bytes, st);
 }
 
 Workspace::~Workspace() {
+  if (g_uws.active) {
+    g_uws.off = saved_off_;
+    --a_->depth;
+    a_->mu.unlock();
+    return;
+  }
   if (fallback_ && p) cudaFreeAsync(p, st);
+  if (fallback_) a_->fb -= fb_bytes_;
   a_->off = saved_off_;
   if (--a_->depth == 0 && a_->high > a_->cap) {
     if (a_->base) cudaFreeAsync(a_->base, st);
@@ -566,6 +608,18 @@ Workspace::~Workspace() {
     }
   }
   a_->mu.unlock();
+}
+
+void scratch_measure_begin(cudaStream_t st) {
+  ArenaState* a = arena_for(st);
+  std::lock_guard<std::recursive_mutex> g(a->mu);
+  a->high = a->off;
+}
+
+size_t scratch_measure_end(cudaStream_t st) {
+  ArenaState* a = arena_for(st);
+  std::lock_guard<std::recursive_mutex> g(a->mu);
+  return a->high - a->off;
 }
 
 // ---- main-kernel timing (bench roofline) ----------------------------------
