@@ -963,6 +963,70 @@ __global__ void __launch_bounds__(256) pool_fwd_pipe_kernel(PoolGeom g, const T*
   cpa_wait<0>();
 }
 
+// Channels-innermost forward (NHWC-like views, x.sc == y.sc == 1): a block
+// = one output row segment (n, p, 32 q) x 32 channels; lane = channel, so
+// every window load and y store is a contiguous 32-channel run; the argmax
+// (logical NCHW index, stored in the dense [N][C][P][Q] buffer) goes
+// through a shared-memory transpose so its stores are q-contiguous.
+template <typename T>
+__global__ void __launch_bounds__(256) pool_fwd_cl_kernel(PoolGeom g, const T* __restrict__ x,
+                                                          T* __restrict__ y, int64_t* argmax,
+                                                          int kind, int nqb, int ncb) {
+  __shared__ int64_t am[32][33];
+  const int H = int(g.H), W = int(g.W), P = int(g.P), Q = int(g.Q), C = int(g.C);
+  const int wh = int(g.wh), ww = int(g.ww);
+  uint32_t b = blockIdx.x;
+  const int cb = int(b % uint32_t(ncb));
+  b /= uint32_t(ncb);
+  const int qb = int(b % uint32_t(nqb));
+  b /= uint32_t(nqb);
+  const int p = int(b % uint32_t(P)), n = int(b / uint32_t(P));
+  const int lane = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 8 q rows per pass
+  const int c = cb * 32 + lane;
+  const bool cok = c < C;
+  const T* xb = x + int64_t(n) * g.x.sn + int64_t(cok ? c : 0) * g.x.sc;
+  const int hs0 = p * int(g.sh) - int(g.ph);
+  const int hs = max(0, hs0), he = min(H, hs0 + wh);
+  for (int qi = ty; qi < 32; qi += 8) {
+    const int q = qb * 32 + qi;
+    if (q >= Q) break;
+    const int ws0 = q * int(g.sw) - int(g.pw);
+    const int ws = max(0, ws0), we = min(W, ws0 + ww);
+    T out = T(0);
+    int64_t bi = 0;
+    if (cok) {
+      if (kind == 0) {
+        T best = xb[int64_t(hs) * g.x.sh + int64_t(ws) * g.x.sw];
+        int bh = hs, bw = ws;
+        for (int h = hs; h < he; h++)
+          for (int w = ws; w < we; w++) {
+            const T v = xb[int64_t(h) * g.x.sh + int64_t(w) * g.x.sw];
+            const bool take = v > best || (v != v && best == best);
+            best = take ? v : best;
+            bh = take ? h : bh;
+            bw = take ? w : bw;
+          }
+        out = best;
+        bi = ((int64_t(n) * C + c) * H + bh) * W + bw;
+      } else {
+        T sacc = T(0);
+        for (int h = hs; h < he; h++)
+          for (int w = ws; w < we; w++) sacc = dadd<T>(sacc, xb[int64_t(h) * g.x.sh + int64_t(w) * g.x.sw]);
+        out = sacc / T((he - hs) * (we - ws));
+      }
+      y[int64_t(n) * g.y.sn + int64_t(c) * g.y.sc + int64_t(p) * g.y.sh + int64_t(q) * g.y.sw] = out;
+    }
+    am[lane][qi] = bi;
+  }
+  if (kind != 0 || !argmax) return;
+  __syncthreads();
+  // argmax rows: channel cb*32 + r, q-contiguous
+  for (int r = ty; r < 32; r += 8) {
+    const int cc = cb * 32 + r, q = qb * 32 + lane;
+    if (cc < C && q < Q) argmax[((int64_t(n) * C + cc) * P + p) * Q + q] = am[r][lane];
+  }
+}
+
 template <typename T, int KW>
 __global__ void __launch_bounds__(256) pool_fwd_plane_kernel(PoolGeom g, const T* __restrict__ x,
                                                              T* __restrict__ y, int64_t* argmax,
@@ -1219,6 +1283,21 @@ cudaError_t pool_forward(const PoolProblem& pp, Dtype dt, const View4& xv, const
   PoolGeom g = pool_geom(pp, xv, yv);
   const size_t eb = dt == F32 ? 4 : 8;
   const size_t psm = size_t(xv.h) * xv.w * eb;
+  if (xv.sc == 1 && yv.sc == 1 && xv.c >= 16 && !getenv("DNNP_POOL_NO_CL")) {
+    // channels innermost: channel-vectorised rows instead of planes
+    const int nqb = int(ceil_div(pp.Q, 32)), ncb = int(ceil_div(xv.c, 32));
+    const int64_t blocks = xv.n * pp.P * nqb * ncb;
+    if (blocks < (int64_t(1) << 31)) {
+      if (dt == F32)
+        pool_fwd_cl_kernel<float><<<unsigned(blocks), 256, 0, st>>>(g, (const float*)x, (float*)y,
+                                                                    argmax, pp.kind, nqb, ncb);
+      else
+        pool_fwd_cl_kernel<double><<<unsigned(blocks), 256, 0, st>>>(
+            g, (const double*)x, (double*)y, argmax, pp.kind, nqb, ncb);
+      note_launch();
+      return cudaGetLastError();
+    }
+  }
   const bool dense_planes = xv.sw == 1 && xv.sh == xv.w;
   const int pitch = int(((xv.h * xv.w + 16 / eb) * eb + 15) / 16 * 16 / eb);
   const size_t ppipe = size_t(2) * pitch * eb;
