@@ -410,10 +410,22 @@ def main():
     dom_avg = float(np.mean(kv)) if kv else float(np.mean(op_ms[dominant]))
     achieved = layers[dl]["flops"] / (dom_avg / 1e3) / 1e12
     traffic = None
+    ingest = None
     tpath = os.path.join(ROOT, "profiles", "dominant_traffic.json")
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get(f"{layers[dl]['name']}.{PASSES[dpi]}")
+            tj = json.load(open(tpath))
+            key = f"{layers[dl]['name']}.{PASSES[dpi]}"
+            traffic = tj.get(key)
+            ib = tj.get("ingest", {}).get(key)
+            if ib:
+                # L2 -> SM operand ingest (ncu bytes per launch over the live
+                # kernel time) against ~57 B/clk/SM x 148 SMs at the max clock
+                # (profiles/r01/tma_burst_probe.txt): the bound of narrow-N GEMMs
+                ceil_tbs = 57.0 * 148 * 1.965e9 / 1e12
+                ach = ib / (dom_avg / 1e3) / 1e12
+                ingest = {"bytes_per_launch": ib, "achieved_TBps": round(ach, 2),
+                          "ceiling_TBps": round(ceil_tbs, 2), "frac": round(ach / ceil_tbs, 3)}
         except Exception:
             traffic = None
 
@@ -454,7 +466,8 @@ def main():
                      "peak_basis": f"TF32 dense = 1/2 of bf16 {bf16} TF/s, {peak_src}",
                      "bf16x3_ceiling": round(bf16 / 3.0, 1),
                      "frac_of_bf16x3_ceiling": round(achieved / (bf16 / 3.0), 4),
-                     "work_per_launch_flops": layers[dl]["flops"]},
+                     "work_per_launch_flops": layers[dl]["flops"],
+                     "l2_to_sm_ingest": ingest},
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
     }
