@@ -155,7 +155,6 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
     int it = 0;
     for (int tile = blockIdx.x; tile < P.tiles; tile += gridDim.x) {
       const int64_t mbase = int64_t(tile / P.nt) * kBM;
-      const int n0 = (tile % P.nt) * BN;
       int ih0[RPT], iw0[RPT];
       int64_t pix0[RPT];
       bool rok[RPT];
@@ -422,57 +421,6 @@ __device__ __forceinline__ int phase_tap(int ph, int dh, int lo, int u, int pad,
   return t0 + u * jr;  // gather offset r'
 }
 
-// One block row per GEMM column (filter row `row`), threads along the packed
-// reduction index k: coalesced 16-bit stores, 32-bit index math only.
-__global__ void __launch_bounds__(256) pack_filter_kernel(PackGeom g, const float* __restrict__ f,
-                                                          __nv_bfloat16* __restrict__ hi,
-                                                          __nv_bfloat16* __restrict__ lo,
-                                                          uint32_t* __restrict__ ctab,
-                                                          uint32_t* __restrict__ coltab) {
-  const int row = blockIdx.y;
-  const int nS = g.dgrad ? g.winW : g.S;
-  int c_col = 0, ph = 0, pw = 0;
-  if (g.dgrad) {
-    const int phase = row / g.C;
-    c_col = row - phase * g.C;
-    ph = phase / g.v;
-    pw = phase - ph * g.v;
-  }
-  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < g.Ktot; k += gridDim.x * blockDim.x) {
-    const int ch = k >> 3, i = k & 7;
-    float val = 0.0f;
-    if (ch < g.KC) {
-      const int tap = ch / g.Cgrp, grp = ch - tap * g.Cgrp;
-      const int dh = tap / nS, dw = tap - dh * nS;
-      const int cin = grp * 8 + i;
-      if (row == 0 && i == 0)
-        ctab[ch] = (uint32_t(dh) << 24) | (uint32_t(dw) << 16) | uint32_t(grp * 8);
-      if (!g.dgrad) {
-        if (row < g.K && cin < g.C) val = fetch_filter(g, f, row, cin, dh, dw);
-      } else if (row < g.Ncol && cin < g.K) {
-        const int rp = phase_tap(ph, dh, g.lo_h, g.u, g.pad_h, g.R);
-        const int sp = phase_tap(pw, dw, g.lo_w, g.v, g.pad_w, g.S);
-        if (rp >= 0 && sp >= 0) val = fetch_filter(g, f, cin, c_col, rp, sp);
-      }
-    }
-    if (g.dgrad && k == 0 && row < g.Ncol) {
-      uint32_t e;
-      if (g.su * g.sv > 1) {  // space-to-depth column (rh, rw, c)
-        const int q = row / g.C0, c = row - q * g.C0;
-        e = (uint32_t(q / g.sv) << 24) | (uint32_t(q % g.sv) << 16) | uint32_t(c);
-      } else {
-        e = (uint32_t(ph) << 24) | (uint32_t(pw) << 16) | uint32_t(c_col);
-      }
-      coltab[row] = e;
-    }
-    __nv_bfloat16 h, l;
-    split_bf16(val, h, l);
-    const int64_t o = int64_t(row) * g.Ktot + k;
-    hi[o] = h;
-    lo[o] = l;
-  }
-}
-
 // Filter packing, one block per (GEMM column row, tap): the tap's gather
 // offsets (and the bwd-data phase taps) are resolved once per block, threads
 // walk the tap's Cpf reduction channels (coalesced 2-byte stores).  Block
@@ -539,7 +487,7 @@ __global__ void __launch_bounds__(128) pack_filter_tap_kernel(PackGeom g, const 
 
 // Scatter form of the filter packing: one thread per filter element (read
 // coalesced) computes its single position in the packed GEMM operand; the
-// padding is zeroed by a memset first.  Inverse of pack_filter_kernel's map:
+// padding is zeroed by a memset first.  Inverse of the tap kernel's map:
 // gather offset r' -> (space-to-depth tap r'/su, phase r'%su); for the
 // super-pixel bwd-data form t0 = r' % u, jr = r' / u, phase ph = (t0 - pad)
 // mod u and window tap dh = base(ph) - jr - lo.

@@ -1372,7 +1372,7 @@ cudaError_t pool_backward(const PoolProblem& pp, Dtype dt, const View4& dyv, con
   const size_t eb = dt == F32 ? 4 : 8;
   const size_t psm = ((size_t(dyv.h) * dyv.w * 4 + 15) & ~size_t(15)) + size_t(dyv.h) * dyv.w * eb +
                      (pp.kind == 0 ? size_t(dxv.h) * dxv.w * eb : 0);
-  if (psm <= 48 * 1024 && dxv.n * dxv.c < (int64_t(1) << 31) &&
+  if (psm <= 48 * 1024 && dxv.n * dxv.c < (int64_t(1) << 31) && !getenv("DNNP_POOL_BWD_DIRECT") &&
       dxv.h * dxv.w < (int64_t(1) << 31)) {
     tc::Workspace ws(st);
     cudaError_t e = ws.alloc(sizeof(int));
