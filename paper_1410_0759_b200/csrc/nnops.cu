@@ -968,10 +968,11 @@ __global__ void __launch_bounds__(256) pool_fwd_pipe_kernel(PoolGeom g, const T*
 // every window load and y store is a contiguous 32-channel run; the argmax
 // (logical NCHW index, stored in the dense [N][C][P][Q] buffer) goes
 // through a shared-memory transpose so its stores are q-contiguous.
-template <typename T>
+template <typename T, int KIND>
 __global__ void __launch_bounds__(256) pool_fwd_cl_kernel(PoolGeom g, const T* __restrict__ x,
                                                           T* __restrict__ y, int64_t* argmax,
-                                                          int kind, int nqb, int ncb) {
+                                                          int nqb, int ncb) {
+  constexpr int kind = KIND;
   __shared__ int64_t am[32][33];
   const int H = int(g.H), W = int(g.W), P = int(g.P), Q = int(g.Q), C = int(g.C);
   const int wh = int(g.wh), ww = int(g.ww);
@@ -981,13 +982,64 @@ __global__ void __launch_bounds__(256) pool_fwd_cl_kernel(PoolGeom g, const T* _
   const int qb = int(b % uint32_t(nqb));
   b /= uint32_t(nqb);
   const int p = int(b % uint32_t(P)), n = int(b / uint32_t(P));
-  const int lane = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 8 q rows per pass
+  const int lane = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 8 x 4 consecutive q
   const int c = cb * 32 + lane;
   const bool cok = c < C;
   const T* xb = x + int64_t(n) * g.x.sn + int64_t(cok ? c : 0) * g.x.sc;
   const int hs0 = p * int(g.sh) - int(g.ph);
   const int hs = max(0, hs0), he = min(H, hs0 + wh);
-  for (int qi = ty; qi < 32; qi += 8) {
+  // 3 x 3 / stride 2 (AlexNet pool): a thread takes 4 consecutive outputs
+  // whose windows overlap, issuing the 3 x 9 loads together (27 instead of
+  // 36), when the four windows are interior
+  if (KIND != 0 && wh == 3 && ww == 3 && g.sh == 2 && g.sw == 2 && hs0 >= 0 && hs0 + 3 <= H) {
+    const int q0 = qb * 32 + ty * 4;
+    const int ws0 = q0 * 2 - int(g.pw);
+    if (cok && q0 + 3 < Q && ws0 >= 0 && ws0 + 9 <= W) {
+      T v[3][9];
+#pragma unroll
+      for (int a = 0; a < 3; a++)
+#pragma unroll
+        for (int b = 0; b < 9; b++)
+          v[a][b] = xb[int64_t(hs0 + a) * g.x.sh + int64_t(ws0 + b) * g.x.sw];
+#pragma unroll
+      for (int k = 0; k < 4; k++) {
+        T out;
+        int64_t bi = 0;
+        if (kind == 0) {
+          T best = v[0][2 * k];
+          int bk = 0;
+#pragma unroll
+          for (int a = 0; a < 3; a++)
+#pragma unroll
+            for (int b = 0; b < 3; b++) {
+              if (a == 0 && b == 0) continue;
+              const T u = v[a][2 * k + b];
+              const bool take = u > best || (u != u && best == best);
+              best = take ? u : best;
+              bk = take ? a * 3 + b : bk;
+            }
+          out = best;
+          bi = ((int64_t(n) * C + c) * H + hs0 + bk / 3) * W + ws0 + 2 * k + bk % 3;
+        } else {
+          T sacc = T(0);
+#pragma unroll
+          for (int a = 0; a < 3; a++)
+#pragma unroll
+            for (int b = 0; b < 3; b++) sacc = dadd<T>(sacc, v[a][2 * k + b]);
+          out = sacc / T(9);
+        }
+        y[int64_t(n) * g.y.sn + int64_t(c) * g.y.sc + int64_t(p) * g.y.sh +
+          int64_t(q0 + k) * g.y.sw] = out;
+        am[lane][ty * 4 + k] = bi;
+      }
+      goto done;
+    }
+  }
+  // generic path: average pooling keeps the fast path's 4 consecutive
+  // outputs per thread; max pooling interleaves the warps over q (measured
+  // faster for it: neighbouring windows are read at the same time)
+  for (int k = 0; k < 4; k++) {
+    const int qi = kind != 0 ? ty * 4 + k : ty + 8 * k;
     const int q = qb * 32 + qi;
     if (q >= Q) break;
     const int ws0 = q * int(g.sw) - int(g.pw);
@@ -1018,6 +1070,7 @@ __global__ void __launch_bounds__(256) pool_fwd_cl_kernel(PoolGeom g, const T* _
     }
     am[lane][qi] = bi;
   }
+done:
   if (kind != 0 || !argmax) return;
   __syncthreads();
   // argmax rows: channel cb*32 + r, q-contiguous
@@ -1288,12 +1341,18 @@ cudaError_t pool_forward(const PoolProblem& pp, Dtype dt, const View4& xv, const
     const int nqb = int(ceil_div(pp.Q, 32)), ncb = int(ceil_div(xv.c, 32));
     const int64_t blocks = xv.n * pp.P * nqb * ncb;
     if (blocks < (int64_t(1) << 31)) {
-      if (dt == F32)
-        pool_fwd_cl_kernel<float><<<unsigned(blocks), 256, 0, st>>>(g, (const float*)x, (float*)y,
-                                                                    argmax, pp.kind, nqb, ncb);
-      else
-        pool_fwd_cl_kernel<double><<<unsigned(blocks), 256, 0, st>>>(
-            g, (const double*)x, (double*)y, argmax, pp.kind, nqb, ncb);
+      auto go = [&](auto tag, auto kc) {
+        using TT = decltype(tag);
+        pool_fwd_cl_kernel<TT, decltype(kc)::value><<<unsigned(blocks), 256, 0, st>>>(
+            g, (const TT*)x, (TT*)y, argmax, nqb, ncb);
+      };
+      using I0 = std::integral_constant<int, 0>;
+      using I1 = std::integral_constant<int, 1>;
+      if (dt == F32) {
+        if (pp.kind == 0) go(float(), I0()); else go(float(), I1());
+      } else {
+        if (pp.kind == 0) go(double(), I0()); else go(double(), I1());
+      }
       note_launch();
       return cudaGetLastError();
     }
