@@ -1360,7 +1360,10 @@ cudaError_t pool_forward(const PoolProblem& pp, Dtype dt, const View4& xv, const
   const bool dense_planes = xv.sw == 1 && xv.sh == xv.w;
   const int pitch = int(((xv.h * xv.w + 16 / eb) * eb + 15) / 16 * 16 / eb);
   const size_t ppipe = size_t(2) * pitch * eb;
-  if (dense_planes && ppipe <= 96 * 1024 && xv.n * xv.c < (int64_t(1) << 31) &&
+  // the cp.async pipeline pays for fp64 planes (max-pool 50 -> 61% of HBM);
+  // fp32 stays on the one-plane-per-block kernel (issue-bound either way,
+  // and faster on channel-slice views)
+  if (dt == F64 && dense_planes && ppipe <= 96 * 1024 && xv.n * xv.c < (int64_t(1) << 31) &&
       !getenv("DNNP_POOL_NO_PIPE") && !getenv("DNNP_POOL_DIRECT")) {
     const int kw = (pp.wh == pp.ww && (pp.wh == 2 || pp.wh == 3)) ? int(pp.wh) : 0;
     const int per_sm = std::max(1, int(std::min<size_t>(4, (200 * 1024) / ppipe)));
