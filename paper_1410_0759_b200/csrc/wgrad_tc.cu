@@ -657,8 +657,15 @@ cudaError_t wgrad_tma(const ConvProblem& p, const float* dy, const float* x, flo
   const int mt = mrows / (128 * nc), nt = ncols / bn;
   // pixels per stage: 64 (measured faster than 32 even where only two
   // 64-deep stages fit, e.g. conv2 BN=192: 202 vs 266 us)
-  int px = 64;
-  if (getenv("DNNP_WG_PX")) px = atoi(getenv("DNNP_WG_PX")) == 32 ? 32 : 64;
+  // 128 pixels per stage when each CTA holds <= 64 dy channels (conv1:
+  // 146 -> 126 us): the TMA engine spends ~200-280 cycles per box whatever
+  // its size up to 16 KB, so bigger boxes move more bytes per box; the
+  // 96 KB stages still double-buffer.  Wider dy tiles would leave one stage.
+  int px = bn / nc <= 64 ? 128 : 64;
+  if (const char* e = getenv("DNNP_WG_PX")) {
+    const int v = atoi(e);
+    px = v == 32 ? 32 : (v == 128 ? 128 : 64);
+  }
   const int64_t kblocks = ceil_div(NPQ, px);
   int64_t splits = std::max<int64_t>(1, int64_t(kNumSMs) / (int64_t(mt) * nt * nc));
   splits = std::min<int64_t>({splits, std::max<int64_t>(1, kblocks / 4), 256});
@@ -752,7 +759,9 @@ cudaError_t wgrad_tma(const ConvProblem& p, const float* dy, const float* x, flo
       default: return launch_wgrad_tma<256, 1, PX>(prm, grid, st);
     }
   };
-  e = px == 32 ? go(std::integral_constant<int, 32>()) : go(std::integral_constant<int, 64>());
+  e = px == 32    ? go(std::integral_constant<int, 32>())
+      : px == 128 ? go(std::integral_constant<int, 128>())
+                  : go(std::integral_constant<int, 64>());
   if (e != cudaSuccess) return e;
   if (want_trace) {
     static unsigned long long h[8192];
