@@ -433,8 +433,12 @@ static dnnp_status run_pipelined(cudaStream_t st, Stager& sg, std::vector<ChunkB
     if ((rs = sg.scratch(span_bytes(b.d), &b.dev))) return rs;
     total += span_bytes(b.d);
   }
+  // ~16 MB chunks (2..16 of them; more, smaller chunks measured slower:
+  // every chunk repeats the packing and GEMM launches, tools/e2e_probe.py)
   static const int64_t shift = getenv("DNNP_PIPE_SHIFT") ? atoll(getenv("DNNP_PIPE_SHIFT")) : 24;
-  const int64_t chunks = std::max<int64_t>(2, std::min<int64_t>({16, N, int64_t(total >> shift)}));
+  static const int64_t minc = getenv("DNNP_PIPE_MIN") ? atoll(getenv("DNNP_PIPE_MIN")) : 2;
+  const int64_t chunks =
+      std::max<int64_t>(std::min<int64_t>(minc, N), std::min<int64_t>({16, N, int64_t(total >> shift)}));
   const int64_t nb = (N + chunks - 1) / chunks;
   cudaStream_t ci, co;
   copy_streams(&ci, &co);

@@ -33,3 +33,26 @@ def main():
 
 if __name__ == "__main__":
     main()
+
+
+def multi():
+    """H2D split over k streams (do several copy engines help one direction?)."""
+    n = 512 * 1024 * 1024
+    h = torch.empty(n // 4, pin_memory=True)
+    d = torch.empty(n // 4, device="cuda")
+    for k in (1, 2, 4):
+        ss = [torch.cuda.Stream() for _ in range(k)]
+        part = (n // 4) // k
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(3):
+            for i, s in enumerate(ss):
+                with torch.cuda.stream(s):
+                    d[i * part:(i + 1) * part].copy_(h[i * part:(i + 1) * part], non_blocking=True)
+        torch.cuda.synchronize()
+        dt = (time.perf_counter() - t0) / 3
+        print(f"H2D over {k} streams: {n / dt / 1e9:.1f} GB/s", flush=True)
+
+
+if __name__ == "__main__" and len(__import__("sys").argv) > 1:
+    multi()
