@@ -485,6 +485,76 @@ __global__ void __launch_bounds__(128) pack_filter_tap_kernel(PackGeom g, const 
   }
 }
 
+// Forward filter packing, one block per GEMM column row (all taps): the
+// row's filter f[k][:][:][:] (contiguous C*R*S floats) is staged in shared
+// memory with coalesced loads, then each warp writes whole taps of the packed
+// row (lanes along the channels).  Coalesced, but only Np blocks: measured
+// slower than the per-(tap, row) kernel (8.3 vs ~5 us per AlexNet layer), so
+// it is opt-in (DNNP_PACK_ROWS).
+__global__ void __launch_bounds__(256) pack_filter_row_kernel(PackGeom g, const float* __restrict__ f,
+                                                              __nv_bfloat16* __restrict__ hi,
+                                                              __nv_bfloat16* __restrict__ lo,
+                                                              uint32_t* __restrict__ ctab,
+                                                              uint32_t* __restrict__ coltab, int taps) {
+  extern __shared__ float sf[];
+  const int row = blockIdx.x;
+  const int Cpf = g.Cgrp * 8;
+  const int64_t rbase = int64_t(row) * g.Ktot;
+  const int e = row / g.Ncol0, r0 = row - e * g.Ncol0;
+  const int nf = g.C0 * g.R0 * g.S0;
+  const bool live = row < g.Ncol && r0 < g.K;
+  if (live) {
+    const float* src = f + int64_t(r0) * nf;
+    for (int i = threadIdx.x; i < nf; i += blockDim.x) sf[i] = __ldg(src + i);
+  }
+  if (threadIdx.x == 0 && row < g.Ncol && g.bw > 1) {
+    const uint32_t eh = g.bdir ? uint32_t(e) : 0u, ew = g.bdir ? 0u : uint32_t(e);
+    coltab[row] = (eh << 24) | (ew << 16) | uint32_t(r0);
+  }
+  if (row == 0)
+    for (int i = threadIdx.x; i < taps * g.Cgrp; i += blockDim.x) {
+      const int tap = i / g.Cgrp, grp = i - tap * g.Cgrp;
+      ctab[i] = (uint32_t(tap / g.tapW) << 24) | (uint32_t(tap % g.tapW) << 16) | uint32_t(grp * 8);
+    }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int tap = warp; tap < taps; tap += nw) {
+    const int dhb = tap / g.tapW, dwb = tap - dhb * g.tapW;
+    const int dw = g.bdir ? dwb : dwb - e * g.vstep;
+    const int dh = g.bdir ? dhb - e * g.ustep : dhb;
+    const bool tap_ok = live && dw >= 0 && dw < g.Sg && dh >= 0 && dh < g.Rg;
+    for (int cin = lane; cin < Cpf; cin += 32) {
+      float val = 0.0f;
+      if (tap_ok && cin < g.C) {
+        // fetch_filter's map, reading the staged row
+        int c = cin, rh = 0, rw = 0;
+        if (g.su * g.sv > 1) {
+          const int ph = cin / g.C0;
+          c = cin - ph * g.C0;
+          rw = ph % g.sv;
+          rh = ph / g.sv;
+        }
+        int r = dh * g.su + rh, s2 = dw * g.sv + rw;
+        if (c < g.C0 && r < g.R0 && s2 < g.S0) {
+          if (g.flip) {
+            r = g.R0 - 1 - r;
+            s2 = g.S0 - 1 - s2;
+          }
+          val = sf[(c * g.R0 + r) * g.S0 + s2];
+        }
+      }
+      __nv_bfloat16 h, l;
+      split_bf16(val, h, l);
+      hi[rbase + tap * Cpf + cin] = h;
+      lo[rbase + tap * Cpf + cin] = l;
+    }
+  }
+  for (int k = taps * Cpf + threadIdx.x; k < g.Ktot; k += blockDim.x) {
+    hi[rbase + k] = __float2bfloat16_rn(0.0f);
+    lo[rbase + k] = __float2bfloat16_rn(0.0f);
+  }
+}
+
 // Scatter form of the filter packing: one thread per filter element (read
 // coalesced) computes its single position in the packed GEMM operand; the
 // padding is zeroed by a memset first.  Inverse of the tap kernel's map:
@@ -750,7 +820,12 @@ cudaError_t run_gemm(const ConvProblem& p, Gemm g, const __nv_bfloat16* a_hi,
   auto* b_lo = b_hi + flt;
   auto* ctab = reinterpret_cast<uint32_t*>(b_lo + flt);
   auto* coltab = ctab + pg.KC + 1;
-  if (!getenv("DNNP_PACK_SCATTER") || pg.bw > 1) {
+  const size_t frow = size_t(pg.C0) * pg.R0 * pg.S0 * sizeof(float);
+  // (row-staged variant: opt-in, measured slower -- Np blocks are too few)
+  if (!pg.dgrad && frow <= 48 * 1024 && getenv("DNNP_PACK_ROWS")) {
+    pack_filter_row_kernel<<<unsigned(pg.Np), 256, frow, st>>>(pg, f, b_hi, b_lo, ctab, coltab,
+                                                               taps);
+  } else if (!getenv("DNNP_PACK_SCATTER") || pg.bw > 1) {
     const dim3 fgrid(unsigned(taps + 1), unsigned(pg.Np));
     pack_filter_tap_kernel<<<fgrid, 128, 0, st>>>(pg, f, b_hi, b_lo, ctab, coltab, taps);
   } else {
