@@ -275,3 +275,12 @@ def test_wgrad_pairs_32_channel_dy_blocks(shape):
         check(run_case(shape, passes=("bwd_filter",), seed=17))
     with env(DNNP_WG_NO_BW32=1):
         check(run_case(shape, passes=("bwd_filter",), seed=17))
+
+
+def test_row_staged_filter_pack_variant():
+    """The opt-in row-staged forward filter pack (DNNP_PACK_ROWS) across the
+    plain, space-to-depth, folded and row-blocked forward geometries."""
+    with env(DNNP_PACK_ROWS=1):
+        for shape in [(2, 24, 11, 9, 40, 3, 3, 1, 1, 1, 1), (2, 3, 32, 36, 64, 11, 11, 4, 4, 2, 2),
+                      (2, 3, 17, 19, 24, 5, 7, 1, 1, 2, 3), (2, 32, 13, 13, 256, 3, 3, 1, 1, 1, 1)]:
+            check(run_case(shape, passes=("fwd",), seed=18))
