@@ -63,6 +63,7 @@ _SIGS = {
     "dnnp_conv_output_shape": [vp, vp, vp, c_i64p, c_i64p, c_i64p, c_i64p],
     "dnnp_convolution_forward": [vp, vp, vp, vp, vp, vp, vp, ctypes.c_int, vp, vp, vp],
     "dnnp_convolution_backward_data": [vp, vp, vp, vp, vp, vp, ctypes.c_int, vp, vp],
+    "dnnp_convolution_backward": [vp, vp, vp, vp, vp, vp, vp, vp, ctypes.c_int, vp, vp, vp, vp],
     "dnnp_get_convolution_workspace_size": [vp, ctypes.c_int, vp, vp, vp, vp, ctypes.c_int,
                                             ctypes.POINTER(ctypes.c_size_t)],
     "dnnp_convolution_forward_ex": [vp, vp, vp, vp, vp, vp, vp, ctypes.c_int, vp, vp, vp, vp,

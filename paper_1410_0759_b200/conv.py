@@ -303,6 +303,21 @@ def conv_backward_filter(dy: TensorView, x: TensorView, conv: ConvDesc, engine, 
         _ENGINE_CODE[engine], df.desc.c_desc(), df.ptr), "convolution_backward_filter")
 
 
+def conv_backward(dy: TensorView, f: FilterView, x: TensorView, conv: ConvDesc, engine,
+                  dx: TensorView, df: FilterView) -> None:
+    """Additive fused backward of one layer: dx and df in one call (dy packed
+    once for both tensor-core GEMMs); same results as conv_backward_data +
+    conv_backward_filter."""
+    engine = as_engine(engine)
+    out_shape = _check_triplet(x, f, conv)
+    _check_out(dy, out_shape, x.desc.dtype, "output gradient")
+    bind_stream(dy, f, x, dx, df)
+    _lib.check(_lib.lib().dnnp_convolution_backward(
+        _lib.handle(), f.desc.c_desc(), f.ptr, dy.desc.c_desc(), dy.ptr, x.desc.c_desc(), x.ptr,
+        conv.c_desc(), _ENGINE_CODE[engine], dx.desc.c_desc(), dx.ptr, df.desc.c_desc(), df.ptr),
+        "convolution_backward")
+
+
 def conv_backward_bias(dy: TensorView, db: TensorView | None = None) -> TensorView:
     """Per-output-map sum of dy, shape (1, K, 1, 1) (conv.py:754-760)."""
     d = dy.desc

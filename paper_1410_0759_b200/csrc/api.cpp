@@ -1018,6 +1018,59 @@ dnnp_status dnnp_convolution_backward_bias(dnnp_handle handle, dnnp_tensor_desc 
   return sg.finish(e);
 }
 
+// ------------------------------------------------ fused backward (additive)
+
+// dx and dw of one layer in one call (a training step's backward): the same
+// checks as dnnp_convolution_backward_data / _backward_filter; on the
+// tensor-core path dy is packed once for both GEMMs.
+dnnp_status dnnp_convolution_backward(dnnp_handle handle, dnnp_filter_desc fd, const void* f,
+                                      dnnp_tensor_desc dyd, const void* dy, dnnp_tensor_desc xd,
+                                      const void* x, dnnp_conv_desc cd, dnnp_engine engine,
+                                      dnnp_tensor_desc dxd, void* dx, dnnp_filter_desc dfd,
+                                      void* df) {
+  if (!reg_has(handle, KIND_HANDLE)) return fail(DNNP_STATUS_BAD_PARAM, "bad handle");
+  if (!filter_usable(fd, f) || !tensor_usable(dyd, dy) || !tensor_usable(xd, x) ||
+      !tensor_usable(dxd, dx) || !filter_usable(dfd, df))
+    return fail(DNNP_STATUS_BAD_PARAM, "convolution_backward: unusable descriptor or buffer");
+  if (!reg_has(cd, KIND_CONV) || !cd->configured)
+    return fail(DNNP_STATUS_BAD_PARAM, "conv descriptor not configured");
+  if (!engine_valid(engine)) return fail(DNNP_STATUS_BAD_PARAM, "bad engine");
+  dnnp_status st;
+  if ((st = bind_view(dyd, "dy")) || (st = bind_view(dxd, "dx")) || (st = bind_view(xd, "x")))
+    return st;
+  if (xd->n != dxd->n || xd->c != dxd->c || xd->h != dxd->h || xd->w != dxd->w ||
+      xd->elem != dxd->elem)
+    return fail(DNNP_STATUS_SHAPE_MISMATCH, "convolution_backward: x and dx differ in shape");
+  if (fd->k != dfd->k || fd->c != dfd->c || fd->r != dfd->r || fd->s != dfd->s ||
+      fd->elem != dfd->elem)
+    return fail(DNNP_STATUS_SHAPE_MISMATCH, "convolution_backward: w and dw differ in shape");
+  int64_t P, Q;
+  if ((st = conv_shape(xd, fd, cd, &P, &Q))) return st;
+  if ((st = check_out(dyd, xd->n, fd->k, P, Q, xd->elem, "output gradient"))) return st;
+  dnnp::ConvProblem pr = make_problem(xd, fd, cd, dyd, P, Q);
+  if ((st = check_decode_range(pr))) return st;
+  if ((st = need_device())) return st;
+  // dx must use dx's strides (same as x's here when the views agree)
+  dnnp::ConvProblem prd = pr;
+  prd.x = view_of(dxd);
+  if (prd.x.sn != pr.x.sn || prd.x.sc != pr.x.sc || prd.x.sh != pr.x.sh || prd.x.sw != pr.x.sw) {
+    // different x / dx layouts: the two plain calls
+    if ((st = dnnp_convolution_backward_data(handle, fd, f, dyd, dy, cd, engine, dxd, dx))) return st;
+    return dnnp_convolution_backward_filter(handle, xd, x, dyd, dy, cd, engine, dfd, df);
+  }
+  Stager sg(handle->stream);
+  void *dff, *ddy, *dxx, *ddx, *ddf;
+  size_t fbytes = size_t(fd->k * fd->c * fd->r * fd->s) * elem_size(fd->elem);
+  if ((st = sg.add(f, fbytes, false, true, &dff))) return st;
+  if ((st = sg.add(dy, span_bytes(dyd), false, true, &ddy))) return st;
+  if ((st = sg.add(x, span_bytes(xd), false, true, &dxx))) return st;
+  if ((st = sg.add(dx, span_bytes(dxd), true, cd->accumulate || !dense_view(dxd), &ddx))) return st;
+  if ((st = sg.add(df, fbytes, true, cd->accumulate != 0, &ddf))) return st;
+  cudaError_t e = dnnp::conv_backward_both(pr, dnnp::Dtype(xd->elem), ddy, dff, dxx, ddx, ddf,
+                                           cd->accumulate != 0, handle->math, handle->stream);
+  return sg.finish(e);
+}
+
 // ------------------------------------------------ workspace (additive)
 
 dnnp_status dnnp_convolution_forward_ex(dnnp_handle handle, const void* alpha,

@@ -571,6 +571,29 @@ cudaError_t conv_backward_filter(const ConvProblem& p, Dtype dt, const void* dy,
                    : simt_bwd_filter<double>(p, dy, x, df, accumulate, st);
 }
 
+cudaError_t conv_backward_both(const ConvProblem& p, Dtype dt, const void* dy, const void* f,
+                               const void* x, void* dx, void* df, bool accumulate, int math,
+                               cudaStream_t st) {
+  cudaError_t e;
+  const bool tcd = use_tc(p, dt, math, DGRAD, &e);
+  if (e != cudaSuccess) return e;
+  const bool tcw = use_tc(p, dt, math, WGRAD, &e);
+  if (e != cudaSuccess) return e;
+  // one dy pack serves both GEMMs when their packed widths agree (K % 64 == 0)
+  if (tcd && tcw && p.K % 64 == 0 && !getenv("DNNP_NO_SHARED_DY")) {
+    tc::ScratchScope* sc = tc::scratch_open(st);
+    e = tc::shared_dy_pack(sc, p.y, static_cast<const float*>(dy), int(p.K), st);
+    if (e == cudaSuccess) e = conv_backward_data(p, dt, dy, f, dx, accumulate, math, st);
+    if (e == cudaSuccess) e = conv_backward_filter(p, dt, dy, x, df, accumulate, math, st);
+    tc::shared_dy_clear();
+    tc::scratch_close(sc);
+    return e;
+  }
+  e = conv_backward_data(p, dt, dy, f, dx, accumulate, math, st);
+  if (e == cudaSuccess) e = conv_backward_filter(p, dt, dy, x, df, accumulate, math, st);
+  return e;
+}
+
 static bool same_strides(const View4& a, const View4& b) {
   return a.sn == b.sn && a.sc == b.sc && a.sh == b.sh && a.sw == b.sw;
 }

@@ -1329,6 +1329,12 @@ cudaError_t run_tc(bool dgrad, const ConvProblem& p, const float* in, const View
   }
   const size_t act = size_t(p.N) * IH * IW * Cp;
   Workspace ws(st);
+  {
+    // dy already packed by the fused backward entry (same view and width)
+    const __nv_bfloat16 *ph = nullptr, *pl = nullptr;
+    if (dgrad && !fold && packed_get(in, inv, Cp, &ph, &pl))
+      return run_gemm(p, g, ph, pl, IH, IW, Cp, f, out, outv, alpha, beta, epi, st);
+  }
   cudaError_t e = ws.alloc(act * 4 + 256);
   if (e != cudaSuccess) return e;
   auto* a_hi = static_cast<__nv_bfloat16*>(ws.p);

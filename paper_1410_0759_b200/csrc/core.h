@@ -56,6 +56,12 @@ void scratch_close(ScratchScope* s);
 void user_workspace_begin(void* base, size_t bytes);
 // ends the override; *need = the bytes the call asked for in total
 void user_workspace_end(size_t* need);
+// Fused backward: pack dy once into scratch from scope sc and register it
+// for the backward-data / backward-filter calls that follow on this thread;
+// shared_dy_clear() ends the registration.
+cudaError_t shared_dy_pack(ScratchScope* sc, const View4& v, const float* dy, int Cp,
+                           cudaStream_t st);
+void shared_dy_clear();
 // scratch footprint measurement of one call on stream st
 void scratch_measure_begin(cudaStream_t st);
 size_t scratch_measure_end(cudaStream_t st);
@@ -91,6 +97,11 @@ cudaError_t conv_forward_fused(const ConvProblem& p, Dtype dt, const void* x, co
 cudaError_t conv_backward_data_fused(const ConvProblem& p, Dtype dt, const void* dy,
                                      const void* f, void* dx, bool accumulate, int math,
                                      const ConvEpilogue& ep, cudaStream_t st);
+// Fused backward (additive): dx and df from one dy; on the tensor-core path
+// dy is packed once for both GEMMs.  Same results as the two calls.
+cudaError_t conv_backward_both(const ConvProblem& p, Dtype dt, const void* dy, const void* f,
+                               const void* x, void* dx, void* df, bool accumulate, int math,
+                               cudaStream_t st);
 // df := conv_bwd_filter(dy, x) (+ df if accumulate)
 cudaError_t conv_backward_filter(const ConvProblem& p, Dtype dt, const void* dy, const void* x,
                                  void* df, bool accumulate, int math, cudaStream_t st);

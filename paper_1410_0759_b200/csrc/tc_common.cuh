@@ -91,6 +91,15 @@ cudaError_t pack_act_fold(const View4& v, const float* x, int S, int vv, int pad
 // whether folding applies (and pays) for a problem; s2d takes precedence
 bool fold_taps(int64_t C, int64_t S, int64_t u, int64_t v, bool s2d);
 
+// Packed-operand reuse inside one fused call (thread local): the fused
+// backward entry packs dy once and registers it; backward-data and
+// backward-filter then take the registered planes instead of repacking.
+void packed_set(const float* src, const View4& v, int Cp, const __nv_bfloat16* hi,
+                const __nv_bfloat16* lo);
+bool packed_get(const float* src, const View4& v, int Cp, const __nv_bfloat16** hi,
+                const __nv_bfloat16** lo);
+void packed_clear();
+
 // Strided fp32 4-D view -> channel-innermost bf16 hi/lo planes
 // [n][h][w][Cp] (Cp = channels padded to a multiple of 8, zero filled).
 cudaError_t pack_act(const View4& v, const float* x, int Cp, __nv_bfloat16* hi, __nv_bfloat16* lo,

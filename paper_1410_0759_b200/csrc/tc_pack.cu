@@ -788,6 +788,48 @@ cudaError_t make_tmap_im2col(CUtensorMap* map, const void* base, const Im2colGeo
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
+struct PackedRef {
+  const float* src = nullptr;
+  View4 v{};
+  int Cp = 0;
+  const __nv_bfloat16* hi = nullptr;
+  const __nv_bfloat16* lo = nullptr;
+};
+static thread_local PackedRef g_packed;
+
+void packed_set(const float* src, const View4& v, int Cp, const __nv_bfloat16* hi,
+                const __nv_bfloat16* lo) {
+  g_packed = PackedRef{src, v, Cp, hi, lo};
+}
+
+bool packed_get(const float* src, const View4& v, int Cp, const __nv_bfloat16** hi,
+                const __nv_bfloat16** lo) {
+  const PackedRef& r = g_packed;
+  if (!r.src || r.src != src || r.Cp != Cp || r.v.n != v.n || r.v.c != v.c || r.v.h != v.h ||
+      r.v.w != v.w || r.v.sn != v.sn || r.v.sc != v.sc || r.v.sh != v.sh || r.v.sw != v.sw)
+    return false;
+  *hi = r.hi;
+  *lo = r.lo;
+  return true;
+}
+
+void packed_clear() { g_packed = PackedRef{}; }
+
+cudaError_t shared_dy_pack(ScratchScope* sc, const View4& v, const float* dy, int Cp,
+                           cudaStream_t st) {
+  const size_t elems = size_t(v.n) * v.h * v.w * Cp;
+  void* buf = nullptr;
+  cudaError_t e = scratch_alloc(sc, elems * 4, &buf);
+  if (e != cudaSuccess) return e;
+  auto* hi = static_cast<__nv_bfloat16*>(buf);
+  auto* lo = hi + elems;
+  if ((e = pack_act(v, dy, Cp, hi, lo, st)) != cudaSuccess) return e;
+  packed_set(dy, v, Cp, hi, lo);
+  return cudaSuccess;
+}
+
+void shared_dy_clear() { packed_clear(); }
+
 bool fold_taps(int64_t C, int64_t S, int64_t u, int64_t v, bool s2d) {
   if (s2d || getenv("DNNP_TC_NO_FOLD") || S < 2 || S * C > 64 || v > 8) return false;
   // reduction per vertical tap: folded S*C padded once vs C padded S times

@@ -682,7 +682,15 @@ cudaError_t wgrad_tma(const ConvProblem& p, const float* dy, const float* x, flo
   auto* x_hi = dy_lo + dy_elems;
   auto* x_lo = x_hi + x_elems;
   float* part = reinterpret_cast<float*>(x_lo + x_elems);
-  if ((e = pack_act(p.y, dy, Kp64, dy_hi, dy_lo, st)) != cudaSuccess) return e;
+  {
+    const __nv_bfloat16 *ph = nullptr, *pl = nullptr;
+    if (packed_get(dy, p.y, Kp64, &ph, &pl)) {  // packed once by the fused backward entry
+      dy_hi = const_cast<__nv_bfloat16*>(ph);
+      dy_lo = const_cast<__nv_bfloat16*>(pl);
+    } else if ((e = pack_act(p.y, dy, Kp64, dy_hi, dy_lo, st)) != cudaSuccess) {
+      return e;
+    }
+  }
   if (fold)
     e = pack_act_fold(p.x, x, int(p.S), int(p.v), int(p.pad_w), IW, Cp, x_hi, x_lo, st);
   else if (s2d)
