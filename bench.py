@@ -137,6 +137,15 @@ def build_views(dp, layers, torch, device):
         L["dfv"] = dp.FilterView(dp.make_filter_desc(k, c, r, r), L["df"])
 
 
+def run_step_fused(dp, layers, torch):
+    """The same step through the framework's fused backward entry (dx and dW
+    of a layer in one call, dy packed once) -- informational, not the
+    headline (which keeps the reference API's three calls per layer)."""
+    for L in layers:
+        dp.conv_forward(L["xv"], L["fv"], L["cd"], "implicit", L["yv"])
+        dp.conv_backward(L["dyv"], L["fv"], L["xv"], L["cd"], "implicit", L["dxv"], L["dfv"])
+
+
 def run_step(dp, layers, torch, events=None, allreduce=None):
     for li, L in enumerate(layers):
         ops = (
@@ -363,6 +372,34 @@ def main():
     for i, v in pre_kern.items():
         kern_ms.setdefault(i, v)
 
+    # the framework path: fused backward entry, replayed as a graph (N=1 only)
+    fused_ms = None
+    if graph is not None and hasattr(dp, "conv_backward"):
+        try:
+            run_step_fused(dp, layers, torch)
+            torch.cuda.synchronize()
+            cap2 = torch.cuda.Stream()
+            cap2.wait_stream(torch.cuda.current_stream())
+            g2 = torch.cuda.CUDAGraph()
+            with torch.cuda.stream(cap2):
+                with torch.cuda.graph(g2, stream=cap2):
+                    run_step_fused(dp, layers, torch)
+            torch.cuda.synchronize()
+            ts = []
+            for _ in range(max(3, args.steps)):
+                flush.fill_(1.0)
+                torch.cuda.synchronize()
+                f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                f0.record()
+                g2.replay()
+                f1.record()
+                torch.cuda.synchronize()
+                ts.append(f0.elapsed_time(f1))
+            fused_ms = float(np.median(ts))
+            del g2
+        except Exception:
+            fused_ms = None
+
     # eager submission of the same step, uninstrumented (for reference)
     eager_ms = []
     for _ in range(3):
@@ -447,6 +484,7 @@ def main():
                    "l2": "flushed (256 MiB write) between timed steps",
                    "submission": graph_note,
                    "eager_ms_per_step": round(float(np.median(eager_ms)), 4),
+                   "fused_backward_ms_per_step": (round(fused_ms, 4) if fused_ms else None),
                    "math": ["default(tcgen05 BF16x3 when eligible)", "simt_fp32",
                             "tcgen05_bf16x3"][args.math]},
         "pct_tf32_peak": round(100 * value / ws / tf32_peak, 2),
