@@ -389,9 +389,10 @@ struct PackGeom {
   // output columns, GEMM column = e * Ncol0 + n; the blocked taps along w
   // (tapW) map to the unblocked tap dw = dwb - e * vstep (valid in [0, Sg)).
   int tapH, tapW, bw, Ncol0, vstep, Sg;
-  // bdir = 1: the block runs down the output rows instead (forward only):
-  // blocked tap row dhb maps to dh = dhb - e * ustep (valid in [0, Rg))
-  int bdir, ustep, Rg;
+  // bdir = 1: the block runs down the output rows instead: blocked tap row
+  // dhb maps to dh = dhb - e * ustep (valid in [0, Rg)); bdir = 2: a 2-D
+  // block of bh rows x bw columns, e = eh * bw + ew
+  int bdir, ustep, Rg, bh;
 };
 
 __device__ __forceinline__ float fetch_filter(const PackGeom& g, const float* __restrict__ f,
@@ -442,8 +443,10 @@ __global__ void __launch_bounds__(128) pack_filter_tap_kernel(PackGeom g, const 
   }
   const int dhb = tap / g.tapW, dwb = tap - (tap / g.tapW) * g.tapW;
   const int e = row / g.Ncol0, r0 = row - e * g.Ncol0;  // column block, unblocked column
-  const int dw = g.bdir ? dwb : dwb - e * g.vstep;
-  const int dh = g.bdir ? dhb - e * g.ustep : dhb;
+  const int eh = g.bdir == 2 ? e / g.bw : (g.bdir ? e : 0);
+  const int ew = g.bdir == 2 ? e - eh * g.bw : (g.bdir ? 0 : e);
+  const int dw = dwb - ew * g.vstep;
+  const int dh = dhb - eh * g.ustep;
   const bool tap_ok = row < g.Ncol && dw >= 0 && dw < g.Sg && dh >= 0 && dh < g.Rg;
   int c_col = 0, rp = -1, sp = -1, ph = 0, pw = 0;
   if (g.dgrad && row < g.Ncol) {
@@ -455,18 +458,16 @@ __global__ void __launch_bounds__(128) pack_filter_tap_kernel(PackGeom g, const 
     sp = tap_ok ? phase_tap(pw, dw, g.lo_w, g.v, g.pad_w, g.S) : -1;
   }
   if (tap == 0 && threadIdx.x == 0 && row < g.Ncol && (g.dgrad || g.bw > 1)) {
-    uint32_t eh, ew, ec;
+    uint32_t oh_, ow_, oc_;
     if (!g.dgrad) {
-      eh = g.bdir ? uint32_t(e) : 0u, ew = g.bdir ? 0u : uint32_t(e), ec = uint32_t(r0);
+      oh_ = uint32_t(eh), ow_ = uint32_t(ew), oc_ = uint32_t(r0);
     } else if (g.su * g.sv > 1) {  // space-to-depth column (rh, rw, c)
       const int q = r0 / g.C0;
-      eh = uint32_t(q / g.sv), ew = uint32_t(e * g.sv + q % g.sv), ec = uint32_t(r0 - q * g.C0);
-    } else if (g.bdir) {
-      eh = uint32_t(e * g.u + ph), ew = uint32_t(pw), ec = uint32_t(c_col);
+      oh_ = uint32_t(q / g.sv), ow_ = uint32_t(e * g.sv + q % g.sv), oc_ = uint32_t(r0 - q * g.C0);
     } else {
-      eh = uint32_t(ph), ew = uint32_t(e * g.v + pw), ec = uint32_t(c_col);
+      oh_ = uint32_t(eh * g.u + ph), ow_ = uint32_t(ew * g.v + pw), oc_ = uint32_t(c_col);
     }
-    coltab[row] = (eh << 24) | (ew << 16) | ec;
+    coltab[row] = (oh_ << 24) | (ow_ << 16) | oc_;
   }
   if (row == 0)
     for (int grp = threadIdx.x; grp < g.Cgrp; grp += blockDim.x)
@@ -1243,6 +1244,7 @@ cudaError_t run_tc(bool dgrad, const ConvProblem& p, const float* in, const View
   pg.Sg = pg.tapW;
   pg.Rg = pg.tapH;
   pg.bdir = 0;
+  pg.bh = 1;
   pg.ustep = dgrad ? 1 : g.u;
   pg.bw = 1;
   pg.Ncol0 = pg.Ncol;
@@ -1302,7 +1304,21 @@ cudaError_t run_tc(bool dgrad, const ConvProblem& p, const float* in, const View
       gb.o_W = int(p.W);
       gb.o_ph = gb.o_pw = 0;
     }
-    if (tma_geometry_ok(gb, IH, IW, pb.tapH, pb.tapW, Nimg * gb.OH * gb.OW)) g = gb;
+    // very narrow unit-stride bwd-data (bw > 2): also 2 rows -> a 2 x bw
+    // block (N = 2 bw C; table2 layer1, C = 3)
+    if (dgrad && !s2d && bw > 2 && 2 * pb.Ncol <= 128 && !env_off("DNNP_TC_NO_2D")) {
+      Gemm g2 = gb;
+      PackGeom& p2 = g2.pg;
+      p2.bdir = 2;
+      p2.bh = 2;
+      p2.Ncol = 2 * pb.Ncol;
+      p2.tapH = pg.tapH + pg.ustep;
+      g2.OH = int(ceil_div(g.OH, 2));
+      g2.u = g.u * 2;
+      g2.o_u = 2;
+      if (tma_geometry_ok(g2, IH, IW, p2.tapH, p2.tapW, Nimg * g2.OH * g2.OW)) gb = g2;
+    }
+    if (tma_geometry_ok(gb, IH, IW, gb.pg.tapH, gb.pg.tapW, Nimg * gb.OH * gb.OW)) g = gb;
   } else if ((!dgrad || dgrad_rows) && g.tma && !fold && g.out_mode == 0 && pg.Ncol <= 64 &&
              !env_off("DNNP_TC_NO_VBLOCK")) {
     // Row blocking for narrow forward GEMMs (conv1: K = 64): one GEMM row

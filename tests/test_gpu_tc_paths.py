@@ -246,6 +246,8 @@ def test_wide_column_blocking(shape):
     check(run_case(shape, passes=("bwd_data",), accumulate=True, seed=15))
     with env(DNNP_TC_BW2=1):
         check(run_case(shape, passes=("bwd_data",), seed=15))
+    with env(DNNP_TC_NO_2D=1):  # columns only (the default adds 2 rows: a 2 x bw block)
+        check(run_case(shape, passes=("bwd_data",), seed=15))
 
 
 @pytest.mark.parametrize("shape", [(2, 3, 40, 44, 24, 11, 11, 1, 1, 0, 0),
