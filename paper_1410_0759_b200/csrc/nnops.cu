@@ -704,8 +704,10 @@ __global__ void __launch_bounds__(256) pool_fwd_kernel(PoolGeom g, const T* __re
 // Backward as a gather over the windows covering each input element, in
 // ascending (p, q) order starting from 0: this is exactly the summation
 // order of the reference's zero-fill + np.add.at / per-window += loops
-// (nnops.py:218-246), so max and average backward are bit-exact.
-template <typename T>
+// (nnops.py:218-246), so max and average backward are bit-exact.  CL walks
+// the elements channel-fastest (n, h, w, c) for channels-innermost views, so
+// dy reads and dx writes coalesce there.
+template <typename T, bool CL = false>
 __global__ void __launch_bounds__(256) pool_bwd_kernel(PoolGeom g, const T* __restrict__ dy,
                                                        T* __restrict__ dx,
                                                        const int64_t* __restrict__ argmax,
@@ -715,9 +717,15 @@ __global__ void __launch_bounds__(256) pool_bwd_kernel(PoolGeom g, const T* __re
   const uint32_t stride = gridDim.x * blockDim.x;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < uint32_t(total); i += stride) {
     uint32_t t, w, h, c, n;
-    mdivmod(i, g.dW, t, w);
-    mdivmod(t, g.dH, t, h);
-    mdivmod(t, g.dC, n, c);
+    if (CL) {
+      mdivmod(i, g.dC, t, c);
+      mdivmod(t, g.dW, t, w);
+      mdivmod(t, g.dH, n, h);
+    } else {
+      mdivmod(i, g.dW, t, w);
+      mdivmod(t, g.dH, t, h);
+      mdivmod(t, g.dC, n, c);
+    }
     // p covers h iff p*sh - ph <= h < p*sh - ph + wh
     const int hp = int(h) + int(g.ph), wp = int(w) + int(g.pw);
     const int p0 = hp - wh + 1 > 0 ? int(mdiv(uint32_t(hp - wh + sh), g.dSH)) : 0;
@@ -1171,9 +1179,24 @@ __global__ void __launch_bounds__(256) pool_bwd_plane_kernel(PoolGeom g, const T
   const int wh = int(g.wh), ww = int(g.ww), sh = int(g.sh), sw = int(g.sw);
   const int ph = int(g.ph), pw = int(g.pw);
   const int PQ = P * Q, HW = H * W;
-  int* as = reinterpret_cast<int*>(psm);  // max: plane-local argmax (h * W + w) or -1
-  T* ds = reinterpret_cast<T*>(psm + ((size_t(PQ) * 4 + 15) & ~size_t(15)));  // dy (avg: dy / count)
+  // covering-window ranges per input row / column, shared by every plane:
+  // rowtab[h] = (p0, p1), coltab[w] = (q0, q1)
+  int2* rowtab = reinterpret_cast<int2*>(psm);
+  int2* coltab = rowtab + H;
+  uint8_t* body = psm + ((size_t(H + W) * 8 + 15) & ~size_t(15));
+  int* as = reinterpret_cast<int*>(body);  // max: plane-local argmax (h * W + w) or -1
+  T* ds = reinterpret_cast<T*>(body + ((size_t(PQ) * 4 + 15) & ~size_t(15)));  // dy (avg: dy / count)
   T* xs = ds + PQ;                        // max: the dx plane being assembled
+  for (int i = threadIdx.x; i < H + W; i += blockDim.x) {
+    const bool row = i < H;
+    const int e = row ? i : i - H;
+    const int k = row ? wh : ww, s = row ? sh : sw, n = row ? P : Q;
+    const int ep = e + (row ? ph : pw);
+    const MagicDiv dv = row ? g.dSH : g.dSW;
+    const int lo = ep - k + 1 > 0 ? int(mdiv(uint32_t(ep - k + s), dv)) : 0;
+    const int hi = min(n - 1, int(mdiv(uint32_t(ep), dv)));
+    rowtab[i] = make_int2(lo, hi);
+  }
   const int planes = int(g.N) * C;
   for (int pl = blockIdx.x; pl < planes; pl += gridDim.x) {
     uint32_t nu, cu;
@@ -1181,15 +1204,34 @@ __global__ void __launch_bounds__(256) pool_bwd_plane_kernel(PoolGeom g, const T
     const T* dyb = dy + int64_t(nu) * g.y.sn + int64_t(cu) * g.y.sc;
     bool badl = false;
     const int64_t abase = int64_t(pl) * HW;
-    for (int i = threadIdx.x; i < PQ; i += blockDim.x) {
+    // staged in batches of LB per thread: all LB loads are issued before any
+    // is consumed, so one block keeps LB round trips in flight, not one
+    constexpr int LB = 4;
+    for (int i0 = threadIdx.x; i0 < PQ; i0 += LB * blockDim.x) {
+      T dv[LB];
+      int64_t av[LB];
+#pragma unroll
+      for (int u = 0; u < LB; u++) {
+        const int i = i0 + u * int(blockDim.x);
+        if (i < PQ) {
+          uint32_t pu, qu;
+          mdivmod(uint32_t(i), g.dQ, pu, qu);
+          dv[u] = dyb[int(pu) * g.y.sh + int(qu) * g.y.sw];
+          if (KIND == 0) av[u] = argmax[int64_t(pl) * PQ + i];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < LB; u++) {
+      const int i = i0 + u * int(blockDim.x);
+      if (i >= PQ) break;
       uint32_t pu, qu;
       mdivmod(uint32_t(i), g.dQ, pu, qu);
       const int p = int(pu), q = int(qu);
-      const T d = dyb[p * g.y.sh + q * g.y.sw];
+      const T d = dv[u];
       const int hs0 = p * sh - ph, ws0 = q * sw - pw;
       if (KIND == 0) {
         ds[i] = d;
-        const int64_t hw = argmax[int64_t(pl) * PQ + i] - abase;
+        const int64_t hw = av[u] - abase;
         int loc = -1;
         if (hw >= 0 && hw < int64_t(HW)) {
           uint32_t h, w;
@@ -1201,6 +1243,7 @@ __global__ void __launch_bounds__(256) pool_bwd_plane_kernel(PoolGeom g, const T
       } else {
         const int cnt = (min(H, hs0 + wh) - max(0, hs0)) * (min(W, ws0 + ww) - max(0, ws0));
         ds[i] = d / T(cnt);  // the reference adds dy / count per window (nnops.py:237-246)
+      }
       }
     }
     if (KIND == 0) {
@@ -1217,11 +1260,8 @@ __global__ void __launch_bounds__(256) pool_bwd_plane_kernel(PoolGeom g, const T
         if (t < 0) continue;
         uint32_t hu, wu;
         mdivmod(uint32_t(t), g.dW, hu, wu);
-        const int hp = int(hu) + ph, wp = int(wu) + pw;
-        const int p0 = hp - wh + 1 > 0 ? int(mdiv(uint32_t(hp - wh + sh), g.dSH)) : 0;
-        const int p1 = min(P - 1, int(mdiv(uint32_t(hp), g.dSH)));
-        const int q0 = wp - ww + 1 > 0 ? int(mdiv(uint32_t(wp - ww + sw), g.dSW)) : 0;
-        const int q1 = min(Q - 1, int(mdiv(uint32_t(wp), g.dSW)));
+        const int2 pr = rowtab[hu], qr = coltab[wu];
+        const int p0 = pr.x, p1 = pr.y, q0 = qr.x, q1 = qr.y;
         bool first = true;
         T acc = T(0);
         for (int p = p0; p <= p1; p++)
@@ -1248,11 +1288,8 @@ __global__ void __launch_bounds__(256) pool_bwd_plane_kernel(PoolGeom g, const T
       for (int i = threadIdx.x; i < HW; i += blockDim.x) {
         uint32_t hu, wu;
         mdivmod(uint32_t(i), g.dW, hu, wu);
-        const int hp = int(hu) + ph, wp = int(wu) + pw;
-        const int p0 = hp - wh + 1 > 0 ? int(mdiv(uint32_t(hp - wh + sh), g.dSH)) : 0;
-        const int p1 = min(P - 1, int(mdiv(uint32_t(hp), g.dSH)));
-        const int q0 = wp - ww + 1 > 0 ? int(mdiv(uint32_t(wp - ww + sw), g.dSW)) : 0;
-        const int q1 = min(Q - 1, int(mdiv(uint32_t(wp), g.dSW)));
+        const int2 pr = rowtab[hu], qr = coltab[wu];
+        const int p0 = pr.x, p1 = pr.y, q0 = qr.x, q1 = qr.y;
         T acc = T(0);
         if (MAXK > 0) {
 #pragma unroll
@@ -1266,6 +1303,112 @@ __global__ void __launch_bounds__(256) pool_bwd_plane_kernel(PoolGeom g, const T
         }
         dxb[int(hu) * g.x.sh + int(wu) * g.x.sw] = acc;
       }
+    }
+    __syncthreads();
+  }
+}
+
+// Channels-innermost backward: one (n, h) row of dx per block iteration.
+// The dy rows of the windows covering h (at most RM of them) are staged in
+// shared memory channel-fastest (avg: dy / count; max: dy plus the
+// plane-local argmax, validated -- an entry outside its window sets *bad and
+// the serial scatter redoes the op), then every (w, c) of the row sums its
+// covering windows in ascending (p, q) order from 0: the reference order
+// (nnops.py:218-246), so the result is bit-exact.  dy reads and dx writes
+// coalesce along c.
+// V channels per thread (one 16-byte vector when V > 1: needs C, every
+// non-channel stride and both base pointers in units of V).
+template <typename T, int V>
+struct alignas(V * sizeof(T)) ChanVec {
+  T v[V];
+};
+
+template <typename T, int KIND, int V>
+__global__ void __launch_bounds__(256) pool_bwd_cl_kernel(PoolGeom g, const T* __restrict__ dy,
+                                                          T* __restrict__ dx,
+                                                          const int64_t* __restrict__ argmax,
+                                                          int* bad, int RM, MagicDiv dQCV,
+                                                          MagicDiv dCV) {
+  using VT = ChanVec<T, V>;
+  extern __shared__ __align__(16) uint8_t psm[];
+  const int H = int(g.H), W = int(g.W), P = int(g.P), Q = int(g.Q), C = int(g.C);
+  const int wh = int(g.wh), ww = int(g.ww), sh = int(g.sh), sw = int(g.sw);
+  const int ph = int(g.ph), pw = int(g.pw);
+  const int CV = C / V, QCV = Q * CV;
+  int2* coltab = reinterpret_cast<int2*>(psm);
+  VT* ds = reinterpret_cast<VT*>(psm + ((size_t(W) * 8 + 15) & ~size_t(15)));
+  int* as = reinterpret_cast<int*>(ds + size_t(RM) * QCV);  // max: per channel, V per vector
+  for (int w = threadIdx.x; w < W; w += blockDim.x) {
+    const int wp = w + pw;
+    const int lo = wp - ww + 1 > 0 ? int(mdiv(uint32_t(wp - ww + sw), g.dSW)) : 0;
+    coltab[w] = make_int2(lo, min(Q - 1, int(mdiv(uint32_t(wp), g.dSW))));
+  }
+  const int rows = int(g.N) * H;
+  for (int row = blockIdx.x; row < rows; row += gridDim.x) {
+    uint32_t nu, hu;
+    mdivmod(uint32_t(row), g.dH, nu, hu);
+    const int n = int(nu), h = int(hu);
+    const int hp = h + ph;
+    const int p0 = hp - wh + 1 > 0 ? int(mdiv(uint32_t(hp - wh + sh), g.dSH)) : 0;
+    const int p1 = min(P - 1, int(mdiv(uint32_t(hp), g.dSH)));
+    const int nr = max(0, p1 - p0 + 1);
+    const T* dyn = dy + int64_t(n) * g.y.sn;
+    bool badl = false;
+    for (int i = threadIdx.x; i < nr * QCV; i += blockDim.x) {
+      uint32_t r, rem, q, cv;
+      mdivmod(uint32_t(i), dQCV, r, rem);
+      mdivmod(rem, dCV, q, cv);
+      const int p = p0 + int(r);
+      VT d = *reinterpret_cast<const VT*>(dyn + int64_t(cv) * V + p * g.y.sh + int(q) * g.y.sw);
+      const int hs0 = p * sh - ph, ws0 = int(q) * sw - pw;
+      if (KIND == 0) {
+        ds[i] = d;
+#pragma unroll
+        for (int j = 0; j < V; j++) {
+          const int64_t plane = int64_t(n) * C + int64_t(cv) * V + j;
+          const int64_t hw = argmax[(plane * P + p) * Q + q] - plane * H * W;
+          int loc = -1;
+          if (hw >= 0 && hw < int64_t(H) * W) {
+            uint32_t ah, aw;
+            mdivmod(uint32_t(hw), g.dW, ah, aw);
+            if (int(ah) >= hs0 && int(ah) < hs0 + wh && int(aw) >= ws0 && int(aw) < ws0 + ww)
+              loc = int(hw);
+          }
+          badl |= loc < 0;
+          as[i * V + j] = loc;
+        }
+      } else {
+        const int cnt = (min(H, hs0 + wh) - max(0, hs0)) * (min(W, ws0 + ww) - max(0, ws0));
+#pragma unroll
+        for (int j = 0; j < V; j++) d.v[j] = d.v[j] / T(cnt);
+        ds[i] = d;
+      }
+    }
+    if (KIND == 0 && badl) *bad = 1;
+    __syncthreads();
+    T* dxr = dx + int64_t(n) * g.x.sn + int64_t(h) * g.x.sh;
+    for (int e = threadIdx.x; e < W * CV; e += blockDim.x) {
+      uint32_t wu, cv;
+      mdivmod(uint32_t(e), dCV, wu, cv);
+      const int2 qr = coltab[wu];
+      const int me = h * W + int(wu);
+      VT acc;
+#pragma unroll
+      for (int j = 0; j < V; j++) acc.v[j] = T(0);
+      for (int r = 0; r < nr; r++)
+        for (int q = qr.x; q <= qr.y; q++) {
+          const int idx = r * QCV + q * CV + int(cv);
+          const VT d = ds[idx];
+#pragma unroll
+          for (int j = 0; j < V; j++) {
+            if (KIND == 0) {
+              if (as[idx * V + j] == me) acc.v[j] = dadd<T>(acc.v[j], d.v[j]);
+            } else {
+              acc.v[j] = dadd<T>(acc.v[j], d.v[j]);
+            }
+          }
+        }
+      *reinterpret_cast<VT*>(dxr + int64_t(cv) * V + int64_t(wu) * g.x.sw) = acc;
     }
     __syncthreads();
   }
@@ -1432,10 +1575,62 @@ cudaError_t pool_backward(const PoolProblem& pp, Dtype dt, const View4& dyv, con
   if (total >= (int64_t(1) << 32) || ptotal >= (int64_t(1) << 32)) return cudaErrorInvalidValue;
   PoolGeom g = pool_geom(pp, dxv, dyv);
   const size_t eb = dt == F32 ? 4 : 8;
-  const size_t psm = ((size_t(dyv.h) * dyv.w * 4 + 15) & ~size_t(15)) + size_t(dyv.h) * dyv.w * eb +
+  const size_t psm = ((size_t(dxv.h + dxv.w) * 8 + 15) & ~size_t(15)) +
+                     ((size_t(dyv.h) * dyv.w * 4 + 15) & ~size_t(15)) + size_t(dyv.h) * dyv.w * eb +
                      (pp.kind == 0 ? size_t(dxv.h) * dxv.w * eb : 0);
-  if (psm <= 48 * 1024 && dxv.n * dxv.c < (int64_t(1) << 31) && !getenv("DNNP_POOL_BWD_DIRECT") &&
-      dxv.h * dxv.w < (int64_t(1) << 31)) {
+  // channels innermost: the element-wise gather in (n, h, w, c) order (the
+  // plane kernel would read and write every plane at stride C)
+  const bool cl = dxv.sc == 1 && dyv.sc == 1 && dxv.c >= 16 && !getenv("DNNP_POOL_NO_CL");
+  const int rm = int(ceil_div(pp.wh, pp.sh));
+  const size_t clsm = ((size_t(dxv.w) * 8 + 15) & ~size_t(15)) +
+                      size_t(rm) * dyv.w * dyv.c * (eb + (pp.kind == 0 ? 4 : 0));
+  if (cl && clsm <= 48 * 1024 && dxv.n * dxv.h < (int64_t(1) << 31)) {
+    tc::Workspace ws(st);
+    cudaError_t e = ws.alloc(sizeof(int));
+    if (e != cudaSuccess) return e;
+    int* bad = static_cast<int*>(ws.p);
+    cudaMemsetAsync(bad, 0, sizeof(int), st);
+    const unsigned grid = unsigned(std::min<int64_t>(dxv.n * dxv.h, int64_t(1) << 30));
+    // 16-byte channel vectors when every non-channel stride, C and both
+    // base pointers allow it
+    const int vv = int(16 / eb);
+    const bool vec = !getenv("DNNP_POOL_NO_VEC") && dxv.c % vv == 0 &&
+                     dxv.sn % vv == 0 && dxv.sh % vv == 0 && dxv.sw % vv == 0 &&
+                     dyv.sn % vv == 0 && dyv.sh % vv == 0 && dyv.sw % vv == 0 &&
+                     (uintptr_t(dx) % 16) == 0 && (uintptr_t(dy) % 16) == 0;
+    const int cvn = vec ? int(dxv.c) / vv : int(dxv.c);
+    const MagicDiv dqcv = make_magic(uint32_t(dyv.w * cvn)), dcv = make_magic(uint32_t(cvn));
+    auto launch = [&](auto tag, auto kindc) {
+      using TT = decltype(tag);
+      constexpr int VV = int(16 / sizeof(TT));
+      if (vec)
+        pool_bwd_cl_kernel<TT, decltype(kindc)::value, VV><<<grid, 256, clsm, st>>>(
+            g, (const TT*)dy, (TT*)dx, argmax, bad, rm, dqcv, dcv);
+      else
+        pool_bwd_cl_kernel<TT, decltype(kindc)::value, 1><<<grid, 256, clsm, st>>>(
+            g, (const TT*)dy, (TT*)dx, argmax, bad, rm, dqcv, dcv);
+    };
+    using I0 = std::integral_constant<int, 0>;
+    using I1 = std::integral_constant<int, 1>;
+    if (dt == F32) {
+      if (pp.kind == 0) launch(float(), I0()); else launch(float(), I1());
+    } else {
+      if (pp.kind == 0) launch(double(), I0()); else launch(double(), I1());
+    }
+    note_launch();
+    if (pp.kind == 0) {
+      if (dt == F32)
+        pool_bwd_serial<float><<<1, 32, 0, st>>>(g, (const float*)dy, (float*)dx, argmax,
+                                                 ptotal, bad);
+      else
+        pool_bwd_serial<double><<<1, 32, 0, st>>>(g, (const double*)dy, (double*)dx, argmax,
+                                                  ptotal, bad);
+      note_launch();
+    }
+    return cudaGetLastError();
+  }
+  if (!cl && psm <= 48 * 1024 && dxv.n * dxv.c < (int64_t(1) << 31) &&
+      !getenv("DNNP_POOL_BWD_DIRECT") && dxv.h * dxv.w < (int64_t(1) << 31)) {
     tc::Workspace ws(st);
     cudaError_t e = ws.alloc(sizeof(int));
     if (e != cudaSuccess) return e;
@@ -1481,12 +1676,20 @@ cudaError_t pool_backward(const PoolProblem& pp, Dtype dt, const View4& dyv, con
     return cudaGetLastError();
   }
   unsigned grid = grid_for(total, 256, 8);
-  if (dt == F32)
+  if (cl) {
+    if (dt == F32)
+      pool_bwd_kernel<float, true><<<grid, 256, 0, st>>>(g, (const float*)dy, (float*)dx,
+                                                         argmax, pp.kind, total);
+    else
+      pool_bwd_kernel<double, true><<<grid, 256, 0, st>>>(g, (const double*)dy, (double*)dx,
+                                                          argmax, pp.kind, total);
+  } else if (dt == F32) {
     pool_bwd_kernel<float><<<grid, 256, 0, st>>>(g, (const float*)dy, (float*)dx, argmax,
                                                  pp.kind, total);
-  else
+  } else {
     pool_bwd_kernel<double><<<grid, 256, 0, st>>>(g, (const double*)dy, (double*)dx, argmax,
                                                   pp.kind, total);
+  }
   note_launch();
   if (pp.kind == 0) {
     tc::Workspace ws(st);

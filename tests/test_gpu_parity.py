@@ -267,6 +267,50 @@ def test_conv_random_vs_oracle(si, dt, math):
         assert orc.rel_err(to_host(dft), ref) <= tol(dt), ("wgrad", mode)
 
 
+POOL_SHAPES = [
+    # N C H W wh ww sh sw ph pw
+    (2, 24, 17, 15, 3, 3, 2, 2, 0, 0),    # AlexNet pool-like, channels past the NHWC threshold
+    (3, 16, 12, 13, 2, 3, 2, 1, 1, 1),    # padded, overlapping along w only
+    (2, 5, 11, 9, 3, 2, 1, 2, 1, 0),      # few channels (plane kernels in both layouts)
+    (1, 40, 9, 9, 4, 4, 3, 3, 2, 2),      # window > stride + 1, padding on both sides
+    (2, 18, 10, 10, 3, 3, 2, 2, 1, 1),    # NHWC without 16-byte channel vectors in fp32
+]
+
+
+@pytest.mark.parametrize("kind", ["max", "average"])
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+@pytest.mark.parametrize("layout", LAYOUTS)
+@pytest.mark.parametrize("si", range(len(POOL_SHAPES)))
+def test_pool_random_vs_oracle(si, layout, dt, kind):
+    """Pooling forward/backward on random NCHW and NHWC views against the C
+    oracle: argmax, max-pool outputs and both backward passes bit-exact."""
+    import torch
+    N, C, H, W, wh, ww, sh, sw, ph, pw = POOL_SHAPES[si]
+    rng = np.random.default_rng(3000 + si)
+    pd = dp.PoolingDesc(kind, wh, ww, sh, sw, ph, pw)
+    pg = [0 if kind == "max" else 1, wh, ww, sh, sw, ph, pw]
+    xv, x, xg, _ = _rand_view(rng, N, C, H, W, dt, layout, "cuda")
+    _, _, P, Q = dp.pool_out_shape(pd, xv)
+    yv, _, yg, yt = _rand_view(rng, N, C, P, Q, dt, layout, "cuda")
+    am = torch.full((N, C, P, Q), -1, dtype=torch.int64, device="cuda") if kind == "max" else None
+    dp.pool_forward(pd, xv, yv, am)
+    yref = np.zeros(yt.numel(), dtype=dt)
+    amref = np.full(N * C * P * Q, -1, dtype=np.int64)
+    orc.pool_forward(pg, xg, x, yg, yref, amref if kind == "max" else None)
+    ydev = to_host(yt)
+    if kind == "max":
+        assert np.array_equal(to_host(am).reshape(-1), amref)
+        assert np.array_equal(ydev, yref)
+    else:
+        assert orc.rel_err(ydev, yref) <= tol(dt) / 100
+    dyv, dy, dyg, _ = _rand_view(rng, N, C, P, Q, dt, layout, "cuda")
+    dxv, _, dxg, dxt = _rand_view(rng, N, C, H, W, dt, layout, "cuda")
+    dp.pool_backward(pd, yv, dyv, xv, dxv, am)
+    dxref = np.zeros(dxt.numel(), dtype=dt)
+    orc.pool_backward(pg, dyg, dy, dxg, dxref, amref if kind == "max" else None)
+    assert np.array_equal(to_host(dxt), dxref)
+
+
 def test_accumulate_and_beta_semantics():
     torch = torch_cuda()
     rng = np.random.default_rng(3)
