@@ -274,6 +274,7 @@ POOL_SHAPES = [
     (2, 5, 11, 9, 3, 2, 1, 2, 1, 0),      # few channels (plane kernels in both layouts)
     (1, 40, 9, 9, 4, 4, 3, 3, 2, 2),      # window > stride + 1, padding on both sides
     (2, 18, 10, 10, 3, 3, 2, 2, 1, 1),    # NHWC without 16-byte channel vectors in fp32
+    (2, 32, 29, 29, 3, 3, 2, 2, 0, 0),    # NHWC 3x3/2: fast and generic forward threads in one block
 ]
 
 
