@@ -1055,7 +1055,33 @@ __global__ void __launch_bounds__(256) pool_fwd_cl_kernel(PoolGeom g, const T* _
     T out = T(0);
     int64_t bi = 0;
     if (cok) {
-      if (kind == 0) {
+      if (kind == 0 && wh == 3 && ww == 3) {
+        // 3 x 3: all nine (predicated) loads issued before the first compare
+        // (113 -> 87 us on the section-8(d) NHWC shape)
+        T v[9];
+#pragma unroll
+        for (int a = 0; a < 3; a++)
+#pragma unroll
+          for (int b = 0; b < 3; b++) {
+            const int h = hs0 + a, w = ws0 + b;
+            const bool ok = h >= 0 && h < H && w >= 0 && w < W;
+            v[a * 3 + b] = ok ? xb[int64_t(h) * g.x.sh + int64_t(w) * g.x.sw] : T(0);
+          }
+        // first valid element seeds the scan (the reference's window order)
+        T best = T(0);
+        int bk = -1;
+#pragma unroll
+        for (int k9 = 0; k9 < 9; k9++) {
+          const int h = hs0 + k9 / 3, w = ws0 + k9 % 3;
+          const bool ok = h >= 0 && h < H && w >= 0 && w < W;
+          const T u = v[k9];
+          const bool take = ok && (bk < 0 || u > best || (u != u && best == best));
+          best = take ? u : best;
+          bk = take ? k9 : bk;
+        }
+        out = best;
+        bi = ((int64_t(n) * C + c) * H + hs0 + bk / 3) * W + ws0 + bk % 3;
+      } else if (kind == 0) {
         T best = xb[int64_t(hs) * g.x.sh + int64_t(ws) * g.x.sw];
         int bh = hs, bw = ws;
         for (int h = hs; h < he; h++)

@@ -312,6 +312,38 @@ def test_pool_random_vs_oracle(si, layout, dt, kind):
     assert np.array_equal(to_host(dxt), dxref)
 
 
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+@pytest.mark.parametrize("layout", LAYOUTS)
+@pytest.mark.parametrize("pad", [0, 1])
+def test_pool_max_ties_and_nan_vs_oracle(pad, layout, dt):
+    """Max pooling with many ties and scattered NaNs (first max / first NaN
+    in window scan order, nnops.py:157-200): argmax, y and dx bit-exact."""
+    import torch
+    N, C, H, W = 2, 32, 23, 21
+    rng = np.random.default_rng(4000 + pad)
+    pd = dp.PoolingDesc("max", 3, 3, 2, 2, pad, pad)
+    pg = [0, 3, 3, 2, 2, pad, pad]
+    xv, x, xg, xt = _rand_view(rng, N, C, H, W, dt, layout, "cuda")
+    x[:] = rng.integers(-2, 3, x.size).astype(dt)
+    x[rng.random(x.size) < 0.02] = np.nan
+    xt.copy_(torch.from_numpy(x))
+    _, _, P, Q = dp.pool_out_shape(pd, xv)
+    yv, _, yg, yt = _rand_view(rng, N, C, P, Q, dt, layout, "cuda")
+    am = torch.full((N, C, P, Q), -1, dtype=torch.int64, device="cuda")
+    dp.pool_forward(pd, xv, yv, am)
+    yref = np.zeros(yt.numel(), dtype=dt)
+    amref = np.full(N * C * P * Q, -1, dtype=np.int64)
+    orc.pool_forward(pg, xg, x, yg, yref, amref)
+    assert np.array_equal(to_host(am).reshape(-1), amref)
+    assert np.array_equal(to_host(yt), yref, equal_nan=True)
+    dyv, dy, dyg, _ = _rand_view(rng, N, C, P, Q, dt, layout, "cuda")
+    dxv, _, dxg, dxt = _rand_view(rng, N, C, H, W, dt, layout, "cuda")
+    dp.pool_backward(pd, yv, dyv, xv, dxv, am)
+    dxref = np.zeros(dxt.numel(), dtype=dt)
+    orc.pool_backward(pg, dyg, dy, dxg, dxref, amref)
+    assert np.array_equal(to_host(dxt), dxref)
+
+
 def test_accumulate_and_beta_semantics():
     torch = torch_cuda()
     rng = np.random.default_rng(3)
