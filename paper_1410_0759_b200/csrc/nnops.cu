@@ -525,6 +525,56 @@ __global__ void __launch_bounds__(256) softmax_img_apply(ImgGeom ga, const T* a,
   }
 }
 
+// Small groups (G <= 32 * PER, e.g. 1000 classes): one warp per image, the
+// whole group held in registers -- one read and one write per element and a
+// single launch instead of partial + apply.  Same operations as the two
+// kernels above (fmax / exp / divide; dsub / dmul for the backward).
+template <typename T, bool BWD, int PER>
+__global__ void __launch_bounds__(256) softmax_img_warp(ImgGeom ga, const T* a, ImgGeom gb,
+                                                       const T* b, ImgGeom go, T* o, int64_t G,
+                                                       int64_t nimg) {
+  const int lane = threadIdx.x & 31;
+  const int64_t n = int64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (n >= nimg) return;
+  T va[PER], vb[PER];
+#pragma unroll
+  for (int k = 0; k < PER; k++) {
+    const int64_t g = lane + 32 * k;
+    if (g < G) {
+      va[k] = a[img_off(ga, n, uint32_t(g))];
+      if (BWD) vb[k] = b[img_off(gb, n, uint32_t(g))];
+    }
+  }
+  if (!BWD) {
+    T m = T(-INFINITY);
+#pragma unroll
+    for (int k = 0; k < PER; k++)
+      if (lane + 32 * k < G) m = fmax(m, va[k]);
+    m = warp_max(m);
+    T sum = T(0);
+#pragma unroll
+    for (int k = 0; k < PER; k++)
+      if (lane + 32 * k < G) {
+        va[k] = exp(va[k] - m);
+        sum += va[k];
+      }
+    sum = warp_sum(sum);
+#pragma unroll
+    for (int k = 0; k < PER; k++)
+      if (lane + 32 * k < G) o[img_off(go, n, uint32_t(lane + 32 * k))] = va[k] / sum;
+  } else {
+    T d = T(0);
+#pragma unroll
+    for (int k = 0; k < PER; k++)
+      if (lane + 32 * k < G) d += va[k] * vb[k];
+    d = warp_sum(d);
+#pragma unroll
+    for (int k = 0; k < PER; k++)
+      if (lane + 32 * k < G)
+        o[img_off(go, n, uint32_t(lane + 32 * k))] = dmul<T>(va[k], dsub<T>(vb[k], d));
+  }
+}
+
 // per_spatial: one thread per (n, h, w) position, loop over channels.
 struct PosGeom {
   View4 v;
@@ -572,6 +622,21 @@ static cudaError_t softmax_t(int mode, const View4& av, const T* a, const View4*
                              const View4& ov, T* o, cudaStream_t st) {
   if (av.c * av.h * av.w >= (int64_t(1) << 32) || av.n * av.h * av.w >= (int64_t(1) << 32))
     return cudaErrorInvalidValue;
+  if (mode == 0 && av.c * av.h * av.w <= 1024 && !getenv("DNNP_SOFTMAX_NO_WARP")) {
+    const int64_t G = av.c * av.h * av.w;
+    const unsigned grid = unsigned(ceil_div(av.n, 8));
+    ImgGeom ga = img_geom(av), gb = img_geom(bv ? *bv : av), go = img_geom(ov);
+    auto go_per = [&](auto perc) {
+      softmax_img_warp<T, BWD, decltype(perc)::value><<<grid, 256, 0, st>>>(ga, a, gb, b, go, o,
+                                                                           G, av.n);
+    };
+    if (G <= 128) go_per(std::integral_constant<int, 4>());
+    else if (G <= 256) go_per(std::integral_constant<int, 8>());
+    else if (G <= 512) go_per(std::integral_constant<int, 16>());
+    else go_per(std::integral_constant<int, 32>());
+    note_launch();
+    return cudaGetLastError();
+  }
   if (mode == 0) {
     const int64_t G = av.c * av.h * av.w;
     // enough blocks to fill the GPU, at least ~2K elements per block
