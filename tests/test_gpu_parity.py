@@ -344,6 +344,37 @@ def test_pool_max_ties_and_nan_vs_oracle(pad, layout, dt):
     assert np.array_equal(to_host(dxt), dxref)
 
 
+SOFTMAX_SHAPES = [(5, 1000, 1, 1), (3, 10, 3, 3), (4, 7, 6, 6), (2, 3, 13, 13), (2, 5, 16, 16)]
+
+
+@pytest.mark.parametrize("mode", ["per_image", "per_spatial"])
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+@pytest.mark.parametrize("layout", LAYOUTS)
+@pytest.mark.parametrize("si", range(len(SOFTMAX_SHAPES)))
+def test_softmax_random_vs_oracle(si, layout, dt, mode):
+    """Softmax forward / backward against the C oracle across the group
+    sizes of every per-image kernel variant (warp-per-image 4..32 values per
+    lane, and the two-phase form past 1024 elements)."""
+    N, C, H, W = SOFTMAX_SHAPES[si]
+    rng = np.random.default_rng(5000 + si)
+    mcode = 0 if mode == "per_image" else 1
+    import torch
+    xv, x, xg, xt = _rand_view(rng, N, C, H, W, dt, layout, "cuda")
+    x *= 8
+    xt.copy_(torch.from_numpy(x))
+    yv, _, yg, yt = _rand_view(rng, N, C, H, W, dt, layout, "cuda")
+    dp.softmax_forward(mode, xv, yv)
+    yref = np.zeros(yt.numel(), dtype=dt)
+    orc.softmax_forward(mcode, xg, x, yg, yref)
+    assert orc.rel_err(to_host(yt), yref) <= tol(dt)
+    dyv, dy, dyg, _ = _rand_view(rng, N, C, H, W, dt, layout, "cuda")
+    dxv, _, dxg, dxt = _rand_view(rng, N, C, H, W, dt, layout, "cuda")
+    dp.softmax_backward(mode, yv, dyv, dxv)
+    dxref = np.zeros(dxt.numel(), dtype=dt)
+    orc.softmax_backward(mcode, yg, to_host(yt), dyg, dy, dxg, dxref)
+    assert orc.rel_err(to_host(dxt), dxref) <= tol(dt)
+
+
 def test_accumulate_and_beta_semantics():
     torch = torch_cuda()
     rng = np.random.default_rng(3)
