@@ -33,9 +33,13 @@ ALEXNET = [
     ("conv5", 256, 13, 256, 3, 1, 1),
 ]
 PASSES = ("fwd", "bwd_data", "bwd_filter")
+# ONE metric string for both arms (the driver pairs the lines by it); the %
+# of tensor peak is reported in roofline.frac / pct_tf32_peak, not here
+METRIC = "conv TFLOP/s fwd/bwd-data/bwd-filter (AlexNet conv1-5)"
 N_PER_GPU = 128
 REF_SAMPLE_N = 8      # --impl reference: images per timed step (bounded CPU sample)
 CPU_SAMPLE_N = 128    # cpu_baseline leg: the full N=128 workload once (~10-20 s)
+REF_BASE_N = 16       # cpu_baseline leg: real reference (direct engine) images per step
 
 
 def out_extent(h, r, u, pad):
@@ -165,13 +169,18 @@ def run_step(dp, layers, torch, events=None, allreduce=None):
         allreduce.__self__.wait()  # the step ends when every dW is reduced
 
 
-def cpu_baseline(threads, sample_n=2):
+def cpu_baseline(threads, sample_n=2, gpu_out=None):
     """The C oracle (restatement of the reference implicit engine) on host
-    cores, on a bounded sample of the same workload (N=sample_n per layer)."""
+    cores, on a bounded sample of the same workload (N=sample_n per layer).
+    gpu_out: {layer: (y, dx, df)} host copies of the GPU results for the same
+    inputs (sample_n must then be the GPU batch): returns the normalised
+    errors max|gpu - oracle| / max|oracle| per layer and pass as the third
+    value (the parity check of the benchmarked configuration itself)."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle as orc
     total_flops = 0
     dt = 0.0
+    errs = {}
     for idx, (name, c, h, k, r, u, pad) in enumerate(ALEXNET):
         n = sample_n
         p = out_extent(h, r, u, pad)
@@ -191,7 +200,86 @@ def cpu_baseline(threads, sample_n=2):
         orc.conv_backward_filter(xg, x, yg, dy, cg, [k, c, r, r], df, threads=threads)
         dt += time.perf_counter() - t0
         total_flops += 3 * layer_flops(n, c, h, k, r, u, pad)
-    return total_flops / dt / 1e12, dt
+        if gpu_out is not None and name in gpu_out:
+            for pas, got, ref in zip(PASSES, gpu_out[name], (y, dx, df)):
+                errs[f"{name}.{pas}"] = float(np.abs(got.astype(np.float64) - ref).max()
+                                             / max(float(np.abs(ref).max()), 1e-30))
+    return total_flops / dt / 1e12, dt, errs
+
+
+REF_LAYERS_SRC = os.path.join(ROOT, "baseline", "_ref")
+
+
+def ref_worker(engine, n, steps, warmup, threads):
+    """One arm of the real reference (baseline/_ref, the unmodified numpy
+    package through its public API: conv_forward / conv_backward_data /
+    conv_backward_filter, pkg/src/dnnp/conv.py:565-751) on AlexNet conv1-5
+    at N=n; prints per-step seconds as JSON.  Run in a subprocess so that
+    OPENBLAS_NUM_THREADS is fixed before numpy loads."""
+    sys.path.insert(0, REF_LAYERS_SRC)
+    from dnnp.conv import (ConvDesc, FilterView, conv_backward_data, conv_backward_filter,
+                           conv_forward)
+    from dnnp.tensor import TensorView, empty_view, make_desc
+    layers = []
+    for idx, (name, c, h, k, r, u, pad) in enumerate(ALEXNET):
+        p = out_extent(h, r, u, pad)
+        g = np.random.default_rng([2014, idx])  # reference bench.py:151-157
+        x = g.uniform(-0.5, 0.5, (n, c, h, h)).astype(np.float32)
+        f = g.uniform(-0.5, 0.5, (k, c, r, r)).astype(np.float32)
+        dy = g.uniform(-0.5, 0.5, (n, k, p, p)).astype(np.float32)
+        layers.append((ConvDesc(u, u, pad, pad), TensorView.from_array(x),
+                       FilterView.from_array(f), TensorView.from_array(dy),
+                       empty_view(make_desc(n, k, p, p)), empty_view(make_desc(n, c, h, h)),
+                       FilterView.from_array(np.zeros_like(f))))
+
+    def step():
+        for cd, xv, fv, dyv, yv, dxv, dfv in layers:
+            conv_forward(xv, fv, cd, engine, yv, threads=threads)
+            conv_backward_data(dyv, fv, cd, engine, dxv, threads=threads)
+            conv_backward_filter(dyv, xv, cd, engine, dfv, threads=threads)
+    for _ in range(warmup):
+        step()
+    ts = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        step()
+        ts.append(time.perf_counter() - t0)
+    print(json.dumps({"engine": engine, "n": n, "seconds": ts}))
+
+
+def run_reference_arm(engine, n, steps, warmup):
+    """Spawn ref_worker: implicit = the paper's algorithm with the
+    reference's own tile threads (--threads nproc, OPENBLAS_NUM_THREADS=1);
+    direct = the strongest reference CPU path (BLAS threads = nproc; the
+    direct engine ignores --threads, conv.py:575-576).  Returns
+    (TFLOP/s median, seconds per step median) or None if unavailable."""
+    if not os.path.isdir(os.path.join(REF_LAYERS_SRC, "dnnp")):
+        return None
+    nproc = os.cpu_count() or 1
+    env = dict(os.environ)
+    env["OPENBLAS_NUM_THREADS"] = "1" if engine == "implicit" else str(nproc)
+    env["OMP_NUM_THREADS"] = env["OPENBLAS_NUM_THREADS"]
+    threads = nproc if engine == "implicit" else 1
+    cmd = [sys.executable, os.path.abspath(__file__), "--ref-worker", engine, "--batch", str(n),
+           "--steps", str(steps), "--warmup", str(warmup), "--ref-threads", str(threads)]
+    try:
+        out = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=900)
+        rec = json.loads(out.stdout.strip().splitlines()[-1])
+    except Exception:
+        return None
+    sec = float(np.median(rec["seconds"]))
+    flops = 3 * sum(layer_flops(n, c, h, k, r, u, pad) for _, c, h, k, r, u, pad in ALEXNET)
+    return flops / sec / 1e12, sec
+
+
+def cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
 
 
 def dist_env():
@@ -202,33 +290,45 @@ def dist_env():
 
 
 def main_reference(args):
-    """--impl reference: the reference algorithm's CPU implementation (the C
-    oracle port; the reference is pure numpy and is not built here) on the
-    host cores, same metric/config, bounded sample per step."""
+    """--impl reference: the REAL reference (baseline/_ref, unmodified numpy
+    package) on the host cores, same metric/config, a bounded sample per
+    step: its direct engine (the strongest reference CPU path, BLAS over all
+    cores) is the line's value; the implicit engine (the paper's algorithm)
+    is reported beside it.  Falls back to the C oracle port only when
+    baseline/_ref is missing."""
     ws, rank, _ = dist_env()
     if rank != 0:
         return
-    threads = os.cpu_count() or 1
-    vals = []
-    for _ in range(min(args.warmup, 1)):
-        cpu_baseline(threads, sample_n=1)
-    for _ in range(args.steps):
-        v, dt = cpu_baseline(threads, sample_n=REF_SAMPLE_N)
-        vals.append((v, dt))
-    value = float(np.median([v for v, _ in vals]))
-    ms = float(np.median([dt for _, dt in vals])) * 1e3
-    sample = (f"AlexNet conv1-5 fwd+bwd_data+bwd_filter fp32 at N={REF_SAMPLE_N} per step (config N=128 "
-              "scaled; flops linear in N); C oracle restating the reference implicit engine, "
-              f"fwd/bwd-filter threaded over {threads} cores, bwd-data serial as the reference")
+    nproc = os.cpu_count() or 1
+    sample_n = args.ref_n
+    direct = run_reference_arm("direct", sample_n, args.steps, min(args.warmup, 1))
+    implicit = run_reference_arm("implicit", REF_SAMPLE_N, 1, 0) if direct else None
+    if direct is not None:
+        value, sec = direct
+        kind = "reference"
+        sample = (f"AlexNet conv1-5 fwd+bwd_data+bwd_filter fp32 at N={sample_n} per step "
+                  "(config N=128 scaled: flops linear in N); unmodified reference package "
+                  "(baseline/_ref) direct engine, OpenBLAS over all cores")
+    else:
+        vals = [cpu_baseline(nproc, sample_n=REF_SAMPLE_N)[:2] for _ in range(args.steps)]
+        value = float(np.median([v for v, _ in vals]))
+        sec = float(np.median([d for _, d in vals]))
+        kind = "port"
+        sample = (f"AlexNet conv1-5 at N={REF_SAMPLE_N}: C oracle restating the reference "
+                  "implicit engine (baseline/_ref missing)")
+    cb = {"value": value, "unit": "TFLOP/s", "cores": nproc, "kind": kind, "sample": sample,
+          "cpu_model": cpu_model()}
+    if implicit is not None:
+        cb["engines"] = {"direct": round(direct[0], 5), "implicit": round(implicit[0], 5),
+                         "implicit_sample_n": REF_SAMPLE_N}
     print(json.dumps({
-        "impl": "reference", "metric": "conv TFLOP/s fwd/bwd-data/bwd-filter (AlexNet conv1-5)",
+        "impl": "reference", "metric": METRIC,
         "value": value, "unit": "TFLOP/s", "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": "alexnet_conv1-5_fwd_bwdd_bwdf_N128_fp32_nchw",
-                   "sample_n": REF_SAMPLE_N},
-        "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": threads, "kind": "port",
-                         "sample": sample},
+                   "sample_n": sample_n},
+        "cpu_baseline": cb,
         "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }))
@@ -246,7 +346,13 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--batch", type=int, default=N_PER_GPU)
+    ap.add_argument("--ref-n", type=int, default=16,
+                    help="--impl reference: images per timed CPU step")
+    ap.add_argument("--ref-worker", default=None, help=argparse.SUPPRESS)
+    ap.add_argument("--ref-threads", type=int, default=1, help=argparse.SUPPRESS)
     args = ap.parse_args()
+    if args.ref_worker:
+        return ref_worker(args.ref_worker, args.batch, args.steps, args.warmup, args.ref_threads)
     if args.impl == "reference":
         return main_reference(args)
     args.warmup = max(args.warmup, 3)
@@ -413,6 +519,12 @@ def main():
         a1.record()
         torch.cuda.synchronize()
         eager_ms.append(a0.elapsed_time(a1))
+    # host copies of the last step's results (parity check in the cpu leg)
+    gpu_out = {}
+    if ws == 1 and not args.no_cpu:
+        for L in layers:
+            gpu_out[L["name"]] = (L["yv"].buf.cpu().numpy(), L["dxv"].buf.cpu().numpy(),
+                                  L["df"].cpu().numpy())
     if os.environ.get("DNNP_BENCH_DEBUG"):
         for (li, pi), v in op_ms.items():
             print(f"{layers[li]['name']}.{PASSES[pi]}: " + " ".join(f"{x:.3f}" for x in v),
@@ -472,7 +584,7 @@ def main():
         e2e = run_e2e(dp, layers, torch, device, ws, args, step_flops)
 
     line = {
-        "metric": "conv TFLOP/s fwd/bwd-data/bwd-filter (AlexNet conv1-5), % TF32 tensor peak",
+        "metric": METRIC,
         "value": round(value, 3), "unit": "TFLOP/s", "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(total_ms / args.steps, 4),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
@@ -513,13 +625,36 @@ def main():
         line["e2e"] = e2e
     if rank == 0 and ws == 1 and not args.no_cpu:
         threads = os.cpu_count() or 1
-        v, dt = cpu_baseline(threads, sample_n=CPU_SAMPLE_N)
-        line["cpu_baseline"] = {
-            "value": round(v, 5), "unit": "TFLOP/s", "cores": threads, "kind": "port",
-            "sample": f"AlexNet conv1-5 fwd+bwd_data+bwd_filter fp32 at N={CPU_SAMPLE_N} "
-                      f"({dt:.1f} s), C oracle restating the reference implicit engine: "
-                      f"fwd/bwd-filter tiles over {threads} threads, bwd-data serial (as "
-                      "conv.py:668-670)"}
+        # parity of the benchmarked step itself: the C oracle on the same
+        # N=128 inputs, compared with the GPU results of the last step
+        v, dt, perr = cpu_baseline(threads, sample_n=CPU_SAMPLE_N,
+                                   gpu_out=gpu_out if args.batch == CPU_SAMPLE_N else None)
+        if perr:
+            line["parity"] = {"vs": "C oracle (oracle/, pinned to reference golden vectors)",
+                              "metric": "max|gpu - oracle| / max|oracle| per layer and pass",
+                              "tolerance": 1e-4, "max": max(perr.values()),
+                              "pass": max(perr.values()) <= 1e-4,
+                              "errors": {k: float(f"{e:.3g}") for k, e in perr.items()}}
+        direct = run_reference_arm("direct", REF_BASE_N, 2, 1)
+        implicit = run_reference_arm("implicit", REF_SAMPLE_N, 1, 0) if direct else None
+        cb = {"unit": "TFLOP/s", "cores": threads, "cpu_model": cpu_model(),
+              "c_oracle_port": {"value": round(v, 5), "sample": (
+                  f"N={CPU_SAMPLE_N} ({dt:.1f} s): C restatement of the reference implicit "
+                  f"engine, fwd/bwd-filter tiles over {threads} threads, bwd-data serial "
+                  "(as conv.py:668-670)")}}
+        if direct is not None:
+            cb.update({"value": round(direct[0], 5), "kind": "reference",
+                       "sample": (f"AlexNet conv1-5 fwd+bwd_data+bwd_filter fp32 at "
+                                  f"N={REF_BASE_N} per step (flops linear in N): unmodified "
+                                  "reference package (baseline/_ref), direct engine, OpenBLAS "
+                                  f"over {threads} cores"),
+                       "engines": {"direct": round(direct[0], 5),
+                                   "implicit": round(implicit[0], 5) if implicit else None,
+                                   "implicit_sample_n": REF_SAMPLE_N}})
+        else:
+            cb.update({"value": round(v, 5), "kind": "port",
+                       "sample": cb["c_oracle_port"]["sample"]})
+        line["cpu_baseline"] = cb
     if ws > 1:
         dist.barrier()
         dist.destroy_process_group()

@@ -29,6 +29,9 @@ _SIGS = {
     "dnnp_status_string": [ctypes.c_int],
     "dnnp_last_error": [],
     "dnnp_kernel_launch_count": [],
+    "dnnp_reload_tuning": [],
+    "dnnp_magic_divider": [ctypes.c_uint32, ctypes.POINTER(ctypes.c_uint32),
+                           ctypes.POINTER(ctypes.c_uint32), ctypes.POINTER(ctypes.c_int)],
     "dnnp_kernel_timing": [ctypes.c_int],
     "dnnp_scratch_high_water": [ctypes.c_int],
     "dnnp_kernel_times": [ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_int), ctypes.c_int],
@@ -88,6 +91,7 @@ _SIGS = {
     "dnnp_add_broadcast": [vp, vp, vp, vp, vp, vp, vp],
 }
 _RESTYPES = {
+    "dnnp_reload_tuning": None,
     "dnnp_version": c_i64,
     "dnnp_status_string": ctypes.c_char_p,
     "dnnp_last_error": ctypes.c_char_p,
@@ -153,6 +157,19 @@ def get_math():
     v = ctypes.c_int()
     check(lib().dnnp_get_math(handle(), ctypes.byref(v)), "dnnp_get_math")
     return v.value
+
+
+def reload_tuning():
+    """Re-read the DNNP_* kernel-variant switches (cached by the library)."""
+    lib().dnnp_reload_tuning()
+
+
+def magic_divider(d):
+    """(multiplier, shift, add_indicator) of the kernels' index-decode divider."""
+    m, s, a = ctypes.c_uint32(), ctypes.c_uint32(), ctypes.c_int()
+    check(lib().dnnp_magic_divider(int(d), ctypes.byref(m), ctypes.byref(s), ctypes.byref(a)),
+          "dnnp_magic_divider")
+    return int(m.value), int(s.value), bool(a.value)
 
 
 def kernel_launch_count():

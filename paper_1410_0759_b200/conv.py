@@ -12,7 +12,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _lib
-from .errors import EmptyOutput, ShapeMismatch, ZeroExtent
+from .errors import AllocTooLarge, EmptyOutput, ShapeMismatch, ZeroExtent
 from .tensor import (TensorDesc, TensorView, _is_torch, as_dtype, bind_stream, buf_info,
                      elem_code, empty_view, make_desc, scalar_ptr)
 
@@ -222,6 +222,18 @@ def _check_out(out: TensorView, extents, dtype, what):
         raise ShapeMismatch(f"{what} element type {out.desc.dtype}, expected {dtype}")
 
 
+def _lowered_guard(engine, x_desc: TensorDesc, f_desc: FilterDesc, out_shape, max_bytes):
+    """The explicit engine's C R S x N P Q lowered matrix limit (reference
+    conv.py:507-511 / 615-618 / 701): AllocTooLarge above max_lowered_bytes
+    (the library itself refuses anything above the 4 GiB default)."""
+    if engine is not Engine.EXPLICIT:
+        return
+    n, _k, p, q = out_shape
+    need = x_desc.c * f_desc.r * f_desc.s * n * p * q * x_desc.dtype.itemsize
+    if need > max_bytes:
+        raise AllocTooLarge(f"lowered matrix needs {need} bytes, limit {max_bytes}")
+
+
 def _ws(workspace):
     """(pointer, bytes) of a caller workspace: a CUDA tensor (any dtype)."""
     return workspace.data_ptr(), workspace.numel() * workspace.element_size()
@@ -251,6 +263,7 @@ def conv_forward(x: TensorView, f: FilterView, conv: ConvDesc, engine, y: Tensor
     engine = as_engine(engine)
     out_shape = _check_triplet(x, f, conv)
     _check_out(y, out_shape, x.desc.dtype, "output")
+    _lowered_guard(engine, x.desc, f.desc, out_shape, max_lowered_bytes)
     bind_stream(x, f, y)
     a_keep, a = scalar_ptr(alpha, y.desc.dtype)
     b_keep, b = scalar_ptr(beta, y.desc.dtype)
@@ -272,6 +285,7 @@ def conv_backward_data(dy: TensorView, f: FilterView, conv: ConvDesc, engine, dx
     engine = as_engine(engine)
     out_shape = _check_triplet(dx, f, conv)
     _check_out(dy, out_shape, dx.desc.dtype, "output gradient")
+    _lowered_guard(engine, dx.desc, f.desc, out_shape, max_lowered_bytes)
     bind_stream(dy, f, dx)
     if workspace is not None:
         _lib.check(_lib.lib().dnnp_convolution_backward_data_ex(
@@ -291,6 +305,7 @@ def conv_backward_filter(dy: TensorView, x: TensorView, conv: ConvDesc, engine, 
     engine = as_engine(engine)
     out_shape = _check_triplet(x, df, conv)
     _check_out(dy, out_shape, x.desc.dtype, "output gradient")
+    _lowered_guard(engine, x.desc, df.desc, out_shape, max_lowered_bytes)
     bind_stream(dy, x, df)
     if workspace is not None:
         _lib.check(_lib.lib().dnnp_convolution_backward_filter_ex(

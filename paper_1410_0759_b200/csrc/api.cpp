@@ -12,6 +12,7 @@
 #include <cstdio>
 #include <cstring>
 #include <cstdlib>
+#include <deque>
 #include <map>
 #include <mutex>
 #include <new>
@@ -24,6 +25,35 @@
 #include "core.h"
 
 using dnnp::View4;
+
+// --------------------------------------------------------------- tuning
+
+namespace dnnp {
+namespace {
+std::mutex g_tune_mu;
+std::map<std::string, const char*> g_tune;  // name -> cached value (nullptr: unset)
+std::deque<std::string> g_tune_vals;        // grows only: returned pointers stay valid
+}  // namespace
+
+const char* tune_env(const char* name) {
+  std::lock_guard<std::mutex> g(g_tune_mu);
+  auto it = g_tune.find(name);
+  if (it != g_tune.end()) return it->second;
+  const char* v = getenv(name);
+  const char* keep = nullptr;
+  if (v) {
+    g_tune_vals.emplace_back(v);
+    keep = g_tune_vals.back().c_str();
+  }
+  g_tune.emplace(name, keep);
+  return keep;
+}
+
+void tune_reload() {
+  std::lock_guard<std::mutex> g(g_tune_mu);
+  g_tune.clear();
+}
+}  // namespace dnnp
 
 // --------------------------------------------------------------- objects
 
@@ -559,6 +589,22 @@ dnnp_status check_decode_range(const dnnp::ConvProblem& p) {
   return DNNP_STATUS_OK;
 }
 
+// The explicit engine materialises the C R S x N P Q lowered matrix (data
+// matrix forward / backward-filter, gradient matrix backward-data) and
+// refuses it above the reference's limit: AllocTooLarge -> ALLOC_FAILED
+// (conv.py:31, 507-511 lower_explicit, 615-618 backward-data, 701
+// backward-filter via lower_explicit).
+constexpr int64_t kLoweredLimit = int64_t(4) << 30;
+dnnp_status explicit_guard(const dnnp::ConvProblem& pr, dnnp_engine engine, dnnp_elem_type elem,
+                           const char* what) {
+  if (engine != DNNP_ENGINE_EXPLICIT) return DNNP_STATUS_OK;
+  const __int128 need = (__int128)pr.C * pr.R * pr.S * pr.N * pr.P * pr.Q * elem_size(elem);
+  if (need > kLoweredLimit)
+    return fail(DNNP_STATUS_ALLOC_FAILED, "explicit engine (%s): lowered matrix needs %lld bytes, limit %lld",
+                what, (long long)need, (long long)kLoweredLimit);
+  return DNNP_STATUS_OK;
+}
+
 }  // namespace
 
 // =================================================================== ABI
@@ -566,6 +612,20 @@ dnnp_status check_decode_range(const dnnp::ConvProblem& p) {
 extern "C" {
 
 int64_t dnnp_version(void) { return DNNP_VERSION; }
+
+void dnnp_reload_tuning(void) { dnnp::tune_reload(); }
+
+dnnp_status dnnp_magic_divider(uint32_t divisor, uint32_t* multiplier, uint32_t* shift,
+                               int* add_indicator) {
+  if (!multiplier || !shift || !add_indicator)
+    return fail(DNNP_STATUS_BAD_PARAM, "magic_divider: NULL out-pointer");
+  if (divisor < 1) return fail(DNNP_STATUS_BAD_PARAM, "magic_divider: divisor must be >= 1");
+  const dnnp::MagicDiv m = dnnp::make_magic(divisor);
+  *multiplier = m.mul;
+  *shift = m.shift;
+  *add_indicator = int(m.add);
+  return DNNP_STATUS_OK;
+}
 
 const char* dnnp_status_string(dnnp_status status) {
   switch (status) {
@@ -847,10 +907,7 @@ dnnp_status dnnp_convolution_forward(dnnp_handle handle, const void* alpha, dnnp
   dnnp::ConvProblem pr = make_problem(xd, fd, cd, yd, P, Q);
   pr.engine = int(engine);
   if ((st = check_decode_range(pr))) return st;
-  if (engine == DNNP_ENGINE_EXPLICIT &&
-      pr.C * pr.R * pr.S * pr.N * pr.P * pr.Q * int64_t(elem_size(xd->elem)) > (int64_t(4) << 30))
-    return fail(DNNP_STATUS_ALLOC_FAILED,  // AllocTooLarge (reference conv.py:31, 507-511)
-                "explicit engine: lowered data matrix exceeds the 4 GiB limit");
+  if ((st = explicit_guard(pr, engine, xd->elem, "forward"))) return st;
   if ((st = need_device())) return st;
   Stager sg(handle->stream);
   void *dx, *df, *dy;
@@ -904,6 +961,7 @@ dnnp_status dnnp_convolution_backward_data(dnnp_handle handle, dnnp_filter_desc 
   if ((st = check_out(dyd, dxd->n, fd->k, P, Q, dxd->elem, "output gradient"))) return st;
   dnnp::ConvProblem pr = make_problem(dxd, fd, cd, dyd, P, Q);
   if ((st = check_decode_range(pr))) return st;
+  if ((st = explicit_guard(pr, engine, dxd->elem, "backward_data"))) return st;
   if ((st = need_device())) return st;
   Stager sg(handle->stream);
   void *ddy, *dff, *ddx;
@@ -958,6 +1016,7 @@ dnnp_status dnnp_convolution_backward_filter(dnnp_handle handle, dnnp_tensor_des
   if ((st = check_out(dyd, xd->n, fd->k, P, Q, xd->elem, "output gradient"))) return st;
   dnnp::ConvProblem pr = make_problem(xd, fd, cd, dyd, P, Q);
   if ((st = check_decode_range(pr))) return st;
+  if ((st = explicit_guard(pr, engine, xd->elem, "backward_filter"))) return st;
   if ((st = need_device())) return st;
   Stager sg(handle->stream);
   void *dxx, *ddy, *ddf;
@@ -1049,6 +1108,7 @@ dnnp_status dnnp_convolution_backward(dnnp_handle handle, dnnp_filter_desc fd, c
   if ((st = check_out(dyd, xd->n, fd->k, P, Q, xd->elem, "output gradient"))) return st;
   dnnp::ConvProblem pr = make_problem(xd, fd, cd, dyd, P, Q);
   if ((st = check_decode_range(pr))) return st;
+  if ((st = explicit_guard(pr, engine, xd->elem, "backward"))) return st;
   if ((st = need_device())) return st;
   // dx must use dx's strides (same as x's here when the views agree)
   dnnp::ConvProblem prd = pr;
@@ -1113,9 +1173,12 @@ dnnp_status dnnp_convolution_backward_filter_ex(dnnp_handle handle, dnnp_tensor_
   return st;
 }
 
-// Exact device workspace of one pass: the pass runs once on zero-filled
-// device tensors of the descriptors' shapes and the scratch it takes is
-// measured (a setup-time query: it allocates those tensors temporarily).
+// Exact device workspace of one pass, without executing it: the pass is
+// planned exactly as a real call would plan it (same tile choice, same
+// scratch carve-outs), on fake device addresses, with its launches captured
+// into a CUDA graph that is discarded unlaunched.  The returned size includes
+// 1023 bytes of slack for the 1024-byte alignment the *_ex carve-out applies
+// to the caller's base pointer (0 stays 0: nothing is carved).
 dnnp_status dnnp_get_convolution_workspace_size(dnnp_handle handle, int pass,
                                                 dnnp_tensor_desc xd, dnnp_filter_desc fd,
                                                 dnnp_conv_desc cd, dnnp_tensor_desc yd,
@@ -1136,33 +1199,46 @@ dnnp_status dnnp_get_convolution_workspace_size(dnnp_handle handle, int pass,
   dnnp::ConvProblem pr = make_problem(xd, fd, cd, yd, P, Q);
   pr.engine = pass == 0 ? int(engine) : 2;
   if ((st = check_decode_range(pr))) return st;
+  if ((st = explicit_guard(pr, engine, xd->elem, "workspace query"))) return st;
   if ((st = need_device())) return st;
-  cudaStream_t s = handle->stream;
-  const size_t xb = span_bytes(xd), yb = span_bytes(yd);
-  const size_t fb = size_t(fd->k * fd->c * fd->r * fd->s) * elem_size(fd->elem);
-  void *dx = nullptr, *dy = nullptr, *df = nullptr;
-  cudaError_t e = cudaMallocAsync(&dx, xb, s);
-  if (e == cudaSuccess) e = cudaMallocAsync(&dy, yb, s);
-  if (e == cudaSuccess) e = cudaMallocAsync(&df, fb, s);
-  if (e == cudaSuccess) e = cudaMemsetAsync(dx, 0, xb, s);
-  if (e == cudaSuccess) e = cudaMemsetAsync(dy, 0, yb, s);
-  if (e == cudaSuccess) e = cudaMemsetAsync(df, 0, fb, s);
+  // one capture stream per device for queries (capture is thread-local)
+  static std::mutex qmu;
+  static std::map<int, cudaStream_t> qstreams;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaStream_t s = nullptr;
+  {
+    std::lock_guard<std::mutex> g(qmu);
+    cudaStream_t& q = qstreams[dev];
+    if (!q && cudaStreamCreateWithFlags(&q, cudaStreamNonBlocking) != cudaSuccess) q = nullptr;
+    s = q;
+  }
+  if (!s) return cuda_status(cudaErrorNotSupported, "get_convolution_workspace_size");
+  // fake, aligned operand addresses: the captured launches never run
+  void* const fx = reinterpret_cast<void*>(uintptr_t(1) << 42);
+  void* const fy = reinterpret_cast<void*>(uintptr_t(2) << 42);
+  void* const ff = reinterpret_cast<void*>(uintptr_t(3) << 42);
+  cudaError_t e = cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal);
+  size_t need = 0;
   if (e == cudaSuccess) {
-    dnnp::tc::scratch_measure_begin(s);
+    dnnp::tc::dry_run_begin();
     const dnnp::Dtype dt = dnnp::Dtype(xd->elem);
     if (pass == 0)
-      e = dnnp::conv_forward(pr, dt, dx, df, dy, 1.0, 0.0, handle->math, s);
+      e = dnnp::conv_forward(pr, dt, fx, ff, fy, 1.0, 0.0, handle->math, s);
     else if (pass == 1)
-      e = dnnp::conv_backward_data(pr, dt, dy, df, dx, false, handle->math, s);
+      e = dnnp::conv_backward_data(pr, dt, fy, ff, fx, false, handle->math, s);
     else
-      e = dnnp::conv_backward_filter(pr, dt, dy, dx, df, false, handle->math, s);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-    *bytes = dnnp::tc::scratch_measure_end(s);
+      e = dnnp::conv_backward_filter(pr, dt, fy, fx, ff, false, handle->math, s);
+    dnnp::tc::user_workspace_end(&need);
+    cudaGraph_t graph = nullptr;
+    const cudaError_t ce = cudaStreamEndCapture(s, &graph);
+    if (graph) cudaGraphDestroy(graph);
+    if (e == cudaSuccess) e = ce;
   }
-  for (void* p : {dx, dy, df})
-    if (p) cudaFreeAsync(p, s);
-  cudaStreamSynchronize(s);
-  return cuda_status(e, "get_convolution_workspace_size");
+  cudaGetLastError();
+  if (e != cudaSuccess) return cuda_status(e, "get_convolution_workspace_size");
+  *bytes = need ? need + 1023 : 0;
+  return DNNP_STATUS_OK;
 }
 
 // ------------------------------------------------ fused epilogues (additive)

@@ -398,7 +398,7 @@ static cudaError_t launch_simt_cfg(SimtArgs& a, cudaStream_t st) {
 
 template <typename T, int PASS>
 static cudaError_t launch_simt(SimtArgs& a, cudaStream_t st) {
-  if (PASS != WGRAD && a.Ncol <= 16 && a.M >= 4096 && !getenv("DNNP_SIMT_NO_NARROW"))
+  if (PASS != WGRAD && a.Ncol <= 16 && a.M >= 4096 && !::dnnp::tune_env("DNNP_SIMT_NO_NARROW"))
     return launch_simt_cfg<T, PASS, SimtNarrow<T>>(a, st);
   return launch_simt_cfg<T, PASS, SimtCfg<T>>(a, st);
 }
@@ -580,7 +580,7 @@ cudaError_t conv_backward_both(const ConvProblem& p, Dtype dt, const void* dy, c
   const bool tcw = use_tc(p, dt, math, WGRAD, &e);
   if (e != cudaSuccess) return e;
   // one dy pack serves both GEMMs when their packed widths agree (K % 64 == 0)
-  if (tcd && tcw && p.K % 64 == 0 && !getenv("DNNP_NO_SHARED_DY")) {
+  if (tcd && tcw && p.K % 64 == 0 && !::dnnp::tune_env("DNNP_NO_SHARED_DY")) {
     tc::ScratchScope* sc = tc::scratch_open(st);
     e = tc::shared_dy_pack(sc, p.y, static_cast<const float*>(dy), int(p.K), st);
     if (e == cudaSuccess) e = conv_backward_data(p, dt, dy, f, dx, accumulate, math, st);

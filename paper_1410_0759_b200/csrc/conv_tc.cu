@@ -672,7 +672,7 @@ cudaError_t launch_tma(const TmaParams& prm, cudaStream_t st) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  if (getenv("DNNP_TC_DIAG")) {
+  if (::dnnp::diag_env("DNNP_TC_DIAG")) {
     int ncl = -1;
     cudaError_t qe = cudaOccupancyMaxActiveClusters(&ncl, conv_tma_kernel<BN, CB, NC>, &cfg);
     fprintf(stderr, "DIAG conv_tma<%d,%d,%d> smem=%d grid=%d maxActiveClusters=%d (%s)\n", BN, CB, NC,
@@ -707,7 +707,7 @@ void pick_tile_tma(int64_t M, int ncol, int cb, int* bn_out, int* nc_out) {
   double best = 1e30;
   *bn_out = 256;
   *nc_out = 1;
-  const int max_nc = getenv("DNNP_TC_NO_PAIRS") ? 1 : 2;
+  const int max_nc = ::dnnp::tune_env("DNNP_TC_NO_PAIRS") ? 1 : 2;
   for (int nc = 1; nc <= max_nc; nc++) {
     for (int bn : cands) {
       if (bn >= 2 * ncol && bn > 64) continue;
@@ -788,7 +788,7 @@ int pick_cb(int Cp) {
 // every shape at the north_star 1e-4 bar.
 int reduction_segments(int nkb, int depth) {
   int64_t chain = 8192;
-  if (const char* e = getenv("DNNP_TC_CHAIN")) chain = std::max<int64_t>(atoll(e), depth);
+  if (const char* e = ::dnnp::tune_env("DNNP_TC_CHAIN")) chain = std::max<int64_t>(atoll(e), depth);
   const int per = int(std::max<int64_t>(1, chain / depth));
   return std::max(1, (nkb + per - 1) / per);
 }
@@ -810,8 +810,17 @@ cudaError_t run_gemm(const ConvProblem& p, Gemm g, const __nv_bfloat16* a_hi,
   const int64_t M = p.N * g.OH * g.OW;
   int bn = pick_bn(M, pg.Ncol), nc = 1;
   if (g.tma) pick_tile_tma(M, pg.Ncol, CB, &bn, &nc);
-  if (g.tma && getenv("DNNP_TC_NC")) nc = atoi(getenv("DNNP_TC_NC"));
-  if (g.tma && getenv("DNNP_TC_BN")) bn = atoi(getenv("DNNP_TC_BN"));
+  if (g.tma) {
+    // A/B overrides, accepted only for the instantiated tile shapes
+    if (const char* e = ::dnnp::tune_env("DNNP_TC_NC")) {
+      const int v = atoi(e);
+      if (v == 1 || v == 2) nc = v;
+    }
+    if (const char* e = ::dnnp::tune_env("DNNP_TC_BN")) {
+      const int v = atoi(e);
+      if (v == 64 || v == 128 || v == 192 || v == 256) bn = v;
+    }
+  }
   pg.Np = int(ceil_div(pg.Ncol, bn) * bn);
   const size_t flt = size_t(pg.Np) * pg.Ktot;
   Workspace ws(st);
@@ -823,14 +832,15 @@ cudaError_t run_gemm(const ConvProblem& p, Gemm g, const __nv_bfloat16* a_hi,
   auto* coltab = ctab + pg.KC + 1;
   const size_t frow = size_t(pg.C0) * pg.R0 * pg.S0 * sizeof(float);
   // (row-staged variant: opt-in, measured slower -- Np blocks are too few)
-  if (!pg.dgrad && frow <= 48 * 1024 && getenv("DNNP_PACK_ROWS")) {
+  if (!pg.dgrad && frow <= 48 * 1024 && ::dnnp::tune_env("DNNP_PACK_ROWS")) {
     pack_filter_row_kernel<<<unsigned(pg.Np), 256, frow, st>>>(pg, f, b_hi, b_lo, ctab, coltab,
                                                                taps);
-  } else if (!getenv("DNNP_PACK_SCATTER") || pg.bw > 1) {
+  } else if (!::dnnp::tune_env("DNNP_PACK_SCATTER") || pg.bw > 1) {
     const dim3 fgrid(unsigned(taps + 1), unsigned(pg.Np));
     pack_filter_tap_kernel<<<fgrid, 128, 0, st>>>(pg, f, b_hi, b_lo, ctab, coltab, taps);
   } else {
-    if ((e = cudaMemsetAsync(b_hi, 0, flt * 4, st)) != cudaSuccess) return e;  // hi and lo planes
+    if (!tc::dry_run() && (e = cudaMemsetAsync(b_hi, 0, flt * 4, st)) != cudaSuccess)
+      return e;  // hi and lo planes
     const int64_t nf = int64_t(pg.K) * pg.C0 * pg.R0 * pg.S0;
     pack_filter_scatter_kernel<<<grid_for(nf, 256, 8), 256, 0, st>>>(pg, f, b_hi, b_lo);
     note_launch();
@@ -904,8 +914,8 @@ cudaError_t run_gemm(const ConvProblem& p, Gemm g, const __nv_bfloat16* a_hi,
     prm.epi = epi;
     prm.dOHW = make_magic(uint32_t(g.OH * g.OW));
     prm.dOW = make_magic(uint32_t(g.OW));
-    prm.skip = getenv("DNNP_TC_SKIP") ? atoi(getenv("DNNP_TC_SKIP")) : 0;
-    prm.prefetch = getenv("DNNP_TC_PREFETCH") ? atoi(getenv("DNNP_TC_PREFETCH")) : 0;
+    prm.skip = ::dnnp::diag_env("DNNP_TC_SKIP") ? atoi(::dnnp::diag_env("DNNP_TC_SKIP")) : 0;
+    prm.prefetch = ::dnnp::diag_env("DNNP_TC_PREFETCH") ? atoi(::dnnp::diag_env("DNNP_TC_PREFETCH")) : 0;
     int nseg = reduction_segments(nkb, kTK);
     // a gated sum spread over segments cannot also add the caller's dx
     if (epi.gate >= 0 && nseg > 1 && beta != 0.0f) return cudaErrorNotSupported;
@@ -919,8 +929,8 @@ cudaError_t run_gemm(const ConvProblem& p, Gemm g, const __nv_bfloat16* a_hi,
       // enough (>= 32 k-blocks) to amortise the partial-tile fixup (measured:
       // conv3 bwd-data 88 -> 74 us, conv2 bwd-data 150 -> 144 us; neutral or
       // worse for short reductions, conv1 fwd 115 -> 121 us, tools/env_ab.py)
-      const bool sk_want = getenv("DNNP_TC_SK") ? true : nkb >= 32;
-      bool use_sk = nseg == 1 && sk_want && !getenv("DNNP_TC_NO_SK") && W >= 1 && R > 0 &&
+      const bool sk_want = ::dnnp::tune_env("DNNP_TC_SK") ? true : nkb >= 32;
+      bool use_sk = nseg == 1 && sk_want && !::dnnp::tune_env("DNNP_TC_NO_SK") && W >= 1 && R > 0 &&
                     double(R) / G < 0.85 && int64_t(R) * nkb < (int64_t(1) << 30);
       // Split-K for grids under half a wave (small minibatches, SURVEY
       // configs[2]): every tile is cut along the reduction into pieces of
@@ -928,7 +938,7 @@ cudaError_t run_gemm(const ConvProblem& p, Gemm g, const __nv_bfloat16* a_hi,
       // under the accumulation cap, the finisher adds pieces in IEEE fp32.
       {
         const int Gmax = kNumSMs / nc, per_cap = std::max(1, 8192 / kTK);
-        if (!use_sk && !getenv("DNNP_TC_NO_SPLIT") && T * 2 <= Gmax && nkb >= 8 &&
+        if (!use_sk && !::dnnp::tune_env("DNNP_TC_NO_SPLIT") && T * 2 <= Gmax && nkb >= 8 &&
             int64_t(T) * nkb < (int64_t(1) << 30)) {
           int Gs = int(std::min<int64_t>(Gmax, int64_t(T) * (nkb / 4)));
           const int64_t U = int64_t(T) * nkb;
@@ -955,7 +965,8 @@ cudaError_t run_gemm(const ConvProblem& p, Gemm g, const __nv_bfloat16* a_hi,
         if ((e = skw.alloc(part_bytes + cnt_bytes)) != cudaSuccess) return e;
         prm.skws = static_cast<float*>(skw.p);
         prm.skcnt = reinterpret_cast<int*>(static_cast<char*>(skw.p) + part_bytes);
-        if ((e = cudaMemsetAsync(prm.skcnt, 0, cnt_bytes, st)) != cudaSuccess) return e;
+        if (!tc::dry_run() && (e = cudaMemsetAsync(prm.skcnt, 0, cnt_bytes, st)) != cudaSuccess)
+          return e;
         prm.sk = 1;
         prm.W = W;
         prm.U = U;
@@ -963,7 +974,7 @@ cudaError_t run_gemm(const ConvProblem& p, Gemm g, const __nv_bfloat16* a_hi,
       }
     }
     static unsigned long long* tbuf = nullptr;
-    const bool want_trace = getenv("DNNP_TC_TRACE") != nullptr;
+    const bool want_trace = ::dnnp::diag_env("DNNP_TC_TRACE") != nullptr;
     if (want_trace && !tbuf) cudaMalloc(&tbuf, 8192 * sizeof(unsigned long long));
     if (want_trace) cudaMemsetAsync(tbuf, 0, 8192 * sizeof(unsigned long long), st);
     prm.trace = want_trace ? tbuf : nullptr;
@@ -1041,12 +1052,12 @@ cudaError_t run_gemm(const ConvProblem& p, Gemm g, const __nv_bfloat16* a_hi,
   prm.beta = beta;
   prm.plain = (alpha == 1.0f && beta == 0.0f && nkb > 0) ? 1 : 0;
   static unsigned long long* trace_buf = nullptr;
-  const bool want_trace = getenv("DNNP_TC_TRACE") != nullptr;
+  const bool want_trace = ::dnnp::diag_env("DNNP_TC_TRACE") != nullptr;
   if (want_trace && !trace_buf) cudaMalloc(&trace_buf, 8192 * sizeof(unsigned long long));
   if (want_trace) cudaMemsetAsync(trace_buf, 0, 8192 * sizeof(unsigned long long), st);
   prm.trace = want_trace ? trace_buf : nullptr;
-  prm.skip = getenv("DNNP_TC_SKIP") ? atoi(getenv("DNNP_TC_SKIP")) : 0;
-  prm.products = getenv("DNNP_TC_PRODUCTS") ? atoi(getenv("DNNP_TC_PRODUCTS")) : 3;
+  prm.skip = ::dnnp::diag_env("DNNP_TC_SKIP") ? atoi(::dnnp::diag_env("DNNP_TC_SKIP")) : 0;
+  prm.products = ::dnnp::diag_env("DNNP_TC_PRODUCTS") ? atoi(::dnnp::diag_env("DNNP_TC_PRODUCTS")) : 3;
   prm.dOHW = make_magic(uint32_t(g.OH * g.OW));
   prm.dOW = make_magic(uint32_t(g.OW));
   const int nseg = reduction_segments(nkb, kBK);
@@ -1098,7 +1109,7 @@ void phase_window(int u, int pad, int R, int* lo, int* win) {
   *win = mx - mn + 1;
 }
 
-bool env_off(const char* name) { return getenv(name) != nullptr; }
+bool env_off(const char* name) { return ::dnnp::tune_env(name) != nullptr; }
 
 cudaError_t run_tc(bool dgrad, const ConvProblem& p, const float* in, const View4& inv,
                    const float* f, float* out, const View4& outv, float alpha, float beta,
@@ -1326,7 +1337,7 @@ cudaError_t run_tc(bool dgrad, const ConvProblem& p, const float* in, const View
     // per output drop to (R + u) / 2R; unlike column blocking the epilogue
     // stores stay contiguous (lanes = consecutive output columns).
     int bh = 2;
-    if (const char* e = getenv("DNNP_TC_VBH")) bh = std::max(2, std::min(8, atoi(e)));
+    if (const char* e = ::dnnp::tune_env("DNNP_TC_VBH")) bh = std::max(2, std::min(8, atoi(e)));
     Gemm gb = g;
     PackGeom& pb = gb.pg;
     pb.bdir = 1;

@@ -40,7 +40,7 @@ struct ConvProblem {
 };
 
 namespace tc {
-// keep stream-ordered pool memory across synchronizations (release threshold max)
+// create the library's own stream-ordered memory pool on this device (bounded release threshold)
 void pool_keep_memory();
 // Scratch scope for host code (api.cpp): allocations come from the
 // per-stream arena (tc_common.cuh Workspace) and are released when the scope
@@ -56,6 +56,12 @@ void scratch_close(ScratchScope* s);
 void user_workspace_begin(void* base, size_t bytes);
 // ends the override; *need = the bytes the call asked for in total
 void user_workspace_end(size_t* need);
+// Workspace query without executing the pass: scratch is carved from a fake
+// base (high-water measured by user_workspace_end), the caller runs the pass
+// on a capturing stream so no kernel executes, and the few memsets of the
+// pass are skipped while dry_run() is true.
+void dry_run_begin();
+bool dry_run();
 // Fused backward: pack dy once into scratch from scope sc and register it
 // for the backward-data / backward-filter calls that follow on this thread;
 // shared_dy_clear() ends the registration.
@@ -66,6 +72,26 @@ void shared_dy_clear();
 void scratch_measure_begin(cudaStream_t st);
 size_t scratch_measure_end(cudaStream_t st);
 }  // namespace tc
+
+// Tuning switches (DNNP_* environment variables that force one kernel
+// variant for tests and A/B measurements; every default is chosen from the
+// problem shape).  The environment is read once and cached; the additive
+// dnnp_reload_tuning() re-reads it.  None of these changes what is computed
+// (only which correct kernel variant computes it): the diagnostic switches
+// that do (skipped loads / MMAs, single-product MMA, traces) exist only in
+// builds with -DDNNP_DIAG.
+const char* tune_env(const char* name);  // cached getenv
+void tune_reload();
+// Diagnostic switches (DNNP_TC_SKIP / _PRODUCTS / _TRACE / _DIAG / _PREFETCH):
+// compiled out of release builds, where they always read as unset.
+inline const char* diag_env(const char* name) {
+#ifdef DNNP_DIAG
+  return tune_env(name);
+#else
+  (void)name;
+  return nullptr;
+#endif
+}
 
 // Launch bookkeeping: every kernel this library launches bumps a counter
 // so benches/tests can prove native kernels ran.

@@ -19,7 +19,9 @@
 namespace dnnp {
 
 static std::atomic<long long> g_launches{0};
-void note_launch(int count) { g_launches += count; }
+void note_launch(int count) {
+  if (!tc::dry_run()) g_launches += count;  // a workspace query launches nothing
+}
 
 MagicDiv make_magic(uint32_t d) {
   // reference intdiv.py:74-101 (Hacker's Delight unsigned magic numbers)
@@ -622,7 +624,7 @@ static cudaError_t softmax_t(int mode, const View4& av, const T* a, const View4*
                              const View4& ov, T* o, cudaStream_t st) {
   if (av.c * av.h * av.w >= (int64_t(1) << 32) || av.n * av.h * av.w >= (int64_t(1) << 32))
     return cudaErrorInvalidValue;
-  if (mode == 0 && av.c * av.h * av.w <= 1024 && !getenv("DNNP_SOFTMAX_NO_WARP")) {
+  if (mode == 0 && av.c * av.h * av.w <= 1024 && !::dnnp::tune_env("DNNP_SOFTMAX_NO_WARP")) {
     const int64_t G = av.c * av.h * av.w;
     const unsigned grid = unsigned(ceil_div(av.n, 8));
     ImgGeom ga = img_geom(av), gb = img_geom(bv ? *bv : av), go = img_geom(ov);
@@ -1532,7 +1534,7 @@ __global__ void pool_bwd_serial(PoolGeom g, const T* dy, T* dx, const int64_t* a
 // flight, so one block's load phase overlaps another's compute phase.
 static int pool_threads() {
   static int t = [] {
-    const char* e = getenv("DNNP_POOL_THREADS");
+    const char* e = ::dnnp::tune_env("DNNP_POOL_THREADS");
     const int v = e ? atoi(e) : 128;
     return (v == 64 || v == 128 || v == 256) ? v : 128;
   }();
@@ -1540,7 +1542,7 @@ static int pool_threads() {
 }
 static int64_t pool_grid_cap() {
   static int64_t c = [] {
-    const char* e = getenv("DNNP_POOL_GRID");
+    const char* e = ::dnnp::tune_env("DNNP_POOL_GRID");
     return e ? int64_t(atoll(e)) : (int64_t(1) << 30);
   }();
   return c;
@@ -1570,7 +1572,7 @@ cudaError_t pool_forward(const PoolProblem& pp, Dtype dt, const View4& xv, const
   PoolGeom g = pool_geom(pp, xv, yv);
   const size_t eb = dt == F32 ? 4 : 8;
   const size_t psm = size_t(xv.h) * xv.w * eb;
-  if (xv.sc == 1 && yv.sc == 1 && xv.c >= 16 && !getenv("DNNP_POOL_NO_CL")) {
+  if (xv.sc == 1 && yv.sc == 1 && xv.c >= 16 && !::dnnp::tune_env("DNNP_POOL_NO_CL")) {
     // channels innermost: channel-vectorised rows instead of planes
     const int nqb = int(ceil_div(pp.Q, 32)), ncb = int(ceil_div(xv.c, 32));
     const int64_t blocks = xv.n * pp.P * nqb * ncb;
@@ -1598,7 +1600,7 @@ cudaError_t pool_forward(const PoolProblem& pp, Dtype dt, const View4& xv, const
   // fp32 stays on the one-plane-per-block kernel (issue-bound either way,
   // and faster on channel-slice views)
   if (dt == F64 && dense_planes && ppipe <= 96 * 1024 && xv.n * xv.c < (int64_t(1) << 31) &&
-      !getenv("DNNP_POOL_NO_PIPE") && !getenv("DNNP_POOL_DIRECT")) {
+      !::dnnp::tune_env("DNNP_POOL_NO_PIPE") && !::dnnp::tune_env("DNNP_POOL_DIRECT")) {
     const int kw = (pp.wh == pp.ww && (pp.wh == 2 || pp.wh == 3)) ? int(pp.wh) : 0;
     const int per_sm = std::max(1, int(std::min<size_t>(4, (200 * 1024) / ppipe)));
     const unsigned pg = unsigned(std::min<int64_t>(xv.n * xv.c, int64_t(kNumSMs) * per_sm));
@@ -1619,7 +1621,7 @@ cudaError_t pool_forward(const PoolProblem& pp, Dtype dt, const View4& xv, const
     note_launch();
     return cudaGetLastError();
   }
-  if (psm <= 48 * 1024 && xv.n * xv.c < (int64_t(1) << 31) && !getenv("DNNP_POOL_DIRECT")) {
+  if (psm <= 48 * 1024 && xv.n * xv.c < (int64_t(1) << 31) && !::dnnp::tune_env("DNNP_POOL_DIRECT")) {
     const int thr = pool_threads();
     const unsigned pg = unsigned(std::min<int64_t>(xv.n * xv.c, pool_grid_cap()));
     const int kw = (pp.wh == pp.ww && (pp.wh == 2 || pp.wh == 3)) ? int(pp.wh) : 0;
@@ -1671,7 +1673,7 @@ cudaError_t pool_backward(const PoolProblem& pp, Dtype dt, const View4& dyv, con
                      (pp.kind == 0 ? size_t(dxv.h) * dxv.w * eb : 0);
   // channels innermost: the element-wise gather in (n, h, w, c) order (the
   // plane kernel would read and write every plane at stride C)
-  const bool cl = dxv.sc == 1 && dyv.sc == 1 && dxv.c >= 16 && !getenv("DNNP_POOL_NO_CL");
+  const bool cl = dxv.sc == 1 && dyv.sc == 1 && dxv.c >= 16 && !::dnnp::tune_env("DNNP_POOL_NO_CL");
   const int rm = int(ceil_div(pp.wh, pp.sh));
   const size_t clsm = ((size_t(dxv.w) * 8 + 15) & ~size_t(15)) +
                       size_t(rm) * dyv.w * dyv.c * (eb + (pp.kind == 0 ? 4 : 0));
@@ -1685,7 +1687,7 @@ cudaError_t pool_backward(const PoolProblem& pp, Dtype dt, const View4& dyv, con
     // 16-byte channel vectors when every non-channel stride, C and both
     // base pointers allow it
     const int vv = int(16 / eb);
-    const bool vec = !getenv("DNNP_POOL_NO_VEC") && dxv.c % vv == 0 &&
+    const bool vec = !::dnnp::tune_env("DNNP_POOL_NO_VEC") && dxv.c % vv == 0 &&
                      dxv.sn % vv == 0 && dxv.sh % vv == 0 && dxv.sw % vv == 0 &&
                      dyv.sn % vv == 0 && dyv.sh % vv == 0 && dyv.sw % vv == 0 &&
                      (uintptr_t(dx) % 16) == 0 && (uintptr_t(dy) % 16) == 0;
@@ -1721,7 +1723,7 @@ cudaError_t pool_backward(const PoolProblem& pp, Dtype dt, const View4& dyv, con
     return cudaGetLastError();
   }
   if (!cl && psm <= 48 * 1024 && dxv.n * dxv.c < (int64_t(1) << 31) &&
-      !getenv("DNNP_POOL_BWD_DIRECT") && dxv.h * dxv.w < (int64_t(1) << 31)) {
+      !::dnnp::tune_env("DNNP_POOL_BWD_DIRECT") && dxv.h * dxv.w < (int64_t(1) << 31)) {
     tc::Workspace ws(st);
     cudaError_t e = ws.alloc(sizeof(int));
     if (e != cudaSuccess) return e;

@@ -40,7 +40,8 @@ struct Workspace {
   size_t fb_bytes_ = 0;
 };
 
-void pool_keep_memory();
+void pool_keep_memory();     // creates this device's library pool (lib_pool)
+cudaMemPool_t lib_pool();    // the library's stream-ordered pool on the current device
 
 // main-kernel timing hooks (no-ops unless dnnp_kernel_timing(1)); tags:
 // 1 conv TMA, 2 wgrad TMA, 3 conv cp.async, 4 wgrad cp.async

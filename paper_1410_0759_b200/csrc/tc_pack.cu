@@ -451,7 +451,7 @@ cudaError_t pack_act_s2d(const View4& v, const float* x, int u, int vv, int pad_
     const bool quad = (vv == 2 || vv == 4 || vv == 8) && v.sw == 1 && pad_w % 2 == 0 &&
                       v.w % 2 == 0 && v.sh % 2 == 0 && v.sc % 2 == 0 && v.sn % 2 == 0 &&
                       (reinterpret_cast<uintptr_t>(x) & 7) == 0 && sm <= 48 * 1024 &&
-                      v.n * H2 * nwb < (int64_t(1) << 31) && !getenv("DNNP_S2D_NO_QUAD");
+                      v.n * H2 * nwb < (int64_t(1) << 31) && !::dnnp::tune_env("DNNP_S2D_NO_QUAD");
     if (quad) {
       const unsigned grid = unsigned(v.n * H2 * nwb);
       const int threads = int(std::min<int64_t>(512, std::max<int64_t>(128, v.c * u * 32)));
@@ -476,7 +476,7 @@ cudaError_t pack_act_s2d(const View4& v, const float* x, int u, int vv, int pad_
     const bool dense = v.sw == 1 && v.sh == v.w && v.w % 4 == 0 && v.h * v.w <= v.sc &&
                        (reinterpret_cast<uintptr_t>(x) & 15) == 0 && (v.sn % 4) == 0 &&
                        (v.sc % 4) == 0 && sm <= 48 * 1024 && W2 * vv >= v.w + pad_w &&
-                       getenv("DNNP_S2D_DENSE") != nullptr;
+                       ::dnnp::tune_env("DNNP_S2D_DENSE") != nullptr;
     if (dense && v.n * H2 < (int64_t(1) << 31)) {
       pack_act_s2d_dense_kernel<<<unsigned(v.n * H2), 256, sm, st>>>(v, x, u, vv, pad_h, pad_w, H2,
                                                                      W2, Cp, hi, lo);
@@ -484,7 +484,7 @@ cudaError_t pack_act_s2d(const View4& v, const float* x, int u, int vv, int pad_
       return cudaGetLastError();
     }
   }
-  if (getenv("DNNP_S2D_TILE")) {
+  if (::dnnp::tune_env("DNNP_S2D_TILE")) {
     const int64_t jobs = ceil_div(npix, kPix) * ceil_div(Cp, kCh);
     if (jobs >= (int64_t(1) << 31)) return cudaErrorInvalidValue;
     const unsigned grid = unsigned(std::min<int64_t>(jobs, int64_t(kNumSMs) * 32));
@@ -495,7 +495,7 @@ cudaError_t pack_act_s2d(const View4& v, const float* x, int u, int vv, int pad_
     return cudaGetLastError();
   }
   const size_t row_smem = size_t(W2) * (Cp + 1) * sizeof(float);
-  if (getenv("DNNP_S2D_ROWS") && row_smem <= 48 * 1024 && v.n * H2 < (int64_t(1) << 31)) {
+  if (::dnnp::tune_env("DNNP_S2D_ROWS") && row_smem <= 48 * 1024 && v.n * H2 < (int64_t(1) << 31)) {
     const unsigned grid = unsigned(std::min<int64_t>(v.n * H2, int64_t(kNumSMs) * 8));
     pack_act_s2d_row_kernel<<<grid, 256, row_smem, st>>>(v, x, u, vv, pad_h, pad_w, H2, W2, Cp, hi,
                                                          lo);
@@ -539,8 +539,24 @@ struct UserWs {
   char* base = nullptr;
   size_t cap = 0, off = 0, high = 0;
   bool active = false;
+  bool dry = false;  // workspace query: carve-outs from a fake base, nothing runs
 };
 static thread_local UserWs g_uws;
+
+// Fake, 1024-aligned device address the dry run hands out: only ever
+// encoded into tensor maps and kernel parameters of a captured (never
+// launched) graph, never dereferenced.
+static char* const kDryBase = reinterpret_cast<char*>(uintptr_t(1) << 44);
+
+void dry_run_begin() {
+  g_uws = UserWs{};
+  g_uws.base = kDryBase;
+  g_uws.cap = ~size_t(0) >> 2;
+  g_uws.active = true;
+  g_uws.dry = true;
+}
+
+bool dry_run() { return g_uws.active && g_uws.dry; }
 
 void user_workspace_begin(void* base, size_t bytes) {
   g_uws.base = static_cast<char*>(base);
@@ -583,7 +599,7 @@ cudaError_t Workspace::alloc(size_t bytes) {
   fallback_ = true;
   fb_bytes_ = bytes;
   a_->fb += bytes;
-  return cudaMallocAsync(&p, bytes, st);
+  return cudaMallocFromPoolAsync(&p, bytes, lib_pool(), st);
 }
 
 Workspace::~Workspace() {
@@ -599,7 +615,7 @@ Workspace::~Workspace() {
   if (--a_->depth == 0 && a_->high > a_->cap) {
     if (a_->base) cudaFreeAsync(a_->base, st);
     const size_t ncap = a_->high + a_->high / 4;
-    if (cudaMallocAsync(&a_->base, ncap, st) == cudaSuccess) {
+    if (cudaMallocFromPoolAsync(&a_->base, ncap, lib_pool(), st) == cudaSuccess) {
       a_->cap = ncap;
     } else {
       cudaGetLastError();
@@ -698,18 +714,38 @@ void scratch_close(ScratchScope* s) {
   delete s;
 }
 
-void pool_keep_memory() {
-  static bool done = false;
-  if (done) return;
-  done = true;
+// The library's own stream-ordered pool per device (the process' default
+// pool is left alone, so torch's caching allocator and the host application
+// see their memory returned): freed scratch above kPoolKeep bytes goes back
+// to the device at the next synchronisation; the grow-only arenas are live
+// allocations of this pool and are not affected.
+constexpr uint64_t kPoolKeep = uint64_t(256) << 20;
+
+cudaMemPool_t lib_pool() {
+  static std::mutex mu;
+  static std::map<int, cudaMemPool_t> pools;
   int dev = 0;
   cudaGetDevice(&dev);
-  cudaMemPool_t pool;
-  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-    uint64_t thr = UINT64_MAX;
+  std::lock_guard<std::mutex> g(mu);
+  auto it = pools.find(dev);
+  if (it != pools.end()) return it->second;
+  cudaMemPool_t pool = nullptr;
+  cudaMemPoolProps props{};
+  props.allocType = cudaMemAllocationTypePinned;
+  props.location.type = cudaMemLocationTypeDevice;
+  props.location.id = dev;
+  if (cudaMemPoolCreate(&pool, &props) == cudaSuccess) {
+    uint64_t thr = kPoolKeep;
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  } else {
+    cudaGetLastError();
+    cudaDeviceGetDefaultMemPool(&pool, dev);  // untouched attributes
   }
+  pools[dev] = pool;
+  return pool;
 }
+
+void pool_keep_memory() { (void)lib_pool(); }
 
 cudaError_t make_tmap_2d(CUtensorMap* map, const void* base, uint64_t cols, uint64_t rows,
                          uint64_t pitch_elems, uint32_t box_cols, uint32_t box_rows,
@@ -831,7 +867,7 @@ cudaError_t shared_dy_pack(ScratchScope* sc, const View4& v, const float* dy, in
 void shared_dy_clear() { packed_clear(); }
 
 bool fold_taps(int64_t C, int64_t S, int64_t u, int64_t v, bool s2d) {
-  if (s2d || getenv("DNNP_TC_NO_FOLD") || S < 2 || S * C > 64 || v > 8) return false;
+  if (s2d || ::dnnp::tune_env("DNNP_TC_NO_FOLD") || S < 2 || S * C > 64 || v > 8) return false;
   // reduction per vertical tap: folded S*C padded once vs C padded S times
   const int64_t folded = ceil_div(S * C, 16) * 16, plain = S * ceil_div(C, 16) * 16;
   return folded * 4 <= plain * 3;
@@ -858,7 +894,7 @@ cudaError_t pack_act(const View4& v, const float* x, int Cp, __nv_bfloat16* hi, 
     note_launch();
     return cudaGetLastError();
   }
-  const int pj = getenv("DNNP_PACK_PIX") ? atoi(getenv("DNNP_PACK_PIX")) : 64;
+  const int pj = ::dnnp::tune_env("DNNP_PACK_PIX") ? atoi(::dnnp::tune_env("DNNP_PACK_PIX")) : 64;
   if (pj == 64 || pj == 128) {
     const int64_t jobs = ceil_div(npix, int64_t(pj)) * ceil_div(Cp, kCh);
     if (jobs >= (int64_t(1) << 31)) return cudaErrorInvalidValue;

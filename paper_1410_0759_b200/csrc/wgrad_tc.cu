@@ -339,7 +339,7 @@ struct WgTmaParams {
 // ~10%, tools/wg_chain.py).
 static int64_t max_chain(int px) {
   int64_t c = 16384;
-  if (const char* e = getenv("DNNP_WG_CHAIN")) c = std::max<int64_t>(atoll(e), px);
+  if (const char* e = ::dnnp::tune_env("DNNP_WG_CHAIN")) c = std::max<int64_t>(atoll(e), px);
   return c / px * px;
 }
 
@@ -607,8 +607,8 @@ cudaError_t launch_wgrad_tma(const WgTmaParams& prm, dim3 grid, cudaStream_t st)
 // geometry does not fit the im2col tensor map (caller falls back).
 cudaError_t wgrad_tma(const ConvProblem& p, const float* dy, const float* x, float* df, bool acc,
                       cudaStream_t st) {
-  if (getenv("DNNP_TC_NO_TMA")) return cudaErrorNotSupported;
-  const bool s2d = !getenv("DNNP_TC_NO_S2D") && (p.u > 1 || p.v > 1) && p.u <= 8 && p.v <= 8 &&
+  if (::dnnp::tune_env("DNNP_TC_NO_TMA")) return cudaErrorNotSupported;
+  const bool s2d = !::dnnp::tune_env("DNNP_TC_NO_S2D") && (p.u > 1 || p.v > 1) && p.u <= 8 && p.v <= 8 &&
                    p.C * p.u * p.v <= 64;
   // horizontal tap folding (stride-1-style few-channel layers): the S taps
   // as channels, the reduce maps folded channel j*C + c back to s = j
@@ -637,17 +637,23 @@ cudaError_t wgrad_tma(const ConvProblem& p, const float* dy, const float* x, flo
   // the dy columns are whole 64-channel blocks
   const int Kp64 = int(ceil_div(p.K, 64) * 64);
   int bn = Kp64 <= 256 ? Kp64 : (Kp64 % 256 == 0 ? 256 : (Kp64 % 192 == 0 ? 192 : 128));
-  if (getenv("DNNP_TC_BN")) bn = atoi(getenv("DNNP_TC_BN"));
+  if (const char* e = ::dnnp::tune_env("DNNP_TC_BN")) {
+    const int v = atoi(e);  // only the instantiated column tiles
+    if (v == 64 || v == 128 || v == 192 || v == 256) bn = v;
+  }
   // CTA pairs split the dy columns in halves: 64-channel blocks (128-byte
   // swizzle) when bn / 2 is a multiple of 64, else 32-channel blocks (64-byte
   // swizzle) for bn = 192 (conv2 122.9 vs 137.2 us, conv3 67.6 vs 73.9 us);
   // bn = 64 keeps single CTAs (conv1: the 256-row pair tiles pad 576 x-columns
   // to 768, 178 vs 147 us; DNNP_WG_BW32_64 forces the pair)
-  int nc = (bn % 128 == 0 || (bn == 192 && !getenv("DNNP_WG_NO_BW32")) ||
-            (bn == 64 && getenv("DNNP_WG_BW32_64")))
+  int nc = (bn % 128 == 0 || (bn == 192 && !::dnnp::tune_env("DNNP_WG_NO_BW32")) ||
+            (bn == 64 && ::dnnp::tune_env("DNNP_WG_BW32_64")))
                ? 2
                : 1;
-  if (getenv("DNNP_TC_NC")) nc = atoi(getenv("DNNP_TC_NC"));
+  if (const char* e = ::dnnp::tune_env("DNNP_TC_NC")) {
+    const int v = atoi(e);
+    if (v == 1 || v == 2) nc = v;
+  }
   if (nc == 2 && bn % 64) nc = 1;
   if (nc == 2 && bn % 128 && bn != 64 && bn != 192) nc = 1;
   const bool bw32 = nc == 2 && bn % 128 != 0;
@@ -662,7 +668,7 @@ cudaError_t wgrad_tma(const ConvProblem& p, const float* dy, const float* x, flo
   // its size up to 16 KB, so bigger boxes move more bytes per box; the
   // 96 KB stages still double-buffer.  Wider dy tiles would leave one stage.
   int px = bn / nc <= 64 ? 128 : 64;
-  if (const char* e = getenv("DNNP_WG_PX")) {
+  if (const char* e = ::dnnp::tune_env("DNNP_WG_PX")) {
     const int v = atoi(e);
     px = v == 32 ? 32 : (v == 128 ? 128 : 64);
   }
@@ -741,7 +747,7 @@ cudaError_t wgrad_tma(const ConvProblem& p, const float* dy, const float* x, flo
   prm.dPQ = make_magic(uint32_t(p.P * p.Q));
   prm.dQ = make_magic(uint32_t(p.Q));
   static unsigned long long* tbuf = nullptr;
-  const bool want_trace = getenv("DNNP_TC_TRACE") != nullptr;
+  const bool want_trace = ::dnnp::diag_env("DNNP_TC_TRACE") != nullptr;
   if (want_trace && !tbuf) cudaMalloc(&tbuf, 8192 * sizeof(unsigned long long));
   if (want_trace) cudaMemsetAsync(tbuf, 0, 8192 * sizeof(unsigned long long), st);
   prm.trace = want_trace ? tbuf : nullptr;

@@ -22,6 +22,7 @@ TOL = {"f32": 2e-6, "f64": 1e-13}
 def env(**kv):
     old = {k: os.environ.get(k) for k in kv}
     os.environ.update({k: str(v) for k, v in kv.items()})
+    dp._lib.reload_tuning()  # the library caches the switches
     try:
         yield
     finally:
@@ -30,6 +31,7 @@ def env(**kv):
                 os.environ.pop(k, None)
             else:
                 os.environ[k] = v
+        dp._lib.reload_tuning()
 
 
 def rel(a, b):

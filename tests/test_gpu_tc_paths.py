@@ -33,6 +33,7 @@ def env(**kv):
                 os.environ.pop(k, None)
             else:
                 os.environ[k] = str(v)
+        dp._lib.reload_tuning()  # the library caches the switches
         yield
     finally:
         for k, v in old.items():
@@ -40,6 +41,7 @@ def env(**kv):
                 os.environ.pop(k, None)
             else:
                 os.environ[k] = v
+        dp._lib.reload_tuning()
 
 
 def rand_view(rng, n, c, h, w, layout="nchw", fill=None):

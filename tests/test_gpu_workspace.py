@@ -28,8 +28,10 @@ def test_workspace_query_and_ex(shape, pas):
     fd = dp.make_filter_desc(k, c, r, s)
     t = lambda cnt: torch.from_numpy(rng.uniform(-0.5, 0.5, cnt).astype(np.float32)).cuda()
     x, dy, f = t(n * c * h * w), t(n * k * p * q), t(k * c * r * s)
+    launches = dp.kernel_launch_count()
     need = dp.convolution_workspace_size(pas, xd, fd, cd, yd)
     assert need > 0
+    assert dp.kernel_launch_count() == launches  # the query plans, it does not run the pass
 
     def run(ws):
         xv, dyv = dp.TensorView(xd, x), dp.TensorView(yd, dy)
@@ -47,7 +49,12 @@ def test_workspace_query_and_ex(shape, pas):
         return out.buf.clone()
 
     ref = run(None)
-    ws = torch.empty(need + 1024, dtype=torch.uint8, device="cuda")  # + alignment slack
+    # exactly the queried bytes, at a base only 256-byte aligned (the size
+    # includes the slack of the 1024-byte carve-out alignment)
+    raw = torch.empty(need + 2048, dtype=torch.uint8, device="cuda")
+    off = (1024 - raw.data_ptr() % 1024) % 1024 + 256
+    ws = raw[off:off + need]
+    assert ws.numel() == need and ws.data_ptr() % 1024 == 256
     torch.cuda.synchronize()
     dp.scratch_high_water(reset=True)
     got = run(ws)
