@@ -81,6 +81,7 @@ _SIGS = {
                                                   ctypes.c_int, vp, vp, vp, vp],
     "dnnp_convolution_backward_filter": [vp, vp, vp, vp, vp, vp, ctypes.c_int, vp, vp],
     "dnnp_convolution_backward_bias": [vp, vp, vp, vp, vp],
+    "dnnp_convolution_verify_reference": [vp, ctypes.c_int, vp, vp, vp, vp, vp, vp, vp],
     "dnnp_activation_forward": [vp, ctypes.c_int, vp, vp, vp, vp],
     "dnnp_activation_backward": [vp, ctypes.c_int, vp, vp, vp, vp, vp, vp],
     "dnnp_softmax_forward": [vp, ctypes.c_int, vp, vp, vp, vp],

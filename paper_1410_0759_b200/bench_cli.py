@@ -17,7 +17,9 @@ summary rows (suite_mean, suite_weighted).  GPU additions: backward passes
 so the schema is unchanged), seconds are the median of CUDA-event timings of
 device-resident calls.  All three engine labels run the same implicit-GEMM
 kernels (north_star: no multi-backend dispatch).  --verify compares each pass
-with the fp64 GPU path (itself pinned to the C oracle) at the reference's
+with an independent device loop nest in fp64 (dnnp_convolution_verify_reference,
+csrc/conv_verify.cu: the counterpart of the reference's direct-engine check,
+bench.py:196-203; tests pin it to the C oracle) at the reference's
 tolerances (1e-4 f32, 1e-10 f64), applied to max|err| / max(1, max|ref|):
 an absolute bound for unit-scale outputs, the north_star normalised bound for
 the long reductions (dW sums N*P*Q products) whose magnitude grows with the
@@ -216,12 +218,25 @@ def _time(op, repeats):
 
 
 def _reference(layer, prob, pas):
-    """The same pass through the fp64 GPU path on the same inputs."""
+    """The same pass as a plain fp64 loop nest on the device (libdnnp's
+    dnnp_convolution_verify_reference: no packing, no tensor cores, fixed
+    summation order) on the same inputs -- the counterpart of the reference
+    harness's check against its direct engine (bench.py:196-203)."""
     import torch
-    ref = _Problem(layer, "f64", 0, 0, like=prob)
-    ref.op(pas, "implicit")()
+
+    from . import _lib
+    p, q = layer.out_hw()
+    n_out = {"fwd": layer.n * layer.k * p * q, "bwd_data": layer.n * layer.c * layer.h * layer.w,
+             "bwd_filter": layer.k * layer.c * layer.r * layer.s}[pas]
+    out = torch.empty(n_out, dtype=torch.float64, device="cuda")
+    code = PASSES.index(pas)
+    a = prob.x if pas == "fwd" else prob.dy
+    b = prob.f if pas != "bwd_filter" else prob.x
+    _lib.check(_lib.lib().dnnp_convolution_verify_reference(
+        _lib.handle(), code, prob.x.desc.c_desc(), prob.f.desc.c_desc(), prob.cd.c_desc(),
+        prob.y.desc.c_desc(), a.ptr, b.ptr, out.data_ptr()), "convolution_verify_reference")
     torch.cuda.synchronize()
-    return ref.result(pas)
+    return out
 
 
 def run_suite(layers, engines=("implicit",), dtype="f32", batch=None, repeats=5,

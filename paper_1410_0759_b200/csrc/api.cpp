@@ -1241,6 +1241,32 @@ dnnp_status dnnp_get_convolution_workspace_size(dnnp_handle handle, int pass,
   return DNNP_STATUS_OK;
 }
 
+// Verification reference (additive; the GPU CLI's --verify): the pass as a
+// plain fp64 loop nest on the device, independent of the implicit-GEMM
+// kernels.  Device buffers only; out is a dense fp64 buffer of the pass's
+// output extents (y: N K P Q, dx: N C H W, df: K C R S).
+dnnp_status dnnp_convolution_verify_reference(dnnp_handle handle, int pass, dnnp_tensor_desc xd,
+                                              dnnp_filter_desc fd, dnnp_conv_desc cd,
+                                              dnnp_tensor_desc yd, const void* a, const void* b,
+                                              double* out) {
+  if (!reg_has(handle, KIND_HANDLE) || pass < 0 || pass > 2 || !a || !b || !out)
+    return fail(DNNP_STATUS_BAD_PARAM, "convolution_verify_reference: bad arguments");
+  if (!reg_has(xd, KIND_TENSOR) || !xd->configured || !reg_has(yd, KIND_TENSOR) ||
+      !yd->configured || !reg_has(fd, KIND_FILTER) || !fd->configured ||
+      !reg_has(cd, KIND_CONV) || !cd->configured)
+    return fail(DNNP_STATUS_BAD_PARAM, "convolution_verify_reference: descriptor not configured");
+  dnnp_status st;
+  if ((st = bind_view(xd, "x")) || (st = bind_view(yd, "y"))) return st;
+  int64_t P, Q;
+  if ((st = conv_shape(xd, fd, cd, &P, &Q))) return st;
+  if ((st = check_out(yd, xd->n, fd->k, P, Q, xd->elem, "output"))) return st;
+  if ((st = need_device())) return st;
+  const dnnp::ConvProblem pr = make_problem(xd, fd, cd, yd, P, Q);
+  const cudaError_t e = dnnp::conv_verify_reference(pass, pr, dnnp::Dtype(xd->elem), a, b, out,
+                                                    handle->stream);
+  return cuda_status(e, "convolution_verify_reference");
+}
+
 // ------------------------------------------------ fused epilogues (additive)
 
 static bool act_valid(dnnp_activation_kind k);

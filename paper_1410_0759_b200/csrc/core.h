@@ -134,6 +134,11 @@ cudaError_t conv_backward_filter(const ConvProblem& p, Dtype dt, const void* dy,
 // db[k] = sum_{n,p,q} dy[n,k,p,q]  (dy dtype dt, db dtype dbt)
 cudaError_t conv_backward_bias(const View4& dy, Dtype dt, const void* dyp, const View4& db,
                                Dtype dbt, void* dbp, cudaStream_t st);
+// Verification loop nests (conv_verify.cu): pass 0 out = conv(a = x, b = f),
+// 1 out = bwd_data(a = dy, b = f), 2 out = bwd_filter(a = dy, b = x); dense
+// fp64 output, fp64 accumulation, one thread per output element.
+cudaError_t conv_verify_reference(int pass, const ConvProblem& p, Dtype dt, const void* a,
+                                  const void* b, double* out, cudaStream_t st);
 // whether the tcgen05 path would be used for a forward problem (tests/bench)
 bool tc_eligible(const ConvProblem& p, int pass);
 
