@@ -340,7 +340,8 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
-    ap.add_argument("--math", type=int, default=0, help="0 default, 1 SIMT fp32, 2 tcgen05")
+    ap.add_argument("--math", type=int, default=0,
+                    help="0 default (BF16x3), 1 SIMT fp32, 2 force BF16x3, 3 3xTF32")
     ap.add_argument("--eager", action="store_true",
                     help="submit every step eagerly (no CUDA-graph replay at N=1)")
     ap.add_argument("--no-e2e", action="store_true")
@@ -478,6 +479,43 @@ def main():
     for i, v in pre_kern.items():
         kern_ms.setdefault(i, v)
 
+    # the fp32 split sweep: the same step (same calls, same data) in the
+    # 3xTF32 mode, replayed as a graph (N=1 only): step time, throughput and
+    # the fraction of each split's own tensor ceiling (BF16x3: bf16 / 3,
+    # 3xTF32: tf32 / 3 = bf16 / 6)
+    tf32_ms = None
+    if graph is not None and args.math == 0:
+        try:
+            dp.set_math(3)
+            run_step(dp, layers, torch)
+            torch.cuda.synchronize()
+            cap3 = torch.cuda.Stream()
+            cap3.wait_stream(torch.cuda.current_stream())
+            g3 = torch.cuda.CUDAGraph()
+            with torch.cuda.stream(cap3):
+                with torch.cuda.graph(g3, stream=cap3):
+                    run_step(dp, layers, torch)
+            torch.cuda.synchronize()
+            ts = []
+            for _ in range(max(3, args.steps)):
+                flush.fill_(1.0)
+                torch.cuda.synchronize()
+                t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                t0.record()
+                g3.replay()
+                t1.record()
+                torch.cuda.synchronize()
+                ts.append(t0.elapsed_time(t1))
+            tf32_ms = float(np.median(ts))
+            del g3
+        except Exception as e:  # report, never fail the headline
+            print(f"tf32x3 sweep failed: {type(e).__name__}: {e}", file=sys.stderr)
+            tf32_ms = None
+        finally:
+            dp.set_math(args.math)
+            run_step(dp, layers, torch)  # leave the BF16x3 results in the buffers
+            torch.cuda.synchronize()
+
     # the framework path: fused backward entry, replayed as a graph (N=1 only)
     fused_ms = None
     if graph is not None and hasattr(dp, "conv_backward"):
@@ -598,7 +636,7 @@ def main():
                    "eager_ms_per_step": round(float(np.median(eager_ms)), 4),
                    "fused_backward_ms_per_step": (round(fused_ms, 4) if fused_ms else None),
                    "math": ["default(tcgen05 BF16x3 when eligible)", "simt_fp32",
-                            "tcgen05_bf16x3"][args.math]},
+                            "tcgen05_bf16x3", "tcgen05_3xtf32"][args.math]},
         "pct_tf32_peak": round(100 * value / ws / tf32_peak, 2),
         "per_layer": per,
         "per_layer_note": ("ms / tflops: per-op CUDA events of an instrumented eager pass; "
@@ -618,6 +656,7 @@ def main():
                      "frac_of_bf16x3_ceiling": round(achieved / (bf16 / 3.0), 4),
                      "work_per_launch_flops": layers[dl]["flops"],
                      "l2_to_sm_ingest": ingest},
+        "math_sweep": math_sweep(step_flops, total_ms / args.steps, tf32_ms, bf16),
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
     }
@@ -660,6 +699,24 @@ def main():
         dist.destroy_process_group()
     if rank == 0:
         print(json.dumps(line))
+
+
+def math_sweep(step_flops, bf16x3_ms, tf32x3_ms, bf16_peak):
+    """Both fp32 splits of the same step against their own tensor ceilings:
+    BF16x3 issues 3 bf16 MMAs per product (ceiling bf16 / 3), 3xTF32 issues 3
+    tf32 MMAs at half the bf16 rate (ceiling bf16 / 6)."""
+    out = {}
+    for name, ms, ceil in (("bf16x3", bf16x3_ms, bf16_peak / 3.0),
+                           ("tf32x3", tf32x3_ms, bf16_peak / 6.0)):
+        if ms is None:
+            out[name] = None
+            continue
+        tf = step_flops / (ms / 1e3) / 1e12
+        out[name] = {"ms_per_step": round(ms, 4), "tflops": round(tf, 2),
+                     "ceiling_tflops": round(ceil, 1), "frac_of_ceiling": round(tf / ceil, 4)}
+    out["note"] = ("same AlexNet conv1-5 step (graph replay, L2 flushed); algorithmic flops; "
+                   "the split's extra MMAs are not counted")
+    return out
 
 
 def run_e2e(dp, layers, torch, device, ws, args, step_flops):

@@ -695,7 +695,7 @@ dnnp_status dnnp_synchronize(dnnp_handle handle) {
 }
 
 dnnp_status dnnp_set_math(dnnp_handle handle, int math) {
-  if (!reg_has(handle, KIND_HANDLE) || math < DNNP_MATH_DEFAULT || math > DNNP_MATH_TC_BF16X3)
+  if (!reg_has(handle, KIND_HANDLE) || math < DNNP_MATH_DEFAULT || math > DNNP_MATH_TC_TF32X3)
     return fail(DNNP_STATUS_BAD_PARAM, "bad handle or math mode");
   handle->math = math;
   return DNNP_STATUS_OK;

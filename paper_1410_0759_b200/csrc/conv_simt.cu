@@ -451,25 +451,40 @@ static cudaError_t simt_bwd_filter(const ConvProblem& p, const void* dy, const v
   return launch_simt<T, WGRAD>(a, st);
 }
 
-// ---- tensor-core path (conv_tc.cu) -----------------------------------------
+// ---- tensor-core path (conv_tc.cu, wgrad_tc.cu) -----------------------------
+// es: the fp32 split, 2 = BF16x3 (kind::f16), 4 = 3xTF32 (kind::tf32)
 cudaError_t tc_forward(const ConvProblem& p, const float* x, const float* f, float* y,
-                       double alpha, double beta, cudaStream_t st);
+                       double alpha, double beta, cudaStream_t st, int es);
 cudaError_t tc_backward_data(const ConvProblem& p, const float* dy, const float* f, float* dx,
-                             bool acc, cudaStream_t st);
+                             bool acc, cudaStream_t st, int es);
 cudaError_t tc_backward_filter(const ConvProblem& p, const float* dy, const float* x, float* df,
-                               bool acc, cudaStream_t st);
+                               bool acc, cudaStream_t st, int es);
 cudaError_t tc_forward_fused(const ConvProblem& p, const float* x, const float* f, float* y,
-                             double alpha, double beta, const ConvEpilogue& ep, cudaStream_t st);
+                             double alpha, double beta, const ConvEpilogue& ep, cudaStream_t st,
+                             int es);
 cudaError_t tc_backward_data_fused(const ConvProblem& p, const float* dy, const float* f,
-                                   float* dx, bool acc, const ConvEpilogue& ep, cudaStream_t st);
+                                   float* dx, bool acc, const ConvEpilogue& ep, cudaStream_t st,
+                                   int es);
 
-// math: 0 default (tensor cores when eligible), 1 SIMT fp32, 2 force tensor cores
+// math (dnnp_math_mode): 0 default (BF16x3 tensor cores when eligible), 1
+// SIMT fp32, 2 force BF16x3 tensor cores, 3 3xTF32 tensor cores (geometries
+// outside the TMA im2col kernels run the SIMT fp32 kernels instead)
 static bool use_tc(const ConvProblem& p, Dtype dt, int math, int pass, cudaError_t* err) {
   *err = cudaSuccess;
   if (dt != F32 || math == 1) return false;
   bool ok = tc_eligible(p, pass);
   if (!ok && math == 2) *err = cudaErrorNotSupported;
   return ok;
+}
+
+static int split_es(int math) { return math == 3 ? 4 : 2; }
+
+// A 3xTF32 call the TMA kernels cannot take (NotSupported before any
+// output write) continues on the SIMT fp32 kernels.
+static bool tf32_fallback(int math, cudaError_t e) {
+  if (math != 3 || e != cudaErrorNotSupported) return false;
+  cudaGetLastError();
+  return true;
 }
 
 // Explicit lowering (engine EXPLICIT, forward): D[n][(c,r,s)][p][q] =
@@ -544,8 +559,11 @@ cudaError_t conv_forward(const ConvProblem& p, Dtype dt, const void* x, const vo
                          double alpha, double beta, int math, cudaStream_t st) {
   cudaError_t e;
   if (p.engine == 1) return explicit_forward(p, dt, x, f, y, alpha, beta, math, st);
-  if (use_tc(p, dt, math, FWD, &e))
-    return tc_forward(p, (const float*)x, (const float*)f, (float*)y, alpha, beta, st);
+  if (use_tc(p, dt, math, FWD, &e)) {
+    e = tc_forward(p, (const float*)x, (const float*)f, (float*)y, alpha, beta, st, split_es(math));
+    if (!tf32_fallback(math, e)) return e;
+    e = cudaSuccess;
+  }
   if (e != cudaSuccess) return e;
   return dt == F32 ? simt_forward<float>(p, x, f, y, alpha, beta, st)
                    : simt_forward<double>(p, x, f, y, alpha, beta, st);
@@ -554,8 +572,12 @@ cudaError_t conv_forward(const ConvProblem& p, Dtype dt, const void* x, const vo
 cudaError_t conv_backward_data(const ConvProblem& p, Dtype dt, const void* dy, const void* f,
                                void* dx, bool accumulate, int math, cudaStream_t st) {
   cudaError_t e;
-  if (use_tc(p, dt, math, DGRAD, &e))
-    return tc_backward_data(p, (const float*)dy, (const float*)f, (float*)dx, accumulate, st);
+  if (use_tc(p, dt, math, DGRAD, &e)) {
+    e = tc_backward_data(p, (const float*)dy, (const float*)f, (float*)dx, accumulate, st,
+                         split_es(math));
+    if (!tf32_fallback(math, e)) return e;
+    e = cudaSuccess;
+  }
   if (e != cudaSuccess) return e;
   return dt == F32 ? simt_bwd_data<float>(p, dy, f, dx, accumulate, st)
                    : simt_bwd_data<double>(p, dy, f, dx, accumulate, st);
@@ -564,8 +586,12 @@ cudaError_t conv_backward_data(const ConvProblem& p, Dtype dt, const void* dy, c
 cudaError_t conv_backward_filter(const ConvProblem& p, Dtype dt, const void* dy, const void* x,
                                  void* df, bool accumulate, int math, cudaStream_t st) {
   cudaError_t e;
-  if (use_tc(p, dt, math, WGRAD, &e))
-    return tc_backward_filter(p, (const float*)dy, (const float*)x, (float*)df, accumulate, st);
+  if (use_tc(p, dt, math, WGRAD, &e)) {
+    e = tc_backward_filter(p, (const float*)dy, (const float*)x, (float*)df, accumulate, st,
+                           split_es(math));
+    if (!tf32_fallback(math, e)) return e;
+    e = cudaSuccess;
+  }
   if (e != cudaSuccess) return e;
   return dt == F32 ? simt_bwd_filter<float>(p, dy, x, df, accumulate, st)
                    : simt_bwd_filter<double>(p, dy, x, df, accumulate, st);
@@ -580,7 +606,7 @@ cudaError_t conv_backward_both(const ConvProblem& p, Dtype dt, const void* dy, c
   const bool tcw = use_tc(p, dt, math, WGRAD, &e);
   if (e != cudaSuccess) return e;
   // one dy pack serves both GEMMs when their packed widths agree (K % 64 == 0)
-  if (tcd && tcw && p.K % 64 == 0 && !::dnnp::tune_env("DNNP_NO_SHARED_DY")) {
+  if (tcd && tcw && math != 3 && p.K % 64 == 0 && !::dnnp::tune_env("DNNP_NO_SHARED_DY")) {
     tc::ScratchScope* sc = tc::scratch_open(st);
     e = tc::shared_dy_pack(sc, p.y, static_cast<const float*>(dy), int(p.K), st);
     if (e == cudaSuccess) e = conv_backward_data(p, dt, dy, f, dx, accumulate, math, st);
@@ -605,7 +631,8 @@ cudaError_t conv_forward_fused(const ConvProblem& p, Dtype dt, const void* x, co
                                const ConvEpilogue& ep, cudaStream_t st) {
   cudaError_t e;
   if (use_tc(p, dt, math, FWD, &e)) {
-    e = tc_forward_fused(p, (const float*)x, (const float*)f, (float*)y, alpha, beta, ep, st);
+    e = tc_forward_fused(p, (const float*)x, (const float*)f, (float*)y, alpha, beta, ep, st,
+                         split_es(math));
     if (e != cudaErrorNotSupported) return e;
     cudaGetLastError();
   } else if (e != cudaSuccess) {
@@ -627,7 +654,7 @@ cudaError_t conv_backward_data_fused(const ConvProblem& p, Dtype dt, const void*
   if (use_tc(p, dt, math, DGRAD, &e)) {
     if (same_strides(ep.gatev, p.x)) {
       e = tc_backward_data_fused(p, (const float*)dy, (const float*)f, (float*)dx, accumulate,
-                                 ep, st);
+                                 ep, st, split_es(math));
       if (e != cudaErrorNotSupported) return e;
       cudaGetLastError();
     }

@@ -426,19 +426,18 @@ __device__ __forceinline__ int phase_tap(int ph, int dh, int lo, int u, int pad,
 // offsets (and the bwd-data phase taps) are resolved once per block, threads
 // walk the tap's Cpf reduction channels (coalesced 2-byte stores).  Block
 // x == taps zero-fills the K padding tail.
+template <int ES>
 __global__ void __launch_bounds__(128) pack_filter_tap_kernel(PackGeom g, const float* __restrict__ f,
-                                                              __nv_bfloat16* __restrict__ hi,
-                                                              __nv_bfloat16* __restrict__ lo,
+                                                              void* __restrict__ hi,
+                                                              void* __restrict__ lo,
                                                               uint32_t* __restrict__ ctab,
                                                               uint32_t* __restrict__ coltab, int taps) {
   const int row = blockIdx.y, tap = blockIdx.x;
   const int Cpf = g.Cgrp * 8;
   const int64_t rbase = int64_t(row) * g.Ktot;
   if (tap == taps) {  // padding tail of the reduction
-    for (int k = taps * Cpf + threadIdx.x; k < g.Ktot; k += blockDim.x) {
-      hi[rbase + k] = __float2bfloat16_rn(0.0f);
-      lo[rbase + k] = __float2bfloat16_rn(0.0f);
-    }
+    for (int k = taps * Cpf + threadIdx.x; k < g.Ktot; k += blockDim.x)
+      store_split1<ES>(hi, lo, rbase + k, 0.0f);
     return;
   }
   const int dhb = tap / g.tapW, dwb = tap - (tap / g.tapW) * g.tapW;
@@ -479,10 +478,7 @@ __global__ void __launch_bounds__(128) pack_filter_tap_kernel(PackGeom g, const 
     } else if (row < g.Ncol && cin < g.K && rp >= 0 && sp >= 0) {
       val = fetch_filter(g, f, cin, c_col, rp, sp);
     }
-    __nv_bfloat16 h, l;
-    split_bf16(val, h, l);
-    hi[rbase + tap * Cpf + cin] = h;
-    lo[rbase + tap * Cpf + cin] = l;
+    store_split1<ES>(hi, lo, rbase + tap * Cpf + cin, val);
   }
 }
 
@@ -492,9 +488,10 @@ __global__ void __launch_bounds__(128) pack_filter_tap_kernel(PackGeom g, const 
 // row (lanes along the channels).  Coalesced, but only Np blocks: measured
 // slower than the per-(tap, row) kernel (8.3 vs ~5 us per AlexNet layer), so
 // it is opt-in (DNNP_PACK_ROWS).
+template <int ES>
 __global__ void __launch_bounds__(256) pack_filter_row_kernel(PackGeom g, const float* __restrict__ f,
-                                                              __nv_bfloat16* __restrict__ hi,
-                                                              __nv_bfloat16* __restrict__ lo,
+                                                              void* __restrict__ hi,
+                                                              void* __restrict__ lo,
                                                               uint32_t* __restrict__ ctab,
                                                               uint32_t* __restrict__ coltab, int taps) {
   extern __shared__ float sf[];
@@ -544,16 +541,11 @@ __global__ void __launch_bounds__(256) pack_filter_row_kernel(PackGeom g, const 
           val = sf[(c * g.R0 + r) * g.S0 + s2];
         }
       }
-      __nv_bfloat16 h, l;
-      split_bf16(val, h, l);
-      hi[rbase + tap * Cpf + cin] = h;
-      lo[rbase + tap * Cpf + cin] = l;
+      store_split1<ES>(hi, lo, rbase + tap * Cpf + cin, val);
     }
   }
-  for (int k = taps * Cpf + threadIdx.x; k < g.Ktot; k += blockDim.x) {
-    hi[rbase + k] = __float2bfloat16_rn(0.0f);
-    lo[rbase + k] = __float2bfloat16_rn(0.0f);
-  }
+  for (int k = taps * Cpf + threadIdx.x; k < g.Ktot; k += blockDim.x)
+    store_split1<ES>(hi, lo, rbase + k, 0.0f);
 }
 
 // Scatter form of the filter packing: one thread per filter element (read
@@ -562,9 +554,10 @@ __global__ void __launch_bounds__(256) pack_filter_row_kernel(PackGeom g, const 
 // gather offset r' -> (space-to-depth tap r'/su, phase r'%su); for the
 // super-pixel bwd-data form t0 = r' % u, jr = r' / u, phase ph = (t0 - pad)
 // mod u and window tap dh = base(ph) - jr - lo.
+template <int ES>
 __global__ void __launch_bounds__(256) pack_filter_scatter_kernel(PackGeom g, const float* __restrict__ f,
-                                                                  __nv_bfloat16* __restrict__ hi,
-                                                                  __nv_bfloat16* __restrict__ lo) {
+                                                                  void* __restrict__ hi,
+                                                                  void* __restrict__ lo) {
   const int total = g.K * g.C0 * g.R0 * g.S0;
   const int Cpf = g.Cgrp * 8;
   for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * blockDim.x) {
@@ -589,10 +582,7 @@ __global__ void __launch_bounds__(256) pack_filter_scatter_kernel(PackGeom g, co
       const int row = (ph * g.v + pw) * g.C + cg;
       o = int64_t(row) * g.Ktot + (dh * g.winW + dw) * Cpf + k;
     }
-    __nv_bfloat16 h, l;
-    split_bf16(__ldg(f + idx), h, l);
-    hi[o] = h;
-    lo[o] = l;
+    store_split1<ES>(hi, lo, o, __ldg(f + idx));
   }
 }
 
@@ -641,18 +631,18 @@ cudaError_t launch_gemm(const TcParams& prm, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-template <int BN, int CB, int NC>
+template <int BN, int CB, int NC, int ES>
 cudaError_t launch_tma(const TmaParams& prm, cudaStream_t st) {
-  using CC = TCfg<BN, CB, NC>;
+  using CC = TCfg<BN, CB, NC, ES>;
   static int attr_dev = -1;
   int dev = 0;
   cudaGetDevice(&dev);
   if (attr_dev != dev) {
-    cudaError_t e = cudaFuncSetAttribute(conv_tma_kernel<BN, CB, NC>,
+    cudaError_t e = cudaFuncSetAttribute(conv_tma_kernel<BN, CB, NC, ES>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, CC::SMEM);
     if (e != cudaSuccess) return e;
     if (NC == 2) {
-      e = cudaFuncSetAttribute(conv_tma_kernel<BN, CB, NC>,
+      e = cudaFuncSetAttribute(conv_tma_kernel<BN, CB, NC, ES>,
                                cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
       (void)e;
     }
@@ -674,25 +664,25 @@ cudaError_t launch_tma(const TmaParams& prm, cudaStream_t st) {
   cfg.numAttrs = 1;
   if (::dnnp::diag_env("DNNP_TC_DIAG")) {
     int ncl = -1;
-    cudaError_t qe = cudaOccupancyMaxActiveClusters(&ncl, conv_tma_kernel<BN, CB, NC>, &cfg);
-    fprintf(stderr, "DIAG conv_tma<%d,%d,%d> smem=%d grid=%d maxActiveClusters=%d (%s)\n", BN, CB, NC,
+    cudaError_t qe = cudaOccupancyMaxActiveClusters(&ncl, conv_tma_kernel<BN, CB, NC, ES>, &cfg);
+    fprintf(stderr, "DIAG conv_tma<%d,%d,%d,%d> smem=%d grid=%d maxActiveClusters=%d (%s)\n", BN, CB, NC, ES,
             CC::SMEM, clusters * NC, ncl, cudaGetErrorString(qe));
   }
   ktime_begin(st, 1);
-  cudaError_t e = cudaLaunchKernelEx(&cfg, conv_tma_kernel<BN, CB, NC>, prm);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, conv_tma_kernel<BN, CB, NC, ES>, prm);
   ktime_end(st);
   note_launch();
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
-template <int CB, int NC>
+template <int CB, int NC, int ES>
 cudaError_t launch_tma_bn(int bn, const TmaParams& prm, cudaStream_t st) {
   switch (bn) {
-    case 64: return launch_tma<64, CB, NC>(prm, st);
-    case 128: return launch_tma<128, CB, NC>(prm, st);
-    case 192: return launch_tma<192, CB, NC>(prm, st);
-    default: return launch_tma<256, CB, NC>(prm, st);
+    case 64: return launch_tma<64, CB, NC, ES>(prm, st);
+    case 128: return launch_tma<128, CB, NC, ES>(prm, st);
+    case 192: return launch_tma<192, CB, NC, ES>(prm, st);
+    default: return launch_tma<256, CB, NC, ES>(prm, st);
   }
 }
 
@@ -774,7 +764,10 @@ bool tma_geometry_ok(const Gemm& g, int IH, int IW, int taps_h, int taps_w, int6
 // TMA channel block per im2col load: the widest of 64/32/16 whose padding of
 // Cp stays <= 1/3 (wider rows = fewer TMA pixel requests; the TMA engine
 // handles ~1 im2col pixel row per 2.5 cycles whatever its width).
-int pick_cb(int Cp) {
+// 3xTF32 (es = 4): 32-channel blocks only (128-byte rows; the instantiated
+// tf32 kernels), Cp padded up to them by out-of-bounds zero fill.
+int pick_cb(int Cp, int es = 2) {
+  if (es == 4) return 32;
   for (int cb : {64, 32, 16})
     if (ceil_div(Cp, cb) * cb * 3 <= int64_t(Cp) * 4) return cb;
   return 16;
@@ -793,18 +786,21 @@ int reduction_segments(int nkb, int depth) {
   return std::max(1, (nkb + per - 1) / per);
 }
 
-cudaError_t run_gemm(const ConvProblem& p, Gemm g, const __nv_bfloat16* a_hi,
-                     const __nv_bfloat16* a_lo, int IH, int IW, int Cp, const float* f, float* out,
-                     const View4& ov, float alpha, float beta, const EpiOp& epi, cudaStream_t st) {
+// es: bytes per packed element of the planes a_hi / a_lo (2 = BF16x3, 4 =
+// 3xTF32; the tf32 split runs on the TMA kernel only).
+cudaError_t run_gemm(const ConvProblem& p, Gemm g, const void* a_hi, const void* a_lo, int IH,
+                     int IW, int Cp, const float* f, float* out, const View4& ov, float alpha,
+                     float beta, const EpiOp& epi, cudaStream_t st, int es) {
   const bool fused = epi.act >= 0 || epi.gate >= 0 || epi.bias != nullptr;
   if (fused && !g.tma) return cudaErrorNotSupported;  // caller runs the unfused sequence
+  if (es == 4 && !g.tma) return cudaErrorNotSupported;  // caller runs SIMT fp32
   PackGeom& pg = g.pg;
-  const int CB = g.tma ? pick_cb(Cp) : 8;
+  const int CB = g.tma ? pick_cb(Cp, es) : 8;
   const int Cpf = int(ceil_div(Cp, CB) * CB);  // filter columns per tap (channel blocks padded)
   pg.Cgrp = Cpf / 8;
   const int taps = pg.tapH * pg.tapW;
   pg.KC = taps * pg.Cgrp;
-  const int depth = g.tma ? kTK : kBK;
+  const int depth = g.tma ? 128 / es : kBK;  // one stage = 128 bytes of reduction per row
   const int nkb = int(ceil_div(int64_t(pg.KC) * 8, depth));
   pg.Ktot = std::max(1, nkb) * depth;
   const int64_t M = p.N * g.OH * g.OW;
@@ -824,25 +820,35 @@ cudaError_t run_gemm(const ConvProblem& p, Gemm g, const __nv_bfloat16* a_hi,
   pg.Np = int(ceil_div(pg.Ncol, bn) * bn);
   const size_t flt = size_t(pg.Np) * pg.Ktot;
   Workspace ws(st);
-  cudaError_t e = ws.alloc(flt * 4 + size_t(pg.KC + pg.Np + 2) * 4 + 256);
+  cudaError_t e = ws.alloc(flt * 2 * es + size_t(pg.KC + pg.Np + 2) * 4 + 256);
   if (e != cudaSuccess) return e;
-  auto* b_hi = static_cast<__nv_bfloat16*>(ws.p);
-  auto* b_lo = b_hi + flt;
-  auto* ctab = reinterpret_cast<uint32_t*>(b_lo + flt);
+  void* b_hi = ws.p;
+  void* b_lo = static_cast<char*>(ws.p) + flt * es;
+  auto* ctab = reinterpret_cast<uint32_t*>(static_cast<char*>(b_lo) + flt * es);
   auto* coltab = ctab + pg.KC + 1;
   const size_t frow = size_t(pg.C0) * pg.R0 * pg.S0 * sizeof(float);
   // (row-staged variant: opt-in, measured slower -- Np blocks are too few)
   if (!pg.dgrad && frow <= 48 * 1024 && ::dnnp::tune_env("DNNP_PACK_ROWS")) {
-    pack_filter_row_kernel<<<unsigned(pg.Np), 256, frow, st>>>(pg, f, b_hi, b_lo, ctab, coltab,
-                                                               taps);
+    if (es == 4)
+      pack_filter_row_kernel<4><<<unsigned(pg.Np), 256, frow, st>>>(pg, f, b_hi, b_lo, ctab, coltab,
+                                                                    taps);
+    else
+      pack_filter_row_kernel<2><<<unsigned(pg.Np), 256, frow, st>>>(pg, f, b_hi, b_lo, ctab, coltab,
+                                                                    taps);
   } else if (!::dnnp::tune_env("DNNP_PACK_SCATTER") || pg.bw > 1) {
     const dim3 fgrid(unsigned(taps + 1), unsigned(pg.Np));
-    pack_filter_tap_kernel<<<fgrid, 128, 0, st>>>(pg, f, b_hi, b_lo, ctab, coltab, taps);
+    if (es == 4)
+      pack_filter_tap_kernel<4><<<fgrid, 128, 0, st>>>(pg, f, b_hi, b_lo, ctab, coltab, taps);
+    else
+      pack_filter_tap_kernel<2><<<fgrid, 128, 0, st>>>(pg, f, b_hi, b_lo, ctab, coltab, taps);
   } else {
-    if (!tc::dry_run() && (e = cudaMemsetAsync(b_hi, 0, flt * 4, st)) != cudaSuccess)
+    if (!tc::dry_run() && (e = cudaMemsetAsync(b_hi, 0, flt * 2 * es, st)) != cudaSuccess)
       return e;  // hi and lo planes
     const int64_t nf = int64_t(pg.K) * pg.C0 * pg.R0 * pg.S0;
-    pack_filter_scatter_kernel<<<grid_for(nf, 256, 8), 256, 0, st>>>(pg, f, b_hi, b_lo);
+    if (es == 4)
+      pack_filter_scatter_kernel<4><<<grid_for(nf, 256, 8), 256, 0, st>>>(pg, f, b_hi, b_lo);
+    else
+      pack_filter_scatter_kernel<2><<<grid_for(nf, 256, 8), 256, 0, st>>>(pg, f, b_hi, b_lo);
     note_launch();
     pack_tables_kernel<<<grid_for(std::max(pg.KC, pg.Ncol), 256, 2), 256, 0, st>>>(pg, ctab, coltab,
                                                                                   g.tma ? 0 : 1);
@@ -866,16 +872,17 @@ cudaError_t run_gemm(const ConvProblem& p, Gemm g, const __nv_bfloat16* a_hi,
     ig.stride_w = g.v;
     ig.cpp = CB;
     ig.ppc = kBM;
-    const CUtensorMapSwizzle sw = CB == 64   ? CU_TENSOR_MAP_SWIZZLE_128B
-                                  : CB == 32 ? CU_TENSOR_MAP_SWIZZLE_64B
+    const int rb = CB * es;  // sub-tile row bytes = swizzle span
+    const CUtensorMapSwizzle sw = rb == 128  ? CU_TENSOR_MAP_SWIZZLE_128B
+                                  : rb == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
                                              : CU_TENSOR_MAP_SWIZZLE_32B;
-    if ((e = make_tmap_im2col(&prm.tm_ahi, a_hi, ig, sw)) != cudaSuccess) return e;
-    if ((e = make_tmap_im2col(&prm.tm_alo, a_lo, ig, sw)) != cudaSuccess) return e;
+    if ((e = make_tmap_im2col(&prm.tm_ahi, a_hi, ig, sw, es)) != cudaSuccess) return e;
+    if ((e = make_tmap_im2col(&prm.tm_alo, a_lo, ig, sw, es)) != cudaSuccess) return e;
     if ((e = make_tmap_2d(&prm.tm_bhi, b_hi, uint64_t(pg.Ktot), uint64_t(pg.Np), uint64_t(pg.Ktot),
-                          uint32_t(CB), uint32_t(bn / nc), sw)) != cudaSuccess)
+                          uint32_t(CB), uint32_t(bn / nc), sw, es)) != cudaSuccess)
       return e;
     if ((e = make_tmap_2d(&prm.tm_blo, b_lo, uint64_t(pg.Ktot), uint64_t(pg.Np), uint64_t(pg.Ktot),
-                          uint32_t(CB), uint32_t(bn / nc), sw)) != cudaSuccess)
+                          uint32_t(CB), uint32_t(bn / nc), sw, es)) != cudaSuccess)
       return e;
     prm.M = M;
     prm.Ncol = pg.Ncol;
@@ -916,7 +923,7 @@ cudaError_t run_gemm(const ConvProblem& p, Gemm g, const __nv_bfloat16* a_hi,
     prm.dOW = make_magic(uint32_t(g.OW));
     prm.skip = ::dnnp::diag_env("DNNP_TC_SKIP") ? atoi(::dnnp::diag_env("DNNP_TC_SKIP")) : 0;
     prm.prefetch = ::dnnp::diag_env("DNNP_TC_PREFETCH") ? atoi(::dnnp::diag_env("DNNP_TC_PREFETCH")) : 0;
-    int nseg = reduction_segments(nkb, kTK);
+    int nseg = reduction_segments(nkb, depth);
     // a gated sum spread over segments cannot also add the caller's dx
     if (epi.gate >= 0 && nseg > 1 && beta != 0.0f) return cudaErrorNotSupported;
     // stream-K over the last, partial wave of tiles
@@ -937,7 +944,7 @@ cudaError_t run_gemm(const ConvProblem& p, Gemm g, const __nv_bfloat16* a_hi,
       // >= 4 k-blocks spread over up to all SMs; each piece's chain stays
       // under the accumulation cap, the finisher adds pieces in IEEE fp32.
       {
-        const int Gmax = kNumSMs / nc, per_cap = std::max(1, 8192 / kTK);
+        const int Gmax = kNumSMs / nc, per_cap = std::max(1, 8192 / depth);
         if (!use_sk && !::dnnp::tune_env("DNNP_TC_NO_SPLIT") && T * 2 <= Gmax && nkb >= 8 &&
             int64_t(T) * nkb < (int64_t(1) << 30)) {
           int Gs = int(std::min<int64_t>(Gmax, int64_t(T) * (nkb / 4)));
@@ -981,14 +988,16 @@ cudaError_t run_gemm(const ConvProblem& p, Gemm g, const __nv_bfloat16* a_hi,
     prm.nseg = nseg;
     prm.kb_lo = 0;
     {
-      if (nc == 2)
-        e = CB == 64   ? launch_tma_bn<64, 2>(bn, prm, st)
-            : CB == 32 ? launch_tma_bn<32, 2>(bn, prm, st)
-                       : launch_tma_bn<16, 2>(bn, prm, st);
+      if (es == 4)  // 3xTF32: 32 tf32 channels = 128-byte rows
+        e = nc == 2 ? launch_tma_bn<32, 2, 4>(bn, prm, st) : launch_tma_bn<32, 1, 4>(bn, prm, st);
+      else if (nc == 2)
+        e = CB == 64   ? launch_tma_bn<64, 2, 2>(bn, prm, st)
+            : CB == 32 ? launch_tma_bn<32, 2, 2>(bn, prm, st)
+                       : launch_tma_bn<16, 2, 2>(bn, prm, st);
       else
-        e = CB == 64   ? launch_tma_bn<64, 1>(bn, prm, st)
-            : CB == 32 ? launch_tma_bn<32, 1>(bn, prm, st)
-                       : launch_tma_bn<16, 1>(bn, prm, st);
+        e = CB == 64   ? launch_tma_bn<64, 1, 2>(bn, prm, st)
+            : CB == 32 ? launch_tma_bn<32, 1, 2>(bn, prm, st)
+                       : launch_tma_bn<16, 1, 2>(bn, prm, st);
     }
     if (want_trace) {
       static unsigned long long h[8192];
@@ -1033,10 +1042,10 @@ cudaError_t run_gemm(const ConvProblem& p, Gemm g, const __nv_bfloat16* a_hi,
                    uint32_t(bn), CU_TENSOR_MAP_SWIZZLE_64B);
   if (e != cudaSuccess) return e;
   prm.ctab = ctab;
-  prm.a_hi = a_hi;
-  prm.a_lo = a_lo;
-  prm.b_hi = b_hi;
-  prm.b_lo = b_lo;
+  prm.a_hi = static_cast<const __nv_bfloat16*>(a_hi);
+  prm.a_lo = static_cast<const __nv_bfloat16*>(a_lo);
+  prm.b_hi = static_cast<const __nv_bfloat16*>(b_hi);
+  prm.b_lo = static_cast<const __nv_bfloat16*>(b_lo);
   prm.out = out;
   prm.o_sn = ov.sn;
   prm.o_sc = ov.sc;
@@ -1113,7 +1122,7 @@ bool env_off(const char* name) { return ::dnnp::tune_env(name) != nullptr; }
 
 cudaError_t run_tc(bool dgrad, const ConvProblem& p, const float* in, const View4& inv,
                    const float* f, float* out, const View4& outv, float alpha, float beta,
-                   const EpiOp& epi, cudaStream_t st) {
+                   const EpiOp& epi, cudaStream_t st, int es) {
   pool_keep_memory();
   Gemm g{};
   PackGeom& pg = g.pg;
@@ -1354,27 +1363,28 @@ cudaError_t run_tc(bool dgrad, const ConvProblem& p, const float* in, const View
     gb.o_ph = gb.o_pw = 0;
     if (gb.u <= 8 && tma_geometry_ok(gb, IH, IW, pb.tapH, pb.tapW, Nimg * gb.OH * gb.OW)) g = gb;
   }
+  if (es == 4 && !g.tma) return cudaErrorNotSupported;  // 3xTF32 runs on the TMA kernel only
   const size_t act = size_t(p.N) * IH * IW * Cp;
   Workspace ws(st);
   {
-    // dy already packed by the fused backward entry (same view and width)
-    const __nv_bfloat16 *ph = nullptr, *pl = nullptr;
-    if (dgrad && !fold && packed_get(in, inv, Cp, &ph, &pl))
-      return run_gemm(p, g, ph, pl, IH, IW, Cp, f, out, outv, alpha, beta, epi, st);
+    // dy already packed by the fused backward entry (same view, width and split)
+    const void *ph = nullptr, *pl = nullptr;
+    if (dgrad && !fold && packed_get(in, inv, Cp, &ph, &pl, es))
+      return run_gemm(p, g, ph, pl, IH, IW, Cp, f, out, outv, alpha, beta, epi, st, es);
   }
-  cudaError_t e = ws.alloc(act * 4 + 256);
+  cudaError_t e = ws.alloc(act * 2 * es + 256);
   if (e != cudaSuccess) return e;
-  auto* a_hi = static_cast<__nv_bfloat16*>(ws.p);
-  auto* a_lo = a_hi + act;
+  void* a_hi = ws.p;
+  void* a_lo = static_cast<char*>(ws.p) + act * es;
   if (fold)
-    e = pack_act_fold(inv, in, int(p.S), int(p.v), int(p.pad_w), IW, Cp, a_hi, a_lo, st);
+    e = pack_act_fold(inv, in, int(p.S), int(p.v), int(p.pad_w), IW, Cp, a_hi, a_lo, st, es);
   else if (s2d && !dgrad)
     e = pack_act_s2d(inv, in, int(p.u), int(p.v), int(p.pad_h), int(p.pad_w), IH, IW, Cp, a_hi,
-                     a_lo, st);
+                     a_lo, st, es);
   else
-    e = pack_act(inv, in, Cp, a_hi, a_lo, st);
+    e = pack_act(inv, in, Cp, a_hi, a_lo, st, es);
   if (e != cudaSuccess) return e;
-  return run_gemm(p, g, a_hi, a_lo, IH, IW, Cp, f, out, outv, alpha, beta, epi, st);
+  return run_gemm(p, g, a_hi, a_lo, IH, IW, Cp, f, out, outv, alpha, beta, epi, st, es);
 }
 
 }  // namespace
@@ -1399,32 +1409,34 @@ bool tc_eligible(const ConvProblem& p, int pass) {
 static tc::EpiOp no_epi() { return tc::EpiOp{-1, -1, nullptr, 0, nullptr}; }
 
 cudaError_t tc_forward(const ConvProblem& p, const float* x, const float* f, float* y,
-                       double alpha, double beta, cudaStream_t st) {
-  return tc::run_tc(false, p, x, p.x, f, y, p.y, float(alpha), float(beta), no_epi(), st);
+                       double alpha, double beta, cudaStream_t st, int es) {
+  return tc::run_tc(false, p, x, p.x, f, y, p.y, float(alpha), float(beta), no_epi(), st, es);
 }
 
 cudaError_t tc_backward_data(const ConvProblem& p, const float* dy, const float* f, float* dx,
-                             bool acc, cudaStream_t st) {
-  return tc::run_tc(true, p, dy, p.y, f, dx, p.x, 1.0f, acc ? 1.0f : 0.0f, no_epi(), st);
+                             bool acc, cudaStream_t st, int es) {
+  return tc::run_tc(true, p, dy, p.y, f, dx, p.x, 1.0f, acc ? 1.0f : 0.0f, no_epi(), st, es);
 }
 
 // Fused forms; cudaErrorNotSupported (before any write to the output) when
 // the geometry takes a kernel without the fused epilogue.
 cudaError_t tc_forward_fused(const ConvProblem& p, const float* x, const float* f, float* y,
-                             double alpha, double beta, const ConvEpilogue& ep, cudaStream_t st) {
+                             double alpha, double beta, const ConvEpilogue& ep, cudaStream_t st,
+                             int es) {
   tc::EpiOp e = no_epi();
   e.act = ep.act;
   e.bias = static_cast<const float*>(ep.bias);
   e.bias_sc = ep.bias_stride;
-  return tc::run_tc(false, p, x, p.x, f, y, p.y, float(alpha), float(beta), e, st);
+  return tc::run_tc(false, p, x, p.x, f, y, p.y, float(alpha), float(beta), e, st, es);
 }
 
 cudaError_t tc_backward_data_fused(const ConvProblem& p, const float* dy, const float* f,
-                                   float* dx, bool acc, const ConvEpilogue& ep, cudaStream_t st) {
+                                   float* dx, bool acc, const ConvEpilogue& ep, cudaStream_t st,
+                                   int es) {
   tc::EpiOp e = no_epi();
   e.gate = ep.gate;
   e.gatep = static_cast<const float*>(ep.gatep);
-  return tc::run_tc(true, p, dy, p.y, f, dx, p.x, 1.0f, acc ? 1.0f : 0.0f, e, st);
+  return tc::run_tc(true, p, dy, p.y, f, dx, p.x, 1.0f, acc ? 1.0f : 0.0f, e, st, es);
 }
 
 }  // namespace dnnp

@@ -30,7 +30,7 @@
 
 constexpr int kTmaThreads = 10 * 32;  // TMA warp, MMA warp, 8 epilogue warps
 constexpr int kColCache = 512;        // mode-1 column table cached in shared memory
-constexpr int kTK = 64;  // reduction depth of one stage (4 k-steps of 16)
+constexpr int kTK = 64;  // reduction depth of one BF16 stage (4 k-steps of 16)
 
 // Fused epilogue operations (additive C entries
 // dnnp_convolution_bias_activation_forward / _backward_data_activation).
@@ -211,12 +211,20 @@ struct TmaParams {
   unsigned long long* trace;   // debug: CTA-0 clock64 stamps (or null)
 };
 
-template <int BN, int CB, int NC>
+// ES: bytes per packed element, 2 = BF16x3 (kind::f16), 4 = 3xTF32
+// (kind::tf32, fp32 containers).  A stage always holds 128 bytes of
+// reduction per row (kTK bf16 or kTK / 2 tf32 channels) in four 32-byte
+// k-steps, so both splits share the stage geometry and the MMA schedule.
+template <int ES>
+constexpr int stage_depth() { return 128 / ES; }
+
+template <int BN, int CB, int NC, int ES>
 struct TCfg {
   static constexpr int BNL = BN / NC;        // filter rows loaded by each CTA
-  static constexpr int SUB = kTK / CB;       // chunks (sub-tiles) per stage
-  static constexpr int A_SUB = kBM * CB * 2; // bytes of one A sub-tile (one plane)
-  static constexpr int B_SUB = BNL * CB * 2;
+  static constexpr int SUB = stage_depth<ES>() / CB;  // chunks (sub-tiles) per stage
+  static constexpr int RB = CB * ES;         // bytes of one sub-tile row (swizzle span)
+  static constexpr int A_SUB = kBM * RB;     // bytes of one A sub-tile (one plane)
+  static constexpr int B_SUB = BNL * RB;
   static constexpr int A_BYTES = SUB * A_SUB;
   static constexpr int B_BYTES = SUB * B_SUB;
   static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;  // per CTA
@@ -229,10 +237,10 @@ struct TCfg {
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256 + COLTAB_BYTES;
 };
 
-template <int CB>
+template <int RB>  // row bytes of the K-major sub-tile
 __device__ __forceinline__ uint64_t tma_kdesc(uint32_t addr) {
-  if constexpr (CB == 64) return ptx::desc_kmajor_sw128(addr);
-  else if constexpr (CB == 32) return ptx::desc_kmajor_sw64(addr);
+  if constexpr (RB == 128) return ptx::desc_kmajor_sw128(addr);
+  else if constexpr (RB == 64) return ptx::desc_kmajor_sw64(addr);
   else return ptx::desc_kmajor_sw32(addr);
 }
 
@@ -315,9 +323,9 @@ struct WorkIter {
   }
 };
 
-template <int BN, int CB, int NC>
+template <int BN, int CB, int NC, int ES>
 __global__ void __launch_bounds__(kTmaThreads, 1) conv_tma_kernel(const __grid_constant__ TmaParams P) {
-  using C = TCfg<BN, CB, NC>;
+  using C = TCfg<BN, CB, NC, ES>;
   constexpr int S = C::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -452,7 +460,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1) conv_tma_kernel(const __grid_c
   } else if (warp == 1) {
     // ================================================ MMA issuer (leader CTA)
     if (leader) {
-      constexpr uint32_t idesc = ptx::idesc_bf16(kBM * NC, BN, 0, 0);
+      constexpr uint32_t idesc = ES == 4 ? ptx::idesc_tf32(kBM * NC, BN, 0, 0)
+                                         : ptx::idesc_bf16(kBM * NC, BN, 0, 0);
       int it = 0, lt = 0;
       while (wi.next(tile, kb0, kb1, piece, np)) {
         const int buf = lt & 1;
@@ -467,24 +476,21 @@ __global__ void __launch_bounds__(kTmaThreads, 1) conv_tma_kernel(const __grid_c
           if (P.trace && blockIdx.x == 0 && it < 1024 && lane == 0) P.trace[it * 4 + 2] = clock64();
           const uint32_t base = smem0 + s * C::STAGE_BYTES;
 #pragma unroll
-          for (int kk = 0; kk < kTK / 16 && !(P.skip & 4); kk++) {
-            // 16-deep k-step kk: sub-tile kk / (CB/16), +32 B per step inside its rows
-            const int sub = kk / (CB / 16), ko = (kk % (CB / 16)) * 32;
+          for (int kk = 0; kk < 4 && !(P.skip & 4); kk++) {
+            // 32-byte k-step kk (16 bf16 / 8 tf32 deep): sub-tile kk / (RB/32),
+            // +32 B per step inside its rows
+            constexpr int KPS = C::RB / 32;  // k-steps per sub-tile row
+            const int sub = kk / KPS, ko = (kk % KPS) * 32;
             const uint32_t ao = uint32_t(sub * C::A_SUB + ko);
             const uint32_t bo = uint32_t(sub * C::B_SUB + ko);
-            const uint64_t dah = tma_kdesc<CB>(base + ao);
-            const uint64_t dal = tma_kdesc<CB>(base + C::A_BYTES + ao);
-            const uint64_t dbh = tma_kdesc<CB>(base + 2 * C::A_BYTES + bo);
-            const uint64_t dbl = tma_kdesc<CB>(base + 2 * C::A_BYTES + C::B_BYTES + bo);
-            if constexpr (NC == 2) {
-              ptx::mma_bf16_pair_elect(dacc, dal, dbh, idesc, acc);
-              ptx::mma_bf16_pair_elect(dacc, dah, dbl, idesc, 1);
-              ptx::mma_bf16_pair_elect(dacc, dah, dbh, idesc, 1);
-            } else {
-              ptx::mma_bf16_elect(dacc, dal, dbh, idesc, acc);
-              ptx::mma_bf16_elect(dacc, dah, dbl, idesc, 1);
-              ptx::mma_bf16_elect(dacc, dah, dbh, idesc, 1);
-            }
+            const uint64_t dah = tma_kdesc<C::RB>(base + ao);
+            const uint64_t dal = tma_kdesc<C::RB>(base + C::A_BYTES + ao);
+            const uint64_t dbh = tma_kdesc<C::RB>(base + 2 * C::A_BYTES + bo);
+            const uint64_t dbl = tma_kdesc<C::RB>(base + 2 * C::A_BYTES + C::B_BYTES + bo);
+            // lo.hi + hi.lo + hi.hi into one fp32 accumulator (lo.lo dropped)
+            ptx::mma_split_elect<NC, ES>(dacc, dal, dbh, idesc, acc);
+            ptx::mma_split_elect<NC, ES>(dacc, dah, dbl, idesc, 1);
+            ptx::mma_split_elect<NC, ES>(dacc, dah, dbh, idesc, 1);
             acc = 1;
           }
           if constexpr (NC == 2) ptx::mma_commit_pair_elect(&empty[s]);

@@ -30,10 +30,10 @@ struct S2dGeom {
   int u, v, pad_h, pad_w;
 };
 
-template <bool S2D>
+template <bool S2D, int ES>
 __global__ void __launch_bounds__(256) pack_act_kernel(View4 v, const float* __restrict__ x, int Cp,
-                                                       __nv_bfloat16* __restrict__ hi,
-                                                       __nv_bfloat16* __restrict__ lo, int64_t npix,
+                                                       void* __restrict__ hi,
+                                                       void* __restrict__ lo, int64_t npix,
                                                        MagicDiv dHW, MagicDiv dW, S2dGeom sg) {
   __shared__ float tile[kCh][kPix + 1];
   const int lp = threadIdx.x & 31, lc = threadIdx.x >> 5;  // read role: pixel, channel phase
@@ -81,12 +81,11 @@ __global__ void __launch_bounds__(256) pack_act_kernel(View4 v, const float* __r
     __syncthreads();
     const int64_t opix = int64_t(pt) * kPix + wp;
     if (opix < npix && wg * 8 < nch) {
-      __align__(16) __nv_bfloat16 vh[8], vl[8];
+      float v8[8];
 #pragma unroll
-      for (int k = 0; k < 8; k++) split_bf16(tile[wg * 8 + k][wp], vh[k], vl[k]);
+      for (int k = 0; k < 8; k++) v8[k] = tile[wg * 8 + k][wp];
       const int64_t o = opix * Cp + c_lo + wg * 8;
-      *reinterpret_cast<uint4*>(hi + o) = *reinterpret_cast<const uint4*>(vh);
-      *reinterpret_cast<uint4*>(lo + o) = *reinterpret_cast<const uint4*>(vl);
+      store_split8<ES>(hi, lo, o, v8);
     }
     __syncthreads();
   }
@@ -95,10 +94,10 @@ __global__ void __launch_bounds__(256) pack_act_kernel(View4 v, const float* __r
 // Same transpose with 64-pixel jobs: each thread loads 16 values (two
 // 32-pixel halves x 8 channel phases) before the barrier, twice the bytes in
 // flight per synchronisation of the 32-pixel version.
-template <int PIXJ>
+template <int PIXJ, int ES>
 __global__ void __launch_bounds__(256) pack_act_wide_kernel(View4 v, const float* __restrict__ x,
-                                                            int Cp, __nv_bfloat16* __restrict__ hi,
-                                                            __nv_bfloat16* __restrict__ lo,
+                                                            int Cp, void* __restrict__ hi,
+                                                            void* __restrict__ lo,
                                                             uint32_t npix, MagicDiv dHW,
                                                             MagicDiv dW) {
   __shared__ float tile[kCh][PIXJ + 1];
@@ -140,12 +139,11 @@ __global__ void __launch_bounds__(256) pack_act_wide_kernel(View4 v, const float
       const int px = hf * 32 + wp;
       const uint32_t opix = pt * PIXJ + px;
       if (opix < npix && wg * 8 < nch) {
-        __align__(16) __nv_bfloat16 vh[8], vl[8];
+        float v8[8];
 #pragma unroll
-        for (int k = 0; k < 8; k++) split_bf16(tile[wg * 8 + k][px], vh[k], vl[k]);
+        for (int k = 0; k < 8; k++) v8[k] = tile[wg * 8 + k][px];
         const int64_t o = int64_t(opix) * Cp + c_lo + wg * 8;
-        *reinterpret_cast<uint4*>(hi + o) = *reinterpret_cast<const uint4*>(vh);
-        *reinterpret_cast<uint4*>(lo + o) = *reinterpret_cast<const uint4*>(vl);
+        store_split8<ES>(hi, lo, o, v8);
       }
     }
     __syncthreads();
@@ -154,9 +152,10 @@ __global__ void __launch_bounds__(256) pack_act_wide_kernel(View4 v, const float
 
 // Cp <= 16: one thread per pixel reads its C values (pixel-contiguous across
 // the warp for NCHW) and writes Cp/8 16-byte chunks (contiguous across the warp).
+template <int ES>
 __global__ void __launch_bounds__(256) pack_act_small_kernel(View4 v, const float* __restrict__ x,
-                                                             int Cp, __nv_bfloat16* __restrict__ hi,
-                                                             __nv_bfloat16* __restrict__ lo,
+                                                             int Cp, void* __restrict__ hi,
+                                                             void* __restrict__ lo,
                                                              int64_t npix, MagicDiv dHW, MagicDiv dW) {
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   for (int64_t pix = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; pix < npix; pix += stride) {
@@ -165,15 +164,14 @@ __global__ void __launch_bounds__(256) pack_act_small_kernel(View4 v, const floa
     mdivmod(rem, dW, h, w);
     const float* src = x + int64_t(n) * v.sn + int64_t(h) * v.sh + int64_t(w) * v.sw;
     for (int g = 0; g < Cp / 8; g++) {
-      __align__(16) __nv_bfloat16 vh[8], vl[8];
+      float v8[8];
 #pragma unroll
       for (int k = 0; k < 8; k++) {
         const int c = g * 8 + k;
-        split_bf16(c < v.c ? __ldg(src + int64_t(c) * v.sc) : 0.0f, vh[k], vl[k]);
+        v8[k] = c < v.c ? __ldg(src + int64_t(c) * v.sc) : 0.0f;
       }
       const int64_t o = pix * Cp + g * 8;
-      *reinterpret_cast<uint4*>(hi + o) = *reinterpret_cast<const uint4*>(vh);
-      *reinterpret_cast<uint4*>(lo + o) = *reinterpret_cast<const uint4*>(vl);
+      store_split8<ES>(hi, lo, o, v8);
     }
   }
 }
@@ -181,11 +179,12 @@ __global__ void __launch_bounds__(256) pack_act_small_kernel(View4 v, const floa
 // Space-to-depth: one thread per super-pixel (n, h', w'); walks its Cp
 // channels (rh, rw, c) with running counters and writes 16-byte chunks
 // (contiguous across the warp).
+template <int ES>
 __global__ void __launch_bounds__(256) pack_act_s2d_kernel(View4 v, const float* __restrict__ x,
                                                            int u, int vv, int pad_h, int pad_w,
                                                            int H2, int W2, int Cp,
-                                                           __nv_bfloat16* __restrict__ hi,
-                                                           __nv_bfloat16* __restrict__ lo,
+                                                           void* __restrict__ hi,
+                                                           void* __restrict__ lo,
                                                            int64_t npix, MagicDiv dHW, MagicDiv dW) {
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   const int C = int(v.c), Cs = u * vv * C;
@@ -197,7 +196,7 @@ __global__ void __launch_bounds__(256) pack_act_s2d_kernel(View4 v, const float*
     const float* src = x + int64_t(n) * v.sn;
     int c = 0, rw = 0, rh = 0;
     for (int g = 0; g < Cp / 8; g++) {
-      __align__(16) __nv_bfloat16 vh[8], vl[8];
+      float v8[8];
 #pragma unroll
       for (int k = 0; k < 8; k++) {
         float val = 0.0f;
@@ -213,11 +212,10 @@ __global__ void __launch_bounds__(256) pack_act_s2d_kernel(View4 v, const float*
             }
           }
         }
-        split_bf16(val, vh[k], vl[k]);
+        v8[k] = val;
       }
       const int64_t o = pix * Cp + g * 8;
-      *reinterpret_cast<uint4*>(hi + o) = *reinterpret_cast<const uint4*>(vh);
-      *reinterpret_cast<uint4*>(lo + o) = *reinterpret_cast<const uint4*>(vl);
+      store_split8<ES>(hi, lo, o, v8);
     }
   }
 }
@@ -226,11 +224,12 @@ __global__ void __launch_bounds__(256) pack_act_s2d_kernel(View4 v, const float*
 // every channel are read coalesced along w into shared memory as
 // [w'][(rh*v + rw)*C + c], then the contiguous W' x Cp output row is written
 // with 16-byte stores.
+template <int ES>
 __global__ void __launch_bounds__(256) pack_act_s2d_row_kernel(View4 v, const float* __restrict__ x,
                                                                int u, int vv, int pad_h, int pad_w,
                                                                int H2, int W2, int Cp,
-                                                               __nv_bfloat16* __restrict__ hi,
-                                                               __nv_bfloat16* __restrict__ lo) {
+                                                               void* __restrict__ hi,
+                                                               void* __restrict__ lo) {
   extern __shared__ float srow[];
   const int Cps = Cp + 1;  // odd pitch: fewer bank conflicts on the scatter
   const int C = int(v.c);
@@ -260,12 +259,11 @@ __global__ void __launch_bounds__(256) pack_act_s2d_row_kernel(View4 v, const fl
     const int64_t obase = int64_t(row) * W2 * Cp;
     for (int t = threadIdx.x; t < W2 * groups; t += blockDim.x) {
       const int w2 = t / groups, g = t - w2 * groups;
-      __align__(16) __nv_bfloat16 vh[8], vl[8];
+      float v8[8];
 #pragma unroll
-      for (int k = 0; k < 8; k++) split_bf16(srow[w2 * Cps + g * 8 + k], vh[k], vl[k]);
+      for (int k = 0; k < 8; k++) v8[k] = srow[w2 * Cps + g * 8 + k];
       const int64_t o = obase + int64_t(w2) * Cp + g * 8;
-      *reinterpret_cast<uint4*>(hi + o) = *reinterpret_cast<const uint4*>(vh);
-      *reinterpret_cast<uint4*>(lo + o) = *reinterpret_cast<const uint4*>(vl);
+      store_split8<ES>(hi, lo, o, v8);
     }
     __syncthreads();
   }
@@ -276,11 +274,12 @@ __global__ void __launch_bounds__(256) pack_act_s2d_row_kernel(View4 v, const fl
 // 16-byte loads into shared memory (zero margins for the padding), then the
 // W' x Cp output row -- contiguous in the packed plane -- is written with
 // 16-byte stores.
+template <int ES>
 __global__ void __launch_bounds__(256) pack_act_s2d_dense_kernel(View4 v, const float* __restrict__ x,
                                                                  int u, int vv, int pad_h, int pad_w,
                                                                  int H2, int W2, int Cp,
-                                                                 __nv_bfloat16* __restrict__ hi,
-                                                                 __nv_bfloat16* __restrict__ lo) {
+                                                                 void* __restrict__ hi,
+                                                                 void* __restrict__ lo) {
   extern __shared__ float srow[];  // [C*u][SW], SW = W2*v rounded up to 4
   const int C = int(v.c), W = int(v.w);
   const int SW = (W2 * vv + 3) & ~3;
@@ -310,7 +309,7 @@ __global__ void __launch_bounds__(256) pack_act_s2d_dense_kernel(View4 v, const 
   const int64_t obase = int64_t(row) * W2 * Cp;
   for (int t = threadIdx.x; t < W2 * groups; t += blockDim.x) {
     const int w2 = t / groups, g = t - w2 * groups;
-    __align__(16) __nv_bfloat16 vh[8], vl[8];
+    float v8[8];
 #pragma unroll
     for (int k = 0; k < 8; k++) {
       const int cp = g * 8 + k;
@@ -320,11 +319,10 @@ __global__ void __launch_bounds__(256) pack_act_s2d_dense_kernel(View4 v, const 
         const int rh = qq / vv, rw = qq - rh * vv;
         val = srow[(c * u + rh) * SW + w2 * vv + rw];
       }
-      split_bf16(val, vh[k], vl[k]);
+      v8[k] = val;
     }
     const int64_t o = obase + int64_t(w2) * Cp + g * 8;
-    *reinterpret_cast<uint4*>(hi + o) = *reinterpret_cast<const uint4*>(vh);
-    *reinterpret_cast<uint4*>(lo + o) = *reinterpret_cast<const uint4*>(vl);
+    store_split8<ES>(hi, lo, o, v8);
   }
 }
 
@@ -337,12 +335,12 @@ __global__ void __launch_bounds__(256) pack_act_s2d_dense_kernel(View4 v, const 
 // then each thread splits and writes 16-byte hi / lo chunks of the
 // contiguous 64 x Cp output block.  (32 super-pixels per block: 3.4 TB/s,
 // latency-bound; measured per call under ncu.)
-template <int V>
+template <int V, int ES>
 __global__ void __launch_bounds__(512) pack_act_s2d_quad_kernel(View4 v, const float* __restrict__ x,
                                                                 int u, int pad_h, int pad_w, int H2,
                                                                 int W2, int Cp, int nwb,
-                                                                __nv_bfloat16* __restrict__ hi,
-                                                                __nv_bfloat16* __restrict__ lo) {
+                                                                void* __restrict__ hi,
+                                                                void* __restrict__ lo) {
   constexpr int PIX = 64;           // super-pixels per block (two per lane): ~2x the bytes in flight
   extern __shared__ float stile[];  // [PIX][Cp + 1]
   const int C = int(v.c), Cs = u * V * C, pitch = Cp + 1;
@@ -388,22 +386,22 @@ __global__ void __launch_bounds__(512) pack_act_s2d_quad_kernel(View4 v, const f
   for (int t = threadIdx.x; t < PIX * groups; t += blockDim.x) {
     const int pi = t / groups, g = t - pi * groups;
     if (int(wb) * PIX + pi >= W2) continue;
-    __align__(16) __nv_bfloat16 vh[8], vl[8];
+    float v8[8];
 #pragma unroll
-    for (int k = 0; k < 8; k++) split_bf16(stile[pi * pitch + g * 8 + k], vh[k], vl[k]);
+    for (int k = 0; k < 8; k++) v8[k] = stile[pi * pitch + g * 8 + k];
     const int64_t o = obase + int64_t(pi) * Cp + g * 8;
-    *reinterpret_cast<uint4*>(hi + o) = *reinterpret_cast<const uint4*>(vh);
-    *reinterpret_cast<uint4*>(lo + o) = *reinterpret_cast<const uint4*>(vl);
+    store_split8<ES>(hi, lo, o, v8);
   }
 }
 
 // Tap folding: one thread per output pixel (n, h, q), walking its Cp folded
 // channels (j, c) with running counters; loads are pixel-consecutive across
 // the warp (w = q v + j - pad_w), writes 16-byte hi / lo chunks.
+template <int ES>
 __global__ void __launch_bounds__(256) pack_act_fold_kernel(View4 v, const float* __restrict__ x,
                                                             int S, int vv, int pad_w, int Q,
-                                                            int Cp, __nv_bfloat16* __restrict__ hi,
-                                                            __nv_bfloat16* __restrict__ lo,
+                                                            int Cp, void* __restrict__ hi,
+                                                            void* __restrict__ lo,
                                                             uint32_t npix, MagicDiv dHQ,
                                                             MagicDiv dQ) {
   const int C = int(v.c), Cs = S * C;
@@ -416,7 +414,7 @@ __global__ void __launch_bounds__(256) pack_act_fold_kernel(View4 v, const float
     const int wb = int(q) * vv - pad_w;
     int c = 0, j = 0;
     for (int g = 0; g < Cp / 8; g++) {
-      __align__(16) __nv_bfloat16 vh[8], vl[8];
+      float v8[8];
 #pragma unroll
       for (int k = 0; k < 8; k++) {
         float val = 0.0f;
@@ -428,19 +426,19 @@ __global__ void __launch_bounds__(256) pack_act_fold_kernel(View4 v, const float
             ++j;
           }
         }
-        split_bf16(val, vh[k], vl[k]);
+        v8[k] = val;
       }
       const int64_t o = int64_t(pix) * Cp + g * 8;
-      *reinterpret_cast<uint4*>(hi + o) = *reinterpret_cast<const uint4*>(vh);
-      *reinterpret_cast<uint4*>(lo + o) = *reinterpret_cast<const uint4*>(vl);
+      store_split8<ES>(hi, lo, o, v8);
     }
   }
 }
 
 }  // namespace
 
-cudaError_t pack_act_s2d(const View4& v, const float* x, int u, int vv, int pad_h, int pad_w,
-                         int H2, int W2, int Cp, __nv_bfloat16* hi, __nv_bfloat16* lo,
+template <int ES>
+static cudaError_t pack_act_s2d_t(const View4& v, const float* x, int u, int vv, int pad_h, int pad_w,
+                         int H2, int W2, int Cp, void* hi, void* lo,
                          cudaStream_t st) {
   const int64_t npix = v.n * H2 * W2;
   if (npix >= (int64_t(1) << 32)) return cudaErrorInvalidValue;
@@ -457,13 +455,13 @@ cudaError_t pack_act_s2d(const View4& v, const float* x, int u, int vv, int pad_
       const int threads = int(std::min<int64_t>(512, std::max<int64_t>(128, v.c * u * 32)));
       cudaError_t e;
       if (vv == 2)
-        pack_act_s2d_quad_kernel<2><<<grid, threads, sm, st>>>(v, x, u, pad_h, pad_w, H2, W2, Cp,
+        pack_act_s2d_quad_kernel<2, ES><<<grid, threads, sm, st>>>(v, x, u, pad_h, pad_w, H2, W2, Cp,
                                                                nwb, hi, lo);
       else if (vv == 4)
-        pack_act_s2d_quad_kernel<4><<<grid, threads, sm, st>>>(v, x, u, pad_h, pad_w, H2, W2, Cp,
+        pack_act_s2d_quad_kernel<4, ES><<<grid, threads, sm, st>>>(v, x, u, pad_h, pad_w, H2, W2, Cp,
                                                                nwb, hi, lo);
       else
-        pack_act_s2d_quad_kernel<8><<<grid, threads, sm, st>>>(v, x, u, pad_h, pad_w, H2, W2, Cp,
+        pack_act_s2d_quad_kernel<8, ES><<<grid, threads, sm, st>>>(v, x, u, pad_h, pad_w, H2, W2, Cp,
                                                                nwb, hi, lo);
       e = cudaGetLastError();
       note_launch();
@@ -478,7 +476,7 @@ cudaError_t pack_act_s2d(const View4& v, const float* x, int u, int vv, int pad_
                        (v.sc % 4) == 0 && sm <= 48 * 1024 && W2 * vv >= v.w + pad_w &&
                        ::dnnp::tune_env("DNNP_S2D_DENSE") != nullptr;
     if (dense && v.n * H2 < (int64_t(1) << 31)) {
-      pack_act_s2d_dense_kernel<<<unsigned(v.n * H2), 256, sm, st>>>(v, x, u, vv, pad_h, pad_w, H2,
+      pack_act_s2d_dense_kernel<ES><<<unsigned(v.n * H2), 256, sm, st>>>(v, x, u, vv, pad_h, pad_w, H2,
                                                                      W2, Cp, hi, lo);
       note_launch();
       return cudaGetLastError();
@@ -488,7 +486,7 @@ cudaError_t pack_act_s2d(const View4& v, const float* x, int u, int vv, int pad_
     const int64_t jobs = ceil_div(npix, kPix) * ceil_div(Cp, kCh);
     if (jobs >= (int64_t(1) << 31)) return cudaErrorInvalidValue;
     const unsigned grid = unsigned(std::min<int64_t>(jobs, int64_t(kNumSMs) * 32));
-    pack_act_kernel<true><<<grid, 256, 0, st>>>(v, x, Cp, hi, lo, npix,
+    pack_act_kernel<true, ES><<<grid, 256, 0, st>>>(v, x, Cp, hi, lo, npix,
                                                 make_magic(uint32_t(H2 * W2)), make_magic(uint32_t(W2)),
                                                 S2dGeom{u, vv, pad_h, pad_w});
     note_launch();
@@ -497,16 +495,22 @@ cudaError_t pack_act_s2d(const View4& v, const float* x, int u, int vv, int pad_
   const size_t row_smem = size_t(W2) * (Cp + 1) * sizeof(float);
   if (::dnnp::tune_env("DNNP_S2D_ROWS") && row_smem <= 48 * 1024 && v.n * H2 < (int64_t(1) << 31)) {
     const unsigned grid = unsigned(std::min<int64_t>(v.n * H2, int64_t(kNumSMs) * 8));
-    pack_act_s2d_row_kernel<<<grid, 256, row_smem, st>>>(v, x, u, vv, pad_h, pad_w, H2, W2, Cp, hi,
+    pack_act_s2d_row_kernel<ES><<<grid, 256, row_smem, st>>>(v, x, u, vv, pad_h, pad_w, H2, W2, Cp, hi,
                                                          lo);
     note_launch();
     return cudaGetLastError();
   }
-  pack_act_s2d_kernel<<<grid_for(npix, 256, 8), 256, 0, st>>>(
+  pack_act_s2d_kernel<ES><<<grid_for(npix, 256, 8), 256, 0, st>>>(
       v, x, u, vv, pad_h, pad_w, H2, W2, Cp, hi, lo, npix, make_magic(uint32_t(H2 * W2)),
       make_magic(uint32_t(W2)));
   note_launch();
   return cudaGetLastError();
+}
+
+cudaError_t pack_act_s2d(const View4& v, const float* x, int u, int vv, int pad_h, int pad_w,
+                         int H2, int W2, int Cp, void* hi, void* lo,
+                         cudaStream_t st, int es) {
+  return es == 4 ? pack_act_s2d_t<4>(v, x, u, vv, pad_h, pad_w, H2, W2, Cp, hi, lo, st) : pack_act_s2d_t<2>(v, x, u, vv, pad_h, pad_w, H2, W2, Cp, hi, lo, st);
 }
 
 struct ArenaState {
@@ -747,9 +751,13 @@ cudaMemPool_t lib_pool() {
 
 void pool_keep_memory() { (void)lib_pool(); }
 
+static CUtensorMapDataType tmap_dtype(int es) {
+  return es == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+}
+
 cudaError_t make_tmap_2d(CUtensorMap* map, const void* base, uint64_t cols, uint64_t rows,
                          uint64_t pitch_elems, uint32_t box_cols, uint32_t box_rows,
-                         CUtensorMapSwizzle swizzle) {
+                         CUtensorMapSwizzle swizzle, int es) {
   using Fn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                           const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
                           CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
@@ -763,10 +771,10 @@ cudaError_t make_tmap_2d(CUtensorMap* map, const void* base, uint64_t cols, uint
     fn = reinterpret_cast<Fn>(p);
   }
   const cuuint64_t dims[2] = {cols, rows};
-  const cuuint64_t strides[1] = {pitch_elems * 2};
+  const cuuint64_t strides[1] = {pitch_elems * cuuint64_t(es)};
   const cuuint32_t box[2] = {box_cols, box_rows};
   const cuuint32_t estr[2] = {1, 1};
-  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
+  CUresult r = fn(map, tmap_dtype(es), 2, const_cast<void*>(base), dims, strides,
                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
@@ -774,7 +782,7 @@ cudaError_t make_tmap_2d(CUtensorMap* map, const void* base, uint64_t cols, uint
 
 cudaError_t make_tmap_3d(CUtensorMap* map, const void* base, const uint64_t dims[3],
                          const uint64_t strides_bytes[2], const uint32_t box[3],
-                         CUtensorMapSwizzle swizzle) {
+                         CUtensorMapSwizzle swizzle, int es) {
   using Fn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                           const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
                           CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
@@ -791,14 +799,14 @@ cudaError_t make_tmap_3d(CUtensorMap* map, const void* base, const uint64_t dims
   const cuuint64_t st[2] = {strides_bytes[0], strides_bytes[1]};
   const cuuint32_t b[3] = {box[0], box[1], box[2]};
   const cuuint32_t estr[3] = {1, 1, 1};
-  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), d, st, b, estr,
+  CUresult r = fn(map, tmap_dtype(es), 3, const_cast<void*>(base), d, st, b, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
 cudaError_t make_tmap_im2col(CUtensorMap* map, const void* base, const Im2colGeom& g,
-                             CUtensorMapSwizzle swizzle) {
+                             CUtensorMapSwizzle swizzle, int es) {
   using Fn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                           const cuuint64_t*, const int*, const int*, cuuint32_t, cuuint32_t,
                           const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
@@ -812,12 +820,13 @@ cudaError_t make_tmap_im2col(CUtensorMap* map, const void* base, const Im2colGeo
     fn = reinterpret_cast<Fn>(p);
   }
   const cuuint64_t dims[4] = {cuuint64_t(g.C), cuuint64_t(g.W), cuuint64_t(g.H), cuuint64_t(g.N)};
-  const cuuint64_t strides[3] = {cuuint64_t(g.C) * 2, cuuint64_t(g.C) * 2 * g.W,
-                                 cuuint64_t(g.C) * 2 * g.W * g.H};
+  const cuuint64_t eb = cuuint64_t(es);
+  const cuuint64_t strides[3] = {cuuint64_t(g.C) * eb, cuuint64_t(g.C) * eb * g.W,
+                                 cuuint64_t(g.C) * eb * g.W * g.H};
   const int lower[2] = {g.lower_w, g.lower_h};  // W first (innermost spatial dim)
   const int upper[2] = {g.upper_w, g.upper_h};
   const cuuint32_t estr[4] = {1, cuuint32_t(g.stride_w), cuuint32_t(g.stride_h), 1};
-  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides,
+  CUresult r = fn(map, tmap_dtype(es), 4, const_cast<void*>(base), dims, strides,
                   lower, upper, cuuint32_t(g.cpp), cuuint32_t(g.ppc), estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -828,21 +837,22 @@ struct PackedRef {
   const float* src = nullptr;
   View4 v{};
   int Cp = 0;
-  const __nv_bfloat16* hi = nullptr;
-  const __nv_bfloat16* lo = nullptr;
+  int es = 2;
+  const void* hi = nullptr;
+  const void* lo = nullptr;
 };
 static thread_local PackedRef g_packed;
 
-void packed_set(const float* src, const View4& v, int Cp, const __nv_bfloat16* hi,
-                const __nv_bfloat16* lo) {
-  g_packed = PackedRef{src, v, Cp, hi, lo};
+void packed_set(const float* src, const View4& v, int Cp, const void* hi, const void* lo, int es) {
+  g_packed = PackedRef{src, v, Cp, es, hi, lo};
 }
 
-bool packed_get(const float* src, const View4& v, int Cp, const __nv_bfloat16** hi,
-                const __nv_bfloat16** lo) {
+bool packed_get(const float* src, const View4& v, int Cp, const void** hi, const void** lo,
+                int es) {
   const PackedRef& r = g_packed;
-  if (!r.src || r.src != src || r.Cp != Cp || r.v.n != v.n || r.v.c != v.c || r.v.h != v.h ||
-      r.v.w != v.w || r.v.sn != v.sn || r.v.sc != v.sc || r.v.sh != v.sh || r.v.sw != v.sw)
+  if (!r.src || r.src != src || r.Cp != Cp || r.es != es || r.v.n != v.n || r.v.c != v.c ||
+      r.v.h != v.h || r.v.w != v.w || r.v.sn != v.sn || r.v.sc != v.sc || r.v.sh != v.sh ||
+      r.v.sw != v.sw)
     return false;
   *hi = r.hi;
   *lo = r.lo;
@@ -857,10 +867,10 @@ cudaError_t shared_dy_pack(ScratchScope* sc, const View4& v, const float* dy, in
   void* buf = nullptr;
   cudaError_t e = scratch_alloc(sc, elems * 4, &buf);
   if (e != cudaSuccess) return e;
-  auto* hi = static_cast<__nv_bfloat16*>(buf);
+  auto* hi = static_cast<__nv_bfloat16*>(buf);  // BF16x3 planes (the default math)
   auto* lo = hi + elems;
   if ((e = pack_act(v, dy, Cp, hi, lo, st)) != cudaSuccess) return e;
-  packed_set(dy, v, Cp, hi, lo);
+  packed_set(dy, v, Cp, hi, lo, 2);
   return cudaSuccess;
 }
 
@@ -873,23 +883,30 @@ bool fold_taps(int64_t C, int64_t S, int64_t u, int64_t v, bool s2d) {
   return folded * 4 <= plain * 3;
 }
 
-cudaError_t pack_act_fold(const View4& v, const float* x, int S, int vv, int pad_w, int Q, int Cp,
-                          __nv_bfloat16* hi, __nv_bfloat16* lo, cudaStream_t st) {
+template <int ES>
+static cudaError_t pack_act_fold_t(const View4& v, const float* x, int S, int vv, int pad_w, int Q, int Cp,
+                          void* hi, void* lo, cudaStream_t st) {
   const int64_t npix = v.n * v.h * Q;
   if (npix >= (int64_t(1) << 32)) return cudaErrorInvalidValue;
-  pack_act_fold_kernel<<<grid_for(npix, 256, 8), 256, 0, st>>>(
+  pack_act_fold_kernel<ES><<<grid_for(npix, 256, 8), 256, 0, st>>>(
       v, x, S, vv, pad_w, Q, Cp, hi, lo, uint32_t(npix), make_magic(uint32_t(v.h * Q)),
       make_magic(uint32_t(Q)));
   note_launch();
   return cudaGetLastError();
 }
 
-cudaError_t pack_act(const View4& v, const float* x, int Cp, __nv_bfloat16* hi, __nv_bfloat16* lo,
+cudaError_t pack_act_fold(const View4& v, const float* x, int S, int vv, int pad_w, int Q, int Cp,
+                          void* hi, void* lo, cudaStream_t st, int es) {
+  return es == 4 ? pack_act_fold_t<4>(v, x, S, vv, pad_w, Q, Cp, hi, lo, st) : pack_act_fold_t<2>(v, x, S, vv, pad_w, Q, Cp, hi, lo, st);
+}
+
+template <int ES>
+static cudaError_t pack_act_t(const View4& v, const float* x, int Cp, void* hi, void* lo,
                      cudaStream_t st) {
   const int64_t npix = v.n * v.h * v.w;
   if (npix >= (int64_t(1) << 32)) return cudaErrorInvalidValue;
   if (Cp <= 16) {
-    pack_act_small_kernel<<<grid_for(npix, 256, 8), 256, 0, st>>>(
+    pack_act_small_kernel<ES><<<grid_for(npix, 256, 8), 256, 0, st>>>(
         v, x, Cp, hi, lo, npix, make_magic(uint32_t(v.h * v.w)), make_magic(uint32_t(v.w)));
     note_launch();
     return cudaGetLastError();
@@ -900,11 +917,11 @@ cudaError_t pack_act(const View4& v, const float* x, int Cp, __nv_bfloat16* hi, 
     if (jobs >= (int64_t(1) << 31)) return cudaErrorInvalidValue;
     const unsigned grid = unsigned(std::min<int64_t>(jobs, int64_t(kNumSMs) * 16));
     if (pj == 64)
-      pack_act_wide_kernel<64><<<grid, 256, 0, st>>>(v, x, Cp, hi, lo, uint32_t(npix),
+      pack_act_wide_kernel<64, ES><<<grid, 256, 0, st>>>(v, x, Cp, hi, lo, uint32_t(npix),
                                                      make_magic(uint32_t(v.h * v.w)),
                                                      make_magic(uint32_t(v.w)));
     else
-      pack_act_wide_kernel<128><<<grid, 256, 0, st>>>(v, x, Cp, hi, lo, uint32_t(npix),
+      pack_act_wide_kernel<128, ES><<<grid, 256, 0, st>>>(v, x, Cp, hi, lo, uint32_t(npix),
                                                       make_magic(uint32_t(v.h * v.w)),
                                                       make_magic(uint32_t(v.w)));
     note_launch();
@@ -913,11 +930,16 @@ cudaError_t pack_act(const View4& v, const float* x, int Cp, __nv_bfloat16* hi, 
   const int64_t jobs = ceil_div(npix, kPix) * ceil_div(Cp, kCh);
   if (jobs >= (int64_t(1) << 31)) return cudaErrorInvalidValue;
   const unsigned grid = unsigned(std::min<int64_t>(jobs, int64_t(kNumSMs) * 32));
-  pack_act_kernel<false><<<grid, 256, 0, st>>>(v, x, Cp, hi, lo, npix,
+  pack_act_kernel<false, ES><<<grid, 256, 0, st>>>(v, x, Cp, hi, lo, npix,
                                                make_magic(uint32_t(v.h * v.w)),
                                                make_magic(uint32_t(v.w)), S2dGeom{1, 1, 0, 0});
   note_launch();
   return cudaGetLastError();
+}
+
+cudaError_t pack_act(const View4& v, const float* x, int Cp, void* hi, void* lo,
+                     cudaStream_t st, int es) {
+  return es == 4 ? pack_act_t<4>(v, x, Cp, hi, lo, st) : pack_act_t<2>(v, x, Cp, hi, lo, st);
 }
 
 }  // namespace tc

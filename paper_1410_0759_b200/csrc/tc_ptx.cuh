@@ -290,6 +290,16 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, int a_mn_major, 
          (uint32_t(N >> 3) << 17) | (uint32_t(M >> 4) << 24);
 }
 
+// Instruction descriptor, kind::tf32 (A / B format TF32 = 2) with FP32
+// accumulate; operands are fp32 containers, the low 13 mantissa bits unused.
+__host__ __device__ constexpr uint32_t idesc_tf32(int M, int N, int a_mn_major, int b_mn_major) {
+  return (1u << 4)                 // D format F32
+         | (2u << 7)               // A format TF32
+         | (2u << 10)              // B format TF32
+         | (uint32_t(a_mn_major) << 15) | (uint32_t(b_mn_major) << 16) |
+         (uint32_t(N >> 3) << 17) | (uint32_t(M >> 4) << 24);
+}
+
 __device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
                                          uint32_t idesc, uint32_t accumulate) {
   asm volatile(
@@ -349,6 +359,60 @@ __device__ __forceinline__ void mma_commit_pair_elect(uint64_t* bar) {
       "h"(uint16_t(3))
       : "memory");
 }
+__device__ __forceinline__ void mma_tf32_elect(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                               uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred e, p;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void mma_tf32_pair_elect(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                                    uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred e, p;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// One product of the split (BF16x3: ES = 2, kind::f16; 3xTF32: ES = 4,
+// kind::tf32) on one CTA (NC = 1) or a CTA pair (NC = 2).
+template <int NC, int ES>
+__device__ __forceinline__ void mma_split_elect(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                                uint32_t idesc, uint32_t accumulate) {
+  if constexpr (ES == 4) {
+    if constexpr (NC == 2) mma_tf32_pair_elect(tmem_d, adesc, bdesc, idesc, accumulate);
+    else mma_tf32_elect(tmem_d, adesc, bdesc, idesc, accumulate);
+  } else {
+    if constexpr (NC == 2) mma_bf16_pair_elect(tmem_d, adesc, bdesc, idesc, accumulate);
+    else mma_bf16_elect(tmem_d, adesc, bdesc, idesc, accumulate);
+  }
+}
+
+// MN-major operand tile for 32-bit (tf32) elements: the TMA
+// CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B image, descriptor layout type 1
+// (SWIZZLE_128B_BASE32B): 32 MN-contiguous tf32 per 128-byte row, 4-row
+// swizzle atoms (SBO = 512 B), LBO = byte stride between 32-wide MN blocks.
+// Verified on B200 by tools/probe_tf32.cu (the 8-deep k-step advances the
+// start address by 8 rows = 1024 B).
+__device__ __forceinline__ uint64_t desc_mnmajor_b32(uint32_t smem_addr, uint32_t lbo) {
+  uint64_t d = 0;
+  d |= uint64_t((smem_addr >> 4) & 0x3FFF);
+  d |= uint64_t((lbo >> 4) & 0x3FFF) << 16;
+  d |= uint64_t(512 >> 4) << 32;
+  d |= uint64_t(1) << 46;
+  d |= uint64_t(1) << 61;
+  return d;
+}
+
 // Arrive on an mbarrier when all previously issued tcgen05 ops complete.
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile(

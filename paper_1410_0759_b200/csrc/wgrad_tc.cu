@@ -343,15 +343,23 @@ static int64_t max_chain(int px) {
   return c / px * px;
 }
 
-// BW: width (channels) of one dy MN block: 64 (128-byte swizzle) or 32
-// (64-byte swizzle, lets a CTA pair split BN = 64 or 192 into halves)
-template <int BN, int NC, int PX, int BW = 64>
+// ES: bytes per packed element (2 = BF16x3, 4 = 3xTF32).  An x block is one
+// 128-byte-row MN block: XW = 128 / ES channels (64 bf16, 32 tf32) x PX
+// pixels; BW: width (channels) of one dy MN block: 64 bf16 (128-byte
+// swizzle) or 32 (bf16: 64-byte swizzle, lets a CTA pair split BN = 64 or
+// 192 into halves; tf32: the 128-byte rows of the 128B_ATOM_32B swizzle,
+// the only MN-major tf32 layout, tools/probe_tf32.cu).
+template <int BN, int NC, int PX, int BW = 64, int ES = 2>
 struct WgCfg {
-  static constexpr int BLK = PX * 128;         // one 64-wide MN block of x
-  static constexpr int BBLK = PX * BW * 2;     // one BW-wide MN block of dy
+  static constexpr int XW = 128 / ES;          // channels of one x MN block
+  static constexpr int XB = 128 / XW;          // x blocks per 128 columns
+  static constexpr int KSTEP = 32 / ES;        // pixels per MMA k-step
+  static constexpr int BLK = PX * 128;         // one x MN block
+  static constexpr int BBLK = PX * BW * ES;    // one BW-wide MN block of dy
   static constexpr int B_BLKS = BN / NC / BW;  // dy blocks loaded by each CTA
   static_assert(B_BLKS * BW * NC == BN, "dy blocks must tile the CTA's columns");
-  static constexpr int A_BYTES = 2 * BLK;      // 128 x-columns
+  static_assert(ES == 2 || BW * ES == 128, "tf32 dy blocks are 128-byte rows");
+  static constexpr int A_BYTES = XB * BLK;     // 128 x-columns
   static constexpr int B_BYTES = B_BLKS * BBLK;
   static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
   static constexpr int STAGES =
@@ -360,9 +368,9 @@ struct WgCfg {
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
 };
 
-template <int BN, int NC, int PX, int BW>
+template <int BN, int NC, int PX, int BW, int ES>
 __global__ void __launch_bounds__(kWgThreads, 1) wgrad_tma_kernel(const __grid_constant__ WgTmaParams P) {
-  using C = WgCfg<BN, NC, PX, BW>;
+  using C = WgCfg<BN, NC, PX, BW, ES>;
   constexpr int S = C::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -434,11 +442,11 @@ __global__ void __launch_bounds__(kWgThreads, 1) wgrad_tma_kernel(const __grid_c
           const int h0 = P.lower_h + int(pp) * P.u, w0 = P.lower_w + int(qq) * P.v;
           const uint32_t xb = base + (pw == 1 ? C::A_BYTES : 0);
 #pragma unroll
-          for (int j = 0; j < 2; j++) {
-            const int blk = m0 / 64 + j;
+          for (int j = 0; j < C::XB; j++) {
+            const int blk = m0 / C::XW + j;
             const int tap = blk / P.nCB, cb = blk - tap * P.nCB;
             const bool real = tap < P.taps;
-            const int c = real ? cb * 64 : P.Cext;
+            const int c = real ? cb * C::XW : P.Cext;
             const uint16_t dh = uint16_t(real ? tap / P.tapW : 0), dw = uint16_t(real ? tap % P.tapW : 0);
             if constexpr (NC == 2)
               ptx::tma_load_im2col_pair(xb + j * C::BLK, tmx, c, w0, h0, int(img), dw, dh, bar);
@@ -459,7 +467,8 @@ __global__ void __launch_bounds__(kWgThreads, 1) wgrad_tma_kernel(const __grid_c
     }
   } else if (warp == kMmaW) {
     if (leader) {
-      constexpr uint32_t idesc = ptx::idesc_bf16(128 * NC, BN, 1, 1);
+      constexpr uint32_t idesc = ES == 4 ? ptx::idesc_tf32(128 * NC, BN, 1, 1)
+                                         : ptx::idesc_bf16(128 * NC, BN, 1, 1);
       uint32_t acc = 0;
       for (int kb = 0; kb < nkb; kb++) {
         const int s = kb % S;
@@ -468,26 +477,29 @@ __global__ void __launch_bounds__(kWgThreads, 1) wgrad_tma_kernel(const __grid_c
         if (P.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && kb < 1024 && lane == 0)
           P.trace[kb * 4 + 2] = clock64();
         const uint32_t sa = smem0 + s * C::STAGE_BYTES;
-        const uint64_t dah = ptx::desc_mnmajor_sw128(sa, C::BLK, 1024);
-        const uint64_t dal = ptx::desc_mnmajor_sw128(sa + C::A_BYTES, C::BLK, 1024);
         const uint32_t sb = sa + 2 * C::A_BYTES;
-        const uint64_t dbh = BW == 64 ? ptx::desc_mnmajor_sw128(sb, C::BBLK, 1024)
-                                      : ptx::desc_mnmajor_sw64(sb, C::BBLK, 512);
-        const uint64_t dbl = BW == 64 ? ptx::desc_mnmajor_sw128(sb + C::B_BYTES, C::BBLK, 1024)
-                                      : ptx::desc_mnmajor_sw64(sb + C::B_BYTES, C::BBLK, 512);
+        uint64_t dah, dal, dbh, dbl;
+        if constexpr (ES == 4) {
+          dah = ptx::desc_mnmajor_b32(sa, C::BLK);
+          dal = ptx::desc_mnmajor_b32(sa + C::A_BYTES, C::BLK);
+          dbh = ptx::desc_mnmajor_b32(sb, C::BBLK);
+          dbl = ptx::desc_mnmajor_b32(sb + C::B_BYTES, C::BBLK);
+        } else {
+          dah = ptx::desc_mnmajor_sw128(sa, C::BLK, 1024);
+          dal = ptx::desc_mnmajor_sw128(sa + C::A_BYTES, C::BLK, 1024);
+          dbh = BW == 64 ? ptx::desc_mnmajor_sw128(sb, C::BBLK, 1024)
+                         : ptx::desc_mnmajor_sw64(sb, C::BBLK, 512);
+          dbl = BW == 64 ? ptx::desc_mnmajor_sw128(sb + C::B_BYTES, C::BBLK, 1024)
+                         : ptx::desc_mnmajor_sw64(sb + C::B_BYTES, C::BBLK, 512);
+        }
 #pragma unroll
-        for (int kk = 0; kk < PX / 16; kk++) {
-          const uint64_t o = uint64_t(kk * 2048) >> 4;         // 16 pixels of 128 B rows (x)
-          const uint64_t ob = uint64_t(kk * 16 * BW * 2) >> 4;  // 16 pixels of BW*2 B rows (dy)
-          if constexpr (NC == 2) {
-            ptx::mma_bf16_pair_elect(tmem_d, dal + o, dbh + ob, idesc, acc);
-            ptx::mma_bf16_pair_elect(tmem_d, dah + o, dbl + ob, idesc, 1);
-            ptx::mma_bf16_pair_elect(tmem_d, dah + o, dbh + ob, idesc, 1);
-          } else {
-            ptx::mma_bf16_elect(tmem_d, dal + o, dbh + ob, idesc, acc);
-            ptx::mma_bf16_elect(tmem_d, dah + o, dbl + ob, idesc, 1);
-            ptx::mma_bf16_elect(tmem_d, dah + o, dbh + ob, idesc, 1);
-          }
+        for (int kk = 0; kk < PX / C::KSTEP; kk++) {
+          // one k-step = KSTEP pixels: KSTEP rows of 128 B (x), of BW * ES B (dy)
+          const uint64_t o = uint64_t(kk * C::KSTEP * 128) >> 4;
+          const uint64_t ob = uint64_t(kk * C::KSTEP * BW * ES) >> 4;
+          ptx::mma_split_elect<NC, ES>(tmem_d, dal + o, dbh + ob, idesc, acc);
+          ptx::mma_split_elect<NC, ES>(tmem_d, dah + o, dbl + ob, idesc, 1);
+          ptx::mma_split_elect<NC, ES>(tmem_d, dah + o, dbh + ob, idesc, 1);
           acc = 1;
         }
         if constexpr (NC == 2) ptx::mma_commit_pair_elect(&empty[s]);
@@ -569,14 +581,14 @@ __global__ void __launch_bounds__(256) wgrad_reduce_tma(WgReduceGeom g, const fl
   }
 }
 
-template <int BN, int NC, int PX, int BW = 64>
+template <int BN, int NC, int PX, int BW = 64, int ES = 2>
 cudaError_t launch_wgrad_tma(const WgTmaParams& prm, dim3 grid, cudaStream_t st) {
-  using CC = WgCfg<BN, NC, PX, BW>;
+  using CC = WgCfg<BN, NC, PX, BW, ES>;
   static int attr_dev = -1;
   int dev = 0;
   cudaGetDevice(&dev);
   if (attr_dev != dev) {
-    cudaError_t e = cudaFuncSetAttribute(wgrad_tma_kernel<BN, NC, PX, BW>,
+    cudaError_t e = cudaFuncSetAttribute(wgrad_tma_kernel<BN, NC, PX, BW, ES>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, CC::SMEM);
     if (e != cudaSuccess) return e;
     attr_dev = dev;
@@ -594,7 +606,7 @@ cudaError_t launch_wgrad_tma(const WgTmaParams& prm, dim3 grid, cudaStream_t st)
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   ktime_begin(st, 2);
-  cudaError_t e = cudaLaunchKernelEx(&cfg, wgrad_tma_kernel<BN, NC, PX, BW>, prm);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, wgrad_tma_kernel<BN, NC, PX, BW, ES>, prm);
   ktime_end(st);
   note_launch();
   if (e != cudaSuccess) return e;
@@ -606,7 +618,7 @@ cudaError_t launch_wgrad_tma(const WgTmaParams& prm, dim3 grid, cudaStream_t st)
 // TMA path of backward-filter; returns cudaErrorNotSupported when the
 // geometry does not fit the im2col tensor map (caller falls back).
 cudaError_t wgrad_tma(const ConvProblem& p, const float* dy, const float* x, float* df, bool acc,
-                      cudaStream_t st) {
+                      cudaStream_t st, int es) {
   if (::dnnp::tune_env("DNNP_TC_NO_TMA")) return cudaErrorNotSupported;
   const bool s2d = !::dnnp::tune_env("DNNP_TC_NO_S2D") && (p.u > 1 || p.v > 1) && p.u <= 8 && p.v <= 8 &&
                    p.C * p.u * p.v <= 64;
@@ -617,7 +629,8 @@ cudaError_t wgrad_tma(const ConvProblem& p, const float* dy, const float* x, flo
   const int R2 = int(ceil_div(p.R, su)), S2 = fold ? 1 : int(ceil_div(p.S, sv));
   const int Cg = su * sv * int(p.C);                 // GEMM channels per tap
   const int Cp = int(ceil_div(Cg, 16) * 16);         // packed x channels
-  const int nCB = int(ceil_div(Cp, 64)), Cpf = nCB * 64;
+  const int xw = 128 / es;                           // channels of one x block (128-byte rows)
+  const int nCB = int(ceil_div(Cp, xw)), Cpf = nCB * xw;
   const int taps = R2 * S2;
   const int ncolx = taps * Cpf;                      // x-operand extent (padded)
   const int IH = s2d ? int(p.P) - 1 + R2 : int(p.H);
@@ -656,8 +669,8 @@ cudaError_t wgrad_tma(const ConvProblem& p, const float* dy, const float* x, flo
   }
   if (nc == 2 && bn % 64) nc = 1;
   if (nc == 2 && bn % 128 && bn != 64 && bn != 192) nc = 1;
-  const bool bw32 = nc == 2 && bn % 128 != 0;
-  const int dbw = bw32 ? 32 : 64;  // dy block width of the tensor map
+  const bool bw32 = es == 4 || (nc == 2 && bn % 128 != 0);
+  const int dbw = bw32 ? 32 : 64;  // dy block width of the tensor map (tf32: 128-byte rows)
   const int mrows = int(ceil_div(ncolx, 128 * nc) * 128 * nc);
   const int ncols = int(ceil_div(Kp64, bn) * bn);
   const int mt = mrows / (128 * nc), nt = ncols / bn;
@@ -667,8 +680,9 @@ cudaError_t wgrad_tma(const ConvProblem& p, const float* dy, const float* x, flo
   // 146 -> 126 us): the TMA engine spends ~200-280 cycles per box whatever
   // its size up to 16 KB, so bigger boxes move more bytes per box; the
   // 96 KB stages still double-buffer.  Wider dy tiles would leave one stage.
-  int px = bn / nc <= 64 ? 128 : 64;
-  if (const char* e = ::dnnp::tune_env("DNNP_WG_PX")) {
+  // (3xTF32: the same stage bytes, so half the pixels)
+  int px = (bn / nc <= 64 ? 128 : 64) * 2 / es;
+  if (const char* e = ::dnnp::tune_env("DNNP_WG_PX"); e && es == 2) {
     const int v = atoi(e);
     px = v == 32 ? 32 : (v == 128 ? 128 : 64);
   }
@@ -681,28 +695,29 @@ cudaError_t wgrad_tma(const ConvProblem& p, const float* dy, const float* x, flo
   const size_t dy_elems = size_t(NPQ) * Kp64, x_elems = size_t(p.N) * IH * IW * Cp;
   const size_t ws_floats = size_t(splits) * mrows * ncols;
   Workspace wsp(st);
-  cudaError_t e = wsp.alloc((dy_elems + x_elems) * 4 + ws_floats * 4 + 512);
+  cudaError_t e = wsp.alloc((dy_elems + x_elems) * 2 * es + ws_floats * 4 + 512);
   if (e != cudaSuccess) return e;
-  auto* dy_hi = static_cast<__nv_bfloat16*>(wsp.p);
-  auto* dy_lo = dy_hi + dy_elems;
-  auto* x_hi = dy_lo + dy_elems;
-  auto* x_lo = x_hi + x_elems;
-  float* part = reinterpret_cast<float*>(x_lo + x_elems);
+  char* base = static_cast<char*>(wsp.p);
+  void* dy_hi = base;
+  void* dy_lo = base + dy_elems * es;
+  void* x_hi = base + 2 * dy_elems * es;
+  void* x_lo = base + (2 * dy_elems + x_elems) * es;
+  float* part = reinterpret_cast<float*>(base + 2 * (dy_elems + x_elems) * es);
   {
-    const __nv_bfloat16 *ph = nullptr, *pl = nullptr;
-    if (packed_get(dy, p.y, Kp64, &ph, &pl)) {  // packed once by the fused backward entry
-      dy_hi = const_cast<__nv_bfloat16*>(ph);
-      dy_lo = const_cast<__nv_bfloat16*>(pl);
-    } else if ((e = pack_act(p.y, dy, Kp64, dy_hi, dy_lo, st)) != cudaSuccess) {
+    const void *ph = nullptr, *pl = nullptr;
+    if (packed_get(dy, p.y, Kp64, &ph, &pl, es)) {  // packed once by the fused backward entry
+      dy_hi = const_cast<void*>(ph);
+      dy_lo = const_cast<void*>(pl);
+    } else if ((e = pack_act(p.y, dy, Kp64, dy_hi, dy_lo, st, es)) != cudaSuccess) {
       return e;
     }
   }
   if (fold)
-    e = pack_act_fold(p.x, x, int(p.S), int(p.v), int(p.pad_w), IW, Cp, x_hi, x_lo, st);
+    e = pack_act_fold(p.x, x, int(p.S), int(p.v), int(p.pad_w), IW, Cp, x_hi, x_lo, st, es);
   else if (s2d)
-    e = pack_act_s2d(p.x, x, su, sv, int(p.pad_h), int(p.pad_w), IH, IW, Cp, x_hi, x_lo, st);
+    e = pack_act_s2d(p.x, x, su, sv, int(p.pad_h), int(p.pad_w), IH, IW, Cp, x_hi, x_lo, st, es);
   else
-    e = pack_act(p.x, x, Cp, x_hi, x_lo, st);
+    e = pack_act(p.x, x, Cp, x_hi, x_lo, st, es);
   if (e != cudaSuccess) return e;
 
   WgTmaParams prm{};
@@ -717,18 +732,24 @@ cudaError_t wgrad_tma(const ConvProblem& p, const float* dy, const float* x, flo
   ig.upper_w = upper_w;
   ig.stride_h = gu;
   ig.stride_w = gv;
-  ig.cpp = 64;
+  ig.cpp = xw;
   ig.ppc = px;
-  if ((e = make_tmap_im2col(&prm.tm_xhi, x_hi, ig, CU_TENSOR_MAP_SWIZZLE_128B)) != cudaSuccess) return e;
-  if ((e = make_tmap_im2col(&prm.tm_xlo, x_lo, ig, CU_TENSOR_MAP_SWIZZLE_128B)) != cudaSuccess) return e;
+  // MN-major operands: 128-byte swizzle (bf16), the 32-byte-atom 128-byte
+  // swizzle for tf32 (descriptor layout SWIZZLE_128B_BASE32B)
+  const CUtensorMapSwizzle xsw =
+      es == 4 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B;
+  if ((e = make_tmap_im2col(&prm.tm_xhi, x_hi, ig, xsw, es)) != cudaSuccess) return e;
+  if ((e = make_tmap_im2col(&prm.tm_xlo, x_lo, ig, xsw, es)) != cudaSuccess) return e;
   {
     const uint64_t dims[3] = {uint64_t(dbw), uint64_t(NPQ), uint64_t(Kp64 / dbw)};
-    const uint64_t strides[2] = {uint64_t(Kp64) * 2, uint64_t(dbw) * 2};
+    const uint64_t strides[2] = {uint64_t(Kp64) * es, uint64_t(dbw) * es};
     const uint32_t box[3] = {uint32_t(dbw), uint32_t(px), uint32_t(bn / nc / dbw)};
-    const CUtensorMapSwizzle dsw = bw32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B;
-    if ((e = make_tmap_3d(&prm.tm_dyhi, dy_hi, dims, strides, box, dsw)) != cudaSuccess)
+    const CUtensorMapSwizzle dsw = es == 4 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B
+                                   : bw32  ? CU_TENSOR_MAP_SWIZZLE_64B
+                                           : CU_TENSOR_MAP_SWIZZLE_128B;
+    if ((e = make_tmap_3d(&prm.tm_dyhi, dy_hi, dims, strides, box, dsw, es)) != cudaSuccess)
       return e;
-    if ((e = make_tmap_3d(&prm.tm_dylo, dy_lo, dims, strides, box, dsw)) != cudaSuccess)
+    if ((e = make_tmap_3d(&prm.tm_dylo, dy_lo, dims, strides, box, dsw, es)) != cudaSuccess)
       return e;
   }
   prm.pix_per_split = pps;
@@ -773,9 +794,30 @@ cudaError_t wgrad_tma(const ConvProblem& p, const float* dy, const float* x, flo
       default: return launch_wgrad_tma<256, 1, PX>(prm, grid, st);
     }
   };
-  e = px == 32    ? go(std::integral_constant<int, 32>())
-      : px == 128 ? go(std::integral_constant<int, 128>())
-                  : go(std::integral_constant<int, 64>());
+  // 3xTF32: 32-channel dy blocks, 64 pixels per stage for <= 64 dy channels
+  // per CTA, else 32 (the bf16 stage bytes)
+  auto go_tf32 = [&]() -> cudaError_t {
+    if (nc == 2) {
+      switch (bn) {
+        case 64: return launch_wgrad_tma<64, 2, 64, 32, 4>(prm, grid, st);
+        case 128: return launch_wgrad_tma<128, 2, 64, 32, 4>(prm, grid, st);
+        case 192: return launch_wgrad_tma<192, 2, 32, 32, 4>(prm, grid, st);
+        default: return launch_wgrad_tma<256, 2, 32, 32, 4>(prm, grid, st);
+      }
+    }
+    switch (bn) {
+      case 64: return launch_wgrad_tma<64, 1, 64, 32, 4>(prm, grid, st);
+      case 128: return launch_wgrad_tma<128, 1, 32, 32, 4>(prm, grid, st);
+      case 192: return launch_wgrad_tma<192, 1, 32, 32, 4>(prm, grid, st);
+      default: return launch_wgrad_tma<256, 1, 32, 32, 4>(prm, grid, st);
+    }
+  };
+  if (es == 4)
+    e = go_tf32();
+  else
+    e = px == 32    ? go(std::integral_constant<int, 32>())
+        : px == 128 ? go(std::integral_constant<int, 128>())
+                    : go(std::integral_constant<int, 64>());
   if (e != cudaSuccess) return e;
   if (want_trace) {
     static unsigned long long h[8192];
@@ -811,13 +853,14 @@ cudaError_t wgrad_tma(const ConvProblem& p, const float* dy, const float* x, flo
 }  // namespace tc
 
 cudaError_t tc_backward_filter(const ConvProblem& p, const float* dy, const float* x, float* df,
-                               bool acc, cudaStream_t st) {
+                               bool acc, cudaStream_t st, int es) {
   using namespace tc;
   pool_keep_memory();
   {
-    const cudaError_t te = wgrad_tma(p, dy, x, df, acc, st);
+    const cudaError_t te = wgrad_tma(p, dy, x, df, acc, st, es);
     if (te != cudaErrorNotSupported) return te;
   }
+  if (es == 4) return cudaErrorNotSupported;  // 3xTF32: the caller runs SIMT fp32
   const int Kp = int(ceil_div(p.K, 8) * 8), Cp = int(ceil_div(p.C, 8) * 8), Cgrp = Cp / 8;
   const int KC = int(p.R * p.S) * Cgrp;
   const int64_t NPQ = p.N * p.P * p.Q, NHW = p.N * p.H * p.W;
