@@ -51,6 +51,16 @@ def layer_flops(n, c, h, k, r, u, pad):
     return 2 * n * k * c * r * r * p * p
 
 
+def sustained_tf32_peak():
+    """TF32-equivalent sustained peak: 1/2 of the measured back-to-back bf16
+    GEMM rate (MEASURED_PEAKS.json bf16_tflops_sustained)."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh)["bf16_tflops_sustained"] / 2.0
+    except Exception:
+        return None
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -346,6 +356,8 @@ def main():
                     help="submit every step eagerly (no CUDA-graph replay at N=1)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-sustained", action="store_true")
+    ap.add_argument("--no-bw", action="store_true", help="skip the bandwidth-primitive table")
     ap.add_argument("--batch", type=int, default=N_PER_GPU)
     ap.add_argument("--ref-n", type=int, default=16,
                     help="--impl reference: images per timed CPU step")
@@ -478,6 +490,32 @@ def main():
     # the other ops' kernel times: from the instrumented eager pass
     for i, v in pre_kern.items():
         kern_ms.setdefault(i, v)
+
+    # sustained: the same graph replayed back to back for >= 3 s (no flush,
+    # no host sync between steps), clocks sampled meanwhile -- the rate a
+    # training loop sees once the GPU settles at its power-limited clock
+    sustained = None
+    if graph is not None and not args.no_sustained:
+        try:
+            nrep = max(1, int(3000.0 / max(float(np.median(step_ms)), 0.05)))
+            torch.cuda.synchronize()
+            with ClockSampler(local) as clk_s:
+                a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a0.record()
+                for _ in range(nrep):
+                    graph.replay()
+                a1.record()
+                torch.cuda.synchronize()
+            sec = a0.elapsed_time(a1) / 1e3
+            sflops = 3 * sum(L["flops"] for L in layers)
+            sustained = {"seconds": round(sec, 3), "steps": nrep,
+                         "ms_per_step": round(sec * 1e3 / nrep, 4),
+                         "tflops": round(sflops * nrep / sec / 1e12, 2),
+                         "clocks": clk_s.summary(),
+                         "tf32_sustained_peak": sustained_tf32_peak(),
+                         "note": "graph replays back to back, L2 not flushed, inputs resident"}
+        except Exception as e:
+            print(f"sustained run failed: {type(e).__name__}: {e}", file=sys.stderr)
 
     # the fp32 split sweep: the same step (same calls, same data) in the
     # 3xTF32 mode, replayed as a graph (N=1 only): step time, throughput and
@@ -656,12 +694,18 @@ def main():
                      "frac_of_bf16x3_ceiling": round(achieved / (bf16 / 3.0), 4),
                      "work_per_launch_flops": layers[dl]["flops"],
                      "l2_to_sm_ingest": ingest},
+        "sustained": sustained,
         "math_sweep": math_sweep(step_flops, total_ms / args.steps, tf32_ms, bf16),
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
     }
     if e2e is not None:
         line["e2e"] = e2e
+    if rank == 0 and ws == 1 and not args.no_bw:
+        try:
+            line["bandwidth_ops"] = bandwidth_ops(dp, torch, hbm)
+        except Exception as e:
+            print(f"bandwidth ops failed: {type(e).__name__}: {e}", file=sys.stderr)
     if rank == 0 and ws == 1 and not args.no_cpu:
         threads = os.cpu_count() or 1
         # parity of the benchmarked step itself: the C oracle on the same
@@ -717,6 +761,81 @@ def math_sweep(step_flops, bf16x3_ms, tf32x3_ms, bf16_peak):
     out["note"] = ("same AlexNet conv1-5 step (graph replay, L2 flushed); algorithmic flops; "
                    "the split's extra MMAs are not counted")
     return out
+
+
+def bandwidth_ops(dp, torch, hbm_peak):
+    """BASELINE configs[4] / SURVEY 8(d) "B": the bandwidth-bound primitives
+    at their shapes (activation and 3x3/2 pooling on 128x64x55x55, softmax
+    per-image 1024x1000x1x1 and per-spatial 16x21x64x64), fp32, on dense
+    NCHW, NHWC and a channel slice [16:48) of a 64-channel parent.  Each op
+    is timed alone: a 1 GiB write plus a 256 MiB read flush L2 (empty and
+    clean) before it, CUDA events around its launch on the library's stream
+    (the launch is queued behind the flush, so host dispatch is outside the
+    window), median of 5.  Algorithmic bytes per SURVEY 8(d)."""
+    wflush = torch.empty(256 * 1024 * 1024, dtype=torch.float32, device="cuda")
+    rflush = torch.ones(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
+
+    def view(n, c, h, w, layout):
+        if layout == "slice":
+            buf = torch.rand(n * 64 * h * w, device="cuda") - 0.5
+            d = dp.make_desc(n, 32, h, w, layout="custom", strides=[64 * h * w, h * w, w, 1])
+            return dp.TensorView(d, buf[16 * h * w:])
+        d = dp.make_desc(n, c, h, w, layout=layout)
+        return dp.TensorView(d, torch.rand(d.max_offset() + 1, device="cuda") - 0.5)
+
+    def timed(op):
+        op()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(5):
+            wflush.fill_(1.0)
+            rflush.sum()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            op()
+            b.record()
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        return float(np.median(ts))
+
+    out = {}
+    for lay in ("nchw", "nhwc", "slice"):
+        c = 32 if lay == "slice" else 64
+        x, y, dy, dx = (view(128, c, 55, 55, lay) for _ in range(4))
+        E = 128 * c * 55 * 55
+        ops = [("act_fwd_relu", 8 * E, lambda: dp.activation_forward("relu", x, y)),
+               ("act_bwd_relu", 12 * E, lambda: dp.activation_backward("relu", y, dy, dx))]
+        for kind in ("max", "average"):
+            pd = dp.PoolingDesc(kind, 3, 3, 2, 2, 0, 0)
+            py, pdy = view(128, c, 27, 27, lay), view(128, c, 27, 27, lay)
+            am = (torch.empty((128, c, 27, 27), dtype=torch.int64, device="cuda")
+                  if kind == "max" else None)
+            Ep = 128 * c * 27 * 27
+            byt = 4 * E + (12 if kind == "max" else 4) * Ep
+            dp.pool_forward(pd, x, py, am)
+            ops.append((f"pool_fwd_{kind}", byt, lambda pd=pd, py=py, am=am:
+                        dp.pool_forward(pd, x, py, am)))
+            ops.append((f"pool_bwd_{kind}", byt, lambda pd=pd, py=py, pdy=pdy, am=am:
+                        dp.pool_backward(pd, py, pdy, x, dx, am)))
+        for mode, (n, cc, h, w) in (("per_image", (1024, 1000, 1, 1)),
+                                    ("per_spatial", (16, 21, 64, 64))):
+            if lay == "slice":
+                cc = 32
+            a, b, d2 = view(n, cc, h, w, lay), view(n, cc, h, w, lay), view(n, cc, h, w, lay)
+            En = n * cc * h * w
+            ops.append((f"softmax_fwd_{mode}", 8 * En, lambda a=a, b=b, mode=mode:
+                        dp.softmax_forward(mode, a, b)))
+            ops.append((f"softmax_bwd_{mode}", 12 * En, lambda a=a, b=b, d2=d2, mode=mode:
+                        dp.softmax_backward(mode, a, b, d2)))
+        for name, byt, op in ops:
+            ms = timed(op)
+            gbs = byt / (ms / 1e3) / 1e9
+            out[f"{name}.{lay}"] = {"bytes": int(byt), "us": round(ms * 1e3, 2),
+                                    "GBps": round(gbs, 1), "frac_hbm": round(gbs / hbm_peak, 3)}
+    del wflush, rflush
+    return {"hbm_peak_GBps": hbm_peak, "dtype": "f32", "ops": out,
+            "method": "L2 flushed clean (1 GiB write + 256 MiB read) before each op; CUDA "
+                      "events around the op; median of 5; algorithmic bytes (SURVEY 8(d))"}
 
 
 def run_e2e(dp, layers, torch, device, ws, args, step_flops):

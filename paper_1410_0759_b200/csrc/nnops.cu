@@ -531,20 +531,25 @@ __global__ void __launch_bounds__(256) softmax_img_apply(ImgGeom ga, const T* a,
 // whole group held in registers -- one read and one write per element and a
 // single launch instead of partial + apply.  Same operations as the two
 // kernels above (fmax / exp / divide; dsub / dmul for the backward).
-template <typename T, bool BWD, int PER>
+template <typename T, bool BWD, int PER, bool CONTIG>
 __global__ void __launch_bounds__(256) softmax_img_warp(ImgGeom ga, const T* a, ImgGeom gb,
                                                        const T* b, ImgGeom go, T* o, int64_t G,
                                                        int64_t nimg) {
   const int lane = threadIdx.x & 31;
   const int64_t n = int64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (n >= nimg) return;
+  // CONTIG: every operand's image is one dense run (offset n * sn + g): no
+  // index decode per element (the decode cost more than the bytes moved)
+  auto off = [&](const ImgGeom& ig, uint32_t g) -> int64_t {
+    return CONTIG ? n * ig.v.sn + g : img_off(ig, n, g);
+  };
   T va[PER], vb[PER];
 #pragma unroll
   for (int k = 0; k < PER; k++) {
     const int64_t g = lane + 32 * k;
     if (g < G) {
-      va[k] = a[img_off(ga, n, uint32_t(g))];
-      if (BWD) vb[k] = b[img_off(gb, n, uint32_t(g))];
+      va[k] = __ldg(a + off(ga, uint32_t(g)));
+      if (BWD) vb[k] = __ldg(b + off(gb, uint32_t(g)));
     }
   }
   if (!BWD) {
@@ -563,7 +568,7 @@ __global__ void __launch_bounds__(256) softmax_img_warp(ImgGeom ga, const T* a, 
     sum = warp_sum(sum);
 #pragma unroll
     for (int k = 0; k < PER; k++)
-      if (lane + 32 * k < G) o[img_off(go, n, uint32_t(lane + 32 * k))] = va[k] / sum;
+      if (lane + 32 * k < G) o[off(go, uint32_t(lane + 32 * k))] = va[k] / sum;
   } else {
     T d = T(0);
 #pragma unroll
@@ -573,7 +578,70 @@ __global__ void __launch_bounds__(256) softmax_img_warp(ImgGeom ga, const T* a, 
 #pragma unroll
     for (int k = 0; k < PER; k++)
       if (lane + 32 * k < G)
-        o[img_off(go, n, uint32_t(lane + 32 * k))] = dmul<T>(va[k], dsub<T>(vb[k], d));
+        o[off(go, uint32_t(lane + 32 * k))] = dmul<T>(va[k], dsub<T>(vb[k], d));
+  }
+}
+
+// Per-image softmax, one 128-thread block per image (groups of 129..1024
+// elements): each thread holds PER <= 8 elements in registers, so every
+// element is read once and written once; two-level (warp shuffle, then
+// shared memory) reductions.  Four warps per image instead of one keep ~4x
+// the bytes in flight per SM (the warp-per-image form was latency-bound:
+// 1024 images = 7 warps per SM).
+template <typename T, bool BWD, int PER, bool CONTIG>
+__global__ void __launch_bounds__(128) softmax_img_block(ImgGeom ga, const T* a, ImgGeom gb,
+                                                        const T* b, ImgGeom go, T* o, int64_t G) {
+  __shared__ T red[4];
+  const int64_t n = blockIdx.x;
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  auto off = [&](const ImgGeom& ig, uint32_t g) -> int64_t {
+    return CONTIG ? n * ig.v.sn + g : img_off(ig, n, g);
+  };
+  T va[PER], vb[PER];
+#pragma unroll
+  for (int k = 0; k < PER; k++) {
+    const int64_t g = t + 128 * k;
+    if (g < G) {
+      va[k] = __ldg(a + off(ga, uint32_t(g)));
+      if (BWD) vb[k] = __ldg(b + off(gb, uint32_t(g)));
+    }
+  }
+  if (!BWD) {
+    T m = T(-INFINITY);
+#pragma unroll
+    for (int k = 0; k < PER; k++)
+      if (t + 128 * k < G) m = fmax(m, va[k]);
+    m = warp_max(m);
+    if (lane == 0) red[wid] = m;
+    __syncthreads();
+    m = fmax(fmax(red[0], red[1]), fmax(red[2], red[3]));
+    __syncthreads();
+    T sum = T(0);
+#pragma unroll
+    for (int k = 0; k < PER; k++)
+      if (t + 128 * k < G) {
+        va[k] = exp(va[k] - m);
+        sum += va[k];
+      }
+    sum = warp_sum(sum);
+    if (lane == 0) red[wid] = sum;
+    __syncthreads();
+    sum = (red[0] + red[1]) + (red[2] + red[3]);
+#pragma unroll
+    for (int k = 0; k < PER; k++)
+      if (t + 128 * k < G) o[off(go, uint32_t(t + 128 * k))] = va[k] / sum;
+  } else {
+    T d = T(0);
+#pragma unroll
+    for (int k = 0; k < PER; k++)
+      if (t + 128 * k < G) d += va[k] * vb[k];
+    d = warp_sum(d);
+    if (lane == 0) red[wid] = d;
+    __syncthreads();
+    d = (red[0] + red[1]) + (red[2] + red[3]);
+#pragma unroll
+    for (int k = 0; k < PER; k++)
+      if (t + 128 * k < G) o[off(go, uint32_t(t + 128 * k))] = dmul<T>(va[k], dsub<T>(vb[k], d));
   }
 }
 
@@ -612,6 +680,57 @@ __global__ void __launch_bounds__(256) softmax_spatial(PosGeom ga, const T* a, P
   }
 }
 
+// per_spatial with C <= CMAX channels: the position's channels are read
+// once into registers (max, exponentials, sum and output from them; the
+// loop form read the input three times)
+template <typename T, bool BWD, int CMAX>
+__global__ void __launch_bounds__(256) softmax_spatial_reg(PosGeom ga, const T* a, PosGeom gb,
+                                                          const T* b, PosGeom go, T* o,
+                                                          int64_t npos, int C) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t pos = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; pos < npos; pos += stride) {
+    const int64_t ba = pos_base(ga, uint32_t(pos)), bo = pos_base(go, uint32_t(pos));
+    T va[CMAX], vb[CMAX];
+    const int64_t bb = BWD ? pos_base(gb, uint32_t(pos)) : 0;
+#pragma unroll
+    for (int c = 0; c < CMAX; c++)
+      if (c < C) {
+        va[c] = __ldg(a + ba + c * ga.v.sc);
+        if (BWD) vb[c] = __ldg(b + bb + c * gb.v.sc);
+      }
+    if (!BWD) {
+      T m = T(-INFINITY);
+#pragma unroll
+      for (int c = 0; c < CMAX; c++)
+        if (c < C) m = fmax(m, va[c]);
+      T sum = T(0);
+#pragma unroll
+      for (int c = 0; c < CMAX; c++)
+        if (c < C) {
+          va[c] = exp(va[c] - m);
+          sum += va[c];
+        }
+#pragma unroll
+      for (int c = 0; c < CMAX; c++)
+        if (c < C) o[bo + c * go.v.sc] = va[c] / sum;
+    } else {
+      T d = T(0);
+#pragma unroll
+      for (int c = 0; c < CMAX; c++)
+        if (c < C) d += va[c] * vb[c];
+#pragma unroll
+      for (int c = 0; c < CMAX; c++)
+        if (c < C) o[bo + c * go.v.sc] = dmul<T>(va[c], dsub<T>(vb[c], d));
+    }
+  }
+}
+
+// one image's (c, h, w) elements form a single dense run
+static bool img_dense(const View4& v) {
+  return (v.w == 1 || v.sw == 1) && (v.h == 1 || v.sh == v.w * (v.w == 1 ? 1 : v.sw)) &&
+         (v.c == 1 || v.sc == v.h * v.w);
+}
+
 static ImgGeom img_geom(const View4& v) {
   return ImgGeom{v, make_magic(uint32_t(v.h * v.w)), make_magic(uint32_t(v.w))};
 }
@@ -628,14 +747,31 @@ static cudaError_t softmax_t(int mode, const View4& av, const T* a, const View4*
     const int64_t G = av.c * av.h * av.w;
     const unsigned grid = unsigned(ceil_div(av.n, 8));
     ImgGeom ga = img_geom(av), gb = img_geom(bv ? *bv : av), go = img_geom(ov);
+    const bool contig = img_dense(av) && img_dense(ov) && (!bv || img_dense(*bv));
     auto go_per = [&](auto perc) {
-      softmax_img_warp<T, BWD, decltype(perc)::value><<<grid, 256, 0, st>>>(ga, a, gb, b, go, o,
-                                                                           G, av.n);
+      if (contig)
+        softmax_img_warp<T, BWD, decltype(perc)::value, true><<<grid, 256, 0, st>>>(
+            ga, a, gb, b, go, o, G, av.n);
+      else
+        softmax_img_warp<T, BWD, decltype(perc)::value, false><<<grid, 256, 0, st>>>(
+            ga, a, gb, b, go, o, G, av.n);
+    };
+    auto go_blk = [&](auto perc) {
+      constexpr int PER = decltype(perc)::value;
+      const unsigned nb = unsigned(av.n);
+      if (contig)
+        softmax_img_block<T, BWD, PER, true><<<nb, 128, 0, st>>>(ga, a, gb, b, go, o, G);
+      else
+        softmax_img_block<T, BWD, PER, false><<<nb, 128, 0, st>>>(ga, a, gb, b, go, o, G);
     };
     if (G <= 128) go_per(std::integral_constant<int, 4>());
-    else if (G <= 256) go_per(std::integral_constant<int, 8>());
-    else if (G <= 512) go_per(std::integral_constant<int, 16>());
-    else go_per(std::integral_constant<int, 32>());
+    else if (av.n >= (int64_t(1) << 31) || ::dnnp::tune_env("DNNP_SOFTMAX_WARP_ONLY")) {
+      if (G <= 256) go_per(std::integral_constant<int, 8>());
+      else if (G <= 512) go_per(std::integral_constant<int, 16>());
+      else go_per(std::integral_constant<int, 32>());
+    } else if (G <= 256) go_blk(std::integral_constant<int, 2>());
+    else if (G <= 512) go_blk(std::integral_constant<int, 4>());
+    else go_blk(std::integral_constant<int, 8>());
     note_launch();
     return cudaGetLastError();
   }
@@ -657,6 +793,17 @@ static cudaError_t softmax_t(int mode, const View4& av, const T* a, const View4*
     return cudaGetLastError();
   }
   const int64_t npos = av.n * av.h * av.w;
+  if (av.c <= 32 && !::dnnp::tune_env("DNNP_SOFTMAX_NO_REG")) {
+    const unsigned grid = grid_for(npos, 256, 8);
+    if (av.c <= 8)
+      softmax_spatial_reg<T, BWD, 8><<<grid, 256, 0, st>>>(pos_geom(av), a, pos_geom(bv ? *bv : av),
+                                                           b, pos_geom(ov), o, npos, int(av.c));
+    else
+      softmax_spatial_reg<T, BWD, 32><<<grid, 256, 0, st>>>(pos_geom(av), a, pos_geom(bv ? *bv : av),
+                                                            b, pos_geom(ov), o, npos, int(av.c));
+    note_launch();
+    return cudaGetLastError();
+  }
   softmax_spatial<T, BWD><<<grid_for(npos, 256, 8), 256, 0, st>>>(
       pos_geom(av), a, pos_geom(bv ? *bv : av), b, pos_geom(ov), o, npos, av.c);
   note_launch();
@@ -1529,6 +1676,241 @@ __global__ void pool_bwd_serial(PoolGeom g, const T* dy, T* dx, const int64_t* a
   }
 }
 
+// ---------------------------------------------------------------------------
+// 3 x 3 / stride 2 / no padding pooling on planes with unit-stride rows (the
+// AlexNet / OverFeat pooling layer; SURVEY 8(d) "B" shape 55 -> 27).  One
+// warp per (plane, 32 output columns); lane q owns output column q and walks
+// the output rows.  Forward is separable: the 3-wide row reduction of input
+// row h (first max / first NaN in w order, with its column) is computed once
+// and shared by the two output rows whose windows contain it (h = 2p + 2 is
+// the last row of window p and the first of p + 1); the 3-row combination
+// in h order keeps the reference's row-major first-max / first-NaN pick
+// (nnops.py:180-197).  ~20 instructions per output instead of a window scan
+// out of shared memory; every input byte is read from DRAM once.
+template <typename T>
+struct RowBest {
+  T v;
+  int w;
+};
+
+// a later candidate wins when greater, or when it is NaN and the best is not
+template <typename T>
+__device__ __forceinline__ void take_best(RowBest<T>& b, T v, int w) {
+  const bool take = v > b.v || (v != v && b.v == b.v);
+  b.v = take ? v : b.v;
+  b.w = take ? w : b.w;
+}
+
+// Warps: (plane, 32-column block, chunk of kPoolRows output rows); chunks
+// keep the per-warp loop short, so the grid runs as several full waves
+// (one warp per plane was ~1.15 waves of 27-row loops: the tail doubled
+// the time) and more loads are in flight per SM.
+constexpr int kPoolRows = 7;
+
+template <typename T, int KIND>
+__global__ void __launch_bounds__(128) pool3s2_fwd_kernel(PoolGeom g, const T* __restrict__ x,
+                                                          T* __restrict__ y,
+                                                          int64_t* __restrict__ argmax, int nqb,
+                                                          int nrc) {
+  const int H = int(g.H), W = int(g.W), P = int(g.P), Q = int(g.Q), C = int(g.C);
+  const int gw = int((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  const int planes = int(g.N) * C;
+  if (gw >= planes * nqb * nrc) return;
+  const int rc = gw % nrc, t = gw / nrc;
+  const int pl = t / nqb, qb = t - pl * nqb;
+  const int q = qb * 32 + lane;
+  if (q >= Q) return;
+  const int p0 = rc * kPoolRows, p1 = min(P, p0 + kPoolRows);
+  const int n = pl / C, c = pl - n * C;
+  const T* xb = x + int64_t(n) * g.x.sn + int64_t(c) * g.x.sc;
+  T* yb = y + int64_t(n) * g.y.sn + int64_t(c) * g.y.sc + int64_t(q) * g.y.sw;
+  int64_t* ab = argmax ? argmax + int64_t(pl) * P * Q + q : nullptr;
+  const int64_t abase = int64_t(pl) * H * W;
+  const int w0 = 2 * q;
+  // every input value of the chunk is loaded up front (2 RP + 1 rows x 3
+  // columns in registers): one memory latency per warp instead of one per
+  // output row
+  constexpr int NR = 2 * kPoolRows + 1;
+  T v[NR][3];
+#pragma unroll
+  for (int r = 0; r < NR; r++) {
+    const int h = 2 * p0 + r;
+    if (h <= 2 * p1) {
+      const T* row = xb + int64_t(h) * g.x.sh + w0;
+      v[r][0] = __ldg(row);
+      v[r][1] = __ldg(row + 1);
+      v[r][2] = __ldg(row + 2);
+    }
+  }
+  RowBest<T> rb[NR];
+#pragma unroll
+  for (int r = 0; r < NR; r++) {
+    if (KIND == 0) {
+      rb[r].v = v[r][0];
+      rb[r].w = w0;
+      take_best(rb[r], v[r][1], w0 + 1);
+      take_best(rb[r], v[r][2], w0 + 2);
+    } else {
+      rb[r].v = dadd<T>(dadd<T>(v[r][0], v[r][1]), v[r][2]);
+      rb[r].w = 0;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < kPoolRows; i++) {
+    const int p = p0 + i;
+    if (p >= p1) break;
+    const RowBest<T>& r0 = rb[2 * i];
+    const RowBest<T>& r1 = rb[2 * i + 1];
+    const RowBest<T>& r2 = rb[2 * i + 2];
+    if (KIND == 0) {
+      RowBest<T> b = r0;
+      int bh = 2 * p;
+      const bool t1 = r1.v > b.v || (r1.v != r1.v && b.v == b.v);
+      b.v = t1 ? r1.v : b.v;
+      b.w = t1 ? r1.w : b.w;
+      bh = t1 ? 2 * p + 1 : bh;
+      const bool t2 = r2.v > b.v || (r2.v != r2.v && b.v == b.v);
+      b.v = t2 ? r2.v : b.v;
+      b.w = t2 ? r2.w : b.w;
+      bh = t2 ? 2 * p + 2 : bh;
+      yb[int64_t(p) * g.y.sh] = b.v;
+      if (ab) ab[int64_t(p) * Q] = abase + int64_t(bh) * W + b.w;
+    } else {
+      yb[int64_t(p) * g.y.sh] = dadd<T>(dadd<T>(r0.v, r1.v), r2.v) / T(9);
+    }
+  }
+}
+
+// Backward of the same geometry, gather form in the reference's summation
+// order: input (h, w) receives, in ascending (p, q), dy[p][q] of every
+// covering window whose argmax is (h, w) (max) or dy / 9 (average), starting
+// from 0 (nnops.py:203-246, np.add.at in flat (n, c, p, q) order).  Lane l
+// owns window q = 32 jb + l and input columns 2q, 2q + 1; column 2q + 2 is
+// the next lane's 2(q + 1), whose share of window q arrives by shuffle and
+// is added before that lane's own window (ascending q).  Each window's
+// argmax is decoded once into its (row, col) inside the window and the nine
+// per-position contributions are selects (adding +0.0 leaves a sum that
+// starts at +0.0 unchanged, so the result is bit-identical to the scatter).
+// Rows 2p, 2p + 1 complete after window row p; row 2p + 2 carries into p + 1;
+// a row chunk [p0, p1) starts by re-deriving window row p0 - 1's share of
+// input row 2p0.  Max: an argmax outside its window sets *bad (the serial
+// scatter redoes the op).
+template <typename T, int KIND>
+__global__ void __launch_bounds__(128) pool3s2_bwd_kernel(PoolGeom g, const T* __restrict__ dy,
+                                                          T* __restrict__ dx,
+                                                          const int64_t* __restrict__ argmax,
+                                                          int* bad, int nqb, int nrc) {
+  const int H = int(g.H), W = int(g.W), P = int(g.P), Q = int(g.Q), C = int(g.C);
+  const int gw = int((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  const int planes = int(g.N) * C;
+  if (gw >= planes * nqb * nrc) return;  // warp-uniform
+  const int rc = gw % nrc, tt = gw / nrc;
+  const int pl = tt / nqb, jb = tt - pl * nqb;
+  const int q = jb * 32 + lane;           // this lane's window column
+  const int w0 = 2 * q;
+  const int p0 = rc * kPoolRows, p1 = min(P, p0 + kPoolRows);
+  const bool own = q < Q;                 // lane has a window
+  const bool live = w0 < W;               // lane owns input columns
+  const bool has1 = w0 + 1 < W;
+  const bool edge = lane == 0 && q > 0 && q - 1 < Q;  // window q - 1 is in the previous warp
+  const int n = pl / C, c = pl - n * C;
+  const T* dyb = dy + int64_t(n) * g.y.sn + int64_t(c) * g.y.sc;
+  T* dxb = dx + int64_t(n) * g.x.sn + int64_t(c) * g.x.sc + int64_t(w0) * g.x.sw;
+  const int64_t* ab = argmax ? argmax + int64_t(pl) * P * Q : nullptr;
+  const int64_t abase = int64_t(pl) * H * W;
+  // window (p, qq): its dy (avg: / 9) and the argmax position inside the
+  // window, pos = 3 row + col in [0, 9), or -1 when outside (max)
+  auto fetch = [&](int p, int qq, T& d, int& pos) {
+    d = __ldg(dyb + int64_t(p) * g.y.sh + int64_t(qq) * g.y.sw);
+    pos = -1;
+    if (KIND == 0) {
+      const int64_t rel = __ldg(ab + int64_t(p) * Q + qq) - abase -
+                          (int64_t(2 * p) * W + 2 * qq);
+      if (rel >= 0 && rel < 3 * int64_t(W)) {
+        uint32_t r, cc;
+        mdivmod(uint32_t(rel), g.dW, r, cc);
+        if (cc <= 2) pos = int(r) * 3 + int(cc);
+      }
+    } else {
+      d = d / T(9);
+    }
+  };
+  constexpr int NW = kPoolRows + 1;  // window rows p0 - 1 .. p1 - 1
+  T dv[NW], de[NW];
+  int pv[NW], pe[NW];
+#pragma unroll
+  for (int i = 0; i < NW; i++) {
+    const int p = p0 - 1 + i;
+    dv[i] = de[i] = T(0);
+    pv[i] = pe[i] = -1;
+    if (p >= 0 && p < p1) {
+      if (own) fetch(p, q, dv[i], pv[i]);
+      if (edge) fetch(p, q - 1, de[i], pe[i]);
+    }
+  }
+  // the share of window (., q) at window row r, window column cc
+  auto sel = [&](T d, int pos, bool has, int r, int cc) -> T {
+    return has && (KIND != 0 || pos == 3 * r + cc) ? d : T(0);
+  };
+  bool badl = false;
+  T e0 = T(0), e1 = T(0);  // pending row 2p (columns 2q, 2q + 1)
+#pragma unroll
+  for (int i = 0; i < NW; i++) {
+    const int p = p0 - 1 + i;
+    if (p >= p1) break;
+    if (p < p0 && p < 0) continue;
+    // column-2 shares of window q - 1, rows 0..2 (shuffle; lane 0 decodes it)
+    T prev[3];
+#pragma unroll
+    for (int r = 0; r < 3; r++) {
+      const T mine = sel(dv[i], pv[i], own, r, 2);
+      const T up = __shfl_up_sync(0xffffffffu, mine, 1);
+      prev[r] = lane == 0 ? sel(de[i], pe[i], edge, r, 2) : up;
+    }
+    if (p < p0) {  // window row p0 - 1: only its last row (2 p0) is this chunk's
+      e0 = dadd<T>(dadd<T>(T(0), prev[2]), sel(dv[i], pv[i], own, 2, 0));
+      e1 = dadd<T>(T(0), sel(dv[i], pv[i], own, 2, 1));
+      continue;
+    }
+    if (KIND == 0 && own && pv[i] < 0) badl = true;
+    const int h0 = 2 * p;
+    // row h0: pending (window row p - 1), then (p, q - 1), then (p, q)
+    const T o0 = dadd<T>(dadd<T>(e0, prev[0]), sel(dv[i], pv[i], own, 0, 0));
+    const T o1 = dadd<T>(e1, sel(dv[i], pv[i], own, 0, 1));
+    const T m0 = dadd<T>(dadd<T>(T(0), prev[1]), sel(dv[i], pv[i], own, 1, 0));
+    const T m1 = dadd<T>(T(0), sel(dv[i], pv[i], own, 1, 1));
+    e0 = dadd<T>(dadd<T>(T(0), prev[2]), sel(dv[i], pv[i], own, 2, 0));
+    e1 = dadd<T>(T(0), sel(dv[i], pv[i], own, 2, 1));
+    if (live) {
+      T* r0p = dxb + int64_t(h0) * g.x.sh;
+      r0p[0] = o0;
+      if (has1) r0p[g.x.sw] = o1;
+      r0p += g.x.sh;
+      r0p[0] = m0;
+      if (has1) r0p[g.x.sw] = m1;
+    }
+  }
+  if (p1 == P && live) {
+    // the last pending row and any rows past the last window (zero)
+    for (int h = 2 * P; h < H; h++) {
+      const T v0 = h == 2 * P ? e0 : T(0), v1 = h == 2 * P ? e1 : T(0);
+      dxb[int64_t(h) * g.x.sh] = v0;
+      if (has1) dxb[int64_t(h) * g.x.sh + g.x.sw] = v1;
+    }
+  }
+  if (KIND == 0 && badl) atomicExch(bad, 1);
+}
+
+// whether the 3 x 3 / 2 plane kernels take this problem
+static bool pool3s2_ok(const PoolProblem& pp, const View4& xv, const View4& yv) {
+  return pp.wh == 3 && pp.ww == 3 && pp.sh == 2 && pp.sw == 2 && pp.ph == 0 && pp.pw == 0 &&
+         xv.sw == 1 && yv.sw == 1 && xv.h >= 3 && xv.w >= 3 && pp.P == (xv.h - 3) / 2 + 1 &&
+         pp.Q == (xv.w - 3) / 2 + 1 && xv.n * xv.c * ceil_div(xv.w, 64) * ceil_div(xv.h, 14) < (int64_t(1) << 26) &&
+         xv.h * xv.w < (int64_t(1) << 31) && !::dnnp::tune_env("DNNP_POOL_NO_3S2");
+}
+
 // Plane kernels: one (n, c) plane per block iteration, staged in shared
 // memory.  Small blocks and an uncapped grid keep many planes per SM in
 // flight, so one block's load phase overlaps another's compute phase.
@@ -1572,6 +1954,23 @@ cudaError_t pool_forward(const PoolProblem& pp, Dtype dt, const View4& xv, const
   PoolGeom g = pool_geom(pp, xv, yv);
   const size_t eb = dt == F32 ? 4 : 8;
   const size_t psm = size_t(xv.h) * xv.w * eb;
+  if (pool3s2_ok(pp, xv, yv)) {
+    const int nqb = int(ceil_div(pp.Q, 32)), nrc = int(ceil_div(pp.P, kPoolRows));
+    const unsigned blocks = unsigned(ceil_div(xv.n * xv.c * nqb * nrc, 4));
+    if (dt == F32) {
+      if (pp.kind == 0)
+        pool3s2_fwd_kernel<float, 0><<<blocks, 128, 0, st>>>(g, (const float*)x, (float*)y, argmax, nqb, nrc);
+      else
+        pool3s2_fwd_kernel<float, 1><<<blocks, 128, 0, st>>>(g, (const float*)x, (float*)y, argmax, nqb, nrc);
+    } else {
+      if (pp.kind == 0)
+        pool3s2_fwd_kernel<double, 0><<<blocks, 128, 0, st>>>(g, (const double*)x, (double*)y, argmax, nqb, nrc);
+      else
+        pool3s2_fwd_kernel<double, 1><<<blocks, 128, 0, st>>>(g, (const double*)x, (double*)y, argmax, nqb, nrc);
+    }
+    note_launch();
+    return cudaGetLastError();
+  }
   if (xv.sc == 1 && yv.sc == 1 && xv.c >= 16 && !::dnnp::tune_env("DNNP_POOL_NO_CL")) {
     // channels innermost: channel-vectorised rows instead of planes
     const int nqb = int(ceil_div(pp.Q, 32)), ncb = int(ceil_div(xv.c, 32));
@@ -1671,6 +2070,39 @@ cudaError_t pool_backward(const PoolProblem& pp, Dtype dt, const View4& dyv, con
   const size_t psm = ((size_t(dxv.h + dxv.w) * 8 + 15) & ~size_t(15)) +
                      ((size_t(dyv.h) * dyv.w * 4 + 15) & ~size_t(15)) + size_t(dyv.h) * dyv.w * eb +
                      (pp.kind == 0 ? size_t(dxv.h) * dxv.w * eb : 0);
+  if (pool3s2_ok(pp, dxv, dyv)) {
+    int* bad = nullptr;
+    tc::Workspace ws(st);
+    if (pp.kind == 0) {
+      cudaError_t e = ws.alloc(sizeof(int));
+      if (e != cudaSuccess) return e;
+      bad = static_cast<int*>(ws.p);
+      cudaMemsetAsync(bad, 0, sizeof(int), st);
+    }
+    // lanes = window columns plus the input columns past the last window
+    const int nqb = int(ceil_div(ceil_div(dxv.w, 2), 32)), nrc = int(ceil_div(pp.P, kPoolRows));
+    const unsigned blocks = unsigned(ceil_div(dxv.n * dxv.c * nqb * nrc, 4));
+    if (dt == F32) {
+      if (pp.kind == 0)
+        pool3s2_bwd_kernel<float, 0><<<blocks, 128, 0, st>>>(g, (const float*)dy, (float*)dx, argmax, bad, nqb, nrc);
+      else
+        pool3s2_bwd_kernel<float, 1><<<blocks, 128, 0, st>>>(g, (const float*)dy, (float*)dx, argmax, bad, nqb, nrc);
+    } else {
+      if (pp.kind == 0)
+        pool3s2_bwd_kernel<double, 0><<<blocks, 128, 0, st>>>(g, (const double*)dy, (double*)dx, argmax, bad, nqb, nrc);
+      else
+        pool3s2_bwd_kernel<double, 1><<<blocks, 128, 0, st>>>(g, (const double*)dy, (double*)dx, argmax, bad, nqb, nrc);
+    }
+    note_launch();
+    if (pp.kind == 0) {
+      if (dt == F32)
+        pool_bwd_serial<float><<<1, 32, 0, st>>>(g, (const float*)dy, (float*)dx, argmax, ptotal, bad);
+      else
+        pool_bwd_serial<double><<<1, 32, 0, st>>>(g, (const double*)dy, (double*)dx, argmax, ptotal, bad);
+      note_launch();
+    }
+    return cudaGetLastError();
+  }
   // channels innermost: the element-wise gather in (n, h, w, c) order (the
   // plane kernel would read and write every plane at stride C)
   const bool cl = dxv.sc == 1 && dyv.sc == 1 && dxv.c >= 16 && !::dnnp::tune_env("DNNP_POOL_NO_CL");
