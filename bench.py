@@ -358,6 +358,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-sustained", action="store_true")
     ap.add_argument("--no-bw", action="store_true", help="skip the bandwidth-primitive table")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the small-batch sweep")
     ap.add_argument("--batch", type=int, default=N_PER_GPU)
     ap.add_argument("--ref-n", type=int, default=16,
                     help="--impl reference: images per timed CPU step")
@@ -701,6 +702,11 @@ def main():
     }
     if e2e is not None:
         line["e2e"] = e2e
+    if rank == 0 and ws == 1 and not args.no_sweep:
+        try:
+            line["small_batch_sweep"] = small_batch_sweep(dp, torch)
+        except Exception as e:
+            print(f"small-batch sweep failed: {type(e).__name__}: {e}", file=sys.stderr)
     if rank == 0 and ws == 1 and not args.no_bw:
         try:
             line["bandwidth_ops"] = bandwidth_ops(dp, torch, hbm)
@@ -836,6 +842,74 @@ def bandwidth_ops(dp, torch, hbm_peak):
     return {"hbm_peak_GBps": hbm_peak, "dtype": "f32", "ops": out,
             "method": "L2 flushed clean (1 GiB write + 256 MiB read) before each op; CUDA "
                       "events around the op; median of 5; algorithmic bytes (SURVEY 8(d))"}
+
+
+SWEEP_LAYERS = [  # OverFeat-fast conv2 / conv3 (suites/overfeat_vgg.suite): C, H, K, R, pad
+    ("of_conv2", 96, 24, 256, 5, 2),
+    ("of_conv3", 256, 12, 512, 3, 1),
+]
+SWEEP_BATCHES = (1, 2, 4, 8, 16, 32, 64, 128, 256)
+
+
+def small_batch_sweep(dp, torch):
+    """BASELINE configs[2]: forward throughput across minibatch sizes
+    (reference bench.py:260-281 batch_sweep; rate relative to the best in the
+    sweep).  Two per-call times: `device` = 20 calls replayed as one CUDA
+    graph (the GPU's own time, no host dispatch), `eager` = 20 back-to-back
+    calls through the Python API without synchronisation (max of host
+    submission and GPU time, what an eager framework loop sees)."""
+    out = {}
+    for name, c, h, k, r, pad in SWEEP_LAYERS:
+        rows = []
+        for n in SWEEP_BATCHES:
+            p = out_extent(h, r, 1, pad)
+            g = np.random.default_rng([2014, n])
+            x = torch.from_numpy(g.uniform(-0.5, 0.5, n * c * h * h).astype(np.float32)).cuda()
+            f = torch.from_numpy(g.uniform(-0.5, 0.5, k * c * r * r).astype(np.float32)).cuda()
+            xv = dp.TensorView(dp.make_desc(n, c, h, h), x)
+            fv = dp.FilterView(dp.make_filter_desc(k, c, r, r), f)
+            yv = dp.empty_view(dp.make_desc(n, k, p, p), device="cuda")
+            cd = dp.ConvDesc(1, 1, pad, pad)
+            op = lambda: dp.conv_forward(xv, fv, cd, "implicit", yv)  # noqa: E731
+            for _ in range(3):
+                op()
+            torch.cuda.synchronize()
+            reps = 20
+            s = torch.cuda.Stream()
+            s.wait_stream(torch.cuda.current_stream())
+            gr = torch.cuda.CUDAGraph()
+            with torch.cuda.stream(s):
+                with torch.cuda.graph(gr, stream=s):
+                    for _ in range(reps):
+                        op()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            gr.replay()
+            e1.record()
+            torch.cuda.synchronize()
+            dev_us = e0.elapsed_time(e1) * 1e3 / reps
+            del gr
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            e0.record()
+            for _ in range(reps):
+                op()
+            e1.record()
+            torch.cuda.synchronize()
+            eager_us = e0.elapsed_time(e1) * 1e3 / reps
+            fl = layer_flops(n, c, h, k, r, 1, pad)
+            rows.append({"n": n, "device_us": round(dev_us, 2), "eager_us": round(eager_us, 2),
+                         "device_tflops": round(fl / dev_us / 1e6, 2),
+                         "eager_tflops": round(fl / eager_us / 1e6, 2)})
+        best = max(rr["device_tflops"] for rr in rows)
+        best_e = max(rr["eager_tflops"] for rr in rows)
+        for rr in rows:
+            rr["device_pct_of_best"] = round(100 * rr["device_tflops"] / best, 1)
+            rr["eager_pct_of_best"] = round(100 * rr["eager_tflops"] / best_e, 1)
+        out[name] = rows
+    return {"layers": out, "pass": "forward", "dtype": "f32",
+            "note": "rate relative to the best batch of the sweep (reference batch_sweep)"}
 
 
 def run_e2e(dp, layers, torch, device, ws, args, step_flops):

@@ -147,7 +147,11 @@ def handle():
 
 
 def set_stream(stream_ptr):
+    """Bind this thread's handle to a cudaStream_t (skipped when unchanged)."""
+    if getattr(_handles, "stream", -1) == stream_ptr:
+        return
     check(lib().dnnp_set_stream(handle(), vp(stream_ptr)), "dnnp_set_stream")
+    _handles.stream = stream_ptr
 
 
 def set_math(mode):

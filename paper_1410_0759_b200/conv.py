@@ -7,6 +7,7 @@ for fp32 by default, SIMT DFMA for fp64) through the C ABI.
 from __future__ import annotations
 
 import enum
+import functools
 from dataclasses import dataclass
 
 import numpy as np
@@ -62,6 +63,13 @@ class FilterDesc:
     s: int
     dtype: np.dtype
 
+    def __hash__(self):
+        h = self.__dict__.get("_hash")
+        if h is None:
+            h = hash((self.k, self.c, self.r, self.s, self.dtype))
+            object.__setattr__(self, "_hash", h)
+        return h
+
     def __post_init__(self):
         for e in (self.k, self.c, self.r, self.s):
             if e < 1:
@@ -113,6 +121,7 @@ class FilterView:
         self.buf = buf
         self.is_cuda = cuda
         self._torch = _is_torch(buf)
+        self._dev = buf.device.index if cuda else None
 
     @property
     def ptr(self):
@@ -149,6 +158,13 @@ class ConvDesc:
     pad_w: int = 0
     mode: ConvMode = ConvMode.CONVOLUTION
     accumulate: bool = False
+
+    def __hash__(self):
+        h = self.__dict__.get("_hash")
+        if h is None:
+            h = hash((self.u, self.v, self.pad_h, self.pad_w, self.mode, self.accumulate))
+            object.__setattr__(self, "_hash", h)
+        return h
 
     def __post_init__(self):
         if self.u < 1 or self.v < 1:
@@ -255,67 +271,76 @@ def convolution_workspace_size(pass_, x_desc, f_desc, conv: ConvDesc, y_desc,
     return int(out.value)
 
 
+@functools.lru_cache(maxsize=1024)
+def _plan(pass_, in_desc, f_desc, conv, out_desc, engine, max_lowered_bytes):
+    """Validated call plan, cached per (pass, descriptors, engine, limit):
+    the checks the reference makes (same order and exceptions) and the native
+    descriptor handles, so a repeated call does no Python-side work beyond
+    reading pointers.  pass_: 0 forward (in = x, out = y), 1 backward-data
+    (in = dx, out = dy), 2 backward-filter (in = x, out = dy, f = df)."""
+    engine = as_engine(engine)
+    if in_desc.dtype != f_desc.dtype:
+        raise ShapeMismatch(f"element types {in_desc.dtype} vs {f_desc.dtype}")
+    out_shape = conv_out_shape(in_desc, f_desc, conv)
+    what = "output" if pass_ == 0 else "output gradient"
+    if out_desc.extents != tuple(out_shape):
+        raise ShapeMismatch(f"{what} extents {out_desc.extents}, expected {tuple(out_shape)}")
+    if out_desc.dtype != in_desc.dtype:
+        raise ShapeMismatch(f"{what} element type {out_desc.dtype}, expected {in_desc.dtype}")
+    _lowered_guard(engine, in_desc, f_desc, out_shape, max_lowered_bytes)
+    return (in_desc.c_desc(), f_desc.c_desc(), conv.c_desc(), out_desc.c_desc(),
+            _ENGINE_CODE[engine])
+
+
 def conv_forward(x: TensorView, f: FilterView, conv: ConvDesc, engine, y: TensorView,
                  alpha: float = 1.0, beta: float = 0.0, *, tile=None, threads: int = 1,
                  max_lowered_bytes: int = 4 << 30, workspace=None) -> None:
     """y := alpha * conv(x, f) + beta * y (accumulate forces beta=1).
     workspace: optional CUDA tensor the pass takes its scratch from."""
-    engine = as_engine(engine)
-    out_shape = _check_triplet(x, f, conv)
-    _check_out(y, out_shape, x.desc.dtype, "output")
-    _lowered_guard(engine, x.desc, f.desc, out_shape, max_lowered_bytes)
+    xd, fd, cd, yd, ecode = _plan(0, x.desc, f.desc, conv, y.desc, engine, max_lowered_bytes)
     bind_stream(x, f, y)
     a_keep, a = scalar_ptr(alpha, y.desc.dtype)
     b_keep, b = scalar_ptr(beta, y.desc.dtype)
     if workspace is not None:
         _lib.check(_lib.lib().dnnp_convolution_forward_ex(
-            _lib.handle(), a, x.desc.c_desc(), x.ptr, f.desc.c_desc(), f.ptr, conv.c_desc(),
-            _ENGINE_CODE[engine], b, y.desc.c_desc(), y.ptr, *_ws(workspace)),
+            _lib.handle(), a, xd, x.ptr, fd, f.ptr, cd, ecode, b, yd, y.ptr, *_ws(workspace)),
             "convolution_forward_ex")
         return
     _lib.check(_lib.lib().dnnp_convolution_forward(
-        _lib.handle(), a, x.desc.c_desc(), x.ptr, f.desc.c_desc(), f.ptr, conv.c_desc(),
-        _ENGINE_CODE[engine], b, y.desc.c_desc(), y.ptr), "convolution_forward")
+        _lib.handle(), a, xd, x.ptr, fd, f.ptr, cd, ecode, b, yd, y.ptr), "convolution_forward")
 
 
 def conv_backward_data(dy: TensorView, f: FilterView, conv: ConvDesc, engine, dx: TensorView,
                        *, tile=None, threads: int = 1, max_lowered_bytes: int = 4 << 30,
                        workspace=None) -> None:
     """Gradient with respect to the input; accumulate mode adds into dx."""
-    engine = as_engine(engine)
-    out_shape = _check_triplet(dx, f, conv)
-    _check_out(dy, out_shape, dx.desc.dtype, "output gradient")
-    _lowered_guard(engine, dx.desc, f.desc, out_shape, max_lowered_bytes)
+    dxd, fd, cd, dyd, ecode = _plan(1, dx.desc, f.desc, conv, dy.desc, engine,
+                                    max_lowered_bytes)
     bind_stream(dy, f, dx)
     if workspace is not None:
         _lib.check(_lib.lib().dnnp_convolution_backward_data_ex(
-            _lib.handle(), f.desc.c_desc(), f.ptr, dy.desc.c_desc(), dy.ptr, conv.c_desc(),
-            _ENGINE_CODE[engine], dx.desc.c_desc(), dx.ptr, *_ws(workspace)),
+            _lib.handle(), fd, f.ptr, dyd, dy.ptr, cd, ecode, dxd, dx.ptr, *_ws(workspace)),
             "convolution_backward_data_ex")
         return
     _lib.check(_lib.lib().dnnp_convolution_backward_data(
-        _lib.handle(), f.desc.c_desc(), f.ptr, dy.desc.c_desc(), dy.ptr, conv.c_desc(),
-        _ENGINE_CODE[engine], dx.desc.c_desc(), dx.ptr), "convolution_backward_data")
+        _lib.handle(), fd, f.ptr, dyd, dy.ptr, cd, ecode, dxd, dx.ptr),
+        "convolution_backward_data")
 
 
 def conv_backward_filter(dy: TensorView, x: TensorView, conv: ConvDesc, engine, df: FilterView,
                          *, tile=None, threads: int = 1,
                          max_lowered_bytes: int = 4 << 30, workspace=None) -> None:
     """Gradient with respect to the filter; accumulate mode adds into df."""
-    engine = as_engine(engine)
-    out_shape = _check_triplet(x, df, conv)
-    _check_out(dy, out_shape, x.desc.dtype, "output gradient")
-    _lowered_guard(engine, x.desc, df.desc, out_shape, max_lowered_bytes)
+    xd, fd, cd, dyd, ecode = _plan(2, x.desc, df.desc, conv, dy.desc, engine, max_lowered_bytes)
     bind_stream(dy, x, df)
     if workspace is not None:
         _lib.check(_lib.lib().dnnp_convolution_backward_filter_ex(
-            _lib.handle(), x.desc.c_desc(), x.ptr, dy.desc.c_desc(), dy.ptr, conv.c_desc(),
-            _ENGINE_CODE[engine], df.desc.c_desc(), df.ptr, *_ws(workspace)),
+            _lib.handle(), xd, x.ptr, dyd, dy.ptr, cd, ecode, fd, df.ptr, *_ws(workspace)),
             "convolution_backward_filter_ex")
         return
     _lib.check(_lib.lib().dnnp_convolution_backward_filter(
-        _lib.handle(), x.desc.c_desc(), x.ptr, dy.desc.c_desc(), dy.ptr, conv.c_desc(),
-        _ENGINE_CODE[engine], df.desc.c_desc(), df.ptr), "convolution_backward_filter")
+        _lib.handle(), xd, x.ptr, dyd, dy.ptr, cd, ecode, fd, df.ptr),
+        "convolution_backward_filter")
 
 
 def conv_backward(dy: TensorView, f: FilterView, x: TensorView, conv: ConvDesc, engine,

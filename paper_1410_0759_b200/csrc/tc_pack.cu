@@ -4,7 +4,11 @@
 // 16-byte writes are coalesced.
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
+#include <deque>
 #include <map>
+#include <string>
+#include <unordered_map>
 #include <mutex>
 #include <atomic>
 #include <vector>
@@ -751,13 +755,74 @@ cudaMemPool_t lib_pool() {
 
 void pool_keep_memory() { (void)lib_pool(); }
 
+// Encoded tensor maps are cached by their full argument list (base address
+// included): a repeated call on the same buffers -- every step of a training
+// loop, the arena's planes at the same offsets -- skips the driver encode
+// (~1 us each, four per convolution).  FIFO eviction past kTmapCache entries.
+constexpr size_t kTmapCache = 512;
+struct TmapCache {
+  std::mutex mu;
+  std::unordered_map<std::string, CUtensorMap> map;
+  std::deque<std::string> order;
+};
+static TmapCache& tmap_cache() {
+  static TmapCache* c = new TmapCache;  // lives for the process
+  return *c;
+}
+template <class Key, class F>
+static cudaError_t cached_tmap(CUtensorMap* out, const Key& k, F&& encode) {
+  std::string key(reinterpret_cast<const char*>(&k), sizeof(Key));
+  TmapCache& c = tmap_cache();
+  {
+    std::lock_guard<std::mutex> g(c.mu);
+    auto it = c.map.find(key);
+    if (it != c.map.end()) {
+      *out = it->second;
+      return cudaSuccess;
+    }
+  }
+  const cudaError_t e = encode(out);
+  if (e == cudaSuccess) {
+    std::lock_guard<std::mutex> g(c.mu);
+    if (c.map.size() >= kTmapCache) {
+      c.map.erase(c.order.front());
+      c.order.pop_front();
+    }
+    if (c.map.emplace(key, *out).second) c.order.push_back(key);
+  }
+  return e;
+}
+
 static CUtensorMapDataType tmap_dtype(int es) {
   return es == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
 }
 
+static cudaError_t encode_tmap_2d(CUtensorMap* map, const void* base, uint64_t cols, uint64_t rows,
+                                  uint64_t pitch_elems, uint32_t box_cols, uint32_t box_rows,
+                                  CUtensorMapSwizzle swizzle, int es);
+
 cudaError_t make_tmap_2d(CUtensorMap* map, const void* base, uint64_t cols, uint64_t rows,
                          uint64_t pitch_elems, uint32_t box_cols, uint32_t box_rows,
                          CUtensorMapSwizzle swizzle, int es) {
+  struct K {
+    int kind;
+    int es;
+    const void* base;
+    uint64_t cols, rows, pitch;
+    uint32_t bc, br;
+    int sw;
+  } k;
+  memset(&k, 0, sizeof k);
+  k.kind = 2; k.es = es; k.base = base; k.cols = cols; k.rows = rows; k.pitch = pitch_elems;
+  k.bc = box_cols; k.br = box_rows; k.sw = int(swizzle);
+  return cached_tmap(map, k, [&](CUtensorMap* m) {
+    return encode_tmap_2d(m, base, cols, rows, pitch_elems, box_cols, box_rows, swizzle, es);
+  });
+}
+
+static cudaError_t encode_tmap_2d(CUtensorMap* map, const void* base, uint64_t cols, uint64_t rows,
+                                  uint64_t pitch_elems, uint32_t box_cols, uint32_t box_rows,
+                                  CUtensorMapSwizzle swizzle, int es) {
   using Fn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                           const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
                           CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
@@ -780,9 +845,34 @@ cudaError_t make_tmap_2d(CUtensorMap* map, const void* base, uint64_t cols, uint
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
+static cudaError_t encode_tmap_3d(CUtensorMap* map, const void* base, const uint64_t dims[3],
+                                  const uint64_t strides_bytes[2], const uint32_t box[3],
+                                  CUtensorMapSwizzle swizzle, int es);
+
 cudaError_t make_tmap_3d(CUtensorMap* map, const void* base, const uint64_t dims[3],
                          const uint64_t strides_bytes[2], const uint32_t box[3],
                          CUtensorMapSwizzle swizzle, int es) {
+  struct K {
+    int kind;
+    int es;
+    const void* base;
+    uint64_t d[3], s[2];
+    uint32_t b[3];
+    int sw;
+  } k;
+  memset(&k, 0, sizeof k);
+  k.kind = 3; k.es = es; k.base = base;
+  for (int i = 0; i < 3; i++) k.d[i] = dims[i], k.b[i] = box[i];
+  k.s[0] = strides_bytes[0]; k.s[1] = strides_bytes[1];
+  k.sw = int(swizzle);
+  return cached_tmap(map, k, [&](CUtensorMap* m) {
+    return encode_tmap_3d(m, base, dims, strides_bytes, box, swizzle, es);
+  });
+}
+
+static cudaError_t encode_tmap_3d(CUtensorMap* map, const void* base, const uint64_t dims[3],
+                                  const uint64_t strides_bytes[2], const uint32_t box[3],
+                                  CUtensorMapSwizzle swizzle, int es) {
   using Fn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                           const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
                           CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
@@ -805,8 +895,27 @@ cudaError_t make_tmap_3d(CUtensorMap* map, const void* base, const uint64_t dims
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
+static cudaError_t encode_tmap_im2col(CUtensorMap* map, const void* base, const Im2colGeom& g,
+                                      CUtensorMapSwizzle swizzle, int es);
+
 cudaError_t make_tmap_im2col(CUtensorMap* map, const void* base, const Im2colGeom& g,
                              CUtensorMapSwizzle swizzle, int es) {
+  struct K {
+    int kind;
+    int es;
+    const void* base;
+    Im2colGeom g;
+    int sw;
+  } k;
+  memset(&k, 0, sizeof k);
+  k.kind = 4; k.es = es; k.base = base; k.g = g; k.sw = int(swizzle);
+  return cached_tmap(map, k, [&](CUtensorMap* m) {
+    return encode_tmap_im2col(m, base, g, swizzle, es);
+  });
+}
+
+static cudaError_t encode_tmap_im2col(CUtensorMap* map, const void* base, const Im2colGeom& g,
+                                      CUtensorMapSwizzle swizzle, int es) {
   using Fn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                           const cuuint64_t*, const int*, const int*, cuuint32_t, cuuint32_t,
                           const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
