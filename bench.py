@@ -379,6 +379,9 @@ def main():
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
     if ws > 1:
+        # NCCL INFO lines (transport / ring setup) in the log: evidence of the
+        # ranks' communicator for the driver
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
         dist.init_process_group("nccl", device_id=device)
     dp.set_math(args.math)
 
@@ -388,9 +391,18 @@ def main():
     # layers' work; the step waits for them at its end (inside the timing)
     overlap = None
     allreduce = None
+    comm_note = None
     if ws > 1:
-        from paper_1410_0759_b200.dist import OverlappedAllreduce
-        overlap = OverlappedAllreduce()
+        # the library's own NCCL communicator (libdnnp loads libnccl; torch
+        # only broadcasts the 128-byte unique id and runs the barriers)
+        try:
+            from paper_1410_0759_b200.dist import NativeOverlappedAllreduce
+            overlap = NativeOverlappedAllreduce.from_torch()
+            comm_note = "libdnnp NCCL communicator (dnnp_nccl_comm_create), comm stream"
+        except Exception as e:
+            from paper_1410_0759_b200.dist import OverlappedAllreduce
+            overlap = OverlappedAllreduce()
+            comm_note = f"torch.distributed NCCL (native comm failed: {type(e).__name__})"
         allreduce = overlap.submit
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=device)
 
@@ -435,11 +447,13 @@ def main():
     # dominant kernel is bracketed by CUDA events recorded as external event
     # nodes of the graph (two nodes: timing every kernel this way costs ~8%
     # of the step), so each replay times it inside the timed region.
-    # Multi-GPU runs stay eager (NCCL capture is not exercised here);
+    # Multi-GPU runs capture the step too when the dW reductions go through
+    # the library's own NCCL communicator (the same submission as N=1);
     # --eager forces eager everywhere.
     graph, graph_note = None, "eager"
     launches_per_step = None
-    if ws == 1 and not args.eager:
+    native_comm = comm_note is not None and comm_note.startswith("libdnnp")
+    if (ws == 1 or native_comm) and not args.eager:
         try:
             dp.kernel_timing(True, only=dom_idx)
             l0 = dp.kernel_launch_count()
@@ -448,7 +462,7 @@ def main():
             g = torch.cuda.CUDAGraph()
             with torch.cuda.stream(cap):
                 with torch.cuda.graph(g, stream=cap):
-                    run_step(dp, layers, torch)
+                    run_step(dp, layers, torch, allreduce=allreduce)
             launches_per_step = dp.kernel_launch_count() - l0
             torch.cuda.synchronize()
             g.replay()
@@ -670,6 +684,7 @@ def main():
                    "batch_per_gpu": args.batch, "global_batch": args.batch * ws,
                    "layers": "torchvision AlexNet conv1-5 (64/192/384/256/256)",
                    "parallelism": f"batch-shard dp{ws}" + (" + dW allreduce" if ws > 1 else ""),
+                   "comm": comm_note,
                    "l2": "flushed (256 MiB write) between timed steps",
                    "submission": graph_note,
                    "eager_ms_per_step": round(float(np.median(eager_ms)), 4),

@@ -82,6 +82,11 @@ _SIGS = {
     "dnnp_convolution_backward_filter": [vp, vp, vp, vp, vp, vp, ctypes.c_int, vp, vp],
     "dnnp_convolution_backward_bias": [vp, vp, vp, vp, vp],
     "dnnp_convolution_verify_reference": [vp, ctypes.c_int, vp, vp, vp, vp, vp, vp, vp],
+    "dnnp_nccl_unique_id": [vp, ctypes.c_size_t],
+    "dnnp_nccl_comm_create": [vp, vp, ctypes.c_int, ctypes.c_int],
+    "dnnp_set_nccl_comm": [vp, vp],
+    "dnnp_allreduce_sum": [vp, vp, c_i64, ctypes.c_int],
+    "dnnp_convolution_backward_filter_allreduce": [vp, vp, vp, vp, vp, vp, ctypes.c_int, vp, vp],
     "dnnp_activation_forward": [vp, ctypes.c_int, vp, vp, vp, vp],
     "dnnp_activation_backward": [vp, ctypes.c_int, vp, vp, vp, vp, vp, vp],
     "dnnp_softmax_forward": [vp, ctypes.c_int, vp, vp, vp, vp],

@@ -61,6 +61,8 @@ struct dnnp_context {
   int64_t threads = 1;
   cudaStream_t stream = nullptr;
   int math = DNNP_MATH_DEFAULT;
+  void* comm = nullptr;     // ncclComm_t for the batch-sharded backward-filter
+  bool owns_comm = false;   // created by dnnp_nccl_comm_create (destroyed with the handle)
 };
 
 struct dnnp_tensor_desc_t {
@@ -658,6 +660,7 @@ dnnp_status dnnp_create(dnnp_handle* handle) {
 
 dnnp_status dnnp_destroy(dnnp_handle handle) {
   if (!reg_remove(handle, KIND_HANDLE)) return fail(DNNP_STATUS_BAD_PARAM, "not a live handle");
+  if (handle->owns_comm) dnnp::nccl::comm_destroy(handle->comm);
   delete handle;
   return DNNP_STATUS_OK;
 }
@@ -1265,6 +1268,114 @@ dnnp_status dnnp_convolution_verify_reference(dnnp_handle handle, int pass, dnnp
   const cudaError_t e = dnnp::conv_verify_reference(pass, pr, dnnp::Dtype(xd->elem), a, b, out,
                                                     handle->stream);
   return cuda_status(e, "convolution_verify_reference");
+}
+
+// ------------------------------------------------ NCCL (additive)
+
+static dnnp_status nccl_status(int r, const char* what) {
+  if (r == 0) return DNNP_STATUS_OK;
+  return fail(DNNP_STATUS_NOT_SUPPORTED, "%s: NCCL error %d (%s)", what, r,
+              dnnp::nccl::error_string(r));
+}
+
+dnnp_status dnnp_nccl_unique_id(void* id, size_t bytes) {
+  if (!id || bytes < 128) return fail(DNNP_STATUS_BAD_PARAM, "nccl_unique_id: need 128 bytes");
+  const char* why = nullptr;
+  if (!dnnp::nccl::available(&why)) return fail(DNNP_STATUS_NOT_SUPPORTED, "%s", why);
+  return nccl_status(dnnp::nccl::unique_id(id), "ncclGetUniqueId");
+}
+
+dnnp_status dnnp_nccl_comm_create(dnnp_handle handle, const void* id, int nranks, int rank) {
+  if (!reg_has(handle, KIND_HANDLE) || !id || nranks < 1 || rank < 0 || rank >= nranks)
+    return fail(DNNP_STATUS_BAD_PARAM, "nccl_comm_create: bad arguments");
+  const char* why = nullptr;
+  if (!dnnp::nccl::available(&why)) return fail(DNNP_STATUS_NOT_SUPPORTED, "%s", why);
+  dnnp_status st;
+  if ((st = need_device())) return st;
+  void* comm = nullptr;
+  if ((st = nccl_status(dnnp::nccl::comm_init(&comm, id, nranks, rank), "ncclCommInitRank")))
+    return st;
+  if (handle->owns_comm) dnnp::nccl::comm_destroy(handle->comm);
+  handle->comm = comm;
+  handle->owns_comm = true;
+  return DNNP_STATUS_OK;
+}
+
+dnnp_status dnnp_set_nccl_comm(dnnp_handle handle, void* comm) {
+  if (!reg_has(handle, KIND_HANDLE)) return fail(DNNP_STATUS_BAD_PARAM, "bad handle");
+  if (handle->owns_comm) dnnp::nccl::comm_destroy(handle->comm);
+  handle->comm = comm;
+  handle->owns_comm = false;
+  return DNNP_STATUS_OK;
+}
+
+dnnp_status dnnp_allreduce_sum(dnnp_handle handle, void* buf, int64_t count, dnnp_elem_type type) {
+  if (!reg_has(handle, KIND_HANDLE) || !buf || count < 0 || !elem_valid(type))
+    return fail(DNNP_STATUS_BAD_PARAM, "allreduce_sum: bad arguments");
+  if (!handle->comm) return fail(DNNP_STATUS_BAD_PARAM, "allreduce_sum: no communicator on the handle");
+  if (!is_device_ptr(buf)) return fail(DNNP_STATUS_BAD_PARAM, "allreduce_sum: device buffer required");
+  return nccl_status(dnnp::nccl::allreduce_sum(buf, buf, size_t(count), type == DNNP_F64,
+                                               handle->comm, handle->stream),
+                     "ncclAllReduce");
+}
+
+// Backward-filter of a batch shard followed by ONE allreduce(sum) of dW over
+// the handle's communicator: each rank passes its own N/G
+// images of x and dy; df receives the gradient of the whole minibatch.
+// Accumulate adds the reduced gradient to the prior df AFTER the reduction
+// (reducing df itself would sum G copies of it).  Device buffers only.
+dnnp_status dnnp_convolution_backward_filter_allreduce(dnnp_handle handle, dnnp_tensor_desc xd,
+                                                       const void* x, dnnp_tensor_desc dyd,
+                                                       const void* dy, dnnp_conv_desc cd,
+                                                       dnnp_engine engine, dnnp_filter_desc fd,
+                                                       void* df) {
+  if (!reg_has(handle, KIND_HANDLE)) return fail(DNNP_STATUS_BAD_PARAM, "bad handle");
+  if (!handle->comm)
+    return fail(DNNP_STATUS_BAD_PARAM, "backward_filter_allreduce: no communicator on the handle");
+  if (!tensor_usable(xd, x) || !tensor_usable(dyd, dy) || !filter_usable(fd, df))
+    return fail(DNNP_STATUS_BAD_PARAM, "backward_filter_allreduce: unusable descriptor or buffer");
+  if (!reg_has(cd, KIND_CONV) || !cd->configured)
+    return fail(DNNP_STATUS_BAD_PARAM, "conv descriptor not configured");
+  if (!engine_valid(engine)) return fail(DNNP_STATUS_BAD_PARAM, "bad engine");
+  dnnp_status st;
+  if ((st = bind_view(dyd, "dy")) || (st = bind_view(xd, "x"))) return st;
+  int64_t P, Q;
+  if ((st = conv_shape(xd, fd, cd, &P, &Q))) return st;
+  if ((st = check_out(dyd, xd->n, fd->k, P, Q, xd->elem, "output gradient"))) return st;
+  dnnp::ConvProblem pr = make_problem(xd, fd, cd, dyd, P, Q);
+  if ((st = check_decode_range(pr))) return st;
+  if ((st = explicit_guard(pr, engine, xd->elem, "backward_filter_allreduce"))) return st;
+  if ((st = need_device())) return st;
+  if (!is_device_ptr(x) || !is_device_ptr(dy) || !is_device_ptr(df))
+    return fail(DNNP_STATUS_BAD_PARAM, "backward_filter_allreduce: device buffers required");
+  const size_t count = size_t(fd->k * fd->c * fd->r * fd->s);
+  const bool f64 = fd->elem == DNNP_F64;
+  const dnnp::Dtype dt = dnnp::Dtype(xd->elem);
+  if (!cd->accumulate) {
+    cudaError_t e = dnnp::conv_backward_filter(pr, dt, dy, x, df, false, handle->math, handle->stream);
+    if (e != cudaSuccess) return cuda_status(e, "backward_filter_allreduce");
+    return nccl_status(dnnp::nccl::allreduce_sum(df, df, count, f64, handle->comm, handle->stream),
+                       "ncclAllReduce");
+  }
+  // accumulate: partial into scratch (non-accumulating), reduce it, then df += sum
+  dnnp::tc::ScratchScope* sc = dnnp::tc::scratch_open(handle->stream);
+  void* part = nullptr;
+  cudaError_t e = dnnp::tc::scratch_alloc(sc, count * elem_size(fd->elem), &part);
+  if (e == cudaSuccess)
+    e = dnnp::conv_backward_filter(pr, dt, dy, x, part, false, handle->math, handle->stream);
+  if (e != cudaSuccess) {
+    dnnp::tc::scratch_close(sc);
+    return cuda_status(e, "backward_filter_allreduce");
+  }
+  st = nccl_status(dnnp::nccl::allreduce_sum(part, part, count, f64, handle->comm, handle->stream),
+                   "ncclAllReduce");
+  if (!st) {
+    const View4 v{1, int64_t(count), 1, 1, int64_t(count), 1, 1, 1};
+    st = cuda_status(dnnp::transform(dt, v, part, v, df, 1.0, 1.0, handle->stream),
+                     "backward_filter_allreduce accumulate");
+  }
+  dnnp::tc::scratch_close(sc);
+  return st;
 }
 
 // ------------------------------------------------ fused epilogues (additive)

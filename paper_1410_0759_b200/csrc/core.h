@@ -142,6 +142,17 @@ cudaError_t conv_verify_reference(int pass, const ConvProblem& p, Dtype dt, cons
 // whether the tcgen05 path would be used for a forward problem (tests/bench)
 bool tc_eligible(const ConvProblem& p, int pass);
 
+// ---- NCCL, loaded at run time (nccl_dist.cpp) ------------------------------
+namespace nccl {
+bool available(const char** why);
+const char* error_string(int r);
+int unique_id(void* out128);                                     // ncclResult_t
+int comm_init(void** comm, const void* id128, int nranks, int rank);
+int comm_destroy(void* comm);
+int allreduce_sum(const void* send, void* recv, size_t count, bool f64, void* comm,
+                  cudaStream_t st);
+}  // namespace nccl
+
 // ---- elementwise / reductions (nnops.cu) -----------------------------------
 cudaError_t activation_forward(int kind, Dtype dt, const View4& xv, const void* x,
                                const View4& yv, void* y, cudaStream_t st);

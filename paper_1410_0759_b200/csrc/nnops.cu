@@ -877,12 +877,12 @@ __global__ void __launch_bounds__(256) pool_fwd_kernel(PoolGeom g, const T* __re
         }
         out = best;
         if (argmax)
-          argmax[i] = ((int64_t(n) * C + c) * H + hs0 + bk / KW) * W + ws0 + bk % KW;
+          argmax[i] = ((int64_t(n) * C + c) * H + hs0 + bk / (KW > 0 ? KW : 1)) * W + ws0 + bk % (KW > 0 ? KW : 1);
       } else {
         T sacc = T(0);
 #pragma unroll
         for (int k = 0; k < KW * KW; k++) sacc = dadd<T>(sacc, v[k]);
-        out = sacc / T(KW * KW);
+        out = sacc / T(KW > 0 ? KW * KW : 1);
       }
     } else if (kind == 0) {
       T best = xb[hs * xsh + ws * xsw];
@@ -1153,7 +1153,7 @@ __global__ void __launch_bounds__(256) pool_fwd_pipe_kernel(PoolGeom g, const T*
           for (int a = 0; a < KW; a++)
 #pragma unroll
             for (int b = 0; b < KW; b++) sacc = dadd<T>(sacc, xs[b0 + a * W + b]);
-          out = sacc / T(KW * KW);
+          out = sacc / T(KW > 0 ? KW * KW : 1);
         }
       } else {
         const int hs = max(0, hs0), he = min(H, hs0 + wh);
@@ -1374,7 +1374,7 @@ __global__ void __launch_bounds__(256) pool_fwd_plane_kernel(PoolGeom g, const T
           for (int a = 0; a < KW; a++)
 #pragma unroll
             for (int b = 0; b < KW; b++) sacc = dadd<T>(sacc, xs[base + a * W + b]);
-          out = sacc / T(KW * KW);
+          out = sacc / T(KW > 0 ? KW * KW : 1);
         }
       } else if (kind == 0) {
         T best = xs[hs * W + ws];

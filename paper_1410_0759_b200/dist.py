@@ -7,13 +7,20 @@ dW over NCCL (NVLink / NVSwitch).  With `accumulate`, the reduced gradient is
 added to the prior df after the allreduce (otherwise G copies of the prior df
 would be summed).
 
-torch.distributed is the plumbing (any backend: nccl on GPUs, gloo for the
-CPU tests); the convolution math is libdnnp.so.
+Two ways to run the reduction: the library's own NCCL communicator
+(`NativeComm`: libdnnp loads libnccl at run time, the reduction is enqueued
+by the C ABI on the library's stream -- no torch needed by a C caller, and it
+is captured into CUDA graphs like the kernels), or torch.distributed (any
+backend: nccl on GPUs, gloo for the CPU tests).  The convolution math is
+libdnnp.so either way.
 """
 from __future__ import annotations
 
-from .conv import ConvDesc, FilterView, conv_backward_filter
-from .tensor import TensorView, make_desc
+import ctypes
+
+from . import _lib
+from .conv import ConvDesc, FilterView, _plan, conv_backward_filter
+from .tensor import TensorView, bind_stream, make_desc
 
 
 def batch_shard(n_total: int, rank: int, world: int) -> tuple[int, int]:
@@ -102,3 +109,112 @@ def conv_backward_filter_dp(dy: TensorView, x: TensorView, conv: ConvDesc, engin
                          engine, pv)
     allreduce_filter_grad(part, group)
     df.buf.add_(part)
+
+
+class NativeComm:
+    """The library's NCCL communicator on this thread's handle.
+
+    `NativeComm.unique_id()` on one rank (128 bytes), shipped to every rank by
+    any means (torch.distributed broadcast, a file, MPI), then
+    `NativeComm(uid, world, rank)` on each; `from_torch(group)` does both over
+    an initialised torch.distributed group.  The handle owns the
+    communicator.
+    """
+
+    def __init__(self, uid: bytes, world: int, rank: int):
+        if len(uid) != 128:
+            raise ValueError("an NCCL unique id is 128 bytes")
+        self.world, self.rank = world, rank
+        buf = ctypes.create_string_buffer(uid, 128)
+        _lib.check(_lib.lib().dnnp_nccl_comm_create(_lib.handle(), buf, world, rank),
+                   "dnnp_nccl_comm_create")
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = ctypes.create_string_buffer(128)
+        _lib.check(_lib.lib().dnnp_nccl_unique_id(buf, 128), "dnnp_nccl_unique_id")
+        return buf.raw
+
+    @classmethod
+    def from_torch(cls, group=None):
+        import torch.distributed as dist
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        obj = [cls.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        return cls(obj[0], world, rank)
+
+    def allreduce(self, t):
+        """In-place sum of a CUDA tensor over the communicator, on torch's
+        current stream."""
+        import torch
+        bind_stream(TensorView(make_desc(1, 1, 1, t.numel(), elem_type=(
+            "f64" if t.dtype == torch.float64 else "f32")), t))
+        _lib.check(_lib.lib().dnnp_allreduce_sum(_lib.handle(), t.data_ptr(), t.numel(),
+                                                 1 if t.dtype == torch.float64 else 0),
+                   "dnnp_allreduce_sum")
+        return t
+
+
+def conv_backward_filter_allreduce(dy: TensorView, x: TensorView, conv: ConvDesc, engine,
+                                   df: FilterView) -> None:
+    """Backward-filter of this rank's shard plus ONE allreduce(sum) of dW over
+    the library's NCCL communicator (NativeComm), in a single C call
+    (dnnp_convolution_backward_filter_allreduce); accumulate adds the reduced
+    gradient after the reduction.  CUDA tensors only."""
+    xd, fd, cd, dyd, ecode = _plan(2, x.desc, df.desc, conv, dy.desc, engine, 4 << 30)
+    bind_stream(dy, x, df)
+    _lib.check(_lib.lib().dnnp_convolution_backward_filter_allreduce(
+        _lib.handle(), xd, x.ptr, dyd, dy.ptr, cd, ecode, fd, df.ptr),
+        "convolution_backward_filter_allreduce")
+
+
+class NativeOverlappedAllreduce:
+    """dW allreduces over the library's NCCL communicator on a dedicated
+    communication stream (each layer's reduction overlaps the
+    remaining backward work).  A second library handle owns the stream and
+    the communicator; `submit(t)` orders the reduction of `t` after the
+    kernels queued so far on the compute stream, `wait()` makes the compute
+    stream wait for every submitted reduction.  Capturable into a CUDA graph
+    (the cross-stream dependencies are events)."""
+
+    def __init__(self, uid: bytes, world: int, rank: int):
+        import torch
+        L = _lib.lib()
+        self.h = ctypes.c_void_p()
+        _lib.check(L.dnnp_create(ctypes.byref(self.h)), "dnnp_create")
+        self.stream = torch.cuda.Stream()
+        _lib.check(L.dnnp_set_stream(self.h, ctypes.c_void_p(self.stream.cuda_stream)),
+                   "dnnp_set_stream")
+        buf = ctypes.create_string_buffer(uid, 128)
+        _lib.check(L.dnnp_nccl_comm_create(self.h, buf, world, rank), "dnnp_nccl_comm_create")
+        self.pending = 0
+
+    @classmethod
+    def from_torch(cls, group=None):
+        import torch.distributed as dist
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        obj = [NativeComm.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        return cls(obj[0], world, rank)
+
+    def submit(self, t):
+        import torch
+        ev = torch.cuda.Event()
+        ev.record()  # the producing kernels, on the compute stream
+        self.stream.wait_event(ev)
+        _lib.check(_lib.lib().dnnp_allreduce_sum(self.h, t.data_ptr(), t.numel(),
+                                                 1 if t.dtype == torch.float64 else 0),
+                   "dnnp_allreduce_sum")
+        self.pending += 1
+        return t
+
+    def wait(self):
+        import torch
+        if self.pending:
+            torch.cuda.current_stream().wait_stream(self.stream)
+        self.pending = 0
+
+    def close(self):
+        if self.h:
+            _lib.lib().dnnp_destroy(self.h)
+            self.h = None
