@@ -482,6 +482,89 @@ __global__ void __launch_bounds__(128) pack_filter_tap_kernel(PackGeom g, const 
   }
 }
 
+// Filter packing, one thread per 8 consecutive packed elements (one GEMM
+// column row, one tap, 8 reduction channels): a grid-stride loop over the
+// whole [Np][Ktot] operand, one 16-byte store per plane (bf16) and 8 gathered
+// filter loads.  The same element map as the per-(tap, row) kernel, which
+// spawned (taps + 1) x Np tiny blocks (4-11 us per AlexNet layer, launch
+// and scheduling bound for ~1 M elements); the column (bwd-data / blocked)
+// and chunk tables are filled by the same grid.
+template <int ES>
+__global__ void __launch_bounds__(256) pack_filter_vec_kernel(PackGeom g, const float* __restrict__ f,
+                                                              void* __restrict__ hi,
+                                                              void* __restrict__ lo,
+                                                              uint32_t* __restrict__ ctab,
+                                                              uint32_t* __restrict__ coltab, int taps,
+                                                              MagicDiv dK8, MagicDiv dC8) {
+  const int Cpf = g.Cgrp * 8;
+  const uint32_t k8n = uint32_t(g.Ktot / 8);
+  const uint32_t total8 = uint32_t(g.Np) * k8n;
+  const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x, stride = gridDim.x * blockDim.x;
+  for (uint32_t i = tid; i < total8; i += stride) {
+    uint32_t row32, k8;
+    mdivmod(i, dK8, row32, k8);
+    const int row = int(row32), kcol = int(k8) * 8;
+    float v[8];
+#pragma unroll
+    for (int j = 0; j < 8; j++) v[j] = 0.0f;
+    if (kcol < taps * Cpf && row < g.Ncol) {
+      uint32_t tapu, c8;
+      mdivmod(k8, dC8, tapu, c8);
+      const int tap = int(tapu), cin0 = int(c8) * 8;
+      const int dhb = tap / g.tapW, dwb = tap - dhb * g.tapW;
+      const int e = row / g.Ncol0, r0 = row - e * g.Ncol0;
+      const int eh = g.bdir == 2 ? e / g.bw : (g.bdir ? e : 0);
+      const int ew = g.bdir == 2 ? e - eh * g.bw : (g.bdir ? 0 : e);
+      const int dw = dwb - ew * g.vstep, dh = dhb - eh * g.ustep;
+      const bool tap_ok = dw >= 0 && dw < g.Sg && dh >= 0 && dh < g.Rg;
+      if (!g.dgrad) {
+        if (tap_ok && r0 < g.K) {
+#pragma unroll
+          for (int j = 0; j < 8; j++)
+            if (cin0 + j < g.C) v[j] = fetch_filter(g, f, r0, cin0 + j, dh, dw);
+        }
+      } else {
+        const int phase = r0 / g.C, c_col = r0 - phase * g.C;
+        const int ph = phase / g.v, pw = phase - ph * g.v;
+        const int rp = phase_tap(ph, dh, g.lo_h, g.u, g.pad_h, g.R);
+        const int sp = tap_ok ? phase_tap(pw, dw, g.lo_w, g.v, g.pad_w, g.S) : -1;
+        if (rp >= 0 && sp >= 0) {
+#pragma unroll
+          for (int j = 0; j < 8; j++)
+            if (cin0 + j < g.K) v[j] = fetch_filter(g, f, cin0 + j, c_col, rp, sp);
+        }
+      }
+    }
+    store_split8<ES>(hi, lo, int64_t(row) * g.Ktot + kcol, v);
+  }
+  // chunk table (cp.async gather; row 0 of the per-tap kernel)
+  for (uint32_t i = tid; i < uint32_t(taps * g.Cgrp); i += stride) {
+    const int tap = int(i) / g.Cgrp, grp = int(i) - tap * g.Cgrp;
+    ctab[i] = (uint32_t(tap / g.tapW) << 24) | (uint32_t(tap % g.tapW) << 16) | uint32_t(grp * 8);
+  }
+  // column table (bwd-data phases / blocked columns)
+  if (g.dgrad || g.bw > 1) {
+    for (uint32_t i = tid; i < uint32_t(g.Ncol); i += stride) {
+      const int row = int(i);
+      const int e = row / g.Ncol0, r0 = row - e * g.Ncol0;
+      const int eh = g.bdir == 2 ? e / g.bw : (g.bdir ? e : 0);
+      const int ew = g.bdir == 2 ? e - eh * g.bw : (g.bdir ? 0 : e);
+      uint32_t oh_, ow_, oc_;
+      if (!g.dgrad) {
+        oh_ = uint32_t(eh), ow_ = uint32_t(ew), oc_ = uint32_t(r0);
+      } else if (g.su * g.sv > 1) {  // space-to-depth column (rh, rw, c)
+        const int q = r0 / g.C0;
+        oh_ = uint32_t(q / g.sv), ow_ = uint32_t(e * g.sv + q % g.sv), oc_ = uint32_t(r0 - q * g.C0);
+      } else {
+        const int phase = r0 / g.C, c_col = r0 - phase * g.C;
+        const int ph = phase / g.v, pw = phase - ph * g.v;
+        oh_ = uint32_t(eh * g.u + ph), ow_ = uint32_t(ew * g.v + pw), oc_ = uint32_t(c_col);
+      }
+      coltab[row] = (oh_ << 24) | (ow_ << 16) | oc_;
+    }
+  }
+}
+
 // Forward filter packing, one block per GEMM column row (all taps): the
 // row's filter f[k][:][:][:] (contiguous C*R*S floats) is staged in shared
 // memory with coalesced loads, then each warp writes whole taps of the packed
@@ -835,12 +918,24 @@ cudaError_t run_gemm(const ConvProblem& p, Gemm g, const void* a_hi, const void*
     else
       pack_filter_row_kernel<2><<<unsigned(pg.Np), 256, frow, st>>>(pg, f, b_hi, b_lo, ctab, coltab,
                                                                     taps);
-  } else if (!::dnnp::tune_env("DNNP_PACK_SCATTER") || pg.bw > 1) {
+  } else if (::dnnp::tune_env("DNNP_PACK_TAP")) {
+    // per-(tap, row) blocks (the round-1 kernel; A/B only)
     const dim3 fgrid(unsigned(taps + 1), unsigned(pg.Np));
     if (es == 4)
       pack_filter_tap_kernel<4><<<fgrid, 128, 0, st>>>(pg, f, b_hi, b_lo, ctab, coltab, taps);
     else
       pack_filter_tap_kernel<2><<<fgrid, 128, 0, st>>>(pg, f, b_hi, b_lo, ctab, coltab, taps);
+  } else if (!::dnnp::tune_env("DNNP_PACK_SCATTER") || pg.bw > 1) {
+    const int64_t total8 = int64_t(pg.Np) * (pg.Ktot / 8);
+    if (total8 >= (int64_t(1) << 32)) return cudaErrorInvalidValue;
+    const unsigned fgrid = grid_for(std::max<int64_t>(total8, pg.KC), 256, 8);
+    const MagicDiv dK8 = make_magic(uint32_t(pg.Ktot / 8)), dC8 = make_magic(uint32_t(pg.Cgrp));
+    if (es == 4)
+      pack_filter_vec_kernel<4><<<fgrid, 256, 0, st>>>(pg, f, b_hi, b_lo, ctab, coltab, taps, dK8,
+                                                       dC8);
+    else
+      pack_filter_vec_kernel<2><<<fgrid, 256, 0, st>>>(pg, f, b_hi, b_lo, ctab, coltab, taps, dK8,
+                                                       dC8);
   } else {
     if (!tc::dry_run() && (e = cudaMemsetAsync(b_hi, 0, flt * 2 * es, st)) != cudaSuccess)
       return e;  // hi and lo planes
