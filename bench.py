@@ -669,6 +669,17 @@ def main():
         except Exception:
             traffic = None
 
+    # the dominant op's DRAM traffic with its operand packs (ncu over the
+    # op's kernels, profiles/r02/op_traffic.json) against its algorithmic
+    # x + f + y bytes: the pack pre-pass's share of the traffic
+    op_traffic = None
+    opath = os.path.join(ROOT, "profiles", "r02", "op_traffic.json")
+    if os.path.exists(opath):
+        try:
+            op_traffic = json.load(open(opath))["ops"].get(f"{layers[dl]['name']}.{PASSES[dpi]}")
+        except Exception:
+            op_traffic = None
+
     # ---- e2e: same step through the C ABI with pinned HOST buffers --------
     e2e = None
     if not args.no_e2e:
@@ -709,7 +720,8 @@ def main():
                      "bf16x3_ceiling": round(bf16 / 3.0, 1),
                      "frac_of_bf16x3_ceiling": round(achieved / (bf16 / 3.0), 4),
                      "work_per_launch_flops": layers[dl]["flops"],
-                     "l2_to_sm_ingest": ingest},
+                     "l2_to_sm_ingest": ingest,
+                     "op_traffic": op_traffic},
         "sustained": sustained,
         "math_sweep": math_sweep(step_flops, total_ms / args.steps, tf32_ms, bf16),
         "gpu_launches": int(launches),
