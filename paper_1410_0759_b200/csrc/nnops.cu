@@ -1707,79 +1707,117 @@ __device__ __forceinline__ void take_best(RowBest<T>& b, T v, int w) {
 // the time) and more loads are in flight per SM.
 constexpr int kPoolRows = 7;
 
-template <typename T, int KIND>
+// One chunk of RP output rows of one lane: the 2 RP + 1 input rows x 3
+// columns are loaded up front (one memory latency per warp), row-reduced,
+// then combined in h order.  Offsets are 32-bit inside one image (the host
+// checks the image span), rows / columns step by the view's strides, so the
+// same code serves unit-stride rows (lane = output column) and
+// channels-innermost views (lane = channel).  RP is a compile-time count:
+// full chunks carry no per-row predicates.
+template <typename T, int KIND, int RP>
+__device__ __forceinline__ void pool3s2_fwd_chunk(const T* __restrict__ xi, int xo, int xsh, int xsw,
+                                                  T* __restrict__ yi, int yo, int ysh,
+                                                  int64_t* __restrict__ ab, int64_t abase, int aq,
+                                                  int W, int p0, int w0) {
+  constexpr int NR = 2 * RP + 1;
+  T v[NR][3];
+#pragma unroll
+  for (int r = 0; r < NR; r++) {
+    const int o = xo + (2 * p0 + r) * xsh;
+    v[r][0] = __ldg(xi + o);
+    v[r][1] = __ldg(xi + o + xsw);
+    v[r][2] = __ldg(xi + o + 2 * xsw);
+  }
+  T bv[NR];
+  int bw[NR];
+#pragma unroll
+  for (int r = 0; r < NR; r++) {
+    if (KIND == 0) {
+      // a later value wins when greater, or when it is NaN and the best is not
+      T b = v[r][0];
+      int w = 0;
+      bool t = v[r][1] > b || (v[r][1] != v[r][1] && b == b);
+      b = t ? v[r][1] : b;
+      w = t ? 1 : w;
+      t = v[r][2] > b || (v[r][2] != v[r][2] && b == b);
+      bv[r] = t ? v[r][2] : b;
+      bw[r] = t ? 2 : w;
+    } else {
+      bv[r] = dadd<T>(dadd<T>(v[r][0], v[r][1]), v[r][2]);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < RP; i++) {
+    const int p = p0 + i;
+    if (KIND == 0) {
+      T b = bv[2 * i];
+      int code = bw[2 * i];  // 3 * (row in window) + column
+      bool t = bv[2 * i + 1] > b || (bv[2 * i + 1] != bv[2 * i + 1] && b == b);
+      b = t ? bv[2 * i + 1] : b;
+      code = t ? 3 + bw[2 * i + 1] : code;
+      t = bv[2 * i + 2] > b || (bv[2 * i + 2] != bv[2 * i + 2] && b == b);
+      b = t ? bv[2 * i + 2] : b;
+      code = t ? 6 + bw[2 * i + 2] : code;
+      yi[yo + p * ysh] = b;
+      if (ab) {
+        const int rr = code >= 6 ? 2 : (code >= 3 ? 1 : 0);
+        ab[int64_t(p) * aq] = abase + int64_t(2 * p + rr) * W + (w0 + code - 3 * rr);
+      }
+    } else {
+      yi[yo + p * ysh] = dadd<T>(dadd<T>(bv[2 * i], bv[2 * i + 1]), bv[2 * i + 2]) / T(9);
+    }
+  }
+}
+
+// Warps: (image or plane, 32 lanes, chunk of kPoolRows output rows).
+// CL = 0: lane = output column q of one (n, c) plane; CL = 1: lane =
+// channel c of one output column q (channels-innermost views).
+template <typename T, int KIND, int CL>
 __global__ void __launch_bounds__(128) pool3s2_fwd_kernel(PoolGeom g, const T* __restrict__ x,
                                                           T* __restrict__ y,
-                                                          int64_t* __restrict__ argmax, int nqb,
+                                                          int64_t* __restrict__ argmax, int nlb,
                                                           int nrc) {
   const int H = int(g.H), W = int(g.W), P = int(g.P), Q = int(g.Q), C = int(g.C);
   const int gw = int((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   const int lane = threadIdx.x & 31;
-  const int planes = int(g.N) * C;
-  if (gw >= planes * nqb * nrc) return;
+  // CL = 0: warps over (n, c, q block, row chunk); CL = 1: (n, q, c block, row chunk)
+  const int outer = CL ? int(g.N) * Q : int(g.N) * C;
+  if (gw >= outer * nlb * nrc) return;
   const int rc = gw % nrc, t = gw / nrc;
-  const int pl = t / nqb, qb = t - pl * nqb;
-  const int q = qb * 32 + lane;
-  if (q >= Q) return;
-  const int p0 = rc * kPoolRows, p1 = min(P, p0 + kPoolRows);
-  const int n = pl / C, c = pl - n * C;
-  const T* xb = x + int64_t(n) * g.x.sn + int64_t(c) * g.x.sc;
-  T* yb = y + int64_t(n) * g.y.sn + int64_t(c) * g.y.sc + int64_t(q) * g.y.sw;
+  const int o = t / nlb, lb = t - o * nlb;
+  int n, c, q;
+  if (CL) {
+    n = o / Q;
+    q = o - n * Q;
+    c = lb * 32 + lane;
+    if (c >= C) return;
+  } else {
+    n = o / C;
+    c = o - n * C;
+    q = lb * 32 + lane;
+    if (q >= Q) return;
+  }
+  const int p0 = rc * kPoolRows, rows = min(P - p0, kPoolRows);
+  const int w0 = 2 * q;
+  const T* xi = x + int64_t(n) * g.x.sn;
+  T* yi = y + int64_t(n) * g.y.sn;
+  const int xo = int(c * g.x.sc + w0 * g.x.sw), yo = int(c * g.y.sc + q * g.y.sw);
+  const int xsh = int(g.x.sh), xsw = int(g.x.sw), ysh = int(g.y.sh);
+  const int pl = n * C + c;
   int64_t* ab = argmax ? argmax + int64_t(pl) * P * Q + q : nullptr;
   const int64_t abase = int64_t(pl) * H * W;
-  const int w0 = 2 * q;
-  // every input value of the chunk is loaded up front (2 RP + 1 rows x 3
-  // columns in registers): one memory latency per warp instead of one per
-  // output row
-  constexpr int NR = 2 * kPoolRows + 1;
-  T v[NR][3];
-#pragma unroll
-  for (int r = 0; r < NR; r++) {
-    const int h = 2 * p0 + r;
-    if (h <= 2 * p1) {
-      const T* row = xb + int64_t(h) * g.x.sh + w0;
-      v[r][0] = __ldg(row);
-      v[r][1] = __ldg(row + 1);
-      v[r][2] = __ldg(row + 2);
-    }
+#define DNNP_POOL_CHUNK(RP)                                                                   \
+  pool3s2_fwd_chunk<T, KIND, RP>(xi, xo, xsh, xsw, yi, yo, ysh, ab, abase, Q, W, p0, w0)
+  switch (rows) {
+    case 7: DNNP_POOL_CHUNK(7); break;
+    case 6: DNNP_POOL_CHUNK(6); break;
+    case 5: DNNP_POOL_CHUNK(5); break;
+    case 4: DNNP_POOL_CHUNK(4); break;
+    case 3: DNNP_POOL_CHUNK(3); break;
+    case 2: DNNP_POOL_CHUNK(2); break;
+    default: DNNP_POOL_CHUNK(1); break;
   }
-  RowBest<T> rb[NR];
-#pragma unroll
-  for (int r = 0; r < NR; r++) {
-    if (KIND == 0) {
-      rb[r].v = v[r][0];
-      rb[r].w = w0;
-      take_best(rb[r], v[r][1], w0 + 1);
-      take_best(rb[r], v[r][2], w0 + 2);
-    } else {
-      rb[r].v = dadd<T>(dadd<T>(v[r][0], v[r][1]), v[r][2]);
-      rb[r].w = 0;
-    }
-  }
-#pragma unroll
-  for (int i = 0; i < kPoolRows; i++) {
-    const int p = p0 + i;
-    if (p >= p1) break;
-    const RowBest<T>& r0 = rb[2 * i];
-    const RowBest<T>& r1 = rb[2 * i + 1];
-    const RowBest<T>& r2 = rb[2 * i + 2];
-    if (KIND == 0) {
-      RowBest<T> b = r0;
-      int bh = 2 * p;
-      const bool t1 = r1.v > b.v || (r1.v != r1.v && b.v == b.v);
-      b.v = t1 ? r1.v : b.v;
-      b.w = t1 ? r1.w : b.w;
-      bh = t1 ? 2 * p + 1 : bh;
-      const bool t2 = r2.v > b.v || (r2.v != r2.v && b.v == b.v);
-      b.v = t2 ? r2.v : b.v;
-      b.w = t2 ? r2.w : b.w;
-      bh = t2 ? 2 * p + 2 : bh;
-      yb[int64_t(p) * g.y.sh] = b.v;
-      if (ab) ab[int64_t(p) * Q] = abase + int64_t(bh) * W + b.w;
-    } else {
-      yb[int64_t(p) * g.y.sh] = dadd<T>(dadd<T>(r0.v, r1.v), r2.v) / T(9);
-    }
-  }
+#undef DNNP_POOL_CHUNK
 }
 
 // Backward of the same geometry, gather form in the reference's summation
@@ -1904,11 +1942,26 @@ __global__ void __launch_bounds__(128) pool3s2_bwd_kernel(PoolGeom g, const T* _
 }
 
 // whether the 3 x 3 / 2 plane kernels take this problem
-static bool pool3s2_ok(const PoolProblem& pp, const View4& xv, const View4& yv) {
+// the geometry of the 3 x 3 / 2 kernels (no padding, every window inside)
+static bool pool3s2_geom(const PoolProblem& pp, const View4& xv, const View4& yv) {
+  auto span = [](const View4& v) {  // largest element offset inside one image
+    return (v.c - 1) * v.sc + (v.h - 1) * v.sh + (v.w - 1) * v.sw;
+  };
   return pp.wh == 3 && pp.ww == 3 && pp.sh == 2 && pp.sw == 2 && pp.ph == 0 && pp.pw == 0 &&
-         xv.sw == 1 && yv.sw == 1 && xv.h >= 3 && xv.w >= 3 && pp.P == (xv.h - 3) / 2 + 1 &&
-         pp.Q == (xv.w - 3) / 2 + 1 && xv.n * xv.c * ceil_div(xv.w, 64) * ceil_div(xv.h, 14) < (int64_t(1) << 26) &&
-         xv.h * xv.w < (int64_t(1) << 31) && !::dnnp::tune_env("DNNP_POOL_NO_3S2");
+         xv.h >= 3 && xv.w >= 3 && pp.P == (xv.h - 3) / 2 + 1 && pp.Q == (xv.w - 3) / 2 + 1 &&
+         span(xv) < (int64_t(1) << 31) && span(yv) < (int64_t(1) << 31) &&
+         xv.n * xv.c * xv.h * xv.w < (int64_t(1) << 40) &&
+         xv.n * xv.c * ceil_div(xv.w, 64) * ceil_div(xv.h, 14) < (int64_t(1) << 26) &&
+         xv.n * pp.Q * ceil_div(xv.c, 32) * ceil_div(xv.h, 14) < (int64_t(1) << 26) &&
+         !::dnnp::tune_env("DNNP_POOL_NO_3S2");
+}
+// forward: any strides (lanes along w for unit-stride rows, else along c)
+static bool pool3s2_ok(const PoolProblem& pp, const View4& xv, const View4& yv) {
+  return pool3s2_geom(pp, xv, yv);
+}
+// backward: unit-stride rows (lanes along w, shuffles between windows)
+static bool pool3s2_bwd_ok(const PoolProblem& pp, const View4& xv, const View4& yv) {
+  return pool3s2_geom(pp, xv, yv) && xv.sw == 1 && yv.sw == 1;
 }
 
 // Plane kernels: one (n, c) plane per block iteration, staged in shared
@@ -1955,18 +2008,24 @@ cudaError_t pool_forward(const PoolProblem& pp, Dtype dt, const View4& xv, const
   const size_t eb = dt == F32 ? 4 : 8;
   const size_t psm = size_t(xv.h) * xv.w * eb;
   if (pool3s2_ok(pp, xv, yv)) {
-    const int nqb = int(ceil_div(pp.Q, 32)), nrc = int(ceil_div(pp.P, kPoolRows));
-    const unsigned blocks = unsigned(ceil_div(xv.n * xv.c * nqb * nrc, 4));
+    // lanes along the unit-stride dimension: output columns (rows with sw
+    // == 1) or channels (channels-innermost views)
+    const bool cl = xv.sw != 1;
+    const int nlb = int(ceil_div(cl ? xv.c : pp.Q, 32)), nrc = int(ceil_div(pp.P, kPoolRows));
+    const unsigned blocks = unsigned(ceil_div(xv.n * (cl ? pp.Q : xv.c) * nlb * nrc, 4));
+    auto go = [&](auto tag, auto kind, auto clc) {
+      using TT = decltype(tag);
+      pool3s2_fwd_kernel<TT, decltype(kind)::value, decltype(clc)::value><<<blocks, 128, 0, st>>>(
+          g, (const TT*)x, (TT*)y, argmax, nlb, nrc);
+    };
+    using I0 = std::integral_constant<int, 0>;
+    using I1 = std::integral_constant<int, 1>;
     if (dt == F32) {
-      if (pp.kind == 0)
-        pool3s2_fwd_kernel<float, 0><<<blocks, 128, 0, st>>>(g, (const float*)x, (float*)y, argmax, nqb, nrc);
-      else
-        pool3s2_fwd_kernel<float, 1><<<blocks, 128, 0, st>>>(g, (const float*)x, (float*)y, argmax, nqb, nrc);
+      if (pp.kind == 0) { if (cl) go(float(), I0(), I1()); else go(float(), I0(), I0()); }
+      else { if (cl) go(float(), I1(), I1()); else go(float(), I1(), I0()); }
     } else {
-      if (pp.kind == 0)
-        pool3s2_fwd_kernel<double, 0><<<blocks, 128, 0, st>>>(g, (const double*)x, (double*)y, argmax, nqb, nrc);
-      else
-        pool3s2_fwd_kernel<double, 1><<<blocks, 128, 0, st>>>(g, (const double*)x, (double*)y, argmax, nqb, nrc);
+      if (pp.kind == 0) { if (cl) go(double(), I0(), I1()); else go(double(), I0(), I0()); }
+      else { if (cl) go(double(), I1(), I1()); else go(double(), I1(), I0()); }
     }
     note_launch();
     return cudaGetLastError();
@@ -2070,7 +2129,7 @@ cudaError_t pool_backward(const PoolProblem& pp, Dtype dt, const View4& dyv, con
   const size_t psm = ((size_t(dxv.h + dxv.w) * 8 + 15) & ~size_t(15)) +
                      ((size_t(dyv.h) * dyv.w * 4 + 15) & ~size_t(15)) + size_t(dyv.h) * dyv.w * eb +
                      (pp.kind == 0 ? size_t(dxv.h) * dxv.w * eb : 0);
-  if (pool3s2_ok(pp, dxv, dyv)) {
+  if (pool3s2_bwd_ok(pp, dxv, dyv)) {
     int* bad = nullptr;
     tc::Workspace ws(st);
     if (pp.kind == 0) {
