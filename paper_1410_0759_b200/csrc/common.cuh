@@ -47,6 +47,15 @@ __device__ __forceinline__ float dsub<float>(float a, float b) { return __fsub_r
 template <>
 __device__ __forceinline__ double dsub<double>(double a, double b) { return __dsub_rn(a, b); }
 
+// Programmatic dependent launch (sm_90+): a producer lets the next kernel
+// of the stream launch early (trigger); a kernel launched with the
+// programmatic-serialization attribute waits for its prerequisite grid to
+// complete -- memory visible -- before it touches what that grid wrote.
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 inline unsigned grid_for(int64_t work, int threads, int waves_cap = 32) {

@@ -563,6 +563,11 @@ __global__ void __launch_bounds__(256) pack_filter_vec_kernel(PackGeom g, const 
       coltab[row] = (oh_ << 24) | (ow_ << 16) | oc_;
     }
   }
+  pdl_trigger();
+  // launched programmatically after the operand pack (which it does not
+  // read): complete only once that pack has, so the GEMM's single wait
+  // covers both producers
+  pdl_wait();
 }
 
 // Forward filter packing, one block per GEMM column row (all taps): the
@@ -738,13 +743,15 @@ cudaError_t launch_tma(const TmaParams& prm, cudaStream_t st) {
   cfg.blockDim = dim3(kTmaThreads);
   cfg.dynamicSmemBytes = CC::SMEM;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = NC;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  unsigned nattr = 1;
+  add_pdl_attr(attr, &nattr);  // prologue overlaps the packs; pdl_wait() before any operand read
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = nattr;
   if (::dnnp::diag_env("DNNP_TC_DIAG")) {
     int ncl = -1;
     cudaError_t qe = cudaOccupancyMaxActiveClusters(&ncl, conv_tma_kernel<BN, CB, NC, ES>, &cfg);
@@ -930,12 +937,20 @@ cudaError_t run_gemm(const ConvProblem& p, Gemm g, const void* a_hi, const void*
     if (total8 >= (int64_t(1) << 32)) return cudaErrorInvalidValue;
     const unsigned fgrid = grid_for(std::max<int64_t>(total8, pg.KC), 256, 8);
     const MagicDiv dK8 = make_magic(uint32_t(pg.Ktot / 8)), dC8 = make_magic(uint32_t(pg.Cgrp));
-    if (es == 4)
-      pack_filter_vec_kernel<4><<<fgrid, 256, 0, st>>>(pg, f, b_hi, b_lo, ctab, coltab, taps, dK8,
-                                                       dC8);
-    else
-      pack_filter_vec_kernel<2><<<fgrid, 256, 0, st>>>(pg, f, b_hi, b_lo, ctab, coltab, taps, dK8,
-                                                       dC8);
+    cudaLaunchConfig_t fc{};
+    fc.gridDim = dim3(fgrid);
+    fc.blockDim = dim3(256);
+    fc.stream = st;
+    cudaLaunchAttribute fa[1];
+    unsigned nfa = 0;
+    add_pdl_attr(fa, &nfa);
+    fc.attrs = fa;
+    fc.numAttrs = nfa;
+    e = es == 4 ? cudaLaunchKernelEx(&fc, pack_filter_vec_kernel<4>, pg, f, b_hi, b_lo, ctab, coltab,
+                                     taps, dK8, dC8)
+                : cudaLaunchKernelEx(&fc, pack_filter_vec_kernel<2>, pg, f, b_hi, b_lo, ctab, coltab,
+                                     taps, dK8, dC8);
+    if (e != cudaSuccess) return e;
   } else {
     if (!tc::dry_run() && (e = cudaMemsetAsync(b_hi, 0, flt * 2 * es, st)) != cudaSuccess)
       return e;  // hi and lo planes

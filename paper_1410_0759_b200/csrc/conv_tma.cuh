@@ -366,6 +366,10 @@ __global__ void __launch_bounds__(kTmaThreads, 1) conv_tma_kernel(const __grid_c
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   const uint32_t smem0 = ptx::smem_u32(smem);
+  // launched programmatically behind the operand / filter packs: everything
+  // above (barriers, TMEM) overlapped their tail; nothing below may run
+  // before their writes are visible
+  pdl_wait();
   WorkIter wi;
   wi.init(P, cid, ncl);
   int tile, kb0, kb1, piece, np;

@@ -93,6 +93,17 @@ struct Workspace {
   size_t fb_bytes_ = 0;
 };
 
+// Programmatic dependent launch for the kernel chain of one call (operand
+// pack -> filter pack -> GEMM): appends the programmatic-serialization
+// attribute unless DNNP_NO_PDL; the dependent kernel calls pdl_wait() before
+// reading its producers' output.
+inline void add_pdl_attr(cudaLaunchAttribute* attrs, unsigned* n) {
+  if (::dnnp::tune_env("DNNP_NO_PDL")) return;
+  attrs[*n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attrs[*n].val.programmaticStreamSerializationAllowed = 1;
+  ++*n;
+}
+
 void pool_keep_memory();     // creates this device's library pool (lib_pool)
 cudaMemPool_t lib_pool();    // the library's stream-ordered pool on the current device
 

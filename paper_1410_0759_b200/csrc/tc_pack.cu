@@ -93,6 +93,7 @@ __global__ void __launch_bounds__(256) pack_act_kernel(View4 v, const float* __r
     }
     __syncthreads();
   }
+  pdl_trigger();  // this CTA is done: the call's next kernel may launch
 }
 
 // Same transpose with 64-pixel jobs: each thread loads 16 values (two
@@ -152,6 +153,7 @@ __global__ void __launch_bounds__(256) pack_act_wide_kernel(View4 v, const float
     }
     __syncthreads();
   }
+  pdl_trigger();  // this CTA is done: the call's next kernel may launch
 }
 
 // Cp <= 16: one thread per pixel reads its C values (pixel-contiguous across
@@ -178,6 +180,7 @@ __global__ void __launch_bounds__(256) pack_act_small_kernel(View4 v, const floa
       store_split8<ES>(hi, lo, o, v8);
     }
   }
+  pdl_trigger();  // this CTA is done: the call's next kernel may launch
 }
 
 // Space-to-depth: one thread per super-pixel (n, h', w'); walks its Cp
@@ -222,6 +225,7 @@ __global__ void __launch_bounds__(256) pack_act_s2d_kernel(View4 v, const float*
       store_split8<ES>(hi, lo, o, v8);
     }
   }
+  pdl_trigger();  // this CTA is done: the call's next kernel may launch
 }
 
 // Space-to-depth, one block per output row (n, h'): the u input rows of
@@ -271,6 +275,7 @@ __global__ void __launch_bounds__(256) pack_act_s2d_row_kernel(View4 v, const fl
     }
     __syncthreads();
   }
+  pdl_trigger();  // this CTA is done: the call's next kernel may launch
 }
 
 // Space-to-depth fast path for dense NCHW rows (sw == 1, sh == W, W % 4 == 0):
@@ -328,6 +333,7 @@ __global__ void __launch_bounds__(256) pack_act_s2d_dense_kernel(View4 v, const 
     const int64_t o = obase + int64_t(w2) * Cp + g * 8;
     store_split8<ES>(hi, lo, o, v8);
   }
+  pdl_trigger();  // this CTA is done: the call's next kernel may launch
 }
 
 // Space-to-depth for dense NCHW input with even v and pad_w (AlexNet conv1:
@@ -396,6 +402,7 @@ __global__ void __launch_bounds__(512) pack_act_s2d_quad_kernel(View4 v, const f
     const int64_t o = obase + int64_t(pi) * Cp + g * 8;
     store_split8<ES>(hi, lo, o, v8);
   }
+  pdl_trigger();  // this CTA is done: the call's next kernel may launch
 }
 
 // Tap folding: one thread per output pixel (n, h, q), walking its Cp folded
@@ -436,6 +443,7 @@ __global__ void __launch_bounds__(256) pack_act_fold_kernel(View4 v, const float
       store_split8<ES>(hi, lo, o, v8);
     }
   }
+  pdl_trigger();  // this CTA is done: the call's next kernel may launch
 }
 
 }  // namespace

@@ -99,6 +99,7 @@ __global__ void __launch_bounds__(kThreads, 1) wgrad_tc_kernel(const __grid_cons
   ptx::tc_fence_after();
   const uint32_t tmem_d = *tmem_slot;
   const uint32_t smem0 = ptx::smem_u32(smem);
+  pdl_wait();  // programmatic launch behind the packs: read nothing they write before this
 
   if (warp < kProdWarps) {
     // A (dy, dense per pixel) arrives by TMA; B (im2col of x) is gathered with
@@ -407,6 +408,7 @@ __global__ void __launch_bounds__(kWgThreads, 1) wgrad_tma_kernel(const __grid_c
   ptx::tc_fence_after();
   const uint32_t tmem_d = *tmem_slot;
   const uint32_t smem0 = ptx::smem_u32(smem);
+  pdl_wait();  // programmatic launch behind the packs: read nothing they write before this
 
   if (warp < 3) {
     // three producers (one TMA instruction costs its thread ~110-130 cycles):
@@ -598,13 +600,15 @@ cudaError_t launch_wgrad_tma(const WgTmaParams& prm, dim3 grid, cudaStream_t st)
   cfg.blockDim = dim3(kWgThreads);
   cfg.dynamicSmemBytes = CC::SMEM;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = NC;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  unsigned nattr = 1;
+  add_pdl_attr(attr, &nattr);
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = nattr;
   ktime_begin(st, 2);
   cudaError_t e = cudaLaunchKernelEx(&cfg, wgrad_tma_kernel<BN, NC, PX, BW, ES>, prm);
   ktime_end(st);
