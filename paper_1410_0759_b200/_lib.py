@@ -11,7 +11,7 @@ import threading
 from . import errors
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdnnp.so")
+LIB_PATH = os.environ.get("DNNP_LIB_PATH") or os.path.join(_HERE, "libdnnp.so")  # override: A/B builds
 
 OK, BAD_PARAM, SHAPE_MISMATCH, ALLOC_FAILED, NOT_SUPPORTED = 0, 1, 2, 3, 4
 F32, F64 = 0, 1

@@ -14,6 +14,8 @@
 //                 over NPQ with a fixed-order reduction (deterministic).
 #include <algorithm>
 
+#include <type_traits>
+
 #include "common.cuh"
 #include "tc_common.cuh"
 
@@ -50,6 +52,12 @@ struct SimtCfg<float> {
 template <>
 struct SimtCfg<double> {
   static constexpr int BM = 64, BN = 64, BK = 8, TM = 4, TN = 4;
+};
+// fp64 backward-data: 16-deep k-steps halve the barriers per FMA of the
+// phase-gathered reduction (AlexNet conv2-5 bwd-data 5.2-8.5 -> 6.4-9.6 TF/s;
+// the same change costs forward / backward-filter, tools/bench_f64.py)
+struct SimtCfgDgrad64 {
+  static constexpr int BM = 64, BN = 64, BK = 16, TM = 4, TN = 4;
 };
 // Narrow GEMM outputs (N <= 16 columns, e.g. table2 layer1 bwd-data: C = 3):
 // a 64-wide tile wastes >= 75% of its FMAs, so rows take the width.
@@ -400,6 +408,8 @@ template <typename T, int PASS>
 static cudaError_t launch_simt(SimtArgs& a, cudaStream_t st) {
   if (PASS != WGRAD && a.Ncol <= 16 && a.M >= 4096 && !::dnnp::tune_env("DNNP_SIMT_NO_NARROW"))
     return launch_simt_cfg<T, PASS, SimtNarrow<T>>(a, st);
+  if constexpr (PASS == DGRAD && std::is_same<T, double>::value)
+    return launch_simt_cfg<T, PASS, SimtCfgDgrad64>(a, st);
   return launch_simt_cfg<T, PASS, SimtCfg<T>>(a, st);
 }
 
