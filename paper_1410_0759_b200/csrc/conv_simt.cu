@@ -72,12 +72,25 @@ struct SimtNarrow<double> {
   static constexpr int BM = 128, BN = 16, BK = 16, TM = 4, TN = 2;
 };
 
-// A(m, k) element of the pass' left operand.
+// Outputs of at most 4 columns (AlexNet conv1 bwd-data: C = 3): one row per
+// thread and the whole width in registers, so 3/4 of the FMAs are useful
+// instead of 3/16 (fp64 conv1 bwd-data N=16 2.75 -> see tools/bench_f64.py).
+struct SimtTiny {
+  static constexpr int BM = 64, BN = 4, BK = 16, TM = 1, TN = 4;
+};
+
+// Row (output-pixel) context of an A operand row.  FWD / DGRAD: A(m, k) =
+// src[base + koff(k)] when 0 <= hb + dr(k) < lim_h and 0 <= wb + dw(k) <
+// lim_w, so the per-element work is two adds, two compares and a load; the
+// k decode (dr, dw, koff) is done once per k-step by one lane (KDec below).
+//   FWD:   hb, wb = p*u - pad_h, q*v - pad_w; base = x(n, hb, wb); dr = r
+//   DGRAD: hb, wb = i + (ph + pad_h) / u, j + (pw + pad_w) / v (the dy row
+//          of tap 0 of the phase); base = dy(n, hb, wb); dr = -jr, so that
+//          hb + dr = (h + pad_h - r) / u exactly for the phase's taps r
 template <typename T, int PASS>
 struct RowCtx {
   int64_t base;     // pass-specific row base offset
-  int32_t hb, wb;   // FWD: p*u - pad_h, q*v - pad_w; DGRAD: h + pad_h, w + pad_w
-  uint32_t n;
+  int32_t hb, wb;
   bool valid;
 };
 
@@ -87,103 +100,76 @@ __device__ __forceinline__ RowCtx<T, PASS> row_ctx(const SimtArgs& a, int64_t m)
   rc.valid = m < a.M;
   const ConvProblem& p = a.p;
   if (!rc.valid) {
-    rc.base = 0; rc.hb = rc.wb = 0; rc.n = 0;
+    rc.base = 0; rc.hb = rc.wb = 0;
     return rc;
   }
   if (PASS == FWD) {
     uint32_t n, rem, pp, qq;
     mdivmod(uint32_t(m), a.dPQ, n, rem);
     mdivmod(rem, a.dQ, pp, qq);
-    rc.n = n;
-    rc.base = int64_t(n) * p.x.sn;
     rc.hb = int32_t(pp * p.u - p.pad_h);
     rc.wb = int32_t(qq * p.v - p.pad_w);
+    rc.base = int64_t(n) * p.x.sn + int64_t(rc.hb) * p.x.sh + int64_t(rc.wb) * p.x.sw;
   } else if (PASS == DGRAD) {
     uint32_t n, rem, i, j;
     mdivmod(uint32_t(m), a.dHWph, n, rem);
     mdivmod(rem, a.dWph, i, j);
     const int u = int(p.u), v = int(p.v);
     const int ph = int(blockIdx.z) / v, pw = int(blockIdx.z) - (int(blockIdx.z) / v) * v;
-    const int h = int(i) * u + ph, w = int(j) * v + pw;
-    rc.valid = h < p.H && w < p.W;
-    rc.n = n;
-    rc.base = int64_t(n) * p.y.sn;
-    rc.hb = int32_t(h + p.pad_h);
-    rc.wb = int32_t(w + p.pad_w);
+    rc.valid = int(i) * u + ph < p.H && int(j) * v + pw < p.W;
+    rc.hb = int32_t(i) + (ph + int(p.pad_h)) / u;
+    rc.wb = int32_t(j) + (pw + int(p.pad_w)) / v;
+    rc.base = int64_t(n) * p.y.sn + int64_t(rc.hb) * p.y.sh + int64_t(rc.wb) * p.y.sw;
   } else {  // WGRAD: row = output channel k of dy
-    rc.n = 0;
     rc.base = m * p.y.sc;
     rc.hb = rc.wb = 0;
   }
   return rc;
 }
 
+// Per-k decode of the FWD / DGRAD reduction index, computed by lane k - k0
+// of each warp and broadcast with shuffles (every thread used to redo the two
+// magic divisions per element: 3-4x the FMA count of a thin tile).  An
+// out-of-range k (past kend, or a tap outside the phase) gets dr = kNoTap,
+// which fails the row bound check, and boff = -1.
+constexpr int32_t kNoTap = -(1 << 30);
+struct KDec {
+  int64_t aoff;  // A: channel / tap offset from the row base
+  int64_t boff;  // DGRAD B: f[kk][0][r][s] offset (add col * R * S)
+  int32_t dr, dw;
+};
+
 template <typename T, int PASS>
-__device__ __forceinline__ T load_a(const SimtArgs& a, const RowCtx<T, PASS>& rc, int64_t k,
-                                    int t0h, int t0w) {
+__device__ __forceinline__ KDec k_decode(const SimtArgs& a, int64_t k, int64_t kend, int t0h,
+                                         int t0w) {
+  KDec d;
+  d.aoff = 0;
+  d.boff = -1;
+  d.dr = kNoTap;
+  d.dw = 0;
+  if (k >= kend) return d;
   const ConvProblem& p = a.p;
-  if (!rc.valid || k >= a.Kred) return T(0);
-  const T* src = static_cast<const T*>(a.a_src);
   if (PASS == FWD) {
     uint32_t c, rs, r, s;
     mdivmod(uint32_t(k), a.dRS, c, rs);
     mdivmod(rs, a.dS, r, s);
-    const int32_t hr = p.flip ? int32_t(p.R - 1 - r) : int32_t(r);
-    const int32_t wr = p.flip ? int32_t(p.S - 1 - s) : int32_t(s);
-    const int32_t h = rc.hb + hr, w = rc.wb + wr;
-    if (uint32_t(h) >= uint32_t(p.H) || uint32_t(w) >= uint32_t(p.W)) return T(0);
-    return src[rc.base + int64_t(c) * p.x.sc + int64_t(h) * p.x.sh + int64_t(w) * p.x.sw];
-  } else if (PASS == DGRAD) {
-    uint32_t kk, rs, jr, js;
-    mdivmod(uint32_t(k), a.dRSph, kk, rs);
-    mdivmod(rs, a.dSph, jr, js);
-    const int32_t ro = t0h + int32_t(p.u) * int32_t(jr);  // gather offset
-    const int32_t so = t0w + int32_t(p.v) * int32_t(js);
-    if (ro >= p.R || so >= p.S) return T(0);
-    const int32_t th = rc.hb - ro, tw = rc.wb - so;  // = p*u, q*v exactly
-    if (th < 0 || tw < 0) return T(0);
-    const uint32_t pp = mdiv(uint32_t(th), a.dU), qq = mdiv(uint32_t(tw), a.dV);
-    if (pp >= uint32_t(p.P) || qq >= uint32_t(p.Q)) return T(0);
-    return src[rc.base + int64_t(kk) * p.y.sc + int64_t(pp) * p.y.sh + int64_t(qq) * p.y.sw];
+    d.dr = p.flip ? int32_t(p.R - 1 - r) : int32_t(r);
+    d.dw = p.flip ? int32_t(p.S - 1 - s) : int32_t(s);
+    d.aoff = int64_t(c) * p.x.sc + int64_t(d.dr) * p.x.sh + int64_t(d.dw) * p.x.sw;
   } else {
-    uint32_t n, rem, pp, qq;
-    mdivmod(uint32_t(k), a.dPQ, n, rem);
-    mdivmod(rem, a.dQ, pp, qq);
-    return src[rc.base + int64_t(n) * p.y.sn + int64_t(pp) * p.y.sh + int64_t(qq) * p.y.sw];
-  }
-}
-
-// B(col, k) element of the right operand (stored as [col][k]).
-template <typename T, int PASS>
-__device__ __forceinline__ T load_b(const SimtArgs& a, int64_t col, int64_t k, int t0h, int t0w) {
-  const ConvProblem& p = a.p;
-  if (col >= a.Ncol || k >= a.Kred) return T(0);
-  const T* src = static_cast<const T*>(a.b_src);
-  if (PASS == FWD) {
-    return src[col * a.Kred + k];  // f[kout][crs]
-  } else if (PASS == DGRAD) {
     uint32_t kk, rs, jr, js;
     mdivmod(uint32_t(k), a.dRSph, kk, rs);
     mdivmod(rs, a.dSph, jr, js);
-    const int32_t ro = t0h + int32_t(p.u) * int32_t(jr);
+    const int32_t ro = t0h + int32_t(p.u) * int32_t(jr);  // filter tap of this phase
     const int32_t so = t0w + int32_t(p.v) * int32_t(js);
-    if (ro >= p.R || so >= p.S) return T(0);
+    if (ro >= p.R || so >= p.S) return d;
+    d.dr = -int32_t(jr);
+    d.dw = -int32_t(js);
+    d.aoff = int64_t(kk) * p.y.sc - int64_t(jr) * p.y.sh - int64_t(js) * p.y.sw;
     const int32_t r = p.flip ? int32_t(p.R - 1 - ro) : ro, s = p.flip ? int32_t(p.S - 1 - so) : so;
-    return src[((int64_t(kk) * p.C + col) * p.R + r) * p.S + s];  // f[kout][c][r][s]
-  } else {
-    uint32_t c, rs, r, s, n, rem, pp, qq;
-    mdivmod(uint32_t(col), a.dRS, c, rs);
-    mdivmod(rs, a.dS, r, s);
-    mdivmod(uint32_t(k), a.dPQ, n, rem);
-    mdivmod(rem, a.dQ, pp, qq);
-    const int32_t hr = p.flip ? int32_t(p.R - 1 - r) : int32_t(r);
-    const int32_t wr = p.flip ? int32_t(p.S - 1 - s) : int32_t(s);
-    const int32_t h = int32_t(pp * p.u - p.pad_h) + hr;
-    const int32_t w = int32_t(qq * p.v - p.pad_w) + wr;
-    if (uint32_t(h) >= uint32_t(p.H) || uint32_t(w) >= uint32_t(p.W)) return T(0);
-    return src[int64_t(n) * p.x.sn + int64_t(c) * p.x.sc + int64_t(h) * p.x.sh +
-               int64_t(w) * p.x.sw];
+    d.boff = (int64_t(kk) * p.C * p.R + r) * p.S + s;  // f[kout][c][r][s]
   }
+  return d;
 }
 
 template <typename T, int PASS, class CFG>
@@ -238,16 +224,83 @@ __global__ void __launch_bounds__((CFG::BM / CFG::TM) * (CFG::BN / CFG::TN))
     t0w = (int(blockIdx.z) - (int(blockIdx.z) / v) * v + int(a.p.pad_w)) % v;
   }
   T ra[LA], rb[LB];
-  auto gload = [&](int64_t k0) {
-#pragma unroll
-    for (int j = 0; j < LA; j++) {
-      int64_t k = k0 + a_ki[j];
-      ra[j] = k < kend ? load_a<T, PASS>(a, rc[j], k, t0h, t0w) : T(0);
-    }
+  const T* asrc = static_cast<const T*>(a.a_src);
+  const T* bsrc = static_cast<const T*>(a.b_src);
+  const uint32_t lim_h = uint32_t(PASS == FWD ? a.p.H : a.p.P);
+  const uint32_t lim_w = uint32_t(PASS == FWD ? a.p.W : a.p.Q);
+  const int64_t fcol = int64_t(a.p.R) * a.p.S;
+  // WGRAD B columns (c, r, s) of this thread: x offset and tap; hr = kNoTap
+  // for columns past Ncol
+  int64_t wq_off[PASS == WGRAD ? LB : 1];
+  int32_t wq_hr[PASS == WGRAD ? LB : 1], wq_wr[PASS == WGRAD ? LB : 1];
+  if constexpr (PASS == WGRAD) {
+    static_assert(NT % BK == 0, "one reduction pixel per thread and k-step");
+    const ConvProblem& p = a.p;
 #pragma unroll
     for (int j = 0; j < LB; j++) {
-      int64_t k = k0 + b_ki[j];
-      rb[j] = k < kend ? load_b<T, PASS>(a, n0 + b_ni[j], k, t0h, t0w) : T(0);
+      const int64_t col = n0 + b_ni[j];
+      wq_off[j] = 0;
+      wq_hr[j] = kNoTap;
+      wq_wr[j] = 0;
+      if (col < a.Ncol) {
+        uint32_t c, rs, r, s;
+        mdivmod(uint32_t(col), a.dRS, c, rs);
+        mdivmod(rs, a.dS, r, s);
+        wq_hr[j] = p.flip ? int32_t(p.R - 1 - r) : int32_t(r);
+        wq_wr[j] = p.flip ? int32_t(p.S - 1 - s) : int32_t(s);
+        wq_off[j] = int64_t(c) * p.x.sc + int64_t(wq_hr[j]) * p.x.sh + int64_t(wq_wr[j]) * p.x.sw;
+      }
+    }
+  }
+  auto gload = [&](int64_t k0) {
+    if constexpr (PASS == WGRAD) {
+      // every load of this thread is at reduction pixel k0 + tid % BK: one
+      // decode per k-step; the column (c, r, s) decode is hoisted (wq_*)
+      const int64_t k = k0 + tid % BK;
+      int64_t aoff = 0, boff = 0;
+      int32_t hk = kNoTap, wk = 0;
+      if (k < kend) {
+        const ConvProblem& p = a.p;
+        uint32_t n, rem, pp, qq;
+        mdivmod(uint32_t(k), a.dPQ, n, rem);
+        mdivmod(rem, a.dQ, pp, qq);
+        aoff = int64_t(n) * p.y.sn + int64_t(pp) * p.y.sh + int64_t(qq) * p.y.sw;
+        hk = int32_t(pp * p.u - p.pad_h);
+        wk = int32_t(qq * p.v - p.pad_w);
+        boff = int64_t(n) * p.x.sn + int64_t(hk) * p.x.sh + int64_t(wk) * p.x.sw;
+      }
+#pragma unroll
+      for (int j = 0; j < LA; j++) ra[j] = rc[j].valid && k < kend ? asrc[rc[j].base + aoff] : T(0);
+#pragma unroll
+      for (int j = 0; j < LB; j++) {
+        const bool ok = uint32_t(hk + wq_hr[j]) < uint32_t(a.p.H) &&
+                        uint32_t(wk + wq_wr[j]) < uint32_t(a.p.W);
+        rb[j] = ok ? bsrc[boff + wq_off[j]] : T(0);
+      }
+    } else {
+      static_assert(BK <= 32 && NT % 32 == 0, "one k per lane");
+      const int lane = tid & 31;
+      const KDec d = k_decode<T, PASS>(a, lane < BK ? k0 + lane : kend, kend, t0h, t0w);
+#pragma unroll
+      for (int j = 0; j < LA; j++) {
+        const int64_t ao = __shfl_sync(0xffffffffu, d.aoff, a_ki[j]);
+        const int32_t dr = __shfl_sync(0xffffffffu, d.dr, a_ki[j]);
+        const int32_t dw = __shfl_sync(0xffffffffu, d.dw, a_ki[j]);
+        const bool ok = rc[j].valid && uint32_t(rc[j].hb + dr) < lim_h &&
+                        uint32_t(rc[j].wb + dw) < lim_w;
+        ra[j] = ok ? asrc[rc[j].base + ao] : T(0);
+      }
+#pragma unroll
+      for (int j = 0; j < LB; j++) {
+        const int64_t col = n0 + b_ni[j];
+        if (PASS == FWD) {
+          const int64_t k = k0 + b_ki[j];
+          rb[j] = k < kend && col < a.Ncol ? bsrc[col * a.Kred + k] : T(0);  // f[kout][crs]
+        } else {
+          const int64_t bo = __shfl_sync(0xffffffffu, d.boff, b_ki[j]);
+          rb[j] = bo >= 0 && col < a.Ncol ? bsrc[bo + col * fcol] : T(0);
+        }
+      }
     }
   };
   auto sstore = [&](int buf) {
@@ -404,8 +457,200 @@ static cudaError_t launch_simt_cfg(SimtArgs& a, cudaStream_t st) {
   return e;
 }
 
+// ---- backward-data for thin outputs (C <= 4) -------------------------------
+// AlexNet conv1 / Table-2 layer1 backward-data produce C = 3 channels from a
+// long reduction (K x taps): as a GEMM every gathered dy element feeds only 3
+// FMAs.  Direct convolution instead: a CTA owns a 32 x 32 tile of one stride
+// phase's pixels, stages the dy halo of one dy channel at a time in shared
+// memory (cp.async, double-buffered, zero-filled outside the image) plus that
+// channel's phase taps, and every thread slides a register window along its
+// row: (8 + nSp - 1) loads and nSp * C broadcast filter loads per 8 * nSp * C
+// FMAs.  Lane = tile row, warp = 8-column group, odd row pitch: the window
+// loads are bank-conflict free.
+namespace thin {
+constexpr int TH = 32, TM = 8, WARPS = 4, TW = WARPS * TM, NT = 32 * WARPS;
+
+__device__ __forceinline__ void cp_async_el(void* dst, const void* src, int bytes, bool ok) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  if (bytes == 8)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src),
+                 "r"(ok ? 8 : 0));
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(d), "l"(src),
+                 "r"(ok ? 4 : 0));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;\n" ::); }
+
+struct Args {
+  ConvProblem p;
+  const void* dy;
+  const void* f;
+  void* dx;
+  int accumulate;
+  int nRp, tiles_w;
+};
+
+template <typename T, int CM, int NSP>
+__global__ void __launch_bounds__(NT) dgrad_thin_kernel(const Args a) {
+  extern __shared__ __align__(16) unsigned char thin_smem[];
+  const ConvProblem& p = a.p;
+  const int u = int(p.u), v = int(p.v), nRp = a.nRp;
+  const int RH = TH + nRp - 1;
+  constexpr int RWP = (TW + NSP - 1) | 1;  // odd pitch: lanes (rows) spread over the banks
+  const int halo = RH * RWP;
+  const int ftaps = nRp * NSP * CM;
+  T* ys = reinterpret_cast<T*>(thin_smem);  // [2][RH][RWP]
+  T* fs = ys + 2 * halo;                    // [2][nRp][NSP][CM]
+
+  const int phase = blockIdx.z, ph = phase / v, pw = phase - (phase / v) * v;
+  const int t0h = (ph + int(p.pad_h)) % u, t0w = (pw + int(p.pad_w)) % v;
+  const int bh = (ph + int(p.pad_h)) / u, bw = (pw + int(p.pad_w)) / v;
+  const int nRv = (int(p.R) - t0h + u - 1) / u;  // phase taps that exist
+  const int nSv = (int(p.S) - t0w + v - 1) / v;
+  const int n = blockIdx.y;
+  const int ti = int(blockIdx.x) / a.tiles_w, tj = int(blockIdx.x) - ti * a.tiles_w;
+  const int i0 = ti * TH, j0 = tj * TW;
+  const int pr0 = i0 + bh - (nRp - 1), pc0 = j0 + bw - (NSP - 1);  // dy origin of the halo
+  const T* dy = static_cast<const T*>(a.dy) + int64_t(n) * p.y.sn;
+  const T* f = static_cast<const T*>(a.f);
+  const int tid = threadIdx.x;
+
+  auto stage = [&](int kk, int b) {
+    const T* src = dy + int64_t(kk) * p.y.sc;
+    T* dst = ys + b * halo;
+    for (int e = tid; e < RH * RWP; e += NT) {
+      const int lr = e / RWP, lc = e - lr * RWP;
+      const int pp = pr0 + lr, qq = pc0 + lc;
+      const bool ok = lc < TW + NSP - 1 && unsigned(pp) < unsigned(p.P) && unsigned(qq) < unsigned(p.Q);
+      cp_async_el(dst + e, ok ? src + int64_t(pp) * p.y.sh + int64_t(qq) * p.y.sw : src,
+                  int(sizeof(T)), ok);
+    }
+    T* fd = fs + b * ftaps;
+    for (int e = tid; e < ftaps; e += NT) {
+      const int c = e % CM, t = e / CM, js = t % NSP, jr = t / NSP;
+      const int r = t0h + u * jr, s = t0w + v * js;
+      const bool ok = c < p.C && jr < nRv && js < nSv;
+      const int rr = p.flip ? int(p.R) - 1 - r : r, ss = p.flip ? int(p.S) - 1 - s : s;
+      cp_async_el(fd + e, ok ? f + ((int64_t(kk) * p.C + c) * p.R + rr) * p.S + ss : f,
+                  int(sizeof(T)), ok);
+    }
+    cp_async_commit();
+  };
+
+  const int li = tid & 31, lj0 = (tid >> 5) * TM;
+  T acc[TM][CM];
+#pragma unroll
+  for (int m = 0; m < TM; m++)
+#pragma unroll
+    for (int c = 0; c < CM; c++) acc[m][c] = T(0);
+
+  stage(0, 0);
+  for (int kk = 0; kk < int(p.K); kk++) {
+    const int b = kk & 1;
+    cp_async_wait0();
+    __syncthreads();  // buffer b landed for everyone; buffer b^1 is free
+    if (kk + 1 < int(p.K)) stage(kk + 1, b ^ 1);
+    const T* yb = ys + b * halo;
+    const T* fb = fs + b * ftaps;
+    for (int jr = 0; jr < nRv; jr++) {
+      const T* row = yb + (li + nRp - 1 - jr) * RWP + lj0;
+      T win[TM + NSP - 1];
+#pragma unroll
+      for (int w = 0; w < TM + NSP - 1; w++) win[w] = row[w];
+      const T* fr = fb + jr * NSP * CM;
+#pragma unroll
+      for (int js = 0; js < NSP; js++) {
+        if (js < nSv) {
+          T fv[CM];
+#pragma unroll
+          for (int c = 0; c < CM; c++) fv[c] = fr[js * CM + c];
+#pragma unroll
+          for (int m = 0; m < TM; m++)
+#pragma unroll
+            for (int c = 0; c < CM; c++) acc[m][c] = fma(win[m + NSP - 1 - js], fv[c], acc[m][c]);
+        }
+      }
+    }
+  }
+
+  const int i = i0 + li, h = i * u + ph;
+  if (h >= p.H) return;
+  T* dx = static_cast<T*>(a.dx) + int64_t(n) * p.x.sn + int64_t(h) * p.x.sh;
+#pragma unroll
+  for (int m = 0; m < TM; m++) {
+    const int w = (j0 + lj0 + m) * v + pw;
+    if (w >= p.W) break;
+#pragma unroll
+    for (int c = 0; c < CM; c++) {
+      if (c < p.C) {
+        T* dst = dx + int64_t(c) * p.x.sc + int64_t(w) * p.x.sw;
+        *dst = a.accumulate ? dadd<T>(*dst, acc[m][c]) : acc[m][c];
+      }
+    }
+  }
+}
+
+template <typename T, int CM, int NSP>
+static cudaError_t launch_cm_nsp(const Args& a, dim3 grid, cudaStream_t st) {
+  const int RH = TH + a.nRp - 1;
+  constexpr int RWP = (TW + NSP - 1) | 1;
+  const size_t smem = sizeof(T) * (2 * size_t(RH) * RWP + 2 * size_t(a.nRp) * NSP * CM);
+  auto k = dgrad_thin_kernel<T, CM, NSP>;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+  }
+  k<<<grid, NT, smem, st>>>(a);
+  note_launch();
+  return cudaGetLastError();
+}
+
+template <typename T, int CM>
+static cudaError_t launch_cm(const Args& a, int nsp, dim3 grid, cudaStream_t st) {
+  if (nsp <= 3) return launch_cm_nsp<T, CM, 3>(a, grid, st);
+  if (nsp <= 5) return launch_cm_nsp<T, CM, 5>(a, grid, st);
+  if (nsp <= 7) return launch_cm_nsp<T, CM, 7>(a, grid, st);
+  if (nsp <= 11) return launch_cm_nsp<T, CM, 11>(a, grid, st);
+  return launch_cm_nsp<T, CM, 16>(a, grid, st);
+}
+
+// C <= 4, phase taps per row <= 16 and a halo that fits shared memory
+bool applies(const ConvProblem& p) {
+  if (p.C > 4 || p.K < 1 || ::dnnp::tune_env("DNNP_SIMT_NO_THIN")) return false;
+  const int64_t nRp = ceil_div(p.R, p.u), nSp = ceil_div(p.S, p.v);
+  if (nSp > 16 || nRp > 64) return false;
+  const int64_t Hph = ceil_div(p.H, p.u), Wph = ceil_div(p.W, p.v);
+  return p.N * Hph * Wph >= 4096 && p.N <= 65535 && p.u * p.v <= 65535;
+}
+
+template <typename T>
+cudaError_t launch(const ConvProblem& p, const void* dy, const void* f, void* dx, bool acc,
+                   cudaStream_t st) {
+  Args a{};
+  a.p = p;
+  a.dy = dy;
+  a.f = f;
+  a.dx = dx;
+  a.accumulate = acc;
+  a.nRp = int(ceil_div(p.R, p.u));
+  const int64_t Hph = ceil_div(p.H, p.u), Wph = ceil_div(p.W, p.v);
+  a.tiles_w = int(ceil_div(Wph, TW));
+  const dim3 grid(unsigned(ceil_div(Hph, TH) * a.tiles_w), unsigned(p.N), unsigned(p.u * p.v));
+  const int nsp = int(ceil_div(p.S, p.v));
+  switch (p.C) {
+    case 1: return launch_cm<T, 1>(a, nsp, grid, st);
+    case 2: return launch_cm<T, 2>(a, nsp, grid, st);
+    case 3: return launch_cm<T, 3>(a, nsp, grid, st);
+    default: return launch_cm<T, 4>(a, nsp, grid, st);
+  }
+}
+}  // namespace thin
+
 template <typename T, int PASS>
 static cudaError_t launch_simt(SimtArgs& a, cudaStream_t st) {
+  if (PASS != WGRAD && a.Ncol <= 4 && a.M >= 4096 && !::dnnp::tune_env("DNNP_SIMT_NO_TINY"))
+    return launch_simt_cfg<T, PASS, SimtTiny>(a, st);
   if (PASS != WGRAD && a.Ncol <= 16 && a.M >= 4096 && !::dnnp::tune_env("DNNP_SIMT_NO_NARROW"))
     return launch_simt_cfg<T, PASS, SimtNarrow<T>>(a, st);
   if constexpr (PASS == DGRAD && std::is_same<T, double>::value)
@@ -444,6 +689,7 @@ static cudaError_t simt_bwd_data(const ConvProblem& p, const void* dy, const voi
   a.Ncol = p.C;
   a.Kred = p.K * a.nRp * a.nSp;
   a.accumulate = acc;
+  if (thin::applies(p)) return thin::launch<T>(p, dy, f, dx, acc, st);
   return launch_simt<T, DGRAD>(a, st);
 }
 template <typename T>

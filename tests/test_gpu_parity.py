@@ -217,6 +217,7 @@ RANDOM_SHAPES = [
     (4, 32, 7, 7, 130, 1, 1, 1, 1, 0, 0),     # 1x1, ragged K
     (4, 3, 40, 40, 8, 5, 5, 1, 1, 2, 2),      # thin GEMMs (narrow SIMT tiles: fwd N=8, dgrad N=3)
     (4, 2, 80, 72, 12, 3, 3, 2, 2, 1, 1),     # thin + strided bwd-data phases
+    (2, 12, 48, 48, 3, 3, 3, 1, 1, 1, 1),     # <= 4 output columns (tiny SIMT tile: fwd N=3)
 ]
 
 

@@ -254,15 +254,19 @@ def test_wide_column_blocking(shape):
 
 @pytest.mark.parametrize("shape", [(2, 3, 40, 44, 24, 11, 11, 1, 1, 0, 0),
                                    (2, 5, 33, 31, 16, 5, 5, 2, 2, 2, 2),
-                                   (3, 12, 30, 30, 8, 3, 3, 1, 1, 1, 1)])
+                                   (3, 12, 30, 30, 8, 3, 3, 1, 1, 1, 1),
+                                   (8, 3, 96, 96, 4, 11, 11, 4, 4, 2, 2)])
 def test_simt_narrow_tiles(shape):
-    """Thin GEMMs (<= 16 output columns) on the SIMT fp32 path take the
-    narrow tile (DNNP_SIMT_NO_NARROW: the square tile); fp64 is covered by
-    test_gpu_parity's narrow shapes."""
+    """Thin GEMMs on the SIMT fp32 path: <= 4 output columns take the tiny
+    tile, <= 16 the narrow one (DNNP_SIMT_NO_TINY / DNNP_SIMT_NO_NARROW step
+    back to the wider tiles); fp64 is covered by test_gpu_parity's thin
+    shapes."""
     dp.set_math(dp.MATH_SIMT_FP32)
     try:
         check(run_case(shape, seed=16))
-        with env(DNNP_SIMT_NO_NARROW=1):
+        with env(DNNP_SIMT_NO_TINY=1):
+            check(run_case(shape, passes=("fwd", "bwd_data"), seed=16))
+        with env(DNNP_SIMT_NO_TINY=1, DNNP_SIMT_NO_NARROW=1):
             check(run_case(shape, passes=("fwd", "bwd_data"), seed=16))
     finally:
         dp.set_math(dp.MATH_DEFAULT)
