@@ -59,6 +59,12 @@ struct SimtCfg<double> {
 struct SimtCfgDgrad64 {
   static constexpr int BM = 64, BN = 64, BK = 16, TM = 4, TN = 4;
 };
+// fp64 GEMMs with at least a wave of 128 x 128 tiles: 8 x 8 outputs per
+// thread (one broadcast A load + one B load per 8 DFMAs per operand; the 4 x 4
+// tile above is shared-memory- and issue-bound at ~35% of the DFMA pipe)
+struct SimtCfgBig64 {
+  static constexpr int BM = 128, BN = 128, BK = 8, TM = 8, TN = 8;
+};
 // Narrow GEMM outputs (N <= 16 columns, e.g. table2 layer1 bwd-data: C = 3):
 // a 64-wide tile wastes >= 75% of its FMAs, so rows take the width.
 template <typename T>
@@ -653,8 +659,20 @@ static cudaError_t launch_simt(SimtArgs& a, cudaStream_t st) {
     return launch_simt_cfg<T, PASS, SimtTiny>(a, st);
   if (PASS != WGRAD && a.Ncol <= 16 && a.M >= 4096 && !::dnnp::tune_env("DNNP_SIMT_NO_NARROW"))
     return launch_simt_cfg<T, PASS, SimtNarrow<T>>(a, st);
-  if constexpr (PASS == DGRAD && std::is_same<T, double>::value)
-    return launch_simt_cfg<T, PASS, SimtCfgDgrad64>(a, st);
+  if constexpr (std::is_same<T, double>::value) {
+    // FWD / DGRAD: a full wave of tiles and <= 1/8 of the columns padding
+    // (AlexNet N=128: conv3-5 fwd +12-17%, conv4/5 bwd-data +7-13%; 64 / 192
+    // output columns lose 25-35%); WGRAD: split-K fills the machine, any
+    // M >= 128 (conv2-5 bwd-filter +10-40%; tools/bench_f64.py)
+    const int64_t ncp = ceil_div(a.Ncol, 128) * 128;
+    const int64_t big_tiles = ceil_div(a.M, 128) * (ncp / 128) *
+                              (PASS == DGRAD ? a.p.u * a.p.v : 1);
+    const bool big = PASS == WGRAD ? a.M >= 128
+                                   : big_tiles >= kNumSMs && (ncp - a.Ncol) * 8 <= ncp;
+    if ((big || ::dnnp::tune_env("DNNP_SIMT_BIG")) && !::dnnp::tune_env("DNNP_SIMT_NO_BIG"))
+      return launch_simt_cfg<T, PASS, SimtCfgBig64>(a, st);
+    if constexpr (PASS == DGRAD) return launch_simt_cfg<T, PASS, SimtCfgDgrad64>(a, st);
+  }
   return launch_simt_cfg<T, PASS, SimtCfg<T>>(a, st);
 }
 

@@ -1,4 +1,4 @@
-"""Backward-data for thin outputs (C <= 4 channels, csrc/conv_simt.cu
+"""fp64 / SIMT-fp32 special tiles.  Backward-data for thin outputs (C <= 4 channels, csrc/conv_simt.cu
 thin::dgrad_thin_kernel): the fp64 and SIMT-fp32 paths run AlexNet conv1 /
 Table-2 layer1 backward-data as a direct convolution over a shared-memory dy
 halo.  Checked against the C oracle on strided phases (u, v > 1 with phases
@@ -79,3 +79,47 @@ def test_thin_dgrad_matches_gemm_tiles(si):
     assert run(*SHAPES[si], np.float64, 900 + si) <= 1e-12
     with env(DNNP_SIMT_NO_THIN=1):
         assert run(*SHAPES[si], np.float64, 900 + si) <= 1e-12
+
+
+# ---- fp64 128 x 128 tiles (SimtCfgBig64) --------------------------------------
+
+BIG_SHAPES = [(2, 24, 11, 9, 40, 3, 3, 1, 1, 1, 1),     # ragged rows / columns / reduction
+              (3, 130, 9, 10, 136, 3, 3, 2, 2, 1, 1),   # > 128 columns, strided phases
+              (2, 16, 15, 15, 256, 5, 5, 1, 1, 2, 2)]   # two full column tiles
+
+
+@pytest.mark.parametrize("si", range(len(BIG_SHAPES)))
+def test_f64_big_tiles_forced(si):
+    """DNNP_SIMT_BIG forces the 8 x 8-per-thread fp64 tile on every pass
+    (by default it needs a full wave of tiles, which test-sized problems
+    do not reach); fwd / bwd-data / bwd-filter against the oracle."""
+    import torch
+    from test_gpu_tc_paths import env
+    n, c, h, w, k, r, s, u, v, ph, pw = BIG_SHAPES[si]
+    rng = np.random.default_rng(950 + si)
+    p, q = dp.output_extent(h, r, u, ph), dp.output_extent(w, s, v, pw)
+    xd = dp.make_desc(n, c, h, w, elem_type="f64")
+    yd = dp.make_desc(n, k, p, q, elem_type="f64")
+    fdsc = dp.make_filter_desc(k, c, r, s, elem_type="f64")
+    x = rng.uniform(-0.5, 0.5, xd.max_offset() + 1)
+    dy = rng.uniform(-0.5, 0.5, yd.max_offset() + 1)
+    f = rng.uniform(-0.5, 0.5, k * c * r * s)
+    cd = dp.ConvDesc(u, v, ph, pw)
+    cu = lambda a: torch.from_numpy(a.copy()).cuda()  # noqa: E731
+    xg, yg, fg = [n, c, h, w, *xd.strides], [n, k, p, q, *yd.strides], [k, c, r, s]
+    cg = [u, v, ph, pw, 0, 0]
+    ry, rdx, rdf = np.zeros(yd.max_offset() + 1), np.zeros(xd.max_offset() + 1), np.zeros(f.size)
+    orc.conv_forward(xg, x, fg, f, cg, yg, ry, threads=os.cpu_count() or 1)
+    orc.conv_backward_data(fg, f, yg, dy, cg, xg, rdx)
+    orc.conv_backward_filter(xg, x, yg, dy, cg, fg, rdf, threads=os.cpu_count() or 1)
+    with env(DNNP_SIMT_BIG=1):
+        yv, dxv = dp.empty_view(yd, device="cuda"), dp.empty_view(xd, device="cuda")
+        dfv = dp.FilterView(fdsc, torch.empty(f.size, dtype=torch.float64, device="cuda"))
+        xv, fv, dyv = dp.TensorView(xd, cu(x)), dp.FilterView(fdsc, cu(f)), dp.TensorView(yd, cu(dy))
+        dp.conv_forward(xv, fv, cd, "implicit", yv)
+        dp.conv_backward_data(dyv, fv, cd, "implicit", dxv)
+        dp.conv_backward_filter(dyv, xv, cd, "implicit", dfv)
+        torch.cuda.synchronize()
+    errs = [orc.rel_err(yv.buf.cpu().numpy(), ry), orc.rel_err(dxv.buf.cpu().numpy(), rdx),
+            orc.rel_err(dfv.buf.cpu().numpy(), rdf)]
+    assert max(errs) <= 1e-12, errs
