@@ -363,6 +363,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
 }
 
 #include "conv_tma.cuh"
+#include "conv_halo.cuh"
 
 // ---------------------------------------------------------- filter packing
 
@@ -1211,6 +1212,172 @@ cudaError_t run_gemm(const ConvProblem& p, Gemm g, const void* a_hi, const void*
   return e;
 }
 
+// ------------------------------------------------------------ halo kernel
+template <int BN, int CB>
+cudaError_t launch_halo(const HaloParams& prm, size_t smem, cudaStream_t st) {
+  auto kern = conv_halo_kernel<BN, CB, 2>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  if (e != cudaSuccess) return e;
+  const int clusters = int(std::min<int64_t>(prm.tiles, kNumSMs / 2));
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(unsigned(clusters * 2));
+  cfg.blockDim = dim3(kHaloThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  unsigned nattr = 1;
+  add_pdl_attr(attr, &nattr);
+  cfg.attrs = attr;
+  cfg.numAttrs = nattr;
+  ktime_begin(st, 1);
+  e = cudaLaunchKernelEx(&cfg, kern, prm);
+  ktime_end(st);
+  note_launch();
+  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
+}
+
+// Halo form of an unblocked stride-1 TMA geometry g (space-to-depth forward
+// or backward-data): returns cudaErrorNotSupported when it does not apply
+// (the caller then runs the im2col kernel).  Forward reads the packed input
+// as produced (its grid already covers every tap: IH = OH + tapH - 1);
+// backward-data packs dy with a zero border of (-lo_h, -lo_w).
+cudaError_t run_halo(bool dgrad, const ConvProblem& p, const Gemm& g, const float* in,
+                     const View4& inv, int IH, int IW, int Cp, const float* f, float* out,
+                     const View4& ov, float alpha, float beta, const EpiOp& epi, cudaStream_t st,
+                     int es) {
+  const bool fused = epi.act >= 0 || epi.gate >= 0 || epi.bias != nullptr;
+  const bool force = ::dnnp::tune_env("DNNP_TC_HALO") != nullptr;
+  if (es != 2 || fused || !g.tma || g.u != 1 || g.v != 1 || ::dnnp::tune_env("DNNP_TC_NO_HALO") != nullptr)
+    return cudaErrorNotSupported;
+  PackGeom pg = g.pg;
+  if (pg.Ncol > kHaloMaxCols || pg.bw != 1 || pg.bdir != 0 || Cp % 16 != 0) return cudaErrorNotSupported;
+  const int tapH = pg.tapH, tapW = pg.tapW;
+  const int top = g.pad_h, left = g.pad_w;  // zero border of the packed grid
+  if (top < 0 || left < 0 || (!dgrad && (top || left))) return cudaErrorNotSupported;
+  const int IHp = g.OH + tapH - 1, IWp = g.OW + tapW - 1;
+  if (!dgrad && (IHp > IH || IWp > IW)) return cudaErrorNotSupported;
+  const int IHg = dgrad ? IHp : IH, IWg = dgrad ? IWp : IW;  // packed grid
+  const int RH = kBM + (tapH - 1) * IWg + (tapW - 1);
+  if (RH > 256) return cudaErrorNotSupported;
+  if (!force && double(g.OH) * g.OW < 0.8 * double(IHg) * IWg) return cudaErrorNotSupported;
+  const int64_t Mflat = p.N * int64_t(IHg) * IWg;
+  if (Mflat + 2 * kBM >= (int64_t(1) << 31)) return cudaErrorNotSupported;
+  const int CB = Cp % 64 == 0 ? 64 : Cp % 32 == 0 ? 32 : 16;
+  const int BN = pg.Ncol <= 48 ? 48 : 64;
+  const int nCB = Cp / CB, taps = tapH * tapW, RB = CB * 2;
+  const uint32_t arr = uint32_t(ceil_div(int64_t(RH) * RB, 1024) * 1024);
+  const uint32_t b_bytes = uint32_t(taps * nCB * 2 * (BN / 2) * RB);
+  const uint32_t stage = uint32_t(nCB) * 2u * arr;
+  const size_t budget = 227 * 1024 - 1024 /* alignment */ - 1024 /* barriers, column table */;
+  if (b_bytes + 2 * size_t(stage) > budget) return cudaErrorNotSupported;
+  const int stages = int(std::min<size_t>(4, (budget - b_bytes) / stage));
+  const size_t smem = size_t(b_bytes) + size_t(stages) * stage + 2048;
+
+  // filter planes [BN][Ktot] in the (tap, channel) order of the halo MMAs
+  pg.Cgrp = Cp / 8;
+  pg.KC = taps * pg.Cgrp;
+  const int depth = 64;
+  const int nkb = int(ceil_div(int64_t(pg.KC) * 8, depth));
+  pg.Ktot = std::max(1, nkb) * depth;
+  pg.Np = BN;
+  const size_t flt = size_t(pg.Np) * pg.Ktot;
+  const size_t act = size_t(Mflat) * Cp;
+  Workspace ws(st);
+  cudaError_t e = ws.alloc(flt * 4 + size_t(pg.KC + pg.Np + 2) * 4 + act * 4 + 512);
+  if (e != cudaSuccess) return e;
+  char* base = static_cast<char*>(ws.p);
+  void* b_hi = base;
+  void* b_lo = base + flt * 2;
+  auto* ctab = reinterpret_cast<uint32_t*>(base + flt * 4);
+  auto* coltab = ctab + pg.KC + 1;
+  char* abase = base + ((flt * 4 + size_t(pg.KC + pg.Np + 2) * 4 + 255) & ~size_t(255));
+  void* a_hi = abase;
+  void* a_lo = abase + act * 2;
+  if (!dgrad)
+    e = pack_act_s2d(inv, in, int(p.u), int(p.v), int(p.pad_h), int(p.pad_w), IH, IW, Cp, a_hi, a_lo,
+                     st, es);
+  else
+    e = pack_act_border(inv, in, Cp, top, left, IHg, IWg, a_hi, a_lo, st, es);
+  if (e != cudaSuccess) return e;
+  {
+    const int64_t total8 = int64_t(pg.Np) * (pg.Ktot / 8);
+    const unsigned fgrid = grid_for(std::max<int64_t>(total8, pg.KC), 256, 8);
+    const MagicDiv dK8 = make_magic(uint32_t(pg.Ktot / 8)), dC8 = make_magic(uint32_t(pg.Cgrp));
+    cudaLaunchConfig_t fc{};
+    fc.gridDim = dim3(fgrid);
+    fc.blockDim = dim3(256);
+    fc.stream = st;
+    cudaLaunchAttribute fa[1];
+    unsigned nfa = 0;
+    add_pdl_attr(fa, &nfa);
+    fc.attrs = fa;
+    fc.numAttrs = nfa;
+    e = cudaLaunchKernelEx(&fc, pack_filter_vec_kernel<2>, pg, f, b_hi, b_lo, ctab, coltab, taps, dK8,
+                           dC8);
+    note_launch();
+    if (e != cudaSuccess) return e;
+  }
+  HaloParams prm{};
+  const CUtensorMapSwizzle sw = RB == 128  ? CU_TENSOR_MAP_SWIZZLE_128B
+                                : RB == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                           : CU_TENSOR_MAP_SWIZZLE_32B;
+  if ((e = make_tmap_2d(&prm.tm_ahi, a_hi, uint64_t(Cp), uint64_t(Mflat), uint64_t(Cp), uint32_t(CB),
+                        uint32_t(RH), sw, 2)) != cudaSuccess)
+    return e;
+  if ((e = make_tmap_2d(&prm.tm_alo, a_lo, uint64_t(Cp), uint64_t(Mflat), uint64_t(Cp), uint32_t(CB),
+                        uint32_t(RH), sw, 2)) != cudaSuccess)
+    return e;
+  if ((e = make_tmap_2d(&prm.tm_bhi, b_hi, uint64_t(pg.Ktot), uint64_t(pg.Np), uint64_t(pg.Ktot),
+                        uint32_t(CB), uint32_t(BN / 2), sw, 2)) != cudaSuccess)
+    return e;
+  if ((e = make_tmap_2d(&prm.tm_blo, b_lo, uint64_t(pg.Ktot), uint64_t(pg.Np), uint64_t(pg.Ktot),
+                        uint32_t(CB), uint32_t(BN / 2), sw, 2)) != cudaSuccess)
+    return e;
+  prm.Mflat = Mflat;
+  prm.IWp = IWg;
+  prm.tapH = tapH;
+  prm.tapW = tapW;
+  prm.nCB = nCB;
+  prm.RH = RH;
+  prm.OHv = g.OH;
+  prm.OWv = g.OW;
+  prm.Ncol = pg.Ncol;
+  prm.tiles = int(ceil_div(Mflat, int64_t(2 * kBM)));
+  prm.stages = stages;
+  prm.arr_bytes = arr;
+  prm.b_bytes = b_bytes;
+  prm.dImg = make_magic(uint32_t(IHg * IWg));
+  prm.dW = make_magic(uint32_t(IWg));
+  prm.out = out;
+  prm.o_sn = ov.sn;
+  prm.o_sc = ov.sc;
+  prm.o_sh = ov.sh;
+  prm.o_sw = ov.sw;
+  prm.out_mode = g.out_mode;
+  prm.o_u = g.o_u;
+  prm.o_v = g.o_v;
+  prm.o_H = g.o_H;
+  prm.o_W = g.o_W;
+  prm.o_ph = g.o_ph;
+  prm.o_pw = g.o_pw;
+  prm.coltab = coltab;
+  prm.alpha = alpha;
+  prm.beta = beta;
+  prm.plain = alpha == 1.0f && beta == 0.0f;
+  // experiments (-DDNNP_DIAG builds): 1 = no loads after the first stages, 2 = no stores, 4 = no MMAs
+  prm.dbg = ::dnnp::diag_env("DNNP_HALO_DBG") ? atoi(::dnnp::diag_env("DNNP_HALO_DBG")) : 0;
+  if (BN == 48)
+    return CB == 64 ? launch_halo<48, 64>(prm, smem, st)
+           : CB == 32 ? launch_halo<48, 32>(prm, smem, st) : launch_halo<48, 16>(prm, smem, st);
+  return CB == 64 ? launch_halo<64, 64>(prm, smem, st)
+         : CB == 32 ? launch_halo<64, 32>(prm, smem, st) : launch_halo<64, 16>(prm, smem, st);
+}
+
 // super-pixel window of one spatial dim: offsets base(ph) - jr over all phases
 void phase_window(int u, int pad, int R, int* lo, int* win) {
   int mn = 1 << 30, mx = -(1 << 30);
@@ -1379,6 +1546,12 @@ cudaError_t run_tc(bool dgrad, const ConvProblem& p, const float* in, const View
   pg.bw = 1;
   pg.Ncol0 = pg.Ncol;
   pg.vstep = dgrad ? 1 : g.v;
+  if (s2d) {
+    // AlexNet conv1: halo tiles instead of one im2col box per tap
+    const cudaError_t he = run_halo(dgrad, p, g, in, inv, IH, IW, Cp, f, out, outv, alpha, beta, epi,
+                                    st, es);
+    if (he != cudaErrorNotSupported) return he;
+  }
   // Column blocking for small GEMM N (conv2 bwd-data C=64): one GEMM row computes bw = 2
   // adjacent output columns, doubling N; the A operand (im2col, the bulk of
   // the TMA traffic) shrinks to (S + v) / (2 S) of its bytes.

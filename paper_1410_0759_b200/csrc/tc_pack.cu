@@ -99,12 +99,18 @@ __global__ void __launch_bounds__(256) pack_act_kernel(View4 v, const float* __r
 // Same transpose with 64-pixel jobs: each thread loads 16 values (two
 // 32-pixel halves x 8 channel phases) before the barrier, twice the bytes in
 // flight per synchronisation of the 32-pixel version.
+// Border: the packed grid is (Hp, Wp) with the tensor at (top, left) and
+// zeros around it (Hp = 0: the tensor's own grid); the halo kernel's input.
+struct Border {
+  int top, left, Hp, Wp;
+};
+
 template <int PIXJ, int ES>
 __global__ void __launch_bounds__(256) pack_act_wide_kernel(View4 v, const float* __restrict__ x,
                                                             int Cp, void* __restrict__ hi,
                                                             void* __restrict__ lo,
                                                             uint32_t npix, MagicDiv dHW,
-                                                            MagicDiv dW) {
+                                                            MagicDiv dW, Border bd = Border{0, 0, 0, 0}) {
   __shared__ float tile[kCh][PIXJ + 1];
   constexpr int HALVES = PIXJ / 32;
   const int lp = threadIdx.x & 31, lc = threadIdx.x >> 5;  // read role: pixel, channel phase
@@ -126,7 +132,9 @@ __global__ void __launch_bounds__(256) pack_act_wide_kernel(View4 v, const float
         uint32_t n, rem, h, w;
         mdivmod(pix, dHW, n, rem);
         mdivmod(rem, dW, h, w);
-        src = x + int64_t(n) * v.sn + int64_t(h) * v.sh + int64_t(w) * v.sw + int64_t(c_lo) * v.sc;
+        const int hh = int(h) - bd.top, ww = int(w) - bd.left;
+        if (!bd.Hp || (unsigned(hh) < unsigned(v.h) && unsigned(ww) < unsigned(v.w)))
+          src = x + int64_t(n) * v.sn + int64_t(hh) * v.sh + int64_t(ww) * v.sw + int64_t(c_lo) * v.sc;
       }
 #pragma unroll
       for (int i = 0; i < kCh / 8; i++) {
@@ -1052,6 +1060,27 @@ static cudaError_t pack_act_t(const View4& v, const float* x, int Cp, void* hi, 
                                                make_magic(uint32_t(v.w)), S2dGeom{1, 1, 0, 0});
   note_launch();
   return cudaGetLastError();
+}
+
+template <int ES>
+static cudaError_t pack_act_border_t(const View4& v, const float* x, int Cp, int top, int left,
+                                     int Hp, int Wp, void* hi, void* lo, cudaStream_t st) {
+  const int64_t npix = v.n * Hp * Wp;
+  const int64_t jobs = ceil_div(npix, int64_t(64)) * ceil_div(Cp, kCh);
+  if (npix >= (int64_t(1) << 32) || jobs >= (int64_t(1) << 31)) return cudaErrorInvalidValue;
+  const unsigned grid = unsigned(std::min<int64_t>(jobs, int64_t(kNumSMs) * 16));
+  pack_act_wide_kernel<64, ES><<<grid, 256, 0, st>>>(v, x, Cp, hi, lo, uint32_t(npix),
+                                                     make_magic(uint32_t(Hp * Wp)),
+                                                     make_magic(uint32_t(Wp)),
+                                                     Border{top, left, Hp, Wp});
+  note_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t pack_act_border(const View4& v, const float* x, int Cp, int top, int left, int Hp,
+                            int Wp, void* hi, void* lo, cudaStream_t st, int es) {
+  return es == 4 ? pack_act_border_t<4>(v, x, Cp, top, left, Hp, Wp, hi, lo, st)
+                 : pack_act_border_t<2>(v, x, Cp, top, left, Hp, Wp, hi, lo, st);
 }
 
 cudaError_t pack_act(const View4& v, const float* x, int Cp, void* hi, void* lo,
