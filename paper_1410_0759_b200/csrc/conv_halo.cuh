@@ -37,8 +37,9 @@ constexpr int kHaloMaxCols = 64;
 struct HaloParams {
   CUtensorMap tm_ahi;   // packed input planes as [rows][Cp], box {CB, RH}
   CUtensorMap tm_alo;
-  CUtensorMap tm_bhi;   // packed filter [Np][Ktot], box {CB, BN / NC}
+  CUtensorMap tm_bhi;   // packed filter planes [Np][Ktot], box {CB, BN}
   CUtensorMap tm_blo;
+  CUtensorMap tm_bq;    // hi plane, box {CB, BN / 2}
   int64_t Mflat;        // N * IHp * IWp
   int IWp, tapH, tapW, nCB, RH;
   int OHv, OWv;         // valid output extent of one image's flat grid
@@ -60,12 +61,21 @@ struct HaloParams {
 
 template <int BN, int CB, int NC>
 __global__ void __launch_bounds__(kHaloThreads, 1) conv_halo_kernel(const __grid_constant__ HaloParams P) {
-  constexpr int BNL = BN / NC;   // filter rows held by each CTA
   constexpr int RB = CB * 2;     // bytes of one operand row (= swizzle span)
   constexpr int KPS = RB / 32;   // 16-deep k-steps per row
-  constexpr uint32_t B_SUB = BNL * RB;
+  // Resident filter, per (tap, channel block) kc: a P sub-tile of BN rows
+  // (leader: W_hi, peer: W_lo) and a Q sub-tile of BN/2 rows (W_hi rows
+  // [rank * BN/2, +BN/2)).  Per 16-deep k-step the BF16x3 split is two MMAs:
+  //   A_hi x [W_hi | W_lo]  (N = 2 BN: hi.hi -> cols [0, BN), hi.lo -> [BN, 2 BN))
+  //   A_lo x W_hi           (N = BN, accumulated onto cols [0, BN))
+  // and the epilogue adds the two column halves -- 11 KB of operand reads
+  // per SM and k-step instead of 15 KB for three MMAs (with N <= 64 the
+  // MMAs are bound by shared-memory operand reads, not by the tensor pipe).
+  static_assert(NC == 2, "the split across the pair needs both CTAs");
+  constexpr uint32_t P_SUB = BN * RB, Q_SUB = (BN / 2) * RB, KC_BYTES = P_SUB + Q_SUB;
   constexpr int NI = kHaloIssuers;
-  constexpr int TMEM_COLS = NI * BN <= 64 ? 64 : (NI * BN <= 128 ? 128 : 256);
+  constexpr int ACC = 2 * BN;  // accumulator columns per buffer
+  constexpr int TMEM_COLS = NI * ACC <= 128 ? 128 : (NI * ACC <= 256 ? 256 : 512);
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -120,6 +130,7 @@ __global__ void __launch_bounds__(kHaloThreads, 1) conv_halo_kernel(const __grid
       ptx::tma_prefetch(&P.tm_alo);
       ptx::tma_prefetch(&P.tm_bhi);
       ptx::tma_prefetch(&P.tm_blo);
+      ptx::tma_prefetch(&P.tm_bq);
       // resident filter: every (tap, channel block) sub-tile of this CTA's rows
       if (leader) ptx::mbar_arrive_expect_tx(bfull, P.b_bytes * NC);
       else ptx::mbar_arrive_cluster(bfull, 0);
@@ -127,14 +138,9 @@ __global__ void __launch_bounds__(kHaloThreads, 1) conv_halo_kernel(const __grid
         const uint32_t bar = NC == 2 ? ptx::leader_addr(bfull) : ptx::smem_u32(bfull);
         const int kcs = taps * P.nCB;
         for (int kc = 0; kc < kcs; kc++) {
-          const uint32_t d = sb0 + uint32_t(kc) * 2u * B_SUB;
-          if constexpr (NC == 2) {
-            ptx::tma_load_2d_pair(d, &P.tm_bhi, kc * CB, int(rank) * BNL, bar);
-            ptx::tma_load_2d_pair(d + B_SUB, &P.tm_blo, kc * CB, int(rank) * BNL, bar);
-          } else {
-            ptx::tma_load_2d(d, &P.tm_bhi, kc * CB, 0, bfull);
-            ptx::tma_load_2d(d + B_SUB, &P.tm_blo, kc * CB, 0, bfull);
-          }
+          const uint32_t d = sb0 + uint32_t(kc) * KC_BYTES;
+          ptx::tma_load_2d_pair(d, leader ? &P.tm_bhi : &P.tm_blo, kc * CB, 0, bar);
+          ptx::tma_load_2d_pair(d + P_SUB, &P.tm_bq, kc * CB, int(rank) * (BN / 2), bar);
         }
       }
       const uint32_t tx = uint32_t(P.nCB) * 2u * uint32_t(P.RH) * RB;
@@ -167,12 +173,13 @@ __global__ void __launch_bounds__(kHaloThreads, 1) conv_halo_kernel(const __grid
     // (the 14-bit address field cannot carry: shared memory < 256 KB).
     const int mi = warp - 1;
     if (leader) {
-      constexpr uint32_t idesc = ptx::idesc_bf16(kBM * NC, BN, 0, 0);
+      constexpr uint32_t idesc2 = ptx::idesc_bf16(kBM * NC, 2 * BN, 0, 0);
+      constexpr uint32_t idesc1 = ptx::idesc_bf16(kBM * NC, BN, 0, 0);
       ptx::mbar_wait(bfull, 0);
       ptx::tc_fence_after();
       const uint64_t dB0 = tma_kdesc<RB>(sb0), dA0 = tma_kdesc<RB>(sa0);
       const uint32_t arr16 = P.arr_bytes >> 4;
-      const uint32_t dacc = tmem_base + uint32_t(mi * BN);
+      const uint32_t dacc = tmem_base + uint32_t(mi * ACC);
       int it = mi, use = 0;
       for (int tile = cid + mi * ncl; tile < P.tiles; tile += NI * ncl, it += NI, use++) {
         ptx::mbar_wait(&tempty[mi], (use & 1) ^ 1);
@@ -189,16 +196,14 @@ __global__ void __launch_bounds__(kHaloThreads, 1) conv_halo_kernel(const __grid
             const uint64_t dAt = dAs + ((uint32_t(th * P.IWp + tw) * RB) >> 4);
             for (int cb = 0; cb < P.nCB; cb++, kc++) {
               const uint64_t ah = dAt + uint32_t(cb) * 2u * arr16;
-              const uint64_t bh = dB0 + ((uint32_t(kc) * 2u * B_SUB) >> 4);
+              const uint64_t bp = dB0 + ((uint32_t(kc) * KC_BYTES) >> 4);
 #pragma unroll
               for (int kk = 0; kk < KPS; kk++) {
                 const uint64_t dah = ah + 2u * kk, dal = dah + arr16;
-                const uint64_t dbh = bh + 2u * kk, dbl = dbh + (B_SUB >> 4);
-                // lo.hi + hi.lo + hi.hi into one fp32 accumulator (lo.lo dropped)
+                const uint64_t dbp = bp + 2u * kk, dbq = dbp + (P_SUB >> 4);
                 if (!(P.dbg & 4)) {
-                ptx::mma_split_elect<NC, 2>(dacc, dal, dbh, idesc, acc);
-                ptx::mma_split_elect<NC, 2>(dacc, dah, dbl, idesc, 1);
-                ptx::mma_split_elect<NC, 2>(dacc, dah, dbh, idesc, 1);
+                  ptx::mma_split_elect<NC, 2>(dacc, dah, dbp, idesc2, acc);  // hi.hi | hi.lo
+                  ptx::mma_split_elect<NC, 2>(dacc, dal, dbq, idesc1, 1);    // + lo.hi
                 }
                 acc = 1;
               }
@@ -246,8 +251,13 @@ __global__ void __launch_bounds__(kHaloThreads, 1) conv_halo_kernel(const __grid
       ptx::tc_fence_after();
       uint32_t v[32];
       if (c0 < BN) {
-        ptx::tmem_ld32(tmem_base + (uint32_t(ew * 32) << 16) + uint32_t(buf * BN + c0), v);
+        uint32_t w[32];
+        const uint32_t ta = tmem_base + (uint32_t(ew * 32) << 16) + uint32_t(buf * ACC + c0);
+        ptx::tmem_ld32(ta, v);
+        ptx::tmem_ld32(ta + BN, w);
         ptx::tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < 32; i++) v[i] = __float_as_uint(__fadd_rn(__uint_as_float(v[i]), __uint_as_float(w[i])));
       }
       // the accumulator is in registers: hand the buffer back to the MMA
       ptx::tc_fence_before();

@@ -1271,7 +1271,7 @@ cudaError_t run_halo(bool dgrad, const ConvProblem& p, const Gemm& g, const floa
   const int BN = pg.Ncol <= 48 ? 48 : 64;
   const int nCB = Cp / CB, taps = tapH * tapW, RB = CB * 2;
   const uint32_t arr = uint32_t(ceil_div(int64_t(RH) * RB, 1024) * 1024);
-  const uint32_t b_bytes = uint32_t(taps * nCB * 2 * (BN / 2) * RB);
+  const uint32_t b_bytes = uint32_t(taps * nCB * (BN + BN / 2) * RB);  // P + Q sub-tiles
   const uint32_t stage = uint32_t(nCB) * 2u * arr;
   const size_t budget = 227 * 1024 - 1024 /* alignment */ - 1024 /* barriers, column table */;
   if (b_bytes + 2 * size_t(stage) > budget) return cudaErrorNotSupported;
@@ -1333,9 +1333,12 @@ cudaError_t run_halo(bool dgrad, const ConvProblem& p, const Gemm& g, const floa
                         uint32_t(RH), sw, 2)) != cudaSuccess)
     return e;
   if ((e = make_tmap_2d(&prm.tm_bhi, b_hi, uint64_t(pg.Ktot), uint64_t(pg.Np), uint64_t(pg.Ktot),
-                        uint32_t(CB), uint32_t(BN / 2), sw, 2)) != cudaSuccess)
+                        uint32_t(CB), uint32_t(BN), sw, 2)) != cudaSuccess)
     return e;
   if ((e = make_tmap_2d(&prm.tm_blo, b_lo, uint64_t(pg.Ktot), uint64_t(pg.Np), uint64_t(pg.Ktot),
+                        uint32_t(CB), uint32_t(BN), sw, 2)) != cudaSuccess)
+    return e;
+  if ((e = make_tmap_2d(&prm.tm_bq, b_hi, uint64_t(pg.Ktot), uint64_t(pg.Np), uint64_t(pg.Ktot),
                         uint32_t(CB), uint32_t(BN / 2), sw, 2)) != cudaSuccess)
     return e;
   prm.Mflat = Mflat;
