@@ -14,6 +14,7 @@
 #include <type_traits>
 #include <cstdio>
 #include <cstdlib>
+#include <vector>
 
 #include "tc_common.cuh"
 #include "tc_ptx.cuh"
@@ -583,6 +584,8 @@ __global__ void __launch_bounds__(256) wgrad_reduce_tma(WgReduceGeom g, const fl
   }
 }
 
+#include "wgrad_halo.cuh"
+
 template <int BN, int NC, int PX, int BW = 64, int ES = 2>
 cudaError_t launch_wgrad_tma(const WgTmaParams& prm, dim3 grid, cudaStream_t st) {
   using CC = WgCfg<BN, NC, PX, BW, ES>;
@@ -619,11 +622,138 @@ cudaError_t launch_wgrad_tma(const WgTmaParams& prm, dim3 grid, cudaStream_t st)
 
 }  // namespace
 
+// Halo form of the space-to-depth backward-filter (wgrad_halo.cuh):
+// cudaErrorNotSupported when it does not apply.
+cudaError_t wgrad_halo(const ConvProblem& p, const float* dy, const float* x, float* df, bool acc,
+                       cudaStream_t st, int es) {
+  if (es != 2 || ::dnnp::tune_env("DNNP_TC_NO_HALO")) return cudaErrorNotSupported;
+  if (!(p.u > 1 || p.v > 1) || p.u > 8 || p.v > 8 || p.C * p.u * p.v > 64 || p.K > 64)
+    return cudaErrorNotSupported;
+  const int su = int(p.u), sv = int(p.v);
+  const int R2 = int(ceil_div(p.R, su)), S2 = int(ceil_div(p.S, sv));
+  const int IH = int(p.P) - 1 + R2, IW = int(p.Q) - 1 + S2;
+  // leader taps: rows 0, 2, ..; the peer computes each one row down
+  std::vector<int> lt;
+  for (int th = 0; th < R2; th += 2)
+    for (int tw = 0; tw < S2; tw++) lt.push_back(th * S2 + tw);
+  const int ng = int(ceil_div(int64_t(lt.size()), 2));
+  if (ng > kWhMaxG) return cudaErrorNotSupported;
+  WgHaloParams prm{};
+  int shmax = 0;
+  for (int g = 0; g < ng; g++) {
+    for (int b = 0; b < 2; b++) {
+      const size_t i = std::min(lt.size() - 1, size_t(2 * g + b));
+      const int t = lt[i], th = t / S2, tw = t % S2;
+      prm.sh[g][b] = th * IW + tw;
+      shmax = std::max(shmax, prm.sh[g][b]);
+      const bool dup = size_t(2 * g + b) >= lt.size();
+      prm.tap[0][g][b] = dup ? -1 : t;
+      prm.tap[1][g][b] = (dup || th + 1 >= R2) ? -1 : (th + 1) * S2 + tw;
+    }
+  }
+  const int RH = kWhChunk + shmax;
+  if (RH > 256 || IW > 64) return cudaErrorNotSupported;
+  const int64_t npix = p.N * int64_t(IH) * IW;
+  const int64_t chunks = ceil_div(npix, int64_t(kWhChunk));
+  const int64_t Pp = chunks * kWhChunk;
+  const int ncl = int(std::min<int64_t>(chunks, kNumSMs / 2));
+  // accumulation chain per cluster <= max_chain pixels (fp32 TMEM truncation)
+  if (ceil_div(chunks, int64_t(ncl)) * kWhChunk > max_chain(kWhChunk) || Pp >= (int64_t(1) << 31))
+    return cudaErrorNotSupported;
+  const int Cpf = 64, taps = R2 * S2, ncolx = taps * Cpf;
+  const size_t x_elems = size_t(npix) * 64, dy_elems = size_t(64) * Pp;
+  const size_t ws_floats = size_t(ncl) * ncolx * 64;
+  Workspace wsp(st);
+  cudaError_t e = wsp.alloc((x_elems + dy_elems) * 4 + ws_floats * 4 + 1024);
+  if (e != cudaSuccess) return e;
+  char* base = static_cast<char*>(wsp.p);
+  void* x_hi = base;
+  void* x_lo = base + x_elems * 2;
+  auto* d_hi = reinterpret_cast<__nv_bfloat16*>(base + x_elems * 4);
+  auto* d_lo = d_hi + dy_elems;
+  float* part = reinterpret_cast<float*>(base + ((x_elems * 4 + dy_elems * 4 + 255) & ~size_t(255)));
+  if ((e = pack_act_s2d(p.x, x, su, sv, int(p.pad_h), int(p.pad_w), IH, IW, 64, x_hi, x_lo, st, es)) !=
+      cudaSuccess)
+    return e;
+  {
+    const int64_t rows = ceil_div(Pp, int64_t(IW));
+    pack_dy_grid_kernel<<<unsigned(rows), 256, 0, st>>>(p.y, dy, IH, IW, int(p.K), npix, Pp, d_hi, d_lo);
+    note_launch();
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
+  if ((e = make_tmap_2d(&prm.tm_xhi, x_hi, 64, uint64_t(npix), 64, 64, uint32_t(RH),
+                        CU_TENSOR_MAP_SWIZZLE_128B, 2)) != cudaSuccess)
+    return e;
+  if ((e = make_tmap_2d(&prm.tm_xlo, x_lo, 64, uint64_t(npix), 64, 64, uint32_t(RH),
+                        CU_TENSOR_MAP_SWIZZLE_128B, 2)) != cudaSuccess)
+    return e;
+  if ((e = make_tmap_2d(&prm.tm_dhi, d_hi, uint64_t(Pp), uint64_t(p.K), uint64_t(Pp), 64, 64,
+                        CU_TENSOR_MAP_SWIZZLE_128B, 2)) != cudaSuccess)
+    return e;
+  if ((e = make_tmap_2d(&prm.tm_dlo, d_lo, uint64_t(Pp), uint64_t(p.K), uint64_t(Pp), 64, 64,
+                        CU_TENSOR_MAP_SWIZZLE_128B, 2)) != cudaSuccess)
+    return e;
+  if ((e = make_tmap_2d(&prm.tm_dq, d_hi, uint64_t(Pp), uint64_t(p.K), uint64_t(Pp), 64, 32,
+                        CU_TENSOR_MAP_SWIZZLE_128B, 2)) != cudaSuccess)
+    return e;
+  prm.chunks = int(chunks);
+  prm.RH = RH;
+  prm.off1 = IW;
+  prm.ng = ng;
+  prm.Cpf = Cpf;
+  prm.ncolx = ncolx;
+  prm.arr_bytes = uint32_t(ceil_div(int64_t(RH) * 128, 1024) * 1024);
+  prm.ws = part;
+  const size_t smem = size_t(2) * (2 * prm.arr_bytes + 2 * 64 * 128 + 2 * 32 * 128) + 2048;
+  e = cudaFuncSetAttribute(wgrad_halo_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(unsigned(ncl * 2));
+  cfg.blockDim = dim3(kWhThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  unsigned nattr = 1;
+  add_pdl_attr(attr, &nattr);
+  cfg.attrs = attr;
+  cfg.numAttrs = nattr;
+  ktime_begin(st, 2);
+  e = cudaLaunchKernelEx(&cfg, wgrad_halo_kernel, prm);
+  ktime_end(st);
+  note_launch();
+  if (e != cudaSuccess) return e;
+  WgReduceGeom rg{};
+  rg.K = int(p.K);
+  rg.C = int(p.C);
+  rg.R = int(p.R);
+  rg.S = int(p.S);
+  rg.flip = p.flip ? 1 : 0;
+  rg.su = su;
+  rg.sv = sv;
+  rg.S2 = S2;
+  rg.Cpf = Cpf;
+  rg.ncolx = ncolx;
+  rg.splits = ncl;
+  rg.mrows_p = ncolx;
+  rg.ncol_p = 64;
+  wgrad_reduce_tma<<<grid_for(int64_t(ncolx) * p.K, 256, 16), 256, 0, st>>>(rg, part, df, acc ? 1 : 0);
+  note_launch();
+  return cudaGetLastError();
+}
+
 // TMA path of backward-filter; returns cudaErrorNotSupported when the
 // geometry does not fit the im2col tensor map (caller falls back).
 cudaError_t wgrad_tma(const ConvProblem& p, const float* dy, const float* x, float* df, bool acc,
                       cudaStream_t st, int es) {
   if (::dnnp::tune_env("DNNP_TC_NO_TMA")) return cudaErrorNotSupported;
+  {
+    const cudaError_t he = wgrad_halo(p, dy, x, df, acc, st, es);
+    if (he != cudaErrorNotSupported) return he;
+  }
   const bool s2d = !::dnnp::tune_env("DNNP_TC_NO_S2D") && (p.u > 1 || p.v > 1) && p.u <= 8 && p.v <= 8 &&
                    p.C * p.u * p.v <= 64;
   // horizontal tap folding (stride-1-style few-channel layers): the S taps

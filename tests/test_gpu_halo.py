@@ -1,12 +1,15 @@
-"""Halo-tile tensor-core kernel (csrc/conv_halo.cuh): the space-to-depth
-forward and backward-data of strided few-channel convolutions (AlexNet
-conv1) read one halo of packed pixel rows per tile and address every filter
-tap by the UMMA descriptor start row.  Checked against the C oracle: AlexNet
+"""Halo-tile tensor-core kernels (csrc/conv_halo.cuh, csrc/wgrad_halo.cuh):
+the space-to-depth forward, backward-data and backward-filter of strided
+few-channel convolutions (AlexNet conv1) read one halo of packed pixel rows
+per tile and address every filter tap by the UMMA descriptor start row (and,
+for backward-filter, a second tap by the descriptor's leading byte offset).  Checked against the C oracle: AlexNet
 conv1 itself (default selection), and -- with DNNP_TC_HALO forcing the kernel
 past its 80% useful-grid threshold -- the channel-block widths 16 / 32 / 64,
 48- and 64-column tiles, ragged last tiles, both modes, NHWC and strided
 views, alpha / beta and accumulate; DNNP_TC_NO_HALO gives the im2col kernel
 on the same inputs."""
+import os
+
 import numpy as np
 import pytest
 
@@ -19,7 +22,7 @@ pytestmark = pytest.mark.gpu
 TOL = 1e-4
 
 
-def run(n, c, h, w, k, r, s, u, v, ph, pw, seed, passes=("fwd", "bwd_data"), layout="nchw",
+def run(n, c, h, w, k, r, s, u, v, ph, pw, seed, passes=("fwd", "bwd_data", "bwd_filter"), layout="nchw",
         mode="convolution", acc=False, alpha=1.0, beta=0.0):
     import torch
     rng = np.random.default_rng(seed)
@@ -49,7 +52,13 @@ def run(n, c, h, w, k, r, s, u, v, ph, pw, seed, passes=("fwd", "bwd_data"), lay
         ref = dx0.copy()
         orc.conv_backward_data(fg, f, yg, dy, cg, xg, ref)
         errs["bwd_data"] = orc.rel_err(dxv.buf.cpu().numpy(), ref)
-    import torch
+    if "bwd_filter" in passes:
+        df0 = rng.uniform(-0.5, 0.5, k * c * r * s).astype(np.float32)
+        dfv = dp.FilterView(dp.make_filter_desc(k, c, r, s), cu(df0))
+        dp.conv_backward_filter(dp.TensorView(yd, cu(dy)), dp.TensorView(xd, cu(x)), cd, "implicit", dfv)
+        ref = df0.copy()
+        orc.conv_backward_filter(xg, x, yg, dy, cg, fg, ref, threads=os.cpu_count() or 1)
+        errs["bwd_filter"] = orc.rel_err(dfv.buf.cpu().numpy(), ref)
     torch.cuda.synchronize()
     return errs
 
@@ -86,4 +95,4 @@ def test_halo_nhwc_and_blend(si):
     with env(DNNP_TC_HALO=1):
         check(run(*SHAPES[si], 20 + si, layout="nhwc"))
         check(run(*SHAPES[si], 30 + si, alpha=0.75, beta=0.5, passes=("fwd",)))
-        check(run(*SHAPES[si], 40 + si, acc=True, passes=("bwd_data",)))
+        check(run(*SHAPES[si], 40 + si, acc=True, passes=("bwd_data", "bwd_filter")))
