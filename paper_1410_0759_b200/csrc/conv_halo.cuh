@@ -56,6 +56,7 @@ struct HaloParams {
   const uint32_t* coltab;
   float alpha, beta;
   int plain;
+  int fast;  // 3: super-pixel dx rows of a stride-4, pad-2, 3-channel backward-data (see epilogue)
   int dbg;  // experiments only (DNNP_HALO_DBG, -DDNNP_DIAG builds)
 };
 
@@ -222,7 +223,10 @@ __global__ void __launch_bounds__(kHaloThreads, 1) conv_halo_kernel(const __grid
   } else {
     // ================================================ epilogue
     const int ew = warp & 3;                         // TMEM lane quadrant of this warp
-    const int c0 = 32 * ((warp - kHaloEpi0) >> 2);   // this warp's 32 columns
+    const int es = (warp - kHaloEpi0) >> 2;
+    // this warp's columns: 32 per warp set; fast path: one half of the
+    // (ph, pw, c) super-pixel columns each (ph 0-1 / 2-3, 24 columns)
+    const int c0 = P.fast ? 24 * es : 32 * es;
     const int r = ew * 32 + lane;                    // tile row
     const int et = threadIdx.x - kHaloEpi0 * 32;     // 0..255
     if (P.out_mode == 1) {
@@ -265,6 +269,46 @@ __global__ void __launch_bounds__(kHaloThreads, 1) conv_halo_kernel(const __grid
       if (lane == 0) {
         if (NC == 1) ptx::mbar_arrive(&tempty[buf]);
         else ptx::mbar_arrive_cluster(&tempty[buf], 0);
+      }
+      if (P.fast == 3 && !(P.dbg & 2)) {
+        // dx rows of super-pixels (u = v = 4, pad 2, C = 3, plain store):
+        // super-pixel j covers w = 4j - 2 .. 4j + 1, so the aligned float4 at
+        // w = 4j is (pw 2, 3 of j | pw 0, 1 of j + 1): one shuffle pair per
+        // row segment and contiguous 512-byte warp stores instead of 12
+        // scattered 4-byte stores per lane.
+        const int hb = int(oh) * 4 - P.o_ph, wj = int(ow) * 4;
+        const uint32_t key = ok ? img * 65536u + oh : 0xFFFFFFFFu;
+        const uint32_t nkey = __shfl_down_sync(0xFFFFFFFFu, key, 1);
+        const int nw = __shfl_down_sync(0xFFFFFFFFu, int(ow), 1);
+        const bool cnext = lane < 31 && ok && nkey == key && nw == int(ow) + 1 && wj + 3 < P.o_W;
+        const bool cprev = __shfl_up_sync(0xFFFFFFFFu, cnext, 1) && lane > 0;
+#pragma unroll
+        for (int php = 0; php < 2; php++) {
+          const int h = hb + 2 * es + php;
+          const bool hok = ok && unsigned(h) < unsigned(P.o_H);
+#pragma unroll
+          for (int c = 0; c < 3; c++) {
+            const float x0 = __uint_as_float(v[(php * 4 + 0) * 3 + c]);
+            const float x1 = __uint_as_float(v[(php * 4 + 1) * 3 + c]);
+            const float x2 = __uint_as_float(v[(php * 4 + 2) * 3 + c]);
+            const float x3 = __uint_as_float(v[(php * 4 + 3) * 3 + c]);
+            const float n0 = __shfl_down_sync(0xFFFFFFFFu, x0, 1);
+            const float n1 = __shfl_down_sync(0xFFFFFFFFu, x1, 1);
+            if (!hok) continue;
+            float* d = P.out + int64_t(img) * P.o_sn + int64_t(c) * P.o_sc + int64_t(h) * P.o_sh + wj;
+            if (cnext) {
+              *reinterpret_cast<float4*>(d) = make_float4(x2, x3, n0, n1);
+            } else {
+              if (wj < P.o_W) d[0] = x2;
+              if (wj + 1 < P.o_W) d[1] = x3;
+            }
+            if (!cprev) {
+              if (wj >= 2 && wj - 2 < P.o_W) d[-2] = x0;
+              if (wj >= 1 && wj - 1 < P.o_W) d[-1] = x1;
+            }
+          }
+        }
+        continue;
       }
       if (!ok || (P.dbg & 2)) continue;
       if (P.out_mode == 0) {

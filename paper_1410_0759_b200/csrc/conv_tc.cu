@@ -1372,6 +1372,15 @@ cudaError_t run_halo(bool dgrad, const ConvProblem& p, const Gemm& g, const floa
   prm.alpha = alpha;
   prm.beta = beta;
   prm.plain = alpha == 1.0f && beta == 0.0f;
+  {
+    // coalesced super-pixel stores (conv1 backward-data geometry)
+    const uintptr_t a = reinterpret_cast<uintptr_t>(out);
+    prm.fast = (dgrad && g.out_mode == 1 && prm.plain && BN == 48 && pg.Ncol == 48 && p.C == 3 &&
+                g.o_u == 4 && g.o_v == 4 && g.o_pw == 2 && ov.sw == 1 && a % 16 == 0 && ov.sn % 4 == 0 &&
+                ov.sc % 4 == 0 && ov.sh % 4 == 0 && p.N < 65536 && !::dnnp::tune_env("DNNP_HALO_NO_FAST"))
+                   ? 3
+                   : 0;
+  }
   // experiments (-DDNNP_DIAG builds): 1 = no loads after the first stages, 2 = no stores, 4 = no MMAs
   prm.dbg = ::dnnp::diag_env("DNNP_HALO_DBG") ? atoi(::dnnp::diag_env("DNNP_HALO_DBG")) : 0;
   if (BN == 48)
