@@ -203,25 +203,33 @@ __global__ void __launch_bounds__(kWhThreads, 1) wgrad_halo_kernel(const __grid_
 
 // dy [N][K][P][Q] (any strides) -> planes [K][Pp] over the packed input's
 // flat pixel grid p = n*IH*IW + oh*IW + ow (zero where oh >= P, ow >= Q or
-// p >= N*IH*IW), BF16 hi / lo.  Block = one grid row (n, oh) of IW <= 64
-// pixels x all K: lanes walk ow (coalesced reads of a dy row, coalesced
-// writes of a plane row).
+// p >= N*IH*IW), BF16 hi / lo.  A block covers 512 consecutive grid pixels x
+// 8 k (two pixels per thread: 4-byte stores of both planes, coalesced loads
+// along ow).
 __global__ void __launch_bounds__(256) pack_dy_grid_kernel(View4 v, const float* __restrict__ dy,
                                                            int IH, int IW, int K, int64_t npix,
                                                            int64_t Pp, __nv_bfloat16* __restrict__ hi,
                                                            __nv_bfloat16* __restrict__ lo) {
-  const int64_t row = blockIdx.x;  // grid row n * IH + oh (rows past N * IH: zero tail)
-  const int n = int(row / IH), oh = int(row - int64_t(n) * IH);
-  const int ow = threadIdx.x & 63;
-  const int64_t p = row * IW + ow;
-  if (ow >= IW || p >= Pp) return;
-  const bool in = p < npix && oh < v.h && ow < v.w;
-  const float* src = dy + int64_t(n) * v.sn + int64_t(oh) * v.sh + int64_t(ow) * v.sw;
-  for (int k = threadIdx.x >> 6; k < K; k += 4) {
-    const float val = in ? __ldg(src + int64_t(k) * v.sc) : 0.0f;
-    const __nv_bfloat16 h = __float2bfloat16_rn(val);
-    hi[int64_t(k) * Pp + p] = h;
-    lo[int64_t(k) * Pp + p] = __float2bfloat16_rn(val - __bfloat162float(h));
+  const int64_t p = (int64_t(blockIdx.x) * 256 + threadIdx.x) * 2;
+  if (p >= Pp) return;
+  int64_t off[2];
+  bool in[2];
+#pragma unroll
+  for (int e = 0; e < 2; e++) {
+    const int64_t pe = p + e;
+    const int64_t n = pe / (int64_t(IH) * IW);
+    const int rem = int(pe - n * IH * IW), oh = rem / IW, ow = rem - oh * IW;
+    in[e] = pe < npix && oh < v.h && ow < v.w;
+    off[e] = in[e] ? n * v.sn + int64_t(oh) * v.sh + int64_t(ow) * v.sw : 0;
+  }
+  const int k0 = blockIdx.y * 8, k1 = min(K, k0 + 8);
+  for (int k = k0; k < k1; k++) {
+    const float a = in[0] ? __ldg(dy + off[0] + int64_t(k) * v.sc) : 0.0f;
+    const float b = in[1] ? __ldg(dy + off[1] + int64_t(k) * v.sc) : 0.0f;
+    const __nv_bfloat162 h2 = __floats2bfloat162_rn(a, b);
+    const float2 hf = __bfloat1622float2(h2);
+    *reinterpret_cast<__nv_bfloat162*>(hi + int64_t(k) * Pp + p) = h2;
+    *reinterpret_cast<__nv_bfloat162*>(lo + int64_t(k) * Pp + p) = __floats2bfloat162_rn(a - hf.x, b - hf.y);
   }
   pdl_trigger();
 }

@@ -652,7 +652,7 @@ cudaError_t wgrad_halo(const ConvProblem& p, const float* dy, const float* x, fl
     }
   }
   const int RH = kWhChunk + shmax;
-  if (RH > 256 || IW > 64) return cudaErrorNotSupported;
+  if (RH > 256) return cudaErrorNotSupported;
   const int64_t npix = p.N * int64_t(IH) * IW;
   const int64_t chunks = ceil_div(npix, int64_t(kWhChunk));
   const int64_t Pp = chunks * kWhChunk;
@@ -676,8 +676,8 @@ cudaError_t wgrad_halo(const ConvProblem& p, const float* dy, const float* x, fl
       cudaSuccess)
     return e;
   {
-    const int64_t rows = ceil_div(Pp, int64_t(IW));
-    pack_dy_grid_kernel<<<unsigned(rows), 256, 0, st>>>(p.y, dy, IH, IW, int(p.K), npix, Pp, d_hi, d_lo);
+    const dim3 grid(unsigned(ceil_div(Pp, int64_t(512))), unsigned(ceil_div(p.K, int64_t(8))));
+    pack_dy_grid_kernel<<<grid, 256, 0, st>>>(p.y, dy, IH, IW, int(p.K), npix, Pp, d_hi, d_lo);
     note_launch();
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
