@@ -1941,6 +1941,126 @@ __global__ void __launch_bounds__(128) pool3s2_bwd_kernel(PoolGeom g, const T* _
   if (KIND == 0 && badl) atomicExch(bad, 1);
 }
 
+// Lean 3 x 3 / 2 backward (unit-stride dx rows): every window sends its dy
+// (max: to one element, avg: dy / 9 to all nine) and a dx element sums the
+// <= 4 windows that reach it in window row-major order, as the reference's
+// scatter does (bit-exact).  Lane = window column q (and dx columns 2q,
+// 2q + 1), loop = window rows p: per row one window fetch, two shuffles for
+// the left neighbour (p, q - 1), the row-(p - 1) windows carried in
+// registers; outputs the 2 x 2 block (2p + a, 2q + b).
+template <typename T, int KIND>
+__global__ void __launch_bounds__(128) pool3s2_bwd_lean_kernel(PoolGeom g, const T* __restrict__ dy,
+                                                               T* __restrict__ dx,
+                                                               const int64_t* __restrict__ argmax,
+                                                               int* bad, int nqb, int nrc, int rows,
+                                                               int vec) {
+  const int H = int(g.H), W = int(g.W), P = int(g.P), Q = int(g.Q), C = int(g.C);
+  const int gw = int((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  const int planes = int(g.N) * C;
+  if (gw >= planes * nqb * nrc) return;  // warp-uniform
+  const int rc = gw % nrc, tt = gw / nrc;
+  const int pl = tt / nqb, jb = tt - pl * nqb;
+  const int q = jb * 32 + lane;
+  const int p0 = rc * rows, p1 = min(P, p0 + rows);
+  const int n = pl / C, c = pl - n * C;
+  const T* dyb = dy + int64_t(n) * g.y.sn + int64_t(c) * g.y.sc;
+  T* dxb = dx + int64_t(n) * g.x.sn + int64_t(c) * g.x.sc;
+  const int64_t* ab = KIND == 0 ? argmax + int64_t(pl) * P * Q : nullptr;
+  const int64_t abase = int64_t(pl) * H * W;
+  const bool edge = lane == 0 && q > 0 && q - 1 < Q;  // window q - 1 lives in the previous warp
+  bool badl = false;
+  // window (p, qq): value and code = 3 r + cc of its target (max; -1: none),
+  // 9 = every position (avg)
+  auto fetch = [&](int p, int qq, T& v, int& code) {
+    v = T(0);
+    code = -1;
+    if (p < 0 || p >= P || qq < 0 || qq >= Q) return;
+    v = __ldg(dyb + int64_t(p) * g.y.sh + int64_t(qq) * g.y.sw);
+    if (KIND == 0) {
+      const int64_t rel = __ldg(ab + int64_t(p) * Q + qq) - abase - (int64_t(2 * p) * W + 2 * qq);
+      if (rel >= 0 && rel < 3 * int64_t(W)) {
+        const int rl = int(rel);
+        const int r = rl >= 2 * W ? 2 : (rl >= W ? 1 : 0);
+        const int cc = rl - r * W;
+        if (cc <= 2) code = 3 * r + cc;
+      }
+      if (code < 0) badl = true;
+    } else {
+      v = v / T(9);
+      code = 9;
+    }
+  };
+  // contribution of a window with (v, code) to block element (a, b) when it
+  // would reach it at window position (r, cc)
+  auto hit = [](T v, int code, int r, int cc) -> T {
+    return (KIND != 0 ? code == 9 : code == 3 * r + cc) ? v : T(0);
+  };
+  T vU, vUL;  // windows (p - 1, q) and (p - 1, q - 1)
+  int cU, cUL;
+  fetch(p0 - 1, q, vU, cU);
+  {
+    T lv = __shfl_up_sync(0xffffffffu, vU, 1);
+    int lc = __shfl_up_sync(0xffffffffu, cU, 1);
+    if (edge) fetch(p0 - 1, q - 1, lv, lc);
+    vUL = lane == 0 && !edge ? T(0) : lv;
+    cUL = lane == 0 && !edge ? -1 : lc;
+  }
+  const int w0 = 2 * q;
+  const bool live = w0 < W, has1 = w0 + 1 < W;
+  for (int p = p0; p < p1; p++) {
+    T v;
+    int cd;
+    fetch(p, q, v, cd);
+    T vL = __shfl_up_sync(0xffffffffu, v, 1);
+    int cL = __shfl_up_sync(0xffffffffu, cd, 1);
+    if (edge) fetch(p, q - 1, vL, cL);
+    if (lane == 0 && !edge) {
+      vL = T(0);
+      cL = -1;
+    }
+    // window order: (p-1, q-1), (p-1, q), (p, q-1), (p, q)
+    const T o00 = dadd<T>(dadd<T>(dadd<T>(dadd<T>(T(0), hit(vUL, cUL, 2, 2)), hit(vU, cU, 2, 0)),
+                                 hit(vL, cL, 0, 2)), hit(v, cd, 0, 0));
+    const T o01 = dadd<T>(dadd<T>(T(0), hit(vU, cU, 2, 1)), hit(v, cd, 0, 1));
+    const T o10 = dadd<T>(dadd<T>(T(0), hit(vL, cL, 1, 2)), hit(v, cd, 1, 0));
+    const T o11 = dadd<T>(T(0), hit(v, cd, 1, 1));
+    if (live) {
+      T* r0p = dxb + int64_t(2 * p) * g.x.sh + w0;
+      if (vec && has1) {
+        using T2 = typename std::conditional<sizeof(T) == 4, float2, double2>::type;
+        T2 a, b;
+        a.x = o00; a.y = o01;
+        b.x = o10; b.y = o11;
+        *reinterpret_cast<T2*>(r0p) = a;
+        *reinterpret_cast<T2*>(r0p + g.x.sh) = b;
+      } else {
+        r0p[0] = o00;
+        if (has1) r0p[1] = o01;
+        r0p[g.x.sh] = o10;
+        if (has1) r0p[g.x.sh + 1] = o11;
+      }
+    }
+    vUL = vL;
+    cUL = cL;
+    vU = v;
+    cU = cd;
+  }
+  if (p1 == P && live) {
+    // row 2P: the row-(P - 1) windows' last rows; rows past it: zero
+    for (int h = 2 * P; h < H; h++) {
+      T o0 = T(0), o1 = T(0);
+      if (h == 2 * P) {
+        o0 = dadd<T>(dadd<T>(T(0), hit(vUL, cUL, 2, 2)), hit(vU, cU, 2, 0));
+        o1 = dadd<T>(T(0), hit(vU, cU, 2, 1));
+      }
+      dxb[int64_t(h) * g.x.sh + w0] = o0;
+      if (has1) dxb[int64_t(h) * g.x.sh + w0 + 1] = o1;
+    }
+  }
+  if (KIND == 0 && badl) atomicExch(bad, 1);
+}
+
 // whether the 3 x 3 / 2 plane kernels take this problem
 // the geometry of the 3 x 3 / 2 kernels (no padding, every window inside)
 static bool pool3s2_geom(const PoolProblem& pp, const View4& xv, const View4& yv) {
@@ -2141,7 +2261,25 @@ cudaError_t pool_backward(const PoolProblem& pp, Dtype dt, const View4& dyv, con
     // lanes = window columns plus the input columns past the last window
     const int nqb = int(ceil_div(ceil_div(dxv.w, 2), 32)), nrc = int(ceil_div(pp.P, kPoolRows));
     const unsigned blocks = unsigned(ceil_div(dxv.n * dxv.c * nqb * nrc, 4));
-    if (dt == F32) {
+    if (!::dnnp::tune_env("DNNP_POOL_NO_LEAN")) {
+      const int vec = (dxv.sh % 2 == 0 && dxv.sc % 2 == 0 && dxv.sn % 2 == 0 &&
+                       reinterpret_cast<uintptr_t>(dx) % (2 * eb) == 0) ? 1 : 0;
+      const int rows = ::dnnp::tune_env("DNNP_POOL_ROWS") ? std::max(1, atoi(::dnnp::tune_env("DNNP_POOL_ROWS")))
+                                                          : kPoolRows;
+      const int nrl = int(ceil_div(pp.P, rows));
+      const unsigned lblocks = unsigned(ceil_div(dxv.n * dxv.c * nqb * nrl, 4));
+      if (dt == F32) {
+        if (pp.kind == 0)
+          pool3s2_bwd_lean_kernel<float, 0><<<lblocks, 128, 0, st>>>(g, (const float*)dy, (float*)dx, argmax, bad, nqb, nrl, rows, vec);
+        else
+          pool3s2_bwd_lean_kernel<float, 1><<<lblocks, 128, 0, st>>>(g, (const float*)dy, (float*)dx, argmax, bad, nqb, nrl, rows, vec);
+      } else {
+        if (pp.kind == 0)
+          pool3s2_bwd_lean_kernel<double, 0><<<lblocks, 128, 0, st>>>(g, (const double*)dy, (double*)dx, argmax, bad, nqb, nrl, rows, vec);
+        else
+          pool3s2_bwd_lean_kernel<double, 1><<<lblocks, 128, 0, st>>>(g, (const double*)dy, (double*)dx, argmax, bad, nqb, nrl, rows, vec);
+      }
+    } else if (dt == F32) {
       if (pp.kind == 0)
         pool3s2_bwd_kernel<float, 0><<<blocks, 128, 0, st>>>(g, (const float*)dy, (float*)dx, argmax, bad, nqb, nrc);
       else
