@@ -1714,20 +1714,26 @@ constexpr int kPoolRows = 7;
 // same code serves unit-stride rows (lane = output column) and
 // channels-innermost views (lane = channel).  RP is a compile-time count:
 // full chunks carry no per-row predicates.
-template <typename T, int KIND, int RP>
-__device__ __forceinline__ void pool3s2_fwd_chunk(const T* __restrict__ xi, int xo, int xsh, int xsw,
+// EX = false (max): plain '>' comparisons -- the same first-maximum result
+// whenever the chunk holds no NaN; returns whether it saw one (the caller
+// then redoes the chunk with EX = true: the first NaN wins, numpy argmax).
+template <typename T, int KIND, int RP, bool EX = true>
+__device__ __forceinline__ bool pool3s2_fwd_chunk(const T* __restrict__ xi, int xo, int xsh, int xsw,
                                                   T* __restrict__ yi, int yo, int ysh,
                                                   int64_t* __restrict__ ab, int64_t abase, int aq,
                                                   int W, int p0, int w0) {
   constexpr int NR = 2 * RP + 1;
   T v[NR][3];
+  bool nan = false;
 #pragma unroll
   for (int r = 0; r < NR; r++) {
     const int o = xo + (2 * p0 + r) * xsh;
     v[r][0] = __ldg(xi + o);
     v[r][1] = __ldg(xi + o + xsw);
     v[r][2] = __ldg(xi + o + 2 * xsw);
+    if (!EX && KIND == 0) nan |= (v[r][0] != v[r][0]) | (v[r][1] != v[r][1]) | (v[r][2] != v[r][2]);
   }
+  if (!EX && KIND == 0 && nan) return true;
   T bv[NR];
   int bw[NR];
 #pragma unroll
@@ -1736,10 +1742,10 @@ __device__ __forceinline__ void pool3s2_fwd_chunk(const T* __restrict__ xi, int 
       // a later value wins when greater, or when it is NaN and the best is not
       T b = v[r][0];
       int w = 0;
-      bool t = v[r][1] > b || (v[r][1] != v[r][1] && b == b);
+      bool t = v[r][1] > b || (EX && v[r][1] != v[r][1] && b == b);
       b = t ? v[r][1] : b;
       w = t ? 1 : w;
-      t = v[r][2] > b || (v[r][2] != v[r][2] && b == b);
+      t = v[r][2] > b || (EX && v[r][2] != v[r][2] && b == b);
       bv[r] = t ? v[r][2] : b;
       bw[r] = t ? 2 : w;
     } else {
@@ -1752,10 +1758,10 @@ __device__ __forceinline__ void pool3s2_fwd_chunk(const T* __restrict__ xi, int 
     if (KIND == 0) {
       T b = bv[2 * i];
       int code = bw[2 * i];  // 3 * (row in window) + column
-      bool t = bv[2 * i + 1] > b || (bv[2 * i + 1] != bv[2 * i + 1] && b == b);
+      bool t = bv[2 * i + 1] > b || (EX && bv[2 * i + 1] != bv[2 * i + 1] && b == b);
       b = t ? bv[2 * i + 1] : b;
       code = t ? 3 + bw[2 * i + 1] : code;
-      t = bv[2 * i + 2] > b || (bv[2 * i + 2] != bv[2 * i + 2] && b == b);
+      t = bv[2 * i + 2] > b || (EX && bv[2 * i + 2] != bv[2 * i + 2] && b == b);
       b = t ? bv[2 * i + 2] : b;
       code = t ? 6 + bw[2 * i + 2] : code;
       yi[yo + p * ysh] = b;
@@ -1767,6 +1773,7 @@ __device__ __forceinline__ void pool3s2_fwd_chunk(const T* __restrict__ xi, int 
       yi[yo + p * ysh] = dadd<T>(dadd<T>(bv[2 * i], bv[2 * i + 1]), bv[2 * i + 2]) / T(9);
     }
   }
+  return false;
 }
 
 // Warps: (image or plane, 32 lanes, chunk of kPoolRows output rows).
@@ -1807,7 +1814,8 @@ __global__ void __launch_bounds__(128) pool3s2_fwd_kernel(PoolGeom g, const T* _
   int64_t* ab = argmax ? argmax + int64_t(pl) * P * Q + q : nullptr;
   const int64_t abase = int64_t(pl) * H * W;
 #define DNNP_POOL_CHUNK(RP)                                                                   \
-  pool3s2_fwd_chunk<T, KIND, RP>(xi, xo, xsh, xsw, yi, yo, ysh, ab, abase, Q, W, p0, w0)
+  if (pool3s2_fwd_chunk<T, KIND, RP, KIND != 0>(xi, xo, xsh, xsw, yi, yo, ysh, ab, abase, Q, W, p0, w0)) \
+    pool3s2_fwd_chunk<T, KIND, RP, true>(xi, xo, xsh, xsw, yi, yo, ysh, ab, abase, Q, W, p0, w0)
   switch (rows) {
     case 7: DNNP_POOL_CHUNK(7); break;
     case 6: DNNP_POOL_CHUNK(6); break;

@@ -1,7 +1,7 @@
 """One 3x3/2 max-pooling backward at the SURVEY 8(d) shape (128x64x55x55,
 NCHW) in a loop: ncu target for the pooling kernels.
 
-    python tools/pool_prof.py [max|average] [iters]
+    python tools/pool_prof.py [max|average] [iters]      (POOL_FWD=1: the forward)
 """
 import os
 import sys
@@ -27,7 +27,10 @@ def main():
     pd = dp.PoolingDesc(kind, 3, 3, 2, 2, 0, 0)
     dp.pool_forward(pd, x, y, am)
     for _ in range(iters):
-        dp.pool_backward(pd, y, dy, x, dx, am)
+        if os.environ.get("POOL_FWD"):
+            dp.pool_forward(pd, x, y, am)
+        else:
+            dp.pool_backward(pd, y, dy, x, dx, am)
     torch.cuda.synchronize()
 
 
