@@ -71,36 +71,60 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks/throttle reasons sampled during the timed region:
+    the sampler (20 ms period) is started and has produced its first sample
+    before the region begins; samples are time-stamped by a reader thread and
+    only those taken inside the region (plus one period after it) count."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
+    PERIOD_MS = 20
 
     def __init__(self, index):
         self.index = index
         self.proc = None
+        self.stamped = []
+        self.lines = []
+
+    def _reader(self):
+        for ln in self.proc.stdout:
+            self.stamped.append((time.perf_counter(), ln))
 
     def __enter__(self):
+        import threading
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", str(self.PERIOD_MS)],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._reader, daemon=True)
+            self.thread.start()
+            t0 = time.perf_counter()
+            while not self.stamped and time.perf_counter() - t0 < 5.0:
+                time.sleep(0.005)
         except Exception:
             self.proc = None
+        self.t_begin = time.perf_counter()
         return self
 
     def __exit__(self, *a):
-        self.lines = []
+        self.t_end = time.perf_counter()
         if self.proc is not None:
-            time.sleep(0.25)
+            # at least one sample after the region (the region may be shorter than a period)
+            deadline = time.perf_counter() + 1.0
+            while time.perf_counter() < deadline and not any(t > self.t_end for t, _ in self.stamped):
+                time.sleep(0.005)
             self.proc.terminate()
             try:
-                out, _ = self.proc.communicate(timeout=5)
-                self.lines = [ln for ln in out.splitlines() if ln.strip()]
+                self.proc.wait(timeout=5)
             except Exception:
                 self.proc.kill()
+            lim = self.t_end + self.PERIOD_MS / 1e3
+            inside = [ln for t, ln in self.stamped if self.t_begin <= t <= lim and ln.strip()]
+            if not inside:  # a region shorter than one period: the nearest samples
+                inside = [ln for t, ln in self.stamped if t >= self.t_begin][:1]
+            self.lines = inside
 
     def summary(self):
         sm, mx, reasons = [], 0.0, set()
