@@ -1216,8 +1216,18 @@ cudaError_t run_gemm(const ConvProblem& p, Gemm g, const void* a_hi, const void*
 template <int BN, int CB>
 cudaError_t launch_halo(const HaloParams& prm, size_t smem, cudaStream_t st) {
   auto kern = conv_halo_kernel<BN, CB, 2>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-  if (e != cudaSuccess) return e;
+  // the attribute is per device; re-set only when the device or a larger size is asked for
+  static int attr_dev = -1;
+  static size_t attr_smem = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaError_t e = cudaSuccess;
+  if (attr_dev != dev || smem > attr_smem) {
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+    attr_dev = dev;
+    attr_smem = smem;
+  }
   const int clusters = int(std::min<int64_t>(prm.tiles, kNumSMs / 2));
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(unsigned(clusters * 2));

@@ -705,8 +705,18 @@ cudaError_t wgrad_halo(const ConvProblem& p, const float* dy, const float* x, fl
   prm.arr_bytes = uint32_t(ceil_div(int64_t(RH) * 128, 1024) * 1024);
   prm.ws = part;
   const size_t smem = size_t(2) * (2 * prm.arr_bytes + 2 * 64 * 128 + 2 * 32 * 128) + 2048;
-  e = cudaFuncSetAttribute(wgrad_halo_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-  if (e != cudaSuccess) return e;
+  {
+    static int attr_dev = -1;
+    static size_t attr_smem = 0;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (attr_dev != dev || smem > attr_smem) {
+      e = cudaFuncSetAttribute(wgrad_halo_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+      if (e != cudaSuccess) return e;
+      attr_dev = dev;
+      attr_smem = smem;
+    }
+  }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(unsigned(ncl * 2));
   cfg.blockDim = dim3(kWhThreads);
