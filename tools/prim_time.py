@@ -33,12 +33,15 @@ def graph_time(op, reps=20):
             for _ in range(reps):
                 op()
     torch.cuda.synchronize()
+    g.replay()  # the first launch of a graph uploads it: not timed
+    torch.cuda.synchronize()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record()
-    g.replay()
+    for _ in range(3):
+        g.replay()
     b.record()
     torch.cuda.synchronize()
-    return a.elapsed_time(b) / reps
+    return a.elapsed_time(b) / (3 * reps)
 
 
 def cold_time(op, wflush, rflush, reps=5):
