@@ -564,11 +564,12 @@ __global__ void __launch_bounds__(256) pack_filter_vec_kernel(PackGeom g, const 
       coltab[row] = (oh_ << 24) | (ow_ << 16) | oc_;
     }
   }
-  pdl_trigger();
-  // launched programmatically after the operand pack (which it does not
-  // read): complete only once that pack has, so the GEMM's single wait
-  // covers both producers
+  // launched programmatically beside the operand pack (which it does not
+  // read; the pack triggers at its start): complete only once that pack has,
+  // so the GEMM's single wait covers both producers -- and trigger the GEMM
+  // only then, so its persistent CTAs do not take SMs the pack still needs
   pdl_wait();
+  pdl_trigger();
 }
 
 // Forward filter packing, one block per GEMM column row (all taps): the
@@ -1308,11 +1309,13 @@ cudaError_t run_halo(bool dgrad, const ConvProblem& p, const Gemm& g, const floa
   char* abase = base + ((flt * 4 + size_t(pg.KC + pg.Np + 2) * 4 + 255) & ~size_t(255));
   void* a_hi = abase;
   void* a_lo = abase + act * 2;
+  pack_trigger_early(true);  // the filter pack next is independent of this pack (see run_tc)
   if (!dgrad)
     e = pack_act_s2d(inv, in, int(p.u), int(p.v), int(p.pad_h), int(p.pad_w), IH, IW, Cp, a_hi, a_lo,
                      st, es);
   else
     e = pack_act_border(inv, in, Cp, top, left, IHg, IWg, a_hi, a_lo, st, es);
+  pack_trigger_early(false);
   if (e != cudaSuccess) return e;
   {
     const int64_t total8 = int64_t(pg.Np) * (pg.Ktot / 8);
@@ -1681,6 +1684,9 @@ cudaError_t run_tc(bool dgrad, const ConvProblem& p, const float* in, const View
   if (e != cudaSuccess) return e;
   void* a_hi = ws.p;
   void* a_lo = static_cast<char*>(ws.p) + act * es;
+  // the filter pack launched next (programmatic) is independent of this
+  // pack: both run at once; the filter pack's last wait orders the GEMM
+  pack_trigger_early(g.tma);
   if (fold)
     e = pack_act_fold(inv, in, int(p.S), int(p.v), int(p.pad_w), IW, Cp, a_hi, a_lo, st, es);
   else if (s2d && !dgrad)
@@ -1688,6 +1694,7 @@ cudaError_t run_tc(bool dgrad, const ConvProblem& p, const float* in, const View
                      a_lo, st, es);
   else
     e = pack_act(inv, in, Cp, a_hi, a_lo, st, es);
+  pack_trigger_early(false);
   if (e != cudaSuccess) return e;
   return run_gemm(p, g, a_hi, a_lo, IH, IW, Cp, f, out, outv, alpha, beta, epi, st, es);
 }

@@ -169,6 +169,9 @@ void packed_clear();
 // Strided fp32 4-D view -> channel-innermost split planes [n][h][w][Cp]
 // (Cp = channels padded to a multiple of 8, zero filled): BF16 hi / lo (es =
 // 2) or TF32 big / small in fp32 containers (es = 4).
+// The next pack launch on this thread triggers its dependents at its start
+// (the caller launches the independent filter pack programmatically next).
+void pack_trigger_early(bool on);
 // pack_act onto a zero-bordered grid (Hp, Wp), the tensor at (top, left)
 cudaError_t pack_act_border(const View4& v, const float* x, int Cp, int top, int left, int Hp,
                             int Wp, void* hi, void* lo, cudaStream_t st, int es = 2);

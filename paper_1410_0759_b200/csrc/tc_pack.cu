@@ -30,6 +30,12 @@ constexpr int kCh = 64;    // channels per slab
 // (pixel tile, channel slab) jobs.  S2D: the packed pixel grid is the
 // space-to-depth grid (H2 x W2 super-pixels, channel c' = (rh*u2 + rw)*C + c
 // reading x[c][h2*u + rh - pad_h][w2*v + rw - pad_w], zero outside).
+// Early programmatic trigger of the operand packs: set by a caller whose
+// next kernel (the filter pack) does not read the pack's output and itself
+// waits for it before completing -- the two packs then run concurrently.
+thread_local bool t_pack_early = false;
+inline int early_flag() { return t_pack_early ? 1 : 0; }
+
 struct S2dGeom {
   int u, v, pad_h, pad_w;
 };
@@ -110,7 +116,8 @@ __global__ void __launch_bounds__(256) pack_act_wide_kernel(View4 v, const float
                                                             int Cp, void* __restrict__ hi,
                                                             void* __restrict__ lo,
                                                             uint32_t npix, MagicDiv dHW,
-                                                            MagicDiv dW, Border bd = Border{0, 0, 0, 0}) {
+                                                            MagicDiv dW, Border bd = Border{0, 0, 0, 0}, int early = 0) {
+  if (early) pdl_trigger();  // the next kernel does not read this one: let it launch now
   __shared__ float tile[kCh][PIXJ + 1];
   constexpr int HALVES = PIXJ / 32;
   const int lp = threadIdx.x & 31, lc = threadIdx.x >> 5;  // read role: pixel, channel phase
@@ -170,7 +177,8 @@ template <int ES>
 __global__ void __launch_bounds__(256) pack_act_small_kernel(View4 v, const float* __restrict__ x,
                                                              int Cp, void* __restrict__ hi,
                                                              void* __restrict__ lo,
-                                                             int64_t npix, MagicDiv dHW, MagicDiv dW) {
+                                                             int64_t npix, MagicDiv dHW, MagicDiv dW, int early = 0) {
+  if (early) pdl_trigger();  // the next kernel does not read this one: let it launch now
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   for (int64_t pix = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; pix < npix; pix += stride) {
     uint32_t n, rem, h, w;
@@ -200,7 +208,8 @@ __global__ void __launch_bounds__(256) pack_act_s2d_kernel(View4 v, const float*
                                                            int H2, int W2, int Cp,
                                                            void* __restrict__ hi,
                                                            void* __restrict__ lo,
-                                                           int64_t npix, MagicDiv dHW, MagicDiv dW) {
+                                                           int64_t npix, MagicDiv dHW, MagicDiv dW, int early = 0) {
+  if (early) pdl_trigger();  // the next kernel does not read this one: let it launch now
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   const int C = int(v.c), Cs = u * vv * C;
   for (int64_t pix = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; pix < npix; pix += stride) {
@@ -358,7 +367,8 @@ __global__ void __launch_bounds__(512) pack_act_s2d_quad_kernel(View4 v, const f
                                                                 int u, int pad_h, int pad_w, int H2,
                                                                 int W2, int Cp, int nwb,
                                                                 void* __restrict__ hi,
-                                                                void* __restrict__ lo) {
+                                                                void* __restrict__ lo, int early = 0) {
+  if (early) pdl_trigger();  // the next kernel does not read this one: let it launch now
   constexpr int PIX = 64;           // super-pixels per block (two per lane): ~2x the bytes in flight
   extern __shared__ float stile[];  // [PIX][Cp + 1]
   const int C = int(v.c), Cs = u * V * C, pitch = Cp + 1;
@@ -422,7 +432,8 @@ __global__ void __launch_bounds__(256) pack_act_fold_kernel(View4 v, const float
                                                             int Cp, void* __restrict__ hi,
                                                             void* __restrict__ lo,
                                                             uint32_t npix, MagicDiv dHQ,
-                                                            MagicDiv dQ) {
+                                                            MagicDiv dQ, int early = 0) {
+  if (early) pdl_trigger();  // the next kernel does not read this one: let it launch now
   const int C = int(v.c), Cs = S * C;
   for (uint32_t pix = blockIdx.x * blockDim.x + threadIdx.x; pix < npix;
        pix += gridDim.x * blockDim.x) {
@@ -476,13 +487,13 @@ static cudaError_t pack_act_s2d_t(const View4& v, const float* x, int u, int vv,
       cudaError_t e;
       if (vv == 2)
         pack_act_s2d_quad_kernel<2, ES><<<grid, threads, sm, st>>>(v, x, u, pad_h, pad_w, H2, W2, Cp,
-                                                               nwb, hi, lo);
+                                                               nwb, hi, lo, early_flag());
       else if (vv == 4)
         pack_act_s2d_quad_kernel<4, ES><<<grid, threads, sm, st>>>(v, x, u, pad_h, pad_w, H2, W2, Cp,
-                                                               nwb, hi, lo);
+                                                               nwb, hi, lo, early_flag());
       else
         pack_act_s2d_quad_kernel<8, ES><<<grid, threads, sm, st>>>(v, x, u, pad_h, pad_w, H2, W2, Cp,
-                                                               nwb, hi, lo);
+                                                               nwb, hi, lo, early_flag());
       e = cudaGetLastError();
       note_launch();
       return e;
@@ -522,7 +533,7 @@ static cudaError_t pack_act_s2d_t(const View4& v, const float* x, int u, int vv,
   }
   pack_act_s2d_kernel<ES><<<grid_for(npix, 256, 8), 256, 0, st>>>(
       v, x, u, vv, pad_h, pad_w, H2, W2, Cp, hi, lo, npix, make_magic(uint32_t(H2 * W2)),
-      make_magic(uint32_t(W2)));
+      make_magic(uint32_t(W2)), early_flag());
   note_launch();
   return cudaGetLastError();
 }
@@ -1015,7 +1026,7 @@ static cudaError_t pack_act_fold_t(const View4& v, const float* x, int S, int vv
   if (npix >= (int64_t(1) << 32)) return cudaErrorInvalidValue;
   pack_act_fold_kernel<ES><<<grid_for(npix, 256, 8), 256, 0, st>>>(
       v, x, S, vv, pad_w, Q, Cp, hi, lo, uint32_t(npix), make_magic(uint32_t(v.h * Q)),
-      make_magic(uint32_t(Q)));
+      make_magic(uint32_t(Q)), early_flag());
   note_launch();
   return cudaGetLastError();
 }
@@ -1032,7 +1043,7 @@ static cudaError_t pack_act_t(const View4& v, const float* x, int Cp, void* hi, 
   if (npix >= (int64_t(1) << 32)) return cudaErrorInvalidValue;
   if (Cp <= 16) {
     pack_act_small_kernel<ES><<<grid_for(npix, 256, 8), 256, 0, st>>>(
-        v, x, Cp, hi, lo, npix, make_magic(uint32_t(v.h * v.w)), make_magic(uint32_t(v.w)));
+        v, x, Cp, hi, lo, npix, make_magic(uint32_t(v.h * v.w)), make_magic(uint32_t(v.w)), early_flag());
     note_launch();
     return cudaGetLastError();
   }
@@ -1044,11 +1055,13 @@ static cudaError_t pack_act_t(const View4& v, const float* x, int Cp, void* hi, 
     if (pj == 64)
       pack_act_wide_kernel<64, ES><<<grid, 256, 0, st>>>(v, x, Cp, hi, lo, uint32_t(npix),
                                                      make_magic(uint32_t(v.h * v.w)),
-                                                     make_magic(uint32_t(v.w)));
+                                                     make_magic(uint32_t(v.w)), Border{0, 0, 0, 0},
+                                                     early_flag());
     else
       pack_act_wide_kernel<128, ES><<<grid, 256, 0, st>>>(v, x, Cp, hi, lo, uint32_t(npix),
                                                       make_magic(uint32_t(v.h * v.w)),
-                                                      make_magic(uint32_t(v.w)));
+                                                      make_magic(uint32_t(v.w)), Border{0, 0, 0, 0},
+                                                      early_flag());
     note_launch();
     return cudaGetLastError();
   }
@@ -1072,7 +1085,7 @@ static cudaError_t pack_act_border_t(const View4& v, const float* x, int Cp, int
   pack_act_wide_kernel<64, ES><<<grid, 256, 0, st>>>(v, x, Cp, hi, lo, uint32_t(npix),
                                                      make_magic(uint32_t(Hp * Wp)),
                                                      make_magic(uint32_t(Wp)),
-                                                     Border{top, left, Hp, Wp});
+                                                     Border{top, left, Hp, Wp}, early_flag());
   note_launch();
   return cudaGetLastError();
 }
@@ -1082,6 +1095,8 @@ cudaError_t pack_act_border(const View4& v, const float* x, int Cp, int top, int
   return es == 4 ? pack_act_border_t<4>(v, x, Cp, top, left, Hp, Wp, hi, lo, st)
                  : pack_act_border_t<2>(v, x, Cp, top, left, Hp, Wp, hi, lo, st);
 }
+
+void pack_trigger_early(bool on) { t_pack_early = on && !::dnnp::tune_env("DNNP_PACK_LATE"); }
 
 cudaError_t pack_act(const View4& v, const float* x, int Cp, void* hi, void* lo,
                      cudaStream_t st, int es) {
