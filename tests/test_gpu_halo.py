@@ -72,6 +72,16 @@ def test_alexnet_conv1_default():
     check(run(8, 3, 224, 224, 64, 11, 11, 4, 4, 2, 2, 1))
 
 
+@pytest.mark.parametrize("n", [1, 5])
+def test_alexnet_conv1_small_and_odd_batches(n):
+    """Single image (a partial tile per CTA pair, fewer chunks than clusters
+    in the backward-filter split) and an odd batch, default selection; plus
+    alpha / beta and accumulate on the default path."""
+    check(run(n, 3, 224, 224, 64, 11, 11, 4, 4, 2, 2, 50 + n))
+    check(run(n, 3, 224, 224, 64, 11, 11, 4, 4, 2, 2, 60 + n, alpha=-0.5, beta=2.0, passes=("fwd",)))
+    check(run(n, 3, 224, 224, 64, 11, 11, 4, 4, 2, 2, 70 + n, acc=True, passes=("bwd_data", "bwd_filter")))
+
+
 #        N   C   H   W   K   R   S  u  v ph pw
 SHAPES = [(2, 3, 40, 44, 64, 11, 11, 4, 4, 2, 2),    # conv1-like: 48 channels (16-wide blocks), 64 cols
           (3, 3, 61, 57, 40, 11, 11, 4, 4, 2, 2),    # ragged: 40 output channels (48-column tile)
