@@ -112,7 +112,7 @@ struct Border {
 };
 
 template <int PIXJ, int ES>
-__global__ void __launch_bounds__(256) pack_act_wide_kernel(View4 v, const float* __restrict__ x,
+__global__ void __launch_bounds__(256, 8) pack_act_wide_kernel(View4 v, const float* __restrict__ x,
                                                             int Cp, void* __restrict__ hi,
                                                             void* __restrict__ lo,
                                                             uint32_t npix, MagicDiv dHW,
