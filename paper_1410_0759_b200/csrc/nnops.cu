@@ -1957,7 +1957,7 @@ __global__ void __launch_bounds__(128) pool3s2_bwd_kernel(PoolGeom g, const T* _
 // the left neighbour (p, q - 1), the row-(p - 1) windows carried in
 // registers; outputs the 2 x 2 block (2p + a, 2q + b).
 template <typename T, int KIND>
-__global__ void __launch_bounds__(128) pool3s2_bwd_lean_kernel(PoolGeom g, const T* __restrict__ dy,
+__global__ void __launch_bounds__(128, sizeof(T) == 4 ? 12 : 8) pool3s2_bwd_lean_kernel(PoolGeom g, const T* __restrict__ dy,
                                                                T* __restrict__ dx,
                                                                const int64_t* __restrict__ argmax,
                                                                int* bad, int nqb, int nrc, int rows,
