@@ -537,6 +537,13 @@ def main():
     if graph is not None and not args.no_sustained:
         try:
             nrep = max(1, int(3000.0 / max(float(np.median(step_ms)), 0.05)))
+            if ws > 1:
+                # every rank must replay the same number of graphs: each one
+                # holds the dW allreduces (a mismatch would hang the group)
+                t = torch.tensor([nrep], device=device, dtype=torch.int64)
+                dist.all_reduce(t, op=dist.ReduceOp.MIN)
+                nrep = int(t.item())
+                dist.barrier()
             torch.cuda.synchronize()
             with ClockSampler(local) as clk_s:
                 a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
