@@ -366,7 +366,10 @@ struct WgCfg {
   static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
   static constexpr int STAGES =
       (225 * 1024 - 2048) / STAGE_BYTES > 8 ? 8 : (225 * 1024 - 2048) / STAGE_BYTES;
-  static constexpr int TMEM_COLS = BN <= 64 ? 64 : (BN <= 128 ? 128 : 256);
+  // two accumulators, even / odd k-blocks: each fp32 TMEM chain is half the
+  // split's pixels (tcgen05 accumulation truncates: error grows with chain
+  // length); the epilogue adds them in IEEE fp32
+  static constexpr int TMEM_COLS = 2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512);
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
 };
 
@@ -472,9 +475,11 @@ __global__ void __launch_bounds__(kWgThreads, 1) wgrad_tma_kernel(const __grid_c
     if (leader) {
       constexpr uint32_t idesc = ES == 4 ? ptx::idesc_tf32(128 * NC, BN, 1, 1)
                                          : ptx::idesc_bf16(128 * NC, BN, 1, 1);
-      uint32_t acc = 0;
+      uint32_t accv[2] = {0, 0};
       for (int kb = 0; kb < nkb; kb++) {
         const int s = kb % S;
+        const uint32_t dacc = tmem_d + uint32_t((kb & 1) * BN);
+        uint32_t acc = accv[kb & 1];
         ptx::mbar_wait_spin(&full[s], (kb / S) & 1);
         ptx::tc_fence_after();
         if (P.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && kb < 1024 && lane == 0)
@@ -500,11 +505,12 @@ __global__ void __launch_bounds__(kWgThreads, 1) wgrad_tma_kernel(const __grid_c
           // one k-step = KSTEP pixels: KSTEP rows of 128 B (x), of BW * ES B (dy)
           const uint64_t o = uint64_t(kk * C::KSTEP * 128) >> 4;
           const uint64_t ob = uint64_t(kk * C::KSTEP * BW * ES) >> 4;
-          ptx::mma_split_elect<NC, ES>(tmem_d, dal + o, dbh + ob, idesc, acc);
-          ptx::mma_split_elect<NC, ES>(tmem_d, dah + o, dbl + ob, idesc, 1);
-          ptx::mma_split_elect<NC, ES>(tmem_d, dah + o, dbh + ob, idesc, 1);
+          ptx::mma_split_elect<NC, ES>(dacc, dal + o, dbh + ob, idesc, acc);
+          ptx::mma_split_elect<NC, ES>(dacc, dah + o, dbl + ob, idesc, 1);
+          ptx::mma_split_elect<NC, ES>(dacc, dah + o, dbh + ob, idesc, 1);
           acc = 1;
         }
+        accv[kb & 1] = 1;
         if constexpr (NC == 2) ptx::mma_commit_pair_elect(&empty[s]);
         else ptx::mma_commit_elect(&empty[s]);
       }
@@ -521,6 +527,14 @@ __global__ void __launch_bounds__(kWgThreads, 1) wgrad_tma_kernel(const __grid_c
     for (int c0 = 0; c0 < BN; c0 += 32) {
       uint32_t v[32];
       ptx::tmem_ld32(tmem_d + (uint32_t(ew * 32) << 16) + uint32_t(c0), v);
+      if (nkb > 1) {  // the odd k-blocks' accumulator
+        uint32_t w[32];
+        ptx::tmem_ld32(tmem_d + (uint32_t(ew * 32) << 16) + uint32_t(BN + c0), w);
+        ptx::tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < 32; i++)
+          v[i] = __float_as_uint(__fadd_rn(__uint_as_float(v[i]), __uint_as_float(w[i])));
+      }
       ptx::tmem_ld_wait();
 #pragma unroll
       for (int i = 0; i < 32; i += 4) {
