@@ -232,8 +232,13 @@ struct TCfg {
   static constexpr int STAGES = (225 * 1024 - 2048 - COLTAB_BYTES) / STAGE_BYTES > 8
                                     ? 8
                                     : (225 * 1024 - 2048 - COLTAB_BYTES) / STAGE_BYTES;
+  // DUAL (BN <= 128, room in TMEM): even / odd k-blocks of a work item
+  // accumulate into two accumulators the epilogue adds in IEEE fp32 (each
+  // truncating tcgen05 chain is half as long); ACC columns per buffer
+  static constexpr bool DUAL = BN <= 128;
+  static constexpr int ACC = DUAL ? 2 * BN : BN;
   static constexpr int TMEM_COLS =
-      2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512));
+      2 * ACC <= 64 ? 64 : (2 * ACC <= 128 ? 128 : (2 * ACC <= 256 ? 256 : 512));
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256 + COLTAB_BYTES;
 };
 
@@ -471,10 +476,13 @@ __global__ void __launch_bounds__(kTmaThreads, 1) conv_tma_kernel(const __grid_c
         const int buf = lt & 1;
         ptx::mbar_wait(&tempty[buf], ((lt >> 1) & 1) ^ 1);
         ptx::tc_fence_after();
-        const uint32_t dacc = tmem_base + uint32_t(buf * BN);
-        uint32_t acc = 0;
+        const uint32_t dacc0 = tmem_base + uint32_t(buf * C::ACC);
+        uint32_t accv[2] = {0, 0};
         for (int kb = kb0; kb < kb1; kb++, it++) {
           const int s = it % S;
+          const int half = C::DUAL ? ((kb - kb0) & 1) : 0;
+          const uint32_t dacc = dacc0 + uint32_t(half * BN);
+          uint32_t acc = accv[half];
           ptx::mbar_wait_spin(&full[s], (it / S) & 1);
           ptx::tc_fence_after();
           if (P.trace && blockIdx.x == 0 && it < 1024 && lane == 0) P.trace[it * 4 + 2] = clock64();
@@ -497,6 +505,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) conv_tma_kernel(const __grid_c
             ptx::mma_split_elect<NC, ES>(dacc, dah, dbh, idesc, 1);
             acc = 1;
           }
+          accv[half] = 1;
           if constexpr (NC == 2) ptx::mma_commit_pair_elect(&empty[s]);
           else ptx::mma_commit_elect(&empty[s]);
           if (P.trace && blockIdx.x == 0 && it < 1024 && lane == 0) P.trace[it * 4 + 3] = clock64();
@@ -511,6 +520,21 @@ __global__ void __launch_bounds__(kTmaThreads, 1) conv_tma_kernel(const __grid_c
     // 8 warps: quadrant ew = warp % 4 holds TMEM lanes (rows) 32*ew.., the
     // two warp sets split the 32-column chunks between them
     const int ew = warp & 3, es = (warp - 2) >> 2;
+    // 32 accumulator columns of the work item (DUAL: both halves added)
+    auto ld_acc = [&](int buf, int c0, bool two, uint32_t (&v)[32]) {
+      const uint32_t ta = tmem_base + (uint32_t(ew * 32) << 16) + uint32_t(buf * C::ACC + c0);
+      ptx::tmem_ld32(ta, v);
+      if (C::DUAL && two) {
+        uint32_t w[32];
+        ptx::tmem_ld32(ta + BN, w);
+        ptx::tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < 32; i++)
+          v[i] = __float_as_uint(__fadd_rn(__uint_as_float(v[i]), __uint_as_float(w[i])));
+      } else {
+        ptx::tmem_ld_wait();
+      }
+    };
     const int r = ew * 32 + lane;
     const int et = threadIdx.x - 64;  // 0..255 over the eight epilogue warps
     const bool ctab_smem = P.out_mode == 1 && P.Ncol <= kColCache;
@@ -554,8 +578,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) conv_tma_kernel(const __grid_c
 #pragma unroll 1
         for (int c0 = 32 * es; c0 < BN; c0 += 64) {
           uint32_t v[32];
-          ptx::tmem_ld32(tmem_base + (uint32_t(ew * 32) << 16) + uint32_t(buf * BN + c0), v);
-          ptx::tmem_ld_wait();
+          ld_acc(buf, c0, kb1 - kb0 > 1, v);
 #pragma unroll
           for (int i = 0; i < 32; i++) __stcg(mine + (c0 + i) * kBM, __uint_as_float(v[i]));
         }
@@ -588,8 +611,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) conv_tma_kernel(const __grid_c
           if (cbase >= P.Ncol) break;  // warp-uniform: padded columns are never loaded
           uint32_t v[32];
           if (np == 1) {
-            ptx::tmem_ld32(tmem_base + (uint32_t(ew * 32) << 16) + uint32_t(buf * BN + c0), v);
-            ptx::tmem_ld_wait();
+            ld_acc(buf, c0, kb1 - kb0 > 1, v);
           } else {
             const float* src = part + int64_t(c0) * kBM + r;
 #pragma unroll
